@@ -1,0 +1,294 @@
+#!/usr/bin/env python3
+"""bench.py -- tet·steps/s of the fp64 explicit CEM step (ES-FEM strain, stress, crack
+criterion, force assembly, Newmark update, split pass) on B200, and its HBM roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cem|reference] [--config 3]
+
+Workload (BASELINE.json configs[3], the weak-scaling block the metric is quoted on at
+1/2/4/8 GPUs): 100x100x17 Kuhn cells x 6 = 1.02M tets per GPU, E = 32 GPa, nu = 0.2,
+rho = 2450, Gc = 3 J/m^2, 0.5 % pre-damaged tets, 1 MPa traction, crack check every step.
+Inputs are synthetic and seeded (cem_inputs); the per-step working set (~0.4 GB) is
+larger than the 126 MB L2, so no L2 flush is needed between timed steps.
+
+One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tet·steps/sec (fp64 explicit ES-FEM step) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "tet·steps/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def b_alg_per_step(N, E, S):
+    """177 B/node + 17 B/tet + 96 B/edge."""
+    return 177 * N + 17 * E + 96 * S
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.samples = []
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        threading.Thread(target=self._read, daemon=True).start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [l for t, l in self.samples if t0 <= t <= t1] or [l for t, l in self.samples]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1]))
+            except Exception:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_problem(cfg, P=1):
+    import cem_inputs as ci
+    return ci.config(cfg, P=1) if cfg == 3 else ci.config(cfg)
+
+
+def cpu_baseline(prob, budget_s=12.0):
+    """The oracle as it stands, timed on this host's cores on a bounded sample."""
+    import oracle
+    t0 = time.time()
+    o = oracle.Oracle(prob)
+    init_s = time.time() - t0
+    o.run(1, 1)  # first step (page-in)
+    steps, t0 = 0, time.time()
+    while True:
+        o.run(1, 1)
+        steps += 1
+        if time.time() - t0 > budget_s or steps >= 50:
+            break
+    el = time.time() - t0
+    return {"value": prob.n_tets * steps / el, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{prob.name}: {steps} oracle steps (criterion every step) after 1 warm step, "
+                      f"init {init_s:.1f}s excluded"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the same workload (bounded sample per step)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import cem_inputs as ci
+    import oracle
+    # bounded sample: the config-3 block cut to nz' cells so one oracle step is ~0.1-0.3 s
+    nz = int(os.environ.get("CEM_REF_NZ", "2"))
+    prob = ci.weak_scaling_block(P=1, cells_per_rank=(100, 100, nz))
+    o = oracle.Oracle(prob)
+    o.run(args.warmup, 1)
+    t0 = time.time()
+    o.run(args.steps, 1)
+    el = time.time() - t0
+    val = prob.n_tets * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Kuhn lattice, cem_inputs)",
+            "config": {"workload": f"cfg3 sample 100x100x{nz} cells ({prob.n_tets} tets), crack check every step",
+                       "parallelism": "host cores (OpenMP)"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{prob.n_tets} tets x {args.steps} steps"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="cem", choices=["cem", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_2508_04076_b200 as cem
+
+    prob = make_problem(args.config)
+    sim = cem.Simulation.from_problem(prob, device=local)
+    N, E, S = sim.n_nodes, sim.n_tets, sim.n_edges
+    stream = sim.torch_stream
+    crack_every = 1
+
+    # warm-up (untimed)
+    sim.step(args.warmup, crack_every)
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    th0 = time.time()
+    ev0.record(stream)
+    sim.step(args.steps, crack_every)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    th1 = time.time()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = sim.state(records=False)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        tot = torch.tensor([float(E)], device=dev)
+        dist.all_reduce(tot)
+        E_all = float(tot.item())
+    else:
+        E_all = float(E)
+    # per-kernel durations on the launching stream (eager launches bracketed by CUDA events)
+    sim.set_profiling(True)
+    kp0 = time.time()
+    sim.step(args.steps, crack_every)
+    kt = sim.kernel_times()
+    kp1 = time.time()
+    sim.set_profiling(False)
+    sampler.stop()
+    clocks = sampler.summary(th0 - 0.05, max(th1, kp1) + 0.05)
+
+    ms_step = ms / args.steps
+    value = E_all * args.steps / (ms / 1e3)
+    hbm, peak_kind = peaks()
+    balg = b_alg_per_step(N, E, S)
+    achieved = balg / (ms_step / 1e3) / 1e9
+    kernels = {k: {"ms_per_launch": v / args.steps} for k, v in kt.items()}
+    tot_k = sum(v for v in kt.values())
+    for k in kernels:
+        kernels[k]["share"] = kt[k] / tot_k if tot_k > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_per_step.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn lattice, cem_inputs)",
+        "config": {"workload": f"cfg{args.config}: {prob.name} {E} tets/{N} nodes/{S} edges per GPU, "
+                               f"crack check + split pass every step",
+                   "tets_per_gpu": E, "parallelism": f"dp{ws}" if ws > 1 else "1 GPU",
+                   "l2": "per-step working set > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "kernel": "cem_step (one CUDA-graph launch per step)",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "peak_kind": peak_kind, "traffic": traffic,
+                     "b_alg_bytes_per_step": balg},
+        "kernels": kernels,
+        "gpu_launches": int(args.steps * sim.launches_per_step),
+        "clocks": clocks,
+        "n_active_end": int(st.n_active), "splits_total": int(st.rec_elem.size if st.rec_elem is not None else 0),
+    }
+    line["splits_total"] = int(sim.state().rec_elem.size)
+
+    if not args.no_e2e and rank == 0:
+        # end to end through the public API: host mesh -> cem_init_mesh (H2D) -> K steps -> state (D2H)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        sim2 = cem.Simulation.from_problem(prob, device=local)
+        sim2.step(args.steps, crack_every)
+        s2 = sim2.state(records=True)
+        t1 = time.perf_counter()
+        h2d = prob.X.nbytes + prob.tets.nbytes + prob.tet_state.nbytes + prob.tet_gc.nbytes + \
+            prob.tface.nbytes + prob.tface_t.nbytes
+        d2h = 3 * s2.u.nbytes + s2.tet_state.nbytes + s2.mass.nbytes
+        line["e2e"] = {"value": E * args.steps / (t1 - t0), "unit": UNIT,
+                       "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                       "what": "cem_init_mesh from host arrays (host preprocessing + H2D) + K steps + "
+                               "cem_get_state(CEM_HOST)"}
+        sim2.close()
+    if not args.no_cpu_baseline and rank == 0 and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(prob)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

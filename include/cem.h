@@ -1,0 +1,183 @@
+/*
+ * cem.h -- C ABI of libcem.so, the B200 (sm_100a) explicit step of the 3D Crack Element
+ * Method (arXiv 2508.04076, "A GPU-Accelerated Three-Dimensional Crack Element Method
+ * for Transient Dynamic Fracture Simulation").
+ *
+ * One explicit step n -> n+1 (§2.2-§3):
+ *   u_{n+1} = u_n + dt v_n + dt^2/2 a_n
+ *   eps~_s  = sum_{j in inc(s)} w_j B_j u,  w_j = V_j / sum V           (L268-L281, eq:strain_discretization)
+ *   sigma_s = D eps~_s                                                  (L197-L202)
+ *   f_int   = A_j(A_k B_k^T w_j sigma) (1/6) sum_j V_j                  (L340-L367, eq:fint_discretization)
+ *   a_{n+1} = M^-1 (f_ext - f_int(u_{n+1})),  M lumped                   (L392-L416)
+ *   v_{n+1} = v_n + dt [(1-gamma) a_n + gamma a_{n+1}]                  (L417)
+ *   crack criterion G = max(G_I, G_II) > Gc on every active tet          (L426-L476, eq:G-I, eq:G-II)
+ *   split pass: the element is deactivated and excluded from subsequent computations (L151)
+ *
+ * Conventions
+ *  - All floating point is IEEE fp64; indices int32 (meshes up to 2^31-1 entities).
+ *  - Host pointers passed to cem_init_mesh are read during the call only (copied);
+ *    the caller keeps ownership and may free them afterwards.
+ *  - Device memory: either the caller hands a device workspace (opts.workspace, at least
+ *    cem_workspace_size bytes), or an allocation callback (opts.dev_alloc, e.g. a torch
+ *    allocator), or neither, in which case the library uses cudaMalloc and frees on
+ *    cem_destroy.
+ *  - Asynchrony: cem_step enqueues work on opts.stream (NULL = the legacy default stream)
+ *    and returns; cem_get_state and cem_crack_update synchronise that stream.
+ *  - Errors: every call returns a cem_status; cem_last_error(ctx) gives a message (also for
+ *    a NULL ctx: the last error of cem_init_mesh in this thread).  No exception crosses the
+ *    ABI.  A ctx is not thread-safe.
+ *  - Determinism: results are bitwise reproducible run to run (fixed association order,
+ *    no floating-point atomics) and equal to the CPU oracle's (tests/test_gpu_parity.py).
+ */
+#ifndef CEM_H
+#define CEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CEM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define CEM_API __attribute__((visibility("default")))
+#else
+#define CEM_API
+#endif
+
+typedef struct cem_ctx cem_ctx; /* opaque; one per rank / GPU */
+
+typedef enum {
+    CEM_OK = 0,
+    CEM_EINVAL = 1,      /* bad argument: nu >= 0.5, E <= 0, rho <= 0, dt/cfl/gamma out of range, NULL array */
+    CEM_EDEGENERATE = 2, /* |V_e| < 1e-14 * bbox^3 */
+    CEM_ENEGVOL = 3,     /* a tet with negative orientation (det[X1-X0, X2-X0, X3-X0] < 0) */
+    CEM_ETOPOLOGY = 4,   /* node index out of range, repeated node in a tet, duplicate tets */
+    CEM_ENONFINITE = 5,  /* a non-finite u, v or a appeared (see cem_state_out.nonfinite_node) */
+    CEM_ECUDA = 6,       /* a CUDA runtime error (message in cem_last_error) */
+    CEM_ENCCL = 7,       /* multi-GPU communication error */
+    CEM_ESTATE = 8,      /* call not valid in the current state */
+    CEM_ENOMEM = 9       /* workspace too small / allocation failed */
+} cem_status;
+
+/* Isotropic linear elastic material with a Griffith threshold. */
+typedef struct {
+    double E;   /* Young's modulus (Pa), > 0 */
+    double nu;  /* Poisson ratio, -1 < nu < 0.5 */
+    double rho; /* density (kg/m^3), > 0 */
+    double Gc;  /* default critical energy release rate (J/m^2) for tets without tet_gc */
+} cem_material;
+
+/* Tetrahedral mesh (PAPER.md:L264 notation). */
+typedef struct {
+    int64_t n_nodes;
+    const double *X;          /* [n_nodes][3] reference coordinates (m), row-major */
+    int64_t n_tets;
+    const int32_t *tets;      /* [n_tets][4] node ids, positive orientation required */
+    const uint8_t *tet_state; /* NULL | [n_tets]: 0 inactive from the start (notch), 1 active */
+    const double *tet_gc;     /* NULL | [n_tets] per-element Gc (J/m^2); 0 = pre-damaged */
+} cem_mesh_in;
+
+/* Loads (PAPER.md:L191 Dirichlet/Neumann boundaries; L408-L412 external force;
+ * L572-L579 velocity ramp; L1119 constant traction). */
+typedef struct {
+    int64_t n_tfaces;
+    const int32_t *tface;     /* [n_tfaces][3] boundary triangles carrying a traction */
+    const double *tface_t;    /* [n_tfaces][3] traction vector (Pa), constant from t = 0 */
+    int64_t n_vbc;
+    const int32_t *vbc_node;  /* [n_vbc] prescribed-velocity nodes */
+    const uint8_t *vbc_mask;  /* [n_vbc] bit0 = x, bit1 = y, bit2 = z */
+    const double *vbc_v0;     /* [n_vbc][3] target velocity (m/s) */
+    double vbc_t0;            /* ramp time (s): v = (t/t0) v0 for t <= t0, else v0; 0 = step */
+} cem_load_in;
+
+/* flags */
+#define CEM_F_NO_EARLY_OUT 0x1u /* evaluate all 24 crack candidates on every active tet */
+
+typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
+
+typedef struct {
+    double dt;           /* time step (s); <= 0 -> cfl * min_e altitude_e / c_d (R12) */
+    double cfl;          /* default 0.5 */
+    double gamma;        /* Newmark gamma, default 0.5 (central difference) */
+    uint32_t flags;      /* CEM_F_* */
+    int device;          /* CUDA device ordinal */
+    void *stream;        /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = default */
+    void *workspace;     /* optional caller-owned device buffer (>= cem_workspace_size bytes) */
+    size_t workspace_bytes;
+    cem_alloc_fn dev_alloc; /* optional device allocator used when workspace == NULL */
+    void *alloc_user;
+    int rank, nranks;    /* multi-GPU: rank in [0, nranks); nranks <= 1 -> single GPU */
+    void *nccl_comm;     /* ncclComm_t when nranks > 1 */
+} cem_opts;
+
+/* State snapshot.  For CEM_HOST every non-NULL array pointer must point to caller-owned
+ * host memory of the stated size and is filled; for CEM_DEVICE the pointers are set to
+ * device views valid until the next cem_step / cem_crack_update / cem_destroy. */
+#define CEM_HOST 0
+#define CEM_DEVICE 1
+typedef struct {
+    double *u, *v, *a;        /* [n_nodes][3] at t_n (u_n, v_n, a_n) */
+    uint8_t *tet_state;       /* [n_tets] 1 active, 0 inactive */
+    double *mass;             /* [n_nodes] lumped mass (0 = frozen node) */
+    int64_t *rec_step;        /* [rec_capacity] records of split tets, in split order */
+    int32_t *rec_elem;        /*   (step ascending, element id ascending within a step) */
+    int32_t *rec_cand;        /*   candidate k = 6c + 2f + t (R7) */
+    double *rec_G;            /*   energy release rate at the split (J/m^2) */
+    double *rec_area;         /*   crack-surface area (m^2) */
+    int64_t rec_capacity;     /* in: size of the host record arrays */
+    /* scalars (always filled) */
+    int64_t step;             /* n */
+    double time;              /* n dt */
+    double dt;
+    int64_t n_active;         /* active tets */
+    int64_t n_records;        /* total split tets so far */
+    double dissipated;        /* U_d = sum Gc_e * area_e over split tets */
+    int32_t nonfinite;        /* 1 if a non-finite value was produced */
+    int32_t nonfinite_node;   /* lowest offending node id, -1 if none */
+} cem_state_out;
+
+/* Device bytes cem_init_mesh will need for this mesh (builds the edge set to count it). */
+CEM_API cem_status cem_workspace_size(const cem_mesh_in *mesh, const cem_opts *opts, size_t *bytes);
+
+/* Validate the mesh, build the topology (unique edges, edge->tet and node->tet CSR in
+ * ascending tet id), geometry, lumped mass (row sum rho V/4),
+ * nodal traction force (t A/3 per triangle node), the time step, upload to the device
+ * and set u_0 = v_0 = 0, a_0 = M^-1 f_ext (prescribed dofs: v(0), v'(0)).
+ * On failure *ctx is NULL and cem_last_error(NULL) explains. */
+CEM_API cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const cem_load_in *load,
+                         const cem_opts *opts, cem_ctx **ctx);
+
+/* Enqueue nsteps explicit steps.  crack_every > 0: evaluate the crack criterion and run
+ * the split pass after every crack_every-th step (criterion on u_{n+1} and the same
+ * sigma(u_{n+1}) used for f_int, R16); 0 = pure elastodynamics. */
+CEM_API cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every);
+
+/* Criterion + split pass on the current state (u_n, sigma(u_n)) without advancing time;
+ * synchronises; *n_split_out = number of tets split by this call. */
+CEM_API cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out);
+
+/* Synchronise and fill *out (see cem_state_out). Returns CEM_ENONFINITE if flagged. */
+CEM_API cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where);
+
+/* Mesh sizes after init. */
+CEM_API cem_status cem_sizes(const cem_ctx *ctx, int64_t *n_nodes, int64_t *n_tets, int64_t *n_edges);
+
+/* Number of kernel launches cem_step enqueues per step (for launch accounting). */
+CEM_API int32_t cem_launches_per_step(const cem_ctx *ctx);
+
+/* Time (ms, CUDA events on the ctx stream) of each kernel of the last cem_step call that
+ * ran with profiling enabled (cem_set_profiling); names[i] static strings. */
+CEM_API cem_status cem_set_profiling(cem_ctx *ctx, int on);
+CEM_API cem_status cem_kernel_times(const cem_ctx *ctx, int32_t *n, const char **names, double *ms, int32_t cap);
+
+CEM_API const char *cem_last_error(const cem_ctx *ctx);
+CEM_API void cem_destroy(cem_ctx *ctx);
+CEM_API int32_t cem_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CEM_H */
