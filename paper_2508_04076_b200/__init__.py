@@ -165,7 +165,9 @@ class Simulation:
             import torch
             dev = torch.device("cuda", device)
             if stream is None:
-                stream = torch.cuda.current_stream(dev)
+                # a dedicated non-default stream: CUDA graphs cannot be captured on the
+                # legacy default stream
+                stream = torch.cuda.Stream(dev)
             self.torch_stream = stream
             stream_ptr = stream.cuda_stream
 

@@ -19,6 +19,7 @@ struct cem_ctx {
     DevMesh m{};
     DevState s{};
     cudaStream_t stream = nullptr;
+    bool own_stream = false;
     int device = 0;
     void *ws = nullptr;
     size_t ws_bytes = 0;
@@ -305,6 +306,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     auto fail = [&](cem_status s) {
         g_init_err = ctx->err;
         if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
         return s;
     };
@@ -319,6 +321,13 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     if (cudaSetDevice(ctx->device) != cudaSuccess) {
         ctx->err = "cudaSetDevice failed";
         return fail(CEM_ECUDA);
+    }
+    if (!ctx->stream) {  // graphs cannot be captured on the legacy default stream
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            ctx->err = "cudaStreamCreate failed";
+            return fail(CEM_ECUDA);
+        }
+        ctx->own_stream = true;
     }
     Offs o = layout(ctx->h.N, ctx->h.E, ctx->h.S, ctx->h.any_dirichlet);
     if (opts && opts->workspace) {
@@ -358,6 +367,7 @@ void cem_destroy(cem_ctx *ctx) {
     destroy_graphs(ctx);
     for (auto e : ctx->ev) cudaEventDestroy(e);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
 
