@@ -191,6 +191,7 @@ def main():
 
     # warm-up (untimed)
     sim.step(args.warmup, crack_every)
+    l0 = sim.launch_count
     torch.cuda.synchronize(dev)
 
     sampler = ClockSampler(local)
@@ -209,6 +210,7 @@ def main():
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    launches = sim.launch_count - l0
     st = sim.state(records=False)
     if dist:
         t = torch.tensor([ms], device=dev)
@@ -254,12 +256,12 @@ def main():
                                f"crack check + split pass every step",
                    "tets_per_gpu": E, "parallelism": f"dp{ws}" if ws > 1 else "1 GPU",
                    "l2": "per-step working set > 126 MB L2 (no flush needed)"},
-        "roofline": {"bound": "hbm", "kernel": "cem_step (one CUDA-graph launch per step)",
+        "roofline": {"bound": "hbm", "kernel": "k_persistent (one launch runs all K steps)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_kind": peak_kind, "traffic": traffic,
                      "b_alg_bytes_per_step": balg},
         "kernels": kernels,
-        "gpu_launches": int(args.steps * sim.launches_per_step),
+        "gpu_launches": int(launches),
         "clocks": clocks,
         "n_active_end": int(st.n_active), "splits_total": int(st.rec_elem.size if st.rec_elem is not None else 0),
     }

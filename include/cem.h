@@ -95,6 +95,7 @@ typedef struct {
 
 /* flags */
 #define CEM_F_NO_EARLY_OUT 0x1u /* evaluate all 24 crack candidates on every active tet */
+#define CEM_F_STAGED 0x2u       /* one kernel per stage instead of the persistent wavefront kernel */
 
 typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
 
@@ -165,11 +166,12 @@ CEM_API cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where);
 /* Mesh sizes after init. */
 CEM_API cem_status cem_sizes(const cem_ctx *ctx, int64_t *n_nodes, int64_t *n_tets, int64_t *n_edges);
 
-/* Number of kernel launches cem_step enqueues per step (for launch accounting). */
-CEM_API int32_t cem_launches_per_step(const cem_ctx *ctx);
+/* Total number of kernels this context has launched so far (launch accounting). */
+CEM_API int64_t cem_launch_count(const cem_ctx *ctx);
 
-/* Time (ms, CUDA events on the ctx stream) of each kernel of the last cem_step call that
- * ran with profiling enabled (cem_set_profiling); names[i] static strings. */
+/* Profiling: with cem_set_profiling(ctx, 1) cem_step runs one kernel per stage and brackets
+ * each with CUDA events on the ctx stream; cem_kernel_times returns the accumulated ms per
+ * stage since profiling was switched on (names[i] are static strings). */
 CEM_API cem_status cem_set_profiling(cem_ctx *ctx, int on);
 CEM_API cem_status cem_kernel_times(const cem_ctx *ctx, int32_t *n, const char **names, double *ms, int32_t cap);
 

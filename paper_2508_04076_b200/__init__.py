@@ -32,6 +32,7 @@ CEM_OK, CEM_EINVAL, CEM_EDEGENERATE, CEM_ENEGVOL, CEM_ETOPOLOGY, CEM_ENONFINITE,
 STATUS_NAMES = ["CEM_OK", "CEM_EINVAL", "CEM_EDEGENERATE", "CEM_ENEGVOL", "CEM_ETOPOLOGY",
                 "CEM_ENONFINITE", "CEM_ECUDA", "CEM_ENCCL", "CEM_ESTATE", "CEM_ENOMEM"]
 CEM_F_NO_EARLY_OUT = 0x1
+CEM_F_STAGED = 0x2
 CEM_HOST, CEM_DEVICE = 0, 1
 
 D = C.POINTER(C.c_double)
@@ -80,8 +81,8 @@ _lib.cem_step.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
 _lib.cem_crack_update.argtypes = [C.c_void_p, I64]
 _lib.cem_get_state.argtypes = [C.c_void_p, _P(cem_state_out), C.c_int]
 _lib.cem_sizes.argtypes = [C.c_void_p, I64, I64, I64]
-_lib.cem_launches_per_step.argtypes = [C.c_void_p]
-_lib.cem_launches_per_step.restype = C.c_int32
+_lib.cem_launch_count.argtypes = [C.c_void_p]
+_lib.cem_launch_count.restype = C.c_int64
 _lib.cem_set_profiling.argtypes = [C.c_void_p, C.c_int]
 _lib.cem_kernel_times.argtypes = [C.c_void_p, I32, C.POINTER(C.c_char_p), D, C.c_int32]
 _lib.cem_last_error.argtypes = [C.c_void_p]
@@ -93,7 +94,7 @@ for _f in ("cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update"
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTED = ["cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state",
-            "cem_sizes", "cem_launches_per_step", "cem_set_profiling", "cem_kernel_times",
+            "cem_sizes", "cem_launch_count", "cem_set_profiling", "cem_kernel_times",
             "cem_last_error", "cem_destroy", "cem_abi_version"]
 
 
@@ -224,8 +225,9 @@ class Simulation:
         return {names[i].decode(): ms[i] for i in range(n.value)}
 
     @property
-    def launches_per_step(self):
-        return _lib.cem_launches_per_step(self._h)
+    def launch_count(self):
+        """Kernels launched by this simulation so far (cem_launch_count)."""
+        return _lib.cem_launch_count(self._h)
 
     def state(self, records=True, check=True) -> State:
         N, E = self.n_nodes, self.n_tets

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcem.so")
-SOURCES = ["cem_mesh.cpp", "cem_kernels.cu", "cem_api.cu"]
+SOURCES = ["cem_mesh.cpp", "cem_plan.cpp", "cem_kernels.cu", "cem_api.cu"]
 HEADERS = ["cem_internal.h", os.path.join("..", "..", "include", "cem.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

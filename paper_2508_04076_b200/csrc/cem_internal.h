@@ -11,14 +11,16 @@
 
 namespace cem {
 
-// Host-side preprocessed mesh (cem_mesh.cpp).  All arrays are in the caller's numbering.
+// ---------------------------------------------------------------- host preprocessing
+// HostMesh holds the mesh in the caller's ("original") numbering (cem_mesh.cpp).
 struct HostMesh {
     int64_t N = 0, E = 0, S = 0;
     std::vector<double> X;            // [N][3]
     std::vector<int32_t> tet;         // [E][4]
     std::vector<uint8_t> state;       // [E]
     std::vector<double> gc;           // [E]
-    std::vector<double> geo;          // [E][16]: V, c6=V/6, pad, pad, grad[4][3]
+    std::vector<double> V;            // [E]
+    std::vector<double> grad;         // [E][4][3]
     std::vector<int32_t> elem_edge;   // [E][6]
     std::vector<int32_t> edge_nodes;  // [S][2]
     std::vector<int32_t> edge_off;    // [S+1]
@@ -28,68 +30,89 @@ struct HostMesh {
     std::vector<double> mass;         // [N]
     std::vector<double> fext;         // [N][3]
     std::vector<uint8_t> nflag;       // [N] bit0-2 Dirichlet mask, bit3 has f_ext
-    std::vector<double> dir_v0;       // [N][3] (only meaningful where mask bits set)
+    std::vector<double> dir_v0;       // [N][3]
     double lam = 0, mu = 0, l2m = 0, rho = 0;
     double dt = 0, gamma = 0.5, t0 = 0;
     bool any_dirichlet = false;
 };
 
-// builds HostMesh; returns CEM_OK or an error with message
 cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const cem_load_in *ld,
                            const cem_opts *o, HostMesh &h, std::string &err);
 cem_status count_edges(const cem_mesh_in *m, int64_t *S, std::string &err);
 
-// ---------------------------------------------------------------- device views
-struct DevMesh {
-    int64_t N, E, S;
-    const double4 *X;         // [N] (x,y,z,0)
-    const int4 *tet;          // [E]
-    uint8_t *state;           // [E]
-    const double *gc;         // [E]
-    const double *geo;        // [E][16]
-    const int32_t *elem_edge; // [E][6]
-    const int32_t *edge_off;  // [S+1]
-    const int32_t *edge_inc;  // [6E]
-    const int32_t *node_off;  // [N+1]
-    const int32_t *node_ent;  // [4E]
-    double *mass;             // [N]
-    const double4 *fext;      // [N]
-    const uint8_t *nflag;     // [N]
-    const double4 *dir_v0;    // [N]
-    double lam, mu, l2m, rho, dt, gamma, t0;
-    uint32_t flags;
+// ---------------------------------------------------------------- storage plan
+// Storage ("new") numbering: tets sorted by (sweep-axis slab of the centroid, original id),
+// nodes and edges by first appearance in that tet order.  Summation lists keep the
+// ORIGINAL tet order so every sum matches the oracle bit for bit.
+enum Stage { ST_A = 0, ST_B = 1, ST_C = 2, ST_D = 3, ST_COUNT = 4 };
+
+struct Plan {
+    std::vector<int32_t> tet_new2old, tet_old2new, node_new2old, node_old2new, edge_new2old;
+    // storage-order arrays
+    std::vector<int32_t> conn;        // [E][4] new node ids (int4)
+    std::vector<double> geoV, geoC;   // [E] V, V/6
+    std::vector<double> geoG;         // [9][E] gradN1x,1y,1z,2x,...,3z
+    std::vector<int32_t> eedge;       // [6][E] new edge ids
+    std::vector<int32_t> edge_off, edge_inc;   // CSR over new edges, new tet ids, original order
+    std::vector<int32_t> node_off, node_ent;   // CSR over new nodes, (new e << 2 | a), original order
+    std::vector<uint8_t> state;
+    std::vector<double> gc;
+    // blocks and the wavefront schedule
+    int blk = 256;                    // entities per work item
+    int nblk[ST_COUNT] = {0, 0, 0, 0};
+    int maxblk = 0;
+    std::vector<int32_t> dep;         // [ST_COUNT][maxblk][2]: producer block range [lo, hi]
+    std::vector<int32_t> sched;       // [P]: stage << 28 | block
 };
 
-struct DevState {
-    double4 *u[2];            // ping-pong: u[cur] = u_n, u[cur^1] = u_{n+1} (predicted)
-    double4 *v, *a;           // [N]
-    double *tau;              // [E][6]  V_e eps_e
-    double *sig;              // [S][6]  edge stress
-    double *fe;               // [E][12] element nodal forces
-    // split bookkeeping
-    int32_t *ctr;             // [8]: 0 n_flag, 1 nonfinite, 2 first bad node, 3 overflow
-    int64_t *step;            // [1] completed steps n
-    double *Ud;               // [1]
-    int64_t *nrec;            // [1]
-    int32_t *flag_list;       // [cap] unordered flagged tets
-    int32_t *flag_cand;       // [cap]
-    double *flag_G;           // [cap]
-    double *flag_area;        // [cap]
-    uint8_t *flag;            // [E] split flag (fallback path)
-    int64_t *rec_step;        // [E]
+void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p);
+
+// ---------------------------------------------------------------- device view
+struct Dev {
+    int64_t N, E, S;
+    // read-only mesh tables (storage numbering)
+    const int4 *conn;
+    const double *geoV, *geoC, *geoG;
+    const int32_t *eedge;
+    const int32_t *edge_off, *edge_inc;
+    const int32_t *node_off, *node_ent;
+    const double4 *X;
+    const double4 *fext;
+    const uint8_t *nflag;
+    const double4 *dir_v0;
+    const double *gc;
+    const int32_t *tet_orig;   // storage -> original tet id
+    const int32_t *node_orig;  // storage -> original node id
+    // mutable state
+    uint8_t *state;
+    double *mass;
+    int32_t *dirty;            // [N] step stamp of the last split touching the node
+    double4 *ubuf[2];          // u_m lives in ubuf[m & 1]
+    double4 *v, *a;
+    double *trec;              // [E][8]: V_e eps_e (6), V_e if active else 0, pad
+    double *srec;              // [S][8]: sigma_s (6), Gershgorin bound g_s, pad
+    double *fe;                // [E][12]
+    int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] spare
+    int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
     double *rec_G, *rec_area;
-    int32_t flag_cap;
+    // parameters
+    double lam, mu, l2m, rho, dt, hdt2, gamma, omg, t0;
+    uint32_t flags;
+    // persistent wavefront
+    int32_t *cnt;              // [ST_COUNT][maxblk] completed-step counters
+    const int32_t *dep;        // [ST_COUNT][maxblk][2]
+    const int32_t *sched;      // [P]
+    unsigned long long *head;  // work-queue head
+    int blk, P, maxblk;
+    int nblk[ST_COUNT];
 };
 
-enum KernelId { K_STRAIN = 0, K_EDGE, K_FORCE, K_NODE, K_SPLIT, K_COUNT };
-extern const char *kKernelNames[K_COUNT];
-
-// kernels (cem_kernels.cu): enqueue one step on `stream` with u-buffer index `cur`
-void launch_strain(const DevMesh &m, const DevState &s, int cur, cudaStream_t st);
-void launch_edge(const DevMesh &m, const DevState &s, cudaStream_t st);
-void launch_force(const DevMesh &m, const DevState &s, int cur, int crack_every, cudaStream_t st);
-void launch_node(const DevMesh &m, const DevState &s, int cur, cudaStream_t st);
-void launch_split(const DevMesh &m, const DevState &s, int cur, int crack_every, int advance, cudaStream_t st);
+// cem_kernels.cu
+void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
+void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/);
+void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
+int persistent_occupancy();  // resident CTAs per SM of the persistent kernel
+extern const int kThreads;
 
 }  // namespace cem

@@ -1,100 +1,136 @@
 // cem_kernels.cu -- sm_100a kernels of the CEM explicit step.
 //
 // Compiled with --fmad=false: every product and sum rounds exactly as written, in the
-// association order fixed in DESIGN.md ("Association order"), so results are bitwise
-// reproducible and equal to the CPU oracle's.  No floating-point atomics anywhere: each
+// association order fixed by the oracle, so results are
+// bitwise reproducible and equal to the CPU oracle's.  No floating-point atomics: every
 // output is produced by one thread that sums its inputs sequentially in ascending
-// element id (deterministic CSR gathers).
+// ORIGINAL element id (deterministic CSR gathers).
 //
-// Stages (one explicit step n -> n+1, u_{n+1} already predicted):
-//   k_strain  (a1) tau_e = V_e eps_e(u_{n+1})
-//   k_edge    (a2) Vhat_s, eps~_s = (sum tau_e)/Vhat_s, sigma_s
-//   k_force   (a3) f_e = (V_e/6) B^T sum_l sigma_{s(e,l)}; criterion PAPER.md:L340-L367, L426-L476
-//   k_node    (a4) f_int gather, Newmark, BC, predictor u_{n+2}
-//   k_split   (a5) ordered split pass (deactivate, records, mass)
+// Stages of one explicit step s -> s+1 (u_{s+1} already predicted, stored in ubuf[(s+1)&1]):
+//   A  tau_e = V_e eps_e(u_{s+1}) per tet
+//   B  Vhat_s, eps~_s = (sum tau_e)/Vhat_s, sigma_s per edge
+//   C  f_e = (V_e/6) B^T sum_l sigma_{s(e,l)} per tet; crack
+//      criterion with a conservative early-out; split inline
+//   D  f_int gather, Newmark + BC, mass/freeze of split nodes,
+//      predictor u_{s+2} -> ubuf[s&1]
+//
+// k_persistent runs K steps in ONE launch: CTAs pull (stage, block) work items from a
+// global queue in a precomputed wavefront order (cem_plan.cpp) and wait only on the
+// completed-step counters of the producer blocks they read.  Consecutive steps overlap;
+// intermediates stay L2-resident between producer and consumer.
 #include <cstdint>
 
 #include "cem_internal.h"
 
 namespace cem {
 
-const char *kKernelNames[K_COUNT] = {"k_strain", "k_edge", "k_force", "k_node", "k_split"};
+const int kThreads = 256;
 
 namespace {
 
-constexpr int kBlock = 256;
-
-__device__ __forceinline__ double ld_nc(const double *p) { return __ldg(p); }
-__device__ __forceinline__ double4 ldg4(const double4 *p) {
+// read-only tables: non-coherent path
+__device__ __forceinline__ double ldro(const double *p) { return __ldg(p); }
+__device__ __forceinline__ int ldro(const int32_t *p) { return __ldg(p); }
+__device__ __forceinline__ double4 ldro4(const double4 *p) {
     const double2 *q = reinterpret_cast<const double2 *>(p);
     const double2 a = __ldg(q), b = __ldg(q + 1);
     return make_double4(a.x, a.y, b.x, b.y);
 }
+// data written inside the kernel (coherent path; L1 invalidated after every acquire)
+__device__ __forceinline__ double4 ld4(const double4 *p) {
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a = q[0], b = q[1];
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st4(double4 *p, double x, double y, double z, double w) {
+    double2 *q = reinterpret_cast<double2 *>(p);
+    q[0] = make_double2(x, y);
+    q[1] = make_double2(z, w);
+}
 
-// ------------------------------------------------------------------ a1: element strain
-__global__ void __launch_bounds__(kBlock) k_strain(DevMesh m, const double4 *__restrict__ u, double *__restrict__ tau) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= m.E) return;
-    if (!m.state[e]) return;  // inactive: tau is never read (k_edge skips it)
-    const int4 t = __ldg(&m.tet[e]);
-    const double *g = m.geo + 16 * e;
-    const double V = ld_nc(g);
-    const int nid[4] = {t.x, t.y, t.z, t.w};
+// ------------------------------------------------------------------ stage A: element strain
+// eps = sum_a B_a u_a (a = 0..3 in order), Voigt (11,22,33,12,23,13) with engineering
+// shears; gradN0 = -((gradN1 + gradN2) + gradN3); tau = V eps.  Record: tau (6), V if
+// active else 0, pad.
+__device__ __forceinline__ void stage_A(const Dev &d, int64_t e, const double4 *u) {
+    double2 *o = reinterpret_cast<double2 *>(d.trec + 8 * e);
+    if (!d.state[e]) {
+        o[3] = make_double2(0.0, 0.0);  // V slot = 0 marks "inactive" for stage B
+        return;
+    }
+    const int4 t = __ldg(&d.conn[e]);
+    const int64_t E = d.E;
+    double g[4][3];
+#pragma unroll
+    for (int a = 1; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[a][c] = ldro(d.geoG + (int64_t)(3 * (a - 1) + c) * E + e);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+    const double V = ldro(d.geoV + e);
+    const double4 u0 = ld4(&u[t.x]), u1 = ld4(&u[t.y]), u2 = ld4(&u[t.z]), u3 = ld4(&u[t.w]);
+    const double ux[4] = {u0.x, u1.x, u2.x, u3.x}, uy[4] = {u0.y, u1.y, u2.y, u3.y}, uz[4] = {u0.z, u1.z, u2.z, u3.z};
     double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const double4 ua = ldg4(&u[nid[a]]);
-        const double gx = ld_nc(g + 4 + 3 * a), gy = ld_nc(g + 5 + 3 * a), gz = ld_nc(g + 6 + 3 * a);
-        ex = ex + gx * ua.x;
-        ey = ey + gy * ua.y;
-        ez = ez + gz * ua.z;
-        gxy = gxy + (gy * ua.x + gx * ua.y);
-        gyz = gyz + (gz * ua.y + gy * ua.z);
-        gxz = gxz + (gz * ua.x + gx * ua.z);
+        const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
+        ex = ex + gx * ux[a];
+        ey = ey + gy * uy[a];
+        ez = ez + gz * uz[a];
+        gxy = gxy + (gy * ux[a] + gx * uy[a]);
+        gyz = gyz + (gz * uy[a] + gy * uz[a]);
+        gxz = gxz + (gz * ux[a] + gx * uz[a]);
     }
-    double2 *o = reinterpret_cast<double2 *>(tau + 6 * e);
     o[0] = make_double2(V * ex, V * ey);
     o[1] = make_double2(V * ez, V * gxy);
     o[2] = make_double2(V * gyz, V * gxz);
+    o[3] = make_double2(V, 0.0);
 }
 
-// ------------------------------------------------------------------ a2: edge smoothed strain -> stress
-__global__ void __launch_bounds__(kBlock) k_edge(DevMesh m, const double *__restrict__ tau, double *__restrict__ sig) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= m.S) return;
-    const int32_t j0 = __ldg(&m.edge_off[s]), j1 = __ldg(&m.edge_off[s + 1]);
+// ------------------------------------------------------------------ stage B: edge stress
+// Vhat = sum V_e, T = sum tau_e over active incident tets in original-id order;
+// eps~ = T * (1/Vhat); sigma_ii = (lam+2mu) eps_ii + lam (eps_jj + eps_kk), sigma_ij = mu gamma_ij.
+// Also the Gershgorin bound g = max_i sum_j |sigma_ij| (early-out of stage C).
+__device__ __forceinline__ void stage_B(const Dev &d, int64_t s) {
+    const int32_t j0 = ldro(d.edge_off + s), j1 = ldro(d.edge_off + s + 1);
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
     for (int32_t j = j0; j < j1; ++j) {
-        const int32_t e = __ldg(&m.edge_inc[j]);
-        if (!m.state[e]) continue;
-        Vh = Vh + ld_nc(m.geo + 16 * (int64_t)e);
-        const double2 *tp = reinterpret_cast<const double2 *>(tau + 6 * (int64_t)e);
-        const double2 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+        const int32_t e = ldro(d.edge_inc + j);
+        const double2 *r = reinterpret_cast<const double2 *>(d.trec + 8 * (int64_t)e);
+        const double Ve = r[3].x;
+        if (Ve == 0.0) continue;  // inactive tet
+        const double2 a = r[0], b = r[1], c = r[2];
+        Vh = Vh + Ve;
         T0 = T0 + a.x; T1 = T1 + a.y; T2 = T2 + b.x;
         T3 = T3 + b.y; T4 = T4 + c.x; T5 = T5 + c.y;
     }
-    double2 *o = reinterpret_cast<double2 *>(sig + 6 * s);
+    double2 *o = reinterpret_cast<double2 *>(d.srec + 8 * s);
     if (Vh == 0.0) {
-        o[0] = o[1] = o[2] = make_double2(0.0, 0.0);
+        o[0] = o[1] = o[2] = o[3] = make_double2(0.0, 0.0);
         return;
     }
     const double inv = 1.0 / Vh;
     const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-    const double lam = m.lam, mu = m.mu, l2m = m.l2m;
-    o[0] = make_double2(l2m * e11 + lam * (e22 + e33), l2m * e22 + lam * (e11 + e33));
-    o[1] = make_double2(l2m * e33 + lam * (e11 + e22), mu * g12);
-    o[2] = make_double2(mu * g23, mu * g13);
+    const double s0 = d.l2m * e11 + d.lam * (e22 + e33);
+    const double s1 = d.l2m * e22 + d.lam * (e11 + e33);
+    const double s2 = d.l2m * e33 + d.lam * (e11 + e22);
+    const double s3 = d.mu * g12, s4 = d.mu * g23, s5 = d.mu * g13;
+    const double r0 = fabs(s0) + fabs(s3) + fabs(s5);
+    const double r1 = fabs(s1) + fabs(s3) + fabs(s4);
+    const double r2 = fabs(s2) + fabs(s4) + fabs(s5);
+    o[0] = make_double2(s0, s1);
+    o[1] = make_double2(s2, s3);
+    o[2] = make_double2(s4, s5);
+    o[3] = make_double2(fmax(r0, fmax(r1, r2)), 0.0);
 }
 
-// ------------------------------------------------------------------ crack criterion (device)
-// Local edge l -> (p,q), p < q, and the inverse map.
+// ------------------------------------------------------------------ crack criterion (rare path)
 __constant__ int c_ep[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_eq[6] = {1, 2, 3, 2, 3, 3};
 __device__ __forceinline__ int ledge(int a, int b) {
     const int p = a < b ? a : b, q = a < b ? b : a;
     return p == 0 ? q - 1 : (p == 1 ? q + 1 : 5);
 }
-
 struct Vec3 {
     double x, y, z;
 };
@@ -104,11 +140,10 @@ __device__ __forceinline__ Vec3 vcross(Vec3 a, Vec3 b) {
     return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 
-// Principal decomposition of a symmetric 3x3 (Voigt 11,22,33,12,23,13) by cyclic Jacobi
-// with pivots (0,1),(0,2),(1,2), <= 8 sweeps, early stop when all off-diagonals are 0,
-// a pivot with |a_pq| <= 2^-60 (|a_pp|+|a_qq|) zeroed without rotation; rotation
-// theta = (a_qq-a_pp)/(2a_pq), t = sgn(theta)/(|theta|+sqrt(theta^2+1)), c = 1/sqrt(t^2+1),
-// s = t c (R8).  Output: eigenvalues l[3], eigenvector columns ev[i][k].
+// Principal decomposition by cyclic Jacobi (R8): pivots (0,1),(0,2),(1,2),
+// <= 8 sweeps, stop when all off-diagonals are 0, a pivot with |a_pq| <= 2^-60(|a_pp|+|a_qq|)
+// is zeroed without rotation; theta = (a_qq-a_pp)/(2a_pq), t = sgn(theta)/(|theta|+sqrt(theta^2+1)),
+// c = 1/sqrt(t^2+1), s = t c.
 struct Eig {
     double l[3];
     double ev[3][3];
@@ -171,7 +206,7 @@ __device__ void principal(const double *s6, Eig &E) {
     E.deg = deg;
 }
 
-// sigma_G . m, unnormalised (R8): sigma1 |e1.m|, or sigma1 sqrt(sum_{k in deg}(e_k.m)^2)
+// sigma_G . m unnormalised (R8): sigma1 |e1.m|, degenerate top eigenspace -> projector norm
 __device__ double sig_proj(const Eig &E, Vec3 m) {
     const int cnt = (E.deg & 1) + ((E.deg >> 1) & 1) + ((E.deg >> 2) & 1);
     if (cnt == 1) {
@@ -182,19 +217,44 @@ __device__ double sig_proj(const Eig &E, Vec3 m) {
     for (int k = 0; k < 3; ++k) {
         if (!(E.deg >> k & 1)) continue;
         const Vec3 e = {E.ev[0][k], E.ev[1][k], E.ev[2][k]};
-        const double d = vdot(e, m);
-        acc = acc + d * d;
+        const double dd = vdot(e, m);
+        acc = acc + dd * dd;
     }
     return E.l[E.k1] * sqrt(acc);
 }
 
 __device__ __forceinline__ double dsgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
 
-// Full evaluation of the 24 candidates (R7): returns best G, candidate, area.
-__device__ void evaluate_candidates(const Vec3 Xn[4], const Vec3 un[4], const int H[6], const double *sig6[6],
-                                    double &Gbest, int &kbest, double &Abest) {
+// All 24 candidates of tet e (R7): corner c, front {p,q} among the other nodes
+// o0<o1<o2 as (o0,o1),(o0,o2),(o1,o2), r the remaining node, k = 6c + 2f + t;
+// t=0 pattern I (eq:G-I) with m = (X_q-X_p)x(X_r-X_c), t=1 pattern II (eq:G-II) with
+// m = (X_q-X_p)x(X_r-X_p).  Select max G, ties -> larger area, then lower k.
+// Re-gathers its inputs (runs for the few tets that fail the early-out).
+__device__ __noinline__ void evaluate_tet(const Dev &d, int64_t e, const double4 *u, double &Gbest, int &kbest,
+                                          double &Abest) {
+    const int4 t = __ldg(&d.conn[e]);
+    const int nid[4] = {t.x, t.y, t.z, t.w};
+    Vec3 Xn[4], un[4];
+    for (int a = 0; a < 4; ++a) {
+        const double4 x = ldro4(&d.X[nid[a]]);
+        const double4 uu = ld4(&u[nid[a]]);
+        Xn[a] = {x.x, x.y, x.z};
+        un[a] = {uu.x, uu.y, uu.z};
+    }
+    int H[6];
+    for (int l = 0; l < 6; ++l) {
+        const Vec3 du = vsub(un[c_eq[l]], un[c_ep[l]]);
+        const Vec3 dX = vsub(Xn[c_eq[l]], Xn[c_ep[l]]);
+        const Vec3 w = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+        H[l] = vdot(du, w) > 0.0;  // eq:stretch-delta Heaviside, R6
+    }
     Eig eg[6];
-    for (int l = 0; l < 6; ++l) principal(sig6[l], eg[l]);
+    for (int l = 0; l < 6; ++l) {
+        const double *sg = d.srec + 8 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
+        double s6[6];
+        for (int i = 0; i < 6; ++i) s6[i] = sg[i];
+        principal(s6, eg[l]);
+    }
     Gbest = 0.0;
     kbest = -1;
     Abest = 0.0;
@@ -204,9 +264,9 @@ __device__ void evaluate_candidates(const Vec3 Xn[4], const Vec3 un[4], const in
             if (b != c) o[no++] = b;
         for (int f = 0; f < 3; ++f) {
             const int p = o[f == 2 ? 1 : 0], q = o[f == 0 ? 1 : 2], r = o[2 - f];
-            for (int t = 0; t < 2; ++t) {
+            for (int tt = 0; tt < 2; ++tt) {
                 const Vec3 d1 = vsub(Xn[q], Xn[p]);
-                const Vec3 d2 = t == 0 ? vsub(Xn[r], Xn[c]) : vsub(Xn[r], Xn[p]);
+                const Vec3 d2 = tt == 0 ? vsub(Xn[r], Xn[c]) : vsub(Xn[r], Xn[p]);
                 const Vec3 mv = vcross(d1, d2);
                 const double mm = vdot(mv, mv);
                 double Dd[2];
@@ -221,7 +281,7 @@ __device__ void evaluate_candidates(const Vec3 Xn[4], const Vec3 un[4], const in
                     Dd[z] = vdot(du, mv) * dsgn(vdot(dX, mv));
                 }
                 double G, area;
-                if (t == 0) {
+                if (tt == 0) {
                     const double A1 = sig_proj(eg[ledge(p, r)], mv) * Dd[0];
                     const double A2 = sig_proj(eg[ledge(q, r)], mv) * Dd[1];
                     G = (0.5 * (A1 + A2)) / mm;
@@ -231,7 +291,7 @@ __device__ void evaluate_candidates(const Vec3 Xn[4], const Vec3 un[4], const in
                     G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
                     area = sqrt(mm) / 8.0;
                 }
-                const int k = 6 * c + 2 * f + t;
+                const int k = 6 * c + 2 * f + tt;
                 if (kbest < 0 || G > Gbest || (G == Gbest && area > Abest)) {
                     Gbest = G;
                     kbest = k;
@@ -242,126 +302,126 @@ __device__ void evaluate_candidates(const Vec3 Xn[4], const Vec3 un[4], const in
     }
 }
 
-// ------------------------------------------------------------------ a3: element force + criterion
-__global__ void __launch_bounds__(kBlock) k_force(DevMesh m, DevState s, const double4 *__restrict__ u, int crack_every,
-                                                  int force_crack) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= m.E) return;
-    double2 *fo = reinterpret_cast<double2 *>(s.fe + 12 * e);
-    if (!m.state[e]) {
+// split: deactivate now (stage B/C of this step already consumed the
+// state; later readers are next-step stages), append a record (unordered; the host sorts
+// by (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
+__device__ __noinline__ void criterion_full(const Dev &d, int64_t e, const double4 *u, double gc, int64_t rec_step,
+                                            int32_t stamp) {
+    double G, A;
+    int k;
+    evaluate_tet(d, e, u, G, k, A);
+    if (G > gc) {
+        d.state[e] = 0;
+        const int slot = atomicAdd(&d.ctr[0], 1);
+        d.rec_step[slot] = rec_step;
+        d.rec_elem[slot] = ldro(d.tet_orig + e);
+        d.rec_cand[slot] = k;
+        d.rec_G[slot] = G;
+        d.rec_area[slot] = A;
+        const int4 t = __ldg(&d.conn[e]);
+        d.dirty[t.x] = stamp;
+        d.dirty[t.y] = stamp;
+        d.dirty[t.z] = stamp;
+        d.dirty[t.w] = stamp;
+    }
+}
+
+// ------------------------------------------------------------------ stage C: force + criterion
+// S = sum_{l=0..5} sigma_{s(e,l)}; f_{e,a} = c((gx S11 + gy S12) + gz S13), ... with c = V/6.
+// Early-out: every candidate satisfies |G| <= max_l g_{s(e,l)} *
+// max_l |u_q - u_p|; tets below Gc_e (1 - 1e-6) skip the 24-candidate evaluation.
+__device__ __forceinline__ void stage_C(const Dev &d, int64_t e, const double4 *u, bool crack, int64_t rec_step,
+                                        int32_t stamp) {
+    double2 *fo = reinterpret_cast<double2 *>(d.fe + 12 * e);
+    if (!d.state[e]) {
 #pragma unroll
         for (int i = 0; i < 6; ++i) fo[i] = make_double2(0.0, 0.0);
         return;
     }
-    const int32_t *ee = m.elem_edge + 6 * e;
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0;
-    double gmax = 0.0;
-    const double *sp[6];
+    const int64_t E = d.E;
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
 #pragma unroll
     for (int l = 0; l < 6; ++l) {
-        const double *sg = s.sig + 6 * (int64_t)__ldg(&ee[l]);
-        sp[l] = sg;
-        const double2 *q = reinterpret_cast<const double2 *>(sg);
-        const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+        const double2 *q = reinterpret_cast<const double2 *>(d.srec + 8 * (int64_t)ldro(d.eedge + (int64_t)l * E + e));
+        const double2 a = q[0], b = q[1], c = q[2], g = q[3];
         S0 = S0 + a.x; S1 = S1 + a.y; S2 = S2 + b.x;
         S3 = S3 + b.y; S4 = S4 + c.x; S5 = S5 + c.y;
-        // Gershgorin bound on the spectral radius of sigma_s (early-out)
-        const double r0 = fabs(a.x) + fabs(b.y) + fabs(c.y);
-        const double r1 = fabs(a.y) + fabs(b.y) + fabs(c.x);
-        const double r2 = fabs(b.x) + fabs(c.x) + fabs(c.y);
-        gmax = fmax(gmax, fmax(r0, fmax(r1, r2)));
+        gmax = fmax(gmax, g.x);
     }
-    const double *g = m.geo + 16 * e;
-    const double cc = ld_nc(g + 1);  // V_e / 6
+    double g[4][3];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double gx = ld_nc(g + 4 + 3 * a), gy = ld_nc(g + 5 + 3 * a), gz = ld_nc(g + 6 + 3 * a);
-        const double fx = cc * ((gx * S0 + gy * S3) + gz * S5);
-        const double fy = cc * ((gy * S1 + gx * S3) + gz * S4);
-        const double fz = cc * ((gz * S2 + gy * S4) + gx * S5);
-        s.fe[12 * e + 3 * a + 0] = fx;
-        s.fe[12 * e + 3 * a + 1] = fy;
-        s.fe[12 * e + 3 * a + 2] = fz;
-    }
-    // ---------------- crack criterion on (u_{n+1}, sigma(u_{n+1}))
-    if (!force_crack) {
-        if (crack_every <= 0) return;
-        const int64_t n1 = *s.step + 1;
-        if (n1 % crack_every != 0) return;
-    }
-    const int4 t = __ldg(&m.tet[e]);
-    const int nid[4] = {t.x, t.y, t.z, t.w};
-    Vec3 Xn[4], un[4];
+    for (int a = 1; a < 4; ++a)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double4 x = ldg4(&m.X[nid[a]]);
-        const double4 uu = ldg4(&u[nid[a]]);
-        Xn[a] = {x.x, x.y, x.z};
-        un[a] = {uu.x, uu.y, uu.z};
-    }
-    int H[6];
-    double d2max = 0.0;
+        for (int c = 0; c < 3; ++c) g[a][c] = ldro(d.geoG + (int64_t)(3 * (a - 1) + c) * E + e);
 #pragma unroll
-    for (int l = 0; l < 6; ++l) {
-        const Vec3 du = vsub(un[c_eq[l]], un[c_ep[l]]);
-        const Vec3 dX = vsub(Xn[c_eq[l]], Xn[c_ep[l]]);
-        const Vec3 w = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
-        H[l] = vdot(du, w) > 0.0;
-        if (H[l]) d2max = fmax(d2max, vdot(du, du));
+    for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+    const double cc = ldro(d.geoC + e);
+#pragma unroll
+    for (int a = 0; a < 4; a += 2) {
+        const double f0 = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
+        const double f1 = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
+        const double f2 = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
+        const double f3 = cc * ((g[a + 1][0] * S0 + g[a + 1][1] * S3) + g[a + 1][2] * S5);
+        const double f4 = cc * ((g[a + 1][1] * S1 + g[a + 1][0] * S3) + g[a + 1][2] * S4);
+        const double f5 = cc * ((g[a + 1][2] * S2 + g[a + 1][1] * S4) + g[a + 1][0] * S5);
+        fo[3 * (a >> 1) + 0] = make_double2(f0, f1);
+        fo[3 * (a >> 1) + 1] = make_double2(f2, f3);
+        fo[3 * (a >> 1) + 2] = make_double2(f4, f5);
     }
-    const double gc = __ldg(&m.gc[e]);
-    // every candidate satisfies |G| <= gmax * max_l H_l |du_l|
-    if (!(m.flags & CEM_F_NO_EARLY_OUT) && gmax * sqrt(d2max) * (1.0 + 1e-6) <= gc) return;
-    double G, A;
-    int k;
-    evaluate_candidates(Xn, un, H, sp, G, k, A);
-    if (G > gc) {
-        const int slot = atomicAdd(&s.ctr[0], 1);
-        if (slot < s.flag_cap) s.flag_list[slot] = (int32_t)e;
-        s.flag[e] = 1;
-        s.flag_cand[e] = k;
-        s.flag_G[e] = G;
-        s.flag_area[e] = A;
+    if (!crack) return;
+    const double gc = ldro(d.gc + e);
+    if (!(d.flags & CEM_F_NO_EARLY_OUT)) {
+        const int4 t = __ldg(&d.conn[e]);
+        const double4 u0 = ld4(&u[t.x]), u1 = ld4(&u[t.y]), u2 = ld4(&u[t.z]), u3 = ld4(&u[t.w]);
+        const double ux[4] = {u0.x, u1.x, u2.x, u3.x}, uy[4] = {u0.y, u1.y, u2.y, u3.y}, uz[4] = {u0.z, u1.z, u2.z, u3.z};
+        double d2 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 6; ++l) {
+            const int p = l < 3 ? 0 : (l < 5 ? 1 : 2), q = l < 3 ? l + 1 : (l < 5 ? l - 1 : 3);
+            const double dx = ux[q] - ux[p], dy = uy[q] - uy[p], dz = uz[q] - uz[p];
+            d2 = fmax(d2, (dx * dx + dy * dy) + dz * dz);
+        }
+        if (gmax * sqrt(d2) * (1.0 + 1e-6) <= gc) return;
     }
+    criterion_full(d, e, u, gc, rec_step, stamp);
 }
 
-// ------------------------------------------------------------------ a4: node update
-__global__ void __launch_bounds__(kBlock) k_node(DevMesh m, DevState s, const double4 *__restrict__ ucur,
-                                                 double4 *__restrict__ unext, double hdt2) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= m.N) return;
-    const int32_t j0 = __ldg(&m.node_off[k]), j1 = __ldg(&m.node_off[k + 1]);
+// ------------------------------------------------------------------ stage D: node update
+__device__ __forceinline__ void stage_D(const Dev &d, int64_t k, const double4 *u1p, double4 *u2p, int64_t s) {
+    const int32_t j0 = ldro(d.node_off + k), j1 = ldro(d.node_off + k + 1);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     for (int32_t j = j0; j < j1; ++j) {
-        const int32_t ent = __ldg(&m.node_ent[j]);
-        const double *f = s.fe + 12 * (int64_t)(ent >> 2) + 3 * (ent & 3);
-        f0 = f0 + __ldg(f);
-        f1 = f1 + __ldg(f + 1);
-        f2 = f2 + __ldg(f + 2);
+        const int32_t ent = ldro(d.node_ent + j);
+        const double *f = d.fe + 12 * (int64_t)(ent >> 2) + 3 * (ent & 3);
+        f0 = f0 + f[0];
+        f1 = f1 + f[1];
+        f2 = f2 + f[2];
     }
-    const double mk = m.mass[k];
-    const uint8_t fl = __ldg(&m.nflag[k]);
-    const double4 u1 = ucur[k];
-    double4 v = s.v[k], a = s.a[k];
-    const double dt = m.dt, gamma = m.gamma, omg = 1.0 - m.gamma;
-    double4 fx = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (fl & 8) fx = ldg4(&m.fext[k]);
-    const double fi[3] = {f0, f1, f2};
-    const double fe3[3] = {fx.x, fx.y, fx.z};
+    double mk = d.mass[k];
+    const uint8_t fl = __ldg(&d.nflag[k]);
+    const double4 u1 = ld4(&u1p[k]);
+    const double4 v = ld4(&d.v[k]), a = ld4(&d.a[k]);
+    const double dt = d.dt;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    if (fl & 8) {
+        const double4 w = ldro4(&d.fext[k]);
+        fx = w.x; fy = w.y; fz = w.z;
+    }
     double vv[3] = {v.x, v.y, v.z}, aa[3] = {a.x, a.y, a.z};
+    const double fi[3] = {f0, f1, f2}, fe3[3] = {fx, fy, fz};
     double vb0[3] = {0.0, 0.0, 0.0};
     if (fl & 7) {
-        const double4 w = ldg4(&m.dir_v0[k]);
+        const double4 w = ldro4(&d.dir_v0[k]);
         vb0[0] = w.x; vb0[1] = w.y; vb0[2] = w.z;
     }
-    const double t1 = (double)(*s.step + 1) * dt;
+    const double t1 = (double)(s + 1) * dt;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        if (mk == 0.0) {
+        if (mk == 0.0) {  // frozen node (R15)
             vv[c] = 0.0;
             aa[c] = 0.0;
         } else if (fl >> c & 1) {  // prescribed velocity ramp (R17)
-            const double t0 = m.t0, v0 = vb0[c];
+            const double t0 = d.t0, v0 = vb0[c];
             if (t0 <= 0.0) {
                 vv[c] = v0;
                 aa[c] = 0.0;
@@ -369,177 +429,182 @@ __global__ void __launch_bounds__(kBlock) k_node(DevMesh m, DevState s, const do
                 vv[c] = (t1 <= t0) ? (t1 / t0) * v0 : v0;
                 aa[c] = (t1 < t0) ? v0 / t0 : 0.0;
             }
-        } else {
+        } else {  // a = (f_ext - f_int)/m ; v += dt ((1-gamma) a_old + gamma a_new)
             const double an = (fe3[c] - fi[c]) / mk;
-            vv[c] = vv[c] + dt * (omg * aa[c] + gamma * an);
+            vv[c] = vv[c] + dt * (d.omg * aa[c] + d.gamma * an);
             aa[c] = an;
         }
     }
-    s.v[k] = make_double4(vv[0], vv[1], vv[2], 0.0);
-    s.a[k] = make_double4(aa[0], aa[1], aa[2], 0.0);
-    const double un0 = (u1.x + dt * vv[0]) + hdt2 * aa[0];
-    const double un1 = (u1.y + dt * vv[1]) + hdt2 * aa[1];
-    const double un2 = (u1.z + dt * vv[2]) + hdt2 * aa[2];
-    unext[k] = make_double4(un0, un1, un2, 0.0);
+    if (d.dirty[k] == (int32_t)(s + 1)) {
+        // an incident tet split in this step: lumped mass from the active incidences
+        // (original order); m = 0 -> frozen, v = a = 0 (R15)
+        double acc = 0.0;
+        for (int32_t j = j0; j < j1; ++j) {
+            const int32_t ee = ldro(d.node_ent + j) >> 2;
+            if (!d.state[ee]) continue;
+            acc = acc + (d.rho * ldro(d.geoV + ee)) / 4.0;
+        }
+        mk = acc;
+        d.mass[k] = acc;
+        if (acc == 0.0) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) vv[c] = aa[c] = 0.0;
+        }
+    }
+    st4(&d.v[k], vv[0], vv[1], vv[2], 0.0);
+    st4(&d.a[k], aa[0], aa[1], aa[2], 0.0);
+    // predictor u_{s+2} = u_{s+1} + dt v + dt^2/2 a
+    st4(&u2p[k], (u1.x + dt * vv[0]) + d.hdt2 * aa[0], (u1.y + dt * vv[1]) + d.hdt2 * aa[1],
+        (u1.z + dt * vv[2]) + d.hdt2 * aa[2], 0.0);
     if (!isfinite(u1.x) || !isfinite(u1.y) || !isfinite(u1.z) || !isfinite(vv[0]) || !isfinite(vv[1]) ||
         !isfinite(vv[2]) || !isfinite(aa[0]) || !isfinite(aa[1]) || !isfinite(aa[2])) {
-        s.ctr[1] = 1;
-        atomicMin(&s.ctr[2], (int32_t)k);
+        d.ctr[1] = 1;
+        atomicMin(&d.ctr[2], ldro(d.node_orig + k));
     }
 }
 
-// ------------------------------------------------------------------ a5: split pass (single block)
-constexpr int kSplitThreads = 1024;
-constexpr int kSortCap = 8192;
+__device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
+    return crack_every > 0 && ((s + 1) % crack_every) == 0;
+}
 
-__global__ void __launch_bounds__(kSplitThreads) k_split(DevMesh m, DevState s, double4 *__restrict__ u_src,
-                                                         double4 *__restrict__ u_dst, double hdt2, int advance) {
-    __shared__ int32_t list[kSortCap];
-    __shared__ int32_t n_sh;
+// ------------------------------------------------------------------ persistent wavefront kernel
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
+    __shared__ unsigned long long sh_q;
+    const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)d.P;
     const int tid = threadIdx.x;
-    const int32_t n = s.ctr[0];
-    const int64_t step_no = *s.step + (advance ? 1 : 0);
-    if (n == 0) {
+    for (;;) {
+        if (tid == 0) sh_q = atomicAdd(d.head, 1ull);
         __syncthreads();
-        if (tid == 0 && advance) *s.step = step_no;
-        return;
-    }
-    int32_t cnt;
-    int32_t *L;
-    if (n <= kSortCap && n <= s.flag_cap) {
-        // bitonic sort of the unordered flag list (ascending element id)
-        int P = 1;
-        while (P < n) P <<= 1;
-        for (int i = tid; i < P; i += kSplitThreads) list[i] = i < n ? s.flag_list[i] : INT32_MAX;
+        const unsigned long long q = sh_q;
+        if (q >= total) return;
+        const int64_t s = step0 + (int64_t)(q / (unsigned long long)d.P);
+        const int code = __ldg(d.sched + (q % (unsigned long long)d.P));
+        const int g = code >> 28, b = code & 0x0FFFFFFF;
+        // wait for the producer blocks (warp 0; lanes poll counters in parallel)
+        if (tid < 32) {
+            const int lo = __ldg(d.dep + ((int64_t)g * d.maxblk + b) * 2);
+            const int hi = __ldg(d.dep + ((int64_t)g * d.maxblk + b) * 2 + 1);
+            const int pg = g == ST_A ? ST_D : g - 1;
+            const int need = g == ST_A ? (int)s : (int)(s + 1);
+            const int32_t *c = d.cnt + (int64_t)pg * d.maxblk;
+            for (int i = lo + tid; i <= hi; i += 32)
+                while (ld_acquire(c + i) < need) __nanosleep(64);
+            __syncwarp();
+            if (tid == 0) __threadfence();  // order + invalidate this SM's L1 before the reads
+        }
         __syncthreads();
-        for (int k = 2; k <= P; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = tid; i < P; i += kSplitThreads) {
-                    const int ixj = i ^ j;
-                    if (ixj > i) {
-                        const int32_t x = list[i], y = list[ixj];
-                        const bool up = (i & k) == 0;
-                        if ((x > y) == up) {
-                            list[i] = y;
-                            list[ixj] = x;
-                        }
-                    }
-                }
-                __syncthreads();
-            }
-        cnt = n;
-        L = list;
-    } else {
-        // overflow: ordered scan of the flag bytes over all tets into flag_list (capacity E)
-        if (tid == 0) n_sh = 0;
+        const int64_t i0 = (int64_t)b * d.blk;
+        const int64_t i = i0 + tid;
+        const double4 *u1 = d.ubuf[(s + 1) & 1];
+        switch (g) {
+            case ST_A:
+                if (i < d.E) stage_A(d, i, u1);
+                break;
+            case ST_B:
+                if (i < d.S) stage_B(d, i);
+                break;
+            case ST_C:
+                if (i < d.E) stage_C(d, i, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1));
+                break;
+            default:
+                if (i < d.N) stage_D(d, i, u1, d.ubuf[s & 1], s);
+                break;
+        }
         __syncthreads();
-        __shared__ int32_t warp_tot[32];
-        for (int64_t base = 0; base < m.E; base += kSplitThreads) {
-            const int64_t e = base + tid;
-            const int f = (e < m.E) ? s.flag[e] : 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            const int lane = tid & 31, w = tid >> 5;
-            if (lane == 0) warp_tot[w] = __popc(bal);
-            __syncthreads();
-            int off = 0;
-            for (int i = 0; i < w; ++i) off += warp_tot[i];
-            const int pos = n_sh + off + __popc(bal & ((1u << lane) - 1u));
-            if (f) s.flag_list[pos] = (int32_t)e;
-            __syncthreads();
-            if (tid == 0) {
-                int tot = 0;
-                for (int i = 0; i < 32; ++i) tot += warp_tot[i];
-                n_sh += tot;
-            }
-            __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicExch(d.cnt + (int64_t)g * d.maxblk + b, (int)(s + 1));
         }
-        cnt = n_sh;
-        L = s.flag_list;
-    }
-    __syncthreads();
-    const int64_t r0 = *s.nrec;
-    // deactivate + records (ascending element id)
-    for (int i = tid; i < cnt; i += kSplitThreads) {
-        const int32_t e = L[i];
-        m.state[e] = 0;
-        s.flag[e] = 0;
-        s.rec_step[r0 + i] = step_no;
-        s.rec_elem[r0 + i] = e;
-        s.rec_cand[r0 + i] = s.flag_cand[e];
-        s.rec_G[r0 + i] = s.flag_G[e];
-        s.rec_area[r0 + i] = s.flag_area[e];
-    }
-    if (tid == 0) {
-        double Ud = *s.Ud;
-        for (int i = 0; i < cnt; ++i) {
-            const int32_t e = L[i];
-            Ud = Ud + m.gc[e] * s.flag_area[e];
-        }
-        *s.Ud = Ud;
-    }
-    __syncthreads();
-    __threadfence_block();
-    // lumped mass of the nodes of split tets, recomputed from the active incidences
-    const double rho = m.rho, dt = m.dt;
-    for (int i = tid; i < 4 * cnt; i += kSplitThreads) {
-        const int32_t e = L[i >> 2];
-        const int4 t = m.tet[e];
-        const int32_t k = (i & 3) == 0 ? t.x : ((i & 3) == 1 ? t.y : ((i & 3) == 2 ? t.z : t.w));
-        double acc = 0.0;
-        for (int32_t j = m.node_off[k]; j < m.node_off[k + 1]; ++j) {
-            const int32_t ee = m.node_ent[j] >> 2;
-            if (!m.state[ee]) continue;
-            acc = acc + (rho * m.geo[16 * (int64_t)ee]) / 4.0;
-        }
-        m.mass[k] = acc;
-        if (acc == 0.0) {  // frozen node: v = a = 0, prediction restarts from u
-            s.v[k] = make_double4(0.0, 0.0, 0.0, 0.0);
-            s.a[k] = make_double4(0.0, 0.0, 0.0, 0.0);
-            const double4 us = u_src[k];
-            u_dst[k] = make_double4((us.x + dt * 0.0) + hdt2 * 0.0, (us.y + dt * 0.0) + hdt2 * 0.0,
-                                    (us.z + dt * 0.0) + hdt2 * 0.0, 0.0);
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        *s.nrec = r0 + cnt;
-        s.ctr[0] = 0;
-        if (advance) *s.step = step_no;
     }
 }
 
-inline unsigned nblk(int64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
+// ------------------------------------------------------------------ staged kernels (one per stage)
+__global__ void __launch_bounds__(256) k_A(Dev d, int64_t s) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < d.E) stage_A(d, e, d.ubuf[(s + 1) & 1]);
+}
+__global__ void __launch_bounds__(256) k_B(Dev d) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < d.S) stage_B(d, i);
+}
+__global__ void __launch_bounds__(256) k_C(Dev d, int64_t s, int crack_every) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < d.E) stage_C(d, e, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1));
+}
+__global__ void __launch_bounds__(256) k_D(Dev d, int64_t s) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < d.N) stage_D(d, k, d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+}
+
+// criterion on the current state u_n (cem_crack_update)
+__global__ void __launch_bounds__(256) k_A_cur(Dev d, int64_t n) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < d.E) stage_A(d, e, d.ubuf[n & 1]);
+}
+__global__ void __launch_bounds__(256) k_C_cur(Dev d, int64_t n, int32_t stamp) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < d.E) stage_C(d, e, d.ubuf[n & 1], true, n, stamp);
+}
+// nodes of tets split by cem_crack_update: new mass; frozen -> v = a = 0 and the pending
+// prediction u_{n+1} restarts from u_n
+__global__ void __launch_bounds__(256) k_fix_cur(Dev d, int64_t n, int32_t stamp) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= d.N || d.dirty[k] != stamp) return;
+    double acc = 0.0;
+    for (int32_t j = d.node_off[k]; j < d.node_off[k + 1]; ++j) {
+        const int32_t ee = d.node_ent[j] >> 2;
+        if (!d.state[ee]) continue;
+        acc = acc + (d.rho * d.geoV[ee]) / 4.0;
+    }
+    d.mass[k] = acc;
+    if (acc == 0.0) {
+        st4(&d.v[k], 0.0, 0.0, 0.0, 0.0);
+        st4(&d.a[k], 0.0, 0.0, 0.0, 0.0);
+        const double4 un = ld4(&d.ubuf[n & 1][k]);
+        st4(&d.ubuf[(n + 1) & 1][k], (un.x + d.dt * 0.0) + d.hdt2 * 0.0, (un.y + d.dt * 0.0) + d.hdt2 * 0.0,
+            (un.z + d.dt * 0.0) + d.hdt2 * 0.0, 0.0);
+    }
+}
+
+inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
 
-void launch_strain(const DevMesh &m, const DevState &s, int cur, cudaStream_t st) {
-    k_strain<<<nblk(m.E), kBlock, 0, st>>>(m, s.u[cur ^ 1], s.tau);
-}
-void launch_edge(const DevMesh &m, const DevState &s, cudaStream_t st) {
-    k_edge<<<nblk(m.S), kBlock, 0, st>>>(m, s.tau, s.sig);
-}
-void launch_force(const DevMesh &m, const DevState &s, int cur, int crack_every, cudaStream_t st) {
-    k_force<<<nblk(m.E), kBlock, 0, st>>>(m, s, s.u[cur ^ 1], crack_every, 0);
-}
-void launch_node(const DevMesh &m, const DevState &s, int cur, cudaStream_t st) {
-    const double hdt2 = 0.5 * m.dt * m.dt;
-    k_node<<<nblk(m.N), kBlock, 0, st>>>(m, s, s.u[cur ^ 1], s.u[cur], hdt2);
-}
-void launch_split(const DevMesh &m, const DevState &s, int cur, int crack_every, int advance, cudaStream_t st) {
-    (void)crack_every;
-    const double hdt2 = 0.5 * m.dt * m.dt;
-    // step mode: u_{n+1} lives in u[cur^1], u_{n+2} was written to u[cur]
-    k_split<<<1, kSplitThreads, 0, st>>>(m, s, s.u[cur ^ 1], s.u[cur], hdt2, advance);
+int persistent_occupancy() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent, 256, 0);
+    return n;
 }
 
-// criterion-only variant on the current state u_n = u[cur] (cem_crack_update)
-void launch_crack_only(const DevMesh &m, const DevState &s, int cur, cudaStream_t st) {
-    k_strain<<<nblk(m.E), kBlock, 0, st>>>(m, s.u[cur], s.tau);
-    k_edge<<<nblk(m.S), kBlock, 0, st>>>(m, s.tau, s.sig);
-    k_force<<<nblk(m.E), kBlock, 0, st>>>(m, s, s.u[cur], 1, 1);
-    const double hdt2 = 0.5 * m.dt * m.dt;
-    // a node frozen here restarts its prediction u_{n+1} (in u[cur^1]) from u_n (in u[cur])
-    k_split<<<1, kSplitThreads, 0, st>>>(m, s, s.u[cur], s.u[cur ^ 1], hdt2, 0);
+void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st) {
+    cudaMemsetAsync(d.head, 0, sizeof(unsigned long long), st);
+    k_persistent<<<grid, 256, 0, st>>>(d, step0, nsteps, crack_every);
+}
+
+void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
+    if (ev) cudaEventRecord(ev[0], st);
+    k_A<<<nblk(d.E), 256, 0, st>>>(d, s);
+    if (ev) cudaEventRecord(ev[1], st);
+    k_B<<<nblk(d.S), 256, 0, st>>>(d);
+    if (ev) cudaEventRecord(ev[2], st);
+    k_C<<<nblk(d.E), 256, 0, st>>>(d, s, crack_every);
+    if (ev) cudaEventRecord(ev[3], st);
+    k_D<<<nblk(d.N), 256, 0, st>>>(d, s);
+    if (ev) cudaEventRecord(ev[4], st);
+}
+
+void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st) {
+    const int32_t stamp = -(int32_t)(n + 1);
+    k_A_cur<<<nblk(d.E), 256, 0, st>>>(d, n);
+    k_B<<<nblk(d.S), 256, 0, st>>>(d);
+    k_C_cur<<<nblk(d.E), 256, 0, st>>>(d, n, stamp);
+    k_fix_cur<<<nblk(d.N), 256, 0, st>>>(d, n, stamp);
 }
 
 }  // namespace cem

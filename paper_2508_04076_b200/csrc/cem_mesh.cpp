@@ -113,7 +113,8 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
     // ---------------------------------------------------------------- geometry
     // det = d1.(d2 x d3), V = det/6, inv = 1/det, gradN1 = (d2xd3) inv, gradN2 = (d3xd1) inv,
     // gradN3 = (d1xd2) inv, gradN0 = -((gradN1 + gradN2) + gradN3)
-    h.geo.assign(16 * E, 0.0);
+    h.V.assign(E, 0.0);
+    h.grad.assign(12 * E, 0.0);
     int64_t bad_neg = -1, bad_deg = -1;
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < E; ++e) {
@@ -123,7 +124,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         V3 c23 = cross(d2, d3), c31 = cross(d3, d1), c12 = cross(d1, d2);
         double det = dot(d1, c23);
         double V = det / 6.0;
-        double *g = h.geo.data() + 16 * e;
+        double *g = h.grad.data() + 12 * e;
         if (det < 0) {
 #pragma omp critical
             bad_neg = bad_neg < 0 ? e : std::min(bad_neg, e);
@@ -135,15 +136,14 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
             continue;
         }
         double inv = 1.0 / det;
-        g[0] = V;
-        g[1] = V / 6.0;
+        h.V[e] = V;
         double gr[4][3];
         const double cc[3][3] = {{c23.x, c23.y, c23.z}, {c31.x, c31.y, c31.z}, {c12.x, c12.y, c12.z}};
         for (int a = 1; a < 4; ++a)
             for (int c = 0; c < 3; ++c) gr[a][c] = cc[a - 1][c] * inv;
         for (int c = 0; c < 3; ++c) gr[0][c] = -((gr[1][c] + gr[2][c]) + gr[3][c]);
         for (int a = 0; a < 4; ++a)
-            for (int c = 0; c < 3; ++c) g[4 + 3 * a + c] = gr[a][c];
+            for (int c = 0; c < 3; ++c) g[3 * a + c] = gr[a][c];
     }
     if (bad_neg >= 0) {
         err = "tet " + std::to_string(bad_neg) + ": negative orientation";
@@ -219,7 +219,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         for (int32_t j = h.node_off[n]; j < h.node_off[n + 1]; ++j) {
             int32_t e = h.node_ent[j] >> 2;
             if (!h.state[e]) continue;
-            acc = acc + (h.rho * h.geo[16 * (int64_t)e]) / 4.0;
+            acc = acc + (h.rho * h.V[e]) / 4.0;
         }
         h.mass[n] = acc;
     }
@@ -282,7 +282,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
                 double A = 0.5 * std::sqrt(dot(cr, cr));
                 if (A > amax) amax = A;
             }
-            double alt = 3.0 * h.geo[16 * e] / amax;
+            double alt = 3.0 * h.V[e] / amax;
             if (alt < altmin) altmin = alt;
         }
         if (!std::isfinite(altmin)) {
