@@ -60,15 +60,16 @@ struct Layout {
 };
 
 struct Offs {
-    size_t conn, geoV, geoC, geoG, eedge, edge_off, edge_inc, node_off, node_ent, X, fext, nflag, dir_v0, gc;
+    size_t conn, geoV, geoC, geoG, eedge, edge_off, node_off, node_ent, X, fext, nflag, dir_v0, gc;
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, trec, srec, fe, ctr;
-    size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep, sched, head;
+    size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
+    size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, inc_local, fpos, gbase;
     size_t total;
 };
 
-Offs layout(int64_t N, int64_t E, int64_t S, bool dir) {
-    const int64_t nb[4] = {(E + kBlk - 1) / kBlk, (S + kBlk - 1) / kBlk, (E + kBlk - 1) / kBlk, (N + kBlk - 1) / kBlk};
-    const int64_t maxblk = *std::max_element(nb, nb + 4), P = nb[0] + nb[1] + nb[2] + nb[3];
+Offs layout(const HostMesh &h, const Plan &p) {
+    const int64_t N = h.N, E = h.E, S = h.S;
+    const int64_t P = p.nblk[0] + p.nblk[1] + p.nblk[2] + p.nblk[3];
     Layout L;
     Offs o{};
     o.conn = L.take<int4>(E);
@@ -77,13 +78,12 @@ Offs layout(int64_t N, int64_t E, int64_t S, bool dir) {
     o.geoG = L.take<double>(9 * E);
     o.eedge = L.take<int32_t>(6 * E);
     o.edge_off = L.take<int32_t>(S + 1);
-    o.edge_inc = L.take<int32_t>(6 * E);
     o.node_off = L.take<int32_t>(N + 1);
     o.node_ent = L.take<int32_t>(4 * E);
     o.X = L.take<double4>(N);
     o.fext = L.take<double4>(N);
     o.nflag = L.take<uint8_t>(N);
-    o.dir_v0 = L.take<double4>(dir ? N : 1);
+    o.dir_v0 = L.take<double4>(h.any_dirichlet ? N : 1);
     o.gc = L.take<double>(E);
     o.tet_orig = L.take<int32_t>(E);
     o.node_orig = L.take<int32_t>(N);
@@ -96,19 +96,36 @@ Offs layout(int64_t N, int64_t E, int64_t S, bool dir) {
     o.a = L.take<double4>(N);
     o.trec = L.take<double>(8 * E);
     o.srec = L.take<double>(8 * S);
-    o.fe = L.take<double>(12 * E);
+    o.fe = L.take<double4>(p.nslots);
     o.ctr = L.take<int32_t>(8);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
     o.rec_cand = L.take<int32_t>(E);
     o.rec_G = L.take<double>(E);
     o.rec_area = L.take<double>(E);
-    o.cnt = L.take<int32_t>(4 * maxblk);
-    o.dep = L.take<int32_t>(8 * maxblk);
+    o.cnt = L.take<int32_t>(4 * (int64_t)p.maxblk);
+    o.dep_off = L.take<int32_t>((int64_t)p.dep_off.size());
+    o.dep = L.take<int32_t>((int64_t)p.dep.size());
     o.sched = L.take<int32_t>(P);
     o.head = L.take<unsigned long long>(1);
+    o.nl_off = L.take<int32_t>((int64_t)p.nl_off.size());
+    o.nl = L.take<int32_t>((int64_t)p.nl.size());
+    o.lconn = L.take<uint16_t>((int64_t)p.lconn.size());
+    o.el_off = L.take<int32_t>((int64_t)p.el_off.size());
+    o.el = L.take<int32_t>((int64_t)p.el.size());
+    o.ledge = L.take<uint16_t>((int64_t)p.ledge.size());
+    o.tl_off = L.take<int32_t>((int64_t)p.tl_off.size());
+    o.tl = L.take<int32_t>((int64_t)p.tl.size());
+    o.inc_local = L.take<uint16_t>((int64_t)p.inc_local.size());
+    o.fpos = L.take<int32_t>((int64_t)p.fpos.size());
+    o.gbase = L.take<int32_t>((int64_t)p.gbase.size());
     o.total = L.off;
     return o;
+}
+
+int smem_bytes_for(const Plan &p) {
+    const int n = std::max({3 * p.max_nl, 7 * p.max_tl, 7 * p.max_el + 3 * p.max_nl});
+    return 8 * n;
 }
 
 template <class T>
@@ -130,7 +147,6 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.geoG = at<double>(b, o.geoG);
     d.eedge = at<int32_t>(b, o.eedge);
     d.edge_off = at<int32_t>(b, o.edge_off);
-    d.edge_inc = at<int32_t>(b, o.edge_inc);
     d.node_off = at<int32_t>(b, o.node_off);
     d.node_ent = at<int32_t>(b, o.node_ent);
     d.X = at<double4>(b, o.X);
@@ -149,7 +165,19 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.a = at<double4>(b, o.a);
     d.trec = at<double>(b, o.trec);
     d.srec = at<double>(b, o.srec);
-    d.fe = at<double>(b, o.fe);
+    d.fe = at<double4>(b, o.fe);
+    d.nl_off = at<int32_t>(b, o.nl_off);
+    d.nl = at<int32_t>(b, o.nl);
+    d.lconn = at<uint16_t>(b, o.lconn);
+    d.el_off = at<int32_t>(b, o.el_off);
+    d.el = at<int32_t>(b, o.el);
+    d.ledge = at<uint16_t>(b, o.ledge);
+    d.tl_off = at<int32_t>(b, o.tl_off);
+    d.tl = at<int32_t>(b, o.tl);
+    d.inc_local = at<uint16_t>(b, o.inc_local);
+    d.fpos = at<int4>(b, o.fpos);
+    d.gbase = at<int32_t>(b, o.gbase);
+    d.smem_bytes = smem_bytes_for(p);
     d.ctr = at<int32_t>(b, o.ctr);
     d.rec_step = at<int64_t>(b, o.rec_step);
     d.rec_elem = at<int32_t>(b, o.rec_elem);
@@ -157,6 +185,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.rec_G = at<double>(b, o.rec_G);
     d.rec_area = at<double>(b, o.rec_area);
     d.cnt = at<int32_t>(b, o.cnt);
+    d.dep_off = at<int32_t>(b, o.dep_off);
     d.dep = at<int32_t>(b, o.dep);
     d.sched = at<int32_t>(b, o.sched);
     d.head = at<unsigned long long>(b, o.head);
@@ -231,7 +260,6 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.geoG, p.geoG.data(), sizeof(double) * 9 * E));
     CUDA_TRY(put(o.eedge, p.eedge.data(), sizeof(int32_t) * 6 * E));
     CUDA_TRY(put(o.edge_off, p.edge_off.data(), sizeof(int32_t) * (S + 1)));
-    CUDA_TRY(put(o.edge_inc, p.edge_inc.data(), sizeof(int32_t) * p.edge_inc.size()));
     CUDA_TRY(put(o.node_off, p.node_off.data(), sizeof(int32_t) * (N + 1)));
     CUDA_TRY(put(o.node_ent, p.node_ent.data(), sizeof(int32_t) * p.node_ent.size()));
     CUDA_TRY(put(o.X, X4.data(), sizeof(double4) * N));
@@ -250,11 +278,23 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.trec), 0, sizeof(double) * 8 * E, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 8 * S, st));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * 12 * E, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * p.nslots, st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * 4 * p.maxblk, st));
+    CUDA_TRY(put(o.dep_off, p.dep_off.data(), sizeof(int32_t) * p.dep_off.size()));
     CUDA_TRY(put(o.dep, p.dep.data(), sizeof(int32_t) * p.dep.size()));
+    CUDA_TRY(put(o.nl_off, p.nl_off.data(), sizeof(int32_t) * p.nl_off.size()));
+    CUDA_TRY(put(o.nl, p.nl.data(), sizeof(int32_t) * p.nl.size()));
+    CUDA_TRY(put(o.lconn, p.lconn.data(), sizeof(uint16_t) * p.lconn.size()));
+    CUDA_TRY(put(o.el_off, p.el_off.data(), sizeof(int32_t) * p.el_off.size()));
+    CUDA_TRY(put(o.el, p.el.data(), sizeof(int32_t) * p.el.size()));
+    CUDA_TRY(put(o.ledge, p.ledge.data(), sizeof(uint16_t) * p.ledge.size()));
+    CUDA_TRY(put(o.tl_off, p.tl_off.data(), sizeof(int32_t) * p.tl_off.size()));
+    CUDA_TRY(put(o.tl, p.tl.data(), sizeof(int32_t) * p.tl.size()));
+    CUDA_TRY(put(o.inc_local, p.inc_local.data(), sizeof(uint16_t) * p.inc_local.size()));
+    CUDA_TRY(put(o.fpos, p.fpos.data(), sizeof(int32_t) * p.fpos.size()));
+    CUDA_TRY(put(o.gbase, p.gbase.data(), sizeof(int32_t) * p.gbase.size()));
     CUDA_TRY(put(o.sched, p.sched.data(), sizeof(int32_t) * p.sched.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.head), 0, sizeof(unsigned long long), st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -276,11 +316,18 @@ const char *cem_last_error(const cem_ctx *ctx) { return ctx ? ctx->err.c_str() :
 
 cem_status cem_workspace_size(const cem_mesh_in *mesh, const cem_opts *opts, size_t *bytes) {
     if (!mesh || !bytes) return CEM_EINVAL;
-    int64_t S = 0;
-    cem_status st = count_edges(mesh, &S, g_init_err);
+    // the exact size depends on the storage plan: build it (no device work)
+    const cem_material mat = {1.0, 0.0, 1.0, 0.0};
+    cem_opts o{};
+    if (opts) o = *opts;
+    o.dt = 1.0;
+    HostMesh h;
+    Plan p;
+    cem_status st = build_host_mesh(mesh, &mat, nullptr, &o, h, g_init_err);
     if (st) return st;
-    (void)opts;
-    *bytes = layout(mesh->n_nodes, mesh->n_tets, S, true).total;
+    h.any_dirichlet = true;
+    build_plan(h, kBlk, p);
+    *bytes = layout(h, p).total;
     return CEM_OK;
 }
 
@@ -310,11 +357,18 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         ctx->err = "cudaSetDevice failed (no CUDA device?)";
         return fail(CEM_ECUDA);
     }
+    build_plan(ctx->h, kBlk, ctx->p);
+    const int smem = smem_bytes_for(ctx->p);
+    if (smem > 227 * 1024) {
+        ctx->err = "a block's gather list exceeds shared memory (" + std::to_string(smem) + " bytes)";
+        return fail(CEM_EINVAL);
+    }
+    set_smem_limits(smem);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    const int occ = std::max(1, persistent_occupancy());
+    const int occ = std::max(1, persistent_occupancy(smem));
     ctx->grid = sms * occ;
-    build_plan(ctx->h, kBlk, ctx->grid, ctx->p);
+    build_schedule(ctx->p, ctx->grid);
     if (!ctx->stream) {  // graphs / persistent launches never use the legacy default stream
         if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
             ctx->err = "cudaStreamCreate failed";
@@ -322,7 +376,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         }
         ctx->own_stream = true;
     }
-    Offs o = layout(ctx->h.N, ctx->h.E, ctx->h.S, ctx->h.any_dirichlet);
+    Offs o = layout(ctx->h, ctx->p);
     if (opts && opts->workspace) {
         if (opts->workspace_bytes < o.total) {
             ctx->err = "workspace too small: need " + std::to_string(o.total) + " bytes";

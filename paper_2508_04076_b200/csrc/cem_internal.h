@@ -61,11 +61,25 @@ struct Plan {
     int blk = 256;                    // entities per work item
     int nblk[ST_COUNT] = {0, 0, 0, 0};
     int maxblk = 0;
-    std::vector<int32_t> dep;         // [ST_COUNT][maxblk][2]: producer block range [lo, hi]
+    std::vector<int32_t> dep_off;     // [ST_COUNT * maxblk + 1] CSR of producer blocks per (stage, block)
+    std::vector<int32_t> dep;         // producer block ids (of the producing stage)
     std::vector<int32_t> sched;       // [P]: stage << 28 | block
+    // block gather lists (deduplicated producer records staged in shared memory)
+    std::vector<int32_t> nl_off, nl;  // tet block -> sorted unique node ids
+    std::vector<uint16_t> lconn;      // [E][4] index of each tet node in its block's node list
+    std::vector<int32_t> el_off, el;  // tet block -> sorted unique edge ids
+    std::vector<uint16_t> ledge;      // [E][8] index of each tet edge in its block's edge list (6 used)
+    std::vector<int32_t> tl_off, tl;  // edge block -> sorted unique incident tet ids
+    std::vector<uint16_t> inc_local;  // [6E] (CSR order of edge_inc) index into the edge block's tet list
+    std::vector<int32_t> fpos;        // [E][4] slot of f_{e,a} in the node-major force array
+    std::vector<int32_t> gbase;       // [N/32 + 1] warp-interleaved force slots: node k = 32 g + lane,
+                                      //   its j-th incidence at gbase[g] + 32 j + lane
+    int64_t nslots = 0;
+    int max_nl = 0, max_el = 0, max_tl = 0;
 };
 
-void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p);
+void build_plan(const HostMesh &h, int blk, Plan &p);
+void build_schedule(Plan &p, int resident_ctas);
 
 // ---------------------------------------------------------------- device view
 struct Dev {
@@ -91,7 +105,11 @@ struct Dev {
     double4 *v, *a;
     double *trec;              // [E][8]: V_e eps_e (6), V_e if active else 0, pad
     double *srec;              // [S][8]: sigma_s (6), Gershgorin bound g_s, pad
-    double *fe;                // [E][12]
+    double4 *fe;               // [nslots] node-major force slots f_{e,a} (x,y,z,pad) at fpos[e][a]
+    const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *gbase;
+    const int4 *fpos;
+    const uint16_t *lconn, *ledge, *inc_local;
+    int smem_bytes;
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] spare
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
@@ -101,7 +119,7 @@ struct Dev {
     uint32_t flags;
     // persistent wavefront
     int32_t *cnt;              // [ST_COUNT][maxblk] completed-step counters
-    const int32_t *dep;        // [ST_COUNT][maxblk][2]
+    const int32_t *dep_off, *dep;
     const int32_t *sched;      // [P]
     unsigned long long *head;  // work-queue head
     int blk, P, maxblk;
@@ -112,7 +130,8 @@ struct Dev {
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
-int persistent_occupancy();  // resident CTAs per SM of the persistent kernel
+int persistent_occupancy(int smem_bytes);  // resident CTAs per SM of the persistent kernel
+void set_smem_limits(int smem_bytes);
 extern const int kThreads;
 
 }  // namespace cem

@@ -48,17 +48,47 @@ __device__ __forceinline__ void st4(double4 *p, double x, double y, double z, do
     q[1] = make_double2(z, w);
 }
 
+__device__ __forceinline__ double4 ld256(const double4 *p) {  // LDG.E.256 (sm_100)
+    double4 r;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st256(double4 *p, double x, double y, double z, double w) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
+}
+
+// Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
+// (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
+// every later per-thread gather hits shared memory instead of an L1 line of its own.
+__device__ __forceinline__ void stage_nodes(const Dev &d, const double4 *u, int32_t n0, int nn, double *pl) {
+    for (int i = threadIdx.x; i < 3 * nn; i += blockDim.x) {
+        const int r = i / 3, c = i - 3 * r;
+        pl[c * nn + r] = reinterpret_cast<const double *>(u + __ldg(d.nl + n0 + r))[c];
+    }
+}
+__device__ __forceinline__ void stage_records(const double *src, const int32_t *ids, int n, int ncomp, double *pl) {
+    for (int i = threadIdx.x; i < 8 * n; i += blockDim.x) {
+        const int r = i >> 3, c = i & 7;
+        if (c < ncomp) pl[c * n + r] = src[8 * (int64_t)__ldg(ids + r) + c];
+    }
+}
+
 // ------------------------------------------------------------------ stage A: element strain
 // eps = sum_a B_a u_a (a = 0..3 in order), Voigt (11,22,33,12,23,13) with engineering
 // shears; gradN0 = -((gradN1 + gradN2) + gradN3); tau = V eps.  Record: tau (6), V if
 // active else 0, pad.
-__device__ __forceinline__ void stage_A(const Dev &d, int64_t e, const double4 *u) {
-    double2 *o = reinterpret_cast<double2 *>(d.trec + 8 * e);
+__device__ __forceinline__ void block_A(const Dev &d, int b, const double4 *u, double *sm) {
+    const int32_t n0 = __ldg(d.nl_off + b);
+    const int nn = __ldg(d.nl_off + b + 1) - n0;
+    stage_nodes(d, u, n0, nn, sm);
+    __syncthreads();
+    const int64_t e = (int64_t)b * d.blk + threadIdx.x;
+    if (e >= d.E) return;
+    double4 *o = reinterpret_cast<double4 *>(d.trec + 8 * e);
     if (!d.state[e]) {
-        o[3] = make_double2(0.0, 0.0);  // V slot = 0 marks "inactive" for stage B
+        st256(o + 1, 0.0, 0.0, 0.0, 0.0);  // V slot = 0 marks "inactive" for stage B
         return;
     }
-    const int4 t = __ldg(&d.conn[e]);
     const int64_t E = d.E;
     double g[4][3];
 #pragma unroll
@@ -68,45 +98,53 @@ __device__ __forceinline__ void stage_A(const Dev &d, int64_t e, const double4 *
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
     const double V = ldro(d.geoV + e);
-    const double4 u0 = ld4(&u[t.x]), u1 = ld4(&u[t.y]), u2 = ld4(&u[t.z]), u3 = ld4(&u[t.w]);
-    const double ux[4] = {u0.x, u1.x, u2.x, u3.x}, uy[4] = {u0.y, u1.y, u2.y, u3.y}, uz[4] = {u0.z, u1.z, u2.z, u3.z};
+    const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
+    const int li[4] = {lc.x, lc.y, lc.z, lc.w};
     double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
+        const double ux = sm[li[a]], uy = sm[nn + li[a]], uz = sm[2 * nn + li[a]];
         const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
-        ex = ex + gx * ux[a];
-        ey = ey + gy * uy[a];
-        ez = ez + gz * uz[a];
-        gxy = gxy + (gy * ux[a] + gx * uy[a]);
-        gyz = gyz + (gz * uy[a] + gy * uz[a]);
-        gxz = gxz + (gz * ux[a] + gx * uz[a]);
+        ex = ex + gx * ux;
+        ey = ey + gy * uy;
+        ez = ez + gz * uz;
+        gxy = gxy + (gy * ux + gx * uy);
+        gyz = gyz + (gz * uy + gy * uz);
+        gxz = gxz + (gz * ux + gx * uz);
     }
-    o[0] = make_double2(V * ex, V * ey);
-    o[1] = make_double2(V * ez, V * gxy);
-    o[2] = make_double2(V * gyz, V * gxz);
-    o[3] = make_double2(V, 0.0);
+    st256(o, V * ex, V * ey, V * ez, V * gxy);
+    st256(o + 1, V * gyz, V * gxz, V, 0.0);
 }
 
 // ------------------------------------------------------------------ stage B: edge stress
 // Vhat = sum V_e, T = sum tau_e over active incident tets in original-id order;
 // eps~ = T * (1/Vhat); sigma_ii = (lam+2mu) eps_ii + lam (eps_jj + eps_kk), sigma_ij = mu gamma_ij.
 // Also the Gershgorin bound g = max_i sum_j |sigma_ij| (early-out of stage C).
-__device__ __forceinline__ void stage_B(const Dev &d, int64_t s) {
+__device__ __forceinline__ void block_B(const Dev &d, int b, double *sm) {
+    const int32_t t0 = __ldg(d.tl_off + b);
+    const int nt = __ldg(d.tl_off + b + 1) - t0;
+    stage_records(d.trec, d.tl + t0, nt, 7, sm);
+    __syncthreads();
+    const int64_t s = (int64_t)b * d.blk + threadIdx.x;
+    if (s >= d.S) return;
     const int32_t j0 = ldro(d.edge_off + s), j1 = ldro(d.edge_off + s + 1);
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
     for (int32_t j = j0; j < j1; ++j) {
-        const int32_t e = ldro(d.edge_inc + j);
-        const double2 *r = reinterpret_cast<const double2 *>(d.trec + 8 * (int64_t)e);
-        const double Ve = r[3].x;
+        const int r = __ldg(d.inc_local + j);
+        const double Ve = sm[6 * nt + r];
         if (Ve == 0.0) continue;  // inactive tet
-        const double2 a = r[0], b = r[1], c = r[2];
         Vh = Vh + Ve;
-        T0 = T0 + a.x; T1 = T1 + a.y; T2 = T2 + b.x;
-        T3 = T3 + b.y; T4 = T4 + c.x; T5 = T5 + c.y;
+        T0 = T0 + sm[r];
+        T1 = T1 + sm[nt + r];
+        T2 = T2 + sm[2 * nt + r];
+        T3 = T3 + sm[3 * nt + r];
+        T4 = T4 + sm[4 * nt + r];
+        T5 = T5 + sm[5 * nt + r];
     }
-    double2 *o = reinterpret_cast<double2 *>(d.srec + 8 * s);
+    double4 *o = reinterpret_cast<double4 *>(d.srec + 8 * s);
     if (Vh == 0.0) {
-        o[0] = o[1] = o[2] = o[3] = make_double2(0.0, 0.0);
+        st256(o, 0.0, 0.0, 0.0, 0.0);
+        st256(o + 1, 0.0, 0.0, 0.0, 0.0);
         return;
     }
     const double inv = 1.0 / Vh;
@@ -118,10 +156,8 @@ __device__ __forceinline__ void stage_B(const Dev &d, int64_t s) {
     const double r0 = fabs(s0) + fabs(s3) + fabs(s5);
     const double r1 = fabs(s1) + fabs(s3) + fabs(s4);
     const double r2 = fabs(s2) + fabs(s4) + fabs(s5);
-    o[0] = make_double2(s0, s1);
-    o[1] = make_double2(s2, s3);
-    o[2] = make_double2(s4, s5);
-    o[3] = make_double2(fmax(r0, fmax(r1, r2)), 0.0);
+    st256(o, s0, s1, s2, s3);
+    st256(o + 1, s4, s5, fmax(r0, fmax(r1, r2)), 0.0);
 }
 
 // ------------------------------------------------------------------ crack criterion (rare path)
@@ -327,26 +363,46 @@ __device__ __noinline__ void criterion_full(const Dev &d, int64_t e, const doubl
 }
 
 // ------------------------------------------------------------------ stage C: force + criterion
-// S = sum_{l=0..5} sigma_{s(e,l)}; f_{e,a} = c((gx S11 + gy S12) + gz S13), ... with c = V/6.
-// Early-out: every candidate satisfies |G| <= max_l g_{s(e,l)} *
-// max_l |u_q - u_p|; tets below Gc_e (1 - 1e-6) skip the 24-candidate evaluation.
-__device__ __forceinline__ void stage_C(const Dev &d, int64_t e, const double4 *u, bool crack, int64_t rec_step,
-                                        int32_t stamp) {
-    double2 *fo = reinterpret_cast<double2 *>(d.fe + 12 * e);
+// S = sum_{l=0..5} sigma_{s(e,l)}; f_{e,a} = c((gx S11 + gy S12) + gz S13), ... with c = V/6,
+// written to the node-major slot of (e, a).  Early-out: every
+// candidate satisfies |G| <= max_l g_{s(e,l)} * max_l |u_q - u_p|; tets below
+// Gc_e (1 - 1e-6) skip the 24-candidate evaluation.
+__device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
+                                        int32_t stamp, double *sm) {
+    const int32_t s0i = __ldg(d.el_off + b);
+    const int ne = __ldg(d.el_off + b + 1) - s0i;
+    const int32_t n0 = __ldg(d.nl_off + b);
+    const int nn = __ldg(d.nl_off + b + 1) - n0;
+    const bool early = crack && !(d.flags & CEM_F_NO_EARLY_OUT);
+    stage_records(d.srec, d.el + s0i, ne, 7, sm);
+    double *smu = sm + 7 * ne;
+    if (early) stage_nodes(d, u, n0, nn, smu);
+    __syncthreads();
+    const int64_t e = (int64_t)b * d.blk + threadIdx.x;
+    if (e >= d.E) return;
+    const int4 fp = __ldg(d.fpos + e);
     if (!d.state[e]) {
-#pragma unroll
-        for (int i = 0; i < 6; ++i) fo[i] = make_double2(0.0, 0.0);
+        st256(d.fe + fp.x, 0.0, 0.0, 0.0, 0.0);
+        st256(d.fe + fp.y, 0.0, 0.0, 0.0, 0.0);
+        st256(d.fe + fp.z, 0.0, 0.0, 0.0, 0.0);
+        st256(d.fe + fp.w, 0.0, 0.0, 0.0, 0.0);
         return;
     }
     const int64_t E = d.E;
+    const uint4 lq = __ldg(reinterpret_cast<const uint4 *>(d.ledge) + e);
+    const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
+                       (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
     double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
 #pragma unroll
     for (int l = 0; l < 6; ++l) {
-        const double2 *q = reinterpret_cast<const double2 *>(d.srec + 8 * (int64_t)ldro(d.eedge + (int64_t)l * E + e));
-        const double2 a = q[0], b = q[1], c = q[2], g = q[3];
-        S0 = S0 + a.x; S1 = S1 + a.y; S2 = S2 + b.x;
-        S3 = S3 + b.y; S4 = S4 + c.x; S5 = S5 + c.y;
-        gmax = fmax(gmax, g.x);
+        const int r = le[l];
+        S0 = S0 + sm[r];
+        S1 = S1 + sm[ne + r];
+        S2 = S2 + sm[2 * ne + r];
+        S3 = S3 + sm[3 * ne + r];
+        S4 = S4 + sm[4 * ne + r];
+        S5 = S5 + sm[5 * ne + r];
+        gmax = fmax(gmax, sm[6 * ne + r]);
     }
     double g[4][3];
 #pragma unroll
@@ -356,24 +412,26 @@ __device__ __forceinline__ void stage_C(const Dev &d, int64_t e, const double4 *
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
     const double cc = ldro(d.geoC + e);
+    const int slot[4] = {fp.x, fp.y, fp.z, fp.w};
 #pragma unroll
-    for (int a = 0; a < 4; a += 2) {
-        const double f0 = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
-        const double f1 = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
-        const double f2 = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
-        const double f3 = cc * ((g[a + 1][0] * S0 + g[a + 1][1] * S3) + g[a + 1][2] * S5);
-        const double f4 = cc * ((g[a + 1][1] * S1 + g[a + 1][0] * S3) + g[a + 1][2] * S4);
-        const double f5 = cc * ((g[a + 1][2] * S2 + g[a + 1][1] * S4) + g[a + 1][0] * S5);
-        fo[3 * (a >> 1) + 0] = make_double2(f0, f1);
-        fo[3 * (a >> 1) + 1] = make_double2(f2, f3);
-        fo[3 * (a >> 1) + 2] = make_double2(f4, f5);
+    for (int a = 0; a < 4; ++a) {
+        const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
+        const double fy = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
+        const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
+        st256(d.fe + slot[a], fx, fy, fz, 0.0);
     }
     if (!crack) return;
     const double gc = ldro(d.gc + e);
-    if (!(d.flags & CEM_F_NO_EARLY_OUT)) {
-        const int4 t = __ldg(&d.conn[e]);
-        const double4 u0 = ld4(&u[t.x]), u1 = ld4(&u[t.y]), u2 = ld4(&u[t.z]), u3 = ld4(&u[t.w]);
-        const double ux[4] = {u0.x, u1.x, u2.x, u3.x}, uy[4] = {u0.y, u1.y, u2.y, u3.y}, uz[4] = {u0.z, u1.z, u2.z, u3.z};
+    if (early) {
+        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
+        const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+        double ux[4], uy[4], uz[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            ux[a] = smu[li[a]];
+            uy[a] = smu[nn + li[a]];
+            uz[a] = smu[2 * nn + li[a]];
+        }
         double d2 = 0.0;
 #pragma unroll
         for (int l = 0; l < 6; ++l) {
@@ -387,20 +445,24 @@ __device__ __forceinline__ void stage_C(const Dev &d, int64_t e, const double4 *
 }
 
 // ------------------------------------------------------------------ stage D: node update
-__device__ __forceinline__ void stage_D(const Dev &d, int64_t k, const double4 *u1p, double4 *u2p, int64_t s) {
+// f_int,k = sum of the node's force slots in order (= ascending original tet id); the warp
+// reads 32 consecutive slots per incidence index (interleaved layout, cem_plan.cpp).
+__device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p, double4 *u2p, int64_t s) {
+    const int64_t k = (int64_t)b * d.blk + threadIdx.x;
+    if (k >= d.N) return;
     const int32_t j0 = ldro(d.node_off + k), j1 = ldro(d.node_off + k + 1);
+    const double4 *fb = d.fe + __ldg(d.gbase + (k >> 5)) + (k & 31);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    for (int32_t j = j0; j < j1; ++j) {
-        const int32_t ent = ldro(d.node_ent + j);
-        const double *f = d.fe + 12 * (int64_t)(ent >> 2) + 3 * (ent & 3);
-        f0 = f0 + f[0];
-        f1 = f1 + f[1];
-        f2 = f2 + f[2];
+    for (int32_t j = 0; j < j1 - j0; ++j) {
+        const double4 f = ld256(fb + 32 * j);
+        f0 = f0 + f.x;
+        f1 = f1 + f.y;
+        f2 = f2 + f.z;
     }
     double mk = d.mass[k];
     const uint8_t fl = __ldg(&d.nflag[k]);
-    const double4 u1 = ld4(&u1p[k]);
-    const double4 v = ld4(&d.v[k]), a = ld4(&d.a[k]);
+    const double4 u1 = ld256(&u1p[k]);
+    const double4 v = ld256(&d.v[k]), a = ld256(&d.a[k]);
     const double dt = d.dt;
     double fx = 0.0, fy = 0.0, fz = 0.0;
     if (fl & 8) {
@@ -451,11 +513,11 @@ __device__ __forceinline__ void stage_D(const Dev &d, int64_t k, const double4 *
             for (int c = 0; c < 3; ++c) vv[c] = aa[c] = 0.0;
         }
     }
-    st4(&d.v[k], vv[0], vv[1], vv[2], 0.0);
-    st4(&d.a[k], aa[0], aa[1], aa[2], 0.0);
+    st256(&d.v[k], vv[0], vv[1], vv[2], 0.0);
+    st256(&d.a[k], aa[0], aa[1], aa[2], 0.0);
     // predictor u_{s+2} = u_{s+1} + dt v + dt^2/2 a
-    st4(&u2p[k], (u1.x + dt * vv[0]) + d.hdt2 * aa[0], (u1.y + dt * vv[1]) + d.hdt2 * aa[1],
-        (u1.z + dt * vv[2]) + d.hdt2 * aa[2], 0.0);
+    st256(&u2p[k], (u1.x + dt * vv[0]) + d.hdt2 * aa[0], (u1.y + dt * vv[1]) + d.hdt2 * aa[1],
+          (u1.z + dt * vv[2]) + d.hdt2 * aa[2], 0.0);
     if (!isfinite(u1.x) || !isfinite(u1.y) || !isfinite(u1.z) || !isfinite(vv[0]) || !isfinite(vv[1]) ||
         !isfinite(vv[2]) || !isfinite(aa[0]) || !isfinite(aa[1]) || !isfinite(aa[2])) {
         d.ctr[1] = 1;
@@ -474,7 +536,8 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
     return v;
 }
 
-__global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
+__global__ void __launch_bounds__(256, 2) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
+    extern __shared__ double sm[];
     __shared__ unsigned long long sh_q;
     const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)d.P;
     const int tid = threadIdx.x;
@@ -488,33 +551,25 @@ __global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int
         const int g = code >> 28, b = code & 0x0FFFFFFF;
         // wait for the producer blocks (warp 0; lanes poll counters in parallel)
         if (tid < 32) {
-            const int lo = __ldg(d.dep + ((int64_t)g * d.maxblk + b) * 2);
-            const int hi = __ldg(d.dep + ((int64_t)g * d.maxblk + b) * 2 + 1);
+            const int64_t qd = (int64_t)g * d.maxblk + b;
+            const int lo = __ldg(d.dep_off + qd), hi = __ldg(d.dep_off + qd + 1);
             const int pg = g == ST_A ? ST_D : g - 1;
             const int need = g == ST_A ? (int)s : (int)(s + 1);
             const int32_t *c = d.cnt + (int64_t)pg * d.maxblk;
-            for (int i = lo + tid; i <= hi; i += 32)
-                while (ld_acquire(c + i) < need) __nanosleep(64);
+            for (int i = lo + tid; i < hi; i += 32) {
+                const int pb = __ldg(d.dep + i);
+                while (ld_acquire(c + pb) < need) __nanosleep(32);
+            }
             __syncwarp();
             if (tid == 0) __threadfence();  // order + invalidate this SM's L1 before the reads
         }
         __syncthreads();
-        const int64_t i0 = (int64_t)b * d.blk;
-        const int64_t i = i0 + tid;
         const double4 *u1 = d.ubuf[(s + 1) & 1];
         switch (g) {
-            case ST_A:
-                if (i < d.E) stage_A(d, i, u1);
-                break;
-            case ST_B:
-                if (i < d.S) stage_B(d, i);
-                break;
-            case ST_C:
-                if (i < d.E) stage_C(d, i, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1));
-                break;
-            default:
-                if (i < d.N) stage_D(d, i, u1, d.ubuf[s & 1], s);
-                break;
+            case ST_A: block_A(d, b, u1, sm); break;
+            case ST_B: block_B(d, b, sm); break;
+            case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
+            default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
         }
         __syncthreads();
         if (tid == 0) {
@@ -526,30 +581,29 @@ __global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int
 
 // ------------------------------------------------------------------ staged kernels (one per stage)
 __global__ void __launch_bounds__(256) k_A(Dev d, int64_t s) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < d.E) stage_A(d, e, d.ubuf[(s + 1) & 1]);
+    extern __shared__ double sm[];
+    block_A(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
 }
 __global__ void __launch_bounds__(256) k_B(Dev d) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < d.S) stage_B(d, i);
+    extern __shared__ double sm[];
+    block_B(d, blockIdx.x, sm);
 }
 __global__ void __launch_bounds__(256) k_C(Dev d, int64_t s, int crack_every) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < d.E) stage_C(d, e, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1));
+    extern __shared__ double sm[];
+    block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
 }
 __global__ void __launch_bounds__(256) k_D(Dev d, int64_t s) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < d.N) stage_D(d, k, d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+    block_D(d, blockIdx.x, d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
 // criterion on the current state u_n (cem_crack_update)
 __global__ void __launch_bounds__(256) k_A_cur(Dev d, int64_t n) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < d.E) stage_A(d, e, d.ubuf[n & 1]);
+    extern __shared__ double sm[];
+    block_A(d, blockIdx.x, d.ubuf[n & 1], sm);
 }
 __global__ void __launch_bounds__(256) k_C_cur(Dev d, int64_t n, int32_t stamp) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < d.E) stage_C(d, e, d.ubuf[n & 1], true, n, stamp);
+    extern __shared__ double sm[];
+    block_C(d, blockIdx.x, d.ubuf[n & 1], true, n, stamp, sm);
 }
 // nodes of tets split by cem_crack_update: new mass; frozen -> v = a = 0 and the pending
 // prediction u_{n+1} restarts from u_n
@@ -576,34 +630,44 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
 
-int persistent_occupancy() {
+int persistent_occupancy(int smem_bytes) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent, 256, 0);
+    cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent, 256, smem_bytes);
     return n;
+}
+
+void set_smem_limits(int smem_bytes) {
+    cudaFuncSetAttribute(k_A, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_B, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_A_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_C_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
 
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st) {
     cudaMemsetAsync(d.head, 0, sizeof(unsigned long long), st);
-    k_persistent<<<grid, 256, 0, st>>>(d, step0, nsteps, crack_every);
+    k_persistent<<<grid, 256, d.smem_bytes, st>>>(d, step0, nsteps, crack_every);
 }
 
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], st);
-    k_A<<<nblk(d.E), 256, 0, st>>>(d, s);
+    k_A<<<d.nblk[ST_A], 256, d.smem_bytes, st>>>(d, s);
     if (ev) cudaEventRecord(ev[1], st);
-    k_B<<<nblk(d.S), 256, 0, st>>>(d);
+    k_B<<<d.nblk[ST_B], 256, d.smem_bytes, st>>>(d);
     if (ev) cudaEventRecord(ev[2], st);
-    k_C<<<nblk(d.E), 256, 0, st>>>(d, s, crack_every);
+    k_C<<<d.nblk[ST_C], 256, d.smem_bytes, st>>>(d, s, crack_every);
     if (ev) cudaEventRecord(ev[3], st);
-    k_D<<<nblk(d.N), 256, 0, st>>>(d, s);
+    k_D<<<d.nblk[ST_D], 256, 0, st>>>(d, s);
     if (ev) cudaEventRecord(ev[4], st);
 }
 
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st) {
     const int32_t stamp = -(int32_t)(n + 1);
-    k_A_cur<<<nblk(d.E), 256, 0, st>>>(d, n);
-    k_B<<<nblk(d.S), 256, 0, st>>>(d);
-    k_C_cur<<<nblk(d.E), 256, 0, st>>>(d, n, stamp);
+    k_A_cur<<<d.nblk[ST_A], 256, d.smem_bytes, st>>>(d, n);
+    k_B<<<d.nblk[ST_B], 256, d.smem_bytes, st>>>(d);
+    k_C_cur<<<d.nblk[ST_C], 256, d.smem_bytes, st>>>(d, n, stamp);
     k_fix_cur<<<nblk(d.N), 256, 0, st>>>(d, n, stamp);
 }
 

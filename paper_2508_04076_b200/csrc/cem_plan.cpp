@@ -15,7 +15,7 @@
 
 namespace cem {
 
-void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p) {
+void build_plan(const HostMesh &h, int blk, Plan &p) {
     const int64_t N = h.N, E = h.E, S = h.S;
     p.blk = blk;
     // ---------------------------------------------------------------- sweep axis + slabs
@@ -31,17 +31,57 @@ void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p) {
     double vsum = 0.0;
     for (int64_t e = 0; e < E; ++e) vsum += h.V[e];
     const double hb = std::cbrt(6.0 * vsum / (double)E);
+    // slabs of kSlab element layers along the sweep axis; inside a slab, recursive
+    // coordinate bisection of the tet centroids down to leaves of <= blk/2 tets, leaves in
+    // tree order -> every block of blk consecutive tets is a compact 3D patch
+    const int kSlab = 4;
+    std::vector<double> cen(3 * E);
     std::vector<int64_t> key(E);
     for (int64_t e = 0; e < E; ++e) {
-        double c = 0.0;
-        for (int a = 0; a < 4; ++a) c += h.X[3 * (int64_t)h.tet[4 * e + a] + ax];
-        c *= 0.25;
-        key[e] = (int64_t)std::floor((c - lo[ax]) / hb);
+        for (int c = 0; c < 3; ++c) {
+            double x = 0.0;
+            for (int a = 0; a < 4; ++a) x += h.X[3 * (int64_t)h.tet[4 * e + a] + c];
+            cen[3 * e + c] = 0.25 * x;
+        }
+        key[e] = (int64_t)std::floor((cen[3 * e + ax] - lo[ax]) / (kSlab * hb));
     }
     p.tet_new2old.resize(E);
     std::iota(p.tet_new2old.begin(), p.tet_new2old.end(), 0);
     std::stable_sort(p.tet_new2old.begin(), p.tet_new2old.end(),
                      [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+    {
+        const int64_t leaf = std::max(1, blk / 2);
+        std::vector<std::pair<int64_t, int64_t>> stack;
+        int64_t i0 = 0;
+        while (i0 < E) {  // one slab at a time
+            int64_t i1 = i0;
+            while (i1 < E && key[p.tet_new2old[i1]] == key[p.tet_new2old[i0]]) ++i1;
+            stack.push_back({i0, i1});
+            while (!stack.empty()) {
+                auto [a0, a1] = stack.back();
+                stack.pop_back();
+                if (a1 - a0 <= leaf) continue;
+                double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+                for (int64_t i = a0; i < a1; ++i)
+                    for (int c = 0; c < 3; ++c) {
+                        mn[c] = std::min(mn[c], cen[3 * (int64_t)p.tet_new2old[i] + c]);
+                        mx[c] = std::max(mx[c], cen[3 * (int64_t)p.tet_new2old[i] + c]);
+                    }
+                int cx = 0;
+                for (int c = 1; c < 3; ++c)
+                    if (mx[c] - mn[c] > mx[cx] - mn[cx]) cx = c;
+                const int64_t mid = a0 + (a1 - a0) / 2;
+                std::nth_element(p.tet_new2old.begin() + a0, p.tet_new2old.begin() + mid, p.tet_new2old.begin() + a1,
+                                 [&](int32_t x, int32_t y) {
+                                     const double u = cen[3 * (int64_t)x + cx], v = cen[3 * (int64_t)y + cx];
+                                     return u < v || (u == v && x < y);
+                                 });
+                stack.push_back({mid, a1});  // right half processed after the left half
+                stack.push_back({a0, mid});
+            }
+            i0 = i1;
+        }
+    }
     p.tet_old2new.assign(E, -1);
     for (int64_t e = 0; e < E; ++e) p.tet_old2new[p.tet_new2old[e]] = (int32_t)e;
     // nodes and edges by first appearance
@@ -111,6 +151,71 @@ void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p) {
         }
         p.node_off[kn + 1] = (int32_t)j;
     }
+    // ---------------------------------------------------------------- gather lists
+    {
+        const int nbt = (int)((E + blk - 1) / blk), nbs = (int)((S + blk - 1) / blk);
+        p.nl_off.assign(nbt + 1, 0);
+        p.el_off.assign(nbt + 1, 0);
+        p.nl.clear();
+        p.el.clear();
+        p.lconn.assign(4 * E, 0);
+        p.ledge.assign(8 * E, 0);
+        p.max_nl = p.max_el = p.max_tl = 0;
+        std::vector<int32_t> tmp;
+        for (int b = 0; b < nbt; ++b) {
+            const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
+            tmp.assign(p.conn.begin() + 4 * e0, p.conn.begin() + 4 * e1);
+            std::sort(tmp.begin(), tmp.end());
+            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+            for (int64_t e = e0; e < e1; ++e)
+                for (int a = 0; a < 4; ++a)
+                    p.lconn[4 * e + a] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.conn[4 * e + a]) - tmp.begin());
+            p.nl.insert(p.nl.end(), tmp.begin(), tmp.end());
+            p.nl_off[b + 1] = (int32_t)p.nl.size();
+            p.max_nl = std::max(p.max_nl, (int)tmp.size());
+            tmp.clear();
+            for (int64_t e = e0; e < e1; ++e)
+                for (int l = 0; l < 6; ++l) tmp.push_back(p.eedge[(int64_t)l * E + e]);
+            std::sort(tmp.begin(), tmp.end());
+            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+            for (int64_t e = e0; e < e1; ++e)
+                for (int l = 0; l < 6; ++l)
+                    p.ledge[8 * e + l] =
+                        (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.eedge[(int64_t)l * E + e]) - tmp.begin());
+            p.el.insert(p.el.end(), tmp.begin(), tmp.end());
+            p.el_off[b + 1] = (int32_t)p.el.size();
+            p.max_el = std::max(p.max_el, (int)tmp.size());
+        }
+        p.tl_off.assign(nbs + 1, 0);
+        p.tl.clear();
+        p.inc_local.assign(p.edge_inc.size(), 0);
+        for (int b = 0; b < nbs; ++b) {
+            const int64_t s0 = (int64_t)b * blk, s1 = std::min<int64_t>(S, s0 + blk);
+            tmp.assign(p.edge_inc.begin() + p.edge_off[s0], p.edge_inc.begin() + p.edge_off[s1]);
+            std::sort(tmp.begin(), tmp.end());
+            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+            for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j)
+                p.inc_local[j] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.edge_inc[j]) - tmp.begin());
+            p.tl.insert(p.tl.end(), tmp.begin(), tmp.end());
+            p.tl_off[b + 1] = (int32_t)p.tl.size();
+            p.max_tl = std::max(p.max_tl, (int)tmp.size());
+        }
+        // node-major force slots, interleaved per warp of 32 consecutive nodes so that the
+        // lanes of stage D read 32 consecutive slots per incidence index j
+        const int64_t ng = (N + 31) / 32;
+        p.gbase.assign(ng + 1, 0);
+        for (int64_t g = 0; g < ng; ++g) {
+            int32_t mx = 0;
+            for (int64_t k = 32 * g; k < std::min<int64_t>(N, 32 * g + 32); ++k) mx = std::max(mx, p.node_off[k + 1] - p.node_off[k]);
+            p.gbase[g + 1] = p.gbase[g] + 32 * mx;
+        }
+        p.nslots = p.gbase[ng];
+        p.fpos.assign(4 * E, -1);
+        for (int64_t k = 0; k < N; ++k)
+            for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j)
+                p.fpos[4 * (int64_t)(p.node_ent[j] >> 2) + (p.node_ent[j] & 3)] =
+                    p.gbase[k / 32] + 32 * (j - p.node_off[k]) + (int32_t)(k % 32);
+    }
     // ---------------------------------------------------------------- blocks and dependencies
     const int64_t cnt[ST_COUNT] = {E, S, E, N};
     p.maxblk = 0;
@@ -118,56 +223,42 @@ void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p) {
         p.nblk[g] = (int)((cnt[g] + blk - 1) / blk);
         p.maxblk = std::max(p.maxblk, p.nblk[g]);
     }
-    p.dep.assign((size_t)ST_COUNT * p.maxblk * 2, 0);
-    auto setdep = [&](int g, int b, int lo_, int hi_) {
-        p.dep[((size_t)g * p.maxblk + b) * 2] = lo_;
-        p.dep[((size_t)g * p.maxblk + b) * 2 + 1] = hi_;
+    // explicit producer-block lists per (stage, block)
+    std::vector<std::vector<int32_t>> deps((size_t)ST_COUNT * p.maxblk);
+    auto finish = [](std::vector<int32_t> &v) {
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
     };
-    // A-block: D-blocks (previous step) of the nodes of its tets
-    for (int b = 0; b < p.nblk[ST_A]; ++b) {
-        int l = INT32_MAX, u = -1;
-        for (int64_t e = (int64_t)b * blk; e < std::min<int64_t>(E, (int64_t)(b + 1) * blk); ++e)
-            for (int a = 0; a < 4; ++a) {
-                int nb = p.conn[4 * e + a] / blk;
-                l = std::min(l, nb);
-                u = std::max(u, nb);
-            }
-        setdep(ST_A, b, l, u);
+    for (int b = 0; b < p.nblk[ST_A]; ++b) {  // A: D-blocks (previous step) of its nodes
+        auto &v = deps[(size_t)ST_A * p.maxblk + b];
+        for (int32_t i = p.nl_off[b]; i < p.nl_off[b + 1]; ++i) v.push_back(p.nl[i] / blk);
+        finish(v);
     }
-    // B-block: A-blocks of the tets incident to its edges
-    for (int b = 0; b < p.nblk[ST_B]; ++b) {
-        int l = INT32_MAX, u = -1;
-        for (int64_t s = (int64_t)b * blk; s < std::min<int64_t>(S, (int64_t)(b + 1) * blk); ++s)
-            for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j) {
-                int tb = p.edge_inc[j] / blk;
-                l = std::min(l, tb);
-                u = std::max(u, tb);
-            }
-        setdep(ST_B, b, l, u);
+    for (int b = 0; b < p.nblk[ST_B]; ++b) {  // B: A-blocks of its tet list
+        auto &v = deps[(size_t)ST_B * p.maxblk + b];
+        for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i) v.push_back(p.tl[i] / blk);
+        finish(v);
     }
-    // C-block: B-blocks of the edges of its tets
-    for (int b = 0; b < p.nblk[ST_C]; ++b) {
-        int l = INT32_MAX, u = -1;
-        for (int64_t e = (int64_t)b * blk; e < std::min<int64_t>(E, (int64_t)(b + 1) * blk); ++e)
-            for (int q = 0; q < 6; ++q) {
-                int sb = p.eedge[(int64_t)q * E + e] / blk;
-                l = std::min(l, sb);
-                u = std::max(u, sb);
-            }
-        setdep(ST_C, b, l, u);
+    for (int b = 0; b < p.nblk[ST_C]; ++b) {  // C: B-blocks of its edge list
+        auto &v = deps[(size_t)ST_C * p.maxblk + b];
+        for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) v.push_back(p.el[i] / blk);
+        finish(v);
     }
-    // D-block: C-blocks of the tets incident to its nodes (isolated nodes: none)
-    for (int b = 0; b < p.nblk[ST_D]; ++b) {
-        int l = INT32_MAX, u = -1;
+    for (int b = 0; b < p.nblk[ST_D]; ++b) {  // D: C-blocks of the tets of its nodes
+        auto &v = deps[(size_t)ST_D * p.maxblk + b];
         for (int64_t k = (int64_t)b * blk; k < std::min<int64_t>(N, (int64_t)(b + 1) * blk); ++k)
-            for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) {
-                int tb = (p.node_ent[j] >> 2) / blk;
-                l = std::min(l, tb);
-                u = std::max(u, tb);
-            }
-        if (u < 0) l = 0, u = -1;  // empty range
-        setdep(ST_D, b, l, u);
+            for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) v.push_back((p.node_ent[j] >> 2) / blk);
+        finish(v);
     }
+    p.dep_off.assign((size_t)ST_COUNT * p.maxblk + 1, 0);
+    p.dep.clear();
+    for (size_t q = 0; q < deps.size(); ++q) {
+        p.dep.insert(p.dep.end(), deps[q].begin(), deps[q].end());
+        p.dep_off[q + 1] = (int32_t)p.dep.size();
+    }
+}
+
+void build_schedule(Plan &p, int resident_ctas) {
     // ---------------------------------------------------------------- wavefront schedule
     // virtual time: vt(A, b) = b / nA; a consumer sits delta after its latest producer,
     // delta = (resident CTAs) / (items per step), so by the time a CTA dequeues it its
@@ -179,9 +270,9 @@ void build_plan(const HostMesh &h, int blk, int resident_ctas, Plan &p) {
     for (int b = 0; b < p.nblk[ST_A]; ++b) vt[ST_A][b] = (double)b / (double)p.nblk[ST_A];
     for (int g = ST_B; g <= ST_D; ++g)
         for (int b = 0; b < p.nblk[g]; ++b) {
-            const int l = p.dep[((size_t)g * p.maxblk + b) * 2], u = p.dep[((size_t)g * p.maxblk + b) * 2 + 1];
             double m = 0.0;
-            for (int q = l; q <= u; ++q) m = std::max(m, vt[g - 1][q]);
+            const size_t q = (size_t)g * p.maxblk + b;
+            for (int32_t i = p.dep_off[q]; i < p.dep_off[q + 1]; ++i) m = std::max(m, vt[g - 1][p.dep[i]]);
             vt[g][b] = m + delta;
         }
     std::vector<std::pair<double, int32_t>> items;

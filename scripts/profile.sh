@@ -1,12 +1,11 @@
 #!/bin/bash
 # Run on the GPU box: plain bench (must exit 0), then the ncu launch list and one full
-# capture of each step kernel.  Outputs under gpurun_out/.
+# capture of every kernel of a short bench.  Outputs under gpurun_out/.
 set -u
 OUT=gpurun_out
 CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
-# launches: skip init + warm-up (3 steps x 5 kernels)
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 15 -c 40 --csv \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:'k_' -s 15 -c 5 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'k_' -c 24 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1
 echo done
