@@ -63,7 +63,7 @@ struct Offs {
     size_t conn, geoV, geoC, geoG, eedge, edge_off, node_off, node_ent, X, fext, nflag, dir_v0, gc;
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, trec, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
-    size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, inc_local, fpos, gbase;
+    size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, inc_local, fpos, gbase, self, ncons, cons_done;
     size_t total;
 };
 
@@ -119,6 +119,9 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.inc_local = L.take<uint16_t>((int64_t)p.inc_local.size());
     o.fpos = L.take<int32_t>((int64_t)p.fpos.size());
     o.gbase = L.take<int32_t>((int64_t)p.gbase.size());
+    o.self = L.take<Dev>(1);
+    o.ncons = L.take<int32_t>(3 * (int64_t)p.maxblk);
+    o.cons_done = L.take<int32_t>(3 * (int64_t)p.maxblk);
     o.total = L.off;
     return o;
 }
@@ -178,6 +181,9 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.fpos = at<int4>(b, o.fpos);
     d.gbase = at<int32_t>(b, o.gbase);
     d.smem_bytes = smem_bytes_for(p);
+    d.self = at<Dev>(b, o.self);
+    d.ncons = at<int32_t>(b, o.ncons);
+    d.cons_done = at<int32_t>(b, o.cons_done);
     d.ctr = at<int32_t>(b, o.ctr);
     d.rec_step = at<int64_t>(b, o.rec_step);
     d.rec_elem = at<int32_t>(b, o.rec_elem);
@@ -297,6 +303,9 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.gbase, p.gbase.data(), sizeof(int32_t) * p.gbase.size()));
     CUDA_TRY(put(o.sched, p.sched.data(), sizeof(int32_t) * p.sched.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.head), 0, sizeof(unsigned long long), st));
+    CUDA_TRY(put(o.ncons, p.ncons.data(), sizeof(int32_t) * p.ncons.size()));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cons_done), 0, sizeof(int32_t) * 3 * p.maxblk, st));
+    CUDA_TRY(put(o.self, &ctx->d, sizeof(Dev)));
     CUDA_TRY(cudaStreamSynchronize(st));
     return CEM_OK;
 }

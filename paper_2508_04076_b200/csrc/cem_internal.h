@@ -63,6 +63,7 @@ struct Plan {
     int maxblk = 0;
     std::vector<int32_t> dep_off;     // [ST_COUNT * maxblk + 1] CSR of producer blocks per (stage, block)
     std::vector<int32_t> dep;         // producer block ids (of the producing stage)
+    std::vector<int32_t> ncons;       // [3][maxblk] consumer blocks of each A/B/C block (discard counts)
     std::vector<int32_t> sched;       // [P]: stage << 28 | block
     // block gather lists (deduplicated producer records staged in shared memory)
     std::vector<int32_t> nl_off, nl;  // tet block -> sorted unique node ids
@@ -82,6 +83,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p);
 void build_schedule(Plan &p, int resident_ctas);
 
 // ---------------------------------------------------------------- device view
+struct Dev;
 struct Dev {
     int64_t N, E, S;
     // read-only mesh tables (storage numbering)
@@ -110,6 +112,7 @@ struct Dev {
     const int4 *fpos;
     const uint16_t *lconn, *ledge, *inc_local;
     int smem_bytes;
+    const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] spare
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
@@ -120,6 +123,8 @@ struct Dev {
     // persistent wavefront
     int32_t *cnt;              // [ST_COUNT][maxblk] completed-step counters
     const int32_t *dep_off, *dep;
+    const int32_t *ncons;      // [3][maxblk] consumers of each A/B/C block
+    int32_t *cons_done;        // [3][maxblk] consumers finished with the block this step
     const int32_t *sched;      // [P]
     unsigned long long *head;  // work-queue head
     int blk, P, maxblk;

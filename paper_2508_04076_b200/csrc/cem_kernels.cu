@@ -60,16 +60,51 @@ __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, 
 // Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
 // (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
 // every later per-thread gather hits shared memory instead of an L1 line of its own.
+// Loads are issued in batches of kIlp independent index->value pairs so that every thread
+// keeps several L2 round trips in flight (the staging loop is otherwise latency-serialised).
+constexpr int kIlp = 8;
 __device__ __forceinline__ void stage_nodes(const Dev &d, const double4 *u, int32_t n0, int nn, double *pl) {
-    for (int i = threadIdx.x; i < 3 * nn; i += blockDim.x) {
-        const int r = i / 3, c = i - 3 * r;
-        pl[c * nn + r] = reinterpret_cast<const double *>(u + __ldg(d.nl + n0 + r))[c];
+    const int tot = 3 * nn;
+    for (int base = threadIdx.x; base < tot; base += kIlp * blockDim.x) {
+        int32_t id[kIlp];
+        double v[kIlp];
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+            const int i = base + t * blockDim.x;
+            id[t] = i < tot ? __ldg(d.nl + n0 + i / 3) : 0;
+        }
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+            const int i = base + t * blockDim.x;
+            v[t] = i < tot ? reinterpret_cast<const double *>(u + id[t])[i - 3 * (i / 3)] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+            const int i = base + t * blockDim.x;
+            if (i < tot) pl[(i - 3 * (i / 3)) * nn + i / 3] = v[t];
+        }
     }
 }
 __device__ __forceinline__ void stage_records(const double *src, const int32_t *ids, int n, int ncomp, double *pl) {
-    for (int i = threadIdx.x; i < 8 * n; i += blockDim.x) {
-        const int r = i >> 3, c = i & 7;
-        if (c < ncomp) pl[c * n + r] = src[8 * (int64_t)__ldg(ids + r) + c];
+    const int tot = 8 * n;
+    for (int base = threadIdx.x; base < tot; base += kIlp * blockDim.x) {
+        int32_t id[kIlp];
+        double v[kIlp];
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+            const int i = base + t * blockDim.x;
+            id[t] = i < tot ? __ldg(ids + (i >> 3)) : 0;
+        }
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+            const int i = base + t * blockDim.x;
+            v[t] = (i < tot && (i & 7) < ncomp) ? src[8 * (int64_t)id[t] + (i & 7)] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+            const int i = base + t * blockDim.x;
+            if (i < tot && (i & 7) < ncomp) pl[(i & 7) * n + (i >> 3)] = v[t];
+        }
     }
 }
 
@@ -129,8 +164,12 @@ __device__ __forceinline__ void block_B(const Dev &d, int b, double *sm) {
     if (s >= d.S) return;
     const int32_t j0 = ldro(d.edge_off + s), j1 = ldro(d.edge_off + s + 1);
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
+    constexpr int kPre = 8;  // incidence indices prefetched together (Kuhn lattices: <= 6)
+    uint16_t pre[kPre];
+#pragma unroll
+    for (int t = 0; t < kPre; ++t) pre[t] = j0 + t < j1 ? __ldg(d.inc_local + j0 + t) : 0;
     for (int32_t j = j0; j < j1; ++j) {
-        const int r = __ldg(d.inc_local + j);
+        const int r = j - j0 < kPre ? pre[j - j0] : __ldg(d.inc_local + j);
         const double Ve = sm[6 * nt + r];
         if (Ve == 0.0) continue;  // inactive tet
         Vh = Vh + Ve;
@@ -266,8 +305,9 @@ __device__ __forceinline__ double dsgn(double x) { return x > 0.0 ? 1.0 : (x < 0
 // t=0 pattern I (eq:G-I) with m = (X_q-X_p)x(X_r-X_c), t=1 pattern II (eq:G-II) with
 // m = (X_q-X_p)x(X_r-X_p).  Select max G, ties -> larger area, then lower k.
 // Re-gathers its inputs (runs for the few tets that fail the early-out).
-__device__ __noinline__ void evaluate_tet(const Dev &d, int64_t e, const double4 *u, double &Gbest, int &kbest,
+__device__ __noinline__ void evaluate_tet(const Dev *__restrict__ dp, int64_t e, const double4 *u, double &Gbest, int &kbest,
                                           double &Abest) {
+    const Dev &d = *dp;
     const int4 t = __ldg(&d.conn[e]);
     const int nid[4] = {t.x, t.y, t.z, t.w};
     Vec3 Xn[4], un[4];
@@ -341,11 +381,12 @@ __device__ __noinline__ void evaluate_tet(const Dev &d, int64_t e, const double4
 // split: deactivate now (stage B/C of this step already consumed the
 // state; later readers are next-step stages), append a record (unordered; the host sorts
 // by (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
-__device__ __noinline__ void criterion_full(const Dev &d, int64_t e, const double4 *u, double gc, int64_t rec_step,
+__device__ __noinline__ void criterion_full(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc, int64_t rec_step,
                                             int32_t stamp) {
+    const Dev &d = *dp;
     double G, A;
     int k;
-    evaluate_tet(d, e, u, G, k, A);
+    evaluate_tet(dp, e, u, G, k, A);
     if (G > gc) {
         d.state[e] = 0;
         const int slot = atomicAdd(&d.ctr[0], 1);
@@ -380,12 +421,10 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     __syncthreads();
     const int64_t e = (int64_t)b * d.blk + threadIdx.x;
     if (e >= d.E) return;
-    const int4 fp = __ldg(d.fpos + e);
+    double4 *fo = d.fe + 4 * e;  // tet-major record: slot a = f_{e,a} (x, y, z, pad)
     if (!d.state[e]) {
-        st256(d.fe + fp.x, 0.0, 0.0, 0.0, 0.0);
-        st256(d.fe + fp.y, 0.0, 0.0, 0.0, 0.0);
-        st256(d.fe + fp.z, 0.0, 0.0, 0.0, 0.0);
-        st256(d.fe + fp.w, 0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) st256(fo + a, 0.0, 0.0, 0.0, 0.0);
         return;
     }
     const int64_t E = d.E;
@@ -412,13 +451,12 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
     const double cc = ldro(d.geoC + e);
-    const int slot[4] = {fp.x, fp.y, fp.z, fp.w};
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
         const double fy = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
         const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
-        st256(d.fe + slot[a], fx, fy, fz, 0.0);
+        st256(fo + a, fx, fy, fz, 0.0);
     }
     if (!crack) return;
     const double gc = ldro(d.gc + e);
@@ -441,23 +479,32 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         }
         if (gmax * sqrt(d2) * (1.0 + 1e-6) <= gc) return;
     }
-    criterion_full(d, e, u, gc, rec_step, stamp);
+    criterion_full(d.self, e, u, gc, rec_step, stamp);
 }
 
 // ------------------------------------------------------------------ stage D: node update
-// f_int,k = sum of the node's force slots in order (= ascending original tet id); the warp
-// reads 32 consecutive slots per incidence index (interleaved layout, cem_plan.cpp).
+// f_int,k = sum over the node's incidence list (ascending original tet id) of f_{e,a}; the
+// incidence entries are fetched kIlp at a time so the record loads overlap.
 __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p, double4 *u2p, int64_t s) {
     const int64_t k = (int64_t)b * d.blk + threadIdx.x;
     if (k >= d.N) return;
     const int32_t j0 = ldro(d.node_off + k), j1 = ldro(d.node_off + k + 1);
-    const double4 *fb = d.fe + __ldg(d.gbase + (k >> 5)) + (k & 31);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    for (int32_t j = 0; j < j1 - j0; ++j) {
-        const double4 f = ld256(fb + 32 * j);
-        f0 = f0 + f.x;
-        f1 = f1 + f.y;
-        f2 = f2 + f.z;
+    for (int32_t jb = j0; jb < j1; jb += kIlp) {
+        int32_t ent[kIlp];
+        double4 f[kIlp];
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) ent[t] = jb + t < j1 ? ldro(d.node_ent + jb + t) : -1;
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t)
+            if (ent[t] >= 0) f[t] = ld256(d.fe + ent[t]);
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t)
+            if (ent[t] >= 0) {
+                f0 = f0 + f[t].x;
+                f1 = f1 + f[t].y;
+                f2 = f2 + f[t].z;
+            }
     }
     double mk = d.mass[k];
     const uint8_t fl = __ldg(&d.nflag[k]);
@@ -536,27 +583,61 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
     return v;
 }
 
-__global__ void __launch_bounds__(256, 2) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
+__device__ __forceinline__ void discard_l2(const void *p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// Invalidate, without write-back, the L2 lines holding producer block pb's intermediate
+// records (tau / sigma / f_e).  Called by the LAST consumer block of pb in a step, before it
+// publishes its own completion (the next writer of those lines transitively waits for it).
+__device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
+    const char *base;
+    int64_t bytes, off;
+    if (pg == ST_A) {
+        base = reinterpret_cast<const char *>(d.trec);
+        off = (int64_t)pb * d.blk * 64;
+        bytes = min((int64_t)d.blk, d.E - (int64_t)pb * d.blk) * 64;
+    } else if (pg == ST_B) {
+        base = reinterpret_cast<const char *>(d.srec);
+        off = (int64_t)pb * d.blk * 64;
+        bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 64;
+    } else {
+        base = reinterpret_cast<const char *>(d.fe);
+        off = (int64_t)pb * d.blk * 128;
+        bytes = min((int64_t)d.blk, d.E - (int64_t)pb * d.blk) * 128;
+    }
+    for (int64_t l = threadIdx.x; l < bytes / 128; l += blockDim.x) discard_l2(base + off + 128 * l);
+}
+
+__global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
     extern __shared__ double sm[];
     __shared__ unsigned long long sh_q;
+    __shared__ int sh_ndisc;
+    __shared__ int sh_disc[64];
     const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)d.P;
     const int tid = threadIdx.x;
+    unsigned long long qn = 0;
+    if (tid == 0) qn = atomicAdd(d.head, 1ull);
     for (;;) {
-        if (tid == 0) sh_q = atomicAdd(d.head, 1ull);
+        if (tid == 0) {
+            sh_q = qn;
+            qn = atomicAdd(d.head, 1ull);  // next item, in flight while this one runs
+            sh_ndisc = 0;
+        }
         __syncthreads();
         const unsigned long long q = sh_q;
         if (q >= total) return;
         const int64_t s = step0 + (int64_t)(q / (unsigned long long)d.P);
         const int code = __ldg(d.sched + (q % (unsigned long long)d.P));
         const int g = code >> 28, b = code & 0x0FFFFFFF;
+        const int64_t qd = (int64_t)g * d.maxblk + b;
+        const int dlo = __ldg(d.dep_off + qd), dhi = __ldg(d.dep_off + qd + 1);
+        const int pg = g == ST_A ? ST_D : g - 1;
         // wait for the producer blocks (warp 0; lanes poll counters in parallel)
         if (tid < 32) {
-            const int64_t qd = (int64_t)g * d.maxblk + b;
-            const int lo = __ldg(d.dep_off + qd), hi = __ldg(d.dep_off + qd + 1);
-            const int pg = g == ST_A ? ST_D : g - 1;
             const int need = g == ST_A ? (int)s : (int)(s + 1);
             const int32_t *c = d.cnt + (int64_t)pg * d.maxblk;
-            for (int i = lo + tid; i < hi; i += 32) {
+            for (int i = dlo + tid; i < dhi; i += 32) {
                 const int pb = __ldg(d.dep + i);
                 while (ld_acquire(c + pb) < need) __nanosleep(32);
             }
@@ -572,9 +653,30 @@ __global__ void __launch_bounds__(256, 2) k_persistent(Dev d, int64_t step0, int
             default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
         }
         __syncthreads();
+        if (g != ST_A) {
+            // consumers of intermediates: the last one of each producer block discards it
+            if (tid < 32) {
+                int32_t *cd = d.cons_done + (int64_t)(g - 1) * d.maxblk;
+                const int32_t *nc = d.ncons + (int64_t)(g - 1) * d.maxblk;
+                for (int i = dlo + tid; i < dhi; i += 32) {
+                    const int pb = __ldg(d.dep + i);
+                    const int old = atomicAdd(cd + pb, 1);
+                    if (old == __ldg(nc + pb) - 1) {
+                        cd[pb] = 0;
+                        const int slot = atomicAdd(&sh_ndisc, 1);
+                        if (slot < 64) sh_disc[slot] = pb;
+                        else discard_block(d, g - 1, pb);  // (rare) overflow: this lane alone
+                    }
+                }
+            }
+            __syncthreads();
+            const int nd = min(sh_ndisc, 64);
+            for (int i = 0; i < nd; ++i) discard_block(d, g - 1, sh_disc[i]);
+            __syncthreads();
+        }
         if (tid == 0) {
             __threadfence();
-            atomicExch(d.cnt + (int64_t)g * d.maxblk + b, (int)(s + 1));
+            atomicExch(d.cnt + qd, (int)(s + 1));
         }
     }
 }
@@ -588,7 +690,7 @@ __global__ void __launch_bounds__(256) k_B(Dev d) {
     extern __shared__ double sm[];
     block_B(d, blockIdx.x, sm);
 }
-__global__ void __launch_bounds__(256) k_C(Dev d, int64_t s, int crack_every) {
+__global__ void __launch_bounds__(256, 4) k_C(Dev d, int64_t s, int crack_every) {
     extern __shared__ double sm[];
     block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
 }

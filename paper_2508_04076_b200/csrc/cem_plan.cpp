@@ -209,7 +209,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
             for (int64_t k = 32 * g; k < std::min<int64_t>(N, 32 * g + 32); ++k) mx = std::max(mx, p.node_off[k + 1] - p.node_off[k]);
             p.gbase[g + 1] = p.gbase[g] + 32 * mx;
         }
-        p.nslots = p.gbase[ng];
+        p.nslots = 4 * E;  // tet-major force records (node_ent (e<<2|a) indexes them directly)
         p.fpos.assign(4 * E, -1);
         for (int64_t k = 0; k < N; ++k)
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j)
@@ -250,6 +250,10 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) v.push_back((p.node_ent[j] >> 2) / blk);
         finish(v);
     }
+    p.ncons.assign((size_t)3 * p.maxblk, 0);
+    for (int g = ST_B; g <= ST_D; ++g)
+        for (int b = 0; b < p.nblk[g]; ++b)
+            for (int32_t pb : deps[(size_t)g * p.maxblk + b]) p.ncons[(size_t)(g - 1) * p.maxblk + pb]++;
     p.dep_off.assign((size_t)ST_COUNT * p.maxblk + 1, 0);
     p.dep.clear();
     for (size_t q = 0; q < deps.size(); ++q) {
