@@ -95,7 +95,9 @@ typedef struct {
 
 /* flags */
 #define CEM_F_NO_EARLY_OUT 0x1u /* evaluate all 24 crack candidates on every active tet */
-#define CEM_F_STAGED 0x2u       /* one kernel per stage instead of the persistent wavefront kernel */
+#define CEM_F_STAGED 0x2u       /* one kernel per stage (the default; kept for explicitness) */
+#define CEM_F_NO_DISCARD 0x4u   /* persistent kernel: keep consumed intermediates in L2 (no discard) */
+#define CEM_F_PERSISTENT 0x8u   /* one persistent wavefront kernel per cem_step call */
 
 typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
 

@@ -18,7 +18,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcem.so")
+LIB_PATH = os.environ.get("CEM_LIB") or os.path.join(_HERE, "libcem.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -33,6 +33,8 @@ STATUS_NAMES = ["CEM_OK", "CEM_EINVAL", "CEM_EDEGENERATE", "CEM_ENEGVOL", "CEM_E
                 "CEM_ENONFINITE", "CEM_ECUDA", "CEM_ENCCL", "CEM_ESTATE", "CEM_ENOMEM"]
 CEM_F_NO_EARLY_OUT = 0x1
 CEM_F_STAGED = 0x2
+CEM_F_NO_DISCARD = 0x4
+CEM_F_PERSISTENT = 0x8
 CEM_HOST, CEM_DEVICE = 0, 1
 
 D = C.POINTER(C.c_double)

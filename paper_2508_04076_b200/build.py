@@ -30,23 +30,23 @@ def _stale() -> bool:
     return any(os.path.getmtime(f) > t for f in files)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    if not force and out == SO and not _stale():
         return SO
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, os.path.splitext(src)[0] + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = SO + ".tmp"
+    tmp = out + ".tmp"
     subprocess.check_call([NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *objs, "-lgomp"])
-    os.replace(tmp, SO)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    return SO
+    return out
 
 
 if __name__ == "__main__":

@@ -2,6 +2,7 @@
 // host<->device transfers, the persistent-kernel step loop and state readback.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -377,7 +378,11 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     const int occ = std::max(1, persistent_occupancy(smem));
     ctx->grid = sms * occ;
-    build_schedule(ctx->p, ctx->grid);
+    {
+        const char *ev = getenv("CEM_SCHED_SLACK");  // tuning knob: slack in units of resident CTAs
+        const double slack = ev ? atof(ev) : 3.0;
+        build_schedule(ctx->p, (int)(slack * ctx->grid));
+    }
     if (!ctx->stream) {  // graphs / persistent launches never use the legacy default stream
         if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
             ctx->err = "cudaStreamCreate failed";
@@ -446,7 +451,9 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (!ctx || nsteps < 0) return CEM_EINVAL;
     if (nsteps == 0) return CEM_OK;
     if (crack_every < 0) crack_every = 0;
-    const bool staged = ctx->profiling || (ctx->flags & CEM_F_STAGED);
+    // default: one kernel per stage (measured faster than the persistent wavefront kernel on
+    // B200 for the current stage bodies; CEM_F_PERSISTENT selects the latter)
+    const bool staged = ctx->profiling || !(ctx->flags & CEM_F_PERSISTENT);
     if (staged) {
         // one kernel per stage; with profiling, CUDA events bracket every stage
         if (ctx->profiling) {

@@ -609,7 +609,10 @@ __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
     for (int64_t l = threadIdx.x; l < bytes / 128; l += blockDim.x) discard_l2(base + off + 128 * l);
 }
 
-__global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
+#ifndef CEM_PERSIST_MINB
+#define CEM_PERSIST_MINB 4
+#endif
+__global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
     extern __shared__ double sm[];
     __shared__ unsigned long long sh_q;
     __shared__ int sh_ndisc;
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(256, 3) k_persistent(Dev d, int64_t step0, int
             default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
         }
         __syncthreads();
-        if (g != ST_A) {
+        if (g != ST_A && !(d.flags & CEM_F_NO_DISCARD)) {
             // consumers of intermediates: the last one of each producer block discards it
             if (tid < 32) {
                 int32_t *cd = d.cons_done + (int64_t)(g - 1) * d.maxblk;

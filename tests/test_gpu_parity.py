@@ -109,18 +109,25 @@ def test_early_out_is_conservative():
     assert np.array_equal(sa.rec_elem, sb.rec_elem) and np.array_equal(sa.u, sb.u)
 
 
-def test_staged_path_bitwise():
-    """One kernel per stage (CEM_F_STAGED) gives the same bits as the persistent kernel."""
+@pytest.mark.parametrize("flags", ["PERSISTENT", "PERSISTENT|NO_DISCARD"])
+def test_persistent_path_bitwise(flags):
+    """The persistent wavefront kernel gives the same bits as the oracle (and the staged path)."""
     cem = _gpu()
+    fl = 0
+    for f in flags.split("|"):
+        fl |= getattr(cem, "CEM_F_" + f)
     p = ci.weak_scaling_block(P=1, cells_per_rank=(24, 20, 4), steps=150)
-    sim, orc = run_pair(p, 150, 1, chunks=3, flags=cem.CEM_F_STAGED)
+    sim, orc = run_pair(p, 150, 1, chunks=3, flags=fl)
     assert_parity(sim, orc, p)
+    q = ci.config(0)
+    sim, orc = run_pair(q, 200, 1, chunks=2, flags=fl)
+    assert_parity(sim, orc, q)
 
 
 def test_mixed_staged_then_persistent():
     cem = _gpu()
     p = ci.config(0)
-    sim = cem.Simulation.from_problem(p)
+    sim = cem.Simulation.from_problem(p, flags=cem.CEM_F_PERSISTENT)
     orc = oracle.Oracle(p)
     sim.set_profiling(True); sim.step(37, 1); sim.set_profiling(False)
     sim.step(63, 1)
