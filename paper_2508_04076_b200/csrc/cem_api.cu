@@ -62,15 +62,17 @@ struct Layout {
 
 struct Offs {
     size_t conn, geoV, geoC, geoG, eedge, edge_off, node_off, node_ent, X, fext, nflag, dir_v0, gc;
-    size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, trec, srec, fe, ctr;
+    size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, inc_local, fpos, gbase, self, ncons, cons_done;
+    size_t nlb_off, nlb, tconn;
     size_t total;
 };
 
 Offs layout(const HostMesh &h, const Plan &p) {
     const int64_t N = h.N, E = h.E, S = h.S;
-    const int64_t P = p.nblk[0] + p.nblk[1] + p.nblk[2] + p.nblk[3];
+    int64_t P = 0;
+    for (int g = 0; g < ST_COUNT; ++g) P += p.nblk[g];
     Layout L;
     Offs o{};
     o.conn = L.take<int4>(E);
@@ -95,7 +97,6 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.u1 = L.take<double4>(N);
     o.v = L.take<double4>(N);
     o.a = L.take<double4>(N);
-    o.trec = L.take<double>(8 * E);
     o.srec = L.take<double>(8 * S);
     o.fe = L.take<double4>(p.nslots);
     o.ctr = L.take<int32_t>(8);
@@ -104,7 +105,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.rec_cand = L.take<int32_t>(E);
     o.rec_G = L.take<double>(E);
     o.rec_area = L.take<double>(E);
-    o.cnt = L.take<int32_t>(4 * (int64_t)p.maxblk);
+    o.cnt = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
     o.dep_off = L.take<int32_t>((int64_t)p.dep_off.size());
     o.dep = L.take<int32_t>((int64_t)p.dep.size());
     o.sched = L.take<int32_t>(P);
@@ -121,14 +122,17 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.fpos = L.take<int32_t>((int64_t)p.fpos.size());
     o.gbase = L.take<int32_t>((int64_t)p.gbase.size());
     o.self = L.take<Dev>(1);
-    o.ncons = L.take<int32_t>(3 * (int64_t)p.maxblk);
-    o.cons_done = L.take<int32_t>(3 * (int64_t)p.maxblk);
+    o.ncons = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
+    o.cons_done = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
+    o.nlb_off = L.take<int32_t>((int64_t)p.nlb_off.size());
+    o.nlb = L.take<int32_t>((int64_t)p.nlb.size());
+    o.tconn = L.take<uint16_t>((int64_t)p.tconn.size());
     o.total = L.off;
     return o;
 }
 
-int smem_bytes_for(const Plan &p) {
-    const int n = std::max({3 * p.max_nl, 7 * p.max_tl, 7 * p.max_el + 3 * p.max_nl});
+int smem_bytes_for(const Plan &p) {  // odd plane strides, see pstride()
+    const int n = std::max(3 * (p.max_nlb | 1) + 7 * (p.max_tl | 1), 7 * (p.max_el | 1) + 3 * (p.max_nl | 1));
     return 8 * n;
 }
 
@@ -167,7 +171,6 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.ubuf[1] = at<double4>(b, o.u1);
     d.v = at<double4>(b, o.v);
     d.a = at<double4>(b, o.a);
-    d.trec = at<double>(b, o.trec);
     d.srec = at<double>(b, o.srec);
     d.fe = at<double4>(b, o.fe);
     d.nl_off = at<int32_t>(b, o.nl_off);
@@ -185,6 +188,9 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.self = at<Dev>(b, o.self);
     d.ncons = at<int32_t>(b, o.ncons);
     d.cons_done = at<int32_t>(b, o.cons_done);
+    d.nlb_off = at<int32_t>(b, o.nlb_off);
+    d.nlb = at<int32_t>(b, o.nlb);
+    d.tconn = at<uint16_t>(b, o.tconn);
     d.ctr = at<int32_t>(b, o.ctr);
     d.rec_step = at<int64_t>(b, o.rec_step);
     d.rec_elem = at<int32_t>(b, o.rec_elem);
@@ -283,12 +289,11 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.u1, u1.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.v, v4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.trec), 0, sizeof(double) * 8 * E, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 8 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * p.nslots, st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * 4 * p.maxblk, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
     CUDA_TRY(put(o.dep_off, p.dep_off.data(), sizeof(int32_t) * p.dep_off.size()));
     CUDA_TRY(put(o.dep, p.dep.data(), sizeof(int32_t) * p.dep.size()));
     CUDA_TRY(put(o.nl_off, p.nl_off.data(), sizeof(int32_t) * p.nl_off.size()));
@@ -305,7 +310,10 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.sched, p.sched.data(), sizeof(int32_t) * p.sched.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.head), 0, sizeof(unsigned long long), st));
     CUDA_TRY(put(o.ncons, p.ncons.data(), sizeof(int32_t) * p.ncons.size()));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cons_done), 0, sizeof(int32_t) * 3 * p.maxblk, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cons_done), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
+    CUDA_TRY(put(o.nlb_off, p.nlb_off.data(), sizeof(int32_t) * p.nlb_off.size()));
+    CUDA_TRY(put(o.nlb, p.nlb.data(), sizeof(int32_t) * p.nlb.size()));
+    CUDA_TRY(put(o.tconn, p.tconn.data(), sizeof(uint16_t) * p.tconn.size()));
     CUDA_TRY(put(o.self, &ctx->d, sizeof(Dev)));
     CUDA_TRY(cudaStreamSynchronize(st));
     return CEM_OK;
@@ -457,7 +465,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (staged) {
         // one kernel per stage; with profiling, CUDA events bracket every stage
         if (ctx->profiling) {
-            const size_t need = (size_t)(ctx->prof_steps + nsteps) * 5;
+            const size_t need = (size_t)(ctx->prof_steps + nsteps) * (ST_COUNT + 1);
             while (ctx->ev.size() < need) {
                 cudaEvent_t e;
                 CUDA_TRY(cudaEventCreate(&e));
@@ -465,18 +473,18 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
             }
         }
         for (int64_t i = 0; i < nsteps; ++i) {
-            cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * 5 : nullptr;
+            cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * (ST_COUNT + 1) : nullptr;
             launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E);
         }
         CUDA_TRY(cudaGetLastError());
         if (ctx->profiling) ctx->prof_steps += nsteps;
-        ctx->launches += 4 * nsteps;
+        ctx->launches += ST_COUNT * nsteps;
         ctx->step += nsteps;
         return CEM_OK;
     }
     if (ctx->cnt_valid != ctx->step) {
         // steps ran outside the wavefront: every block is complete through ctx->step
-        const int64_t n = 4 * (int64_t)ctx->p.maxblk;
+        const int64_t n = ST_COUNT * (int64_t)ctx->p.maxblk;
         k_fill<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->d.cnt, n, (int32_t)ctx->step);
         ctx->launches += 1;
     }
@@ -489,17 +497,17 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
 }
 
 cem_status cem_kernel_times(const cem_ctx *ctx, int32_t *n, const char **names, double *ms, int32_t cap) {
-    static const char *kNames[4] = {"stage_A_strain", "stage_B_edge_stress", "stage_C_force_criterion",
-                                    "stage_D_node_update"};
+    static const char *kNames[ST_COUNT] = {"stage_AB_strain_edge_stress", "stage_C_force_criterion",
+                                           "stage_D_node_update"};
     if (!ctx || !n) return CEM_EINVAL;
-    *n = 4;
-    if (cap < 4) return CEM_OK;
-    for (int k = 0; k < 4; ++k) {
+    *n = ST_COUNT;
+    if (cap < ST_COUNT) return CEM_OK;
+    for (int k = 0; k < ST_COUNT; ++k) {
         if (names) names[k] = kNames[k];
         double tot = 0.0;
         for (int64_t i = 0; i < ctx->prof_steps; ++i) {
             float t = 0.f;
-            cudaEvent_t *E = const_cast<cudaEvent_t *>(ctx->ev.data()) + i * 5;
+            cudaEvent_t *E = const_cast<cudaEvent_t *>(ctx->ev.data()) + i * (ST_COUNT + 1);
             if (cudaEventSynchronize(E[k + 1]) != cudaSuccess) return CEM_ECUDA;
             if (cudaEventElapsedTime(&t, E[k], E[k + 1]) != cudaSuccess) return CEM_ECUDA;
             tot += t;
@@ -514,7 +522,7 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
     int32_t before = 0, after = 0;
     CUDA_TRY(cudaMemcpyAsync(&before, ctx->d.ctr, sizeof before, cudaMemcpyDeviceToHost, ctx->stream));
     launch_crack_only(ctx->d, ctx->step, ctx->stream);
-    ctx->launches += 4;
+    ctx->launches += 3;
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(&after, ctx->d.ctr, sizeof after, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));

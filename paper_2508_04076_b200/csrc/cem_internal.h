@@ -44,7 +44,9 @@ cem_status count_edges(const cem_mesh_in *m, int64_t *S, std::string &err);
 // Storage ("new") numbering: tets sorted by (sweep-axis slab of the centroid, original id),
 // nodes and edges by first appearance in that tet order.  Summation lists keep the
 // ORIGINAL tet order so every sum matches the oracle bit for bit.
-enum Stage { ST_A = 0, ST_B = 1, ST_C = 2, ST_D = 3, ST_COUNT = 4 };
+// AB: strain of the block's tets + smoothed edge stress (fused), C: element force + crack
+// criterion, D: node update.
+enum Stage { ST_AB = 0, ST_C = 1, ST_D = 2, ST_COUNT = 3 };
 
 struct Plan {
     std::vector<int32_t> tet_new2old, tet_old2new, node_new2old, node_old2new, edge_new2old;
@@ -59,11 +61,11 @@ struct Plan {
     std::vector<double> gc;
     // blocks and the wavefront schedule
     int blk = 256;                    // entities per work item
-    int nblk[ST_COUNT] = {0, 0, 0, 0};
+    int nblk[ST_COUNT] = {0, 0, 0};
     int maxblk = 0;
     std::vector<int32_t> dep_off;     // [ST_COUNT * maxblk + 1] CSR of producer blocks per (stage, block)
     std::vector<int32_t> dep;         // producer block ids (of the producing stage)
-    std::vector<int32_t> ncons;       // [3][maxblk] consumer blocks of each A/B/C block (discard counts)
+    std::vector<int32_t> ncons;       // [ST_COUNT][maxblk] consumer blocks of each block (discard counts)
     std::vector<int32_t> sched;       // [P]: stage << 28 | block
     // block gather lists (deduplicated producer records staged in shared memory)
     std::vector<int32_t> nl_off, nl;  // tet block -> sorted unique node ids
@@ -71,12 +73,14 @@ struct Plan {
     std::vector<int32_t> el_off, el;  // tet block -> sorted unique edge ids
     std::vector<uint16_t> ledge;      // [E][8] index of each tet edge in its block's edge list (6 used)
     std::vector<int32_t> tl_off, tl;  // edge block -> sorted unique incident tet ids
+    std::vector<int32_t> nlb_off, nlb;  // edge block -> sorted unique nodes of its tet list
+    std::vector<uint16_t> tconn;      // [|tl|][4] node index (in nlb) of each tet-list entry
     std::vector<uint16_t> inc_local;  // [6E] (CSR order of edge_inc) index into the edge block's tet list
     std::vector<int32_t> fpos;        // [E][4] slot of f_{e,a} in the node-major force array
     std::vector<int32_t> gbase;       // [N/32 + 1] warp-interleaved force slots: node k = 32 g + lane,
                                       //   its j-th incidence at gbase[g] + 32 j + lane
     int64_t nslots = 0;
-    int max_nl = 0, max_el = 0, max_tl = 0;
+    int max_nl = 0, max_el = 0, max_tl = 0, max_nlb = 0;
 };
 
 void build_plan(const HostMesh &h, int blk, Plan &p);
@@ -105,10 +109,10 @@ struct Dev {
     int32_t *dirty;            // [N] step stamp of the last split touching the node
     double4 *ubuf[2];          // u_m lives in ubuf[m & 1]
     double4 *v, *a;
-    double *trec;              // [E][8]: V_e eps_e (6), V_e if active else 0, pad
     double *srec;              // [S][8]: sigma_s (6), Gershgorin bound g_s, pad
     double4 *fe;               // [nslots] node-major force slots f_{e,a} (x,y,z,pad) at fpos[e][a]
-    const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *gbase;
+    const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *gbase, *nlb_off, *nlb;
+    const uint16_t *tconn;
     const int4 *fpos;
     const uint16_t *lconn, *ledge, *inc_local;
     int smem_bytes;
@@ -123,8 +127,8 @@ struct Dev {
     // persistent wavefront
     int32_t *cnt;              // [ST_COUNT][maxblk] completed-step counters
     const int32_t *dep_off, *dep;
-    const int32_t *ncons;      // [3][maxblk] consumers of each A/B/C block
-    int32_t *cons_done;        // [3][maxblk] consumers finished with the block this step
+    const int32_t *ncons;      // [ST_COUNT][maxblk] consumers of each AB/C block
+    int32_t *cons_done;        // [ST_COUNT][maxblk] consumers finished with the block this step
     const int32_t *sched;      // [P]
     unsigned long long *head;  // work-queue head
     int blk, P, maxblk;

@@ -81,7 +81,7 @@ __device__ __forceinline__ void stage_nodes(const Dev &d, const double4 *u, int3
 #pragma unroll
         for (int t = 0; t < kIlp; ++t) {
             const int i = base + t * blockDim.x;
-            if (i < tot) pl[(i - 3 * (i / 3)) * nn + i / 3] = v[t];
+            if (i < tot) pl[(i - 3 * (i / 3)) * (nn | 1) + i / 3] = v[t];
         }
     }
 }
@@ -103,62 +103,89 @@ __device__ __forceinline__ void stage_records(const double *src, const int32_t *
 #pragma unroll
         for (int t = 0; t < kIlp; ++t) {
             const int i = base + t * blockDim.x;
-            if (i < tot && (i & 7) < ncomp) pl[(i & 7) * n + (i >> 3)] = v[t];
+            if (i < tot && (i & 7) < ncomp) pl[(i & 7) * (n | 1) + (i >> 3)] = v[t];
         }
     }
 }
 
-// ------------------------------------------------------------------ stage A: element strain
-// eps = sum_a B_a u_a (a = 0..3 in order), Voigt (11,22,33,12,23,13) with engineering
-// shears; gradN0 = -((gradN1 + gradN2) + gradN3); tau = V eps.  Record: tau (6), V if
-// active else 0, pad.
-__device__ __forceinline__ void block_A(const Dev &d, int b, const double4 *u, double *sm) {
-    const int32_t n0 = __ldg(d.nl_off + b);
-    const int nn = __ldg(d.nl_off + b + 1) - n0;
-    stage_nodes(d, u, n0, nn, sm);
-    __syncthreads();
-    const int64_t e = (int64_t)b * d.blk + threadIdx.x;
-    if (e >= d.E) return;
-    double4 *o = reinterpret_cast<double4 *>(d.trec + 8 * e);
-    if (!d.state[e]) {
-        st256(o + 1, 0.0, 0.0, 0.0, 0.0);  // V slot = 0 marks "inactive" for stage B
-        return;
-    }
-    const int64_t E = d.E;
-    double g[4][3];
-#pragma unroll
-    for (int a = 1; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) g[a][c] = ldro(d.geoG + (int64_t)(3 * (a - 1) + c) * E + e);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-    const double V = ldro(d.geoV + e);
-    const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
-    const int li[4] = {lc.x, lc.y, lc.z, lc.w};
-    double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double ux = sm[li[a]], uy = sm[nn + li[a]], uz = sm[2 * nn + li[a]];
-        const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
-        ex = ex + gx * ux;
-        ey = ey + gy * uy;
-        ez = ez + gz * uz;
-        gxy = gxy + (gy * ux + gx * uy);
-        gyz = gyz + (gz * uy + gy * uz);
-        gxz = gxz + (gz * ux + gx * uz);
-    }
-    st256(o, V * ex, V * ey, V * ez, V * gxy);
-    st256(o + 1, V * gyz, V * gxz, V, 0.0);
-}
+// plane strides are odd so the 8-byte planes of a record fall into different bank pairs
+__host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
-// ------------------------------------------------------------------ stage B: edge stress
-// Vhat = sum V_e, T = sum tau_e over active incident tets in original-id order;
-// eps~ = T * (1/Vhat); sigma_ii = (lam+2mu) eps_ii + lam (eps_jj + eps_kk), sigma_ij = mu gamma_ij.
-// Also the Gershgorin bound g = max_i sum_j |sigma_ij| (early-out of stage C).
-__device__ __forceinline__ void block_B(const Dev &d, int b, double *sm) {
+// ------------------------------------------------------------------ stage AB: strain + edge stress
+// For the edge block's deduplicated tet list: eps = sum_a B_a u_a (a = 0..3 in order), Voigt
+// (11,22,33,12,23,13) with engineering shears, gradN0 = -((gradN1 + gradN2) + gradN3),
+// tau = V eps -> shared-memory planes (V = 0 marks an inactive tet).
+// Then per edge: Vhat = sum V_e, T = sum tau_e over the active incident tets in original-id
+// order, eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj +
+// eps_kk), sigma_ij = mu gamma_ij, plus the Gershgorin bound
+// g = max_i sum_j |sigma_ij| used by the early-out of stage C.
+__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm) {
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
-    stage_records(d.trec, d.tl + t0, nt, 7, sm);
+    const int32_t n0 = __ldg(d.nlb_off + b);
+    const int nn = __ldg(d.nlb_off + b + 1) - n0;
+    const int un = pstride(nn), tn = pstride(nt);
+    double *U = sm, *T = sm + 3 * un;
+    {  // stage u of the tet list's nodes
+        const int tot = 3 * nn;
+        for (int base = threadIdx.x; base < tot; base += kIlp * blockDim.x) {
+            int32_t id[kIlp];
+            double v[kIlp];
+#pragma unroll
+            for (int t = 0; t < kIlp; ++t) {
+                const int i = base + t * blockDim.x;
+                id[t] = i < tot ? __ldg(d.nlb + n0 + i / 3) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < kIlp; ++t) {
+                const int i = base + t * blockDim.x;
+                v[t] = i < tot ? reinterpret_cast<const double *>(u + id[t])[i - 3 * (i / 3)] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < kIlp; ++t) {
+                const int i = base + t * blockDim.x;
+                if (i < tot) U[(i - 3 * (i / 3)) * un + i / 3] = v[t];
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t E = d.E;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+        const int64_t e = __ldg(d.tl + t0 + i);
+        if (!d.state[e]) {
+            T[6 * tn + i] = 0.0;
+            continue;
+        }
+        double g[4][3];
+#pragma unroll
+        for (int a = 1; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[a][c] = ldro(d.geoG + (int64_t)(3 * (a - 1) + c) * E + e);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+        const double V = ldro(d.geoV + e);
+        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
+        const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+        double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const double ux = U[li[a]], uy = U[un + li[a]], uz = U[2 * un + li[a]];
+            const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
+            ex = ex + gx * ux;
+            ey = ey + gy * uy;
+            ez = ez + gz * uz;
+            gxy = gxy + (gy * ux + gx * uy);
+            gyz = gyz + (gz * uy + gy * uz);
+            gxz = gxz + (gz * ux + gx * uz);
+        }
+        T[i] = V * ex;
+        T[tn + i] = V * ey;
+        T[2 * tn + i] = V * ez;
+        T[3 * tn + i] = V * gxy;
+        T[4 * tn + i] = V * gyz;
+        T[5 * tn + i] = V * gxz;
+        T[6 * tn + i] = V;
+    }
     __syncthreads();
     const int64_t s = (int64_t)b * d.blk + threadIdx.x;
     if (s >= d.S) return;
@@ -170,15 +197,15 @@ __device__ __forceinline__ void block_B(const Dev &d, int b, double *sm) {
     for (int t = 0; t < kPre; ++t) pre[t] = j0 + t < j1 ? __ldg(d.inc_local + j0 + t) : 0;
     for (int32_t j = j0; j < j1; ++j) {
         const int r = j - j0 < kPre ? pre[j - j0] : __ldg(d.inc_local + j);
-        const double Ve = sm[6 * nt + r];
+        const double Ve = T[6 * tn + r];
         if (Ve == 0.0) continue;  // inactive tet
         Vh = Vh + Ve;
-        T0 = T0 + sm[r];
-        T1 = T1 + sm[nt + r];
-        T2 = T2 + sm[2 * nt + r];
-        T3 = T3 + sm[3 * nt + r];
-        T4 = T4 + sm[4 * nt + r];
-        T5 = T5 + sm[5 * nt + r];
+        T0 = T0 + T[r];
+        T1 = T1 + T[tn + r];
+        T2 = T2 + T[2 * tn + r];
+        T3 = T3 + T[3 * tn + r];
+        T4 = T4 + T[4 * tn + r];
+        T5 = T5 + T[5 * tn + r];
     }
     double4 *o = reinterpret_cast<double4 *>(d.srec + 8 * s);
     if (Vh == 0.0) {
@@ -416,7 +443,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int nn = __ldg(d.nl_off + b + 1) - n0;
     const bool early = crack && !(d.flags & CEM_F_NO_EARLY_OUT);
     stage_records(d.srec, d.el + s0i, ne, 7, sm);
-    double *smu = sm + 7 * ne;
+    double *smu = sm + 7 * pstride(ne);
     if (early) stage_nodes(d, u, n0, nn, smu);
     __syncthreads();
     const int64_t e = (int64_t)b * d.blk + threadIdx.x;
@@ -432,16 +459,17 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
                        (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
     double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
+    const int np = pstride(ne);
 #pragma unroll
     for (int l = 0; l < 6; ++l) {
         const int r = le[l];
         S0 = S0 + sm[r];
-        S1 = S1 + sm[ne + r];
-        S2 = S2 + sm[2 * ne + r];
-        S3 = S3 + sm[3 * ne + r];
-        S4 = S4 + sm[4 * ne + r];
-        S5 = S5 + sm[5 * ne + r];
-        gmax = fmax(gmax, sm[6 * ne + r]);
+        S1 = S1 + sm[np + r];
+        S2 = S2 + sm[2 * np + r];
+        S3 = S3 + sm[3 * np + r];
+        S4 = S4 + sm[4 * np + r];
+        S5 = S5 + sm[5 * np + r];
+        gmax = fmax(gmax, sm[6 * np + r]);
     }
     double g[4][3];
 #pragma unroll
@@ -467,8 +495,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             ux[a] = smu[li[a]];
-            uy[a] = smu[nn + li[a]];
-            uz[a] = smu[2 * nn + li[a]];
+            uy[a] = smu[pstride(nn) + li[a]];
+            uz[a] = smu[2 * pstride(nn) + li[a]];
         }
         double d2 = 0.0;
 #pragma unroll
@@ -593,11 +621,7 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
     const char *base;
     int64_t bytes, off;
-    if (pg == ST_A) {
-        base = reinterpret_cast<const char *>(d.trec);
-        off = (int64_t)pb * d.blk * 64;
-        bytes = min((int64_t)d.blk, d.E - (int64_t)pb * d.blk) * 64;
-    } else if (pg == ST_B) {
+    if (pg == ST_AB) {
         base = reinterpret_cast<const char *>(d.srec);
         off = (int64_t)pb * d.blk * 64;
         bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 64;
@@ -635,10 +659,10 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
         const int g = code >> 28, b = code & 0x0FFFFFFF;
         const int64_t qd = (int64_t)g * d.maxblk + b;
         const int dlo = __ldg(d.dep_off + qd), dhi = __ldg(d.dep_off + qd + 1);
-        const int pg = g == ST_A ? ST_D : g - 1;
+        const int pg = g == ST_AB ? ST_D : g - 1;
         // wait for the producer blocks (warp 0; lanes poll counters in parallel)
         if (tid < 32) {
-            const int need = g == ST_A ? (int)s : (int)(s + 1);
+            const int need = g == ST_AB ? (int)s : (int)(s + 1);
             const int32_t *c = d.cnt + (int64_t)pg * d.maxblk;
             for (int i = dlo + tid; i < dhi; i += 32) {
                 const int pb = __ldg(d.dep + i);
@@ -650,13 +674,12 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
         __syncthreads();
         const double4 *u1 = d.ubuf[(s + 1) & 1];
         switch (g) {
-            case ST_A: block_A(d, b, u1, sm); break;
-            case ST_B: block_B(d, b, sm); break;
+            case ST_AB: block_AB(d, b, u1, sm); break;
             case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
             default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
         }
         __syncthreads();
-        if (g != ST_A && !(d.flags & CEM_F_NO_DISCARD)) {
+        if (g != ST_AB && !(d.flags & CEM_F_NO_DISCARD)) {
             // consumers of intermediates: the last one of each producer block discards it
             if (tid < 32) {
                 int32_t *cd = d.cons_done + (int64_t)(g - 1) * d.maxblk;
@@ -685,13 +708,9 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 }
 
 // ------------------------------------------------------------------ staged kernels (one per stage)
-__global__ void __launch_bounds__(256) k_A(Dev d, int64_t s) {
+__global__ void __launch_bounds__(256) k_AB(Dev d, int64_t s) {
     extern __shared__ double sm[];
-    block_A(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
-}
-__global__ void __launch_bounds__(256) k_B(Dev d) {
-    extern __shared__ double sm[];
-    block_B(d, blockIdx.x, sm);
+    block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
 }
 __global__ void __launch_bounds__(256, 4) k_C(Dev d, int64_t s, int crack_every) {
     extern __shared__ double sm[];
@@ -702,11 +721,11 @@ __global__ void __launch_bounds__(256) k_D(Dev d, int64_t s) {
 }
 
 // criterion on the current state u_n (cem_crack_update)
-__global__ void __launch_bounds__(256) k_A_cur(Dev d, int64_t n) {
+__global__ void __launch_bounds__(256) k_AB_cur(Dev d, int64_t n) {
     extern __shared__ double sm[];
-    block_A(d, blockIdx.x, d.ubuf[n & 1], sm);
+    block_AB(d, blockIdx.x, d.ubuf[n & 1], sm);
 }
-__global__ void __launch_bounds__(256) k_C_cur(Dev d, int64_t n, int32_t stamp) {
+__global__ void __launch_bounds__(256, 4) k_C_cur(Dev d, int64_t n, int32_t stamp) {
     extern __shared__ double sm[];
     block_C(d, blockIdx.x, d.ubuf[n & 1], true, n, stamp, sm);
 }
@@ -743,10 +762,9 @@ int persistent_occupancy(int smem_bytes) {
 }
 
 void set_smem_limits(int smem_bytes) {
-    cudaFuncSetAttribute(k_A, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    cudaFuncSetAttribute(k_B, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_AB, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    cudaFuncSetAttribute(k_A_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_AB_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
@@ -758,20 +776,17 @@ void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_ev
 
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], st);
-    k_A<<<d.nblk[ST_A], 256, d.smem_bytes, st>>>(d, s);
+    k_AB<<<d.nblk[ST_AB], 256, d.smem_bytes, st>>>(d, s);
     if (ev) cudaEventRecord(ev[1], st);
-    k_B<<<d.nblk[ST_B], 256, d.smem_bytes, st>>>(d);
-    if (ev) cudaEventRecord(ev[2], st);
     k_C<<<d.nblk[ST_C], 256, d.smem_bytes, st>>>(d, s, crack_every);
-    if (ev) cudaEventRecord(ev[3], st);
+    if (ev) cudaEventRecord(ev[2], st);
     k_D<<<d.nblk[ST_D], 256, 0, st>>>(d, s);
-    if (ev) cudaEventRecord(ev[4], st);
+    if (ev) cudaEventRecord(ev[3], st);
 }
 
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st) {
     const int32_t stamp = -(int32_t)(n + 1);
-    k_A_cur<<<d.nblk[ST_A], 256, d.smem_bytes, st>>>(d, n);
-    k_B<<<d.nblk[ST_B], 256, d.smem_bytes, st>>>(d);
+    k_AB_cur<<<d.nblk[ST_AB], 256, d.smem_bytes, st>>>(d, n);
     k_C_cur<<<d.nblk[ST_C], 256, d.smem_bytes, st>>>(d, n, stamp);
     k_fix_cur<<<nblk(d.N), 256, 0, st>>>(d, n, stamp);
 }

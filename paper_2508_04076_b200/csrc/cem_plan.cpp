@@ -200,6 +200,26 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
             p.tl_off[b + 1] = (int32_t)p.tl.size();
             p.max_tl = std::max(p.max_tl, (int)tmp.size());
         }
+        // nodes of each edge block's tet list (the fused AB stage recomputes tau from them)
+        p.nlb_off.assign(nbs + 1, 0);
+        p.nlb.clear();
+        p.tconn.assign(4 * p.tl.size(), 0);
+        p.max_nlb = 0;
+        std::vector<int32_t> nodes;
+        for (int b = 0; b < nbs; ++b) {
+            nodes.clear();
+            for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
+                for (int a = 0; a < 4; ++a) nodes.push_back(p.conn[4 * (int64_t)p.tl[i] + a]);
+            std::sort(nodes.begin(), nodes.end());
+            nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+            for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
+                for (int a = 0; a < 4; ++a)
+                    p.tconn[4 * (int64_t)i + a] = (uint16_t)(std::lower_bound(nodes.begin(), nodes.end(),
+                                                                               p.conn[4 * (int64_t)p.tl[i] + a]) - nodes.begin());
+            p.nlb.insert(p.nlb.end(), nodes.begin(), nodes.end());
+            p.nlb_off[b + 1] = (int32_t)p.nlb.size();
+            p.max_nlb = std::max(p.max_nlb, (int)nodes.size());
+        }
         // node-major force slots, interleaved per warp of 32 consecutive nodes so that the
         // lanes of stage D read 32 consecutive slots per incidence index j
         const int64_t ng = (N + 31) / 32;
@@ -217,7 +237,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
                     p.gbase[k / 32] + 32 * (j - p.node_off[k]) + (int32_t)(k % 32);
     }
     // ---------------------------------------------------------------- blocks and dependencies
-    const int64_t cnt[ST_COUNT] = {E, S, E, N};
+    const int64_t cnt[ST_COUNT] = {S, E, N};
     p.maxblk = 0;
     for (int g = 0; g < ST_COUNT; ++g) {
         p.nblk[g] = (int)((cnt[g] + blk - 1) / blk);
@@ -229,17 +249,12 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
         std::sort(v.begin(), v.end());
         v.erase(std::unique(v.begin(), v.end()), v.end());
     };
-    for (int b = 0; b < p.nblk[ST_A]; ++b) {  // A: D-blocks (previous step) of its nodes
-        auto &v = deps[(size_t)ST_A * p.maxblk + b];
-        for (int32_t i = p.nl_off[b]; i < p.nl_off[b + 1]; ++i) v.push_back(p.nl[i] / blk);
+    for (int b = 0; b < p.nblk[ST_AB]; ++b) {  // AB: D-blocks (previous step) of its tet list's nodes
+        auto &v = deps[(size_t)ST_AB * p.maxblk + b];
+        for (int32_t i = p.nlb_off[b]; i < p.nlb_off[b + 1]; ++i) v.push_back(p.nlb[i] / blk);
         finish(v);
     }
-    for (int b = 0; b < p.nblk[ST_B]; ++b) {  // B: A-blocks of its tet list
-        auto &v = deps[(size_t)ST_B * p.maxblk + b];
-        for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i) v.push_back(p.tl[i] / blk);
-        finish(v);
-    }
-    for (int b = 0; b < p.nblk[ST_C]; ++b) {  // C: B-blocks of its edge list
+    for (int b = 0; b < p.nblk[ST_C]; ++b) {  // C: AB-blocks of its edge list
         auto &v = deps[(size_t)ST_C * p.maxblk + b];
         for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) v.push_back(p.el[i] / blk);
         finish(v);
@@ -250,8 +265,8 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) v.push_back((p.node_ent[j] >> 2) / blk);
         finish(v);
     }
-    p.ncons.assign((size_t)3 * p.maxblk, 0);
-    for (int g = ST_B; g <= ST_D; ++g)
+    p.ncons.assign((size_t)ST_COUNT * p.maxblk, 0);
+    for (int g = ST_C; g <= ST_D; ++g)
         for (int b = 0; b < p.nblk[g]; ++b)
             for (int32_t pb : deps[(size_t)g * p.maxblk + b]) p.ncons[(size_t)(g - 1) * p.maxblk + pb]++;
     p.dep_off.assign((size_t)ST_COUNT * p.maxblk + 1, 0);
@@ -267,12 +282,13 @@ void build_schedule(Plan &p, int resident_ctas) {
     // virtual time: vt(A, b) = b / nA; a consumer sits delta after its latest producer,
     // delta = (resident CTAs) / (items per step), so by the time a CTA dequeues it its
     // producers have normally completed.  Sorted by vt this is a topological order.
-    const int P = p.nblk[0] + p.nblk[1] + p.nblk[2] + p.nblk[3];
+    int P = 0;
+    for (int g = 0; g < ST_COUNT; ++g) P += p.nblk[g];
     const double delta = std::max(1.0, (double)resident_ctas) / (double)P;
     std::vector<double> vt[ST_COUNT];
     for (int g = 0; g < ST_COUNT; ++g) vt[g].assign(p.nblk[g], 0.0);
-    for (int b = 0; b < p.nblk[ST_A]; ++b) vt[ST_A][b] = (double)b / (double)p.nblk[ST_A];
-    for (int g = ST_B; g <= ST_D; ++g)
+    for (int b = 0; b < p.nblk[ST_AB]; ++b) vt[ST_AB][b] = (double)b / (double)p.nblk[ST_AB];
+    for (int g = ST_C; g <= ST_D; ++g)
         for (int b = 0; b < p.nblk[g]; ++b) {
             double m = 0.0;
             const size_t q = (size_t)g * p.maxblk + b;
