@@ -61,10 +61,10 @@ struct Layout {
 };
 
 struct Offs {
-    size_t conn, geoV, geoC, geoG, eedge, edge_off, node_off, node_ent, X, fext, nflag, dir_v0, gc;
+    size_t conn, geoT, eedge, incE, nodeE, X, fext, nflag, dir_v0, gc;
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
-    size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, inc_local, fpos, gbase, self, ncons, cons_done;
+    size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn;
     size_t total;
 };
@@ -76,13 +76,10 @@ Offs layout(const HostMesh &h, const Plan &p) {
     Layout L;
     Offs o{};
     o.conn = L.take<int4>(E);
-    o.geoV = L.take<double>(E);
-    o.geoC = L.take<double>(E);
-    o.geoG = L.take<double>(9 * E);
+    o.geoT = L.take<double>((int64_t)p.geoT.size());
     o.eedge = L.take<int32_t>(6 * E);
-    o.edge_off = L.take<int32_t>(S + 1);
-    o.node_off = L.take<int32_t>(N + 1);
-    o.node_ent = L.take<int32_t>(4 * E);
+    o.incE = L.take<uint16_t>((int64_t)p.incE.size());
+    o.nodeE = L.take<int32_t>((int64_t)p.nodeE.size());
     o.X = L.take<double4>(N);
     o.fext = L.take<double4>(N);
     o.nflag = L.take<uint8_t>(N);
@@ -98,7 +95,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.v = L.take<double4>(N);
     o.a = L.take<double4>(N);
     o.srec = L.take<double>(8 * S);
-    o.fe = L.take<double4>(p.nslots);
+    o.fe = L.take<double4>(4 * ((E + 31) / 32) * 32);
     o.ctr = L.take<int32_t>(8);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
@@ -118,9 +115,6 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.ledge = L.take<uint16_t>((int64_t)p.ledge.size());
     o.tl_off = L.take<int32_t>((int64_t)p.tl_off.size());
     o.tl = L.take<int32_t>((int64_t)p.tl.size());
-    o.inc_local = L.take<uint16_t>((int64_t)p.inc_local.size());
-    o.fpos = L.take<int32_t>((int64_t)p.fpos.size());
-    o.gbase = L.take<int32_t>((int64_t)p.gbase.size());
     o.self = L.take<Dev>(1);
     o.ncons = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
     o.cons_done = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
@@ -150,13 +144,12 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.E = h.E;
     d.S = h.S;
     d.conn = at<int4>(b, o.conn);
-    d.geoV = at<double>(b, o.geoV);
-    d.geoC = at<double>(b, o.geoC);
-    d.geoG = at<double>(b, o.geoG);
+    d.geoT = at<double>(b, o.geoT);
     d.eedge = at<int32_t>(b, o.eedge);
-    d.edge_off = at<int32_t>(b, o.edge_off);
-    d.node_off = at<int32_t>(b, o.node_off);
-    d.node_ent = at<int32_t>(b, o.node_ent);
+    d.incE = at<uint16_t>(b, o.incE);
+    d.nodeE = at<int32_t>(b, o.nodeE);
+    d.we = p.we;
+    d.wn = p.wn;
     d.X = at<double4>(b, o.X);
     d.fext = at<double4>(b, o.fext);
     d.nflag = at<uint8_t>(b, o.nflag);
@@ -181,9 +174,6 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.ledge = at<uint16_t>(b, o.ledge);
     d.tl_off = at<int32_t>(b, o.tl_off);
     d.tl = at<int32_t>(b, o.tl);
-    d.inc_local = at<uint16_t>(b, o.inc_local);
-    d.fpos = at<int4>(b, o.fpos);
-    d.gbase = at<int32_t>(b, o.gbase);
     d.smem_bytes = smem_bytes_for(p);
     d.self = at<Dev>(b, o.self);
     d.ncons = at<int32_t>(b, o.ncons);
@@ -268,13 +258,10 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
         return cudaMemcpyAsync(at<char>(b, off), src, bytes, cudaMemcpyHostToDevice, st);
     };
     CUDA_TRY(put(o.conn, p.conn.data(), sizeof(int32_t) * 4 * E));
-    CUDA_TRY(put(o.geoV, p.geoV.data(), sizeof(double) * E));
-    CUDA_TRY(put(o.geoC, p.geoC.data(), sizeof(double) * E));
-    CUDA_TRY(put(o.geoG, p.geoG.data(), sizeof(double) * 9 * E));
+    CUDA_TRY(put(o.geoT, p.geoT.data(), sizeof(double) * p.geoT.size()));
     CUDA_TRY(put(o.eedge, p.eedge.data(), sizeof(int32_t) * 6 * E));
-    CUDA_TRY(put(o.edge_off, p.edge_off.data(), sizeof(int32_t) * (S + 1)));
-    CUDA_TRY(put(o.node_off, p.node_off.data(), sizeof(int32_t) * (N + 1)));
-    CUDA_TRY(put(o.node_ent, p.node_ent.data(), sizeof(int32_t) * p.node_ent.size()));
+    CUDA_TRY(put(o.incE, p.incE.data(), sizeof(uint16_t) * p.incE.size()));
+    CUDA_TRY(put(o.nodeE, p.nodeE.data(), sizeof(int32_t) * p.nodeE.size()));
     CUDA_TRY(put(o.X, X4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.fext, f4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.nflag, nflag.data(), N));
@@ -290,7 +277,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.v, v4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 8 * S, st));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * p.nslots, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * 4 * ((E + 31) / 32) * 32, st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
@@ -304,9 +291,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.ledge, p.ledge.data(), sizeof(uint16_t) * p.ledge.size()));
     CUDA_TRY(put(o.tl_off, p.tl_off.data(), sizeof(int32_t) * p.tl_off.size()));
     CUDA_TRY(put(o.tl, p.tl.data(), sizeof(int32_t) * p.tl.size()));
-    CUDA_TRY(put(o.inc_local, p.inc_local.data(), sizeof(uint16_t) * p.inc_local.size()));
-    CUDA_TRY(put(o.fpos, p.fpos.data(), sizeof(int32_t) * p.fpos.size()));
-    CUDA_TRY(put(o.gbase, p.gbase.data(), sizeof(int32_t) * p.gbase.size()));
+
     CUDA_TRY(put(o.sched, p.sched.data(), sizeof(int32_t) * p.sched.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.head), 0, sizeof(unsigned long long), st));
     CUDA_TRY(put(o.ncons, p.ncons.data(), sizeof(int32_t) * p.ncons.size()));

@@ -81,6 +81,12 @@ struct Plan {
                                       //   its j-th incidence at gbase[g] + 32 j + lane
     int64_t nslots = 0;
     int max_nl = 0, max_el = 0, max_tl = 0, max_nlb = 0;
+    // instruction-lean layouts
+    std::vector<double> geoT;         // [E/32][11][32]: V, V/6, gradN1..3 (x,y,z) per warp tile
+    int we = 8;                       // ELL width of edge incidences (multiple of 8)
+    std::vector<uint16_t> incE;       // [S][we] index into the edge block's tet list, 0xFFFF = none
+    int wn = 8;                       // ELL width of node incidences (multiple of 8)
+    std::vector<int32_t> nodeE;       // [N][wn] force slot of each incidence (original order), -1 = none
 };
 
 void build_plan(const HostMesh &h, int blk, Plan &p);
@@ -92,10 +98,7 @@ struct Dev {
     int64_t N, E, S;
     // read-only mesh tables (storage numbering)
     const int4 *conn;
-    const double *geoV, *geoC, *geoG;
     const int32_t *eedge;
-    const int32_t *edge_off, *edge_inc;
-    const int32_t *node_off, *node_ent;
     const double4 *X;
     const double4 *fext;
     const uint8_t *nflag;
@@ -110,11 +113,14 @@ struct Dev {
     double4 *ubuf[2];          // u_m lives in ubuf[m & 1]
     double4 *v, *a;
     double *srec;              // [S][8]: sigma_s (6), Gershgorin bound g_s, pad
-    double4 *fe;               // [nslots] node-major force slots f_{e,a} (x,y,z,pad) at fpos[e][a]
-    const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *gbase, *nlb_off, *nlb;
+    double4 *fe;               // [4E] force slots f_{e,a} (x,y,z,pad); slot(e,a) = ((e>>5)*4 + a)*32 + (e&31)
+    const double *geoT;        // [E/32][11][32] warp-tiled geometry
+    const uint16_t *incE;      // [S][we]
+    const int32_t *nodeE;      // [N][wn]
+    int we, wn;
+    const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
     const uint16_t *tconn;
-    const int4 *fpos;
-    const uint16_t *lconn, *ledge, *inc_local;
+    const uint16_t *lconn, *ledge;
     int smem_bytes;
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] spare

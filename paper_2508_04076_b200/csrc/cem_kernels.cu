@@ -57,6 +57,24 @@ __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, 
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
 }
 
+// warp-tiled geometry: tet e -> tile e>>5, lane e&31, component c at [tile][c][lane]
+__device__ __forceinline__ const double *geo_ptr(const Dev &d, int64_t e) { return d.geoT + (e >> 5) * 352 + (e & 31); }
+__device__ __forceinline__ int64_t slot_tet(int32_t slot) { return ((int64_t)(slot >> 7) << 5) + (slot & 31); }
+
+// lumped mass of node k from its active incidences in original order
+__device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
+    double acc = 0.0;
+    const int32_t *row = d.nodeE + k * d.wn;
+    for (int j = 0; j < d.wn; ++j) {
+        const int32_t sl = __ldg(row + j);
+        if (sl < 0) break;
+        const int64_t e = slot_tet(sl);
+        if (!d.state[e]) continue;
+        acc = acc + (d.rho * __ldg(geo_ptr(d, e))) / 4.0;
+    }
+    return acc;
+}
+
 // Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
 // (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
 // every later per-thread gather hits shared memory instead of an L1 line of its own.
@@ -126,44 +144,28 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const int nn = __ldg(d.nlb_off + b + 1) - n0;
     const int un = pstride(nn), tn = pstride(nt);
     double *U = sm, *T = sm + 3 * un;
-    {  // stage u of the tet list's nodes
-        const int tot = 3 * nn;
-        for (int base = threadIdx.x; base < tot; base += kIlp * blockDim.x) {
-            int32_t id[kIlp];
-            double v[kIlp];
-#pragma unroll
-            for (int t = 0; t < kIlp; ++t) {
-                const int i = base + t * blockDim.x;
-                id[t] = i < tot ? __ldg(d.nlb + n0 + i / 3) : 0;
-            }
-#pragma unroll
-            for (int t = 0; t < kIlp; ++t) {
-                const int i = base + t * blockDim.x;
-                v[t] = i < tot ? reinterpret_cast<const double *>(u + id[t])[i - 3 * (i / 3)] : 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < kIlp; ++t) {
-                const int i = base + t * blockDim.x;
-                if (i < tot) U[(i - 3 * (i / 3)) * un + i / 3] = v[t];
-            }
-        }
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
+        const double4 w = ld256(u + __ldg(d.nlb + n0 + i));
+        U[i] = w.x;
+        U[un + i] = w.y;
+        U[2 * un + i] = w.z;
     }
     __syncthreads();
-    const int64_t E = d.E;
     for (int i = threadIdx.x; i < nt; i += blockDim.x) {
         const int64_t e = __ldg(d.tl + t0 + i);
         if (!d.state[e]) {
             T[6 * tn + i] = 0.0;
             continue;
         }
+        const double *gp = geo_ptr(d, e);
         double g[4][3];
 #pragma unroll
         for (int a = 1; a < 4; ++a)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) g[a][c] = ldro(d.geoG + (int64_t)(3 * (a - 1) + c) * E + e);
+            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
 #pragma unroll
         for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-        const double V = ldro(d.geoV + e);
+        const double V = __ldg(gp);
         const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
         const int li[4] = {lc.x, lc.y, lc.z, lc.w};
         double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
@@ -189,23 +191,25 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     __syncthreads();
     const int64_t s = (int64_t)b * d.blk + threadIdx.x;
     if (s >= d.S) return;
-    const int32_t j0 = ldro(d.edge_off + s), j1 = ldro(d.edge_off + s + 1);
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    constexpr int kPre = 8;  // incidence indices prefetched together (Kuhn lattices: <= 6)
-    uint16_t pre[kPre];
+    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + s * d.we);
+    for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
+        const uint4 q = __ldg(row + (w >> 3));
+        const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int t = 0; t < kPre; ++t) pre[t] = j0 + t < j1 ? __ldg(d.inc_local + j0 + t) : 0;
-    for (int32_t j = j0; j < j1; ++j) {
-        const int r = j - j0 < kPre ? pre[j - j0] : __ldg(d.inc_local + j);
-        const double Ve = T[6 * tn + r];
-        if (Ve == 0.0) continue;  // inactive tet
-        Vh = Vh + Ve;
-        T0 = T0 + T[r];
-        T1 = T1 + T[tn + r];
-        T2 = T2 + T[2 * tn + r];
-        T3 = T3 + T[3 * tn + r];
-        T4 = T4 + T[4 * tn + r];
-        T5 = T5 + T[5 * tn + r];
+        for (int t = 0; t < 8; ++t) {
+            const int r = (qq[t >> 1] >> (16 * (t & 1))) & 0xffff;
+            if (r == 0xffff) continue;
+            const double Ve = T[6 * tn + r];
+            if (Ve == 0.0) continue;  // inactive tet
+            Vh = Vh + Ve;
+            T0 = T0 + T[r];
+            T1 = T1 + T[tn + r];
+            T2 = T2 + T[2 * tn + r];
+            T3 = T3 + T[3 * tn + r];
+            T4 = T4 + T[4 * tn + r];
+            T5 = T5 + T[5 * tn + r];
+        }
     }
     double4 *o = reinterpret_cast<double4 *>(d.srec + 8 * s);
     if (Vh == 0.0) {
@@ -431,10 +435,10 @@ __device__ __noinline__ void criterion_full(const Dev *__restrict__ dp, int64_t 
 }
 
 // ------------------------------------------------------------------ stage C: force + criterion
-// S = sum_{l=0..5} sigma_{s(e,l)}; f_{e,a} = c((gx S11 + gy S12) + gz S13), ... with c = V/6,
-// written to the node-major slot of (e, a).  Early-out: every
-// candidate satisfies |G| <= max_l g_{s(e,l)} * max_l |u_q - u_p|; tets below
-// Gc_e (1 - 1e-6) skip the 24-candidate evaluation.
+// S = sum_{l=0..5} sigma_{s(e,l)}; f_{e,a} = c((gx S11 + gy S12) + gz S13), ... with c = V/6
+// (PAPER.md:L340-L367), written to the warp-tiled force slots.  Early-out (DESIGN.md
+// "Early-out"): every candidate satisfies |G| <= max_l g_{s(e,l)} * max_l |u_q - u_p|; tets
+// below Gc_e (1 - 1e-6) skip the 24-candidate evaluation.
 __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
                                         int32_t stamp, double *sm) {
     const int32_t s0i = __ldg(d.el_off + b);
@@ -442,24 +446,39 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int32_t n0 = __ldg(d.nl_off + b);
     const int nn = __ldg(d.nl_off + b + 1) - n0;
     const bool early = crack && !(d.flags & CEM_F_NO_EARLY_OUT);
-    stage_records(d.srec, d.el + s0i, ne, 7, sm);
-    double *smu = sm + 7 * pstride(ne);
-    if (early) stage_nodes(d, u, n0, nn, smu);
+    const int np = pstride(ne), nq = pstride(nn);
+    double *smu = sm + 7 * np;
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {  // one sigma record per thread
+        const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8 * (int64_t)__ldg(d.el + s0i + i));
+        const double4 x = ld256(r), y = ld256(r + 1);
+        sm[i] = x.x;
+        sm[np + i] = x.y;
+        sm[2 * np + i] = x.z;
+        sm[3 * np + i] = x.w;
+        sm[4 * np + i] = y.x;
+        sm[5 * np + i] = y.y;
+        sm[6 * np + i] = y.z;
+    }
+    if (early)
+        for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+            const double4 w = ld256(u + __ldg(d.nl + n0 + i));
+            smu[i] = w.x;
+            smu[nq + i] = w.y;
+            smu[2 * nq + i] = w.z;
+        }
     __syncthreads();
     const int64_t e = (int64_t)b * d.blk + threadIdx.x;
     if (e >= d.E) return;
-    double4 *fo = d.fe + 4 * e;  // tet-major record: slot a = f_{e,a} (x, y, z, pad)
+    double4 *fo = d.fe + (e >> 5) * 128 + (e & 31);  // slot (e,a) = fo + 32 a
     if (!d.state[e]) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) st256(fo + a, 0.0, 0.0, 0.0, 0.0);
+        for (int a = 0; a < 4; ++a) st256(fo + 32 * a, 0.0, 0.0, 0.0, 0.0);
         return;
     }
-    const int64_t E = d.E;
     const uint4 lq = __ldg(reinterpret_cast<const uint4 *>(d.ledge) + e);
     const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
                        (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
     double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
-    const int np = pstride(ne);
 #pragma unroll
     for (int l = 0; l < 6; ++l) {
         const int r = le[l];
@@ -471,20 +490,21 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         S5 = S5 + sm[5 * np + r];
         gmax = fmax(gmax, sm[6 * np + r]);
     }
+    const double *gp = geo_ptr(d, e);
     double g[4][3];
 #pragma unroll
     for (int a = 1; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) g[a][c] = ldro(d.geoG + (int64_t)(3 * (a - 1) + c) * E + e);
+        for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-    const double cc = ldro(d.geoC + e);
+    const double cc = __ldg(gp + 32);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
         const double fy = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
         const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
-        st256(fo + a, fx, fy, fz, 0.0);
+        st256(fo + 32 * a, fx, fy, fz, 0.0);
     }
     if (!crack) return;
     const double gc = ldro(d.gc + e);
@@ -495,8 +515,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             ux[a] = smu[li[a]];
-            uy[a] = smu[pstride(nn) + li[a]];
-            uz[a] = smu[2 * pstride(nn) + li[a]];
+            uy[a] = smu[nq + li[a]];
+            uz[a] = smu[2 * nq + li[a]];
         }
         double d2 = 0.0;
 #pragma unroll
@@ -511,28 +531,28 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 }
 
 // ------------------------------------------------------------------ stage D: node update
-// f_int,k = sum over the node's incidence list (ascending original tet id) of f_{e,a}; the
-// incidence entries are fetched kIlp at a time so the record loads overlap.
+// f_int,k = sum over the node's ELL row of force slots (ascending original tet id, -1 = end);
+// slot indices are loaded 8 at a time and the 8 record loads issued together.
 __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p, double4 *u2p, int64_t s) {
     const int64_t k = (int64_t)b * d.blk + threadIdx.x;
     if (k >= d.N) return;
-    const int32_t j0 = ldro(d.node_off + k), j1 = ldro(d.node_off + k + 1);
+    const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + k * d.wn);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    for (int32_t jb = j0; jb < j1; jb += kIlp) {
-        int32_t ent[kIlp];
-        double4 f[kIlp];
+    for (int w = 0; w < d.wn; w += 8) {
+        const int4 qa = __ldg(row + (w >> 2)), qb = __ldg(row + (w >> 2) + 1);
+        const int32_t sl[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        double4 f[8];
 #pragma unroll
-        for (int t = 0; t < kIlp; ++t) ent[t] = jb + t < j1 ? ldro(d.node_ent + jb + t) : -1;
+        for (int t = 0; t < 8; ++t)
+            if (sl[t] >= 0) f[t] = ld256(d.fe + sl[t]);
 #pragma unroll
-        for (int t = 0; t < kIlp; ++t)
-            if (ent[t] >= 0) f[t] = ld256(d.fe + ent[t]);
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t)
-            if (ent[t] >= 0) {
+        for (int t = 0; t < 8; ++t)
+            if (sl[t] >= 0) {
                 f0 = f0 + f[t].x;
                 f1 = f1 + f[t].y;
                 f2 = f2 + f[t].z;
             }
+        if (sl[7] < 0) break;
     }
     double mk = d.mass[k];
     const uint8_t fl = __ldg(&d.nflag[k]);
@@ -573,17 +593,11 @@ __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p,
         }
     }
     if (d.dirty[k] == (int32_t)(s + 1)) {
-        // an incident tet split in this step: lumped mass from the active incidences
-        // (original order); m = 0 -> frozen, v = a = 0 (R15)
-        double acc = 0.0;
-        for (int32_t j = j0; j < j1; ++j) {
-            const int32_t ee = ldro(d.node_ent + j) >> 2;
-            if (!d.state[ee]) continue;
-            acc = acc + (d.rho * ldro(d.geoV + ee)) / 4.0;
-        }
-        mk = acc;
-        d.mass[k] = acc;
-        if (acc == 0.0) {
+        // an incident tet split in this step: lumped mass from the active incidences;
+        // m = 0 -> frozen, v = a = 0 (R15)
+        mk = node_mass(d, k);
+        d.mass[k] = mk;
+        if (mk == 0.0) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) vv[c] = aa[c] = 0.0;
         }
@@ -708,15 +722,24 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 }
 
 // ------------------------------------------------------------------ staged kernels (one per stage)
-__global__ void __launch_bounds__(256) k_AB(Dev d, int64_t s) {
+#ifndef CEM_AB_MINB
+#define CEM_AB_MINB 4
+#endif
+#ifndef CEM_C_MINB
+#define CEM_C_MINB 4
+#endif
+#ifndef CEM_D_MINB
+#define CEM_D_MINB 3
+#endif
+__global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
     extern __shared__ double sm[];
     block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
 }
-__global__ void __launch_bounds__(256, 4) k_C(Dev d, int64_t s, int crack_every) {
+__global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every) {
     extern __shared__ double sm[];
     block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
 }
-__global__ void __launch_bounds__(256) k_D(Dev d, int64_t s) {
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     block_D(d, blockIdx.x, d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
@@ -734,12 +757,7 @@ __global__ void __launch_bounds__(256, 4) k_C_cur(Dev d, int64_t n, int32_t stam
 __global__ void __launch_bounds__(256) k_fix_cur(Dev d, int64_t n, int32_t stamp) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= d.N || d.dirty[k] != stamp) return;
-    double acc = 0.0;
-    for (int32_t j = d.node_off[k]; j < d.node_off[k + 1]; ++j) {
-        const int32_t ee = d.node_ent[j] >> 2;
-        if (!d.state[ee]) continue;
-        acc = acc + (d.rho * d.geoV[ee]) / 4.0;
-    }
+    const double acc = node_mass(d, k);
     d.mass[k] = acc;
     if (acc == 0.0) {
         st4(&d.v[k], 0.0, 0.0, 0.0, 0.0);

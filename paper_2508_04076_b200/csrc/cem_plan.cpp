@@ -236,6 +236,32 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
                 p.fpos[4 * (int64_t)(p.node_ent[j] >> 2) + (p.node_ent[j] & 3)] =
                     p.gbase[k / 32] + 32 * (j - p.node_off[k]) + (int32_t)(k % 32);
     }
+    // ---------------------------------------------------------------- instruction-lean layouts
+    {
+        const int64_t nt = (E + 31) / 32;
+        p.geoT.assign(nt * 11 * 32, 0.0);
+        for (int64_t e = 0; e < E; ++e) {
+            double *g = p.geoT.data() + (e >> 5) * 352 + (e & 31);
+            g[0] = p.geoV[e];
+            g[32] = p.geoC[e];
+            for (int c = 0; c < 9; ++c) g[32 * (2 + c)] = p.geoG[(int64_t)c * E + e];
+        }
+        int mx = 1;
+        for (int64_t s = 0; s < S; ++s) mx = std::max(mx, p.edge_off[s + 1] - p.edge_off[s]);
+        p.we = (mx + 7) / 8 * 8;
+        p.incE.assign((size_t)S * p.we, 0xFFFF);
+        for (int64_t s = 0; s < S; ++s)
+            for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j) p.incE[(size_t)s * p.we + (j - p.edge_off[s])] = p.inc_local[j];
+        mx = 1;
+        for (int64_t k = 0; k < N; ++k) mx = std::max(mx, p.node_off[k + 1] - p.node_off[k]);
+        p.wn = (mx + 7) / 8 * 8;
+        p.nodeE.assign((size_t)N * p.wn, -1);
+        for (int64_t k = 0; k < N; ++k)
+            for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) {
+                const int64_t e = p.node_ent[j] >> 2, a = p.node_ent[j] & 3;
+                p.nodeE[(size_t)k * p.wn + (j - p.node_off[k])] = (int32_t)((((e >> 5) * 4 + a) << 5) + (e & 31));
+            }
+    }
     // ---------------------------------------------------------------- blocks and dependencies
     const int64_t cnt[ST_COUNT] = {S, E, N};
     p.maxblk = 0;
