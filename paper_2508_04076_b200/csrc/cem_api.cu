@@ -95,7 +95,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.v = L.take<double4>(N);
     o.a = L.take<double4>(N);
     o.srec = L.take<double>(8 * S);
-    o.fe = L.take<double4>(4 * ((E + 31) / 32) * 32);
+    o.fe = L.take<double4>(4 * ((E + 31) / 32) * 32 + 1);  // + the zero slot
     o.ctr = L.take<int32_t>(8);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
@@ -126,7 +126,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
 }
 
 int smem_bytes_for(const Plan &p) {  // odd plane strides, see pstride()
-    const int n = std::max(3 * (p.max_nlb | 1) + 7 * (p.max_tl | 1), 7 * (p.max_el | 1) + 3 * (p.max_nl | 1));
+    const int n = std::max(3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1), 7 * (p.max_el | 1) + 3 * (p.max_nl | 1));
     return 8 * n;
 }
 
@@ -149,6 +149,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.incE = at<uint16_t>(b, o.incE);
     d.nodeE = at<int32_t>(b, o.nodeE);
     d.we = p.we;
+    d.zslot = p.zslot;
     d.wn = p.wn;
     d.X = at<double4>(b, o.X);
     d.fext = at<double4>(b, o.fext);
@@ -277,7 +278,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.v, v4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 8 * S, st));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * 4 * ((E + 31) / 32) * 32, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * (4 * ((E + 31) / 32) * 32 + 1), st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));

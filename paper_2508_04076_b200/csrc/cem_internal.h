@@ -86,7 +86,8 @@ struct Plan {
     int we = 8;                       // ELL width of edge incidences (multiple of 8)
     std::vector<uint16_t> incE;       // [S][we] index into the edge block's tet list, 0xFFFF = none
     int wn = 8;                       // ELL width of node incidences (multiple of 8)
-    std::vector<int32_t> nodeE;       // [N][wn] force slot of each incidence (original order), -1 = none
+    std::vector<int32_t> nodeE;       // [N][wn] force slot of each incidence (original order), zslot = none
+    int32_t zslot = 0;
 };
 
 void build_plan(const HostMesh &h, int blk, Plan &p);
@@ -118,6 +119,7 @@ struct Dev {
     const uint16_t *incE;      // [S][we]
     const int32_t *nodeE;      // [N][wn]
     int we, wn;
+    int32_t zslot;             // index of the all-zero force slot (ELL padding)
     const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
     const uint16_t *tconn;
     const uint16_t *lconn, *ledge;

@@ -58,7 +58,7 @@ __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, 
 }
 
 // warp-tiled geometry: tet e -> tile e>>5, lane e&31, component c at [tile][c][lane]
-__device__ __forceinline__ const double *geo_ptr(const Dev &d, int64_t e) { return d.geoT + (e >> 5) * 352 + (e & 31); }
+__device__ __forceinline__ const double *geo_ptr(const Dev &d, uint32_t e) { return d.geoT + ((e >> 5) * 352u + (e & 31u)); }
 __device__ __forceinline__ int64_t slot_tet(int32_t slot) { return ((int64_t)(slot >> 7) << 5) + (slot & 31); }
 
 // lumped mass of node k from its active incidences in original order
@@ -67,7 +67,7 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
     const int32_t *row = d.nodeE + k * d.wn;
     for (int j = 0; j < d.wn; ++j) {
         const int32_t sl = __ldg(row + j);
-        if (sl < 0) break;
+        if (sl == d.zslot) break;
         const int64_t e = slot_tet(sl);
         if (!d.state[e]) continue;
         acc = acc + (d.rho * __ldg(geo_ptr(d, e))) / 4.0;
@@ -142,7 +142,7 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const int nt = __ldg(d.tl_off + b + 1) - t0;
     const int32_t n0 = __ldg(d.nlb_off + b);
     const int nn = __ldg(d.nlb_off + b + 1) - n0;
-    const int un = pstride(nn), tn = pstride(nt);
+    const int un = pstride(nn), tn = pstride(nt + 1);  // row nt: all-zero sentinel
     double *U = sm, *T = sm + 3 * un;
     for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
         const double4 w = ld256(u + __ldg(d.nlb + n0 + i));
@@ -151,10 +151,13 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
         U[2 * un + i] = w.z;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-        const int64_t e = __ldg(d.tl + t0 + i);
-        if (!d.state[e]) {
-            T[6 * tn + i] = 0.0;
+    for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
+        const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
+        if (i == nt || !d.state[e]) {
+            // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so
+            // adding +0.0 is bit-identical to skipping the entry.
+#pragma unroll
+            for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
             continue;
         }
         const double *gp = geo_ptr(d, e);
@@ -192,17 +195,15 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const int64_t s = (int64_t)b * d.blk + threadIdx.x;
     if (s >= d.S) return;
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + s * d.we);
+    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
     for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
         const uint4 q = __ldg(row + (w >> 3));
         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-            const int r = (qq[t >> 1] >> (16 * (t & 1))) & 0xffff;
-            if (r == 0xffff) continue;
-            const double Ve = T[6 * tn + r];
-            if (Ve == 0.0) continue;  // inactive tet
-            Vh = Vh + Ve;
+            // padding (0xffff) -> the all-zero sentinel row nt; inactive tets hold zeros
+            const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
+            Vh = Vh + T[6 * tn + r];
             T0 = T0 + T[r];
             T1 = T1 + T[tn + r];
             T2 = T2 + T[2 * tn + r];
@@ -211,7 +212,7 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
             T5 = T5 + T[5 * tn + r];
         }
     }
-    double4 *o = reinterpret_cast<double4 *>(d.srec + 8 * s);
+    double4 *o = reinterpret_cast<double4 *>(d.srec + 8u * (uint32_t)s);
     if (Vh == 0.0) {
         st256(o, 0.0, 0.0, 0.0, 0.0);
         st256(o + 1, 0.0, 0.0, 0.0, 0.0);
@@ -449,7 +450,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int np = pstride(ne), nq = pstride(nn);
     double *smu = sm + 7 * np;
     for (int i = threadIdx.x; i < ne; i += blockDim.x) {  // one sigma record per thread
-        const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8 * (int64_t)__ldg(d.el + s0i + i));
+        const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8u * (uint32_t)__ldg(d.el + s0i + i));
         const double4 x = ld256(r), y = ld256(r + 1);
         sm[i] = x.x;
         sm[np + i] = x.y;
@@ -469,7 +470,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     __syncthreads();
     const int64_t e = (int64_t)b * d.blk + threadIdx.x;
     if (e >= d.E) return;
-    double4 *fo = d.fe + (e >> 5) * 128 + (e & 31);  // slot (e,a) = fo + 32 a
+    double4 *fo = d.fe + (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));  // slot (e,a) = fo + 32 a
     if (!d.state[e]) {
 #pragma unroll
         for (int a = 0; a < 4; ++a) st256(fo + 32 * a, 0.0, 0.0, 0.0, 0.0);
@@ -536,23 +537,22 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p, double4 *u2p, int64_t s) {
     const int64_t k = (int64_t)b * d.blk + threadIdx.x;
     if (k >= d.N) return;
-    const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + k * d.wn);
+    const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     for (int w = 0; w < d.wn; w += 8) {
+        // padding entries point at an all-zero slot: adding +0.0 is an exact no-op here
         const int4 qa = __ldg(row + (w >> 2)), qb = __ldg(row + (w >> 2) + 1);
         const int32_t sl[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
         double4 f[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-            if (sl[t] >= 0) f[t] = ld256(d.fe + sl[t]);
+        for (int t = 0; t < 8; ++t) f[t] = ld256(d.fe + (uint32_t)sl[t]);
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-            if (sl[t] >= 0) {
-                f0 = f0 + f[t].x;
-                f1 = f1 + f[t].y;
-                f2 = f2 + f[t].z;
-            }
-        if (sl[7] < 0) break;
+        for (int t = 0; t < 8; ++t) {
+            f0 = f0 + f[t].x;
+            f1 = f1 + f[t].y;
+            f2 = f2 + f[t].z;
+        }
+        if (sl[7] == d.zslot) break;
     }
     double mk = d.mass[k];
     const uint8_t fl = __ldg(&d.nflag[k]);

@@ -255,7 +255,8 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
         mx = 1;
         for (int64_t k = 0; k < N; ++k) mx = std::max(mx, p.node_off[k + 1] - p.node_off[k]);
         p.wn = (mx + 7) / 8 * 8;
-        p.nodeE.assign((size_t)N * p.wn, -1);
+        p.zslot = (int32_t)(((E + 31) / 32) * 128);  // first slot past the last tile: kept zero
+        p.nodeE.assign((size_t)N * p.wn, p.zslot);
         for (int64_t k = 0; k < N; ++k)
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) {
                 const int64_t e = p.node_ent[j] >> 2, a = p.node_ent[j] & 3;
