@@ -78,53 +78,7 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
 // Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
 // (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
 // every later per-thread gather hits shared memory instead of an L1 line of its own.
-// Loads are issued in batches of kIlp independent index->value pairs so that every thread
-// keeps several L2 round trips in flight (the staging loop is otherwise latency-serialised).
 constexpr int kIlp = 8;
-__device__ __forceinline__ void stage_nodes(const Dev &d, const double4 *u, int32_t n0, int nn, double *pl) {
-    const int tot = 3 * nn;
-    for (int base = threadIdx.x; base < tot; base += kIlp * blockDim.x) {
-        int32_t id[kIlp];
-        double v[kIlp];
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-            const int i = base + t * blockDim.x;
-            id[t] = i < tot ? __ldg(d.nl + n0 + i / 3) : 0;
-        }
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-            const int i = base + t * blockDim.x;
-            v[t] = i < tot ? reinterpret_cast<const double *>(u + id[t])[i - 3 * (i / 3)] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-            const int i = base + t * blockDim.x;
-            if (i < tot) pl[(i - 3 * (i / 3)) * (nn | 1) + i / 3] = v[t];
-        }
-    }
-}
-__device__ __forceinline__ void stage_records(const double *src, const int32_t *ids, int n, int ncomp, double *pl) {
-    const int tot = 8 * n;
-    for (int base = threadIdx.x; base < tot; base += kIlp * blockDim.x) {
-        int32_t id[kIlp];
-        double v[kIlp];
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-            const int i = base + t * blockDim.x;
-            id[t] = i < tot ? __ldg(ids + (i >> 3)) : 0;
-        }
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-            const int i = base + t * blockDim.x;
-            v[t] = (i < tot && (i & 7) < ncomp) ? src[8 * (int64_t)id[t] + (i & 7)] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-            const int i = base + t * blockDim.x;
-            if (i < tot && (i & 7) < ncomp) pl[(i & 7) * (n | 1) + (i >> 3)] = v[t];
-        }
-    }
-}
 
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
@@ -132,127 +86,72 @@ __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 // ------------------------------------------------------------------ stage AB: strain + edge stress
 // For the edge block's deduplicated tet list: eps = sum_a B_a u_a (a = 0..3 in order), Voigt
 // (11,22,33,12,23,13) with engineering shears, gradN0 = -((gradN1 + gradN2) + gradN3),
-// tau = V eps -> shared-memory planes (zeros for inactive tets).
-// Then per edge: Vhat = sum V_e, T = sum tau_e over the incident tets in original-id order,
-// eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj + eps_kk),
-// sigma_ij = mu gamma_ij, plus the Gershgorin bound g = max_i sum_j
-// |sigma_ij| used by the early-out of stage C.
-// Latency structure: every global load of the block is issued in two dependent waves (list
-// indices, then the gathered data) before the first barrier.
-constexpr int kMT = 2;  // tet-list entries per thread held in registers (more -> tail loop)
-
-__device__ __forceinline__ void tau_to_smem(const double g1[9], double V, ushort4 lc, const double *U, int un,
-                                            double *T, int tn, int i) {
-    double g[4][3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        g[1][c] = g1[c];
-        g[2][c] = g1[3 + c];
-        g[3][c] = g1[6 + c];
-        g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-    }
-    const int li[4] = {lc.x, lc.y, lc.z, lc.w};
-    double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double ux = U[li[a]], uy = U[un + li[a]], uz = U[2 * un + li[a]];
-        const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
-        ex = ex + gx * ux;
-        ey = ey + gy * uy;
-        ez = ez + gz * uz;
-        gxy = gxy + (gy * ux + gx * uy);
-        gyz = gyz + (gz * uy + gy * uz);
-        gxz = gxz + (gz * ux + gx * uz);
-    }
-    T[i] = V * ex;
-    T[tn + i] = V * ey;
-    T[2 * tn + i] = V * ez;
-    T[3 * tn + i] = V * gxy;
-    T[4 * tn + i] = V * gyz;
-    T[5 * tn + i] = V * gxz;
-    T[6 * tn + i] = V;
-}
-
-__device__ __forceinline__ void zero_row(double *T, int tn, int i) {
-    // inactive tet / sentinel: exact zeros.  Running sums here never hold -0.0, so adding
-    // +0.0 is bit-identical to skipping the entry.
-#pragma unroll
-    for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
-}
-
+// tau = V eps -> shared-memory planes (V = 0 marks an inactive tet).
+// Then per edge: Vhat = sum V_e, T = sum tau_e over the active incident tets in original-id
+// order, eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj +
+// eps_kk), sigma_ij = mu gamma_ij, plus the Gershgorin bound
+// g = max_i sum_j |sigma_ij| used by the early-out of stage C.
 __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm) {
-    const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
     const int32_t n0 = __ldg(d.nlb_off + b);
     const int nn = __ldg(d.nlb_off + b + 1) - n0;
     const int un = pstride(nn), tn = pstride(nt + 1);  // row nt: all-zero sentinel
     double *U = sm, *T = sm + 3 * un;
-    const int64_t s = (int64_t)b * d.blk + tid;
-    // ---- wave 1: indices (and the ELL row of this thread's edge)
-    uint4 ell[2] = {make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu),
-                    make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu)};
-    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
-    if (s < d.S) {
-        ell[0] = __ldg(row);
-        if (d.we > 8) ell[1] = __ldg(row + 1);
-    }
-    int32_t nid0 = tid < nn ? __ldg(d.nlb + n0 + tid) : 0;
-    uint32_t et[kMT];
-#pragma unroll
-    for (int m = 0; m < kMT; ++m) et[m] = tid + m * nthr < nt ? (uint32_t)__ldg(d.tl + t0 + tid + m * nthr) : 0u;
-    // ---- wave 2: gathered data
-    double4 u0 = tid < nn ? ld256(u + nid0) : make_double4(0, 0, 0, 0);
-    bool act[kMT];
-    double gv[kMT][9], Vv[kMT];
-    ushort4 lcv[kMT];
-#pragma unroll
-    for (int m = 0; m < kMT; ++m) {
-        const int i = tid + m * nthr;
-        act[m] = i < nt && d.state[et[m]];
-        if (act[m]) {
-            const double *gp = geo_ptr(d, et[m]);
-            Vv[m] = __ldg(gp);
-#pragma unroll
-            for (int c = 0; c < 9; ++c) gv[m][c] = __ldg(gp + 32 * (2 + c));
-            lcv[m] = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
-        }
-    }
-    if (tid < nn) {
-        U[tid] = u0.x;
-        U[un + tid] = u0.y;
-        U[2 * un + tid] = u0.z;
-    }
-    for (int i = tid + nthr; i < nn; i += nthr) {  // tail: node lists longer than the block
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
         const double4 w = ld256(u + __ldg(d.nlb + n0 + i));
         U[i] = w.x;
         U[un + i] = w.y;
         U[2 * un + i] = w.z;
     }
     __syncthreads();
-#pragma unroll
-    for (int m = 0; m < kMT; ++m) {
-        const int i = tid + m * nthr;
-        if (act[m]) tau_to_smem(gv[m], Vv[m], lcv[m], U, un, T, tn, i);
-        else if (i <= nt) zero_row(T, tn, i);
-    }
-    for (int i = tid + kMT * nthr; i <= nt; i += nthr) {  // tail: tet lists longer than kMT * block
+    for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
         const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
         if (i == nt || !d.state[e]) {
-            zero_row(T, tn, i);
+            // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so
+            // adding +0.0 is bit-identical to skipping the entry.
+#pragma unroll
+            for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
             continue;
         }
         const double *gp = geo_ptr(d, e);
-        double g1[9];
+        double g[4][3];
 #pragma unroll
-        for (int c = 0; c < 9; ++c) g1[c] = __ldg(gp + 32 * (2 + c));
-        tau_to_smem(g1, __ldg(gp), __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i), U, un, T, tn, i);
+        for (int a = 1; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+        const double V = __ldg(gp);
+        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
+        const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+        double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const double ux = U[li[a]], uy = U[un + li[a]], uz = U[2 * un + li[a]];
+            const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
+            ex = ex + gx * ux;
+            ey = ey + gy * uy;
+            ez = ez + gz * uz;
+            gxy = gxy + (gy * ux + gx * uy);
+            gyz = gyz + (gz * uy + gy * uz);
+            gxz = gxz + (gz * ux + gx * uz);
+        }
+        T[i] = V * ex;
+        T[tn + i] = V * ey;
+        T[2 * tn + i] = V * ez;
+        T[3 * tn + i] = V * gxy;
+        T[4 * tn + i] = V * gyz;
+        T[5 * tn + i] = V * gxz;
+        T[6 * tn + i] = V;
     }
     __syncthreads();
+    const int64_t s = (int64_t)b * d.blk + threadIdx.x;
     if (s >= d.S) return;
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
+    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
     for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
-        const uint4 q = w < 16 ? ell[w >> 3] : __ldg(row + (w >> 3));
+        const uint4 q = __ldg(row + (w >> 3));
         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
