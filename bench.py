@@ -183,9 +183,19 @@ def main():
     torch.cuda.set_device(dev)
     import paper_2508_04076_b200 as cem
 
-    prob = make_problem(args.config)
-    sim = cem.Simulation.from_problem(prob, device=local)
-    N, E, S = sim.n_nodes, sim.n_tets, sim.n_edges
+    if ws > 1:
+        # weak scaling (BASELINE.json configs[3]): global grid (100 P) x 100 x 17, RCB slabs,
+        # one rank per GPU, NCCL halo exchange inside every step
+        import cem_inputs as ci
+        import paper_2508_04076_b200.dist as cdist
+        prob = ci.config(3, P=ws) if args.config == 3 else make_problem(args.config)
+        sim = cdist.DistSimulation(prob, device=local)
+        E = sim.n_tets_owned
+        N, S = sim.sim.n_nodes, sim.sim.n_edges
+    else:
+        prob = make_problem(args.config)
+        sim = cem.Simulation.from_problem(prob, device=local)
+        N, E, S = sim.n_nodes, sim.n_tets, sim.n_edges
     stream = sim.torch_stream
     crack_every = 1
 
@@ -211,7 +221,7 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = sim.launch_count - l0
-    st = sim.state(records=False)
+    st = sim.state(records=False) if ws == 1 else sim.sim.state(records=False)
     if dist:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -222,12 +232,14 @@ def main():
     else:
         E_all = float(E)
     # per-kernel durations on the launching stream (eager launches bracketed by CUDA events)
-    sim.set_profiling(True)
-    kp0 = time.time()
-    sim.step(args.steps, crack_every)
-    kt = sim.kernel_times()
-    kp1 = time.time()
-    sim.set_profiling(False)
+    kt = {}
+    kp0 = kp1 = time.time()
+    if ws == 1:
+        sim.set_profiling(True)
+        sim.step(args.steps, crack_every)
+        kt = sim.kernel_times()
+        kp1 = time.time()
+        sim.set_profiling(False)
     sampler.stop()
     clocks = sampler.summary(th0 - 0.05, max(th1, kp1) + 0.05)
 
@@ -254,7 +266,9 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn lattice, cem_inputs)",
         "config": {"workload": f"cfg{args.config}: {prob.name} {E} tets/{N} nodes/{S} edges per GPU, "
                                f"crack check + split pass every step",
-                   "tets_per_gpu": E, "parallelism": f"dp{ws}" if ws > 1 else "1 GPU",
+                   "tets_per_gpu": E,
+                   "parallelism": f"{ws} GPUs: RCB slabs + 2-ring ghost layer, NCCL halo exchange per step"
+                   if ws > 1 else "1 GPU",
                    "l2": "per-step working set > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "k_persistent (one launch runs all K steps)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -263,11 +277,12 @@ def main():
         "kernels": kernels,
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "n_active_end": int(st.n_active), "splits_total": int(st.rec_elem.size if st.rec_elem is not None else 0),
+        "n_active_end": int(st.n_active),
     }
-    line["splits_total"] = int(sim.state().rec_elem.size)
+    if ws == 1:
+        line["splits_total"] = int(sim.state().rec_elem.size)
 
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e and rank == 0 and ws == 1:
         # end to end through the public API: host mesh -> cem_init_mesh (H2D) -> K steps -> state (D2H)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()

@@ -98,6 +98,7 @@ typedef struct {
 #define CEM_F_STAGED 0x2u       /* one kernel per stage (the default; kept for explicitness) */
 #define CEM_F_NO_DISCARD 0x4u   /* persistent kernel: keep consumed intermediates in L2 (no discard) */
 #define CEM_F_PERSISTENT 0x8u   /* one persistent wavefront kernel per cem_step call */
+#define CEM_F_LOOPBACK 0x10u    /* nranks > 1 emulated in one process (cem_step_group, device copies) */
 
 typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
 
@@ -113,8 +114,25 @@ typedef struct {
     cem_alloc_fn dev_alloc; /* optional device allocator used when workspace == NULL */
     void *alloc_user;
     int rank, nranks;    /* multi-GPU: rank in [0, nranks); nranks <= 1 -> single GPU */
-    void *nccl_comm;     /* ncclComm_t when nranks > 1 */
+    const void *nccl_id; /* nranks > 1 without CEM_F_LOOPBACK: the 128-byte ncclUniqueId that rank 0
+                            obtained from cem_nccl_unique_id and broadcast to all ranks */
 } cem_opts;
+
+/* Domain decomposition of a rank; library-owned arrays,
+ * released by cem_partition_free.  Local tets/nodes are in ascending global id. */
+typedef struct {
+    int64_t n_tets, n_nodes;
+    int32_t *tet_global;      /* [n_tets] global tet id of each local tet */
+    uint8_t *tet_flag;        /* [n_tets] bit0: layer 1 (criterion evaluated here), bit1: owned (recorded here) */
+    int32_t *node_global;     /* [n_nodes] */
+    uint8_t *node_owned;      /* [n_nodes] 1 if this rank updates the node */
+    int32_t n_peers;
+    int32_t *peers;           /* [n_peers] */
+    int64_t *send_node_off, *recv_node_off, *send_tet_off, *recv_tet_off; /* [n_peers + 1] CSR */
+    int32_t *send_nodes, *recv_nodes, *send_tets, *recv_tets;             /* local ids */
+    int32_t *tet_owner;       /* [global n_tets] owning rank of every tet */
+    int32_t *node_owner;      /* [global n_nodes] */
+} cem_part_out;
 
 /* State snapshot.  For CEM_HOST every non-NULL array pointer must point to caller-owned
  * host memory of the stated size and is filled; for CEM_DEVICE the pointers are set to
@@ -164,6 +182,23 @@ CEM_API cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out);
 
 /* Synchronise and fill *out (see cem_state_out). Returns CEM_ENONFINITE if flagged. */
 CEM_API cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where);
+
+/* Host-only: the partition plan rank `rank` of `nranks` uses (no device work). */
+CEM_API cem_status cem_partition(const cem_mesh_in *mesh, int nranks, int rank, cem_part_out *out);
+CEM_API void cem_partition_free(cem_part_out *out);
+
+/* Multi-GPU: 128-byte NCCL unique id for rank 0 to broadcast (opts.nccl_id).  NCCL is loaded at
+ * run time (libnccl.so.2, the one torch uses); CEM_ENCCL if unavailable. */
+CEM_API cem_status cem_nccl_unique_id(void *id128);
+
+/* Loopback multi-rank emulation on one device: step n contexts created with nranks = n,
+ * rank = i and CEM_F_LOOPBACK; the halo exchange runs as device copies in rank order. */
+CEM_API cem_status cem_step_group(cem_ctx **ctxs, int32_t n, int64_t nsteps, int32_t crack_every);
+
+/* Order records by (step, element) and sum U_d = sum Gc_e * area_e in that order (merging
+ * the records of several ranks).  gc is indexed by element id; outputs the permutation. */
+CEM_API cem_status cem_merge_records(int64_t n, const int64_t *step, const int32_t *elem, const double *area,
+                                     const double *gc, int64_t *order_out, double *dissipated_out);
 
 /* Mesh sizes after init. */
 CEM_API cem_status cem_sizes(const cem_ctx *ctx, int64_t *n_nodes, int64_t *n_tets, int64_t *n_edges);

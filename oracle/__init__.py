@@ -67,6 +67,7 @@ def lib():
         L.orc_get_geometry.argtypes = [C.c_void_p, D, D]
         L.orc_get_edges.argtypes = [C.c_void_p, I32, I64]
         L.orc_set_state.argtypes = [C.c_void_p, D, D, D]
+        L.orc_set_active.argtypes = [C.c_void_p, U8]
         L.orc_edge_stress.argtypes = [C.c_void_p, D, D, D]
         L.orc_internal_force.argtypes = [C.c_void_p, D, D]
         L.orc_strain_energy.argtypes = [C.c_void_p, D]; L.orc_strain_energy.restype = C.c_double
@@ -161,6 +162,10 @@ class Oracle:
         v = None if v is None else _c(v, np.float64)
         a = None if a is None else _c(a, np.float64)
         lib().orc_set_state(self.h, _p(u, D), _p(v, D), _p(a, D))
+
+    def set_active(self, state):
+        st = _c(state, np.uint8)
+        lib().orc_set_active(self.h, _p(st, U8))
 
     def records(self):
         n = lib().orc_n_records(self.h)

@@ -760,6 +760,11 @@ ORC_API void orc_set_state(orc_sim *s, const double *u, const double *v, const d
     if (a) memcpy(s->a, a, sizeof(double) * 3 * s->N);
 }
 
+/* overwrite the active flags (tests: halo exchange of the multi-rank decomposition) */
+ORC_API void orc_set_active(orc_sim *s, const uint8_t *state) {
+    for (int64_t e = 0; e < s->E; ++e) s->active[e] = state[e] != 0;
+}
+
 ORC_API void orc_edge_stress(orc_sim *s, const double *u, double *sigma, double *vhat) {
     stage_strain(s, u); stage_edge(s);
     if (sigma) memcpy(sigma, s->sig, sizeof(double) * 6 * s->S);

@@ -35,6 +35,7 @@ CEM_F_NO_EARLY_OUT = 0x1
 CEM_F_STAGED = 0x2
 CEM_F_NO_DISCARD = 0x4
 CEM_F_PERSISTENT = 0x8
+CEM_F_LOOPBACK = 0x10
 CEM_HOST, CEM_DEVICE = 0, 1
 
 D = C.POINTER(C.c_double)
@@ -64,7 +65,7 @@ class cem_opts(C.Structure):
     _fields_ = [("dt", C.c_double), ("cfl", C.c_double), ("gamma", C.c_double), ("flags", C.c_uint32),
                 ("device", C.c_int), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("dev_alloc", ALLOC_FN), ("alloc_user", C.c_void_p),
-                ("rank", C.c_int), ("nranks", C.c_int), ("nccl_comm", C.c_void_p)]
+                ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p)]
 
 
 class cem_state_out(C.Structure):
@@ -95,9 +96,28 @@ for _f in ("cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update"
            "cem_sizes", "cem_set_profiling", "cem_kernel_times"):
     getattr(_lib, _f).restype = C.c_int
 
+class cem_part_out(C.Structure):
+    _fields_ = [("n_tets", C.c_int64), ("n_nodes", C.c_int64), ("tet_global", I32), ("tet_flag", U8),
+                ("node_global", I32), ("node_owned", U8), ("n_peers", C.c_int32), ("peers", I32),
+                ("send_node_off", I64), ("recv_node_off", I64), ("send_tet_off", I64), ("recv_tet_off", I64),
+                ("send_nodes", I32), ("recv_nodes", I32), ("send_tets", I32), ("recv_tets", I32),
+                ("tet_owner", I32), ("node_owner", I32)]
+
+
+_lib.cem_partition.argtypes = [_P(cem_mesh_in), C.c_int, C.c_int, _P(cem_part_out)]
+_lib.cem_partition.restype = C.c_int
+_lib.cem_partition_free.argtypes = [_P(cem_part_out)]
+_lib.cem_nccl_unique_id.argtypes = [C.c_void_p]
+_lib.cem_nccl_unique_id.restype = C.c_int
+_lib.cem_step_group.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_int64, C.c_int32]
+_lib.cem_step_group.restype = C.c_int
+_lib.cem_merge_records.argtypes = [C.c_int64, I64, I32, D, D, I64, D]
+_lib.cem_merge_records.restype = C.c_int
+
 EXPORTED = ["cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state",
             "cem_sizes", "cem_launch_count", "cem_set_profiling", "cem_kernel_times",
-            "cem_last_error", "cem_destroy", "cem_abi_version"]
+            "cem_last_error", "cem_destroy", "cem_abi_version", "cem_partition", "cem_partition_free",
+            "cem_nccl_unique_id", "cem_step_group", "cem_merge_records"]
 
 
 class CemError(RuntimeError):
@@ -143,7 +163,8 @@ class Simulation:
 
     def __init__(self, X, tets, E, nu, rho, Gc=np.inf, tet_state=None, tet_gc=None,
                  tface=None, tface_t=None, vbc_node=None, vbc_mask=None, vbc_v0=None, vbc_t0=0.0,
-                 dt=0.0, cfl=0.5, gamma=0.5, flags=0, device=0, stream=None, use_torch=True):
+                 dt=0.0, cfl=0.5, gamma=0.5, flags=0, device=0, stream=None, use_torch=True,
+                 rank=0, nranks=1, nccl_id=None):
         self._h = C.c_void_p()
         keep = []
         Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, 4))
@@ -186,8 +207,11 @@ class Simulation:
         else:
             self.torch_stream = None
             stream_ptr = stream
+        self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         opts = cem_opts(dt, cfl, gamma, flags, device, stream_ptr, None, 0,
-                        self._alloc_cb if self._alloc_cb is not None else ALLOC_FN(), None, 0, 1, None)
+                        self._alloc_cb if self._alloc_cb is not None else ALLOC_FN(), None, rank, nranks,
+                        None if self._nccl_id is None else C.cast(self._nccl_id, C.c_void_p))
+        self.rank, self.nranks = rank, nranks
         rc = _lib.cem_init_mesh(C.byref(mesh), C.byref(mat), C.byref(load), C.byref(opts), C.byref(self._h))
         if rc != CEM_OK:
             raise CemError(rc, _lib.cem_last_error(None).decode())

@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcem.so")
-SOURCES = ["cem_mesh.cpp", "cem_plan.cpp", "cem_kernels.cu", "cem_api.cu"]
-HEADERS = ["cem_internal.h", os.path.join("..", "..", "include", "cem.h")]
+SOURCES = ["cem_mesh.cpp", "cem_plan.cpp", "cem_part.cpp", "cem_kernels.cu", "cem_dist.cu", "cem_api.cu"]
+HEADERS = ["cem_internal.h", "cem_part.h", "cem_dist.h", os.path.join("..", "..", "include", "cem.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = out + ".tmp"
-    subprocess.check_call([NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *objs, "-lgomp"])
+    subprocess.check_call([NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *objs, "-lgomp", "-ldl"])
     os.replace(tmp, out)
     for o in objs:
         os.remove(o)

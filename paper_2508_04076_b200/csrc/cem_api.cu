@@ -8,7 +8,9 @@
 #include <string>
 #include <vector>
 
+#include "cem_dist.h"
 #include "cem_internal.h"
+#include "cem_part.h"
 
 using namespace cem;
 
@@ -31,6 +33,14 @@ struct cem_ctx {
     std::vector<cudaEvent_t> ev;  // staged profiling: 5 events per step
     int64_t prof_steps = 0;
     std::string err;
+    // multi-GPU (nranks > 1)
+    bool dist = false, loopback = false;
+    int rank = 0, nranks = 1;
+    PartLocal part;
+    Exchange xch;
+    void *comm = nullptr;
+    bool init_exchange_pending = false;
+    std::vector<void *> dist_allocs;
 };
 
 namespace {
@@ -65,7 +75,7 @@ struct Offs {
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
-    size_t nlb_off, nlb, tconn;
+    size_t nlb_off, nlb, tconn, tflag;
     size_t total;
 };
 
@@ -121,6 +131,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.nlb_off = L.take<int32_t>((int64_t)p.nlb_off.size());
     o.nlb = L.take<int32_t>((int64_t)p.nlb.size());
     o.tconn = L.take<uint16_t>((int64_t)p.tconn.size());
+    o.tflag = L.take<uint8_t>(E);
     o.total = L.off;
     return o;
 }
@@ -182,6 +193,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.nlb_off = at<int32_t>(b, o.nlb_off);
     d.nlb = at<int32_t>(b, o.nlb);
     d.tconn = at<uint16_t>(b, o.tconn);
+    d.tflag = at<uint8_t>(b, o.tflag);
     d.ctr = at<int32_t>(b, o.ctr);
     d.rec_step = at<int64_t>(b, o.rec_step);
     d.rec_elem = at<int32_t>(b, o.rec_elem);
@@ -300,6 +312,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.nlb_off, p.nlb_off.data(), sizeof(int32_t) * p.nlb_off.size()));
     CUDA_TRY(put(o.nlb, p.nlb.data(), sizeof(int32_t) * p.nlb.size()));
     CUDA_TRY(put(o.tconn, p.tconn.data(), sizeof(uint16_t) * p.tconn.size()));
+    CUDA_TRY(put(o.tflag, p.tflag.data(), E));
     CUDA_TRY(put(o.self, &ctx->d, sizeof(Dev)));
     CUDA_TRY(cudaStreamSynchronize(st));
     return CEM_OK;
@@ -308,6 +321,187 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
 __global__ void k_fill(int32_t *p, int64_t n, int32_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
+}
+
+
+// ---------------------------------------------------------------- multi-GPU helpers
+struct LocalMesh {
+    std::vector<double> X, tface_t, vbc_v0;
+    std::vector<int32_t> tets, tface, vbc_node;
+    std::vector<uint8_t> state, vbc_mask;
+    std::vector<double> gc;
+};
+
+// the rank's sub-mesh in local numbering (ascending global id, so sums keep the global order)
+void extract_local(const cem_mesh_in *m, const cem_material *mat, const cem_load_in *ld, const PartLocal &L,
+                   LocalMesh &lm) {
+    const int64_t El = L.tet_global.size(), Nl = L.node_global.size();
+    std::vector<int32_t> g2l(m->n_nodes, -1);
+    for (int64_t i = 0; i < Nl; ++i) g2l[L.node_global[i]] = (int32_t)i;
+    lm.X.resize(3 * Nl);
+    for (int64_t i = 0; i < Nl; ++i)
+        for (int c = 0; c < 3; ++c) lm.X[3 * i + c] = m->X[3 * (int64_t)L.node_global[i] + c];
+    lm.tets.resize(4 * El);
+    lm.state.resize(El);
+    lm.gc.resize(El);
+    for (int64_t i = 0; i < El; ++i) {
+        const int64_t e = L.tet_global[i];
+        for (int a = 0; a < 4; ++a) lm.tets[4 * i + a] = g2l[m->tets[4 * e + a]];
+        lm.state[i] = m->tet_state ? m->tet_state[e] : 1;
+        lm.gc[i] = m->tet_gc ? m->tet_gc[e] : mat->Gc;
+    }
+    if (ld)
+        for (int64_t f = 0; f < ld->n_tfaces; ++f) {
+            const int32_t *t = ld->tface + 3 * f;
+            if (g2l[t[0]] < 0 || g2l[t[1]] < 0 || g2l[t[2]] < 0) continue;
+            for (int i = 0; i < 3; ++i) {
+                lm.tface.push_back(g2l[t[i]]);
+                lm.tface_t.push_back(ld->tface_t[3 * f + i]);
+            }
+        }
+    if (ld)
+        for (int64_t b = 0; b < ld->n_vbc; ++b) {
+            if (g2l[ld->vbc_node[b]] < 0) continue;
+            lm.vbc_node.push_back(g2l[ld->vbc_node[b]]);
+            lm.vbc_mask.push_back(ld->vbc_mask[b]);
+            for (int c = 0; c < 3; ++c) lm.vbc_v0.push_back(ld->vbc_v0[3 * b + c]);
+        }
+}
+
+cem_status setup_exchange(cem_ctx *ctx) {
+    const PartLocal &L = ctx->part;
+    const Plan &p = ctx->p;
+    Exchange &x = ctx->xch;
+    x.peers = L.peers;
+    const size_t np = L.peers.size();
+    x.send_off.assign(np + 1, 0);
+    x.recv_off.assign(np + 1, 0);
+    std::vector<int32_t> sn, st, rn, rt;
+    std::vector<int64_t> sndst, stdst, rnsrc, rtsrc;
+    auto pad8 = [](size_t v) { return (v + 7) & ~size_t(7); };
+    for (size_t j = 0; j < np; ++j) {
+        size_t off = x.send_off[j];
+        for (int32_t k : L.send_nodes[j]) {
+            sn.push_back(p.node_old2new[k]);
+            sndst.push_back((int64_t)off);
+            off += 24;
+        }
+        for (int32_t e : L.send_tets[j]) {
+            st.push_back(p.tet_old2new[e]);
+            stdst.push_back((int64_t)off);
+            off += 1;
+        }
+        x.send_off[j + 1] = pad8(off);
+        off = x.recv_off[j];
+        for (int32_t k : L.recv_nodes[j]) {
+            rn.push_back(p.node_old2new[k]);
+            rnsrc.push_back((int64_t)off);
+            off += 24;
+        }
+        for (int32_t e : L.recv_tets[j]) {
+            rt.push_back(p.tet_old2new[e]);
+            rtsrc.push_back((int64_t)off);
+            off += 1;
+        }
+        x.recv_off[j + 1] = pad8(off);
+    }
+    x.n_send_nodes = sn.size();
+    x.n_send_tets = st.size();
+    x.n_recv_nodes = rn.size();
+    x.n_recv_tets = rt.size();
+    auto dev = [&](const void *src, size_t bytes, void **dst) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, bytes ? bytes : 8);
+        if (e != cudaSuccess) return e;
+        ctx->dist_allocs.push_back(*dst);
+        if (bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+        return e;
+    };
+    CUDA_TRY(dev(sn.data(), 4 * sn.size(), (void **)&x.d_send_nodes));
+    CUDA_TRY(dev(st.data(), 4 * st.size(), (void **)&x.d_send_tets));
+    CUDA_TRY(dev(rn.data(), 4 * rn.size(), (void **)&x.d_recv_nodes));
+    CUDA_TRY(dev(rt.data(), 4 * rt.size(), (void **)&x.d_recv_tets));
+    CUDA_TRY(dev(sndst.data(), 8 * sndst.size(), (void **)&x.d_send_ndst));
+    CUDA_TRY(dev(stdst.data(), 8 * stdst.size(), (void **)&x.d_send_tdst));
+    CUDA_TRY(dev(rnsrc.data(), 8 * rnsrc.size(), (void **)&x.d_recv_nsrc));
+    CUDA_TRY(dev(rtsrc.data(), 8 * rtsrc.size(), (void **)&x.d_recv_tsrc));
+    CUDA_TRY(dev(nullptr, x.send_off[np], (void **)&x.d_sendbuf));
+    CUDA_TRY(dev(nullptr, x.recv_off[np], (void **)&x.d_recvbuf));
+    return CEM_OK;
+}
+
+// exchange after a step whose predicted displacement sits in ubuf[parity]
+cem_status exchange_nccl_step(cem_ctx *ctx, int parity) {
+    exchange_pack(ctx->xch, ctx->d.ubuf[parity], ctx->d.state, ctx->stream);
+    if (!exchange_nccl(ctx->xch, ctx->comm, ctx->stream, ctx->err)) return CEM_ENCCL;
+    exchange_unpack(ctx->xch, ctx->d.ubuf[parity], ctx->d.state, ctx->stream);
+    ctx->launches += 2;
+    return CEM_OK;
+}
+
+// loopback: all ranks in this process, transport = device copies on ctxs[0]'s stream
+cem_status exchange_loopback(cem_ctx **c, int n, int parity) {
+    cudaStream_t st = c[0]->stream;
+    for (int r = 0; r < n; ++r) exchange_pack(c[r]->xch, c[r]->d.ubuf[parity], c[r]->d.state, st);
+    for (int r = 0; r < n; ++r) {
+        const Exchange &xs = c[r]->xch;
+        for (size_t j = 0; j < xs.peers.size(); ++j) {
+            const int q = xs.peers[j];
+            const Exchange &xq = c[q]->xch;
+            size_t jq = 0;
+            while (jq < xq.peers.size() && xq.peers[jq] != r) ++jq;
+            const size_t bytes = xs.send_off[j + 1] - xs.send_off[j];
+            if (jq == xq.peers.size() || bytes != xq.recv_off[jq + 1] - xq.recv_off[jq]) {
+                c[r]->err = "loopback exchange lists do not match";
+                return CEM_ESTATE;
+            }
+            if (bytes &&
+                cudaMemcpyAsync(xq.d_recvbuf + xq.recv_off[jq], xs.d_sendbuf + xs.send_off[j], bytes,
+                                cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+                c[r]->err = "loopback copy failed";
+                return CEM_ECUDA;
+            }
+        }
+    }
+    for (int r = 0; r < n; ++r) exchange_unpack(c[r]->xch, c[r]->d.ubuf[parity], c[r]->d.state, st);
+    for (int r = 0; r < n; ++r) c[r]->launches += 2;
+    return CEM_OK;
+}
+
+void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
+    auto dup32 = [](const std::vector<int32_t> &v) {
+        int32_t *p = (int32_t *)malloc(sizeof(int32_t) * (v.size() ? v.size() : 1));
+        if (!v.empty()) std::memcpy(p, v.data(), sizeof(int32_t) * v.size());
+        return p;
+    };
+    auto dup8 = [](const std::vector<uint8_t> &v) {
+        uint8_t *p = (uint8_t *)malloc(v.size() ? v.size() : 1);
+        if (!v.empty()) std::memcpy(p, v.data(), v.size());
+        return p;
+    };
+    auto csr = [&](const std::vector<std::vector<int32_t>> &lists, int64_t **off, int32_t **flat) {
+        std::vector<int32_t> f;
+        *off = (int64_t *)malloc(sizeof(int64_t) * (lists.size() + 1));
+        (*off)[0] = 0;
+        for (size_t j = 0; j < lists.size(); ++j) {
+            f.insert(f.end(), lists[j].begin(), lists[j].end());
+            (*off)[j + 1] = (int64_t)f.size();
+        }
+        *flat = dup32(f);
+    };
+    o->n_tets = L.tet_global.size();
+    o->n_nodes = L.node_global.size();
+    o->tet_global = dup32(L.tet_global);
+    o->tet_flag = dup8(L.tet_flag);
+    o->node_global = dup32(L.node_global);
+    o->node_owned = dup8(L.node_owned);
+    o->n_peers = (int32_t)L.peers.size();
+    o->peers = dup32(std::vector<int32_t>(L.peers.begin(), L.peers.end()));
+    csr(L.send_nodes, &o->send_node_off, &o->send_nodes);
+    csr(L.recv_nodes, &o->recv_node_off, &o->recv_nodes);
+    csr(L.send_tets, &o->send_tet_off, &o->send_tets);
+    csr(L.recv_tets, &o->recv_tet_off, &o->recv_tets);
+    o->tet_owner = dup32(g.tet_owner);
+    o->node_owner = dup32(g.node_owner);
 }
 
 }  // namespace
@@ -348,11 +542,41 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         delete ctx;
         return s;
     };
-    cem_status st = build_host_mesh(mesh, mat, load, opts, ctx->h, ctx->err);
-    if (st) return fail(st);
+    cem_status st;
+    std::vector<uint8_t> tflag_local;
     if (opts && opts->nranks > 1) {
-        ctx->err = "cem_init_mesh: nranks > 1 needs the partitioned driver (paper_2508_04076_b200.dist)";
-        return fail(CEM_EINVAL);
+        // multi-GPU: this rank's sub-mesh with a 2-ring ghost layer
+        if (!mesh || !mesh->X || !mesh->tets || !mat || opts->rank < 0 || opts->rank >= opts->nranks) {
+            ctx->err = "cem_init_mesh: bad multi-rank arguments";
+            return fail(CEM_EINVAL);
+        }
+        ctx->dist = true;
+        ctx->loopback = (opts->flags & CEM_F_LOOPBACK) != 0;
+        ctx->rank = opts->rank;
+        ctx->nranks = opts->nranks;
+        cem_opts lo = *opts;
+        if (!(lo.dt > 0)) {  // the global time step, identical on every rank
+            st = global_cfl_dt(mesh, mat, lo.cfl > 0 ? lo.cfl : 0.5, &lo.dt, ctx->err);
+            if (st) return fail(st);
+        }
+        lo.nranks = 1;
+        PartGlobal g;
+        build_partition(mesh->n_nodes, mesh->X, mesh->n_tets, mesh->tets, opts->nranks, g);
+        build_exchange(g, opts->rank, ctx->part);
+        LocalMesh lm;
+        extract_local(mesh, mat, load, ctx->part, lm);
+        cem_mesh_in m2 = {(int64_t)ctx->part.node_global.size(), lm.X.data(), (int64_t)ctx->part.tet_global.size(),
+                          lm.tets.data(), lm.state.data(), lm.gc.data()};
+        cem_load_in l2 = {(int64_t)lm.tface.size() / 3, lm.tface.data(), lm.tface_t.data(), (int64_t)lm.vbc_node.size(),
+                          lm.vbc_node.data(), lm.vbc_mask.data(), lm.vbc_v0.data(), load ? load->vbc_t0 : 0.0};
+        st = build_host_mesh(&m2, mat, &l2, &lo, ctx->h, ctx->err);
+        if (st) return fail(st);
+        for (size_t i = 0; i < ctx->part.node_owned.size(); ++i)
+            if (!ctx->part.node_owned[i]) ctx->h.nflag[i] |= 16;  // not updated here
+        tflag_local = ctx->part.tet_flag;
+    } else {
+        st = build_host_mesh(mesh, mat, load, opts, ctx->h, ctx->err);
+        if (st) return fail(st);
     }
     ctx->device = opts ? opts->device : 0;
     ctx->flags = opts ? opts->flags : 0;
@@ -361,7 +585,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         ctx->err = "cudaSetDevice failed (no CUDA device?)";
         return fail(CEM_ECUDA);
     }
-    build_plan(ctx->h, kBlk, ctx->p);
+    build_plan(ctx->h, kBlk, ctx->p, tflag_local.empty() ? nullptr : tflag_local.data());
     const int smem = smem_bytes_for(ctx->p);
     if (smem > 227 * 1024) {
         ctx->err = "a block's gather list exceeds shared memory (" + std::to_string(smem) + " bytes)";
@@ -411,6 +635,22 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     bind_views(ctx, o);
     st = upload(ctx, o);
     if (st) return fail(st);
+    if (ctx->dist) {
+        st = setup_exchange(ctx);
+        if (st) return fail(st);
+        if (ctx->loopback) {
+            ctx->init_exchange_pending = true;  // done by the first cem_step_group
+        } else {
+            if (!opts->nccl_id) {
+                ctx->err = "cem_init_mesh: nranks > 1 needs opts.nccl_id (or CEM_F_LOOPBACK)";
+                return fail(CEM_EINVAL);
+            }
+            if (!nccl_comm_init(&ctx->comm, ctx->nranks, ctx->rank, opts->nccl_id, ctx->err)) return fail(CEM_ENCCL);
+            st = exchange_nccl_step(ctx, 1);  // owners' u_1 to the ranks holding their nodes
+            if (st) return fail(st);
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        }
+    }
     *out = ctx;
     return CEM_OK;
 }
@@ -419,6 +659,8 @@ void cem_destroy(cem_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->comm) nccl_comm_destroy(ctx->comm);
+    for (void *p : ctx->dist_allocs) cudaFree(p);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -447,6 +689,22 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (crack_every < 0) crack_every = 0;
     // default: one kernel per stage (measured faster than the persistent wavefront kernel on
     // B200 for the current stage bodies; CEM_F_PERSISTENT selects the latter)
+    if (ctx->dist) {
+        if (ctx->loopback) {
+            ctx->err = "loopback contexts are stepped with cem_step_group";
+            return CEM_ESTATE;
+        }
+        for (int64_t i = 0; i < nsteps; ++i) {
+            const int64_t sstep = ctx->step + i;
+            launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr);
+            ctx->launches += ST_COUNT;
+            cem_status st = exchange_nccl_step(ctx, (int)(sstep & 1));
+            if (st) return st;
+        }
+        CUDA_TRY(cudaGetLastError());
+        ctx->step += nsteps;
+        return CEM_OK;
+    }
     const bool staged = ctx->profiling || !(ctx->flags & CEM_F_PERSISTENT);
     if (staged) {
         // one kernel per stage; with profiling, CUDA events bracket every stage
@@ -505,6 +763,10 @@ cem_status cem_kernel_times(const cem_ctx *ctx, int32_t *n, const char **names, 
 
 cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
     if (!ctx) return CEM_EINVAL;
+    if (ctx->dist) {
+        ctx->err = "cem_crack_update: single-GPU contexts only";
+        return CEM_ESTATE;
+    }
     int32_t before = 0, after = 0;
     CUDA_TRY(cudaMemcpyAsync(&before, ctx->d.ctr, sizeof before, cudaMemcpyDeviceToHost, ctx->stream));
     launch_crack_only(ctx->d, ctx->step, ctx->stream);
@@ -546,6 +808,8 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     });
     double Ud = 0.0;
     for (int64_t i = 0; i < nrec; ++i) Ud = Ud + h.gc[re[ord[i]]] * ra[ord[i]];
+    if (ctx->dist)  // records carry GLOBAL element ids (local ids ascend with global ids: order kept)
+        for (int64_t i = 0; i < nrec; ++i) re[i] = ctx->part.tet_global[re[i]];
     std::vector<uint8_t> stt(E);
     CUDA_TRY(cudaMemcpyAsync(stt.data(), ctx->d.state, E, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -610,6 +874,80 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     out->nonfinite = ctr[1];
     out->nonfinite_node = ctr[1] ? ctr[2] : -1;
     return ctr[1] ? CEM_ENONFINITE : CEM_OK;
+}
+
+cem_status cem_partition(const cem_mesh_in *mesh, int nranks, int rank, cem_part_out *out) {
+    if (!mesh || !mesh->X || !mesh->tets || !out || nranks < 1 || rank < 0 || rank >= nranks) return CEM_EINVAL;
+    for (int64_t i = 0; i < 4 * mesh->n_tets; ++i)
+        if (mesh->tets[i] < 0 || mesh->tets[i] >= mesh->n_nodes) {
+            g_init_err = "cem_partition: node index out of range";
+            return CEM_ETOPOLOGY;
+        }
+    PartGlobal g;
+    PartLocal L;
+    build_partition(mesh->n_nodes, mesh->X, mesh->n_tets, mesh->tets, nranks, g);
+    build_exchange(g, rank, L);
+    fill_part_out(g, L, out);
+    return CEM_OK;
+}
+
+void cem_partition_free(cem_part_out *o) {
+    if (!o) return;
+    free(o->tet_global); free(o->tet_flag); free(o->node_global); free(o->node_owned); free(o->peers);
+    free(o->send_node_off); free(o->recv_node_off); free(o->send_tet_off); free(o->recv_tet_off);
+    free(o->send_nodes); free(o->recv_nodes); free(o->send_tets); free(o->recv_tets);
+    free(o->tet_owner); free(o->node_owner);
+    std::memset(o, 0, sizeof *o);
+}
+
+cem_status cem_nccl_unique_id(void *id128) {
+    if (!id128) return CEM_EINVAL;
+    return nccl_unique_id(id128, g_init_err) ? CEM_OK : CEM_ENCCL;
+}
+
+cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_every) {
+    if (!c || n < 1 || nsteps < 0) return CEM_EINVAL;
+    for (int r = 0; r < n; ++r)
+        if (!c[r] || !c[r]->dist || !c[r]->loopback || c[r]->nranks != n || c[r]->rank != r || c[r]->step != c[0]->step)
+            return CEM_EINVAL;
+    cem_ctx *ctx = c[0];
+    if (crack_every < 0) crack_every = 0;
+    for (int r = 1; r < n; ++r) {  // every rank's work goes on rank 0's stream, in rank order
+        CUDA_TRY(cudaStreamSynchronize(c[r]->stream));
+    }
+    if (c[0]->init_exchange_pending) {
+        cem_status st = exchange_loopback(c, n, 1);
+        if (st) return st;
+        for (int r = 0; r < n; ++r) c[r]->init_exchange_pending = false;
+    }
+    for (int64_t i = 0; i < nsteps; ++i) {
+        const int64_t sstep = c[0]->step + i;
+        for (int r = 0; r < n; ++r) {
+            launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr);
+            c[r]->launches += ST_COUNT;
+        }
+        cem_status st = exchange_loopback(c, n, (int)(sstep & 1));
+        if (st) return st;
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < n; ++r) c[r]->step += nsteps;
+    return CEM_OK;
+}
+
+cem_status cem_merge_records(int64_t n, const int64_t *step, const int32_t *elem, const double *area,
+                             const double *gc, int64_t *order_out, double *dissipated_out) {
+    if (n < 0 || (n > 0 && (!step || !elem || !area || !gc))) return CEM_EINVAL;
+    std::vector<int64_t> ord(n);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+        return step[x] < step[y] || (step[x] == step[y] && elem[x] < elem[y]);
+    });
+    double Ud = 0.0;
+    for (int64_t i = 0; i < n; ++i) Ud = Ud + gc[elem[ord[i]]] * area[ord[i]];
+    if (order_out) std::memcpy(order_out, ord.data(), sizeof(int64_t) * n);
+    if (dissipated_out) *dissipated_out = Ud;
+    return CEM_OK;
 }
 
 }  // extern "C"

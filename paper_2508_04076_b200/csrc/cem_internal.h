@@ -39,6 +39,7 @@ struct HostMesh {
 cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const cem_load_in *ld,
                            const cem_opts *o, HostMesh &h, std::string &err);
 cem_status count_edges(const cem_mesh_in *m, int64_t *S, std::string &err);
+cem_status global_cfl_dt(const cem_mesh_in *m, const cem_material *mat, double cfl, double *dt, std::string &err);
 
 // ---------------------------------------------------------------- storage plan
 // Storage ("new") numbering: tets sorted by (sweep-axis slab of the centroid, original id),
@@ -58,6 +59,7 @@ struct Plan {
     std::vector<int32_t> edge_off, edge_inc;   // CSR over new edges, new tet ids, original order
     std::vector<int32_t> node_off, node_ent;   // CSR over new nodes, (new e << 2 | a), original order
     std::vector<uint8_t> state;
+    std::vector<uint8_t> tflag;       // [E] bit0 evaluate the criterion, bit1 record splits (multi-GPU masks)
     std::vector<double> gc;
     // blocks and the wavefront schedule
     int blk = 256;                    // entities per work item
@@ -90,7 +92,7 @@ struct Plan {
     int32_t zslot = 0;
 };
 
-void build_plan(const HostMesh &h, int blk, Plan &p);
+void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig = nullptr);
 void build_schedule(Plan &p, int resident_ctas);
 
 // ---------------------------------------------------------------- device view
@@ -109,6 +111,7 @@ struct Dev {
     const int32_t *node_orig;  // storage -> original node id
     // mutable state
     uint8_t *state;
+    const uint8_t *tflag;      // [E] bit0 criterion here, bit1 record here (all 3 on one GPU)
     double *mass;
     int32_t *dirty;            // [N] step stamp of the last split touching the node
     double4 *ubuf[2];          // u_m lives in ubuf[m & 1]

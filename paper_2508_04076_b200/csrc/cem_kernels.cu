@@ -78,8 +78,6 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
 // Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
 // (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
 // every later per-thread gather hits shared memory instead of an L1 line of its own.
-constexpr int kIlp = 8;
-
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
@@ -368,19 +366,21 @@ __device__ __noinline__ void evaluate_tet(const Dev *__restrict__ dp, int64_t e,
 // state; later readers are next-step stages), append a record (unordered; the host sorts
 // by (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
 __device__ __noinline__ void criterion_full(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc, int64_t rec_step,
-                                            int32_t stamp) {
+                                            int32_t stamp, bool record) {
     const Dev &d = *dp;
     double G, A;
     int k;
     evaluate_tet(dp, e, u, G, k, A);
     if (G > gc) {
         d.state[e] = 0;
-        const int slot = atomicAdd(&d.ctr[0], 1);
-        d.rec_step[slot] = rec_step;
-        d.rec_elem[slot] = ldro(d.tet_orig + e);
-        d.rec_cand[slot] = k;
-        d.rec_G[slot] = G;
-        d.rec_area[slot] = A;
+        if (record) {  // multi-GPU: only the owning rank records (every holder deactivates)
+            const int slot = atomicAdd(&d.ctr[0], 1);
+            d.rec_step[slot] = rec_step;
+            d.rec_elem[slot] = ldro(d.tet_orig + e);
+            d.rec_cand[slot] = k;
+            d.rec_G[slot] = G;
+            d.rec_area[slot] = A;
+        }
         const int4 t = __ldg(&d.conn[e]);
         d.dirty[t.x] = stamp;
         d.dirty[t.y] = stamp;
@@ -498,6 +498,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         st256(fo + 32 * a, fx, fy, fz, 0.0);
     }
     if (!crack) return;
+    const uint8_t tf = __ldg(d.tflag + e);
+    if (!(tf & 1)) return;  // ghost tet: its owner decides, the state arrives by exchange
     const double gc = ldro(d.gc + e);
     if (early) {
         const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
@@ -518,7 +520,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         }
         if (gmax * sqrt(d2) * (1.0 + 1e-6) <= gc) return;
     }
-    criterion_full(d.self, e, u, gc, rec_step, stamp);
+    criterion_full(d.self, e, u, gc, rec_step, stamp, (tf & 2) != 0);
 }
 
 // ------------------------------------------------------------------ stage D: node update
@@ -527,6 +529,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p, double4 *u2p, int64_t s) {
     const int64_t k = (int64_t)b * d.blk + threadIdx.x;
     if (k >= d.N) return;
+    const uint8_t fl = __ldg(&d.nflag[k]);
+    if (fl & 16) return;  // multi-GPU: another rank owns (and updates) this node
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     for (int w = 0; w < d.wn; w += 8) {
@@ -545,7 +549,6 @@ __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p,
         if (sl[7] == d.zslot) break;
     }
     double mk = d.mass[k];
-    const uint8_t fl = __ldg(&d.nflag[k]);
     const double4 u1 = ld256(&u1p[k]);
     const double4 v = ld256(&d.v[k]), a = ld256(&d.a[k]);
     const double dt = d.dt;
@@ -770,6 +773,9 @@ int persistent_occupancy(int smem_bytes) {
 }
 
 void set_smem_limits(int smem_bytes) {
+    static int cur = 0;  // the attribute is per function: keep the largest any context needs
+    if (smem_bytes <= cur) return;
+    cur = smem_bytes;
     cudaFuncSetAttribute(k_AB, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_AB_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);

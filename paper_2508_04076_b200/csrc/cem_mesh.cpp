@@ -55,6 +55,50 @@ cem_status count_edges(const cem_mesh_in *m, int64_t *S, std::string &err) {
     return CEM_OK;
 }
 
+// dt = cfl * min_{active e} (3 V_e / max face area_e) / c_d, c_d = sqrt((lam + 2 mu)/rho)
+cem_status cfl_dt(int64_t N, const double *X, int64_t E, const int32_t *tets, const uint8_t *state, const double *V,
+                  double l2m, double rho, double cfl, double *dt_out, std::string &err) {
+    (void)N;
+    const double cd = std::sqrt(l2m / rho);
+    double altmin = INFINITY;
+    for (int64_t e = 0; e < E; ++e) {
+        if (!state[e]) continue;
+        double amax = 0.0;
+        for (int f = 0; f < 4; ++f) {
+            const int32_t *t = tets + 4 * e;
+            V3 x0 = node(X, t[kFaceNodes[f][0]]);
+            V3 cr = cross(sub(node(X, t[kFaceNodes[f][1]]), x0), sub(node(X, t[kFaceNodes[f][2]]), x0));
+            double A = 0.5 * std::sqrt(dot(cr, cr));
+            if (A > amax) amax = A;
+        }
+        double alt = 3.0 * V[e] / amax;
+        if (alt < altmin) altmin = alt;
+    }
+    if (!std::isfinite(altmin)) {
+        err = "no active tet to derive dt from";
+        return CEM_EINVAL;
+    }
+    *dt_out = (cfl * altmin) / cd;
+    return CEM_OK;
+}
+
+// the same rule on a mesh given only by arrays (global dt of a partitioned run)
+cem_status global_cfl_dt(const cem_mesh_in *m, const cem_material *mat, double cfl, double *dt, std::string &err) {
+    const int64_t E = m->n_tets;
+    std::vector<double> V(E);
+    std::vector<uint8_t> st(E);
+    for (int64_t e = 0; e < E; ++e) {
+        const int32_t *t = m->tets + 4 * e;
+        V3 x0 = node(m->X, t[0]);
+        V3 d1 = sub(node(m->X, t[1]), x0), d2 = sub(node(m->X, t[2]), x0), d3 = sub(node(m->X, t[3]), x0);
+        V[e] = dot(d1, cross(d2, d3)) / 6.0;
+        st[e] = m->tet_state ? (m->tet_state[e] != 0) : 1;
+    }
+    const double lam = mat->E * mat->nu / ((1.0 + mat->nu) * (1.0 - 2.0 * mat->nu));
+    const double mu = mat->E / (2.0 * (1.0 + mat->nu));
+    return cfl_dt(m->n_nodes, m->X, E, m->tets, st.data(), V.data(), lam + 2.0 * mu, mat->rho, cfl, dt, err);
+}
+
 cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const cem_load_in *ld,
                            const cem_opts *o, HostMesh &h, std::string &err) {
     if (!m || !mat || !m->X || !m->tets || m->n_nodes <= 0 || m->n_tets <= 0) {
@@ -270,26 +314,8 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
     // ---------------------------------------------------------------- time step (R12)
     double dt = o ? o->dt : 0.0;
     if (!(dt > 0)) {
-        const double cd = std::sqrt(h.l2m / h.rho);
-        double altmin = INFINITY;
-        for (int64_t e = 0; e < E; ++e) {
-            if (!h.state[e]) continue;
-            double amax = 0.0;
-            for (int f = 0; f < 4; ++f) {
-                const int32_t *t = m->tets + 4 * e;
-                V3 x0 = node(m->X, t[kFaceNodes[f][0]]);
-                V3 cr = cross(sub(node(m->X, t[kFaceNodes[f][1]]), x0), sub(node(m->X, t[kFaceNodes[f][2]]), x0));
-                double A = 0.5 * std::sqrt(dot(cr, cr));
-                if (A > amax) amax = A;
-            }
-            double alt = 3.0 * h.V[e] / amax;
-            if (alt < altmin) altmin = alt;
-        }
-        if (!std::isfinite(altmin)) {
-            err = "cem_init_mesh: no active tet to derive dt from";
-            return CEM_EINVAL;
-        }
-        dt = (cfl * altmin) / cd;
+        cem_status st = cfl_dt(m->n_nodes, m->X, m->n_tets, m->tets, h.state.data(), h.V.data(), h.l2m, h.rho, cfl, &dt, err);
+        if (st) return st;
     }
     h.dt = dt;
     return CEM_OK;

@@ -15,7 +15,7 @@
 
 namespace cem {
 
-void build_plan(const HostMesh &h, int blk, Plan &p) {
+void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) {
     const int64_t N = h.N, E = h.E, S = h.S;
     p.blk = blk;
     // ---------------------------------------------------------------- sweep axis + slabs
@@ -120,6 +120,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
     p.geoG.resize(9 * E);
     p.eedge.resize(6 * E);
     p.state.resize(E);
+    p.tflag.resize(E);
     p.gc.resize(E);
     for (int64_t en = 0; en < E; ++en) {
         const int64_t eo = p.tet_new2old[en];
@@ -130,6 +131,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p) {
             for (int c = 0; c < 3; ++c) p.geoG[(int64_t)(3 * (a - 1) + c) * E + en] = h.grad[12 * eo + 3 * a + c];
         for (int l = 0; l < 6; ++l) p.eedge[(int64_t)l * E + en] = edge_old2new[h.elem_edge[6 * eo + l]];
         p.state[en] = h.state[eo];
+        p.tflag[en] = tflag_orig ? tflag_orig[eo] : 3;
         p.gc[en] = h.gc[eo];
     }
     p.edge_off.assign(S + 1, 0);
