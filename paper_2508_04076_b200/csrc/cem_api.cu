@@ -413,7 +413,7 @@ cem_status setup_exchange(cem_ctx *ctx) {
         cudaError_t e = cudaMalloc(dst, bytes ? bytes : 8);
         if (e != cudaSuccess) return e;
         ctx->dist_allocs.push_back(*dst);
-        if (bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+        if (bytes && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
         return e;
     };
     CUDA_TRY(dev(sn.data(), 4 * sn.size(), (void **)&x.d_send_nodes));
