@@ -126,6 +126,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.tl_off = L.take<int32_t>((int64_t)p.tl_off.size());
     o.tl = L.take<int32_t>((int64_t)p.tl.size());
     o.self = L.take<Dev>(1);
+    L.take<char>(256);  // tail padding: bulk-copy windows are rounded up to 16 B
     o.ncons = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
     o.cons_done = L.take<int32_t>(ST_COUNT * (int64_t)p.maxblk);
     o.nlb_off = L.take<int32_t>((int64_t)p.nlb_off.size());
@@ -136,9 +137,12 @@ Offs layout(const HostMesh &h, const Plan &p) {
     return o;
 }
 
-int smem_bytes_for(const Plan &p) {  // odd plane strides, see pstride()
-    const int n = std::max(3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1), 7 * (p.max_el | 1) + 3 * (p.max_nl | 1));
-    return 8 * n;
+int smem_bytes_for(const Plan &p) {  // odd plane strides (pstride) + 16-B aligned metadata pieces
+    auto p16 = [](int b) { return (b + 15) & ~15; };
+    const int ab = 8 * (10 * ((p.max_tl + 1) | 1) + 3 * (p.max_nlb | 1)) + 16 + p16(4 * (p.max_nlb + 8)) +
+                   p16(4 * (p.max_tl + 8)) + p16(8 * (p.max_tl + 4)) + p16(2 * p.blk * p.we) + p16(p.max_tl + 8);
+    const int c = 8 * (7 * (p.max_el | 1) + 3 * (p.max_nl | 1));
+    return std::max(ab, c);
 }
 
 template <class T>

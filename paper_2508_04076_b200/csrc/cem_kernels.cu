@@ -78,50 +78,137 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
 // Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
 // (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
 // every later per-thread gather hits shared memory instead of an L1 line of its own.
+// ------------------------------------------------------------------ async staging helpers (sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared (UBLKCP), completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// LDGSTS: 8-byte asynchronous gather into shared memory (no register round trip)
+__device__ __forceinline__ void cp8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory"); }
+
+// 16-byte aligned window [a, a+bytes) covering [p, p + n elements of size sz); returns the element shift
+template <class T>
+__device__ __forceinline__ int bulk_window(const T *p, int n, const T *&a, uint32_t &bytes) {
+    const uintptr_t s = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~uintptr_t(15);
+    a = reinterpret_cast<const T *>(s);
+    bytes = (uint32_t)(e - s);
+    return (int)((reinterpret_cast<uintptr_t>(p) - s) / sizeof(T));
+}
+__host__ __device__ __forceinline__ int pad16(int bytes) { return (bytes + 15) & ~15; }
+
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
 // ------------------------------------------------------------------ stage AB: strain + edge stress
 // For the edge block's deduplicated tet list: eps = sum_a B_a u_a (a = 0..3 in order), Voigt
 // (11,22,33,12,23,13) with engineering shears, gradN0 = -((gradN1 + gradN2) + gradN3),
-// tau = V eps -> shared-memory planes (V = 0 marks an inactive tet).
-// Then per edge: Vhat = sum V_e, T = sum tau_e over the active incident tets in original-id
-// order, eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj +
-// eps_kk), sigma_ij = mu gamma_ij, plus the Gershgorin bound
-// g = max_i sum_j |sigma_ij| used by the early-out of stage C.
-__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm) {
+// tau = V eps -> shared-memory planes (zeros for inactive tets).
+// Then per edge: Vhat = sum V_e, T = sum tau_e over the incident tets in original-id order,
+// eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj + eps_kk),
+// sigma_ij = mu gamma_ij, plus the Gershgorin bound g = max_i sum_j
+// |sigma_ij| used by the early-out of stage C.
+// Data movement: one thread issues TMA bulk copies of the block's contiguous metadata (node
+// list, tet list, local connectivity, ELL rows) onto an mbarrier; then every thread gathers
+// u and the tet geometry straight into shared memory with cp.async (LDGSTS).  Two dependent
+// global waves per block, no registers held across them.
+__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm, uint64_t *bar,
+                                         uint32_t phase) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
     const int32_t n0 = __ldg(d.nlb_off + b);
     const int nn = __ldg(d.nlb_off + b + 1) - n0;
+    const int64_t s0 = (int64_t)b * d.blk;
+    const int ns = (int)min((int64_t)d.blk, d.S - s0);
     const int un = pstride(nn), tn = pstride(nt + 1);  // row nt: all-zero sentinel
-    double *U = sm, *T = sm + 3 * un;
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
-        const double4 w = ld256(u + __ldg(d.nlb + n0 + i));
-        U[i] = w.x;
-        U[un + i] = w.y;
-        U[2 * un + i] = w.z;
+    // shared-memory carve-up (16-B aligned pieces)
+    double *G = sm;                 // [10][tn]: grads 0..8, V at 9; tau/V overwrite 0..6 in place
+    double *U = G + 10 * tn;        // [3][un]
+    char *mp = reinterpret_cast<char *>(U + 3 * un);
+    mp = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(mp) + 15) & ~uintptr_t(15));
+    int32_t *nl_s = reinterpret_cast<int32_t *>(mp);
+    mp += pad16(4 * (nn + 8));
+    int32_t *tl_s = reinterpret_cast<int32_t *>(mp);
+    mp += pad16(4 * (nt + 8));
+    ushort4 *tc_s = reinterpret_cast<ushort4 *>(mp);
+    mp += pad16(8 * (nt + 4));
+    uint16_t *ell_s = reinterpret_cast<uint16_t *>(mp);
+    mp += pad16(2 * d.blk * d.we);
+    uint8_t *st_s = reinterpret_cast<uint8_t *>(mp);
+    // ---- wave 1: TMA bulk copies of the contiguous metadata
+    const int32_t *a_nl, *a_tl;
+    const ushort4 *a_tc;
+    uint32_t b_nl, b_tl, b_tc;
+    const int sh_nl = bulk_window(d.nlb + n0, nn, a_nl, b_nl);
+    const int sh_tl = bulk_window(d.tl + t0, nt, a_tl, b_tl);
+    const int sh_tc = bulk_window(reinterpret_cast<const ushort4 *>(d.tconn) + t0, nt, a_tc, b_tc);
+    const uint32_t b_ell = (uint32_t)(2 * ns * d.we);
+    if (tid == 0) {
+        // order earlier generic-proxy accesses of this shared memory before the async copies
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, b_nl + b_tl + b_tc + b_ell);
+        bulk_g2s(nl_s, a_nl, b_nl, bar);
+        bulk_g2s(tl_s, a_tl, b_tl, bar);
+        bulk_g2s(tc_s, a_tc, b_tc, bar);
+        bulk_g2s(ell_s, d.incE + s0 * d.we, b_ell, bar);
     }
+    mbar_wait(bar, phase);
+    // ---- wave 2: cp.async gathers of u and of the tet geometry (warp-tiled rows)
+    for (int i = tid; i < nn; i += nthr) {
+        const double *w = reinterpret_cast<const double *>(u + nl_s[sh_nl + i]);
+        cp8(U + i, w);
+        cp8(U + un + i, w + 1);
+        cp8(U + 2 * un + i, w + 2);
+    }
+    for (int i = tid; i < nt; i += nthr) {
+        const uint32_t e = (uint32_t)tl_s[sh_tl + i];
+        const double *gp = geo_ptr(d, e);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) cp8(G + c * tn + i, gp + 32 * (2 + c));
+        cp8(G + 9 * tn + i, gp);
+        st_s[i] = d.state[e];
+    }
+    cp_wait_all();
     __syncthreads();
-    for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
-        const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
-        if (i == nt || !d.state[e]) {
-            // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so
+    for (int i = tid; i <= nt; i += nthr) {
+        if (i == nt || !st_s[i]) {
+            // inactive tet / sentinel: exact zeros.  Running sums here never hold -0.0, so
             // adding +0.0 is bit-identical to skipping the entry.
 #pragma unroll
-            for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
+            for (int c = 0; c < 7; ++c) G[c * tn + i] = 0.0;
             continue;
         }
-        const double *gp = geo_ptr(d, e);
         double g[4][3];
 #pragma unroll
         for (int a = 1; a < 4; ++a)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
+            for (int c = 0; c < 3; ++c) g[a][c] = G[(3 * (a - 1) + c) * tn + i];
 #pragma unroll
         for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-        const double V = __ldg(gp);
-        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
+        const double V = G[9 * tn + i];
+        const ushort4 lc = tc_s[sh_tc + i];
         const int li[4] = {lc.x, lc.y, lc.z, lc.w};
         double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
 #pragma unroll
@@ -135,21 +222,22 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
             gyz = gyz + (gz * uy + gy * uz);
             gxz = gxz + (gz * ux + gx * uz);
         }
-        T[i] = V * ex;
-        T[tn + i] = V * ey;
-        T[2 * tn + i] = V * ez;
-        T[3 * tn + i] = V * gxy;
-        T[4 * tn + i] = V * gyz;
-        T[5 * tn + i] = V * gxz;
-        T[6 * tn + i] = V;
+        G[i] = V * ex;
+        G[tn + i] = V * ey;
+        G[2 * tn + i] = V * ez;
+        G[3 * tn + i] = V * gxy;
+        G[4 * tn + i] = V * gyz;
+        G[5 * tn + i] = V * gxz;
+        G[6 * tn + i] = V;
     }
     __syncthreads();
-    const int64_t s = (int64_t)b * d.blk + threadIdx.x;
-    if (s >= d.S) return;
+    if (tid >= ns) return;
+    const int64_t s = s0 + tid;
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
-    for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
-        const uint4 q = __ldg(row + (w >> 3));
+    const uint4 *row = reinterpret_cast<const uint4 *>(ell_s + tid * d.we);
+    const double *T = G;
+    for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B shared load, in order
+        const uint4 q = row[w >> 3];
         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
@@ -172,14 +260,14 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     }
     const double inv = 1.0 / Vh;
     const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-    const double s0 = d.l2m * e11 + d.lam * (e22 + e33);
+    const double s0v = d.l2m * e11 + d.lam * (e22 + e33);
     const double s1 = d.l2m * e22 + d.lam * (e11 + e33);
     const double s2 = d.l2m * e33 + d.lam * (e11 + e22);
     const double s3 = d.mu * g12, s4 = d.mu * g23, s5 = d.mu * g13;
-    const double r0 = fabs(s0) + fabs(s3) + fabs(s5);
+    const double r0 = fabs(s0v) + fabs(s3) + fabs(s5);
     const double r1 = fabs(s1) + fabs(s3) + fabs(s4);
     const double r2 = fabs(s2) + fabs(s4) + fabs(s5);
-    st256(o, s0, s1, s2, s3);
+    st256(o, s0v, s1, s2, s3);
     st256(o + 1, s4, s5, fmax(r0, fmax(r1, r2)), 0.0);
 }
 
@@ -644,14 +732,20 @@ __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
 #define CEM_PERSIST_MINB 4
 #endif
 __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint64_t bar;
     __shared__ unsigned long long sh_q;
     __shared__ int sh_ndisc;
     __shared__ int sh_disc[64];
     const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)d.P;
     const int tid = threadIdx.x;
     unsigned long long qn = 0;
-    if (tid == 0) qn = atomicAdd(d.head, 1ull);
+    uint32_t phase = 0;
+    if (tid == 0) {
+        qn = atomicAdd(d.head, 1ull);
+        mbar_init(&bar, 1);
+    }
+    __syncthreads();
     for (;;) {
         if (tid == 0) {
             sh_q = qn;
@@ -681,7 +775,10 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
         __syncthreads();
         const double4 *u1 = d.ubuf[(s + 1) & 1];
         switch (g) {
-            case ST_AB: block_AB(d, b, u1, sm); break;
+            case ST_AB:
+                block_AB(d, b, u1, sm, &bar, phase);
+                phase ^= 1;
+                break;
             case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
             default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
         }
@@ -725,8 +822,11 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 #define CEM_D_MINB 3
 #endif
 __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
-    extern __shared__ double sm[];
-    block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm, &bar, 0);
 }
 __global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every) {
     extern __shared__ double sm[];
@@ -738,8 +838,11 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
 
 // criterion on the current state u_n (cem_crack_update)
 __global__ void __launch_bounds__(256) k_AB_cur(Dev d, int64_t n) {
-    extern __shared__ double sm[];
-    block_AB(d, blockIdx.x, d.ubuf[n & 1], sm);
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    block_AB(d, blockIdx.x, d.ubuf[n & 1], sm, &bar, 0);
 }
 __global__ void __launch_bounds__(256, 4) k_C_cur(Dev d, int64_t n, int32_t stamp) {
     extern __shared__ double sm[];
