@@ -137,13 +137,9 @@ Offs layout(const HostMesh &h, const Plan &p) {
     return o;
 }
 
-int smem_bytes_for(const Plan &p) {  // odd plane strides (pstride) + 16-B aligned metadata pieces
-    auto p16 = [](int b) { return (b + 15) & ~15; };
-    const int ab = 8 * (10 * ((p.max_tl + 1) | 1) + 3 * (p.max_nlb | 1)) + 16 + p16(4 * (p.max_nlb + 8)) +
-                   p16(4 * (p.max_tl + 8)) + p16(8 * (p.max_tl + 4)) + p16(2 * p.blk * p.we) + p16(p.max_tl + 8);
-    const int c = 8 * (7 * (p.max_el | 1) + 3 * (p.max_nl | 1));
-    return std::max(ab, c);
-}
+int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1)); }
+int smem_c_for(const Plan &p) { return 8 * (7 * (p.max_el | 1) + 3 * (p.max_nl | 1)); }
+int smem_bytes_for(const Plan &p) { return std::max(smem_ab_for(p), smem_c_for(p)); }  // odd plane strides
 
 template <class T>
 T *at(void *base, size_t off) {
@@ -191,6 +187,8 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.tl_off = at<int32_t>(b, o.tl_off);
     d.tl = at<int32_t>(b, o.tl);
     d.smem_bytes = smem_bytes_for(p);
+    d.smem_ab = smem_ab_for(p);
+    d.smem_c = smem_c_for(p);
     d.self = at<Dev>(b, o.self);
     d.ncons = at<int32_t>(b, o.ncons);
     d.cons_done = at<int32_t>(b, o.cons_done);

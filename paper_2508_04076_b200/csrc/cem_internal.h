@@ -126,7 +126,7 @@ struct Dev {
     const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
     const uint16_t *tconn;
     const uint16_t *lconn, *ledge;
-    int smem_bytes;
+    int smem_bytes, smem_ab, smem_c;  // dynamic shared memory: persistent kernel (max), per stage
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] spare
     int64_t *rec_step;

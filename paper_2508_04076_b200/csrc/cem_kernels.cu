@@ -118,97 +118,56 @@ __device__ __forceinline__ int bulk_window(const T *p, int n, const T *&a, uint3
 }
 __host__ __device__ __forceinline__ int pad16(int bytes) { return (bytes + 15) & ~15; }
 
+// programmatic dependent launch (PDL): let the next stage kernel launch early, and wait for
+// the previous one only where its outputs are read
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
 // ------------------------------------------------------------------ stage AB: strain + edge stress
 // For the edge block's deduplicated tet list: eps = sum_a B_a u_a (a = 0..3 in order), Voigt
 // (11,22,33,12,23,13) with engineering shears, gradN0 = -((gradN1 + gradN2) + gradN3),
-// tau = V eps -> shared-memory planes (zeros for inactive tets).
-// Then per edge: Vhat = sum V_e, T = sum tau_e over the incident tets in original-id order,
-// eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj + eps_kk),
-// sigma_ij = mu gamma_ij, plus the Gershgorin bound g = max_i sum_j
-// |sigma_ij| used by the early-out of stage C.
-// Data movement: one thread issues TMA bulk copies of the block's contiguous metadata (node
-// list, tet list, local connectivity, ELL rows) onto an mbarrier; then every thread gathers
-// u and the tet geometry straight into shared memory with cp.async (LDGSTS).  Two dependent
-// global waves per block, no registers held across them.
-__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm, uint64_t *bar,
-                                         uint32_t phase) {
-    const int tid = threadIdx.x, nthr = blockDim.x;
+// tau = V eps -> shared-memory planes (V = 0 marks an inactive tet).
+// Then per edge: Vhat = sum V_e, T = sum tau_e over the active incident tets in original-id
+// order, eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj +
+// eps_kk), sigma_ij = mu gamma_ij, plus the Gershgorin bound
+// g = max_i sum_j |sigma_ij| used by the early-out of stage C.
+__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm) {
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
     const int32_t n0 = __ldg(d.nlb_off + b);
     const int nn = __ldg(d.nlb_off + b + 1) - n0;
-    const int64_t s0 = (int64_t)b * d.blk;
-    const int ns = (int)min((int64_t)d.blk, d.S - s0);
     const int un = pstride(nn), tn = pstride(nt + 1);  // row nt: all-zero sentinel
-    // shared-memory carve-up (16-B aligned pieces)
-    double *G = sm;                 // [10][tn]: grads 0..8, V at 9; tau/V overwrite 0..6 in place
-    double *U = G + 10 * tn;        // [3][un]
-    char *mp = reinterpret_cast<char *>(U + 3 * un);
-    mp = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(mp) + 15) & ~uintptr_t(15));
-    int32_t *nl_s = reinterpret_cast<int32_t *>(mp);
-    mp += pad16(4 * (nn + 8));
-    int32_t *tl_s = reinterpret_cast<int32_t *>(mp);
-    mp += pad16(4 * (nt + 8));
-    ushort4 *tc_s = reinterpret_cast<ushort4 *>(mp);
-    mp += pad16(8 * (nt + 4));
-    uint16_t *ell_s = reinterpret_cast<uint16_t *>(mp);
-    mp += pad16(2 * d.blk * d.we);
-    uint8_t *st_s = reinterpret_cast<uint8_t *>(mp);
-    // ---- wave 1: TMA bulk copies of the contiguous metadata
-    const int32_t *a_nl, *a_tl;
-    const ushort4 *a_tc;
-    uint32_t b_nl, b_tl, b_tc;
-    const int sh_nl = bulk_window(d.nlb + n0, nn, a_nl, b_nl);
-    const int sh_tl = bulk_window(d.tl + t0, nt, a_tl, b_tl);
-    const int sh_tc = bulk_window(reinterpret_cast<const ushort4 *>(d.tconn) + t0, nt, a_tc, b_tc);
-    const uint32_t b_ell = (uint32_t)(2 * ns * d.we);
-    if (tid == 0) {
-        // order earlier generic-proxy accesses of this shared memory before the async copies
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, b_nl + b_tl + b_tc + b_ell);
-        bulk_g2s(nl_s, a_nl, b_nl, bar);
-        bulk_g2s(tl_s, a_tl, b_tl, bar);
-        bulk_g2s(tc_s, a_tc, b_tc, bar);
-        bulk_g2s(ell_s, d.incE + s0 * d.we, b_ell, bar);
+    double *U = sm, *T = sm + 3 * un;
+    pdl_wait();  // u and the tet states come from the previous kernels
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
+        const double4 w = ld256(u + __ldg(d.nlb + n0 + i));
+        U[i] = w.x;
+        U[un + i] = w.y;
+        U[2 * un + i] = w.z;
     }
-    mbar_wait(bar, phase);
-    // ---- wave 2: cp.async gathers of u and of the tet geometry (warp-tiled rows)
-    for (int i = tid; i < nn; i += nthr) {
-        const double *w = reinterpret_cast<const double *>(u + nl_s[sh_nl + i]);
-        cp8(U + i, w);
-        cp8(U + un + i, w + 1);
-        cp8(U + 2 * un + i, w + 2);
-    }
-    for (int i = tid; i < nt; i += nthr) {
-        const uint32_t e = (uint32_t)tl_s[sh_tl + i];
-        const double *gp = geo_ptr(d, e);
-#pragma unroll
-        for (int c = 0; c < 9; ++c) cp8(G + c * tn + i, gp + 32 * (2 + c));
-        cp8(G + 9 * tn + i, gp);
-        st_s[i] = d.state[e];
-    }
-    cp_wait_all();
     __syncthreads();
-    for (int i = tid; i <= nt; i += nthr) {
-        if (i == nt || !st_s[i]) {
-            // inactive tet / sentinel: exact zeros.  Running sums here never hold -0.0, so
+    for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
+        const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
+        if (i == nt || !d.state[e]) {
+            // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so
             // adding +0.0 is bit-identical to skipping the entry.
 #pragma unroll
-            for (int c = 0; c < 7; ++c) G[c * tn + i] = 0.0;
+            for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
             continue;
         }
+        const double *gp = geo_ptr(d, e);
         double g[4][3];
 #pragma unroll
         for (int a = 1; a < 4; ++a)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) g[a][c] = G[(3 * (a - 1) + c) * tn + i];
+            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
 #pragma unroll
         for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-        const double V = G[9 * tn + i];
-        const ushort4 lc = tc_s[sh_tc + i];
+        const double V = __ldg(gp);
+        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
         const int li[4] = {lc.x, lc.y, lc.z, lc.w};
         double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
 #pragma unroll
@@ -222,22 +181,21 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
             gyz = gyz + (gz * uy + gy * uz);
             gxz = gxz + (gz * ux + gx * uz);
         }
-        G[i] = V * ex;
-        G[tn + i] = V * ey;
-        G[2 * tn + i] = V * ez;
-        G[3 * tn + i] = V * gxy;
-        G[4 * tn + i] = V * gyz;
-        G[5 * tn + i] = V * gxz;
-        G[6 * tn + i] = V;
+        T[i] = V * ex;
+        T[tn + i] = V * ey;
+        T[2 * tn + i] = V * ez;
+        T[3 * tn + i] = V * gxy;
+        T[4 * tn + i] = V * gyz;
+        T[5 * tn + i] = V * gxz;
+        T[6 * tn + i] = V;
     }
     __syncthreads();
-    if (tid >= ns) return;
-    const int64_t s = s0 + tid;
+    const int64_t s = (int64_t)b * d.blk + threadIdx.x;
+    if (s >= d.S) return;
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    const uint4 *row = reinterpret_cast<const uint4 *>(ell_s + tid * d.we);
-    const double *T = G;
-    for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B shared load, in order
-        const uint4 q = row[w >> 3];
+    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
+    for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
+        const uint4 q = __ldg(row + (w >> 3));
         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
@@ -260,14 +218,14 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     }
     const double inv = 1.0 / Vh;
     const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-    const double s0v = d.l2m * e11 + d.lam * (e22 + e33);
+    const double s0 = d.l2m * e11 + d.lam * (e22 + e33);
     const double s1 = d.l2m * e22 + d.lam * (e11 + e33);
     const double s2 = d.l2m * e33 + d.lam * (e11 + e22);
     const double s3 = d.mu * g12, s4 = d.mu * g23, s5 = d.mu * g13;
-    const double r0 = fabs(s0v) + fabs(s3) + fabs(s5);
+    const double r0 = fabs(s0) + fabs(s3) + fabs(s5);
     const double r1 = fabs(s1) + fabs(s3) + fabs(s4);
     const double r2 = fabs(s2) + fabs(s4) + fabs(s5);
-    st256(o, s0v, s1, s2, s3);
+    st256(o, s0, s1, s2, s3);
     st256(o + 1, s4, s5, fmax(r0, fmax(r1, r2)), 0.0);
 }
 
@@ -498,6 +456,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #pragma unroll
     for (int m = 0; m < kME; ++m) sid[m] = tid + m * nthr < ne ? (uint32_t)__ldg(d.el + s0i + tid + m * nthr) : 0u;
     const int32_t nid = (early && tid < nn) ? __ldg(d.nl + n0 + tid) : 0;
+    pdl_wait();  // sigma records come from stage AB
     // ---- wave 2: gathered records
     double4 rx[kME], ry[kME];
 #pragma unroll
@@ -620,6 +579,7 @@ __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p,
     const uint8_t fl = __ldg(&d.nflag[k]);
     if (fl & 16) return;  // multi-GPU: another rank owns (and updates) this node
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
+    pdl_wait();  // force slots come from stage C
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     for (int w = 0; w < d.wn; w += 8) {
         // padding entries point at an all-zero slot: adding +0.0 is an exact no-op here
@@ -733,19 +693,13 @@ __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
 #endif
 __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int64_t step0, int64_t nsteps, int crack_every) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ uint64_t bar;
     __shared__ unsigned long long sh_q;
     __shared__ int sh_ndisc;
     __shared__ int sh_disc[64];
     const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)d.P;
     const int tid = threadIdx.x;
     unsigned long long qn = 0;
-    uint32_t phase = 0;
-    if (tid == 0) {
-        qn = atomicAdd(d.head, 1ull);
-        mbar_init(&bar, 1);
-    }
-    __syncthreads();
+    if (tid == 0) qn = atomicAdd(d.head, 1ull);
     for (;;) {
         if (tid == 0) {
             sh_q = qn;
@@ -775,10 +729,7 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
         __syncthreads();
         const double4 *u1 = d.ubuf[(s + 1) & 1];
         switch (g) {
-            case ST_AB:
-                block_AB(d, b, u1, sm, &bar, phase);
-                phase ^= 1;
-                break;
+            case ST_AB: block_AB(d, b, u1, sm); break;
             case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
             default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
         }
@@ -823,26 +774,23 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 #endif
 __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ uint64_t bar;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm, &bar, 0);
+    pdl_trigger();
+    block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
 }
 __global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every) {
     extern __shared__ double sm[];
+    pdl_trigger();
     block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
+    pdl_trigger();
     block_D(d, blockIdx.x, d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
 // criterion on the current state u_n (cem_crack_update)
 __global__ void __launch_bounds__(256) k_AB_cur(Dev d, int64_t n) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ uint64_t bar;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    block_AB(d, blockIdx.x, d.ubuf[n & 1], sm, &bar, 0);
+    block_AB(d, blockIdx.x, d.ubuf[n & 1], sm);
 }
 __global__ void __launch_bounds__(256, 4) k_C_cur(Dev d, int64_t n, int32_t stamp) {
     extern __shared__ double sm[];
@@ -891,11 +839,32 @@ void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_ev
     k_persistent<<<grid, 256, d.smem_bytes, st>>>(d, step0, nsteps, crack_every);
 }
 
+template <class K, class... Args>
+void launch_pdl(K kern, unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
+    if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
+        launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (size_t)d.smem_ab, st, d, s);
+        launch_pdl(k_C, (unsigned)d.nblk[ST_C], (size_t)d.smem_c, st, d, s, crack_every);
+        launch_pdl(k_D, (unsigned)d.nblk[ST_D], (size_t)0, st, d, s);
+        return;
+    }
     if (ev) cudaEventRecord(ev[0], st);
-    k_AB<<<d.nblk[ST_AB], 256, d.smem_bytes, st>>>(d, s);
+    k_AB<<<d.nblk[ST_AB], 256, d.smem_ab, st>>>(d, s);
     if (ev) cudaEventRecord(ev[1], st);
-    k_C<<<d.nblk[ST_C], 256, d.smem_bytes, st>>>(d, s, crack_every);
+    k_C<<<d.nblk[ST_C], 256, d.smem_c, st>>>(d, s, crack_every);
     if (ev) cudaEventRecord(ev[2], st);
     k_D<<<d.nblk[ST_D], 256, 0, st>>>(d, s);
     if (ev) cudaEventRecord(ev[3], st);
@@ -903,8 +872,8 @@ void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t s
 
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st) {
     const int32_t stamp = -(int32_t)(n + 1);
-    k_AB_cur<<<d.nblk[ST_AB], 256, d.smem_bytes, st>>>(d, n);
-    k_C_cur<<<d.nblk[ST_C], 256, d.smem_bytes, st>>>(d, n, stamp);
+    k_AB_cur<<<d.nblk[ST_AB], 256, d.smem_ab, st>>>(d, n);
+    k_C_cur<<<d.nblk[ST_C], 256, d.smem_c, st>>>(d, n, stamp);
     k_fix_cur<<<nblk(d.N), 256, 0, st>>>(d, n, stamp);
 }
 
