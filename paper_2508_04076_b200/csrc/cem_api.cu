@@ -160,6 +160,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.incE = at<uint16_t>(b, o.incE);
     d.nodeE = at<int32_t>(b, o.nodeE);
     d.we = p.we;
+    d.we_max = p.we_max;
     d.zslot = p.zslot;
     d.wn = p.wn;
     d.X = at<double4>(b, o.X);

@@ -86,6 +86,7 @@ struct Plan {
     // instruction-lean layouts
     std::vector<double> geoT;         // [E/32][11][32]: V, V/6, gradN1..3 (x,y,z) per warp tile
     int we = 8;                       // ELL width of edge incidences (multiple of 8)
+    int we_max = 8;                   // largest incidence count (loop bound)
     std::vector<uint16_t> incE;       // [S][we] index into the edge block's tet list, 0xFFFF = none
     int wn = 8;                       // ELL width of node incidences (multiple of 8)
     std::vector<int32_t> nodeE;       // [N][wn] force slot of each incidence (original order), zslot = none
@@ -121,7 +122,7 @@ struct Dev {
     const double *geoT;        // [E/32][11][32] warp-tiled geometry
     const uint16_t *incE;      // [S][we]
     const int32_t *nodeE;      // [N][wn]
-    int we, wn;
+    int we, wn, we_max;        // ELL widths; we_max = largest edge incidence count
     int32_t zslot;             // index of the all-zero force slot (ELL padding)
     const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
     const uint16_t *tconn;

@@ -197,8 +197,10 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
         const uint4 q = __ldg(row + (w >> 3));
         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+        const int lim = d.we_max - w;  // warp-uniform: slots past the mesh's max incidence are skipped
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
+            if (t >= lim) break;
             // padding (0xffff) -> the all-zero sentinel row nt; inactive tets hold zeros
             const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
             Vh = Vh + T[6 * tn + r];

@@ -251,6 +251,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         int mx = 1;
         for (int64_t s = 0; s < S; ++s) mx = std::max(mx, p.edge_off[s + 1] - p.edge_off[s]);
         p.we = (mx + 7) / 8 * 8;
+        p.we_max = mx;
         p.incE.assign((size_t)S * p.we, 0xFFFF);
         for (int64_t s = 0; s < S; ++s)
             for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j) p.incE[(size_t)s * p.we + (j - p.edge_off[s])] = p.inc_local[j];
