@@ -56,7 +56,12 @@ thread_local std::string g_init_err;
         }                                                                             \
     } while (0)
 
-constexpr int kBlk = 256;  // entities per work item (= threads per CTA)
+// entities per work item (= threads per CTA); CEM_BLK (128 or 256) is a tuning knob
+int block_size() {
+    const char *e = getenv("CEM_BLK");
+    const int b = e ? atoi(e) : 256;
+    return (b == 128 || b == 256) ? b : 256;
+}
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -527,7 +532,7 @@ cem_status cem_workspace_size(const cem_mesh_in *mesh, const cem_opts *opts, siz
     cem_status st = build_host_mesh(mesh, &mat, nullptr, &o, h, g_init_err);
     if (st) return st;
     h.any_dirichlet = true;
-    build_plan(h, kBlk, p);
+    build_plan(h, block_size(), p);
     *bytes = layout(h, p).total;
     return CEM_OK;
 }
@@ -588,7 +593,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         ctx->err = "cudaSetDevice failed (no CUDA device?)";
         return fail(CEM_ECUDA);
     }
-    build_plan(ctx->h, kBlk, ctx->p, tflag_local.empty() ? nullptr : tflag_local.data());
+    build_plan(ctx->h, block_size(), ctx->p, tflag_local.empty() ? nullptr : tflag_local.data());
     const int smem = smem_bytes_for(ctx->p);
     if (smem > 227 * 1024) {
         ctx->err = "a block's gather list exceeds shared memory (" + std::to_string(smem) + " bytes)";
@@ -597,7 +602,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     set_smem_limits(smem);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    const int occ = std::max(1, persistent_occupancy(smem));
+    const int occ = std::max(1, persistent_occupancy(smem, ctx->p.blk));
     ctx->grid = sms * occ;
     {
         const char *ev = getenv("CEM_SCHED_SLACK");  // tuning knob: slack in units of resident CTAs

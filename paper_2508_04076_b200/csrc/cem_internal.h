@@ -151,7 +151,7 @@ struct Dev {
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
-int persistent_occupancy(int smem_bytes);  // resident CTAs per SM of the persistent kernel
+int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel
 void set_smem_limits(int smem_bytes);
 extern const int kThreads;
 

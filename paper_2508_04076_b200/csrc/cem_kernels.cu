@@ -818,10 +818,10 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
 
-int persistent_occupancy(int smem_bytes) {
+int persistent_occupancy(int smem_bytes, int blk) {
     int n = 0;
     cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent, 256, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent, blk, smem_bytes);
     return n;
 }
 
@@ -838,14 +838,14 @@ void set_smem_limits(int smem_bytes) {
 
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st) {
     cudaMemsetAsync(d.head, 0, sizeof(unsigned long long), st);
-    k_persistent<<<grid, 256, d.smem_bytes, st>>>(d, step0, nsteps, crack_every);
+    k_persistent<<<grid, d.blk, d.smem_bytes, st>>>(d, step0, nsteps, crack_every);
 }
 
 template <class K, class... Args>
-void launch_pdl(K kern, unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(blk);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -858,24 +858,24 @@ void launch_pdl(K kern, unsigned grid, size_t smem, cudaStream_t st, Args... arg
 
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
-        launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (size_t)d.smem_ab, st, d, s);
-        launch_pdl(k_C, (unsigned)d.nblk[ST_C], (size_t)d.smem_c, st, d, s, crack_every);
-        launch_pdl(k_D, (unsigned)d.nblk[ST_D], (size_t)0, st, d, s);
+        launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
+        launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
+        launch_pdl(k_D, (unsigned)d.nblk[ST_D], (unsigned)d.blk, (size_t)0, st, d, s);
         return;
     }
     if (ev) cudaEventRecord(ev[0], st);
-    k_AB<<<d.nblk[ST_AB], 256, d.smem_ab, st>>>(d, s);
+    k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
     if (ev) cudaEventRecord(ev[1], st);
-    k_C<<<d.nblk[ST_C], 256, d.smem_c, st>>>(d, s, crack_every);
+    k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
     if (ev) cudaEventRecord(ev[2], st);
-    k_D<<<d.nblk[ST_D], 256, 0, st>>>(d, s);
+    k_D<<<d.nblk[ST_D], d.blk, 0, st>>>(d, s);
     if (ev) cudaEventRecord(ev[3], st);
 }
 
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st) {
     const int32_t stamp = -(int32_t)(n + 1);
-    k_AB_cur<<<d.nblk[ST_AB], 256, d.smem_ab, st>>>(d, n);
-    k_C_cur<<<d.nblk[ST_C], 256, d.smem_c, st>>>(d, n, stamp);
+    k_AB_cur<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, n);
+    k_C_cur<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, n, stamp);
     k_fix_cur<<<nblk(d.N), 256, 0, st>>>(d, n, stamp);
 }
 
