@@ -56,6 +56,13 @@ __device__ __forceinline__ double4 ld256(const double4 *p) {  // LDG.E.256 (sm_1
 __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, double w) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
 }
+// Data produced inside the same (persistent) kernel by other CTAs is read at L2 (.cg,
+// LDG.STRONG.GPU): no stale L1 lines, so no SM-wide L1 invalidation is needed per work item.
+__device__ __forceinline__ double4 ldcg256(const double4 *p) {
+    double4 r;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
 
 // warp-tiled geometry: tet e -> tile e>>5, lane e&31, component c at [tile][c][lane]
 __device__ __forceinline__ const double *geo_ptr(const Dev &d, uint32_t e) { return d.geoT + ((e >> 5) * 352u + (e & 31u)); }
@@ -69,7 +76,7 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
         const int32_t sl = __ldg(row + j);
         if (sl == d.zslot) break;
         const int64_t e = slot_tet(sl);
-        if (!d.state[e]) continue;
+        if (!__ldcg(d.state + e)) continue;
         acc = acc + (d.rho * __ldg(geo_ptr(d, e))) / 4.0;
     }
     return acc;
@@ -143,7 +150,7 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     double *U = sm, *T = sm + 3 * un;
     pdl_wait();  // u and the tet states come from the previous kernels
     for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
-        const double4 w = ld256(u + __ldg(d.nlb + n0 + i));
+        const double4 w = ldcg256(u + __ldg(d.nlb + n0 + i));
         U[i] = w.x;
         U[un + i] = w.y;
         U[2 * un + i] = w.z;
@@ -151,7 +158,7 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     __syncthreads();
     for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
         const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
-        if (i == nt || !d.state[e]) {
+        if (i == nt || !__ldcg(d.state + e)) {
             // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so
             // adding +0.0 is bit-identical to skipping the entry.
 #pragma unroll
@@ -345,7 +352,7 @@ __device__ __noinline__ void evaluate_tet(const Dev *__restrict__ dp, int64_t e,
     Vec3 Xn[4], un[4];
     for (int a = 0; a < 4; ++a) {
         const double4 x = ldro4(&d.X[nid[a]]);
-        const double4 uu = ld4(&u[nid[a]]);
+        const double4 uu = ldcg256(&u[nid[a]]);
         Xn[a] = {x.x, x.y, x.z};
         un[a] = {uu.x, uu.y, uu.z};
     }
@@ -360,7 +367,7 @@ __device__ __noinline__ void evaluate_tet(const Dev *__restrict__ dp, int64_t e,
     for (int l = 0; l < 6; ++l) {
         const double *sg = d.srec + 8 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
         double s6[6];
-        for (int i = 0; i < 6; ++i) s6[i] = sg[i];
+        for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
         principal(s6, eg[l]);
     }
     Gbest = 0.0;
@@ -465,10 +472,10 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     for (int m = 0; m < kME; ++m)
         if (tid + m * nthr < ne) {
             const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8u * sid[m]);
-            rx[m] = ld256(r);
-            ry[m] = ld256(r + 1);
+            rx[m] = ldcg256(r);
+            ry[m] = ldcg256(r + 1);
         }
-    const double4 uw = (early && tid < nn) ? ld256(u + nid) : make_double4(0, 0, 0, 0);
+    const double4 uw = (early && tid < nn) ? ldcg256(u + nid) : make_double4(0, 0, 0, 0);
 #pragma unroll
     for (int m = 0; m < kME; ++m) {
         const int i = tid + m * nthr;
@@ -484,7 +491,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     }
     for (int i = tid + kME * nthr; i < ne; i += nthr) {  // tail
         const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8u * (uint32_t)__ldg(d.el + s0i + i));
-        const double4 x = ld256(r), y = ld256(r + 1);
+        const double4 x = ldcg256(r), y = ldcg256(r + 1);
         sm[i] = x.x;
         sm[np + i] = x.y;
         sm[2 * np + i] = x.z;
@@ -500,7 +507,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
             smu[2 * nq + tid] = uw.z;
         }
         for (int i = tid + nthr; i < nn; i += nthr) {
-            const double4 w = ld256(u + __ldg(d.nl + n0 + i));
+            const double4 w = ldcg256(u + __ldg(d.nl + n0 + i));
             smu[i] = w.x;
             smu[nq + i] = w.y;
             smu[2 * nq + i] = w.z;
@@ -510,7 +517,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int64_t e = (int64_t)b * d.blk + threadIdx.x;
     if (e >= d.E) return;
     double4 *fo = d.fe + (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));  // slot (e,a) = fo + 32 a
-    if (!d.state[e]) {
+    if (!__ldcg(d.state + e)) {
 #pragma unroll
         for (int a = 0; a < 4; ++a) st256(fo + 32 * a, 0.0, 0.0, 0.0, 0.0);
         return;
@@ -589,7 +596,7 @@ __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p,
         const int32_t sl[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
         double4 f[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) f[t] = ld256(d.fe + (uint32_t)sl[t]);
+        for (int t = 0; t < 8; ++t) f[t] = ldcg256(d.fe + (uint32_t)sl[t]);
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             f0 = f0 + f[t].x;
@@ -598,9 +605,9 @@ __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p,
         }
         if (sl[7] == d.zslot) break;
     }
-    double mk = d.mass[k];
-    const double4 u1 = ld256(&u1p[k]);
-    const double4 v = ld256(&d.v[k]), a = ld256(&d.a[k]);
+    double mk = __ldcg(d.mass + k);
+    const double4 u1 = ldcg256(&u1p[k]);
+    const double4 v = ldcg256(&d.v[k]), a = ldcg256(&d.a[k]);
     const double dt = d.dt;
     double fx = 0.0, fy = 0.0, fz = 0.0;
     if (fl & 8) {
@@ -635,7 +642,7 @@ __device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p,
             aa[c] = an;
         }
     }
-    if (d.dirty[k] == (int32_t)(s + 1)) {
+    if (__ldcg(d.dirty + k) == (int32_t)(s + 1)) {
         // an incident tet split in this step: lumped mass from the active incidences;
         // m = 0 -> frozen, v = a = 0 (R15)
         mk = node_mass(d, k);
@@ -725,8 +732,7 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
                 const int pb = __ldg(d.dep + i);
                 while (ld_acquire(c + pb) < need) __nanosleep(32);
             }
-            __syncwarp();
-            if (tid == 0) __threadfence();  // order + invalidate this SM's L1 before the reads
+            __syncwarp();  // produced data is read with .cg loads (L2): no L1 invalidation needed
         }
         __syncthreads();
         const double4 *u1 = d.ubuf[(s + 1) & 1];

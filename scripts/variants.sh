@@ -1,4 +1,6 @@
 #!/bin/bash
-for lib in paper_2508_04076_b200/libcem.so build/libcem_ab4.so build/libcem_ab3c3.so; do
-  CEM_LIB=$lib timeout 120 python scripts/variant_bench.py 2 200
+export CEM_SCHED_SLACK=8
+for blk in 256 128; do
+  for fl in 0 12; do CEM_BLK=$blk timeout 120 python scripts/variant_bench.py $fl 200 | sed "s/^/blk=$blk /"; done
 done
+CEM_BLK=128 timeout 300 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "cfg0_full or weak_block or persistent" 2>&1 | tail -1
