@@ -64,6 +64,8 @@ int block_size() {
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+// force slots: 4 per tet in 32-tet tiles, + the all-zero slot
+int64_t fe_slots(int64_t E) { return 4 * ((E + 31) / 32) * 32 + 1; }
 
 struct Layout {
     size_t off = 0;
@@ -109,8 +111,8 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.u1 = L.take<double4>(N);
     o.v = L.take<double4>(N);
     o.a = L.take<double4>(N);
-    o.srec = L.take<double>(8 * S);
-    o.fe = L.take<double4>(4 * ((E + 31) / 32) * 32 + 1);  // + the zero slot
+    o.srec = L.take<double>(6 * S);
+    o.fe = L.take<double4>(fe_slots(E));  // + the zero slot
     o.ctr = L.take<int32_t>(8);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
@@ -297,8 +299,8 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.u1, u1.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.v, v4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 8 * S, st));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * (4 * ((E + 31) / 32) * 32 + 1), st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 6 * S, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * fe_slots(E), st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
@@ -796,6 +798,9 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     CUDA_TRY(cudaMemcpyAsync(ctr, ctx->d.ctr, sizeof ctr, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const int64_t nrec = ctr[0];
+#ifdef CEM_POLL_STATS
+    fprintf(stderr, "[cem poll stats] polls AB %d C %d D %d, items that waited %d\n", ctr[4], ctr[5], ctr[6], ctr[7]);
+#endif
     // records: unordered on the device; ordered here by (step, element) and U_d summed in
     // that order (the oracle's split-pass order)
     std::vector<int64_t> rs(nrec);

@@ -117,8 +117,8 @@ struct Dev {
     int32_t *dirty;            // [N] step stamp of the last split touching the node
     double4 *ubuf[2];          // u_m lives in ubuf[m & 1]
     double4 *v, *a;
-    double *srec;              // [S][8]: sigma_s (6), Gershgorin bound g_s, pad
-    double4 *fe;               // [4E] force slots f_{e,a} (x,y,z,pad); slot(e,a) = ((e>>5)*4 + a)*32 + (e&31)
+    double *srec;              // [S][6]: sigma_s (11,22,33,12,23,13), 48-B records
+    double4 *fe;               // [4E] force slots f_{e,a} (x,y,z,0); slot(e,a) = ((e>>5)*4 + a)*32 + (e&31)
     const double *geoT;        // [E/32][11][32] warp-tiled geometry
     const uint16_t *incE;      // [S][we]
     const int32_t *nodeE;      // [N][wn]

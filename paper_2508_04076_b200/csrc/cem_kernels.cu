@@ -56,6 +56,14 @@ __device__ __forceinline__ double4 ld256(const double4 *p) {  // LDG.E.256 (sm_1
 __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, double w) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
 }
+__device__ __forceinline__ void st128(double *p, double x, double y) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ double2 ldcg128(const double *p) {
+    double2 r;
+    asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
 // Data produced inside the same (persistent) kernel by other CTAs is read at L2 (.cg,
 // LDG.STRONG.GPU): no stale L1 lines, so no SM-wide L1 invalidation is needed per work item.
 __device__ __forceinline__ double4 ldcg256(const double4 *p) {
@@ -139,70 +147,111 @@ __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 // tau = V eps -> shared-memory planes (V = 0 marks an inactive tet).
 // Then per edge: Vhat = sum V_e, T = sum tau_e over the active incident tets in original-id
 // order, eps~ = T * (1/Vhat), sigma_ii = (lam+2mu) eps_ii + lam (eps_jj +
-// eps_kk), sigma_ij = mu gamma_ij, plus the Gershgorin bound
-// g = max_i sum_j |sigma_ij| used by the early-out of stage C.
+// eps_kk), sigma_ij = mu gamma_ij, stored as a packed 48-B record.
+// tau = V eps of one tet from its staged nodes (a = 0..3 in order) into row i of the planes
+__device__ __forceinline__ void tau_row(double *T, int tn, int i, const double *U, int un, const double (&g)[4][3],
+                                        double V, ushort4 lc) {
+    const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+    double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const double ux = U[li[a]], uy = U[un + li[a]], uz = U[2 * un + li[a]];
+        const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
+        ex = ex + gx * ux;
+        ey = ey + gy * uy;
+        ez = ez + gz * uz;
+        gxy = gxy + (gy * ux + gx * uy);
+        gyz = gyz + (gz * uy + gy * uz);
+        gxz = gxz + (gz * ux + gx * uz);
+    }
+    T[i] = V * ex;
+    T[tn + i] = V * ey;
+    T[2 * tn + i] = V * ez;
+    T[3 * tn + i] = V * gxy;
+    T[4 * tn + i] = V * gyz;
+    T[5 * tn + i] = V * gxz;
+    T[6 * tn + i] = V;
+}
+__device__ __forceinline__ void zero_row(double *T, int tn, int i) {
+#pragma unroll
+    for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
+}
+// the 9 stored gradients (nodes 1..3) and V of tet e; gradN0 = -((gradN1 + gradN2) + gradN3)
+__device__ __forceinline__ void load_geo(const Dev &d, uint32_t e, double (&g)[4][3], double &V) {
+    const double *gp = geo_ptr(d, e);
+#pragma unroll
+    for (int a = 1; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
+    V = __ldg(gp);
+}
+__device__ __forceinline__ void grad0(double (&g)[4][3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+}
+
 __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
     const int32_t n0 = __ldg(d.nlb_off + b);
     const int nn = __ldg(d.nlb_off + b + 1) - n0;
     const int un = pstride(nn), tn = pstride(nt + 1);  // row nt: all-zero sentinel
     double *U = sm, *T = sm + 3 * un;
+    // static tables of this thread's first tet and node before the dependency wait (they
+    // overlap the previous stage's tail and the u gather)
+    const bool has0 = tid < nt;
+    const uint32_t e0 = has0 ? (uint32_t)__ldg(d.tl + t0 + tid) : 0u;
+    double g0[4][3], V0 = 0.0;
+    ushort4 lc0 = make_ushort4(0, 0, 0, 0);
+    if (has0) {
+        load_geo(d, e0, g0, V0);
+        lc0 = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + tid);
+    }
+    const int32_t k0 = tid < nn ? __ldg(d.nlb + n0 + tid) : 0;
     pdl_wait();  // u and the tet states come from the previous kernels
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) {  // one node per thread
+    const uint8_t act0 = has0 ? __ldcg(d.state + e0) : (uint8_t)0;
+    if (tid < nn) {  // one node per thread
+        const double4 w = ldcg256(u + k0);
+        U[tid] = w.x;
+        U[un + tid] = w.y;
+        U[2 * un + tid] = w.z;
+    }
+    for (int i = tid + nthr; i < nn; i += nthr) {
         const double4 w = ldcg256(u + __ldg(d.nlb + n0 + i));
         U[i] = w.x;
         U[un + i] = w.y;
         U[2 * un + i] = w.z;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
+    // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so adding
+    // +0.0 is bit-identical to skipping the entry.
+    if (act0) {
+        grad0(g0);
+        tau_row(T, tn, tid, U, un, g0, V0, lc0);
+    } else if (tid <= nt) {
+        zero_row(T, tn, tid);
+    }
+    for (int i = tid + nthr; i <= nt; i += nthr) {
         const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
+        double g[4][3], V;
+        load_geo(d, e, g, V);
+        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + min(i, nt - 1));
         if (i == nt || !__ldcg(d.state + e)) {
-            // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so
-            // adding +0.0 is bit-identical to skipping the entry.
-#pragma unroll
-            for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
+            zero_row(T, tn, i);
             continue;
         }
-        const double *gp = geo_ptr(d, e);
-        double g[4][3];
-#pragma unroll
-        for (int a = 1; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
-#pragma unroll
-        for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-        const double V = __ldg(gp);
-        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i);
-        const int li[4] = {lc.x, lc.y, lc.z, lc.w};
-        double ex = 0.0, ey = 0.0, ez = 0.0, gxy = 0.0, gyz = 0.0, gxz = 0.0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const double ux = U[li[a]], uy = U[un + li[a]], uz = U[2 * un + li[a]];
-            const double gx = g[a][0], gy = g[a][1], gz = g[a][2];
-            ex = ex + gx * ux;
-            ey = ey + gy * uy;
-            ez = ez + gz * uz;
-            gxy = gxy + (gy * ux + gx * uy);
-            gyz = gyz + (gz * uy + gy * uz);
-            gxz = gxz + (gz * ux + gx * uz);
-        }
-        T[i] = V * ex;
-        T[tn + i] = V * ey;
-        T[2 * tn + i] = V * ez;
-        T[3 * tn + i] = V * gxy;
-        T[4 * tn + i] = V * gyz;
-        T[5 * tn + i] = V * gxz;
-        T[6 * tn + i] = V;
+        grad0(g);
+        tau_row(T, tn, i, U, un, g, V, lc);
     }
-    __syncthreads();
-    const int64_t s = (int64_t)b * d.blk + threadIdx.x;
-    if (s >= d.S) return;
-    double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
+    const int64_t s = (int64_t)b * d.blk + tid;
+    const bool hs = s < d.S;
     const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
-    for (int w = 0; w < d.we; w += 8) {  // ELL row: 8 incidences per 16-B load, in order
-        const uint4 q = __ldg(row + (w >> 3));
+    uint4 q = hs ? __ldg(row) : make_uint4(0, 0, 0, 0);  // first 8 incidences, before the barrier
+    __syncthreads();
+    if (!hs) return;
+    double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
+    for (int w = 0;;) {  // ELL row: 8 incidences per 16-B load, in order
         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
         const int lim = d.we_max - w;  // warp-uniform: slots past the mesh's max incidence are skipped
 #pragma unroll
@@ -218,24 +267,22 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
             T4 = T4 + T[4 * tn + r];
             T5 = T5 + T[5 * tn + r];
         }
+        w += 8;
+        if (w >= d.we_max) break;  // (we_max <= we)
+        q = __ldg(row + (w >> 3));
     }
-    double4 *o = reinterpret_cast<double4 *>(d.srec + 8u * (uint32_t)s);
+    double *o = d.srec + 6u * (uint32_t)s;  // 48-B record, 16-B aligned
     if (Vh == 0.0) {
-        st256(o, 0.0, 0.0, 0.0, 0.0);
-        st256(o + 1, 0.0, 0.0, 0.0, 0.0);
+        st128(o, 0.0, 0.0);
+        st128(o + 2, 0.0, 0.0);
+        st128(o + 4, 0.0, 0.0);
         return;
     }
     const double inv = 1.0 / Vh;
     const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-    const double s0 = d.l2m * e11 + d.lam * (e22 + e33);
-    const double s1 = d.l2m * e22 + d.lam * (e11 + e33);
-    const double s2 = d.l2m * e33 + d.lam * (e11 + e22);
-    const double s3 = d.mu * g12, s4 = d.mu * g23, s5 = d.mu * g13;
-    const double r0 = fabs(s0) + fabs(s3) + fabs(s5);
-    const double r1 = fabs(s1) + fabs(s3) + fabs(s4);
-    const double r2 = fabs(s2) + fabs(s4) + fabs(s5);
-    st256(o, s0, s1, s2, s3);
-    st256(o + 1, s4, s5, fmax(r0, fmax(r1, r2)), 0.0);
+    st128(o, d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33));
+    st128(o + 2, d.l2m * e33 + d.lam * (e11 + e22), d.mu * g12);
+    st128(o + 4, d.mu * g23, d.mu * g13);
 }
 
 // ------------------------------------------------------------------ crack criterion (rare path)
@@ -365,7 +412,7 @@ __device__ __noinline__ void evaluate_tet(const Dev *__restrict__ dp, int64_t e,
     }
     Eig eg[6];
     for (int l = 0; l < 6; ++l) {
-        const double *sg = d.srec + 8 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
+        const double *sg = d.srec + 6 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
         double s6[6];
         for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
         principal(s6, eg[l]);
@@ -449,6 +496,21 @@ __device__ __noinline__ void criterion_full(const Dev *__restrict__ dp, int64_t 
 // (PAPER.md:L340-L367), written to the warp-tiled force slots.  Early-out (DESIGN.md
 // "Early-out"): every candidate satisfies |G| <= max_l g_{s(e,l)} * max_l |u_q - u_p|; tets
 // below Gc_e (1 - 1e-6) skip the 24-candidate evaluation.
+#ifndef CEM_C_KME
+#define CEM_C_KME 3
+#endif
+__device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double2 x, double2 y, double2 z) {
+    sm[i] = x.x;
+    sm[np + i] = x.y;
+    sm[2 * np + i] = y.x;
+    sm[3 * np + i] = y.y;
+    sm[4 * np + i] = z.x;
+    sm[5 * np + i] = z.y;
+    const double r0 = fabs(x.x) + fabs(y.y) + fabs(z.y);
+    const double r1 = fabs(x.y) + fabs(y.y) + fabs(z.x);
+    const double r2 = fabs(y.x) + fabs(z.x) + fabs(z.y);
+    sm[6 * np + i] = fmax(r0, fmax(r1, r2));
+}
 __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
                                         int32_t stamp, double *sm) {
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -460,45 +522,32 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int np = pstride(ne), nq = pstride(nn);
     double *smu = sm + 7 * np;
     // ---- wave 1: list indices
-    constexpr int kME = 2;  // sigma records per thread in flight (more -> tail loop)
+    constexpr int kME = CEM_C_KME;  // sigma records per thread in flight (more -> tail loop)
     uint32_t sid[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m) sid[m] = tid + m * nthr < ne ? (uint32_t)__ldg(d.el + s0i + tid + m * nthr) : 0u;
     const int32_t nid = (early && tid < nn) ? __ldg(d.nl + n0 + tid) : 0;
     pdl_wait();  // sigma records come from stage AB
-    // ---- wave 2: gathered records
-    double4 rx[kME], ry[kME];
+    // ---- wave 2: gathered records (3 x 16-B loads each) -> planes 0..5; plane 6 holds the
+    // Gershgorin bound g_s = max_i sum_j |sigma_ij| used by the early-out
+    double2 rx[kME], ry[kME], rz[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m)
         if (tid + m * nthr < ne) {
-            const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8u * sid[m]);
-            rx[m] = ldcg256(r);
-            ry[m] = ldcg256(r + 1);
+            const double *r = d.srec + 6u * sid[m];
+            rx[m] = ldcg128(r);
+            ry[m] = ldcg128(r + 2);
+            rz[m] = ldcg128(r + 4);
         }
     const double4 uw = (early && tid < nn) ? ldcg256(u + nid) : make_double4(0, 0, 0, 0);
 #pragma unroll
     for (int m = 0; m < kME; ++m) {
         const int i = tid + m * nthr;
-        if (i < ne) {
-            sm[i] = rx[m].x;
-            sm[np + i] = rx[m].y;
-            sm[2 * np + i] = rx[m].z;
-            sm[3 * np + i] = rx[m].w;
-            sm[4 * np + i] = ry[m].x;
-            sm[5 * np + i] = ry[m].y;
-            sm[6 * np + i] = ry[m].z;
-        }
+        if (i < ne) stage_sigma(sm, np, i, rx[m], ry[m], rz[m]);
     }
     for (int i = tid + kME * nthr; i < ne; i += nthr) {  // tail
-        const double4 *r = reinterpret_cast<const double4 *>(d.srec + 8u * (uint32_t)__ldg(d.el + s0i + i));
-        const double4 x = ldcg256(r), y = ldcg256(r + 1);
-        sm[i] = x.x;
-        sm[np + i] = x.y;
-        sm[2 * np + i] = x.z;
-        sm[3 * np + i] = x.w;
-        sm[4 * np + i] = y.x;
-        sm[5 * np + i] = y.y;
-        sm[6 * np + i] = y.z;
+        const double *r = d.srec + 6u * (uint32_t)__ldg(d.el + s0i + i);
+        stage_sigma(sm, np, i, ldcg128(r), ldcg128(r + 2), ldcg128(r + 4));
     }
     if (early) {
         if (tid < nn) {
@@ -513,16 +562,31 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
             smu[2 * nq + i] = w.z;
         }
     }
-    __syncthreads();
+    // this thread's tet: state and static tables issued before the barrier, so their latency
+    // overlaps the other warps' staging
     const int64_t e = (int64_t)b * d.blk + threadIdx.x;
-    if (e >= d.E) return;
-    double4 *fo = d.fe + (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));  // slot (e,a) = fo + 32 a
-    if (!__ldcg(d.state + e)) {
+    const bool he = e < d.E;
+    const uint8_t act = he ? __ldcg(d.state + e) : (uint8_t)0;
+    uint4 lq = make_uint4(0, 0, 0, 0);
+    double g[4][3], cc = 0.0;
+    if (he) {
+        lq = __ldg(reinterpret_cast<const uint4 *>(d.ledge) + e);
+        const double *gp = geo_ptr(d, (uint32_t)e);
+#pragma unroll
+        for (int a = 1; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
+        cc = __ldg(gp + 32);
+    }
+    __syncthreads();
+    if (!he) return;
+    // slot (e,a) = fo + 32 a (x, y, z, 0): one 32-B sector per slot
+    double4 *fo = d.fe + (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));
+    if (!act) {
 #pragma unroll
         for (int a = 0; a < 4; ++a) st256(fo + 32 * a, 0.0, 0.0, 0.0, 0.0);
         return;
     }
-    const uint4 lq = __ldg(reinterpret_cast<const uint4 *>(d.ledge) + e);
     const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
                        (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
     double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
@@ -537,15 +601,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         S5 = S5 + sm[5 * np + r];
         gmax = fmax(gmax, sm[6 * np + r]);
     }
-    const double *gp = geo_ptr(d, e);
-    double g[4][3];
-#pragma unroll
-    for (int a = 1; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-    const double cc = __ldg(gp + 32);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
@@ -580,85 +637,78 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 }
 
 // ------------------------------------------------------------------ stage D: node update
-// f_int,k = sum over the node's ELL row of force slots (ascending original tet id, -1 = end);
-// slot indices are loaded 8 at a time and the 8 record loads issued together.
-__device__ __forceinline__ void block_D(const Dev &d, int b, const double4 *u1p, double4 *u2p, int64_t s) {
-    const int64_t k = (int64_t)b * d.blk + threadIdx.x;
+// Four lanes per node, lane c = component c (lane 3 carries the zero w component): the three
+// component sums f_int,k,c = sum over the node's ELL row of force-slot components (ascending
+// original tet id) are independent, so splitting them across lanes keeps every sum sequential
+// in the oracle's order while a warp reads whole 32-B slot sectors with 8-B loads and holds
+// 4x fewer registers per slot in flight.  Newmark + BC are per component as well.
+__device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
+    const int c = threadIdx.x & 3;
+    const int64_t k = kbase + (threadIdx.x >> 2);
     if (k >= d.N) return;
     const uint8_t fl = __ldg(&d.nflag[k]);
     if (fl & 16) return;  // multi-GPU: another rank owns (and updates) this node
+    // static tables before the dependency wait (overlaps the previous stage's tail)
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
+    int4 qa = __ldg(row), qb = __ldg(row + 1);
+    const double fxc = (fl & 8) ? __ldg(reinterpret_cast<const double *>(d.fext + k) + c) : 0.0;
+    const double vb0 = (fl & 7) ? __ldg(reinterpret_cast<const double *>(d.dir_v0 + k) + c) : 0.0;
     pdl_wait();  // force slots come from stage C
-    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    for (int w = 0; w < d.wn; w += 8) {
+    const double *fec = reinterpret_cast<const double *>(d.fe) + c;  // lane c: component c of each slot
+    double f = 0.0;
+    for (int w = 0;;) {
         // padding entries point at an all-zero slot: adding +0.0 is an exact no-op here
-        const int4 qa = __ldg(row + (w >> 2)), qb = __ldg(row + (w >> 2) + 1);
         const int32_t sl[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-        double4 f[8];
+        double x[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) f[t] = ldcg256(d.fe + (uint32_t)sl[t]);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            f0 = f0 + f[t].x;
-            f1 = f1 + f[t].y;
-            f2 = f2 + f[t].z;
+        for (int t = 0; t < 8; ++t) x[t] = __ldcg(fec + 4u * (uint32_t)sl[t]);
+        w += 8;
+        const bool more = sl[7] != d.zslot && w < d.wn;
+        if (more) {
+            qa = __ldg(row + (w >> 2));
+            qb = __ldg(row + (w >> 2) + 1);
         }
-        if (sl[7] == d.zslot) break;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) f = f + x[t];
+        if (!more) break;
     }
     double mk = __ldcg(d.mass + k);
-    const double4 u1 = ldcg256(&u1p[k]);
-    const double4 v = ldcg256(&d.v[k]), a = ldcg256(&d.a[k]);
+    const double u1 = __ldcg(reinterpret_cast<const double *>(u1p + k) + c);
+    double vv = __ldcg(reinterpret_cast<const double *>(d.v + k) + c);
+    double aa = __ldcg(reinterpret_cast<const double *>(d.a + k) + c);
     const double dt = d.dt;
-    double fx = 0.0, fy = 0.0, fz = 0.0;
-    if (fl & 8) {
-        const double4 w = ldro4(&d.fext[k]);
-        fx = w.x; fy = w.y; fz = w.z;
-    }
-    double vv[3] = {v.x, v.y, v.z}, aa[3] = {a.x, a.y, a.z};
-    const double fi[3] = {f0, f1, f2}, fe3[3] = {fx, fy, fz};
-    double vb0[3] = {0.0, 0.0, 0.0};
-    if (fl & 7) {
-        const double4 w = ldro4(&d.dir_v0[k]);
-        vb0[0] = w.x; vb0[1] = w.y; vb0[2] = w.z;
-    }
     const double t1 = (double)(s + 1) * dt;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        if (mk == 0.0) {  // frozen node (R15)
-            vv[c] = 0.0;
-            aa[c] = 0.0;
-        } else if (fl >> c & 1) {  // prescribed velocity ramp (R17)
-            const double t0 = d.t0, v0 = vb0[c];
-            if (t0 <= 0.0) {
-                vv[c] = v0;
-                aa[c] = 0.0;
-            } else {
-                vv[c] = (t1 <= t0) ? (t1 / t0) * v0 : v0;
-                aa[c] = (t1 < t0) ? v0 / t0 : 0.0;
-            }
-        } else {  // a = (f_ext - f_int)/m ; v += dt ((1-gamma) a_old + gamma a_new)
-            const double an = (fe3[c] - fi[c]) / mk;
-            vv[c] = vv[c] + dt * (d.omg * aa[c] + d.gamma * an);
-            aa[c] = an;
+    if (c == 3) {
+        vv = aa = 0.0;
+    } else if (mk == 0.0) {  // frozen node (R15)
+        vv = 0.0;
+        aa = 0.0;
+    } else if (fl >> c & 1) {  // prescribed velocity ramp (R17)
+        const double t0 = d.t0;
+        if (t0 <= 0.0) {
+            vv = vb0;
+            aa = 0.0;
+        } else {
+            vv = (t1 <= t0) ? (t1 / t0) * vb0 : vb0;
+            aa = (t1 < t0) ? vb0 / t0 : 0.0;
         }
+    } else {  // a = (f_ext - f_int)/m ; v += dt ((1-gamma) a_old + gamma a_new)
+        const double an = (fxc - f) / mk;
+        vv = vv + dt * (d.omg * aa + d.gamma * an);
+        aa = an;
     }
     if (__ldcg(d.dirty + k) == (int32_t)(s + 1)) {
         // an incident tet split in this step: lumped mass from the active incidences;
         // m = 0 -> frozen, v = a = 0 (R15)
         mk = node_mass(d, k);
-        d.mass[k] = mk;
-        if (mk == 0.0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) vv[c] = aa[c] = 0.0;
-        }
+        if (c == 0) d.mass[k] = mk;
+        if (mk == 0.0) vv = aa = 0.0;
     }
-    st256(&d.v[k], vv[0], vv[1], vv[2], 0.0);
-    st256(&d.a[k], aa[0], aa[1], aa[2], 0.0);
+    reinterpret_cast<double *>(d.v + k)[c] = vv;
+    reinterpret_cast<double *>(d.a + k)[c] = aa;
     // predictor u_{s+2} = u_{s+1} + dt v + dt^2/2 a
-    st256(&u2p[k], (u1.x + dt * vv[0]) + d.hdt2 * aa[0], (u1.y + dt * vv[1]) + d.hdt2 * aa[1],
-          (u1.z + dt * vv[2]) + d.hdt2 * aa[2], 0.0);
-    if (!isfinite(u1.x) || !isfinite(u1.y) || !isfinite(u1.z) || !isfinite(vv[0]) || !isfinite(vv[1]) ||
-        !isfinite(vv[2]) || !isfinite(aa[0]) || !isfinite(aa[1]) || !isfinite(aa[2])) {
+    reinterpret_cast<double *>(u2p + k)[c] = c == 3 ? 0.0 : (u1 + dt * vv) + d.hdt2 * aa;
+    if (c < 3 && (!isfinite(u1) || !isfinite(vv) || !isfinite(aa))) {
         d.ctr[1] = 1;
         atomicMin(&d.ctr[2], ldro(d.node_orig + k));
     }
@@ -669,9 +719,9 @@ __device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
 }
 
 // ------------------------------------------------------------------ persistent wavefront kernel
-__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+__device__ __forceinline__ int ld_relaxed(const int32_t *p) {  // poll without invalidating L1
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -687,8 +737,8 @@ __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
     int64_t bytes, off;
     if (pg == ST_AB) {
         base = reinterpret_cast<const char *>(d.srec);
-        off = (int64_t)pb * d.blk * 64;
-        bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 64;
+        off = (int64_t)pb * d.blk * 48;
+        bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 48;
     } else {
         base = reinterpret_cast<const char *>(d.fe);
         off = (int64_t)pb * d.blk * 128;
@@ -728,18 +778,33 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
         if (tid < 32) {
             const int need = g == ST_AB ? (int)s : (int)(s + 1);
             const int32_t *c = d.cnt + (int64_t)pg * d.maxblk;
+            int polls = 0;
             for (int i = dlo + tid; i < dhi; i += 32) {
                 const int pb = __ldg(d.dep + i);
-                while (ld_acquire(c + pb) < need) __nanosleep(32);
+                while (ld_relaxed(c + pb) < need) {
+                    ++polls;
+                    __nanosleep(64);
+                }
             }
-            __syncwarp();  // produced data is read with .cg loads (L2): no L1 invalidation needed
+            __syncwarp();
+            if (tid == 0) __threadfence();  // one acquire-side fence per item (produced data is read via .cg)
+#ifdef CEM_POLL_STATS
+            polls = __reduce_add_sync(0xffffffffu, polls);
+            if (tid == 0) {
+                atomicAdd(&d.ctr[4 + g], polls);
+                if (polls) atomicAdd(&d.ctr[7], 1);
+            }
+#endif
         }
         __syncthreads();
         const double4 *u1 = d.ubuf[(s + 1) & 1];
         switch (g) {
             case ST_AB: block_AB(d, b, u1, sm); break;
             case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
-            default: block_D(d, b, u1, d.ubuf[s & 1], s); break;
+            default:
+                for (int j = 0; j < 4; ++j)  // a D item covers blk nodes, 4 lanes per node
+                    block_D(d, (int64_t)b * d.blk + j * (d.blk >> 2), u1, d.ubuf[s & 1], s);
+                break;
         }
         __syncthreads();
         if (g != ST_AB && !(d.flags & CEM_F_NO_DISCARD)) {
@@ -778,7 +843,7 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 #define CEM_C_MINB 4
 #endif
 #ifndef CEM_D_MINB
-#define CEM_D_MINB 3
+#define CEM_D_MINB 6
 #endif
 __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
     extern __shared__ __align__(16) double sm[];
@@ -792,7 +857,7 @@ __global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int cra
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     pdl_trigger();
-    block_D(d, blockIdx.x, d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+    block_D(d, (int64_t)blockIdx.x * (blockDim.x >> 2), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
 // criterion on the current state u_n (cem_crack_update)
@@ -821,6 +886,10 @@ __global__ void __launch_bounds__(256) k_fix_cur(Dev d, int64_t n, int32_t stamp
 }
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
+inline unsigned nblk_d(const Dev &d) {  // staged D: blk/4 nodes per CTA
+    const int64_t per = d.blk >> 2;
+    return (unsigned)((d.N + per - 1) / per);
+}
 
 }  // namespace
 
@@ -866,7 +935,7 @@ void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t s
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
         launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
         launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
-        launch_pdl(k_D, (unsigned)d.nblk[ST_D], (unsigned)d.blk, (size_t)0, st, d, s);
+        launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
         return;
     }
     if (ev) cudaEventRecord(ev[0], st);
@@ -874,7 +943,7 @@ void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t s
     if (ev) cudaEventRecord(ev[1], st);
     k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
     if (ev) cudaEventRecord(ev[2], st);
-    k_D<<<d.nblk[ST_D], d.blk, 0, st>>>(d, s);
+    k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     if (ev) cudaEventRecord(ev[3], st);
 }
 

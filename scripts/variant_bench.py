@@ -23,3 +23,12 @@ e1.record(sim.torch_stream)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / steps
 print(f"lib={os.path.basename(cem.LIB_PATH)} flags={flags} cfg={cfg}: {ms*1e3:.1f} us/step  {p.n_tets/ms/1e6:.2f} G tet-steps/s")
+if os.environ.get("CEM_STATS"):
+    sim.state()  # libcem built with -DCEM_POLL_STATS prints the dependency-poll counters here
+if os.environ.get("CEM_STAGES"):
+    sim.set_profiling(True)
+    sim.step(100, 1)
+    torch.cuda.synchronize()
+    kt = sim.kernel_times()
+    print("  stages (events between kernels, no PDL overlap): " +
+          ", ".join(f"{k.split('_')[1]} {v * 10:.1f} us" for k, v in kt.items()))
