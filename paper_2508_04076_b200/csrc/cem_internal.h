@@ -5,11 +5,27 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "../../include/cem.h"
 
 namespace cem {
+
+// phase timer of the host preprocessing (CEM_TIMING=1 prints to stderr)
+struct PhaseClock {
+    bool on = getenv("CEM_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[cem timing] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+        t = n;
+    }
+};
 
 // ---------------------------------------------------------------- host preprocessing
 // HostMesh holds the mesh in the caller's ("original") numbering (cem_mesh.cpp).
@@ -78,10 +94,6 @@ struct Plan {
     std::vector<int32_t> nlb_off, nlb;  // edge block -> sorted unique nodes of its tet list
     std::vector<uint16_t> tconn;      // [|tl|][4] node index (in nlb) of each tet-list entry
     std::vector<uint16_t> inc_local;  // [6E] (CSR order of edge_inc) index into the edge block's tet list
-    std::vector<int32_t> fpos;        // [E][4] slot of f_{e,a} in the node-major force array
-    std::vector<int32_t> gbase;       // [N/32 + 1] warp-interleaved force slots: node k = 32 g + lane,
-                                      //   its j-th incidence at gbase[g] + 32 j + lane
-    int64_t nslots = 0;
     int max_nl = 0, max_el = 0, max_tl = 0, max_nlb = 0;
     // instruction-lean layouts
     std::vector<double> geoT;         // [E/32][11][32]: V, V/6, gradN1..3 (x,y,z) per warp tile

@@ -568,8 +568,15 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const bool he = e < d.E;
     const uint8_t act = he ? __ldcg(d.state + e) : (uint8_t)0;
     uint4 lq = make_uint4(0, 0, 0, 0);
-    double g[4][3], cc = 0.0;
+    double g[4][3], cc = 0.0, gc = 0.0;
+    uint8_t tf = 0;
+    ushort4 lc = make_ushort4(0, 0, 0, 0);
     if (he) {
+        if (crack) {  // criterion inputs (static): issued with the rest, not after the force
+            tf = __ldg(d.tflag + e);
+            gc = ldro(d.gc + e);
+            if (early) lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
+        }
         lq = __ldg(reinterpret_cast<const uint4 *>(d.ledge) + e);
         const double *gp = geo_ptr(d, (uint32_t)e);
 #pragma unroll
@@ -611,11 +618,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         st256(fo + 32 * a, fx, fy, fz, 0.0);
     }
     if (!crack) return;
-    const uint8_t tf = __ldg(d.tflag + e);
     if (!(tf & 1)) return;  // ghost tet: its owner decides, the state arrives by exchange
-    const double gc = ldro(d.gc + e);
     if (early) {
-        const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
         const int li[4] = {lc.x, lc.y, lc.z, lc.w};
         double ux[4], uy[4], uz[4];
 #pragma unroll

@@ -2,6 +2,7 @@
 // lumped mass, traction force, time step.  Compiled with
 // -ffp-contract=off so every expression rounds exactly as written (DESIGN.md
 // "Association order"); OpenMP only over independent outputs.
+#include <parallel/algorithm>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -36,7 +37,7 @@ void edge_keys(const cem_mesh_in *m, std::vector<std::pair<uint64_t, int64_t>> &
             uint64_t lo = std::min(i, j), hi = std::max(i, j);
             k[6 * e + l] = {lo << 32 | hi, 6 * e + l};
         }
-    std::sort(k.begin(), k.end());
+    __gnu_parallel::sort(k.begin(), k.end());  // keys are unique pairs: the order is total
 }
 
 }  // namespace
@@ -126,6 +127,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         h.state[e] = m->tet_state ? (m->tet_state[e] != 0) : 1;
         h.gc[e] = m->tet_gc ? m->tet_gc[e] : mat->Gc;
     }
+    PhaseClock clk;
     // ---------------------------------------------------------------- validation
     for (int64_t e = 0; e < E; ++e) {
         const int32_t *t = m->tets + 4 * e;
@@ -154,6 +156,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         }
     const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
     const double vtol = 1e-14 * ext * ext * ext;
+    clk.mark("mesh: validation");
     // ---------------------------------------------------------------- geometry
     // det = d1.(d2 x d3), V = det/6, inv = 1/det, gradN1 = (d2xd3) inv, gradN2 = (d3xd1) inv,
     // gradN3 = (d1xd2) inv, gradN0 = -((gradN1 + gradN2) + gradN3)
@@ -197,6 +200,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         err = "tet " + std::to_string(bad_deg) + ": degenerate (|V| < 1e-14 bbox^3)";
         return CEM_EDEGENERATE;
     }
+    clk.mark("mesh: geometry");
     // ---------------------------------------------------------------- duplicate tets
     {
         std::vector<std::pair<uint64_t, uint64_t>> tk(E);
@@ -207,13 +211,14 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
             std::sort(v, v + 4);
             tk[e] = {((uint64_t)(uint32_t)v[0] << 32) | (uint32_t)v[1], ((uint64_t)(uint32_t)v[2] << 32) | (uint32_t)v[3]};
         }
-        std::sort(tk.begin(), tk.end());
+        __gnu_parallel::sort(tk.begin(), tk.end());
         for (int64_t e = 1; e < E; ++e)
             if (tk[e] == tk[e - 1]) {
                 err = "duplicate tets (same node set)";
                 return CEM_ETOPOLOGY;
             }
     }
+    clk.mark("mesh: duplicate tets");
     // ---------------------------------------------------------------- edges (ES-FEM smoothing domains)
     {
         std::vector<std::pair<uint64_t, int64_t>> k;
@@ -239,6 +244,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         }
         h.edge_off[S] = (int32_t)k.size();
     }
+    clk.mark("mesh: edges");
     // ---------------------------------------------------------------- node incidence (ascending e)
     h.node_off.assign(N + 1, 0);
     for (int64_t i = 0; i < 4 * E; ++i) h.node_off[m->tets[i] + 1]++;
@@ -311,6 +317,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         h.any_dirichlet = true;
         h.t0 = ld->vbc_t0;
     }
+    clk.mark("mesh: incidence/mass/loads");
     // ---------------------------------------------------------------- time step (R12)
     double dt = o ? o->dt : 0.0;
     if (!(dt > 0)) {

@@ -15,9 +15,144 @@
 
 namespace cem {
 
+namespace {
+
+// ---------------------------------------------------------------- bank-aware row placement
+// The stage kernels gather fp64 rows from shared-memory planes.  For 8-byte loads a half-warp
+// (16 lanes) is served per pass; two lanes reading different rows r != r' with r = r' (mod 16)
+// hit the same bank pair and serialise.  Given the groups of items one half-warp instruction
+// reads together, colour every item with k = row mod 16 so that a group's items get distinct
+// colours where possible (greedy, most-constrained item first, then a swap pass that lowers
+// sum_g sum_k cnt[g][k]^2).  Colour capacities are exact, so rows stay 0..n-1; inside a colour
+// items keep ascending order (gather locality).  Returns row[item].
+void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_t> &gitem, std::vector<int32_t> &row) {
+    row.assign(n, 0);
+    if (n <= 16) {
+        std::iota(row.begin(), row.end(), 0);
+        return;
+    }
+    const int ng = (int)goff.size() - 1;
+    std::vector<int32_t> moff(n + 1, 0), mem;
+    for (int g = 0; g < ng; ++g)
+        for (int32_t i = goff[g]; i < goff[g + 1]; ++i) moff[gitem[i] + 1]++;
+    for (int i = 0; i < n; ++i) moff[i + 1] += moff[i];
+    mem.resize(moff[n]);
+    {
+        std::vector<int32_t> f(moff.begin(), moff.end() - 1);
+        for (int g = 0; g < ng; ++g)
+            for (int32_t i = goff[g]; i < goff[g + 1]; ++i) mem[f[gitem[i]]++] = g;
+    }
+    std::vector<int32_t> cnt((size_t)ng * 16, 0), col(n, -1), cap(16);
+    for (int k = 0; k < 16; ++k) cap[k] = n / 16 + (k < n % 16 ? 1 : 0);
+    std::vector<int32_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return moff[a + 1] - moff[a] > moff[b + 1] - moff[b]; });
+    for (int it : order) {
+        int best = -1;
+        long bc = 0;
+        for (int k = 0; k < 16; ++k) {
+            if (!cap[k]) continue;
+            long c = 0;
+            for (int32_t j = moff[it]; j < moff[it + 1]; ++j) c += cnt[(size_t)mem[j] * 16 + k];
+            c = c * 1024 - cap[k];
+            if (best < 0 || c < bc) best = k, bc = c;
+        }
+        col[it] = best;
+        cap[best]--;
+        for (int32_t j = moff[it]; j < moff[it + 1]; ++j) cnt[(size_t)mem[j] * 16 + best]++;
+    }
+    // swap pass: move a to its best colour k, b (colour k) to a's colour, if the sum of squares drops
+    std::vector<std::vector<int32_t>> byc(16);
+    for (int i = 0; i < n; ++i) byc[col[i]].push_back(i);
+    auto move_delta = [&](int it, int from, int to) {  // change of sum cnt^2 when `it` moves
+        long dd = 0;
+        for (int32_t j = moff[it]; j < moff[it + 1]; ++j) {
+            const int32_t *c = &cnt[(size_t)mem[j] * 16];
+            dd += 2L * (c[to] - c[from] + 1);
+        }
+        return dd;
+    };
+    auto apply = [&](int it, int from, int to) {
+        for (int32_t j = moff[it]; j < moff[it + 1]; ++j) {
+            cnt[(size_t)mem[j] * 16 + from]--;
+            cnt[(size_t)mem[j] * 16 + to]++;
+        }
+        col[it] = to;
+    };
+    for (int pass = 0; pass < 1; ++pass) {
+        bool any = false;
+        for (int a = 0; a < n; ++a) {
+            const int ka = col[a];
+            int kb = -1;
+            long da = 0;
+            for (int k = 0; k < 16; ++k) {
+                if (k == ka) continue;
+                const long d = move_delta(a, ka, k);
+                if (kb < 0 || d < da) kb = k, da = d;
+            }
+            if (da >= 0) continue;
+            apply(a, ka, kb);
+            int bb = -1;
+            long db = 0;
+            for (int b : byc[kb]) {
+                if (b == a) continue;
+                const long d = move_delta(b, kb, ka);
+                if (bb < 0 || d < db) bb = b, db = d;
+            }
+            if (bb >= 0 && da + db < 0) {
+                apply(bb, kb, ka);
+                auto &A = byc[ka], &B = byc[kb];
+                A.erase(std::find(A.begin(), A.end(), a));
+                B.erase(std::find(B.begin(), B.end(), bb));
+                A.push_back(bb);
+                B.push_back(a);
+                any = true;
+            } else {
+                apply(a, kb, ka);  // undo
+            }
+        }
+        if (!any) break;
+    }
+    for (int k = 0; k < 16; ++k) {
+        auto &v = byc[k];
+        std::sort(v.begin(), v.end());
+        for (size_t q = 0; q < v.size(); ++q) row[v[q]] = (int32_t)(16 * q + k);
+    }
+}
+
+// groups of the items read together: lanes [h0, h0+16) x column l of tab (row stride `stride`)
+template <class T>
+void half_warp_groups(const T *tab, int64_t lo, int64_t hi, int stride, int width, std::vector<int32_t> &goff,
+                      std::vector<int32_t> &gitem, int skip = -1) {
+    goff.assign(1, 0);
+    gitem.clear();
+    for (int64_t h0 = lo; h0 < hi; h0 += 16)
+        for (int l = 0; l < width; ++l) {
+            const size_t st = gitem.size();
+            for (int64_t i = h0; i < std::min<int64_t>(hi, h0 + 16); ++i) {
+                const int v = (int)tab[(int64_t)stride * i + l];
+                if (v != skip) gitem.push_back(v);
+            }
+            std::sort(gitem.begin() + st, gitem.end());
+            gitem.erase(std::unique(gitem.begin() + st, gitem.end()), gitem.end());
+            goff.push_back((int32_t)gitem.size());
+        }
+}
+
+// reorder list[off..off+n) so that item i moves to row[i]
+template <class T>
+void permute_rows(T *list, int n, const std::vector<int32_t> &row) {
+    std::vector<T> tmp(list, list + n);
+    for (int i = 0; i < n; ++i) list[row[i]] = tmp[i];
+}
+
+}  // namespace
+
 void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) {
     const int64_t N = h.N, E = h.E, S = h.S;
     p.blk = blk;
+    PhaseClock clk;
     // ---------------------------------------------------------------- sweep axis + slabs
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int64_t n = 0; n < N; ++n)
@@ -37,6 +172,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     const int kSlab = 4;
     std::vector<double> cen(3 * E);
     std::vector<int64_t> key(E);
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < E; ++e) {
         for (int c = 0; c < 3; ++c) {
             double x = 0.0;
@@ -51,11 +187,15 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
                      [&](int32_t x, int32_t y) { return key[x] < key[y]; });
     {
         const int64_t leaf = std::max(1, blk / 2);
-        std::vector<std::pair<int64_t, int64_t>> stack;
-        int64_t i0 = 0;
-        while (i0 < E) {  // one slab at a time
-            int64_t i1 = i0;
-            while (i1 < E && key[p.tet_new2old[i1]] == key[p.tet_new2old[i0]]) ++i1;
+        std::vector<int64_t> slab0;  // slab boundaries in the key-sorted order
+        for (int64_t i = 0; i < E; ++i)
+            if (i == 0 || key[p.tet_new2old[i]] != key[p.tet_new2old[i - 1]]) slab0.push_back(i);
+        slab0.push_back(E);
+        const int64_t nslab = (int64_t)slab0.size() - 1;
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t sl = 0; sl < nslab; ++sl) {  // slabs are independent
+            std::vector<std::pair<int64_t, int64_t>> stack;
+            const int64_t i0 = slab0[sl], i1 = slab0[sl + 1];
             stack.push_back({i0, i1});
             while (!stack.empty()) {
                 auto [a0, a1] = stack.back();
@@ -79,11 +219,11 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
                 stack.push_back({mid, a1});  // right half processed after the left half
                 stack.push_back({a0, mid});
             }
-            i0 = i1;
         }
     }
     p.tet_old2new.assign(E, -1);
     for (int64_t e = 0; e < E; ++e) p.tet_old2new[p.tet_new2old[e]] = (int32_t)e;
+    clk.mark("plan: tet order");
     // nodes and edges by first appearance
     p.node_old2new.assign(N, -1);
     p.node_new2old.clear();
@@ -113,6 +253,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             p.node_old2new[k] = (int32_t)p.node_new2old.size();
             p.node_new2old.push_back((int32_t)k);
         }
+    clk.mark("plan: node/edge order");
     // ---------------------------------------------------------------- storage-order tables
     p.conn.resize(4 * E);
     p.geoV.resize(E);
@@ -122,6 +263,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     p.state.resize(E);
     p.tflag.resize(E);
     p.gc.resize(E);
+#pragma omp parallel for schedule(static)
     for (int64_t en = 0; en < E; ++en) {
         const int64_t eo = p.tet_new2old[en];
         for (int a = 0; a < 4; ++a) p.conn[4 * en + a] = p.node_old2new[h.tet[4 * eo + a]];
@@ -135,113 +277,166 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         p.gc[en] = h.gc[eo];
     }
     p.edge_off.assign(S + 1, 0);
-    p.edge_inc.resize(h.edge_inc.size());
-    for (int64_t sn = 0, j = 0; sn < S; ++sn) {
+    for (int64_t sn = 0; sn < S; ++sn) {
         const int32_t so = p.edge_new2old[sn];
-        p.edge_off[sn] = (int32_t)j;
+        p.edge_off[sn + 1] = p.edge_off[sn] + (h.edge_off[so + 1] - h.edge_off[so]);
+    }
+    p.edge_inc.resize(h.edge_inc.size());
+#pragma omp parallel for schedule(static)
+    for (int64_t sn = 0; sn < S; ++sn) {
+        const int32_t so = p.edge_new2old[sn];
+        int32_t j = p.edge_off[sn];
         for (int32_t i = h.edge_off[so]; i < h.edge_off[so + 1]; ++i) p.edge_inc[j++] = p.tet_old2new[h.edge_inc[i]];
-        p.edge_off[sn + 1] = (int32_t)j;
     }
     p.node_off.assign(N + 1, 0);
-    p.node_ent.resize(h.node_ent.size());
-    for (int64_t kn = 0, j = 0; kn < N; ++kn) {
+    for (int64_t kn = 0; kn < N; ++kn) {
         const int32_t ko = p.node_new2old[kn];
-        p.node_off[kn] = (int32_t)j;
+        p.node_off[kn + 1] = p.node_off[kn] + (h.node_off[ko + 1] - h.node_off[ko]);
+    }
+    p.node_ent.resize(h.node_ent.size());
+#pragma omp parallel for schedule(static)
+    for (int64_t kn = 0; kn < N; ++kn) {
+        const int32_t ko = p.node_new2old[kn];
+        int32_t j = p.node_off[kn];
         for (int32_t i = h.node_off[ko]; i < h.node_off[ko + 1]; ++i) {
             const int32_t ent = h.node_ent[i];
             p.node_ent[j++] = (p.tet_old2new[ent >> 2] << 2) | (ent & 3);
         }
-        p.node_off[kn + 1] = (int32_t)j;
     }
+    clk.mark("plan: storage tables");
     // ---------------------------------------------------------------- gather lists
     {
         const int nbt = (int)((E + blk - 1) / blk), nbs = (int)((S + blk - 1) / blk);
-        p.nl_off.assign(nbt + 1, 0);
-        p.el_off.assign(nbt + 1, 0);
-        p.nl.clear();
-        p.el.clear();
+        // per-block lists built in parallel, then concatenated
+        auto concat = [](std::vector<std::vector<int32_t>> &parts, std::vector<int32_t> &off, std::vector<int32_t> &out,
+                         int &mx) {
+            off.assign(parts.size() + 1, 0);
+            mx = 0;
+            for (size_t b = 0; b < parts.size(); ++b) {
+                off[b + 1] = off[b] + (int32_t)parts[b].size();
+                mx = std::max(mx, (int)parts[b].size());
+            }
+            out.resize(off.back());
+#pragma omp parallel for schedule(static)
+            for (int64_t b = 0; b < (int64_t)parts.size(); ++b) std::copy(parts[b].begin(), parts[b].end(), out.begin() + off[b]);
+        };
         p.lconn.assign(4 * E, 0);
         p.ledge.assign(8 * E, 0);
-        p.max_nl = p.max_el = p.max_tl = 0;
-        std::vector<int32_t> tmp;
-        for (int b = 0; b < nbt; ++b) {
-            const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
-            tmp.assign(p.conn.begin() + 4 * e0, p.conn.begin() + 4 * e1);
-            std::sort(tmp.begin(), tmp.end());
-            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-            for (int64_t e = e0; e < e1; ++e)
-                for (int a = 0; a < 4; ++a)
-                    p.lconn[4 * e + a] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.conn[4 * e + a]) - tmp.begin());
-            p.nl.insert(p.nl.end(), tmp.begin(), tmp.end());
-            p.nl_off[b + 1] = (int32_t)p.nl.size();
-            p.max_nl = std::max(p.max_nl, (int)tmp.size());
-            tmp.clear();
-            for (int64_t e = e0; e < e1; ++e)
-                for (int l = 0; l < 6; ++l) tmp.push_back(p.eedge[(int64_t)l * E + e]);
-            std::sort(tmp.begin(), tmp.end());
-            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-            for (int64_t e = e0; e < e1; ++e)
-                for (int l = 0; l < 6; ++l)
-                    p.ledge[8 * e + l] =
-                        (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.eedge[(int64_t)l * E + e]) - tmp.begin());
-            p.el.insert(p.el.end(), tmp.begin(), tmp.end());
-            p.el_off[b + 1] = (int32_t)p.el.size();
-            p.max_el = std::max(p.max_el, (int)tmp.size());
+        {
+            std::vector<std::vector<int32_t>> nlv(nbt), elv(nbt);
+#pragma omp parallel for schedule(dynamic, 16)
+            for (int b = 0; b < nbt; ++b) {
+                const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
+                auto &tn = nlv[b];
+                tn.assign(p.conn.begin() + 4 * e0, p.conn.begin() + 4 * e1);
+                std::sort(tn.begin(), tn.end());
+                tn.erase(std::unique(tn.begin(), tn.end()), tn.end());
+                for (int64_t e = e0; e < e1; ++e)
+                    for (int a = 0; a < 4; ++a)
+                        p.lconn[4 * e + a] = (uint16_t)(std::lower_bound(tn.begin(), tn.end(), p.conn[4 * e + a]) - tn.begin());
+                auto &te = elv[b];
+                for (int64_t e = e0; e < e1; ++e)
+                    for (int l = 0; l < 6; ++l) te.push_back(p.eedge[(int64_t)l * E + e]);
+                std::sort(te.begin(), te.end());
+                te.erase(std::unique(te.begin(), te.end()), te.end());
+                for (int64_t e = e0; e < e1; ++e)
+                    for (int l = 0; l < 6; ++l)
+                        p.ledge[8 * e + l] =
+                            (uint16_t)(std::lower_bound(te.begin(), te.end(), p.eedge[(int64_t)l * E + e]) - te.begin());
+            }
+            concat(nlv, p.nl_off, p.nl, p.max_nl);
+            concat(elv, p.el_off, p.el, p.max_el);
         }
-        p.tl_off.assign(nbs + 1, 0);
-        p.tl.clear();
         p.inc_local.assign(p.edge_inc.size(), 0);
-        for (int b = 0; b < nbs; ++b) {
-            const int64_t s0 = (int64_t)b * blk, s1 = std::min<int64_t>(S, s0 + blk);
-            tmp.assign(p.edge_inc.begin() + p.edge_off[s0], p.edge_inc.begin() + p.edge_off[s1]);
-            std::sort(tmp.begin(), tmp.end());
-            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-            for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j)
-                p.inc_local[j] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.edge_inc[j]) - tmp.begin());
-            p.tl.insert(p.tl.end(), tmp.begin(), tmp.end());
-            p.tl_off[b + 1] = (int32_t)p.tl.size();
-            p.max_tl = std::max(p.max_tl, (int)tmp.size());
+        {
+            std::vector<std::vector<int32_t>> tlv(nbs);
+#pragma omp parallel for schedule(dynamic, 16)
+            for (int b = 0; b < nbs; ++b) {
+                const int64_t s0 = (int64_t)b * blk, s1 = std::min<int64_t>(S, s0 + blk);
+                auto &tmp = tlv[b];
+                tmp.assign(p.edge_inc.begin() + p.edge_off[s0], p.edge_inc.begin() + p.edge_off[s1]);
+                std::sort(tmp.begin(), tmp.end());
+                tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+                for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j)
+                    p.inc_local[j] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.edge_inc[j]) - tmp.begin());
+            }
+            concat(tlv, p.tl_off, p.tl, p.max_tl);
         }
+        clk.mark("plan: gather lists");
+        // bank-aware order of each edge block's tet list: lanes = edges, column t = t-th incidence
+        {
+            std::vector<uint16_t> incw((size_t)S * 8, 0xFFFF);  // first 8 incidences per edge (ELL view)
+            for (int64_t s = 0; s < S; ++s)
+                for (int32_t j = p.edge_off[s]; j < std::min(p.edge_off[s + 1], p.edge_off[s] + 8); ++j)
+                    incw[8 * s + (j - p.edge_off[s])] = p.inc_local[j];
+            int wmax = 1;
+            for (int64_t s = 0; s < S; ++s) wmax = std::max(wmax, p.edge_off[s + 1] - p.edge_off[s]);
+            wmax = std::min(wmax, 8);
+#pragma omp parallel for schedule(dynamic, 16)
+            for (int b = 0; b < nbs; ++b) {
+                std::vector<int32_t> goff, gitem, row;
+                const int64_t s0 = (int64_t)b * blk, s1 = std::min<int64_t>(S, s0 + blk);
+                const int nt = p.tl_off[b + 1] - p.tl_off[b];
+                half_warp_groups(incw.data(), s0, s1, 8, wmax, goff, gitem, 0xFFFF);
+                bank_rows(nt, goff, gitem, row);
+                permute_rows(p.tl.data() + p.tl_off[b], nt, row);
+                for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j) p.inc_local[j] = (uint16_t)row[p.inc_local[j]];
+            }
+        }
+        clk.mark("plan: bank order (tets)");
         // nodes of each edge block's tet list (the fused AB stage recomputes tau from them)
-        p.nlb_off.assign(nbs + 1, 0);
-        p.nlb.clear();
         p.tconn.assign(4 * p.tl.size(), 0);
-        p.max_nlb = 0;
-        std::vector<int32_t> nodes;
+        {
+            std::vector<std::vector<int32_t>> nbv(nbs);
+#pragma omp parallel for schedule(dynamic, 16)
+            for (int b = 0; b < nbs; ++b) {
+                auto &nodes = nbv[b];
+                for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
+                    for (int a = 0; a < 4; ++a) nodes.push_back(p.conn[4 * (int64_t)p.tl[i] + a]);
+                std::sort(nodes.begin(), nodes.end());
+                nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+                for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
+                    for (int a = 0; a < 4; ++a)
+                        p.tconn[4 * (int64_t)i + a] = (uint16_t)(std::lower_bound(nodes.begin(), nodes.end(),
+                                                                                   p.conn[4 * (int64_t)p.tl[i] + a]) - nodes.begin());
+            }
+            concat(nbv, p.nlb_off, p.nlb, p.max_nlb);
+        }
+        clk.mark("plan: AB node lists");
+        // bank-aware order of the staged node lists: AB (lanes = tet-list rows, column a) and
+        // C's early-out (lanes = tets, column a); C's edge lists (lanes = tets, column l)
+#pragma omp parallel for schedule(dynamic, 16)
         for (int b = 0; b < nbs; ++b) {
-            nodes.clear();
-            for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
-                for (int a = 0; a < 4; ++a) nodes.push_back(p.conn[4 * (int64_t)p.tl[i] + a]);
-            std::sort(nodes.begin(), nodes.end());
-            nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
-            for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
-                for (int a = 0; a < 4; ++a)
-                    p.tconn[4 * (int64_t)i + a] = (uint16_t)(std::lower_bound(nodes.begin(), nodes.end(),
-                                                                               p.conn[4 * (int64_t)p.tl[i] + a]) - nodes.begin());
-            p.nlb.insert(p.nlb.end(), nodes.begin(), nodes.end());
-            p.nlb_off[b + 1] = (int32_t)p.nlb.size();
-            p.max_nlb = std::max(p.max_nlb, (int)nodes.size());
+            std::vector<int32_t> goff, gitem, row;
+            const int32_t t0 = p.tl_off[b];
+            const int nt = p.tl_off[b + 1] - t0, nn = p.nlb_off[b + 1] - p.nlb_off[b];
+            half_warp_groups(p.tconn.data() + 4 * (int64_t)t0, 0, nt, 4, 4, goff, gitem);
+            bank_rows(nn, goff, gitem, row);
+            permute_rows(p.nlb.data() + p.nlb_off[b], nn, row);
+            for (int64_t i = 4 * (int64_t)t0; i < 4 * (int64_t)(t0 + nt); ++i) p.tconn[i] = (uint16_t)row[p.tconn[i]];
         }
-        // node-major force slots, interleaved per warp of 32 consecutive nodes so that the
-        // lanes of stage D read 32 consecutive slots per incidence index j
-        const int64_t ng = (N + 31) / 32;
-        p.gbase.assign(ng + 1, 0);
-        for (int64_t g = 0; g < ng; ++g) {
-            int32_t mx = 0;
-            for (int64_t k = 32 * g; k < std::min<int64_t>(N, 32 * g + 32); ++k) mx = std::max(mx, p.node_off[k + 1] - p.node_off[k]);
-            p.gbase[g + 1] = p.gbase[g] + 32 * mx;
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int b = 0; b < nbt; ++b) {
+            std::vector<int32_t> goff, gitem, row;
+            const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
+            const int ne = p.el_off[b + 1] - p.el_off[b], nn = p.nl_off[b + 1] - p.nl_off[b];
+            half_warp_groups(p.ledge.data(), e0, e1, 8, 6, goff, gitem);
+            bank_rows(ne, goff, gitem, row);
+            permute_rows(p.el.data() + p.el_off[b], ne, row);
+            for (int64_t e = e0; e < e1; ++e)
+                for (int l = 0; l < 6; ++l) p.ledge[8 * e + l] = (uint16_t)row[p.ledge[8 * e + l]];
+            half_warp_groups(p.lconn.data(), e0, e1, 4, 4, goff, gitem);
+            bank_rows(nn, goff, gitem, row);
+            permute_rows(p.nl.data() + p.nl_off[b], nn, row);
+            for (int64_t i = 4 * e0; i < 4 * e1; ++i) p.lconn[i] = (uint16_t)row[p.lconn[i]];
         }
-        p.nslots = 4 * E;  // tet-major force records (node_ent (e<<2|a) indexes them directly)
-        p.fpos.assign(4 * E, -1);
-        for (int64_t k = 0; k < N; ++k)
-            for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j)
-                p.fpos[4 * (int64_t)(p.node_ent[j] >> 2) + (p.node_ent[j] & 3)] =
-                    p.gbase[k / 32] + 32 * (j - p.node_off[k]) + (int32_t)(k % 32);
+        clk.mark("plan: bank order (nodes, edges)");
     }
     // ---------------------------------------------------------------- instruction-lean layouts
     {
         const int64_t nt = (E + 31) / 32;
         p.geoT.assign(nt * 11 * 32, 0.0);
+#pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < E; ++e) {
             double *g = p.geoT.data() + (e >> 5) * 352 + (e & 31);
             g[0] = p.geoV[e];
@@ -253,6 +448,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         p.we = (mx + 7) / 8 * 8;
         p.we_max = mx;
         p.incE.assign((size_t)S * p.we, 0xFFFF);
+#pragma omp parallel for schedule(static)
         for (int64_t s = 0; s < S; ++s)
             for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j) p.incE[(size_t)s * p.we + (j - p.edge_off[s])] = p.inc_local[j];
         mx = 1;
@@ -260,12 +456,14 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         p.wn = (mx + 7) / 8 * 8;
         p.zslot = (int32_t)(((E + 31) / 32) * 128);  // first slot past the last tile: kept zero
         p.nodeE.assign((size_t)N * p.wn, p.zslot);
+#pragma omp parallel for schedule(static)
         for (int64_t k = 0; k < N; ++k)
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) {
                 const int64_t e = p.node_ent[j] >> 2, a = p.node_ent[j] & 3;
                 p.nodeE[(size_t)k * p.wn + (j - p.node_off[k])] = (int32_t)((((e >> 5) * 4 + a) << 5) + (e & 31));
             }
     }
+    clk.mark("plan: ELL tables");
     // ---------------------------------------------------------------- blocks and dependencies
     const int64_t cnt[ST_COUNT] = {S, E, N};
     p.maxblk = 0;
@@ -279,16 +477,19 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         std::sort(v.begin(), v.end());
         v.erase(std::unique(v.begin(), v.end()), v.end());
     };
+#pragma omp parallel for schedule(dynamic, 64)
     for (int b = 0; b < p.nblk[ST_AB]; ++b) {  // AB: D-blocks (previous step) of its tet list's nodes
         auto &v = deps[(size_t)ST_AB * p.maxblk + b];
         for (int32_t i = p.nlb_off[b]; i < p.nlb_off[b + 1]; ++i) v.push_back(p.nlb[i] / blk);
         finish(v);
     }
+#pragma omp parallel for schedule(dynamic, 64)
     for (int b = 0; b < p.nblk[ST_C]; ++b) {  // C: AB-blocks of its edge list
         auto &v = deps[(size_t)ST_C * p.maxblk + b];
         for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) v.push_back(p.el[i] / blk);
         finish(v);
     }
+#pragma omp parallel for schedule(dynamic, 64)
     for (int b = 0; b < p.nblk[ST_D]; ++b) {  // D: C-blocks of the tets of its nodes
         auto &v = deps[(size_t)ST_D * p.maxblk + b];
         for (int64_t k = (int64_t)b * blk; k < std::min<int64_t>(N, (int64_t)(b + 1) * blk); ++k)
@@ -304,7 +505,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     for (size_t q = 0; q < deps.size(); ++q) {
         p.dep.insert(p.dep.end(), deps[q].begin(), deps[q].end());
         p.dep_off[q + 1] = (int32_t)p.dep.size();
-    }
+    }    clk.mark("plan: dependencies");
 }
 
 void build_schedule(Plan &p, int resident_ctas) {
