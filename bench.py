@@ -252,13 +252,14 @@ def main():
     tot_k = sum(v for v in kt.values())
     for k in kernels:
         kernels[k]["share"] = kt[k] / tot_k if tot_k > 0 else None
-    traffic = None
+    traffic = traffic_live = None
     tpath = os.path.join(ROOT, "profiles", "traffic_per_step.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_step")
+            tj = json.load(open(tpath))
+            traffic, traffic_live = tj.get("dram_bytes_per_step"), tj.get("dram_bytes_per_step_live")
         except Exception:
-            traffic = None
+            traffic = traffic_live = None
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -273,7 +274,11 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "cem_step: k_AB + k_C + k_D per step (PDL-chained); unit = one step",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_kind": peak_kind, "traffic": traffic,
-                     "b_alg_bytes_per_step": balg},
+                     "b_alg_bytes_per_step": balg,
+                     # DRAM bytes the step really moves (ncu, no flush between kernels; profiles/) over
+                     # this run's step time: the share of HBM bandwidth the kernels sustain
+                     "traffic_live": traffic_live,
+                     "dram_frac_live": (traffic_live / (ms_step / 1e3) / 1e9 / hbm) if traffic_live else None},
         "kernels": kernels,
         "gpu_launches": int(launches),
         "clocks": clocks,

@@ -1,47 +1,60 @@
 #!/usr/bin/env python3
-"""Summarise gpurun_out/{launches.csv, prof_stages.ncu-rep} into profiles/ (per round)."""
+"""Summarise gpurun_out/{launches.csv, live_traffic.csv, prof_stages.ncu-rep} (scripts/round_profile.sh)
+into profiles/: <round>_ncu_summary.md, <round>_launches.csv, <round>_live_traffic.csv, traffic_per_step.json."""
 import csv
 import json
 import os
 import shutil
 import subprocess
 import sys
-from collections import defaultdict
+from collections import OrderedDict, defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 out_dir = os.path.join(ROOT, "profiles")
 g = os.path.join(ROOT, "gpurun_out")
+STAGES = ("k_AB", "k_C", "k_D")
 
-# ---- launch list: per-launch device time and DRAM bytes
-rows = list(csv.reader(open(os.path.join(g, "launches.csv"))))
-hi = [i for i, r in enumerate(rows) if "Metric Name" in r][0]
-h = rows[hi]
-L = defaultdict(dict)
-for r in rows[hi + 1:]:
-    if len(r) < len(h):
-        continue
-    k = (int(r[h.index("ID")]), r[h.index("Kernel Name")].split("(")[0].split("::")[-1])
-    L[k][r[h.index("Metric Name")]] = float(r[h.index("Metric Value")].replace(",", ""))
-launches = [(i, n, m) for (i, n), m in sorted(L.items())]
-stage = [x for x in launches if x[1] in ("k_AB", "k_C", "k_D")]
-# steps = consecutive (k_AB, k_C, k_D) triples; use the last complete step (steady state)
-steps = []
-for j in range(len(stage) - 2):
-    if [stage[j][1], stage[j + 1][1], stage[j + 2][1]] == ["k_AB", "k_C", "k_D"]:
-        steps.append(stage[j:j + 3])
-last = steps[-1]
-traffic = sum(m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"] for _, _, m in last)
-t_step = sum(m["gpu__time_duration.sum"] for _, _, m in last)
-json.dump({"round": rnd, "dram_bytes_per_step": traffic, "ncu_step_time_ns": t_step,
-           "per_kernel": {n: {"time_ns": m["gpu__time_duration.sum"], "dram_read": m["dram__bytes_read.sum"],
-                              "dram_write": m["dram__bytes_write.sum"]} for _, n, m in last},
-           "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                     "--clock-control none (cold-cache, serialised launches)"},
-          open(os.path.join(out_dir, "traffic_per_step.json"), "w"), indent=1)
+
+def metric_csv(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Metric Name" in r][0]
+    h = rows[hi]
+    L = OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) < len(h):
+            continue
+        k = (int(r[h.index("ID")]), r[h.index("Kernel Name")].split("(")[0].split("::")[-1])
+        L.setdefault(k, {})[r[h.index("Metric Name")]] = float(r[h.index("Metric Value")].replace(",", ""))
+    return [(i, n, m) for (i, n), m in L.items()]
+
+
+def steps_of(launches):
+    st = [x for x in launches if x[1] in STAGES]
+    out = []
+    for j in range(len(st) - 2):
+        if [st[j][1], st[j + 1][1], st[j + 2][1]] == list(STAGES):
+            out.append(st[j:j + 3])
+    return out
+
+
+# ---- launch list of the bench command (cold cache, serialised): shares per step
+launch_steps = steps_of(metric_csv(os.path.join(g, "launches.csv")))
+lastL = launch_steps[-1]
+t_launch = sum(m["gpu__time_duration.sum"] for _, _, m in lastL)
 shutil.copy(os.path.join(g, "launches.csv"), os.path.join(out_dir, f"{rnd}_launches.csv"))
+# ---- live traffic (no flush), steady state: average over the captured steps
+live_steps = steps_of(metric_csv(os.path.join(g, "live_traffic.csv")))
+live = defaultdict(lambda: defaultdict(float))
+for stp in live_steps:
+    for _, n, m in stp:
+        for k, v in m.items():
+            live[n][k] += v / len(live_steps)
+live_bytes = sum(live[n]["dram__bytes_read.sum"] + live[n]["dram__bytes_write.sum"] for n in STAGES)
+live_t = sum(live[n]["gpu__time_duration.sum"] for n in STAGES)
+shutil.copy(os.path.join(g, "live_traffic.csv"), os.path.join(out_dir, f"{rnd}_live_traffic.csv"))
 
-# ---- full captures
+# ---- full captures (steady state)
 raw = subprocess.run(["ncu", "-i", os.path.join(g, "prof_stages.ncu-rep"), "--page", "raw", "--csv"],
                      capture_output=True, text=True).stdout
 rr = list(csv.reader(raw.splitlines()))
@@ -55,28 +68,52 @@ def gv(r, k):
         return float("nan")
 
 
-lines = [f"# {rnd} — stage kernels, config 3 (1.02M tets), one B200", "",
-         "Source: `scripts/round_profile.sh` (ncu --set full --clock-control none, one launch of each stage "
-         "kernel in the steady state) and the launch list `" + f"{rnd}_launches.csv`.", "",
-         f"Per-step DRAM traffic (sum over k_AB, k_C, k_D of one step, launch list): **{traffic/1e6:.1f} MB** "
-         f"vs B_alg = 168.0 MB; serialised ncu step time {t_step/1e3:.1f} µs.", "",
-         "| kernel | time (µs) | DRAM R/W (MB) | DRAM % | L1 % | L2 % | warps active % | IPC | fp64 pipe % | regs | top stalls |",
-         "|---|---|---|---|---|---|---|---|---|---|---|"]
+def mb(r, k):
+    unit = U[H.index(k)]
+    scale = {"G": 1e3, "M": 1.0, "K": 1e-3}.get(unit[:1], 1e-6)
+    return gv(r, k) * scale
+
+
+full = OrderedDict()
 for r in rr[2:]:
-    name = r[H.index("Kernel Name")].split("(")[0].split("::")[-1]
+    full[r[H.index("Kernel Name")].split("(")[0].split("::")[-1]] = r
+cold_bytes = sum((mb(full[n], "dram__bytes_read.sum") + mb(full[n], "dram__bytes_write.sum")) * 1e6 for n in STAGES)
+json.dump({"round": rnd,
+           "dram_bytes_per_step": cold_bytes,
+           "dram_bytes_per_step_live": live_bytes,
+           "ncu_step_time_ns_live": live_t,
+           "per_kernel_live": {n: {"time_ns": live[n]["gpu__time_duration.sum"], "dram_read": live[n]["dram__bytes_read.sum"],
+                                   "dram_write": live[n]["dram__bytes_write.sum"]} for n in STAGES},
+           "source": {"dram_bytes_per_step": "ncu --set full (default cache flush) of k_AB, k_C, k_D at step ~350",
+                      "dram_bytes_per_step_live": "ncu --cache-control none --metrics dram__bytes_*.sum, steady state"}},
+          open(os.path.join(out_dir, "traffic_per_step.json"), "w"), indent=1)
+
+lines = [f"# {rnd} — stage kernels, config 3 (1.02M tets), one B200", "",
+         "Source: `scripts/round_profile.sh`: `ncu --set full --clock-control none` of one launch of each stage kernel "
+         "at step ~350 (steady state, `scripts/variant_bench.py`, same kernels and config as `bench.py`), "
+         f"the live-traffic pass `{rnd}_live_traffic.csv` (`--cache-control none`) and the launch list "
+         f"`{rnd}_launches.csv` of `bench.py --steps 4 --warmup 3`.", "",
+         f"Per-step DRAM traffic, live (no flush): **{live_bytes/1e6:.1f} MB** in {live_t/1e3:.1f} µs of serialised kernel "
+         f"time = {live_bytes/live_t:.0f} GB/s; cold (ncu flushes L2 before each kernel): {cold_bytes/1e6:.1f} MB. "
+         f"B_alg = 168.0 MB.", "",
+         "| kernel | time (µs) | DRAM R/W live (MB) | DRAM R/W cold (MB) | DRAM % | L1 % | L2 % | warps active % | IPC | fp64 pipe % | regs | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+for n in STAGES:
+    r = full[n]
     st = sorted(((gv(r, c), c.replace("smsp__pcsamp_warps_issue_stalled_", "")) for c in H
                  if c.startswith("smsp__pcsamp_warps_issue_stalled_") and not c.endswith("not_issued")), reverse=True)
     tot = sum(v for v, _ in st) or 1
-    unit = U[H.index("dram__bytes_read.sum")]
-    scale = 1e3 if unit.startswith("G") else (1.0 if unit.startswith("M") else 1e-3)
-    lines.append(f"| {name} | {gv(r, 'gpu__time_duration.sum'):.1f} | {gv(r, 'dram__bytes_read.sum')*scale:.0f}/"
-                 f"{gv(r, 'dram__bytes_write.sum')*scale:.0f} | {gv(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.0f} | "
+    lines.append(f"| {n} | {gv(r, 'gpu__time_duration.sum'):.1f} | {live[n]['dram__bytes_read.sum']/1e6:.0f}/"
+                 f"{live[n]['dram__bytes_write.sum']/1e6:.0f} | {mb(r, 'dram__bytes_read.sum'):.0f}/"
+                 f"{mb(r, 'dram__bytes_write.sum'):.0f} | {gv(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.0f} | "
                  f"{gv(r, 'l1tex__throughput.avg.pct_of_peak_sustained_active'):.0f} | "
                  f"{gv(r, 'lts__throughput.avg.pct_of_peak_sustained_elapsed'):.0f} | "
                  f"{gv(r, 'sm__warps_active.avg.pct_of_peak_sustained_active'):.0f} | "
                  f"{gv(r, 'sm__inst_executed.avg.per_cycle_active'):.2f} | "
                  f"{gv(r, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active'):.0f} | "
                  f"{gv(r, 'launch__registers_per_thread'):.0f} | "
-                 + ", ".join(f"{n} {100*v/tot:.0f}%" for v, n in st[:3]) + " |")
+                 + ", ".join(f"{nm} {100*v/tot:.0f}%" for v, nm in st[:3]) + " |")
+lines += ["", f"Launch list (cold, serialised) of one bench step: " +
+          ", ".join(f"{n} {m['gpu__time_duration.sum']/1e3:.1f} µs" for _, n, m in lastL) + f" (sum {t_launch/1e3:.1f} µs)."]
 open(os.path.join(out_dir, f"{rnd}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
