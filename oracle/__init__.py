@@ -80,6 +80,7 @@ def lib():
         L.orc_newmark_free.argtypes = [C.c_int64, D, D, D, D, D, C.c_double, C.c_double]
         L.orc_predict.argtypes = [C.c_int64, D, D, D, C.c_double]
         L.orc_num_threads.restype = C.c_int
+        L.orc_energy.argtypes = [C.c_void_p, D]
         _lib = L
     return _lib
 
@@ -200,6 +201,12 @@ class Oracle:
         G = np.empty(self.E); k = np.empty(self.E, np.int32); A = np.empty(self.E); fl = np.empty(self.E, np.uint8)
         lib().orc_criterion(self.h, _p(u, D), _p(G, D), _p(k, I32), _p(A, D), _p(fl, U8))
         return G, k, A, fl
+
+    def energy(self):
+        """Energy ledger at the current step: kinetic, strain, external, reaction, dissipated."""
+        out = np.empty(5)
+        lib().orc_energy(self.h, _p(out, D))
+        return dict(kinetic=out[0], strain=out[1], external=out[2], reaction=out[3], dissipated=out[4])
 
     def candidates(self, u, e):
         u = _c(u, np.float64); G = np.empty(24); A = np.empty(24)

@@ -69,6 +69,11 @@ typedef struct orc_sim {
     double *u, *v, *a;    /* [N][3] */
     int64_t step;
     double Ud;
+    /* energy ledger: reaction work of the prescribed dofs */
+    double Wr;
+    double *rprev;        /* [N][3] support force R at the previous step (prescribed dofs) */
+    double *uold;         /* [N][3] u_n while step n -> n+1 runs */
+    int has_dir;
     orc_record *rec; int64_t nrec, caprec;
     /* scratch */
     double *tau;          /* [E][6] */
@@ -241,7 +246,7 @@ ORC_API void orc_destroy(orc_sim *s) {
     free(s->nod_ent); free(s->m); free(s->fext); free(s->dir); free(s->dir_v0);
     free(s->u); free(s->v); free(s->a); free(s->rec); free(s->tau); free(s->sig); free(s->vhat);
     free(s->fe); free(s->fint); free(s->eig); free(s->G); free(s->cand);
-    free(s->area); free(s->flag);
+    free(s->area); free(s->flag); free(s->rprev); free(s->uold);
     free(s);
 }
 
@@ -687,7 +692,34 @@ ORC_API orc_sim *orc_create(int64_t n_nodes, const double *X, int64_t n_tets, co
         }
     }
     s->step = 0; s->Ud = 0.0;
+    /* support force of the prescribed dofs at t = 0 (energy ledger) */
+    s->rprev = xcalloc(3 * n_nodes, sizeof(double)); s->uold = xcalloc(3 * n_nodes, sizeof(double));
+    s->Wr = 0.0; s->has_dir = 0;
+    for (int64_t k = 0; k < n_nodes; ++k)
+        for (int c = 0; c < 3; ++c)
+            if (dof_prescribed(s, k, c)) {
+                int64_t i = 3 * k + c;
+                s->has_dir = 1;
+                s->rprev[i] = s->m[k] * s->a[i] - (s->fext[i] - s->fint[i]);
+            }
     return s;
+}
+
+/* ---------------------------------------------------------------- energy ledger (N1)
+ * Support force of a prescribed dof at t_{n+1}: R = m a_{n+1} - (f_ext - f_int(u_{n+1}))
+ * (the force the constraint applies, PAPER.md:L416 solved for the missing load); its work
+ * over the step by the trapezoidal rule, W_R += 1/2 (R_n + R_{n+1}) (u_{n+1} - u_n)
+ * (SPEC.md update_energy_ledger: "reaction work on Dirichlet dofs"; R22).
+ * Sequential over k ascending, c = x, y, z. */
+static void reaction_work(orc_sim *s) {
+    for (int64_t k = 0; k < s->N; ++k)
+        for (int c = 0; c < 3; ++c) {
+            if (!dof_prescribed(s, k, c)) continue;
+            const int64_t i = 3 * k + c;
+            const double R = s->m[k] * s->a[i] - (s->fext[i] - s->fint[i]);
+            s->Wr = s->Wr + 0.5 * (s->rprev[i] + R) * (s->u[i] - s->uold[i]);
+            s->rprev[i] = R;
+        }
 }
 
 /* ---------------------------------------------------------------- run
@@ -699,6 +731,7 @@ ORC_API int orc_run(orc_sim *s, int64_t nsteps, int32_t crack_every) {
     for (int64_t it = 0; it < nsteps; ++it) {
         const int64_t n1 = s->step + 1;
         const double t1 = (double)n1 * s->dt;
+        if (s->has_dir) memcpy(s->uold, s->u, sizeof(double) * 3 * s->N);
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < 3 * s->N; ++i) s->u[i] = (s->u[i] + s->dt * s->v[i]) + hdt2 * s->a[i];
         internal_force(s, s->u);
@@ -711,6 +744,7 @@ ORC_API int orc_run(orc_sim *s, int64_t nsteps, int32_t crack_every) {
                 if (!isfinite(s->u[i]) || !isfinite(s->v[i]) || !isfinite(s->a[i])) bad = 1;
             }
         }
+        if (s->has_dir) reaction_work(s);
         if (crack_every > 0 && n1 % crack_every == 0) {
             criterion(s, s->u);
             split_pass(s, n1);
@@ -797,6 +831,28 @@ ORC_API double orc_strain_energy(orc_sim *s, const double *u) {
         U += psi * (s->vhat[k] / 6.0);
     }
     return U;
+}
+
+/* energy ledger at the current step n (SPEC.md update_energy_ledger):
+ *   out[0] kinetic  T = 1/2 sum_k m_k (v_k . v_k)          (lumped mass)
+ *   out[1] strain   U = sum_s psi(eps~_s) Vhat_s / 6       (orc_strain_energy)
+ *   out[2] external W = sum_k f_ext,k . u_k                (constant tractions from t = 0 and
+ *                                                           u_0 = 0: the telescoped f.du sum, R22)
+ *   out[3] reaction W_R (trapezoidal support-force work, reaction_work)
+ *   out[4] dissipated U_d = sum Gc_e A_e over the splits   (R-U_d)
+ * sums sequential over k (then x, y, z) ascending. */
+ORC_API void orc_energy(orc_sim *s, double *out) {
+    double T = 0.0, W = 0.0;
+    for (int64_t k = 0; k < s->N; ++k) {
+        const double *v = s->v + 3 * k, *u = s->u + 3 * k, *f = s->fext + 3 * k;
+        T = T + s->m[k] * ((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+        W = W + ((f[0] * u[0] + f[1] * u[1]) + f[2] * u[2]);
+    }
+    out[0] = 0.5 * T;
+    out[1] = orc_strain_energy(s, s->u);
+    out[2] = W;
+    out[3] = s->Wr;
+    out[4] = s->Ud;
 }
 
 /* criterion on an arbitrary u (uses sigma(u)); outputs per tet G_e, candidate, area, flag */
