@@ -183,6 +183,26 @@ CEM_API cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out);
 /* Synchronise and fill *out (see cem_state_out). Returns CEM_ENONFINITE if flagged. */
 CEM_API cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where);
 
+/* Energy ledger at the current step n (SPEC.md update_energy_ledger;
+ * oracle/cem_oracle.c orc_energy defines each quantity and its association order):
+ *   kinetic        T   = 1/2 sum_k m_k |v_k|^2
+ *   strain         U   = sum_s psi(eps~_s) Vhat_s / 6, psi = 1/2 lam tr(eps~)^2 + mu eps~:eps~
+ *                        (L197-L202; Vhat_s / 6 = the smoothing-domain volume)
+ *   external_work  W   = sum_k f_ext,k . u_k  (tractions constant from t = 0 and u_0 = 0: the
+ *                        f_ext . du sum telescoped, R22)
+ *   reaction_work  W_R = sum over steps of 1/2 (R_n + R_{n+1}) (u_{n+1} - u_n) on prescribed
+ *                        dofs, R = m a - (f_ext - f_int) the support force (R22)
+ *   dissipated     U_d = sum Gc_e A_e over the split records                 (L206)
+ * Per-element terms are the oracle's bit for bit; the sums run over per-block partials in a
+ * fixed order (run-to-run deterministic, equal to the oracle's sequential sums to rounding).
+ * Synchronises the ctx stream; launches two kernels.  CEM_ESTATE for a multi-rank context. */
+typedef struct {
+    int64_t step;
+    double time;
+    double kinetic, strain, external_work, reaction_work, dissipated;
+} cem_energy_out;
+CEM_API cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out);
+
 /* Host-only: the partition plan rank `rank` of `nranks` uses (no device work). */
 CEM_API cem_status cem_partition(const cem_mesh_in *mesh, int nranks, int rank, cem_part_out *out);
 CEM_API void cem_partition_free(cem_part_out *out);

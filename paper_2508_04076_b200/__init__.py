@@ -76,6 +76,11 @@ class cem_state_out(C.Structure):
                 ("nonfinite", C.c_int32), ("nonfinite_node", C.c_int32)]
 
 
+class cem_energy_out(C.Structure):
+    _fields_ = [("step", C.c_int64), ("time", C.c_double), ("kinetic", C.c_double), ("strain", C.c_double),
+                ("external_work", C.c_double), ("reaction_work", C.c_double), ("dissipated", C.c_double)]
+
+
 _P = C.POINTER
 _lib.cem_workspace_size.argtypes = [_P(cem_mesh_in), _P(cem_opts), _P(C.c_size_t)]
 _lib.cem_init_mesh.argtypes = [_P(cem_mesh_in), _P(cem_material), _P(cem_load_in), _P(cem_opts),
@@ -83,6 +88,7 @@ _lib.cem_init_mesh.argtypes = [_P(cem_mesh_in), _P(cem_material), _P(cem_load_in
 _lib.cem_step.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
 _lib.cem_crack_update.argtypes = [C.c_void_p, I64]
 _lib.cem_get_state.argtypes = [C.c_void_p, _P(cem_state_out), C.c_int]
+_lib.cem_energy.argtypes = [C.c_void_p, _P(cem_energy_out)]
 _lib.cem_sizes.argtypes = [C.c_void_p, I64, I64, I64]
 _lib.cem_launch_count.argtypes = [C.c_void_p]
 _lib.cem_launch_count.restype = C.c_int64
@@ -93,7 +99,7 @@ _lib.cem_last_error.restype = C.c_char_p
 _lib.cem_destroy.argtypes = [C.c_void_p]
 _lib.cem_abi_version.restype = C.c_int32
 for _f in ("cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state",
-           "cem_sizes", "cem_set_profiling", "cem_kernel_times"):
+           "cem_sizes", "cem_set_profiling", "cem_kernel_times", "cem_energy"):
     getattr(_lib, _f).restype = C.c_int
 
 class cem_part_out(C.Structure):
@@ -114,7 +120,7 @@ _lib.cem_step_group.restype = C.c_int
 _lib.cem_merge_records.argtypes = [C.c_int64, I64, I32, D, D, I64, D]
 _lib.cem_merge_records.restype = C.c_int
 
-EXPORTED = ["cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state",
+EXPORTED = ["cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state", "cem_energy",
             "cem_sizes", "cem_launch_count", "cem_set_profiling", "cem_kernel_times",
             "cem_last_error", "cem_destroy", "cem_abi_version", "cem_partition", "cem_partition_free",
             "cem_nccl_unique_id", "cem_step_group", "cem_merge_records"]
@@ -273,6 +279,14 @@ class Simulation:
         nr = min(out.n_records, cap)
         return State(u, v, a, st, m, out.step, out.time, out.dt, out.n_active, out.dissipated,
                      out.nonfinite, out.nonfinite_node, rs[:nr], re[:nr], rk[:nr], rg[:nr], ra[:nr])
+
+    def energy(self) -> dict:
+        """Energy ledger at the current step (cem_energy): kinetic, strain, external, reaction,
+        dissipated (J)."""
+        out = cem_energy_out()
+        self._check(_lib.cem_energy(self._h, C.byref(out)))
+        return dict(step=out.step, time=out.time, kinetic=out.kinetic, strain=out.strain,
+                    external=out.external_work, reaction=out.reaction_work, dissipated=out.dissipated)
 
     def close(self):
         if self._h:

@@ -41,6 +41,8 @@ struct cem_ctx {
     void *comm = nullptr;
     bool init_exchange_pending = false;
     std::vector<void *> dist_allocs;
+    double *epart = nullptr;      // energy-ledger partials (device)
+    int64_t n_epart_edges = 0, n_epart_nodes = 0, n_wr = 0;
 };
 
 namespace {
@@ -77,12 +79,16 @@ struct Layout {
     }
 };
 
+// staged D blocks (blk/4 nodes each): one reaction-work accumulator per block
+int64_t n_wr_blocks(int64_t N, int blk) { return (N + (blk >> 2) - 1) / (blk >> 2); }
+
 struct Offs {
     size_t conn, geoT, eedge, incE, nodeE, X, fext, nflag, dir_v0, gc;
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, tflag;
+    size_t rprev, wr_blk, epart;
     size_t total;
 };
 
@@ -112,7 +118,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.v = L.take<double4>(N);
     o.a = L.take<double4>(N);
     o.srec = L.take<double>(6 * S);
-    o.fe = L.take<double4>(fe_slots(E));  // + the zero slot
+    o.fe = L.take<double>(CEM_FES * fe_slots(E));  // + the zero slot
     o.ctr = L.take<int32_t>(8);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
@@ -140,6 +146,9 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.nlb = L.take<int32_t>((int64_t)p.nlb.size());
     o.tconn = L.take<uint16_t>((int64_t)p.tconn.size());
     o.tflag = L.take<uint8_t>(E);
+    o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
+    o.wr_blk = L.take<double>(n_wr_blocks(N, p.blk));
+    o.epart = L.take<double>(p.nblk[ST_AB] + 2 * ((N + 255) / 256));
     o.total = L.off;
     return o;
 }
@@ -185,7 +194,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.v = at<double4>(b, o.v);
     d.a = at<double4>(b, o.a);
     d.srec = at<double>(b, o.srec);
-    d.fe = at<double4>(b, o.fe);
+    d.fe = at<double>(b, o.fe);
     d.nl_off = at<int32_t>(b, o.nl_off);
     d.nl = at<int32_t>(b, o.nl);
     d.lconn = at<uint16_t>(b, o.lconn);
@@ -229,6 +238,12 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.P = (int)p.sched.size();
     d.maxblk = p.maxblk;
     for (int g = 0; g < ST_COUNT; ++g) d.nblk[g] = p.nblk[g];
+    d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
+    d.wr_blk = at<double>(b, o.wr_blk);
+    ctx->epart = at<double>(b, o.epart);
+    ctx->n_epart_edges = p.nblk[ST_AB];
+    ctx->n_epart_nodes = (h.N + 255) / 256;
+    ctx->n_wr = n_wr_blocks(h.N, p.blk);
 }
 
 cem_status upload(cem_ctx *ctx, const Offs &o) {
@@ -299,8 +314,21 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.u1, u1.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.v, v4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
+    // energy ledger: support force at t = 0 of the prescribed dofs, R_0 = m a_0 - (f_ext - 0)
+    // (f_int(u_0 = 0) = 0; oracle orc_create), reaction-work accumulators zeroed
+    if (h.any_dirichlet) {
+        std::vector<double> r0(3 * N, 0.0);
+        for (int64_t kn = 0; kn < N; ++kn) {
+            const int64_t n = p.node_new2old[kn];
+            const double aa[3] = {a4[kn].x, a4[kn].y, a4[kn].z};
+            for (int c = 0; c < 3; ++c)
+                if (h.nflag[n] >> c & 1) r0[3 * kn + c] = h.mass[n] * aa[c] - (h.fext[3 * n + c] - 0.0);
+        }
+        CUDA_TRY(put(o.rprev, r0.data(), sizeof(double) * 3 * N));
+    }
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.wr_blk), 0, sizeof(double) * n_wr_blocks(N, p.blk), st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 6 * S, st));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double4) * fe_slots(E), st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
@@ -785,6 +813,41 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
     CUDA_TRY(cudaMemcpyAsync(&after, ctx->d.ctr, sizeof after, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (n_split_out) *n_split_out = after - before;
+    return CEM_OK;
+}
+
+cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
+    if (!ctx || !out) return CEM_EINVAL;
+    if (ctx->dist || ctx->nranks > 1) {
+        ctx->err = "cem_energy: single-context runs only";
+        return CEM_ESTATE;
+    }
+    cudaStream_t st = ctx->stream;
+    cem_state_out so{};
+    const cem_status rc = cem_get_state(ctx, &so, CEM_HOST);  // synchronises; U_d, nonfinite
+    if (rc != CEM_OK) return rc;
+    launch_energy(ctx->d, ctx->step, ctx->epart, ctx->epart + ctx->n_epart_edges, st);
+    ctx->launches += 2;
+    std::vector<double> pe(ctx->n_epart_edges + 2 * ctx->n_epart_nodes), wr(ctx->n_wr);
+    CUDA_TRY(cudaMemcpyAsync(pe.data(), ctx->epart, sizeof(double) * pe.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(wr.data(), ctx->d.wr_blk, sizeof(double) * wr.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    double U = 0.0, T = 0.0, W = 0.0, Wr = 0.0;  // partials summed in block order
+    for (int64_t i = 0; i < ctx->n_epart_edges; ++i) U = U + pe[i];
+    for (int64_t i = 0; i < ctx->n_epart_nodes; ++i) {
+        T = T + pe[ctx->n_epart_edges + 2 * i];
+        W = W + pe[ctx->n_epart_edges + 2 * i + 1];
+    }
+    if (ctx->d.rprev)
+        for (double x : wr) Wr = Wr + x;
+    out->step = ctx->step;
+    out->time = (double)ctx->step * ctx->h.dt;
+    out->kinetic = 0.5 * T;
+    out->strain = U;
+    out->external_work = W;
+    out->reaction_work = Wr;
+    out->dissipated = so.dissipated;
     return CEM_OK;
 }
 

@@ -15,6 +15,11 @@
 
 namespace cem {
 
+// doubles per force slot: 4 = (x, y, z, 0) in one 32-B sector, 3 = packed (x, y, z)
+#ifndef CEM_FES
+#define CEM_FES 4
+#endif
+
 // phase timer of the host preprocessing (CEM_TIMING=1 prints to stderr)
 struct PhaseClock {
     bool on = getenv("CEM_TIMING") != nullptr;
@@ -129,8 +134,10 @@ struct Dev {
     int32_t *dirty;            // [N] step stamp of the last split touching the node
     double4 *ubuf[2];          // u_m lives in ubuf[m & 1]
     double4 *v, *a;
+    double *rprev;             // [N][3] support force of prescribed dofs at the last step (NULL: none)
+    double *wr_blk;            // [staged D blocks] reaction work accumulated per block (energy ledger)
     double *srec;              // [S][6]: sigma_s (11,22,33,12,23,13), 48-B records
-    double4 *fe;               // [4E] force slots f_{e,a} (x,y,z,0); slot(e,a) = ((e>>5)*4 + a)*32 + (e&31)
+    double *fe;                // [4E][CEM_FES] force slots f_{e,a}; slot(e,a) = ((e>>5)*4 + a)*32 + (e&31)
     const double *geoT;        // [E/32][11][32] warp-tiled geometry
     const uint16_t *incE;      // [S][we]
     const int32_t *nodeE;      // [N][wn]
@@ -162,6 +169,7 @@ struct Dev {
 // cem_kernels.cu
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
 void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/);
+void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel
 void set_smem_limits(int smem_bytes);

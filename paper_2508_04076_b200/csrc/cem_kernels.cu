@@ -56,6 +56,20 @@ __device__ __forceinline__ double4 ld256(const double4 *p) {  // LDG.E.256 (sm_1
 __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, double w) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
 }
+__device__ __forceinline__ void store_slot(double *p, double x, double y, double z) {
+#if CEM_FES == 4
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(0.0) : "memory");
+#else
+    // 24-B slot at an 8-B boundary: one 16-B and one 8-B store, ordered by alignment
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x), "d"(y) : "memory");
+        p[2] = z;
+    } else {
+        p[0] = x;
+        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p + 1), "d"(y), "d"(z) : "memory");
+    }
+#endif
+}
 __device__ __forceinline__ void st128(double *p, double x, double y) {
     asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
@@ -141,6 +155,20 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
+// deterministic block sum (fixed shuffle tree, then the warps in order); valid in thread 0.
+// Every thread of the block must call it.
+__device__ __forceinline__ double block_sum(double x, double *red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = x + __shfl_down_sync(0xffffffffu, x, o);
+    __syncthreads();  // red may still be read by a previous call
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = t + red[i];
+    return t;
+}
+
 // ------------------------------------------------------------------ stage AB: strain + edge stress
 // For the edge block's deduplicated tet list: eps = sum_a B_a u_a (a = 0..3 in order), Voigt
 // (11,22,33,12,23,13) with engineering shears, gradN0 = -((gradN1 + gradN2) + gradN3),
@@ -190,7 +218,7 @@ __device__ __forceinline__ void grad0(double (&g)[4][3]) {
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
 }
 
-__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm) {
+__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm, double *epart = nullptr) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
@@ -249,28 +277,45 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
     uint4 q = hs ? __ldg(row) : make_uint4(0, 0, 0, 0);  // first 8 incidences, before the barrier
     __syncthreads();
-    if (!hs) return;
     double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    for (int w = 0;;) {  // ELL row: 8 incidences per 16-B load, in order
-        const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
-        const int lim = d.we_max - w;  // warp-uniform: slots past the mesh's max incidence are skipped
+    if (hs) {
+        for (int w = 0;;) {  // ELL row: 8 incidences per 16-B load, in order
+            const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+            const int lim = d.we_max - w;  // warp-uniform: slots past the mesh's max incidence are skipped
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            if (t >= lim) break;
-            // padding (0xffff) -> the all-zero sentinel row nt; inactive tets hold zeros
-            const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
-            Vh = Vh + T[6 * tn + r];
-            T0 = T0 + T[r];
-            T1 = T1 + T[tn + r];
-            T2 = T2 + T[2 * tn + r];
-            T3 = T3 + T[3 * tn + r];
-            T4 = T4 + T[4 * tn + r];
-            T5 = T5 + T[5 * tn + r];
+            for (int t = 0; t < 8; ++t) {
+                if (t >= lim) break;
+                // padding (0xffff) -> the all-zero sentinel row nt; inactive tets hold zeros
+                const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
+                Vh = Vh + T[6 * tn + r];
+                T0 = T0 + T[r];
+                T1 = T1 + T[tn + r];
+                T2 = T2 + T[2 * tn + r];
+                T3 = T3 + T[3 * tn + r];
+                T4 = T4 + T[4 * tn + r];
+                T5 = T5 + T[5 * tn + r];
+            }
+            w += 8;
+            if (w >= d.we_max) break;  // (we_max <= we)
+            q = __ldg(row + (w >> 3));
         }
-        w += 8;
-        if (w >= d.we_max) break;  // (we_max <= we)
-        q = __ldg(row + (w >> 3));
     }
+    if (epart) {
+        // energy ledger: psi(eps~_s) Vhat_s / 6, psi = 1/2 lam tr^2 + mu eps:eps (oracle
+        // orc_strain_energy, same association), summed per block in a fixed order
+        double U = 0.0;
+        if (hs && Vh != 0.0) {
+            const double inv = 1.0 / Vh;
+            const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
+            const double tr = e11 + e22 + e33;
+            const double ee = e11 * e11 + e22 * e22 + e33 * e33 + 0.5 * (g12 * g12 + g23 * g23 + g13 * g13);
+            U = (0.5 * d.lam * tr * tr + d.mu * ee) * (Vh / 6.0);
+        }
+        const double t = block_sum(U, sm);  // the planes are no longer read
+        if (tid == 0) epart[b] = t;
+        return;
+    }
+    if (!hs) return;
     double *o = d.srec + 6u * (uint32_t)s;  // 48-B record, 16-B aligned
     if (Vh == 0.0) {
         st128(o, 0.0, 0.0);
@@ -587,11 +632,11 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     }
     __syncthreads();
     if (!he) return;
-    // slot (e,a) = fo + 32 a (x, y, z, 0): one 32-B sector per slot
-    double4 *fo = d.fe + (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));
+    // slot (e,a) = slot0 + 32 a, CEM_FES doubles per slot
+    double *fo = d.fe + CEM_FES * (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));
     if (!act) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) st256(fo + 32 * a, 0.0, 0.0, 0.0, 0.0);
+        for (int a = 0; a < 4; ++a) store_slot(fo + 32 * CEM_FES * a, 0.0, 0.0, 0.0);
         return;
     }
     const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
@@ -615,7 +660,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
         const double fy = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
         const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
-        st256(fo + 32 * a, fx, fy, fz, 0.0);
+        store_slot(fo + 32 * CEM_FES * a, fx, fy, fz);
     }
     if (!crack) return;
     if (!(tf & 1)) return;  // ghost tet: its owner decides, the state arrives by exchange
@@ -646,26 +691,26 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 // original tet id) are independent, so splitting them across lanes keeps every sum sequential
 // in the oracle's order while a warp reads whole 32-B slot sectors with 8-B loads and holds
 // 4x fewer registers per slot in flight.  Newmark + BC are per component as well.
-__device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
+__device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
     const int c = threadIdx.x & 3;
     const int64_t k = kbase + (threadIdx.x >> 2);
-    if (k >= d.N) return;
+    if (k >= d.N) return 0.0;
     const uint8_t fl = __ldg(&d.nflag[k]);
-    if (fl & 16) return;  // multi-GPU: another rank owns (and updates) this node
+    if (fl & 16) return 0.0;  // multi-GPU: another rank owns (and updates) this node
     // static tables before the dependency wait (overlaps the previous stage's tail)
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
     int4 qa = __ldg(row), qb = __ldg(row + 1);
     const double fxc = (fl & 8) ? __ldg(reinterpret_cast<const double *>(d.fext + k) + c) : 0.0;
     const double vb0 = (fl & 7) ? __ldg(reinterpret_cast<const double *>(d.dir_v0 + k) + c) : 0.0;
     pdl_wait();  // force slots come from stage C
-    const double *fec = reinterpret_cast<const double *>(d.fe) + c;  // lane c: component c of each slot
+    const double *fec = d.fe + (c < 3 ? c : 0);  // lane c: component c of each slot (lane 3: unused sum)
     double f = 0.0;
     for (int w = 0;;) {
         // padding entries point at an all-zero slot: adding +0.0 is an exact no-op here
         const int32_t sl[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
         double x[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) x[t] = __ldcg(fec + 4u * (uint32_t)sl[t]);
+        for (int t = 0; t < 8; ++t) x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
         w += 8;
         const bool more = sl[7] != d.zslot && w < d.wn;
         if (more) {
@@ -701,6 +746,16 @@ __device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const doubl
         vv = vv + dt * (d.omg * aa + d.gamma * an);
         aa = an;
     }
+    double wr = 0.0;
+    if (d.rprev && c < 3 && (fl >> c & 1)) {
+        // energy ledger: support force R = m a - (f_ext - f_int) of the prescribed dof and its
+        // trapezoidal work 1/2 (R_s + R_{s+1}) (u_{s+1} - u_s) (oracle reaction_work, R22)
+        const double R = mk * aa - (fxc - f);
+        const double us = __ldcg(reinterpret_cast<const double *>(u2p + k) + c);  // u_s, overwritten below
+        double *rp = d.rprev + 3 * k + c;
+        wr = 0.5 * (*rp + R) * (u1 - us);
+        *rp = R;
+    }
     if (__ldcg(d.dirty + k) == (int32_t)(s + 1)) {
         // an incident tet split in this step: lumped mass from the active incidences;
         // m = 0 -> frozen, v = a = 0 (R15)
@@ -715,6 +770,16 @@ __device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const doubl
     if (c < 3 && (!isfinite(u1) || !isfinite(vv) || !isfinite(aa))) {
         d.ctr[1] = 1;
         atomicMin(&d.ctr[2], ldro(d.node_orig + k));
+    }
+    return wr;
+}
+
+__device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
+    const double w = node_update(d, kbase, u1p, u2p, s);
+    if (d.rprev) {  // prescribed dofs present: this block's reaction-work increment, fixed order
+        __shared__ double red[32];
+        const double t = block_sum(w, red);
+        if (threadIdx.x == 0) d.wr_blk[kbase / (blockDim.x >> 2)] += t;
     }
 }
 
@@ -745,8 +810,8 @@ __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
         bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 48;
     } else {
         base = reinterpret_cast<const char *>(d.fe);
-        off = (int64_t)pb * d.blk * 128;
-        bytes = min((int64_t)d.blk, d.E - (int64_t)pb * d.blk) * 128;
+        off = (int64_t)pb * d.blk * 32 * CEM_FES;
+        bytes = min((int64_t)d.blk, d.E - (int64_t)pb * d.blk) * 32 * CEM_FES;
     }
     for (int64_t l = threadIdx.x; l < bytes / 128; l += blockDim.x) discard_l2(base + off + 128 * l);
 }
@@ -864,6 +929,31 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     block_D(d, (int64_t)blockIdx.x * (blockDim.x >> 2), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
+// energy ledger on the current state u_n, v_n (cem_energy): per-block partials, fixed order
+__global__ void __launch_bounds__(256) k_energy_edges(Dev d, int64_t n, double *part) {
+    extern __shared__ __align__(16) double sm[];
+    block_AB(d, blockIdx.x, d.ubuf[n & 1], sm, part);
+}
+__global__ void __launch_bounds__(256) k_energy_nodes(Dev d, int64_t n, double *part) {
+    __shared__ double red[32];
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double t = 0.0, w = 0.0;
+    if (k < d.N && !(__ldg(&d.nflag[k]) & 16)) {
+        const double4 v = ld4(&d.v[k]), u = ld4(&d.ubuf[n & 1][k]);
+        t = d.mass[k] * ((v.x * v.x + v.y * v.y) + v.z * v.z);  // oracle orc_energy
+        if (__ldg(&d.nflag[k]) & 8) {
+            const double4 f = ldro4(&d.fext[k]);
+            w = (f.x * u.x + f.y * u.y) + f.z * u.z;
+        }
+    }
+    const double ts = block_sum(t, red);
+    const double ws = block_sum(w, red);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = ts;
+        part[2 * blockIdx.x + 1] = ws;
+    }
+}
+
 // criterion on the current state u_n (cem_crack_update)
 __global__ void __launch_bounds__(256) k_AB_cur(Dev d, int64_t n) {
     extern __shared__ __align__(16) double sm[];
@@ -911,6 +1001,7 @@ void set_smem_limits(int smem_bytes) {
     cudaFuncSetAttribute(k_AB, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_AB_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_energy_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
@@ -949,6 +1040,11 @@ void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t s
     if (ev) cudaEventRecord(ev[2], st);
     k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     if (ev) cudaEventRecord(ev[3], st);
+}
+
+void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st) {
+    k_energy_edges<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, n, part_edges);
+    k_energy_nodes<<<nblk(d.N), 256, 0, st>>>(d, n, part_nodes);
 }
 
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st) {
