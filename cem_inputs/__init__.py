@@ -243,6 +243,44 @@ def edge_impact_plate(cells=(200, 100, 9), dims=(0.2, 0.1, 0.009), seed=2, v0=16
                    cells=tuple(cells), dims=tuple(dims), node_ijk=ijk)
 
 
+CONCRETE_CT = dict(E=36e9, nu=0.18, rho=2400.0, Gc=65.0)  # PAPER.md:L1343 (Ozbolt et al. concrete)
+
+
+def compact_tension(cells=(60, 60, 12), dims=(0.2, 0.2, 0.04), seed=5, v0=3.318, t0=100e-6,
+                    slot_depth=0.4, steps=1250, material=CONCRETE_CT, name=None):
+    """Dynamic compact tension stand-in.
+
+    The paper's geometry figure is missing; approximated as a W x H x B block with a vertical
+    slot (two cells wide, inactive) cut from the top face to depth slot_depth * H at mid-width.
+    The slot's right face (node column i = nx/2 + 1) is driven in x by the ramp v = (t/t0) v0
+    (t0 = 100 us, v0 = 1.375 / 3.318 / 3.993 m/s), its left face
+    (i = nx/2 - 1) is held at v_x = 0.  The crack grows from the slot tip towards y = 0.
+    """
+    nx, ny, nz = cells
+    X, tets, ijk = kuhn_lattice(cells, dims, seed)
+    E = tets.shape[0]
+    cell = _cell_of_tet(E)
+    ci = cell % nx; cj = (cell // nx) % ny
+    depth = max(1, int(round(slot_depth * ny)))
+    state = np.ones(E, np.uint8)
+    state[((ci == nx // 2 - 1) | (ci == nx // 2)) & (cj >= ny - depth)] = 0
+    gc = np.full(E, material["Gc"], np.float64)
+    on_slot = ijk[:, 1] >= ny - depth
+    right = np.nonzero(on_slot & (ijk[:, 0] == nx // 2 + 1))[0]
+    left = np.nonzero(on_slot & (ijk[:, 0] == nx // 2 - 1))[0]
+    vbc_node = np.concatenate([left, right]).astype(np.int32)
+    order = np.argsort(vbc_node, kind="stable")
+    vbc_node = vbc_node[order]
+    vbc_v0 = np.zeros((vbc_node.size, 3))
+    vbc_v0[:, 0] = np.concatenate([np.zeros(left.size), np.full(right.size, v0)])[order]
+    vbc_mask = np.full(vbc_node.size, 1, np.uint8)
+    return Problem(name=name or f"compact_tension{tuple(cells)}_v{v0}", X=X, tets=tets, tet_state=state,
+                   tet_gc=gc, E=material["E"], nu=material["nu"], rho=material["rho"], Gc=material["Gc"],
+                   tface=np.zeros((0, 3), np.int32), tface_t=np.zeros((0, 3)), vbc_node=vbc_node,
+                   vbc_mask=vbc_mask, vbc_v0=vbc_v0, vbc_t0=t0, steps=steps, cells=tuple(cells),
+                   dims=tuple(dims), node_ijk=ijk)
+
+
 def weak_scaling_block(P=1, cells_per_rank=(100, 100, 17), h=1e-3, seed=3, predamage=0.005,
                        steps=1000):
     """Config 3: (100P) x 100 x 17 cells, h = 1 mm, no notch, 0.5% pre-damaged tets (Gc_e = 0)."""
@@ -268,10 +306,13 @@ def config(k: int, P: int = 1) -> Problem:
         return p
     if k == 4:
         return notched_plate((400, 160, 20), seed=4, steps=10000, name="cfg4")
+    if k in (5, 6, 7):  # N2: dynamic compact tension, the paper's three loading rates
+        v0 = {5: 1.375, 6: 3.318, 7: 3.993}[k]
+        return compact_tension(v0=v0, name=f"cfg{k}_ct_v{v0}")
     raise ValueError(k)
 
 
-CONFIGS = {0: "cfg0", 1: "cfg1", 2: "cfg2", 3: "cfg3", 4: "cfg4"}
+CONFIGS = {0: "cfg0", 1: "cfg1", 2: "cfg2", 3: "cfg3", 4: "cfg4", 5: "cfg5_ct", 6: "cfg6_ct", 7: "cfg7_ct"}
 
 
 def single_tet(L=1.0):

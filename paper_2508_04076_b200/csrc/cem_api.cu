@@ -88,7 +88,7 @@ struct Offs {
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, tflag;
-    size_t rprev, wr_blk, epart;
+    size_t rprev, wr_blk, epart, crit_list;
     size_t total;
 };
 
@@ -149,12 +149,14 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.wr_blk = L.take<double>(n_wr_blocks(N, p.blk));
     o.epart = L.take<double>(p.nblk[ST_AB] + 2 * ((N + 255) / 256));
+    o.crit_list = L.take<int32_t>(E);
     o.total = L.off;
     return o;
 }
 
 int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1)); }
-int smem_c_for(const Plan &p) { return 8 * (7 * (p.max_el | 1) + 3 * (p.max_nl | 1)); }
+// stage C reuses its staging area for the warps' criterion scratch (<= 8 warps x ~840 B)
+int smem_c_for(const Plan &p) { return std::max(8 * (7 * (p.max_el | 1) + 3 * (p.max_nl | 1)), 8 * 1024); }
 int smem_bytes_for(const Plan &p) { return std::max(smem_ab_for(p), smem_c_for(p)); }  // odd plane strides
 
 template <class T>
@@ -240,6 +242,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     for (int g = 0; g < ST_COUNT; ++g) d.nblk[g] = p.nblk[g];
     d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
     d.wr_blk = at<double>(b, o.wr_blk);
+    d.crit_list = at<int32_t>(b, o.crit_list);
     ctx->epart = at<double>(b, o.epart);
     ctx->n_epart_edges = p.nblk[ST_AB];
     ctx->n_epart_nodes = (h.N + 255) / 256;
@@ -734,8 +737,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
-            launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr);
-            ctx->launches += ST_COUNT;
+            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr);
             cem_status st = exchange_nccl_step(ctx, (int)(sstep & 1));
             if (st) return st;
         }
@@ -756,11 +758,10 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * (ST_COUNT + 1) : nullptr;
-            launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E);
+            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E);
         }
         CUDA_TRY(cudaGetLastError());
         if (ctx->profiling) ctx->prof_steps += nsteps;
-        ctx->launches += ST_COUNT * nsteps;
         ctx->step += nsteps;
         return CEM_OK;
     }
@@ -999,8 +1000,7 @@ cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_
     for (int64_t i = 0; i < nsteps; ++i) {
         const int64_t sstep = c[0]->step + i;
         for (int r = 0; r < n; ++r) {
-            launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr);
-            c[r]->launches += ST_COUNT;
+            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr);
         }
         cem_status st = exchange_loopback(c, n, (int)(sstep & 1));
         if (st) return st;

@@ -148,7 +148,8 @@ struct Dev {
     const uint16_t *lconn, *ledge;
     int smem_bytes, smem_ab, smem_c;  // dynamic shared memory: persistent kernel (max), per stage
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
-    int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] spare
+    int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length
+    int32_t *crit_list;        // [E] tets stage C flagged for the full criterion this step (staged path)
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
     double *rec_G, *rec_area;
@@ -168,7 +169,7 @@ struct Dev {
 
 // cem_kernels.cu
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
-void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/);
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*4 or null*/);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel

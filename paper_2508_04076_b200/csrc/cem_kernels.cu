@@ -431,109 +431,174 @@ __device__ double sig_proj(const Eig &E, Vec3 m) {
 
 __device__ __forceinline__ double dsgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
 
-// All 24 candidates of tet e (R7): corner c, front {p,q} among the other nodes
-// o0<o1<o2 as (o0,o1),(o0,o2),(o1,o2), r the remaining node, k = 6c + 2f + t;
-// t=0 pattern I (eq:G-I) with m = (X_q-X_p)x(X_r-X_c), t=1 pattern II (eq:G-II) with
-// m = (X_q-X_p)x(X_r-X_p).  Select max G, ties -> larger area, then lower k.
-// Re-gathers its inputs (runs for the few tets that fail the early-out).
-__device__ __noinline__ void evaluate_tet(const Dev *__restrict__ dp, int64_t e, const double4 *u, double &Gbest, int &kbest,
-                                          double &Abest) {
-    const Dev &d = *dp;
-    const int4 t = __ldg(&d.conn[e]);
-    const int nid[4] = {t.x, t.y, t.z, t.w};
-    Vec3 Xn[4], un[4];
-    for (int a = 0; a < 4; ++a) {
-        const double4 x = ldro4(&d.X[nid[a]]);
-        const double4 uu = ldcg256(&u[nid[a]]);
-        Xn[a] = {x.x, x.y, x.z};
-        un[a] = {uu.x, uu.y, uu.z};
-    }
+// Full criterion of one tet, evaluated by a whole warp (the tets that fail the early-out;
+// called with all 32 lanes, uniform arguments).  Lanes 0-3 gather the nodes, lanes 0-5 the
+// Heaviside flags and the principal pair of their edge's sigma (R6, R8), lanes
+// 0-23 one candidate each, k = 6c + 2f + t (R7): corner c, front {p,q} among the other nodes
+// o0<o1<o2 as (o0,o1),(o0,o2),(o1,o2), r the remaining node; t=0 pattern I (eq:G-I) with
+// m = (X_q-X_p)x(X_r-X_c), t=1 pattern II (eq:G-II) with m = (X_q-X_p)x(X_r-X_p).  The
+// selection (max G, ties -> larger area, then lower k; R14) is a butterfly argmax over
+// (G, area, -k), which equals the oracle's sequential scan.  Split: deactivate
+// now (this step's readers of the state are done), append a record (unordered; sorted by
+// (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
+#ifndef CEM_CRIT_COOP_MAX
+#define CEM_CRIT_COOP_MAX 1
+#endif
+struct CritScratch {
+    double X[4][3], U[4][3];
     int H[6];
-    for (int l = 0; l < 6; ++l) {
-        const Vec3 du = vsub(un[c_eq[l]], un[c_ep[l]]);
-        const Vec3 dX = vsub(Xn[c_eq[l]], Xn[c_ep[l]]);
-        const Vec3 w = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
-        H[l] = vdot(du, w) > 0.0;  // eq:stretch-delta Heaviside, R6
-    }
     Eig eg[6];
-    for (int l = 0; l < 6; ++l) {
-        const double *sg = d.srec + 6 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
-        double s6[6];
-        for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
-        principal(s6, eg[l]);
-    }
-    Gbest = 0.0;
-    kbest = -1;
-    Abest = 0.0;
-    for (int c = 0; c < 4; ++c) {
-        int o[3], no = 0;
-        for (int b = 0; b < 4; ++b)
-            if (b != c) o[no++] = b;
-        for (int f = 0; f < 3; ++f) {
-            const int p = o[f == 2 ? 1 : 0], q = o[f == 0 ? 1 : 2], r = o[2 - f];
-            for (int tt = 0; tt < 2; ++tt) {
-                const Vec3 d1 = vsub(Xn[q], Xn[p]);
-                const Vec3 d2 = tt == 0 ? vsub(Xn[r], Xn[c]) : vsub(Xn[r], Xn[p]);
-                const Vec3 mv = vcross(d1, d2);
-                const double mm = vdot(mv, mv);
-                double Dd[2];
-                const int ends[2] = {p, q};
-                for (int z = 0; z < 2; ++z) {
-                    const int b = ends[z];
-                    if (!H[ledge(c, b)]) {
-                        Dd[z] = 0.0;
-                        continue;
-                    }
-                    const Vec3 du = vsub(un[b], un[c]), dX = vsub(Xn[b], Xn[c]);
-                    Dd[z] = vdot(du, mv) * dsgn(vdot(dX, mv));
-                }
-                double G, area;
-                if (tt == 0) {
-                    const double A1 = sig_proj(eg[ledge(p, r)], mv) * Dd[0];
-                    const double A2 = sig_proj(eg[ledge(q, r)], mv) * Dd[1];
-                    G = (0.5 * (A1 + A2)) / mm;
-                    area = sqrt(mm) / 4.0;
-                } else {
-                    const double Sg = sig_proj(eg[ledge(c, r)], mv);
-                    G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
-                    area = sqrt(mm) / 8.0;
-                }
-                const int k = 6 * c + 2 * f + tt;
-                if (kbest < 0 || G > Gbest || (G == Gbest && area > Abest)) {
-                    Gbest = G;
-                    kbest = k;
-                    Abest = area;
-                }
-            }
+};
+
+static_assert(sizeof(CritScratch) <= 1024, "stage C's staging area holds 8 warp scratches of <= 1 KB");
+
+__device__ void candidate(const CritScratch &w, int k, double &G, double &area) {
+    const int c = k / 6, f = (k % 6) / 2, tt = k & 1;
+    int o[3], no = 0;
+    for (int b = 0; b < 4; ++b)
+        if (b != c) o[no++] = b;
+    const int p = o[f == 2 ? 1 : 0], q = o[f == 0 ? 1 : 2], r = o[2 - f];
+    auto X = [&](int a) { return Vec3{w.X[a][0], w.X[a][1], w.X[a][2]}; };
+    auto U = [&](int a) { return Vec3{w.U[a][0], w.U[a][1], w.U[a][2]}; };
+    const Vec3 d1 = vsub(X(q), X(p));
+    const Vec3 d2 = tt == 0 ? vsub(X(r), X(c)) : vsub(X(r), X(p));
+    const Vec3 mv = vcross(d1, d2);
+    const double mm = vdot(mv, mv);
+    double Dd[2];
+    const int ends[2] = {p, q};
+    for (int z = 0; z < 2; ++z) {
+        const int b = ends[z];
+        if (!w.H[ledge(c, b)]) {
+            Dd[z] = 0.0;
+            continue;
         }
+        const Vec3 du = vsub(U(b), U(c)), dX = vsub(X(b), X(c));
+        Dd[z] = vdot(du, mv) * dsgn(vdot(dX, mv));
+    }
+    if (tt == 0) {
+        const double A1 = sig_proj(w.eg[ledge(p, r)], mv) * Dd[0];
+        const double A2 = sig_proj(w.eg[ledge(q, r)], mv) * Dd[1];
+        G = (0.5 * (A1 + A2)) / mm;
+        area = sqrt(mm) / 4.0;
+    } else {
+        const double Sg = sig_proj(w.eg[ledge(c, r)], mv);
+        G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
+        area = sqrt(mm) / 8.0;
     }
 }
 
-// split: deactivate now (stage B/C of this step already consumed the
-// state; later readers are next-step stages), append a record (unordered; the host sorts
-// by (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
-__device__ __noinline__ void criterion_full(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc, int64_t rec_step,
-                                            int32_t stamp, bool record) {
-    const Dev &d = *dp;
-    double G, A;
-    int k;
-    evaluate_tet(dp, e, u, G, k, A);
-    if (G > gc) {
-        d.state[e] = 0;
-        if (record) {  // multi-GPU: only the owning rank records (every holder deactivates)
-            const int slot = atomicAdd(&d.ctr[0], 1);
-            d.rec_step[slot] = rec_step;
-            d.rec_elem[slot] = ldro(d.tet_orig + e);
-            d.rec_cand[slot] = k;
-            d.rec_G[slot] = G;
-            d.rec_area[slot] = A;
-        }
-        const int4 t = __ldg(&d.conn[e]);
-        d.dirty[t.x] = stamp;
-        d.dirty[t.y] = stamp;
-        d.dirty[t.z] = stamp;
-        d.dirty[t.w] = stamp;
+__device__ __forceinline__ void split_tet(const Dev &d, int64_t e, int4 t, double G, int k, double A, int64_t rec_step,
+                                          int32_t stamp, bool record) {
+    d.state[e] = 0;
+    if (record) {  // multi-GPU: only the owning rank records (every holder deactivates)
+        const int slot = atomicAdd(&d.ctr[0], 1);
+        d.rec_step[slot] = rec_step;
+        d.rec_elem[slot] = ldro(d.tet_orig + e);
+        d.rec_cand[slot] = k;
+        d.rec_G[slot] = G;
+        d.rec_area[slot] = A;
     }
+    d.dirty[t.x] = stamp;
+    d.dirty[t.y] = stamp;
+    d.dirty[t.z] = stamp;
+    d.dirty[t.w] = stamp;
+}
+
+// The same criterion evaluated by one lane (used when many lanes of a warp need it: they
+// then run it side by side): the oracle's sequential scan over k = 0..23.
+__device__ __noinline__ void criterion_lane(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc,
+                                            int64_t rec_step, int32_t stamp, bool record) {
+    const Dev &d = *dp;
+    CritScratch w;
+    const int4 t = __ldg(&d.conn[e]);
+    const int nid[4] = {t.x, t.y, t.z, t.w};
+    for (int a = 0; a < 4; ++a) {
+        const double4 x = ldro4(&d.X[nid[a]]);
+        const double4 uu = ldcg256(&u[nid[a]]);
+        w.X[a][0] = x.x;
+        w.X[a][1] = x.y;
+        w.X[a][2] = x.z;
+        w.U[a][0] = uu.x;
+        w.U[a][1] = uu.y;
+        w.U[a][2] = uu.z;
+    }
+    for (int l = 0; l < 6; ++l) {
+        const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
+                         w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
+        const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
+                         w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
+        const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+        w.H[l] = vdot(du, ww) > 0.0;
+        const double *sg = d.srec + 6 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
+        double s6[6];
+        for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
+        principal(s6, w.eg[l]);
+    }
+    double Gb = 0.0, Ab = 0.0;
+    int kb = -1;
+    for (int k = 0; k < 24; ++k) {
+        double G, A;
+        candidate(w, k, G, A);
+        if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
+            Gb = G;
+            kb = k;
+            Ab = A;
+        }
+    }
+    if (Gb > gc) split_tet(d, e, t, Gb, kb, Ab, rec_step, stamp, record);
+}
+
+__device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc,
+                                            int64_t rec_step, int32_t stamp, bool record, CritScratch &w) {
+    const Dev &d = *dp;
+    const int lane = threadIdx.x & 31;
+    const int4 t = __ldg(&d.conn[e]);
+    if (lane < 4) {
+        const int n = lane == 0 ? t.x : (lane == 1 ? t.y : (lane == 2 ? t.z : t.w));
+        const double4 x = ldro4(&d.X[n]);
+        const double4 uu = ldcg256(&u[n]);
+        w.X[lane][0] = x.x;
+        w.X[lane][1] = x.y;
+        w.X[lane][2] = x.z;
+        w.U[lane][0] = uu.x;
+        w.U[lane][1] = uu.y;
+        w.U[lane][2] = uu.z;
+    }
+    __syncwarp();
+    if (lane < 6) {
+        const int l = lane;
+        const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
+                         w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
+        const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
+                         w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
+        const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+        w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
+        const double *sg = d.srec + 6 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
+        double s6[6];
+        for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
+        Eig eg;
+        principal(s6, eg);
+        w.eg[l] = eg;
+    }
+    __syncwarp();
+    double G = -INFINITY, A = -INFINITY;
+    int k = 1 << 20;
+    if (lane < 24) {
+        candidate(w, lane, G, A);
+        k = lane;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double G2 = __shfl_xor_sync(0xffffffffu, G, o), A2 = __shfl_xor_sync(0xffffffffu, A, o);
+        const int k2 = __shfl_xor_sync(0xffffffffu, k, o);
+        if (G2 > G || (G2 == G && (A2 > A || (A2 == A && k2 < k)))) {
+            G = G2;
+            A = A2;
+            k = k2;
+        }
+    }
+    if (lane == 0 && G > gc) split_tet(d, e, t, G, k, A, rec_step, stamp, record);
+    __syncwarp();  // the scratch is reused by the warp's next call
 }
 
 // ------------------------------------------------------------------ stage C: force + criterion
@@ -557,7 +622,7 @@ __device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double2 x
     sm[6 * np + i] = fmax(r0, fmax(r1, r2));
 }
 __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
-                                        int32_t stamp, double *sm) {
+                                        int32_t stamp, double *sm, bool defer = false) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t s0i = __ldg(d.el_off + b);
     const int ne = __ldg(d.el_off + b + 1) - s0i;
@@ -631,58 +696,91 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         cc = __ldg(gp + 32);
     }
     __syncthreads();
-    if (!he) return;
-    // slot (e,a) = slot0 + 32 a, CEM_FES doubles per slot
-    double *fo = d.fe + CEM_FES * (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));
-    if (!act) {
+    bool need = false;  // this tet needs the full criterion (failed the early-out)
+    if (he) {
+        // slot (e,a) = slot0 + 32 a, CEM_FES doubles per slot
+        double *fo = d.fe + CEM_FES * (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));
+        if (!act) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) store_slot(fo + 32 * CEM_FES * a, 0.0, 0.0, 0.0);
+            for (int a = 0; a < 4; ++a) store_slot(fo + 32 * CEM_FES * a, 0.0, 0.0, 0.0);
+        } else {
+            const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
+                               (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
+            double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
+#pragma unroll
+            for (int l = 0; l < 6; ++l) {
+                const int r = le[l];
+                S0 = S0 + sm[r];
+                S1 = S1 + sm[np + r];
+                S2 = S2 + sm[2 * np + r];
+                S3 = S3 + sm[3 * np + r];
+                S4 = S4 + sm[4 * np + r];
+                S5 = S5 + sm[5 * np + r];
+                gmax = fmax(gmax, sm[6 * np + r]);
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
+                const double fy = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
+                const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
+                store_slot(fo + 32 * CEM_FES * a, fx, fy, fz);
+            }
+            // ghost tets (tflag bit 0 clear): the owner decides, the state arrives by exchange
+            need = crack && (tf & 1);
+            if (need && early) {
+                const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+                double ux[4], uy[4], uz[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    ux[a] = smu[li[a]];
+                    uy[a] = smu[nq + li[a]];
+                    uz[a] = smu[2 * nq + li[a]];
+                }
+                double d2 = 0.0;
+#pragma unroll
+                for (int l = 0; l < 6; ++l) {
+                    const int p = l < 3 ? 0 : (l < 5 ? 1 : 2), q = l < 3 ? l + 1 : (l < 5 ? l - 1 : 3);
+                    const double dx = ux[q] - ux[p], dy = uy[q] - uy[p], dz = uz[q] - uz[p];
+                    d2 = fmax(d2, (dx * dx + dy * dy) + dz * dz);
+                }
+                need = !(gmax * sqrt(d2) * (1.0 + 1e-6) <= gc);
+            }
+        }
+    }
+    if (!crack) return;  // block-uniform
+    if (defer) {
+        // staged path: append the flagged tets to the step's list (warp-aggregated); k_crit
+        // evaluates them all concurrently, one warp per tet, before stage D
+        const unsigned mm = __ballot_sync(0xffffffffu, need);
+        if (mm) {
+            const int lane = threadIdx.x & 31, lead = __ffs(mm) - 1;
+            int base = 0;
+            if (lane == lead) base = atomicAdd(&d.ctr[3], __popc(mm));
+            base = __shfl_sync(0xffffffffu, base, lead);
+            if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = (int32_t)e;
+        }
         return;
     }
-    const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
-                       (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
-#pragma unroll
-    for (int l = 0; l < 6; ++l) {
-        const int r = le[l];
-        S0 = S0 + sm[r];
-        S1 = S1 + sm[np + r];
-        S2 = S2 + sm[2 * np + r];
-        S3 = S3 + sm[3 * np + r];
-        S4 = S4 + sm[4 * np + r];
-        S5 = S5 + sm[5 * np + r];
-        gmax = fmax(gmax, sm[6 * np + r]);
+    // few flagged tets in the warp: the warp evaluates them one after another, 24 candidates
+    // in parallel (scratch in the staging area, free after the barrier); many: each lane
+    // evaluates its own (side by side)
+    unsigned m = __ballot_sync(0xffffffffu, need);
+    __syncthreads();
+    if (__popc(m) > CEM_CRIT_COOP_MAX) {
+        if (need) criterion_lane(d.self, e, u, gc, rec_step, stamp, (tf & 2) != 0);
+        return;
     }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
-        const double fy = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
-        const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
-        store_slot(fo + 32 * CEM_FES * a, fx, fy, fz);
+    CritScratch &cs = reinterpret_cast<CritScratch *>(sm)[threadIdx.x >> 5];
+    while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t te = __shfl_sync(0xffffffffu, e, src);
+        const double tgc = __shfl_sync(0xffffffffu, gc, src);
+        const int trec = __shfl_sync(0xffffffffu, (int)(tf & 2), src);
+        criterion_warp(d.self, te, u, tgc, rec_step, stamp, trec != 0, cs);
     }
-    if (!crack) return;
-    if (!(tf & 1)) return;  // ghost tet: its owner decides, the state arrives by exchange
-    if (early) {
-        const int li[4] = {lc.x, lc.y, lc.z, lc.w};
-        double ux[4], uy[4], uz[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            ux[a] = smu[li[a]];
-            uy[a] = smu[nq + li[a]];
-            uz[a] = smu[2 * nq + li[a]];
-        }
-        double d2 = 0.0;
-#pragma unroll
-        for (int l = 0; l < 6; ++l) {
-            const int p = l < 3 ? 0 : (l < 5 ? 1 : 2), q = l < 3 ? l + 1 : (l < 5 ? l - 1 : 3);
-            const double dx = ux[q] - ux[p], dy = uy[q] - uy[p], dz = uz[q] - uz[p];
-            d2 = fmax(d2, (dx * dx + dy * dy) + dz * dz);
-        }
-        if (gmax * sqrt(d2) * (1.0 + 1e-6) <= gc) return;
-    }
-    criterion_full(d.self, e, u, gc, rec_step, stamp, (tf & 2) != 0);
 }
 
 // ------------------------------------------------------------------ stage D: node update
@@ -694,6 +792,10 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
     const int c = threadIdx.x & 3;
     const int64_t k = kbase + (threadIdx.x >> 2);
+    if (kbase == 0 && threadIdx.x == 0) {  // k_crit (if any) has consumed the step's list
+        pdl_wait();
+        d.ctr[3] = 0;
+    }
     if (k >= d.N) return 0.0;
     const uint8_t fl = __ldg(&d.nflag[k]);
     if (fl & 16) return 0.0;  // multi-GPU: another rank owns (and updates) this node
@@ -783,7 +885,7 @@ __device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const doubl
     }
 }
 
-__device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
+__host__ __device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
     return crack_every > 0 && ((s + 1) % crack_every) == 0;
 }
 
@@ -922,7 +1024,20 @@ __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
 __global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every) {
     extern __shared__ double sm[];
     pdl_trigger();
-    block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
+    block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true);
+}
+// full criterion of the tets stage C flagged (ctr[3] of them in crit_list), one warp per tet
+__global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
+    __shared__ CritScratch scratch[8];
+    pdl_trigger();
+    pdl_wait();  // the list and the sigma records come from stage C / AB
+    const int n = *(volatile int32_t *)&d.ctr[3];
+    const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+    for (int i = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); i < n; i += nw) {
+        const int64_t e = d.crit_list[i];
+        criterion_warp(d.self, e, d.ubuf[(s + 1) & 1], ldro(d.gc + e), s + 1, (int32_t)(s + 1),
+                       (__ldg(d.tflag + e) & 2) != 0, scratch[threadIdx.x >> 5]);
+    }
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     pdl_trigger();
@@ -1026,20 +1141,25 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-void launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
+    const bool crit = crack_on(crack_every, s);
+    const unsigned gcrit = 148 * 8;  // one warp per flagged tet, grid-stride
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
         launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
         launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
+        if (crit) launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
         launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
-        return;
+        return crit ? 4 : 3;
     }
-    if (ev) cudaEventRecord(ev[0], st);
+    cudaEventRecord(ev[0], st);
     k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
-    if (ev) cudaEventRecord(ev[1], st);
+    cudaEventRecord(ev[1], st);
     k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
-    if (ev) cudaEventRecord(ev[2], st);
+    if (crit) k_crit<<<gcrit, 256, 0, st>>>(d, s);  // timed with stage C
+    cudaEventRecord(ev[2], st);
     k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
-    if (ev) cudaEventRecord(ev[3], st);
+    cudaEventRecord(ev[3], st);
+    return crit ? 4 : 3;
 }
 
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st) {

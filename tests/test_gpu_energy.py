@@ -87,3 +87,16 @@ def test_ledger_full_size_edge_impact():
     sim.step(6, 1)
     orc.run(6, 1)
     _check(sim.energy(), orc.energy(), p.n_tets * 6)
+
+
+def test_ledger_compact_tension():
+    """N2 workload: driven and held slot faces both enter the reaction work."""
+    cem = _gpu()
+    p = ci.compact_tension(cells=(24, 24, 3), dims=(0.2, 0.2, 0.025), v0=60.0, t0=20e-6)
+    sim = cem.Simulation.from_problem(p)
+    orc = oracle.Oracle(p)
+    sim.step(200, 1)
+    orc.run(200, 1)
+    g, o = sim.energy(), orc.energy()
+    _check(g, o, p.n_tets * 6)
+    assert o["reaction"] > 0.0

@@ -200,3 +200,19 @@ def test_full_size_config_bitwise(k, steps):
     p = ci.config(k)
     sim, orc = run_pair(p, steps, 1)
     assert_parity(sim, orc, p)
+
+
+@pytest.mark.parametrize("v0", [1.375, 3.993])
+def test_compact_tension_dirichlet_branching(v0):
+    """N2 workload: slot faces driven / held in x, fracture every step."""
+    p = ci.compact_tension(cells=(24, 24, 3), dims=(0.2, 0.2, 0.025), v0=40 * v0, t0=20e-6)
+    sim, orc = run_pair(p, 300)
+    g = assert_parity(sim, orc, p)
+    assert g.rec_elem.size > 0
+
+
+def test_compact_tension_full_size():
+    """cfg6 (259k tets, v0 = 3.318 m/s) in the launch configuration bench.py uses."""
+    p = ci.config(6)
+    sim, orc = run_pair(p, 8)
+    assert_parity(sim, orc, p)

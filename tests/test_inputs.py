@@ -92,3 +92,19 @@ def test_edge_impact_plate_small():
     assert p.vbc_node.size == (12 * 3 // 4 - 12 // 4 + 1) * 3
     assert np.all(p.X[p.vbc_node, 0] == 0.0)
     assert (p.tet_state == 0).sum() == 2 * (20 // 4) * 2 * 6
+
+
+def test_compact_tension_small():
+    """N2 stand-in: a two-cell slot from the top to 40 % depth; right slot face driven in x, left held."""
+    nx, ny, nz = 16, 20, 3
+    p = ci.compact_tension(cells=(nx, ny, nz), dims=(0.16, 0.2, 0.03), v0=3.318)
+    depth = 8
+    assert (p.tet_state == 0).sum() == 2 * depth * nz * 6
+    assert p.vbc_node.size == 2 * (depth + 1) * (nz + 1)
+    assert np.all(np.diff(p.vbc_node) > 0)
+    assert np.all(p.vbc_mask == 1)
+    ijk = p.node_ijk[p.vbc_node]
+    assert set(np.unique(ijk[:, 0])) == {nx // 2 - 1, nx // 2 + 1}
+    assert np.all(p.vbc_v0[ijk[:, 0] == nx // 2 + 1, 0] == 3.318)
+    assert np.all(p.vbc_v0[ijk[:, 0] == nx // 2 - 1] == 0.0)
+    assert p.vbc_t0 == 100e-6 and p.E == 36e9 and p.nu == 0.18 and p.Gc == 65.0
