@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 VB="python scripts/variant_bench.py 0 400"
 $VB > $OUT/plain_vb.log 2>&1 || { echo "variant_bench failed"; exit 1; }
 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-    -k regex:'k_(AB|C|D)$' -s 1050 -c 9 --csv --log-file $OUT/live_traffic.csv $VB > $OUT/ncu_live.log 2>&1
+    -k regex:'k_(AB|C|crit|D)$' -s 1400 -c 12 --csv --log-file $OUT/live_traffic.csv $VB > $OUT/ncu_live.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'k_(AB|C|D)$' -s 1050 -c 3 -o $OUT/prof_stages \
     $VB > $OUT/ncu_full.log 2>&1
 echo done

@@ -30,11 +30,18 @@ def metric_csv(path):
 
 
 def steps_of(launches):
-    st = [x for x in launches if x[1] in STAGES]
-    out = []
-    for j in range(len(st) - 2):
-        if [st[j][1], st[j + 1][1], st[j + 2][1]] == list(STAGES):
-            out.append(st[j:j + 3])
+    """Complete steps k_AB, k_C, [k_crit], k_D in launch order (k_crit: the criterion list kernel)."""
+    st = [x for x in launches if x[1] in STAGES + ("k_crit",)]
+    out, cur = [], []
+    for x in st:
+        if x[1] == "k_AB":
+            cur = [x]
+        elif cur:
+            cur.append(x)
+            if x[1] == "k_D":
+                if [y[1] for y in cur if y[1] != "k_crit"] == list(STAGES):
+                    out.append(cur)
+                cur = []
     return out
 
 
@@ -50,8 +57,9 @@ for stp in live_steps:
     for _, n, m in stp:
         for k, v in m.items():
             live[n][k] += v / len(live_steps)
-live_bytes = sum(live[n]["dram__bytes_read.sum"] + live[n]["dram__bytes_write.sum"] for n in STAGES)
-live_t = sum(live[n]["gpu__time_duration.sum"] for n in STAGES)
+ALL = STAGES + (("k_crit",) if "k_crit" in live else ())
+live_bytes = sum(live[n]["dram__bytes_read.sum"] + live[n]["dram__bytes_write.sum"] for n in ALL)
+live_t = sum(live[n]["gpu__time_duration.sum"] for n in ALL)
 shutil.copy(os.path.join(g, "live_traffic.csv"), os.path.join(out_dir, f"{rnd}_live_traffic.csv"))
 
 # ---- full captures (steady state)
@@ -83,7 +91,7 @@ json.dump({"round": rnd,
            "dram_bytes_per_step_live": live_bytes,
            "ncu_step_time_ns_live": live_t,
            "per_kernel_live": {n: {"time_ns": live[n]["gpu__time_duration.sum"], "dram_read": live[n]["dram__bytes_read.sum"],
-                                   "dram_write": live[n]["dram__bytes_write.sum"]} for n in STAGES},
+                                   "dram_write": live[n]["dram__bytes_write.sum"]} for n in ALL},
            "source": {"dram_bytes_per_step": "ncu --set full (default cache flush) of k_AB, k_C, k_D at step ~350",
                       "dram_bytes_per_step_live": "ncu --cache-control none --metrics dram__bytes_*.sum, steady state"}},
           open(os.path.join(out_dir, "traffic_per_step.json"), "w"), indent=1)
