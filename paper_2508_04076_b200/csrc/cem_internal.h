@@ -15,9 +15,11 @@
 
 namespace cem {
 
-// doubles per force slot: 4 = (x, y, z, 0) in one 32-B sector, 3 = packed (x, y, z)
+// force-slot layout: 3 (default) = the 4 slots of a tet packed (12 doubles, 96 B per tet, slot
+// index 4e + a, written with three 256-bit stores); 4 = warp-tiled (x, y, z, 0) slots, one 32-B
+// sector each, slot index ((e>>5)*4 + a)*32 + (e&31)
 #ifndef CEM_FES
-#define CEM_FES 4
+#define CEM_FES 3
 #endif
 
 // phase timer of the host preprocessing (CEM_TIMING=1 prints to stderr)
@@ -137,7 +139,7 @@ struct Dev {
     double *rprev;             // [N][3] support force of prescribed dofs at the last step (NULL: none)
     double *wr_blk;            // [staged D blocks] reaction work accumulated per block (energy ledger)
     double *srec;              // [S][6]: sigma_s (11,22,33,12,23,13), 48-B records
-    double *fe;                // [4E][CEM_FES] force slots f_{e,a}; slot(e,a) = ((e>>5)*4 + a)*32 + (e&31)
+    double *fe;                // force slots f_{e,a}, CEM_FES doubles per slot (see CEM_FES)
     const double *geoT;        // [E/32][11][32] warp-tiled geometry
     const uint16_t *incE;      // [S][we]
     const int32_t *nodeE;      // [N][wn]

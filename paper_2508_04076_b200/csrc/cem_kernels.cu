@@ -88,7 +88,11 @@ __device__ __forceinline__ double4 ldcg256(const double4 *p) {
 
 // warp-tiled geometry: tet e -> tile e>>5, lane e&31, component c at [tile][c][lane]
 __device__ __forceinline__ const double *geo_ptr(const Dev &d, uint32_t e) { return d.geoT + ((e >> 5) * 352u + (e & 31u)); }
+#if CEM_FES == 3
+__device__ __forceinline__ int64_t slot_tet(int32_t slot) { return slot >> 2; }  // slot = 4e + a
+#else
 __device__ __forceinline__ int64_t slot_tet(int32_t slot) { return ((int64_t)(slot >> 7) << 5) + (slot & 31); }
+#endif
 
 // lumped mass of node k from its active incidences in original order
 __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
@@ -698,11 +702,20 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     __syncthreads();
     bool need = false;  // this tet needs the full criterion (failed the early-out)
     if (he) {
+#if CEM_FES == 3
+        // the tet's 4 slots packed (f0, f1, f2, f3: 12 doubles, 96 B) -> three 256-bit stores
+        double *fo = d.fe + 12 * (uint32_t)e;
+#else
         // slot (e,a) = slot0 + 32 a, CEM_FES doubles per slot
         double *fo = d.fe + CEM_FES * (((uint32_t)e >> 5) * 128u + ((uint32_t)e & 31u));
+#endif
         if (!act) {
+#if CEM_FES == 3
+            for (int q = 0; q < 3; ++q) st256(reinterpret_cast<double4 *>(fo) + q, 0.0, 0.0, 0.0, 0.0);
+#else
 #pragma unroll
             for (int a = 0; a < 4; ++a) store_slot(fo + 32 * CEM_FES * a, 0.0, 0.0, 0.0);
+#endif
         } else {
             const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
                                (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
@@ -720,6 +733,18 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
             }
 #pragma unroll
             for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+#if CEM_FES == 3
+            double f[12];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                f[3 * a] = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
+                f[3 * a + 1] = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
+                f[3 * a + 2] = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
+            }
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                st256(reinterpret_cast<double4 *>(fo) + q, f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+#else
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 const double fx = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
@@ -727,6 +752,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
                 const double fz = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
                 store_slot(fo + 32 * CEM_FES * a, fx, fy, fz);
             }
+#endif
             // ghost tets (tflag bit 0 clear): the owner decides, the state arrives by exchange
             need = crack && (tf & 1);
             if (need && early) {

@@ -460,7 +460,11 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         for (int64_t k = 0; k < N; ++k)
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) {
                 const int64_t e = p.node_ent[j] >> 2, a = p.node_ent[j] & 3;
+#if CEM_FES == 3
+                p.nodeE[(size_t)k * p.wn + (j - p.node_off[k])] = (int32_t)(4 * e + a);  // packed per tet
+#else
                 p.nodeE[(size_t)k * p.wn + (j - p.node_off[k])] = (int32_t)((((e >> 5) * 4 + a) << 5) + (e & 31));
+#endif
             }
     }
     clk.mark("plan: ELL tables");
