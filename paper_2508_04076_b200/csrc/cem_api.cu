@@ -87,7 +87,7 @@ struct Offs {
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
-    size_t nlb_off, nlb, tconn, tflag;
+    size_t nlb_off, nlb, tconn, trow, nrow, tflag;
     size_t rprev, wr_blk, epart, crit_list;
     size_t total;
 };
@@ -145,6 +145,8 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.nlb_off = L.take<int32_t>((int64_t)p.nlb_off.size());
     o.nlb = L.take<int32_t>((int64_t)p.nlb.size());
     o.tconn = L.take<uint16_t>((int64_t)p.tconn.size());
+    o.trow = L.take<uint16_t>((int64_t)p.trow.size());
+    o.nrow = L.take<uint16_t>((int64_t)p.nrow.size());
     o.tflag = L.take<uint8_t>(E);
     o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.wr_blk = L.take<double>(n_wr_blocks(N, p.blk));
@@ -214,6 +216,8 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.nlb_off = at<int32_t>(b, o.nlb_off);
     d.nlb = at<int32_t>(b, o.nlb);
     d.tconn = at<uint16_t>(b, o.tconn);
+    d.trow = at<uint16_t>(b, o.trow);
+    d.nrow = at<uint16_t>(b, o.nrow);
     d.tflag = at<uint8_t>(b, o.tflag);
     d.ctr = at<int32_t>(b, o.ctr);
     d.rec_step = at<int64_t>(b, o.rec_step);
@@ -353,6 +357,8 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.nlb_off, p.nlb_off.data(), sizeof(int32_t) * p.nlb_off.size()));
     CUDA_TRY(put(o.nlb, p.nlb.data(), sizeof(int32_t) * p.nlb.size()));
     CUDA_TRY(put(o.tconn, p.tconn.data(), sizeof(uint16_t) * p.tconn.size()));
+    CUDA_TRY(put(o.trow, p.trow.data(), sizeof(uint16_t) * p.trow.size()));
+    CUDA_TRY(put(o.nrow, p.nrow.data(), sizeof(uint16_t) * p.nrow.size()));
     CUDA_TRY(put(o.tflag, p.tflag.data(), E));
     CUDA_TRY(put(o.self, &ctx->d, sizeof(Dev)));
     CUDA_TRY(cudaStreamSynchronize(st));

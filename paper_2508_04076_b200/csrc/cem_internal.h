@@ -99,7 +99,9 @@ struct Plan {
     std::vector<uint16_t> ledge;      // [E][8] index of each tet edge in its block's edge list (6 used)
     std::vector<int32_t> tl_off, tl;  // edge block -> sorted unique incident tet ids
     std::vector<int32_t> nlb_off, nlb;  // edge block -> sorted unique nodes of its tet list
-    std::vector<uint16_t> tconn;      // [|tl|][4] node index (in nlb) of each tet-list entry
+    std::vector<uint16_t> tconn;      // [|tl|][4] staging row (in nlb) of each tet-list entry's nodes
+    std::vector<uint16_t> trow;       // [|tl|] shared-memory row of each tet-list entry (bank-aware)
+    std::vector<uint16_t> nrow;       // [|nlb|] shared-memory row of each node-list entry (bank-aware)
     std::vector<uint16_t> inc_local;  // [6E] (CSR order of edge_inc) index into the edge block's tet list
     int max_nl = 0, max_el = 0, max_tl = 0, max_nlb = 0;
     // instruction-lean layouts
@@ -146,7 +148,7 @@ struct Dev {
     int we, wn, we_max;        // ELL widths; we_max = largest edge incidence count
     int32_t zslot;             // index of the all-zero force slot (ELL padding)
     const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
-    const uint16_t *tconn;
+    const uint16_t *tconn, *trow, *nrow;
     const uint16_t *lconn, *ledge;
     int smem_bytes, smem_ab, smem_c;  // dynamic shared memory: persistent kernel (max), per stage
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)

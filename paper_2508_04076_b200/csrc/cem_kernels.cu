@@ -236,45 +236,50 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const uint32_t e0 = has0 ? (uint32_t)__ldg(d.tl + t0 + tid) : 0u;
     double g0[4][3], V0 = 0.0;
     ushort4 lc0 = make_ushort4(0, 0, 0, 0);
+    int r0 = tid;  // shared-memory row of this thread's tet (bank-aware order, trow)
     if (has0) {
         load_geo(d, e0, g0, V0);
         lc0 = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + tid);
+        r0 = __ldg(d.trow + t0 + tid);
     }
     const int32_t k0 = tid < nn ? __ldg(d.nlb + n0 + tid) : 0;
+    const int q0 = tid < nn ? __ldg(d.nrow + n0 + tid) : 0;
     pdl_wait();  // u and the tet states come from the previous kernels
     const uint8_t act0 = has0 ? __ldcg(d.state + e0) : (uint8_t)0;
-    if (tid < nn) {  // one node per thread
+    if (tid < nn) {  // one node per thread (list in ascending order, rows bank-aware)
         const double4 w = ldcg256(u + k0);
-        U[tid] = w.x;
-        U[un + tid] = w.y;
-        U[2 * un + tid] = w.z;
+        U[q0] = w.x;
+        U[un + q0] = w.y;
+        U[2 * un + q0] = w.z;
     }
     for (int i = tid + nthr; i < nn; i += nthr) {
         const double4 w = ldcg256(u + __ldg(d.nlb + n0 + i));
-        U[i] = w.x;
-        U[un + i] = w.y;
-        U[2 * un + i] = w.z;
+        const int q = __ldg(d.nrow + n0 + i);
+        U[q] = w.x;
+        U[un + q] = w.y;
+        U[2 * un + q] = w.z;
     }
     __syncthreads();
     // inactive tet / sentinel: exact zeros. Running sums here never hold -0.0, so adding
     // +0.0 is bit-identical to skipping the entry.
     if (act0) {
         grad0(g0);
-        tau_row(T, tn, tid, U, un, g0, V0, lc0);
+        tau_row(T, tn, r0, U, un, g0, V0, lc0);
     } else if (tid <= nt) {
-        zero_row(T, tn, tid);
+        zero_row(T, tn, r0);  // (tid == nt: the sentinel row)
     }
     for (int i = tid + nthr; i <= nt; i += nthr) {
         const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
         double g[4][3], V;
         load_geo(d, e, g, V);
         const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + min(i, nt - 1));
+        const int r = i < nt ? (int)__ldg(d.trow + t0 + i) : nt;
         if (i == nt || !__ldcg(d.state + e)) {
-            zero_row(T, tn, i);
+            zero_row(T, tn, r);
             continue;
         }
         grad0(g);
-        tau_row(T, tn, i, U, un, g, V, lc);
+        tau_row(T, tn, r, U, un, g, V, lc);
     }
     const int64_t s = (int64_t)b * d.blk + tid;
     const bool hs = s < d.S;

@@ -372,6 +372,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             int wmax = 1;
             for (int64_t s = 0; s < S; ++s) wmax = std::max(wmax, p.edge_off[s + 1] - p.edge_off[s]);
             wmax = std::min(wmax, 8);
+            p.trow.assign(p.tl.size(), 0);
 #pragma omp parallel for schedule(dynamic, 16)
             for (int b = 0; b < nbs; ++b) {
                 std::vector<int32_t> goff, gitem, row;
@@ -379,7 +380,9 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
                 const int nt = p.tl_off[b + 1] - p.tl_off[b];
                 half_warp_groups(incw.data(), s0, s1, 8, wmax, goff, gitem, 0xFFFF);
                 bank_rows(nt, goff, gitem, row);
-                permute_rows(p.tl.data() + p.tl_off[b], nt, row);
+                // the list keeps ascending tet order (thread i gathers entry i: coalesced); entry i
+                // writes its tau into shared-memory row trow[i]
+                for (int i = 0; i < nt; ++i) p.trow[p.tl_off[b] + i] = (uint16_t)row[i];
                 for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j) p.inc_local[j] = (uint16_t)row[p.inc_local[j]];
             }
         }
@@ -405,6 +408,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         clk.mark("plan: AB node lists");
         // bank-aware order of the staged node lists: AB (lanes = tet-list rows, column a) and
         // C's early-out (lanes = tets, column a); C's edge lists (lanes = tets, column l)
+        p.nrow.assign(p.nlb.size(), 0);
 #pragma omp parallel for schedule(dynamic, 16)
         for (int b = 0; b < nbs; ++b) {
             std::vector<int32_t> goff, gitem, row;
@@ -412,7 +416,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             const int nt = p.tl_off[b + 1] - t0, nn = p.nlb_off[b + 1] - p.nlb_off[b];
             half_warp_groups(p.tconn.data() + 4 * (int64_t)t0, 0, nt, 4, 4, goff, gitem);
             bank_rows(nn, goff, gitem, row);
-            permute_rows(p.nlb.data() + p.nlb_off[b], nn, row);
+            for (int i = 0; i < nn; ++i) p.nrow[p.nlb_off[b] + i] = (uint16_t)row[i];  // staging row of entry i
             for (int64_t i = 4 * (int64_t)t0; i < 4 * (int64_t)(t0 + nt); ++i) p.tconn[i] = (uint16_t)row[p.tconn[i]];
         }
 #pragma omp parallel for schedule(dynamic, 16)
