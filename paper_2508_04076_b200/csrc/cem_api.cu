@@ -158,7 +158,11 @@ Offs layout(const HostMesh &h, const Plan &p) {
 
 int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1)); }
 // stage C reuses its staging area for the warps' criterion scratch (<= 8 warps x ~840 B)
-int smem_c_for(const Plan &p) { return std::max(8 * (7 * (p.max_el | 1) + 3 * (p.max_nl | 1)), 8 * 1024); }
+// (CEM_C_GEOX adds 3 planes of node coordinates; the default keeps stage C's shared memory small:
+// its blocks then share the SM with a larger L1, which stage C measurably needs)
+int smem_c_for(const Plan &p) {
+    return std::max(8 * (6 * (p.max_el | 1) + (CEM_C_GEOX ? 6 : 3) * (p.max_nl | 1)), 8 * 1024);
+}
 int smem_bytes_for(const Plan &p) { return std::max(smem_ab_for(p), smem_c_for(p)); }  // odd plane strides
 
 template <class T>

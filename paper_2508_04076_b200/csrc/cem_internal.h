@@ -22,6 +22,12 @@ namespace cem {
 #define CEM_FES 3
 #endif
 
+// 1: stage C recomputes the element geometry from staged node coordinates instead of reading
+// the 88-B geometry record (-75 MB/step DRAM, but +4 KB shared memory per block: slower)
+#ifndef CEM_C_GEOX
+#define CEM_C_GEOX 0
+#endif
+
 // phase timer of the host preprocessing (CEM_TIMING=1 prints to stderr)
 struct PhaseClock {
     bool on = getenv("CEM_TIMING") != nullptr;

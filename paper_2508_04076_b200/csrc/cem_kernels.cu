@@ -618,6 +618,7 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
 #ifndef CEM_C_KME
 #define CEM_C_KME 3
 #endif
+
 __device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double2 x, double2 y, double2 z) {
     sm[i] = x.x;
     sm[np + i] = x.y;
@@ -625,10 +626,6 @@ __device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double2 x
     sm[3 * np + i] = y.y;
     sm[4 * np + i] = z.x;
     sm[5 * np + i] = z.y;
-    const double r0 = fabs(x.x) + fabs(y.y) + fabs(z.y);
-    const double r1 = fabs(x.y) + fabs(y.y) + fabs(z.x);
-    const double r2 = fabs(y.x) + fabs(z.x) + fabs(z.y);
-    sm[6 * np + i] = fmax(r0, fmax(r1, r2));
 }
 __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
                                         int32_t stamp, double *sm, bool defer = false) {
@@ -639,16 +636,27 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int nn = __ldg(d.nl_off + b + 1) - n0;
     const bool early = crack && !(d.flags & CEM_F_NO_EARLY_OUT);
     const int np = pstride(ne), nq = pstride(nn);
-    double *smu = sm + 7 * np;
+    double *smu = sm + 6 * np;
     // ---- wave 1: list indices
     constexpr int kME = CEM_C_KME;  // sigma records per thread in flight (more -> tail loop)
     uint32_t sid[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m) sid[m] = tid + m * nthr < ne ? (uint32_t)__ldg(d.el + s0i + tid + m * nthr) : 0u;
+#if CEM_C_GEOX
+    // geometry from the block's node coordinates (static: staged before the dependency wait)
+    double *smx = smu + 3 * nq;
+    const int32_t nid = tid < nn ? __ldg(d.nl + n0 + tid) : 0;
+    for (int i = tid; i < nn; i += nthr) {
+        const double4 x = ldro4(&d.X[i == tid ? nid : __ldg(d.nl + n0 + i)]);
+        smx[i] = x.x;
+        smx[nq + i] = x.y;
+        smx[2 * nq + i] = x.z;
+    }
+#else
     const int32_t nid = (early && tid < nn) ? __ldg(d.nl + n0 + tid) : 0;
+#endif
     pdl_wait();  // sigma records come from stage AB
-    // ---- wave 2: gathered records (3 x 16-B loads each) -> planes 0..5; plane 6 holds the
-    // Gershgorin bound g_s = max_i sum_j |sigma_ij| used by the early-out
+    // ---- wave 2: gathered records (3 x 16-B loads each) -> planes 0..5
     double2 rx[kME], ry[kME], rz[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m)
@@ -694,17 +702,41 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         if (crack) {  // criterion inputs (static): issued with the rest, not after the force
             tf = __ldg(d.tflag + e);
             gc = ldro(d.gc + e);
+#if !CEM_C_GEOX
             if (early) lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
+#endif
         }
         lq = __ldg(reinterpret_cast<const uint4 *>(d.ledge) + e);
+#if CEM_C_GEOX
+        lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
+#else
         const double *gp = geo_ptr(d, (uint32_t)e);
 #pragma unroll
         for (int a = 1; a < 4; ++a)
 #pragma unroll
             for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
         cc = __ldg(gp + 32);
+#endif
     }
     __syncthreads();
+#if CEM_C_GEOX
+    if (he) {
+        // the host preprocessing's formula (cem_mesh.cpp, = the oracle's): d_a = X_a - X_0,
+        // det = d1.(d2 x d3), gradN1..3 = (d2xd3, d3xd1, d1xd2) / det, c = (det / 6) / 6
+        const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+        Vec3 xa[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xa[a] = Vec3{smx[li[a]], smx[nq + li[a]], smx[2 * nq + li[a]]};
+        const Vec3 d1 = vsub(xa[1], xa[0]), d2 = vsub(xa[2], xa[0]), d3 = vsub(xa[3], xa[0]);
+        const Vec3 c23 = vcross(d2, d3), c31 = vcross(d3, d1), c12 = vcross(d1, d2);
+        const double det = vdot(d1, c23);
+        const double inv = 1.0 / det;
+        cc = (det / 6.0) / 6.0;
+        g[1][0] = c23.x * inv; g[1][1] = c23.y * inv; g[1][2] = c23.z * inv;
+        g[2][0] = c31.x * inv; g[2][1] = c31.y * inv; g[2][2] = c31.z * inv;
+        g[3][0] = c12.x * inv; g[3][1] = c12.y * inv; g[3][2] = c12.z * inv;
+    }
+#endif
     bool need = false;  // this tet needs the full criterion (failed the early-out)
     if (he) {
 #if CEM_FES == 3
@@ -728,13 +760,20 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
                 const int r = le[l];
-                S0 = S0 + sm[r];
-                S1 = S1 + sm[np + r];
-                S2 = S2 + sm[2 * np + r];
-                S3 = S3 + sm[3 * np + r];
-                S4 = S4 + sm[4 * np + r];
-                S5 = S5 + sm[5 * np + r];
-                gmax = fmax(gmax, sm[6 * np + r]);
+                const double a0 = sm[r], a1 = sm[np + r], a2 = sm[2 * np + r];
+                const double a3 = sm[3 * np + r], a4 = sm[4 * np + r], a5 = sm[5 * np + r];
+                S0 = S0 + a0;
+                S1 = S1 + a1;
+                S2 = S2 + a2;
+                S3 = S3 + a3;
+                S4 = S4 + a4;
+                S5 = S5 + a5;
+                if (early) {  // Gershgorin bound g_s = max_i sum_j |sigma_ij| of the edge
+                    const double r0 = fabs(a0) + fabs(a3) + fabs(a5);
+                    const double r1 = fabs(a1) + fabs(a3) + fabs(a4);
+                    const double r2 = fabs(a2) + fabs(a4) + fabs(a5);
+                    gmax = fmax(gmax, fmax(r0, fmax(r1, r2)));
+                }
             }
 #pragma unroll
             for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
