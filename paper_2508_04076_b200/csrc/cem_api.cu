@@ -88,7 +88,7 @@ struct Offs {
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
-    size_t rprev, wr_blk, epart, crit_list;
+    size_t rprev, wr_blk, epart, crit_list, vhat, edge_dirty, e_off, e_inc;
     size_t total;
 };
 
@@ -152,11 +152,15 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.wr_blk = L.take<double>(n_wr_blocks(N, p.blk));
     o.epart = L.take<double>(p.nblk[ST_AB] + 2 * ((N + 255) / 256));
     o.crit_list = L.take<int32_t>(E);
+    o.vhat = L.take<double>(S);
+    o.edge_dirty = L.take<uint8_t>(S);
+    o.e_off = L.take<int32_t>(S + 1);
+    o.e_inc = L.take<int32_t>((int64_t)p.edge_inc.size());
     o.total = L.off;
     return o;
 }
 
-int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1)); }
+int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 6 * ((p.max_tl + 1) | 1)); }
 // stage C reuses its staging area for the warps' criterion scratch (<= 8 warps x ~840 B)
 // (CEM_C_GEOX adds 3 planes of node coordinates; the default keeps stage C's shared memory small:
 // its blocks then share the SM with a larger L1, which stage C measurably needs)
@@ -251,6 +255,10 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
     d.wr_blk = at<double>(b, o.wr_blk);
     d.crit_list = at<int32_t>(b, o.crit_list);
+    d.vhat = at<double>(b, o.vhat);
+    d.edge_dirty = at<uint8_t>(b, o.edge_dirty);
+    d.e_off = at<int32_t>(b, o.e_off);
+    d.e_inc = at<int32_t>(b, o.e_inc);
     ctx->epart = at<double>(b, o.epart);
     ctx->n_epart_edges = p.nblk[ST_AB];
     ctx->n_epart_nodes = (h.N + 255) / 256;
@@ -338,6 +346,22 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
         CUDA_TRY(put(o.rprev, r0.data(), sizeof(double) * 3 * N));
     }
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.wr_blk), 0, sizeof(double) * n_wr_blocks(N, p.blk), st));
+    // Vhat_s = sum of V_e over the active incident tets in ascending original id (the oracle's
+    // stage_edge order); kept in a table, recomputed by stage AB for edges marked dirty by a split
+    {
+        std::vector<double> vh(S, 0.0);
+#pragma omp parallel for schedule(static)
+        for (int64_t s = 0; s < S; ++s) {
+            double acc = 0.0;
+            for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j)
+                if (p.state[p.edge_inc[j]]) acc = acc + p.geoV[p.edge_inc[j]];
+            vh[s] = acc;
+        }
+        CUDA_TRY(put(o.vhat, vh.data(), sizeof(double) * S));
+    }
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.edge_dirty), 0, S, st));
+    CUDA_TRY(put(o.e_off, p.edge_off.data(), sizeof(int32_t) * (S + 1)));
+    CUDA_TRY(put(o.e_inc, p.edge_inc.data(), sizeof(int32_t) * p.edge_inc.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 6 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
@@ -484,7 +508,7 @@ cem_status setup_exchange(cem_ctx *ctx) {
 cem_status exchange_nccl_step(cem_ctx *ctx, int parity) {
     exchange_pack(ctx->xch, ctx->d.ubuf[parity], ctx->d.state, ctx->stream);
     if (!exchange_nccl(ctx->xch, ctx->comm, ctx->stream, ctx->err)) return CEM_ENCCL;
-    exchange_unpack(ctx->xch, ctx->d.ubuf[parity], ctx->d.state, ctx->stream);
+    exchange_unpack(ctx->xch, ctx->d.ubuf[parity], ctx->d.state, ctx->d.eedge, ctx->h.E, ctx->d.edge_dirty, ctx->stream);
     ctx->launches += 2;
     return CEM_OK;
 }
@@ -513,7 +537,8 @@ cem_status exchange_loopback(cem_ctx **c, int n, int parity) {
             }
         }
     }
-    for (int r = 0; r < n; ++r) exchange_unpack(c[r]->xch, c[r]->d.ubuf[parity], c[r]->d.state, st);
+    for (int r = 0; r < n; ++r)
+        exchange_unpack(c[r]->xch, c[r]->d.ubuf[parity], c[r]->d.state, c[r]->d.eedge, c[r]->h.E, c[r]->d.edge_dirty, st);
     for (int r = 0; r < n; ++r) c[r]->launches += 2;
     return CEM_OK;
 }

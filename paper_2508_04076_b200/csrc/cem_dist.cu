@@ -33,13 +33,18 @@ __global__ void k_pack(const double4 *__restrict__ u, const uint8_t *__restrict_
 
 __global__ void k_unpack(double4 *__restrict__ u, uint8_t *__restrict__ state, const int32_t *__restrict__ nidx,
                          int64_t nn, const int64_t *__restrict__ nsrc, const int32_t *__restrict__ tidx, int64_t nt,
-                         const int64_t *__restrict__ tsrc, const uint8_t *__restrict__ buf) {
+                         const int64_t *__restrict__ tsrc, const uint8_t *__restrict__ buf,
+                         const int32_t *__restrict__ eedge, int64_t E, uint8_t *__restrict__ edge_dirty) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nn) {
         const double *o = reinterpret_cast<const double *>(buf + nsrc[i]);
         u[nidx[i]] = make_double4(o[0], o[1], o[2], 0.0);
     } else if (i < nn + nt) {
-        state[tidx[i - nn]] = buf[tsrc[i - nn]];
+        const int32_t e = tidx[i - nn];
+        const uint8_t v = buf[tsrc[i - nn]];
+        if (state[e] && !v)  // a ghost tet split on its owner: its edges' Vhat change
+            for (int l = 0; l < 6; ++l) edge_dirty[eedge[(int64_t)l * E + e]] = 1;
+        state[e] = v;
     }
 }
 
@@ -135,11 +140,12 @@ void exchange_pack(const Exchange &x, const double4 *u, const uint8_t *state, cu
                                           x.n_send_tets, x.d_send_tdst, x.d_sendbuf);
 }
 
-void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, cudaStream_t st) {
+void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, const int32_t *eedge, int64_t E,
+                     uint8_t *edge_dirty, cudaStream_t st) {
     const int64_t tot = x.n_recv_nodes + x.n_recv_tets;
     if (tot)
         k_unpack<<<nblk(tot), 256, 0, st>>>(u, state, x.d_recv_nodes, x.n_recv_nodes, x.d_recv_nsrc, x.d_recv_tets,
-                                            x.n_recv_tets, x.d_recv_tsrc, x.d_recvbuf);
+                                            x.n_recv_tets, x.d_recv_tsrc, x.d_recvbuf, eedge, E, edge_dirty);
 }
 
 bool exchange_nccl(const Exchange &x, void *comm, cudaStream_t st, std::string &err) {

@@ -25,7 +25,8 @@ bool nccl_unique_id(void *id128, std::string &err);
 bool nccl_comm_init(void **comm, int nranks, int rank, const void *id128, std::string &err);
 void nccl_comm_destroy(void *comm);
 void exchange_pack(const Exchange &x, const double4 *u, const uint8_t *state, cudaStream_t st);
-void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, cudaStream_t st);
+void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, const int32_t *eedge, int64_t E,
+                     uint8_t *edge_dirty, cudaStream_t st);
 bool exchange_nccl(const Exchange &x, void *comm, cudaStream_t st, std::string &err);
 
 }  // namespace cem

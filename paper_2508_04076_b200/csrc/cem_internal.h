@@ -160,6 +160,9 @@ struct Dev {
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length
     int32_t *crit_list;        // [E] tets stage C flagged for the full criterion this step (staged path)
+    double *vhat;              // [S] Vhat_s = sum V_e over the active incident tets (original order)
+    uint8_t *edge_dirty;       // [S] 1: an incident tet split since stage AB last recomputed vhat[s]
+    const int32_t *e_off, *e_inc;  // edge -> incident tets (storage ids, ascending original id)
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
     double *rec_G, *rec_area;

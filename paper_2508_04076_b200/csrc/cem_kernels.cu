@@ -202,11 +202,21 @@ __device__ __forceinline__ void tau_row(double *T, int tn, int i, const double *
     T[3 * tn + i] = V * gxy;
     T[4 * tn + i] = V * gyz;
     T[5 * tn + i] = V * gxz;
-    T[6 * tn + i] = V;
 }
 __device__ __forceinline__ void zero_row(double *T, int tn, int i) {
 #pragma unroll
-    for (int c = 0; c < 7; ++c) T[c * tn + i] = 0.0;
+    for (int c = 0; c < 6; ++c) T[c * tn + i] = 0.0;
+}
+// Vhat_s = sum of V_e over the edge's active incident tets in ascending original id (the
+// oracle's stage_edge sum); inactive tets are skipped (equivalently: add +0.0)
+__device__ __noinline__ double vhat_recompute(const Dev *__restrict__ dp, int64_t s) {
+    const Dev &d = *dp;
+    double acc = 0.0;
+    for (int32_t j = __ldg(d.e_off + s); j < __ldg(d.e_off + s + 1); ++j) {
+        const int32_t e = __ldg(d.e_inc + j);
+        if (__ldcg(d.state + e)) acc = acc + __ldg(geo_ptr(d, (uint32_t)e));
+    }
+    return acc;
 }
 // the 9 stored gradients (nodes 1..3) and V of tet e; gradN0 = -((gradN1 + gradN2) + gradN3)
 __device__ __forceinline__ void load_geo(const Dev &d, uint32_t e, double (&g)[4][3], double &V) {
@@ -285,8 +295,22 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const bool hs = s < d.S;
     const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
     uint4 q = hs ? __ldg(row) : make_uint4(0, 0, 0, 0);  // first 8 incidences, before the barrier
+    double Vh = 0.0;
+    if (hs) {
+        // Vhat from the table; an edge with a tet split since the last step is recomputed
+        // (splits mark their 6 edges; ghost splits arrive marked by the halo unpack)
+        if (__ldcg(d.edge_dirty + s)) {
+            Vh = vhat_recompute(d.self, s);
+            if (!epart) {
+                d.vhat[s] = Vh;
+                d.edge_dirty[s] = 0;
+            }
+        } else {
+            Vh = __ldcg(d.vhat + s);
+        }
+    }
     __syncthreads();
-    double Vh = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
+    double T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
     if (hs) {
         for (int w = 0;;) {  // ELL row: 8 incidences per 16-B load, in order
             const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
@@ -296,7 +320,6 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
                 if (t >= lim) break;
                 // padding (0xffff) -> the all-zero sentinel row nt; inactive tets hold zeros
                 const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
-                Vh = Vh + T[6 * tn + r];
                 T0 = T0 + T[r];
                 T1 = T1 + T[tn + r];
                 T2 = T2 + T[2 * tn + r];
@@ -499,6 +522,8 @@ __device__ void candidate(const CritScratch &w, int k, double &G, double &area) 
 __device__ __forceinline__ void split_tet(const Dev &d, int64_t e, int4 t, double G, int k, double A, int64_t rec_step,
                                           int32_t stamp, bool record) {
     d.state[e] = 0;
+#pragma unroll
+    for (int l = 0; l < 6; ++l) d.edge_dirty[ldro(d.eedge + (int64_t)l * d.E + e)] = 1;  // their Vhat changes
     if (record) {  // multi-GPU: only the owning rank records (every holder deactivates)
         const int slot = atomicAdd(&d.ctr[0], 1);
         d.rec_step[slot] = rec_step;
