@@ -254,6 +254,12 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     }
     const int32_t k0 = tid < nn ? __ldg(d.nlb + n0 + tid) : 0;
     const int q0 = tid < nn ? __ldg(d.nrow + n0 + tid) : 0;
+    // the second tet's list entry (most blocks hold 1.5 tets per thread): index, row, nodes
+    const int i1 = tid + nthr;
+    const bool has1 = i1 < nt;
+    const uint32_t e1 = has1 ? (uint32_t)__ldg(d.tl + t0 + i1) : 0u;
+    const int r1 = has1 ? (int)__ldg(d.trow + t0 + i1) : nt;
+    const ushort4 lc1 = has1 ? __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i1) : make_ushort4(0, 0, 0, 0);
     pdl_wait();  // u and the tet states come from the previous kernels
     const uint8_t act0 = has0 ? __ldcg(d.state + e0) : (uint8_t)0;
     if (tid < nn) {  // one node per thread (list in ascending order, rows bank-aware)
@@ -278,7 +284,19 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     } else if (tid <= nt) {
         zero_row(T, tn, r0);  // (tid == nt: the sentinel row)
     }
-    for (int i = tid + nthr; i <= nt; i += nthr) {
+    if (has1) {  // second tet: indices prefetched, geometry and state issued together
+        double g[4][3], V;
+        load_geo(d, e1, g, V);
+        if (__ldcg(d.state + e1)) {
+            grad0(g);
+            tau_row(T, tn, r1, U, un, g, V, lc1);
+        } else {
+            zero_row(T, tn, r1);
+        }
+    } else if (i1 == nt) {
+        zero_row(T, tn, nt);  // sentinel
+    }
+    for (int i = tid + 2 * nthr; i <= nt; i += nthr) {
         const uint32_t e = i < nt ? (uint32_t)__ldg(d.tl + t0 + i) : 0u;
         double g[4][3], V;
         load_geo(d, e, g, V);
@@ -299,14 +317,14 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     if (hs) {
         // Vhat from the table; an edge with a tet split since the last step is recomputed
         // (splits mark their 6 edges; ghost splits arrive marked by the halo unpack)
-        if (__ldcg(d.edge_dirty + s)) {
+        const uint8_t dirty = __ldcg(d.edge_dirty + s);
+        Vh = __ldcg(d.vhat + s);  // issued together with the flag (one round trip)
+        if (dirty) {
             Vh = vhat_recompute(d.self, s);
             if (!epart) {
                 d.vhat[s] = Vh;
                 d.edge_dirty[s] = 0;
             }
-        } else {
-            Vh = __ldcg(d.vhat + s);
         }
     }
     __syncthreads();
