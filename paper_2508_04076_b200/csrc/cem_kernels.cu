@@ -918,6 +918,12 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
     const double fxc = (fl & 8) ? __ldg(reinterpret_cast<const double *>(d.fext + k) + c) : 0.0;
     const double vb0 = (fl & 7) ? __ldg(reinterpret_cast<const double *>(d.dir_v0 + k) + c) : 0.0;
     pdl_wait();  // force slots come from stage C
+    // node state issued before the slot gathers (consumed after them)
+    double mk = __ldcg(d.mass + k);
+    const double u1 = __ldcg(reinterpret_cast<const double *>(u1p + k) + c);
+    double vv = __ldcg(reinterpret_cast<const double *>(d.v + k) + c);
+    double aa = __ldcg(reinterpret_cast<const double *>(d.a + k) + c);
+    const int32_t dirty = __ldcg(d.dirty + k);
     const double *fec = d.fe + (c < 3 ? c : 0);  // lane c: component c of each slot (lane 3: unused sum)
     double f = 0.0;
     for (int w = 0;;) {
@@ -936,10 +942,6 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
         for (int t = 0; t < 8; ++t) f = f + x[t];
         if (!more) break;
     }
-    double mk = __ldcg(d.mass + k);
-    const double u1 = __ldcg(reinterpret_cast<const double *>(u1p + k) + c);
-    double vv = __ldcg(reinterpret_cast<const double *>(d.v + k) + c);
-    double aa = __ldcg(reinterpret_cast<const double *>(d.a + k) + c);
     const double dt = d.dt;
     const double t1 = (double)(s + 1) * dt;
     if (c == 3) {
@@ -971,7 +973,7 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
         wr = 0.5 * (*rp + R) * (u1 - us);
         *rp = R;
     }
-    if (__ldcg(d.dirty + k) == (int32_t)(s + 1)) {
+    if (dirty == (int32_t)(s + 1)) {
         // an incident tet split in this step: lumped mass from the active incidences;
         // m = 0 -> frozen, v = a = 0 (R15)
         mk = node_mass(d, k);
@@ -1127,7 +1129,7 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 #define CEM_C_MINB 4
 #endif
 #ifndef CEM_D_MINB
-#define CEM_D_MINB 6
+#define CEM_D_MINB 5
 #endif
 __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
     extern __shared__ __align__(16) double sm[];
