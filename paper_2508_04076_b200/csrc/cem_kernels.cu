@@ -491,6 +491,9 @@ __device__ __forceinline__ double dsgn(double x) { return x > 0.0 ? 1.0 : (x < 0
 // (G, area, -k), which equals the oracle's sequential scan.  Split: deactivate
 // now (this step's readers of the state are done), append a record (unordered; sorted by
 // (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
+#ifndef CEM_D_BATCH
+#define CEM_D_BATCH 8  // stage D: force slots gathered per batch (multiple of 4)
+#endif
 #ifndef CEM_CRIT_COOP_MAX
 #define CEM_CRIT_COOP_MAX 1
 #endif
@@ -914,7 +917,10 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
     if (fl & 16) return 0.0;  // multi-GPU: another rank owns (and updates) this node
     // static tables before the dependency wait (overlaps the previous stage's tail)
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
-    int4 qa = __ldg(row), qb = __ldg(row + 1);
+    constexpr int kB = CEM_D_BATCH, kQ = kB / 4;  // slots per batch, int4 index loads per batch
+    int4 q[kQ];
+#pragma unroll
+    for (int j = 0; j < kQ; ++j) q[j] = j * 4 < d.wn ? __ldg(row + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
     const double fxc = (fl & 8) ? __ldg(reinterpret_cast<const double *>(d.fext + k) + c) : 0.0;
     const double vb0 = (fl & 7) ? __ldg(reinterpret_cast<const double *>(d.dir_v0 + k) + c) : 0.0;
     pdl_wait();  // force slots come from stage C
@@ -928,18 +934,26 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
     double f = 0.0;
     for (int w = 0;;) {
         // padding entries point at an all-zero slot: adding +0.0 is an exact no-op here
-        const int32_t sl[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-        double x[8];
+        int32_t sl[kB];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
-        w += 8;
-        const bool more = sl[7] != d.zslot && w < d.wn;
+        for (int j = 0; j < kQ; ++j) {
+            sl[4 * j] = q[j].x;
+            sl[4 * j + 1] = q[j].y;
+            sl[4 * j + 2] = q[j].z;
+            sl[4 * j + 3] = q[j].w;
+        }
+        double x[kB];
+#pragma unroll
+        for (int t = 0; t < kB; ++t) x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+        w += kB;
+        const bool more = sl[kB - 1] != d.zslot && w < d.wn;
         if (more) {
-            qa = __ldg(row + (w >> 2));
-            qb = __ldg(row + (w >> 2) + 1);
+#pragma unroll
+            for (int j = 0; j < kQ; ++j)
+                q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
         }
 #pragma unroll
-        for (int t = 0; t < 8; ++t) f = f + x[t];
+        for (int t = 0; t < kB; ++t) f = f + x[t];
         if (!more) break;
     }
     const double dt = d.dt;
@@ -1131,6 +1145,7 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 #ifndef CEM_D_MINB
 #define CEM_D_MINB 5
 #endif
+
 __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
     extern __shared__ __align__(16) double sm[];
     pdl_trigger();
