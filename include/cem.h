@@ -195,7 +195,9 @@ CEM_API cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where);
  *   dissipated     U_d = sum Gc_e A_e over the split records                 (L206)
  * Per-element terms are the oracle's bit for bit; the sums run over per-block partials in a
  * fixed order (run-to-run deterministic, equal to the oracle's sequential sums to rounding).
- * Synchronises the ctx stream; launches two kernels.  CEM_ESTATE for a multi-rank context. */
+ * Synchronises the ctx stream; launches two kernels.  Multi-rank: the rank's share (its owned
+ * nodes, the edges whose lowest-id incident tet it owns, its records); the sum over ranks is
+ * the ledger of the whole mesh. */
 typedef struct {
     int64_t step;
     double time;

@@ -88,7 +88,7 @@ struct Offs {
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
-    size_t rprev, wr_blk, epart, crit_list, vhat, edge_dirty, e_off, e_inc;
+    size_t rprev, wr_blk, epart, crit_list, vhat, edge_dirty, e_off, e_inc, edge_own;
     size_t total;
 };
 
@@ -156,6 +156,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.edge_dirty = L.take<uint8_t>(S);
     o.e_off = L.take<int32_t>(S + 1);
     o.e_inc = L.take<int32_t>((int64_t)p.edge_inc.size());
+    o.edge_own = L.take<uint8_t>(S);
     o.total = L.off;
     return o;
 }
@@ -259,6 +260,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.edge_dirty = at<uint8_t>(b, o.edge_dirty);
     d.e_off = at<int32_t>(b, o.e_off);
     d.e_inc = at<int32_t>(b, o.e_inc);
+    d.edge_own = at<uint8_t>(b, o.edge_own);
     ctx->epart = at<double>(b, o.epart);
     ctx->n_epart_edges = p.nblk[ST_AB];
     ctx->n_epart_nodes = (h.N + 255) / 256;
@@ -362,6 +364,15 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.edge_dirty), 0, S, st));
     CUDA_TRY(put(o.e_off, p.edge_off.data(), sizeof(int32_t) * (S + 1)));
     CUDA_TRY(put(o.e_inc, p.edge_inc.data(), sizeof(int32_t) * p.edge_inc.size()));
+    // energy ledger ownership of an edge: the owner of its lowest-id incident tet (the first
+    // entry of its incidence list; on one GPU every edge is owned).  Edges this rank owns are
+    // edges of its layer-1 tets, whose incidences are complete locally.
+    {
+        std::vector<uint8_t> own(S, 1);
+        for (int64_t s = 0; s < S; ++s)
+            if (p.edge_off[s + 1] > p.edge_off[s]) own[s] = (p.tflag[p.edge_inc[p.edge_off[s]]] & 2) ? 1 : 0;
+        CUDA_TRY(put(o.edge_own, own.data(), S));
+    }
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 6 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
@@ -854,10 +865,6 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
 
 cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
     if (!ctx || !out) return CEM_EINVAL;
-    if (ctx->dist || ctx->nranks > 1) {
-        ctx->err = "cem_energy: single-context runs only";
-        return CEM_ESTATE;
-    }
     cudaStream_t st = ctx->stream;
     cem_state_out so{};
     const cem_status rc = cem_get_state(ctx, &so, CEM_HOST);  // synchronises; U_d, nonfinite

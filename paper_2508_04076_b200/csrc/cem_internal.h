@@ -163,6 +163,7 @@ struct Dev {
     double *vhat;              // [S] Vhat_s = sum V_e over the active incident tets (original order)
     uint8_t *edge_dirty;       // [S] 1: an incident tet split since stage AB last recomputed vhat[s]
     const int32_t *e_off, *e_inc;  // edge -> incident tets (storage ids, ascending original id)
+    const uint8_t *edge_own;   // [S] 1 if this rank counts the edge in the energy ledger
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
     double *rec_G, *rec_area;

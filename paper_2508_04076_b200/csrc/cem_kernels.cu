@@ -354,7 +354,7 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
         // energy ledger: psi(eps~_s) Vhat_s / 6, psi = 1/2 lam tr^2 + mu eps:eps (oracle
         // orc_strain_energy, same association), summed per block in a fixed order
         double U = 0.0;
-        if (hs && Vh != 0.0) {
+        if (hs && Vh != 0.0 && __ldg(d.edge_own + s)) {
             const double inv = 1.0 / Vh;
             const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
             const double tr = e11 + e22 + e33;

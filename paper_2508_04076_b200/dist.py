@@ -102,6 +102,14 @@ class LoopbackGroup:
     def launch_count(self):
         return sum(s.launch_count for s in self.sims)
 
+    def energy(self):
+        """Energy ledger of the whole mesh: the sum of the ranks' shares (cem_energy)."""
+        parts = [s.energy() for s in self.sims]
+        out = dict(parts[0])
+        for k in ("kinetic", "strain", "external", "reaction", "dissipated"):
+            out[k] = sum(p[k] for p in parts)
+        return out
+
 
 class DistSimulation:
     """One rank of a torchrun job (one GPU per rank, NCCL halo exchange inside cem_step)."""
@@ -132,6 +140,18 @@ class DistSimulation:
     @property
     def launch_count(self):
         return self.sim.launch_count
+
+    def energy(self):
+        """Energy ledger of the whole mesh (the ranks' shares summed with all_reduce); every rank
+        gets the same dict."""
+        import torch
+        e = self.sim.energy()
+        keys = ("kinetic", "strain", "external", "reaction", "dissipated")
+        t = torch.tensor([e[k] for k in keys], dtype=torch.float64, device=f"cuda:{self.sim.device}")
+        self.dist.all_reduce(t)
+        out = dict(e)
+        out.update({k: float(v) for k, v in zip(keys, t.tolist())})
+        return out
 
     def state(self, gather=True):
         """Local state; with gather=True rank 0 returns the assembled global state (others None)."""

@@ -52,3 +52,22 @@ def test_loopback_weak_block_predamage():
 def test_loopback_dirichlet():
     p = ci.edge_impact_plate(cells=(30, 16, 3), dims=(0.03, 0.016, 0.003), steps=0)
     check(p, 3, 120)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_energy_ledger(P):
+    """The ranks' ledger shares (owned nodes, owned edges, own records) sum to the whole
+    mesh's ledger: equal to the oracle's to the rounding bound of the sums."""
+    dist = _gpu()
+    p = ci.compact_tension(cells=(24, 24, 3), dims=(0.2, 0.2, 0.025), v0=60.0, t0=20e-6)
+    grp = dist.LoopbackGroup(p, P)
+    orc = oracle.Oracle(p)
+    grp.step(150, 1)
+    orc.run(150, 1)
+    g, o = grp.energy(), orc.energy()
+    tol = 4 * 6 * p.n_tets * np.finfo(np.float64).eps
+    scale = max(abs(o[k]) for k in ("kinetic", "strain", "external", "reaction"))
+    for k in ("kinetic", "strain", "external", "reaction"):
+        assert abs(g[k] - o[k]) <= tol * scale, (k, g[k], o[k])
+    assert g["dissipated"] == pytest.approx(o["dissipated"], rel=1e-12)
+    assert o["reaction"] > 0.0 and o["dissipated"] > 0.0
