@@ -10,9 +10,12 @@
 //   A  tau_e = V_e eps_e(u_{s+1}) per tet
 //   B  Vhat_s, eps~_s = (sum tau_e)/Vhat_s, sigma_s per edge
 //   C  f_e = (V_e/6) B^T sum_l sigma_{s(e,l)} per tet; crack
-//      criterion with a conservative early-out; split inline
+//      criterion's conservative early-out; the tets that fail it
+//      are listed for k_crit (24 candidates, one warp per tet),
+//      which splits
 //   D  f_int gather, Newmark + BC, mass/freeze of split nodes,
-//      predictor u_{s+2} -> ubuf[s&1]
+//      predictor u_{s+2} -> ubuf[s&1] (+ reaction work, N1)
+// Vhat_s is kept per edge (table, recomputed only where a split changed it).
 //
 // k_persistent runs K steps in ONE launch: CTAs pull (stage, block) work items from a
 // global queue in a precomputed wavefront order (cem_plan.cpp) and wait only on the
@@ -48,28 +51,14 @@ __device__ __forceinline__ void st4(double4 *p, double x, double y, double z, do
     q[1] = make_double2(z, w);
 }
 
-__device__ __forceinline__ double4 ld256(const double4 *p) {  // LDG.E.256 (sm_100)
-    double4 r;
-    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void st256(double4 *p, double x, double y, double z, double w) {
+[[maybe_unused]] __device__ __forceinline__ void st256(double4 *p, double x, double y, double z, double w) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
 }
-__device__ __forceinline__ void store_slot(double *p, double x, double y, double z) {
 #if CEM_FES == 4
+__device__ __forceinline__ void store_slot(double *p, double x, double y, double z) {  // (x, y, z, 0)
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(0.0) : "memory");
-#else
-    // 24-B slot at an 8-B boundary: one 16-B and one 8-B store, ordered by alignment
-    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x), "d"(y) : "memory");
-        p[2] = z;
-    } else {
-        p[0] = x;
-        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p + 1), "d"(y), "d"(z) : "memory");
-    }
-#endif
 }
+#endif
 __device__ __forceinline__ void st128(double *p, double x, double y) {
     asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
@@ -108,48 +97,9 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
     return acc;
 }
 
-// Shared-memory staging: a block's deduplicated producer records are loaded cooperatively
-// (8 lanes per 64-B record, 3 lanes per node) into component planes plane[c][r], so that
-// every later per-thread gather hits shared memory instead of an L1 line of its own.
-// ------------------------------------------------------------------ async staging helpers (sm_100a)
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// TMA bulk copy global -> shared (UBLKCP), completion counted on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-            smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-// LDGSTS: 8-byte asynchronous gather into shared memory (no register round trip)
-__device__ __forceinline__ void cp8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory"); }
-
-// 16-byte aligned window [a, a+bytes) covering [p, p + n elements of size sz); returns the element shift
-template <class T>
-__device__ __forceinline__ int bulk_window(const T *p, int n, const T *&a, uint32_t &bytes) {
-    const uintptr_t s = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
-    const uintptr_t e = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~uintptr_t(15);
-    a = reinterpret_cast<const T *>(s);
-    bytes = (uint32_t)(e - s);
-    return (int)((reinterpret_cast<uintptr_t>(p) - s) / sizeof(T));
-}
-__host__ __device__ __forceinline__ int pad16(int bytes) { return (bytes + 15) & ~15; }
+// Shared-memory staging: a block's deduplicated producer records (u of its nodes, sigma of its
+// edges) are loaded once into component planes plane[c][row], so that every later per-thread
+// gather hits shared memory; rows are assigned bank-aware by the plan (cem_plan.cpp bank_rows).
 
 // programmatic dependent launch (PDL): let the next stage kernel launch early, and wait for
 // the previous one only where its outputs are read
