@@ -99,6 +99,10 @@ typedef struct {
 #define CEM_F_NO_DISCARD 0x4u   /* persistent kernel: keep consumed intermediates in L2 (no discard) */
 #define CEM_F_PERSISTENT 0x8u   /* one persistent wavefront kernel per cem_step call */
 #define CEM_F_LOOPBACK 0x10u    /* nranks > 1 emulated in one process (cem_step_group, device copies) */
+#define CEM_F_P2P 0x20u         /* loopback: the P2P halo path (stage D stores into the peers' buffers).
+                                 * Multi-GPU (NCCL) contexts use the P2P halo whenever every rank can
+                                 * map its peers' buffers (CUDA IPC over NVLink) and a self-check at
+                                 * init passes; CEM_NO_P2P=1 in the environment keeps NCCL send/recv. */
 
 typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
 

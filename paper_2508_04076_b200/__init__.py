@@ -36,6 +36,7 @@ CEM_F_STAGED = 0x2
 CEM_F_NO_DISCARD = 0x4
 CEM_F_PERSISTENT = 0x8
 CEM_F_LOOPBACK = 0x10
+CEM_F_P2P = 0x20
 CEM_HOST, CEM_DEVICE = 0, 1
 
 D = C.POINTER(C.c_double)

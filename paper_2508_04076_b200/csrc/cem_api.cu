@@ -41,6 +41,7 @@ struct cem_ctx {
     void *comm = nullptr;
     bool init_exchange_pending = false;
     std::vector<void *> dist_allocs;
+    P2P p2p;                      // P2P halo (multi-GPU), see cem_dist.h
     double *epart = nullptr;      // energy-ledger partials (device)
     int64_t n_epart_edges = 0, n_epart_nodes = 0, n_wr = 0;
 };
@@ -524,6 +525,210 @@ cem_status exchange_nccl_step(cem_ctx *ctx, int parity) {
     return CEM_OK;
 }
 
+// ---------------------------------------------------------------- P2P halo
+// Tables of this rank's stores into the peers' receive buffers: peer j's buffer for step parity
+// par is peer_recv[par][j] (already offset to the segment the peer keeps for this rank); a node
+// record sits at 24 i in the segment (i-th send node), a tet state byte after the node records.
+cem_status p2p_tables(cem_ctx *ctx, const std::vector<uint8_t *> &r0, const std::vector<uint8_t *> &r1,
+                      const std::vector<int64_t *> &flag_addr) {
+    const PartLocal &L = ctx->part;
+    const Plan &p = ctx->p;
+    P2P &q = ctx->p2p;
+    const int np = (int)L.peers.size();
+    const int64_t N = ctx->h.N, E = ctx->h.E;
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> ne(N), te(E);
+    for (int j = 0; j < np; ++j) {
+        const auto &sn = L.send_nodes[j], &stt = L.send_tets[j];
+        for (size_t i = 0; i < sn.size(); ++i) ne[p.node_old2new[sn[i]]].push_back({j, (int32_t)(24 * i)});
+        for (size_t i = 0; i < stt.size(); ++i)
+            te[p.tet_old2new[stt[i]]].push_back({j, (int32_t)(24 * sn.size() + i)});
+    }
+    auto csr = [](const std::vector<std::vector<std::pair<int32_t, int32_t>>> &v, std::vector<int32_t> &off,
+                  std::vector<int32_t> &peer, std::vector<int32_t> &byte) {
+        off.assign(v.size() + 1, 0);
+        for (size_t k = 0; k < v.size(); ++k) {
+            off[k + 1] = off[k] + (int32_t)v[k].size();
+            for (auto &e : v[k]) {
+                peer.push_back(e.first);
+                byte.push_back(e.second);
+            }
+        }
+    };
+    std::vector<int32_t> noff, npeer, nbyte, toff, tpeer, tbyte;
+    csr(ne, noff, npeer, nbyte);
+    csr(te, toff, tpeer, tbyte);
+    std::vector<uint8_t *> pr(2 * np);
+    std::vector<int32_t> prank(np);
+    for (int j = 0; j < np; ++j) {
+        pr[j] = r0[j];
+        pr[np + j] = r1[j];
+        prank[j] = L.peers[j];
+    }
+    auto dev = [&](const void *src, size_t bytes, void **dst) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, bytes ? bytes : 8);
+        if (e != cudaSuccess) return e;
+        ctx->dist_allocs.push_back(*dst);
+        if (bytes && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+        return e;
+    };
+    CUDA_TRY(dev(pr.data(), sizeof(uint8_t *) * pr.size(), (void **)&q.d_peer_recv));
+    CUDA_TRY(dev(flag_addr.data(), sizeof(int64_t *) * flag_addr.size(), (void **)&q.d_peer_flag));
+    CUDA_TRY(dev(prank.data(), 4 * prank.size(), (void **)&q.d_peer_rank));
+    CUDA_TRY(dev(noff.data(), 4 * noff.size(), (void **)&q.d_noff));
+    CUDA_TRY(dev(npeer.data(), 4 * npeer.size(), (void **)&q.d_npeer));
+    CUDA_TRY(dev(nbyte.data(), 4 * nbyte.size(), (void **)&q.d_nbyte));
+    CUDA_TRY(dev(toff.data(), 4 * toff.size(), (void **)&q.d_toff));
+    CUDA_TRY(dev(tpeer.data(), 4 * tpeer.size(), (void **)&q.d_tpeer));
+    CUDA_TRY(dev(tbyte.data(), 4 * tbyte.size(), (void **)&q.d_tbyte));
+    return CEM_OK;
+}
+
+// this rank's receive buffers for the P2P halo, initialised from the exchanged state
+cem_status p2p_alloc(cem_ctx *ctx) {
+    P2P &q = ctx->p2p;
+    const size_t bytes = std::max<size_t>(8, ctx->xch.recv_off.back());
+    for (int par = 0; par < 2; ++par) {
+        CUDA_TRY(cudaMalloc(&q.recv[par], bytes));
+        ctx->dist_allocs.push_back(q.recv[par]);
+        CUDA_TRY(cudaMemcpy(q.recv[par], ctx->xch.d_recvbuf, bytes, cudaMemcpyDeviceToDevice));
+    }
+    CUDA_TRY(cudaMalloc(&q.flags, sizeof(int64_t) * std::max(1, ctx->nranks)));
+    ctx->dist_allocs.push_back(q.flags);
+    CUDA_TRY(cudaMemset(q.flags, 0, sizeof(int64_t) * std::max(1, ctx->nranks)));
+    return CEM_OK;
+}
+
+void p2p_enable(cem_ctx *ctx) {
+    P2P &q = ctx->p2p;
+    Dev &d = ctx->d;
+    d.p2p_recv = q.d_peer_recv;
+    d.p2p_np = (int)ctx->part.peers.size();
+    d.p2p_noff = q.d_noff;
+    d.p2p_npeer = q.d_npeer;
+    d.p2p_nbyte = q.d_nbyte;
+    d.p2p_toff = q.d_toff;
+    d.p2p_tpeer = q.d_tpeer;
+    d.p2p_tbyte = q.d_tbyte;
+    q.on = true;
+}
+
+// Real multi-GPU: the receive buffers and flags are exported with CUDA IPC, the handles and the
+// segment offsets all-gathered over NCCL, the peers' allocations mapped (peer access over
+// NVLink).  Self-check before use: u_1 pushed through the P2P path must equal what the NCCL
+// exchange delivered, on every rank; otherwise the halo stays on NCCL.
+struct P2PBlob {
+    cudaIpcMemHandle_t recv0, recv1, flags;
+    int64_t seg_off_by_src[64];
+};
+cem_status p2p_setup_nccl(cem_ctx *ctx) {
+    const int R = ctx->nranks, me = ctx->rank;
+    const PartLocal &L = ctx->part;
+    const int np = (int)L.peers.size();
+    if (R > 64 || np == 0) return CEM_OK;
+    P2P &q = ctx->p2p;
+    cem_status st = p2p_alloc(ctx);
+    if (st) return st;
+    P2PBlob mine{};
+    for (int i = 0; i < 64; ++i) mine.seg_off_by_src[i] = -1;
+    for (int j = 0; j < np; ++j) mine.seg_off_by_src[L.peers[j]] = (int64_t)ctx->xch.recv_off[j];
+    if (cudaIpcGetMemHandle(&mine.recv0, q.recv[0]) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.recv1, q.recv[1]) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.flags, q.flags) != cudaSuccess) {
+        cudaGetLastError();
+        return CEM_OK;  // no IPC: NCCL halo
+    }
+    void *dsend = nullptr, *drecv = nullptr;
+    CUDA_TRY(cudaMalloc(&dsend, sizeof(P2PBlob)));
+    CUDA_TRY(cudaMalloc(&drecv, sizeof(P2PBlob) * R));
+    ctx->dist_allocs.push_back(dsend);
+    ctx->dist_allocs.push_back(drecv);
+    CUDA_TRY(cudaMemcpy(dsend, &mine, sizeof(P2PBlob), cudaMemcpyHostToDevice));
+    if (!nccl_allgather_bytes(dsend, drecv, sizeof(P2PBlob), ctx->comm, ctx->stream, ctx->err)) return CEM_ENCCL;
+    std::vector<P2PBlob> all(R);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), drecv, sizeof(P2PBlob) * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::vector<uint8_t *> r0(np), r1(np);
+    std::vector<int64_t *> fl(np);
+    int64_t ok = 1;
+    for (int j = 0; j < np && ok; ++j) {
+        const P2PBlob &b = all[L.peers[j]];
+        void *a0 = nullptr, *a1 = nullptr, *af = nullptr;
+        if (b.seg_off_by_src[me] < 0 ||
+            cudaIpcOpenMemHandle(&a0, b.recv0, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&a1, b.recv1, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&af, b.flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+            break;
+        }
+        q.opened.push_back(a0);
+        q.opened.push_back(a1);
+        q.opened.push_back(af);
+        r0[j] = static_cast<uint8_t *>(a0) + b.seg_off_by_src[me];
+        r1[j] = static_cast<uint8_t *>(a1) + b.seg_off_by_src[me];
+        fl[j] = static_cast<int64_t *>(af) + me;
+    }
+    int64_t *dflag = nullptr;
+    CUDA_TRY(cudaMalloc(&dflag, 2 * sizeof(int64_t)));
+    ctx->dist_allocs.push_back(dflag);
+    if (ok) {
+        st = p2p_tables(ctx, r0, r1, fl);
+        if (st) return st;
+        // self-check: push u_1 into the peers' buffers[1], sync, compare with the NCCL delivery
+        p2p_push_nodes(q, ctx->d.ubuf[1], ctx->h.N, 1, np, ctx->stream);
+        p2p_sync(q, np, 1, true, ctx->stream);
+        CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int64_t), ctx->stream));
+        count_mismatch(q.recv[1], ctx->xch.d_recvbuf, ctx->xch.d_recv_nsrc, ctx->xch.n_recv_nodes, 24, dflag,
+                       ctx->stream);
+        int64_t bad = 0;
+        CUDA_TRY(cudaMemcpyAsync(&bad, dflag, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        ok = bad == 0;
+    }
+    // every rank must agree: the largest "not ok" over the ranks decides
+    const int64_t notok = ok ? 0 : 1;
+    CUDA_TRY(cudaMemcpy(dflag, &notok, sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (!nccl_allreduce_max_i64(dflag, dflag + 1, 1, ctx->comm, ctx->stream, ctx->err)) return CEM_ENCCL;
+    int64_t any_bad = 1;
+    CUDA_TRY(cudaMemcpyAsync(&any_bad, dflag + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (any_bad == 0) {
+        p2p_enable(ctx);
+        CUDA_TRY(cudaMemcpy(const_cast<Dev *>(ctx->d.self), &ctx->d, sizeof(Dev), cudaMemcpyHostToDevice));
+    }
+    return CEM_OK;
+}
+
+// Loopback emulation (tests, one device): the peers' buffers are the other contexts' own.
+cem_status p2p_setup_loopback(cem_ctx **c, int n) {
+    for (int r = 0; r < n; ++r) {
+        cem_ctx *ctx = c[r];
+        cem_status st = p2p_alloc(ctx);
+        if (st) return st;
+    }
+    for (int r = 0; r < n; ++r) {
+        cem_ctx *ctx = c[r];
+        const PartLocal &L = ctx->part;
+        const int np = (int)L.peers.size();
+        std::vector<uint8_t *> r0(np), r1(np);
+        std::vector<int64_t *> fl(np);
+        for (int j = 0; j < np; ++j) {
+            cem_ctx *pc = c[L.peers[j]];
+            size_t off = 0;
+            for (size_t i = 0; i < pc->part.peers.size(); ++i)
+                if (pc->part.peers[i] == r) off = pc->xch.recv_off[i];
+            r0[j] = pc->p2p.recv[0] + off;
+            r1[j] = pc->p2p.recv[1] + off;
+            fl[j] = pc->p2p.flags + r;
+        }
+        cem_status st = p2p_tables(ctx, r0, r1, fl);
+        if (st) return st;
+        p2p_enable(ctx);
+        CUDA_TRY(cudaMemcpy(const_cast<Dev *>(ctx->d.self), &ctx->d, sizeof(Dev), cudaMemcpyHostToDevice));
+    }
+    return CEM_OK;
+}
+
 // loopback: all ranks in this process, transport = device copies on ctxs[0]'s stream
 cem_status exchange_loopback(cem_ctx **c, int n, int parity) {
     cudaStream_t st = c[0]->stream;
@@ -736,6 +941,10 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
             st = exchange_nccl_step(ctx, 1);  // owners' u_1 to the ranks holding their nodes
             if (st) return fail(st);
             CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            if (!getenv("CEM_NO_P2P")) {  // NVLink P2P halo when every rank can map its peers
+                st = p2p_setup_nccl(ctx);
+                if (st) return fail(st);
+            }
         }
     }
     *out = ctx;
@@ -746,6 +955,7 @@ void cem_destroy(cem_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->ev) cudaEventDestroy(e);
+    for (void *p : ctx->p2p.opened) cudaIpcCloseMemHandle(p);
     if (ctx->comm) nccl_comm_destroy(ctx->comm);
     for (void *p : ctx->dist_allocs) cudaFree(p);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
@@ -784,6 +994,13 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
             ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr);
+            if (ctx->p2p.on) {  // stage D / the split pass already stored into the peers' buffers
+                p2p_sync(ctx->p2p, (int)ctx->part.peers.size(), sstep + 2, true, ctx->stream);
+                exchange_unpack(ctx->xch, ctx->d.ubuf[sstep & 1], ctx->d.state, ctx->d.eedge, ctx->h.E,
+                                ctx->d.edge_dirty, ctx->stream, ctx->p2p.recv[sstep & 1]);
+                ctx->launches += 2;
+                continue;
+            }
             cem_status st = exchange_nccl_step(ctx, (int)(sstep & 1));
             if (st) return st;
         }
@@ -1037,12 +1254,25 @@ cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_
     if (c[0]->init_exchange_pending) {
         cem_status st = exchange_loopback(c, n, 1);
         if (st) return st;
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         for (int r = 0; r < n; ++r) c[r]->init_exchange_pending = false;
+        if (c[0]->flags & CEM_F_P2P) {
+            st = p2p_setup_loopback(c, n);
+            if (st) return st;
+        }
     }
     for (int64_t i = 0; i < nsteps; ++i) {
         const int64_t sstep = c[0]->step + i;
         for (int r = 0; r < n; ++r) {
             c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr);
+        }
+        if (c[0]->p2p.on) {  // the stores went straight into the peers' buffers; stream order syncs
+            for (int r = 0; r < n; ++r) {
+                exchange_unpack(c[r]->xch, c[r]->d.ubuf[sstep & 1], c[r]->d.state, c[r]->d.eedge, c[r]->h.E,
+                                c[r]->d.edge_dirty, ctx->stream, c[r]->p2p.recv[sstep & 1]);
+                c[r]->launches += 1;
+            }
+            continue;
         }
         cem_status st = exchange_loopback(c, n, (int)(sstep & 1));
         if (st) return st;

@@ -40,12 +40,60 @@ __global__ void k_unpack(double4 *__restrict__ u, uint8_t *__restrict__ state, c
         const double *o = reinterpret_cast<const double *>(buf + nsrc[i]);
         u[nidx[i]] = make_double4(o[0], o[1], o[2], 0.0);
     } else if (i < nn + nt) {
+        // states only go 1 -> 0 (splits are irreversible): apply the transition, never revert
+        // (the P2P buffers carry a state byte only in the step it changes)
         const int32_t e = tidx[i - nn];
-        const uint8_t v = buf[tsrc[i - nn]];
-        if (state[e] && !v)  // a ghost tet split on its owner: its edges' Vhat change
+        if (state[e] && !buf[tsrc[i - nn]]) {  // a ghost tet split on its owner: its edges' Vhat change
             for (int l = 0; l < 6; ++l) edge_dirty[eedge[(int64_t)l * E + e]] = 1;
-        state[e] = v;
+            state[e] = 0;
+        }
     }
+}
+
+__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
+    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// one warp: lane j signals peer j (after a system fence: the stage kernels' remote stores,
+// complete by stream order, are ordered before the flag), then waits for peer j's flag
+__global__ void k_p2p_sync(int64_t *flags, int64_t *const *peer_flag, const int32_t *peer_rank, int np, int64_t target,
+                           int wait) {
+    __threadfence_system();
+    for (int j = threadIdx.x; j < np; j += blockDim.x) st_release_sys(peer_flag[j], target);
+    if (wait)
+        for (int j = threadIdx.x; j < np; j += blockDim.x)
+            while (ld_acquire_sys(flags + peer_rank[j]) < target) __nanosleep(100);
+    __syncwarp();
+    __threadfence_system();
+}
+
+__global__ void k_p2p_push(const double4 *__restrict__ u, int64_t N, const int32_t *__restrict__ off,
+                           const int32_t *__restrict__ peer, const int32_t *__restrict__ byte, uint8_t *const *recv, int np,
+                           int par) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    for (int32_t i = off[k]; i < off[k + 1]; ++i) {
+        const double4 w = u[k];
+        double *o = reinterpret_cast<double *>(recv[par * np + peer[i]] + byte[i]);
+        o[0] = w.x;
+        o[1] = w.y;
+        o[2] = w.z;
+    }
+}
+
+__global__ void k_mismatch(const uint8_t *a, const uint8_t *b, const int64_t *pos, int64_t n, int64_t width, int64_t *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int64_t j = 0; j < width; ++j)
+        if (a[pos[i] + j] != b[pos[i] + j]) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(out), 1ull);
+            return;
+        }
 }
 
 // ---------------------------------------------------------------- NCCL, loaded at run time
@@ -59,6 +107,8 @@ typedef int (*fn_destroy)(ncclComm_t);
 typedef int (*fn_sendrecv)(void *, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_group)();
 typedef const char *(*fn_err)(int);
+typedef int (*fn_allgather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t);
 struct Nccl {
     void *h = nullptr;
     fn_getid getid;
@@ -67,6 +117,8 @@ struct Nccl {
     fn_sendrecv send, recv;
     fn_group gstart, gend;
     fn_err err;
+    fn_allgather allgather;
+    fn_allreduce allreduce;
 };
 Nccl &nccl() {
     static Nccl n;
@@ -81,6 +133,8 @@ Nccl &nccl() {
         n.gstart = (fn_group)dlsym(n.h, "ncclGroupStart");
         n.gend = (fn_group)dlsym(n.h, "ncclGroupEnd");
         n.err = (fn_err)dlsym(n.h, "ncclGetErrorString");
+        n.allgather = (fn_allgather)dlsym(n.h, "ncclAllGather");
+        n.allreduce = (fn_allreduce)dlsym(n.h, "ncclAllReduce");
         if (!n.getid || !n.init || !n.send || !n.recv || !n.gstart || !n.gend) {
             dlclose(n.h);
             n.h = nullptr;
@@ -141,11 +195,48 @@ void exchange_pack(const Exchange &x, const double4 *u, const uint8_t *state, cu
 }
 
 void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, const int32_t *eedge, int64_t E,
-                     uint8_t *edge_dirty, cudaStream_t st) {
+                     uint8_t *edge_dirty, cudaStream_t st, const uint8_t *recvbuf) {
     const int64_t tot = x.n_recv_nodes + x.n_recv_tets;
     if (tot)
         k_unpack<<<nblk(tot), 256, 0, st>>>(u, state, x.d_recv_nodes, x.n_recv_nodes, x.d_recv_nsrc, x.d_recv_tets,
-                                            x.n_recv_tets, x.d_recv_tsrc, x.d_recvbuf, eedge, E, edge_dirty);
+                                            x.n_recv_tets, x.d_recv_tsrc, recvbuf ? recvbuf : x.d_recvbuf, eedge, E,
+                                            edge_dirty);
+}
+
+void p2p_sync(const P2P &q, int npeers, int64_t target, bool wait, cudaStream_t st) {
+    if (npeers) k_p2p_sync<<<1, 32, 0, st>>>(q.flags, q.d_peer_flag, q.d_peer_rank, npeers, target, wait ? 1 : 0);
+}
+
+void p2p_push_nodes(const P2P &q, const double4 *u, int64_t N, int par, int npeers, cudaStream_t st) {
+    if (N) k_p2p_push<<<nblk(N), 256, 0, st>>>(u, N, q.d_noff, q.d_npeer, q.d_nbyte, q.d_peer_recv, npeers, par);
+}
+
+void count_mismatch(const uint8_t *a, const uint8_t *b, const int64_t *pos, int64_t n, int64_t width, int64_t *out,
+                    cudaStream_t st) {
+    if (n) k_mismatch<<<nblk(n), 256, 0, st>>>(a, b, pos, n, width, out);
+}
+
+bool nccl_allgather_bytes(const void *d_send, void *d_recv, size_t bytes, void *comm, cudaStream_t st, std::string &err) {
+    Nccl &n = nccl();
+    if (!n.h || !n.allgather) {
+        err = "ncclAllGather not available";
+        return false;
+    }
+    const int rc = n.allgather(d_send, d_recv, bytes, kNcclUint8, (ncclComm_t)comm, st);
+    if (rc) err = std::string("ncclAllGather: ") + (n.err ? n.err(rc) : "error");
+    return rc == 0;
+}
+
+bool nccl_allreduce_max_i64(const void *d_send, void *d_recv, size_t count, void *comm, cudaStream_t st, std::string &err) {
+    Nccl &n = nccl();
+    if (!n.h || !n.allreduce) {
+        err = "ncclAllReduce not available";
+        return false;
+    }
+    constexpr int kNcclInt64 = 4, kNcclMax = 2;
+    const int rc = n.allreduce(d_send, d_recv, count, kNcclInt64, kNcclMax, (ncclComm_t)comm, st);
+    if (rc) err = std::string("ncclAllReduce: ") + (n.err ? n.err(rc) : "error");
+    return rc == 0;
 }
 
 bool exchange_nccl(const Exchange &x, void *comm, cudaStream_t st, std::string &err) {

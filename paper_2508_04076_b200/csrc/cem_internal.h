@@ -164,6 +164,11 @@ struct Dev {
     uint8_t *edge_dirty;       // [S] 1: an incident tet split since stage AB last recomputed vhat[s]
     const int32_t *e_off, *e_inc;  // edge -> incident tets (storage ids, ascending original id)
     const uint8_t *edge_own;   // [S] 1 if this rank counts the edge in the energy ledger
+    // P2P halo (multi-GPU); p2p_np = 0: the halo goes through NCCL / loopback copies
+    uint8_t *const *p2p_recv;  // [2][p2p_np] peer receive buffer (+ this rank's segment) per step parity
+    int p2p_np;
+    const int32_t *p2p_noff, *p2p_npeer, *p2p_nbyte;  // storage node -> (peer, byte in segment) CSR
+    const int32_t *p2p_toff, *p2p_tpeer, *p2p_tbyte;  // storage tet -> (peer, byte in segment) CSR
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
     double *rec_G, *rec_area;

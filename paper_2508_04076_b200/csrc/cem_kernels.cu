@@ -495,6 +495,14 @@ __device__ __forceinline__ void split_tet(const Dev &d, int64_t e, int4 t, doubl
     d.state[e] = 0;
 #pragma unroll
     for (int l = 0; l < 6; ++l) d.edge_dirty[ldro(d.eedge + (int64_t)l * d.E + e)] = 1;  // their Vhat changes
+    if (d.p2p_np && record) {
+        // P2P halo: the owner stores the new state byte into the buffers of the peers holding the
+        // tet as a ghost (parity of the step whose sync consumes it: s for step s -> s+1,
+        // n for cem_crack_update at step n, which uses negative stamps)
+        const int par = (int)((stamp > 0 ? rec_step - 1 : rec_step) & 1);
+        for (int32_t i = __ldg(d.p2p_toff + e); i < __ldg(d.p2p_toff + e + 1); ++i)
+            d.p2p_recv[par * d.p2p_np + __ldg(d.p2p_tpeer + i)][__ldg(d.p2p_tbyte + i)] = 0;
+    }
     if (record) {  // multi-GPU: only the owning rank records (every holder deactivates)
         const int slot = atomicAdd(&d.ctr[0], 1);
         d.rec_step[slot] = rec_step;
@@ -947,7 +955,11 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
     reinterpret_cast<double *>(d.v + k)[c] = vv;
     reinterpret_cast<double *>(d.a + k)[c] = aa;
     // predictor u_{s+2} = u_{s+1} + dt v + dt^2/2 a
-    reinterpret_cast<double *>(u2p + k)[c] = c == 3 ? 0.0 : (u1 + dt * vv) + d.hdt2 * aa;
+    const double u2 = c == 3 ? 0.0 : (u1 + dt * vv) + d.hdt2 * aa;
+    reinterpret_cast<double *>(u2p + k)[c] = u2;
+    if (d.p2p_np && c < 3)  // P2P halo: the peers holding this owned node receive u_{s+2} now
+        for (int32_t i = __ldg(d.p2p_noff + k); i < __ldg(d.p2p_noff + k + 1); ++i)
+            reinterpret_cast<double *>(d.p2p_recv[(s & 1) * d.p2p_np + __ldg(d.p2p_npeer + i)] + __ldg(d.p2p_nbyte + i))[c] = u2;
     if (c < 3 && (!isfinite(u1) || !isfinite(vv) || !isfinite(aa))) {
         d.ctr[1] = 1;
         atomicMin(&d.ctr[2], ldro(d.node_orig + k));

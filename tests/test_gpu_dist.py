@@ -71,3 +71,24 @@ def test_loopback_energy_ledger(P):
         assert abs(g[k] - o[k]) <= tol * scale, (k, g[k], o[k])
     assert g["dissipated"] == pytest.approx(o["dissipated"], rel=1e-12)
     assert o["reaction"] > 0.0 and o["dissipated"] > 0.0
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_loopback_p2p_halo(P):
+    """The P2P halo (stage D and the split pass store into the peers' receive buffers, the
+    receiver unpacks after the step) gives the same bits as the single-domain oracle."""
+    dist = _gpu()
+    import paper_2508_04076_b200 as cem
+    for prob, steps in ((ci.config(0), 200),
+                        (ci.compact_tension(cells=(24, 24, 3), dims=(0.2, 0.2, 0.025), v0=60.0, t0=20e-6), 150)):
+        grp = dist.LoopbackGroup(prob, P, flags=cem.CEM_F_P2P)
+        orc = oracle.Oracle(prob)
+        for _ in range(2):
+            grp.step(steps // 2, 1)
+            orc.run(steps // 2, 1)
+        g, o, r = grp.state(), orc.state(), orc.records()
+        for k in ("u", "v", "a"):
+            assert np.array_equal(g[k], o[k]), k
+        assert np.array_equal(g["tet_state"], o["state"])
+        assert np.array_equal(g["rec_elem"], r.elem) and np.array_equal(g["rec_G"], r.G)
+        assert g["rec_elem"].size > 0
