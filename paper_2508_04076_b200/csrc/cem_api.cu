@@ -621,22 +621,40 @@ struct P2PBlob {
     int64_t seg_off_by_src[64];
 };
 cem_status p2p_setup_nccl(cem_ctx *ctx) {
+    // every rank takes part in every collective below, whatever its own outcome (a rank that
+    // returned early would leave the others waiting); the verdicts are all-reduced
     const int R = ctx->nranks, me = ctx->rank;
     const PartLocal &L = ctx->part;
     const int np = (int)L.peers.size();
-    if (R > 64 || np == 0) return CEM_OK;
     P2P &q = ctx->p2p;
-    cem_status st = p2p_alloc(ctx);
-    if (st) return st;
+    int64_t *dflag = nullptr;
+    CUDA_TRY(cudaMalloc(&dflag, 2 * sizeof(int64_t)));
+    ctx->dist_allocs.push_back(dflag);
+    auto all_ok = [&](bool ok, bool &out) -> cem_status {  // logical AND over the ranks
+        const int64_t notok = ok ? 0 : 1;
+        CUDA_TRY(cudaMemcpy(dflag, &notok, sizeof(int64_t), cudaMemcpyHostToDevice));
+        if (!nccl_allreduce_max_i64(dflag, dflag + 1, 1, ctx->comm, ctx->stream, ctx->err)) return CEM_ENCCL;
+        int64_t any = 1;
+        CUDA_TRY(cudaMemcpyAsync(&any, dflag + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        out = any == 0;
+        return CEM_OK;
+    };
+    bool ok = R <= 64;
+    if (ok && p2p_alloc(ctx) != CEM_OK) ok = false;
     P2PBlob mine{};
     for (int i = 0; i < 64; ++i) mine.seg_off_by_src[i] = -1;
-    for (int j = 0; j < np; ++j) mine.seg_off_by_src[L.peers[j]] = (int64_t)ctx->xch.recv_off[j];
-    if (cudaIpcGetMemHandle(&mine.recv0, q.recv[0]) != cudaSuccess ||
-        cudaIpcGetMemHandle(&mine.recv1, q.recv[1]) != cudaSuccess ||
-        cudaIpcGetMemHandle(&mine.flags, q.flags) != cudaSuccess) {
-        cudaGetLastError();
-        return CEM_OK;  // no IPC: NCCL halo
+    if (ok) {
+        for (int j = 0; j < np; ++j) mine.seg_off_by_src[L.peers[j]] = (int64_t)ctx->xch.recv_off[j];
+        if (cudaIpcGetMemHandle(&mine.recv0, q.recv[0]) != cudaSuccess ||
+            cudaIpcGetMemHandle(&mine.recv1, q.recv[1]) != cudaSuccess ||
+            cudaIpcGetMemHandle(&mine.flags, q.flags) != cudaSuccess)
+            ok = false;
     }
+    cudaGetLastError();
+    bool every = false;
+    cem_status st = all_ok(ok, every);
+    if (st || !every) return st;
     void *dsend = nullptr, *drecv = nullptr;
     CUDA_TRY(cudaMalloc(&dsend, sizeof(P2PBlob)));
     CUDA_TRY(cudaMalloc(&drecv, sizeof(P2PBlob) * R));
@@ -649,7 +667,6 @@ cem_status p2p_setup_nccl(cem_ctx *ctx) {
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     std::vector<uint8_t *> r0(np), r1(np);
     std::vector<int64_t *> fl(np);
-    int64_t ok = 1;
     for (int j = 0; j < np && ok; ++j) {
         const P2PBlob &b = all[L.peers[j]];
         void *a0 = nullptr, *a1 = nullptr, *af = nullptr;
@@ -657,8 +674,7 @@ cem_status p2p_setup_nccl(cem_ctx *ctx) {
             cudaIpcOpenMemHandle(&a0, b.recv0, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
             cudaIpcOpenMemHandle(&a1, b.recv1, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
             cudaIpcOpenMemHandle(&af, b.flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            ok = 0;
+            ok = false;
             break;
         }
         q.opened.push_back(a0);
@@ -668,34 +684,28 @@ cem_status p2p_setup_nccl(cem_ctx *ctx) {
         r1[j] = static_cast<uint8_t *>(a1) + b.seg_off_by_src[me];
         fl[j] = static_cast<int64_t *>(af) + me;
     }
-    int64_t *dflag = nullptr;
-    CUDA_TRY(cudaMalloc(&dflag, 2 * sizeof(int64_t)));
-    ctx->dist_allocs.push_back(dflag);
-    if (ok) {
-        st = p2p_tables(ctx, r0, r1, fl);
-        if (st) return st;
-        // self-check: push u_1 into the peers' buffers[1], sync, compare with the NCCL delivery
-        p2p_push_nodes(q, ctx->d.ubuf[1], ctx->h.N, 1, np, ctx->stream);
-        p2p_sync(q, np, 1, true, ctx->stream);
-        CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int64_t), ctx->stream));
-        count_mismatch(q.recv[1], ctx->xch.d_recvbuf, ctx->xch.d_recv_nsrc, ctx->xch.n_recv_nodes, 24, dflag,
-                       ctx->stream);
-        int64_t bad = 0;
-        CUDA_TRY(cudaMemcpyAsync(&bad, dflag, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        ok = bad == 0;
-    }
-    // every rank must agree: the largest "not ok" over the ranks decides
-    const int64_t notok = ok ? 0 : 1;
-    CUDA_TRY(cudaMemcpy(dflag, &notok, sizeof(int64_t), cudaMemcpyHostToDevice));
-    if (!nccl_allreduce_max_i64(dflag, dflag + 1, 1, ctx->comm, ctx->stream, ctx->err)) return CEM_ENCCL;
-    int64_t any_bad = 1;
-    CUDA_TRY(cudaMemcpyAsync(&any_bad, dflag + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    cudaGetLastError();
+    if (ok && p2p_tables(ctx, r0, r1, fl) != CEM_OK) ok = false;
+    st = all_ok(ok, every);  // every rank can store into its peers: run the self-check together
+    if (st || !every) return st;
+    // self-check: poison buffer 1, push u_1 into the peers' buffers[1], sync, compare with the
+    // NCCL delivery, then restore the buffer (its state bytes) from that delivery
+    const size_t rbytes = std::max<size_t>(8, ctx->xch.recv_off.back());
+    CUDA_TRY(cudaMemsetAsync(q.recv[1], 0xff, rbytes, ctx->stream));
+    st = all_ok(true, every);  // every buffer poisoned before anybody pushes
+    if (st) return st;
+    p2p_push_nodes(q, ctx->d.ubuf[1], ctx->h.N, 1, np, ctx->stream);
+    p2p_sync(q, np, 1, true, ctx->stream);
+    CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int64_t), ctx->stream));
+    count_mismatch(q.recv[1], ctx->xch.d_recvbuf, ctx->xch.d_recv_nsrc, ctx->xch.n_recv_nodes, 24, dflag, ctx->stream);
+    int64_t bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, dflag, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (any_bad == 0) {
-        p2p_enable(ctx);
-        CUDA_TRY(cudaMemcpy(const_cast<Dev *>(ctx->d.self), &ctx->d, sizeof(Dev), cudaMemcpyHostToDevice));
-    }
+    CUDA_TRY(cudaMemcpyAsync(q.recv[1], ctx->xch.d_recvbuf, rbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    st = all_ok(bad == 0, every);
+    if (st || !every) return st;
+    p2p_enable(ctx);
+    CUDA_TRY(cudaMemcpy(const_cast<Dev *>(ctx->d.self), &ctx->d, sizeof(Dev), cudaMemcpyHostToDevice));
     return CEM_OK;
 }
 
