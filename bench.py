@@ -271,7 +271,7 @@ def main():
                    "parallelism": f"{ws} GPUs: RCB slabs + 2-ring ghost layer, NCCL halo exchange per step"
                    if ws > 1 else "1 GPU",
                    "l2": "per-step working set > 126 MB L2 (no flush needed)"},
-        "roofline": {"bound": "hbm", "kernel": "cem_step: k_AB + k_C + k_D per step (PDL-chained); unit = one step",
+        "roofline": {"bound": "hbm", "kernel": "cem_step: k_AB + k_C (+ k_crit on crack steps) + k_D per step (PDL-chained); unit = one step",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_kind": peak_kind, "traffic": traffic,
                      "b_alg_bytes_per_step": balg,
