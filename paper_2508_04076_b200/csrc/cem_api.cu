@@ -43,7 +43,7 @@ struct cem_ctx {
     std::vector<void *> dist_allocs;
     P2P p2p;                      // P2P halo (multi-GPU), see cem_dist.h
     double *epart = nullptr;      // energy-ledger partials (device)
-    int64_t n_epart_edges = 0, n_epart_nodes = 0, n_wr = 0;
+    int64_t n_epart_edges = 0, n_epart_nodes = 0;
 };
 
 namespace {
@@ -80,16 +80,13 @@ struct Layout {
     }
 };
 
-// staged D blocks (blk/4 nodes each): one reaction-work accumulator per block
-int64_t n_wr_blocks(int64_t N, int blk) { return (N + (blk >> 2) - 1) / (blk >> 2); }
-
 struct Offs {
     size_t conn, geoT, eedge, incE, nodeE, X, fext, nflag, dir_v0, gc;
     size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
-    size_t rprev, wr_blk, epart, crit_list, vhat, edge_dirty, e_off, e_inc, edge_own;
+    size_t rprev, wr_dof, epart, crit_list, vhat, edge_dirty, e_off, e_inc, edge_own;
     size_t total;
 };
 
@@ -150,8 +147,8 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.nrow = L.take<uint16_t>((int64_t)p.nrow.size());
     o.tflag = L.take<uint8_t>(E);
     o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
-    o.wr_blk = L.take<double>(n_wr_blocks(N, p.blk));
-    o.epart = L.take<double>(p.nblk[ST_AB] + 2 * ((N + 255) / 256));
+    o.wr_dof = L.take<double>(h.any_dirichlet ? 3 * N : 1);
+    o.epart = L.take<double>(p.nblk[ST_AB] + 3 * ((N + 255) / 256));
     o.crit_list = L.take<int32_t>(E);
     o.vhat = L.take<double>(S);
     o.edge_dirty = L.take<uint8_t>(S);
@@ -255,7 +252,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.maxblk = p.maxblk;
     for (int g = 0; g < ST_COUNT; ++g) d.nblk[g] = p.nblk[g];
     d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
-    d.wr_blk = at<double>(b, o.wr_blk);
+    d.wr_dof = at<double>(b, o.wr_dof);
     d.crit_list = at<int32_t>(b, o.crit_list);
     d.vhat = at<double>(b, o.vhat);
     d.edge_dirty = at<uint8_t>(b, o.edge_dirty);
@@ -265,7 +262,6 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     ctx->epart = at<double>(b, o.epart);
     ctx->n_epart_edges = p.nblk[ST_AB];
     ctx->n_epart_nodes = (h.N + 255) / 256;
-    ctx->n_wr = n_wr_blocks(h.N, p.blk);
 }
 
 cem_status upload(cem_ctx *ctx, const Offs &o) {
@@ -348,7 +344,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
         }
         CUDA_TRY(put(o.rprev, r0.data(), sizeof(double) * 3 * N));
     }
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.wr_blk), 0, sizeof(double) * n_wr_blocks(N, p.blk), st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.wr_dof), 0, sizeof(double) * (h.any_dirichlet ? 3 * N : 1), st));
     // Vhat_s = sum of V_e over the active incident tets in ascending original id (the oracle's
     // stage_edge order); kept in a table, recomputed by stage AB for edges marked dirty by a split
     {
@@ -1098,19 +1094,17 @@ cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
     if (rc != CEM_OK) return rc;
     launch_energy(ctx->d, ctx->step, ctx->epart, ctx->epart + ctx->n_epart_edges, st);
     ctx->launches += 2;
-    std::vector<double> pe(ctx->n_epart_edges + 2 * ctx->n_epart_nodes), wr(ctx->n_wr);
+    std::vector<double> pe(ctx->n_epart_edges + 3 * ctx->n_epart_nodes);
     CUDA_TRY(cudaMemcpyAsync(pe.data(), ctx->epart, sizeof(double) * pe.size(), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(wr.data(), ctx->d.wr_blk, sizeof(double) * wr.size(), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
     double U = 0.0, T = 0.0, W = 0.0, Wr = 0.0;  // partials summed in block order
     for (int64_t i = 0; i < ctx->n_epart_edges; ++i) U = U + pe[i];
     for (int64_t i = 0; i < ctx->n_epart_nodes; ++i) {
-        T = T + pe[ctx->n_epart_edges + 2 * i];
-        W = W + pe[ctx->n_epart_edges + 2 * i + 1];
+        T = T + pe[ctx->n_epart_edges + 3 * i];
+        W = W + pe[ctx->n_epart_edges + 3 * i + 1];
+        Wr = Wr + pe[ctx->n_epart_edges + 3 * i + 2];
     }
-    if (ctx->d.rprev)
-        for (double x : wr) Wr = Wr + x;
     out->step = ctx->step;
     out->time = (double)ctx->step * ctx->h.dt;
     out->kinetic = 0.5 * T;

@@ -145,7 +145,7 @@ struct Dev {
     double4 *ubuf[2];          // u_m lives in ubuf[m & 1]
     double4 *v, *a;
     double *rprev;             // [N][3] support force of prescribed dofs at the last step (NULL: none)
-    double *wr_blk;            // [staged D blocks] reaction work accumulated per block (energy ledger)
+    double *wr_dof;            // [N][3] reaction work accumulated per prescribed dof (energy ledger)
     double *srec;              // [S][6]: sigma_s (11,22,33,12,23,13), 48-B records
     double *fe;                // force slots f_{e,a}, CEM_FES doubles per slot (see CEM_FES)
     const double *geoT;        // [E/32][11][32] warp-tiled geometry

@@ -863,16 +863,20 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 // original tet id) are independent, so splitting them across lanes keeps every sum sequential
 // in the oracle's order while a warp reads whole 32-B slot sectors with 8-B loads and holds
 // 4x fewer registers per slot in flight.  Newmark + BC are per component as well.
-__device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
+// nodes per D block: four lanes per node (lane 3 carries the zero w component)
+__host__ __device__ __forceinline__ int d_nodes_per_block(int threads) { return threads >> 2; }
+
+__device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t kend, const double4 *u1p, double4 *u2p,
+                                            int64_t s) {
     const int c = threadIdx.x & 3;
     const int64_t k = kbase + (threadIdx.x >> 2);
     if (kbase == 0 && threadIdx.x == 0) {  // k_crit (if any) has consumed the step's list
         pdl_wait();
         d.ctr[3] = 0;
     }
-    if (k >= d.N) return 0.0;
+    if (k >= kend) return;
     const uint8_t fl = __ldg(&d.nflag[k]);
-    if (fl & 16) return 0.0;  // multi-GPU: another rank owns (and updates) this node
+    if (fl & 16) return;  // multi-GPU: another rank owns (and updates) this node
     // static tables before the dependency wait (overlaps the previous stage's tail)
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
     constexpr int kB = CEM_D_BATCH, kQ = kB / 4;  // slots per batch, int4 index loads per batch
@@ -935,14 +939,14 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
         vv = vv + dt * (d.omg * aa + d.gamma * an);
         aa = an;
     }
-    double wr = 0.0;
     if (d.rprev && c < 3 && (fl >> c & 1)) {
         // energy ledger: support force R = m a - (f_ext - f_int) of the prescribed dof and its
-        // trapezoidal work 1/2 (R_s + R_{s+1}) (u_{s+1} - u_s) (oracle reaction_work, R22)
+        // trapezoidal work 1/2 (R_s + R_{s+1}) (u_{s+1} - u_s) (oracle reaction_work, R22),
+        // accumulated per dof (one writer: independent of how nodes are blocked)
         const double R = mk * aa - (fxc - f);
         const double us = __ldcg(reinterpret_cast<const double *>(u2p + k) + c);  // u_s, overwritten below
         double *rp = d.rprev + 3 * k + c;
-        wr = 0.5 * (*rp + R) * (u1 - us);
+        d.wr_dof[3 * k + c] += 0.5 * (*rp + R) * (u1 - us);
         *rp = R;
     }
     if (dirty == (int32_t)(s + 1)) {
@@ -952,10 +956,10 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
         if (c == 0) d.mass[k] = mk;
         if (mk == 0.0) vv = aa = 0.0;
     }
-    reinterpret_cast<double *>(d.v + k)[c] = vv;
-    reinterpret_cast<double *>(d.a + k)[c] = aa;
     // predictor u_{s+2} = u_{s+1} + dt v + dt^2/2 a
     const double u2 = c == 3 ? 0.0 : (u1 + dt * vv) + d.hdt2 * aa;
+    reinterpret_cast<double *>(d.v + k)[c] = vv;
+    reinterpret_cast<double *>(d.a + k)[c] = aa;
     reinterpret_cast<double *>(u2p + k)[c] = u2;
     if (d.p2p_np && c < 3)  // P2P halo: the peers holding this owned node receive u_{s+2} now
         for (int32_t i = __ldg(d.p2p_noff + k); i < __ldg(d.p2p_noff + k + 1); ++i)
@@ -964,16 +968,13 @@ __device__ __forceinline__ double node_update(const Dev &d, int64_t kbase, const
         d.ctr[1] = 1;
         atomicMin(&d.ctr[2], ldro(d.node_orig + k));
     }
-    return wr;
 }
 
-__device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, const double4 *u1p, double4 *u2p, int64_t s) {
-    const double w = node_update(d, kbase, u1p, u2p, s);
-    if (d.rprev) {  // prescribed dofs present: this block's reaction-work increment, fixed order
-        __shared__ double red[32];
-        const double t = block_sum(w, red);
-        if (threadIdx.x == 0) d.wr_blk[kbase / (blockDim.x >> 2)] += t;
-    }
+
+
+__device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, int64_t kend, const double4 *u1p, double4 *u2p,
+                                        int64_t s) {
+    node_update(d, kbase, min(kend, d.N), u1p, u2p, s);
 }
 
 __host__ __device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
@@ -1064,8 +1065,8 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
             case ST_AB: block_AB(d, b, u1, sm); break;
             case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
             default:
-                for (int j = 0; j < 4; ++j)  // a D item covers blk nodes, 4 lanes per node
-                    block_D(d, (int64_t)b * d.blk + j * (d.blk >> 2), u1, d.ubuf[s & 1], s);
+                for (int64_t k0 = (int64_t)b * d.blk; k0 < (int64_t)(b + 1) * d.blk; k0 += d_nodes_per_block(blockDim.x))
+                    block_D(d, k0, (int64_t)(b + 1) * d.blk, u1, d.ubuf[s & 1], s);  // a D item covers blk nodes
                 break;
         }
         __syncthreads();
@@ -1133,7 +1134,8 @@ __global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     pdl_trigger();
-    block_D(d, (int64_t)blockIdx.x * (blockDim.x >> 2), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+    const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
+    block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
 // energy ledger on the current state u_n, v_n (cem_energy): per-block partials, fixed order
@@ -1144,7 +1146,7 @@ __global__ void __launch_bounds__(256) k_energy_edges(Dev d, int64_t n, double *
 __global__ void __launch_bounds__(256) k_energy_nodes(Dev d, int64_t n, double *part) {
     __shared__ double red[32];
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double t = 0.0, w = 0.0;
+    double t = 0.0, w = 0.0, r = 0.0;
     if (k < d.N && !(__ldg(&d.nflag[k]) & 16)) {
         const double4 v = ld4(&d.v[k]), u = ld4(&d.ubuf[n & 1][k]);
         t = d.mass[k] * ((v.x * v.x + v.y * v.y) + v.z * v.z);  // oracle orc_energy
@@ -1152,12 +1154,15 @@ __global__ void __launch_bounds__(256) k_energy_nodes(Dev d, int64_t n, double *
             const double4 f = ldro4(&d.fext[k]);
             w = (f.x * u.x + f.y * u.y) + f.z * u.z;
         }
+        if (d.rprev) r = (d.wr_dof[3 * k] + d.wr_dof[3 * k + 1]) + d.wr_dof[3 * k + 2];
     }
     const double ts = block_sum(t, red);
     const double ws = block_sum(w, red);
+    const double rs = block_sum(r, red);
     if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = ts;
-        part[2 * blockIdx.x + 1] = ws;
+        part[3 * blockIdx.x] = ts;
+        part[3 * blockIdx.x + 1] = ws;
+        part[3 * blockIdx.x + 2] = rs;
     }
 }
 
@@ -1187,8 +1192,8 @@ __global__ void __launch_bounds__(256) k_fix_cur(Dev d, int64_t n, int32_t stamp
 }
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
-inline unsigned nblk_d(const Dev &d) {  // staged D: blk/4 nodes per CTA
-    const int64_t per = d.blk >> 2;
+inline unsigned nblk_d(const Dev &d) {  // staged D: 10 nodes per warp
+    const int64_t per = d_nodes_per_block(d.blk);
     return (unsigned)((d.N + per - 1) / per);
 }
 
