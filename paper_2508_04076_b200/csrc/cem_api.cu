@@ -82,7 +82,7 @@ struct Layout {
 
 struct Offs {
     size_t conn, geoT, eedge, incE, nodeE, X, fext, nflag, dir_v0, gc;
-    size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, fe, ctr;
+    size_t tet_orig, node_orig, state, mass, dirty, u0, u1, v, a, srec, srec2, fe, ctr;
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
@@ -115,7 +115,8 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.u1 = L.take<double4>(N);
     o.v = L.take<double4>(N);
     o.a = L.take<double4>(N);
-    o.srec = L.take<double>(6 * S);
+    o.srec = L.take<double>(4 * S);
+    o.srec2 = L.take<double>(2 * S);
     o.fe = L.take<double>(CEM_FES * fe_slots(E));  // + the zero slot
     o.ctr = L.take<int32_t>(8);
     o.rec_step = L.take<int64_t>(E);
@@ -205,6 +206,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.v = at<double4>(b, o.v);
     d.a = at<double4>(b, o.a);
     d.srec = at<double>(b, o.srec);
+    d.srec2 = at<double>(b, o.srec2);
     d.fe = at<double>(b, o.fe);
     d.nl_off = at<int32_t>(b, o.nl_off);
     d.nl = at<int32_t>(b, o.nl);
@@ -370,7 +372,8 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
             if (p.edge_off[s + 1] > p.edge_off[s]) own[s] = (p.tflag[p.edge_inc[p.edge_off[s]]] & 2) ? 1 : 0;
         CUDA_TRY(put(o.edge_own, own.data(), S));
     }
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 6 * S, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 4 * S, st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec2), 0, sizeof(double) * 2 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
     int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));

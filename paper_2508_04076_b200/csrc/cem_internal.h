@@ -146,7 +146,8 @@ struct Dev {
     double4 *v, *a;
     double *rprev;             // [N][3] support force of prescribed dofs at the last step (NULL: none)
     double *wr_dof;            // [N][3] reaction work accumulated per prescribed dof (energy ledger)
-    double *srec;              // [S][6]: sigma_s (11,22,33,12,23,13), 48-B records
+    double *srec;              // [S][4]: sigma_s (11, 22, 33, 12), 32-B records
+    double *srec2;             // [S][2]: sigma_s (23, 13), 16-B records
     double *fe;                // force slots f_{e,a}, CEM_FES doubles per slot (see CEM_FES)
     const double *geoT;        // [E/32][11][32] warp-tiled geometry
     const uint16_t *incE;      // [S][we]

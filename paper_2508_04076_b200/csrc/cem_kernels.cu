@@ -316,18 +316,19 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
         return;
     }
     if (!hs) return;
-    double *o = d.srec + 6u * (uint32_t)s;  // 48-B record, 16-B aligned
+    // sigma_s in two planes: (11, 22, 33, 12) as one 32-B record, (23, 13) as one 16-B record
+    double4 *o4 = reinterpret_cast<double4 *>(d.srec) + s;
+    double *o2 = d.srec2 + 2 * s;
     if (Vh == 0.0) {
-        st128(o, 0.0, 0.0);
-        st128(o + 2, 0.0, 0.0);
-        st128(o + 4, 0.0, 0.0);
+        st256(o4, 0.0, 0.0, 0.0, 0.0);
+        st128(o2, 0.0, 0.0);
         return;
     }
     const double inv = 1.0 / Vh;
     const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-    st128(o, d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33));
-    st128(o + 2, d.l2m * e33 + d.lam * (e11 + e22), d.mu * g12);
-    st128(o + 4, d.mu * g23, d.mu * g13);
+    st256(o4, d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33), d.l2m * e33 + d.lam * (e11 + e22),
+          d.mu * g12);
+    st128(o2, d.mu * g23, d.mu * g13);
 }
 
 // ------------------------------------------------------------------ crack criterion (rare path)
@@ -444,6 +445,18 @@ __device__ __forceinline__ double dsgn(double x) { return x > 0.0 ? 1.0 : (x < 0
 #ifndef CEM_D_BATCH
 #define CEM_D_BATCH 8  // stage D: force slots gathered per batch (multiple of 4)
 #endif
+// sigma_s of edge s from its two planes (rare path)
+__device__ __forceinline__ void load_sigma(const Dev &d, int64_t s, double *s6) {
+    const double4 a = ldcg256(reinterpret_cast<const double4 *>(d.srec) + s);
+    const double2 b = ldcg128(d.srec2 + 2 * s);
+    s6[0] = a.x;
+    s6[1] = a.y;
+    s6[2] = a.z;
+    s6[3] = a.w;
+    s6[4] = b.x;
+    s6[5] = b.y;
+}
+
 #ifndef CEM_CRIT_COOP_MAX
 #define CEM_CRIT_COOP_MAX 1
 #endif
@@ -542,9 +555,8 @@ __device__ __noinline__ void criterion_lane(const Dev *__restrict__ dp, int64_t 
                          w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
         const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
         w.H[l] = vdot(du, ww) > 0.0;
-        const double *sg = d.srec + 6 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
         double s6[6];
-        for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
+        load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + e), s6);
         principal(s6, w.eg[l]);
     }
     double Gb = 0.0, Ab = 0.0;
@@ -586,9 +598,8 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
                          w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
         const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
         w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
-        const double *sg = d.srec + 6 * (int64_t)ldro(d.eedge + (int64_t)l * d.E + e);
         double s6[6];
-        for (int i = 0; i < 6; ++i) s6[i] = __ldcg(sg + i);
+        load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + e), s6);
         Eig eg;
         principal(s6, eg);
         w.eg[l] = eg;
@@ -623,11 +634,11 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
 #define CEM_C_KME 3
 #endif
 
-__device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double2 x, double2 y, double2 z) {
+__device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double4 x, double2 z) {
     sm[i] = x.x;
     sm[np + i] = x.y;
-    sm[2 * np + i] = y.x;
-    sm[3 * np + i] = y.y;
+    sm[2 * np + i] = x.z;
+    sm[3 * np + i] = x.w;
     sm[4 * np + i] = z.x;
     sm[5 * np + i] = z.y;
 }
@@ -660,25 +671,24 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int32_t nid = (early && tid < nn) ? __ldg(d.nl + n0 + tid) : 0;
 #endif
     pdl_wait();  // sigma records come from stage AB
-    // ---- wave 2: gathered records (3 x 16-B loads each) -> planes 0..5
-    double2 rx[kME], ry[kME], rz[kME];
+    // ---- wave 2: gathered records (one 32-B and one 16-B load each) -> planes 0..5
+    double4 rx[kME];
+    double2 rz[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m)
         if (tid + m * nthr < ne) {
-            const double *r = d.srec + 6u * sid[m];
-            rx[m] = ldcg128(r);
-            ry[m] = ldcg128(r + 2);
-            rz[m] = ldcg128(r + 4);
+            rx[m] = ldcg256(reinterpret_cast<const double4 *>(d.srec) + sid[m]);
+            rz[m] = ldcg128(d.srec2 + 2u * sid[m]);
         }
     const double4 uw = (early && tid < nn) ? ldcg256(u + nid) : make_double4(0, 0, 0, 0);
 #pragma unroll
     for (int m = 0; m < kME; ++m) {
         const int i = tid + m * nthr;
-        if (i < ne) stage_sigma(sm, np, i, rx[m], ry[m], rz[m]);
+        if (i < ne) stage_sigma(sm, np, i, rx[m], rz[m]);
     }
     for (int i = tid + kME * nthr; i < ne; i += nthr) {  // tail
-        const double *r = d.srec + 6u * (uint32_t)__ldg(d.el + s0i + i);
-        stage_sigma(sm, np, i, ldcg128(r), ldcg128(r + 2), ldcg128(r + 4));
+        const uint32_t r = (uint32_t)__ldg(d.el + s0i + i);
+        stage_sigma(sm, np, i, ldcg256(reinterpret_cast<const double4 *>(d.srec) + r), ldcg128(d.srec2 + 2u * r));
     }
     if (early) {
         if (tid < nn) {
@@ -998,10 +1008,10 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
     const char *base;
     int64_t bytes, off;
-    if (pg == ST_AB) {
+    if (pg == ST_AB) {  // the 16-B plane is left to the normal eviction
         base = reinterpret_cast<const char *>(d.srec);
-        off = (int64_t)pb * d.blk * 48;
-        bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 48;
+        off = (int64_t)pb * d.blk * 32;
+        bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 32;
     } else {
         base = reinterpret_cast<const char *>(d.fe);
         off = (int64_t)pb * d.blk * 32 * CEM_FES;
