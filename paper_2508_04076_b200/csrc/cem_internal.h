@@ -24,6 +24,11 @@ namespace cem {
 
 // 1: stage C recomputes the element geometry from staged node coordinates instead of reading
 // the 88-B geometry record (-75 MB/step DRAM, but +4 KB shared memory per block: slower)
+// geometry layout: 0 (default) = warp-tiled planes (ten coalesced 8-B loads per tet), 1 = one
+// 96-B record per tet (three 32-B loads; measured slower: 161 vs 158 us/step on config 3)
+#ifndef CEM_GEO_AOS
+#define CEM_GEO_AOS 0
+#endif
 #ifndef CEM_C_GEOX
 #define CEM_C_GEOX 0
 #endif
@@ -111,7 +116,7 @@ struct Plan {
     std::vector<uint16_t> inc_local;  // [6E] (CSR order of edge_inc) index into the edge block's tet list
     int max_nl = 0, max_el = 0, max_tl = 0, max_nlb = 0;
     // instruction-lean layouts
-    std::vector<double> geoT;         // [E/32][11][32]: V, V/6, gradN1..3 (x,y,z) per warp tile
+    std::vector<double> geoT;         // geometry: [E][12] records or [E/32][11][32] tiles (CEM_GEO_AOS)
     int we = 8;                       // ELL width of edge incidences (multiple of 8)
     int we_max = 8;                   // largest incidence count (loop bound)
     std::vector<uint16_t> incE;       // [S][we] index into the edge block's tet list, 0xFFFF = none
@@ -149,7 +154,7 @@ struct Dev {
     double *srec;              // [S][4]: sigma_s (11, 22, 33, 12), 32-B records
     double *srec2;             // [S][2]: sigma_s (23, 13), 16-B records
     double *fe;                // force slots f_{e,a}, CEM_FES doubles per slot (see CEM_FES)
-    const double *geoT;        // [E/32][11][32] warp-tiled geometry
+    const double *geoT;        // geometry records (CEM_GEO_AOS) or warp-tiled planes
     const uint16_t *incE;      // [S][we]
     const int32_t *nodeE;      // [N][wn]
     int we, wn, we_max;        // ELL widths; we_max = largest edge incidence count

@@ -75,8 +75,37 @@ __device__ __forceinline__ double4 ldcg256(const double4 *p) {
     return r;
 }
 
+__device__ __forceinline__ double4 ldro256(const double *p) {  // read-only 32-B load (LDG.E.256.CONSTANT)
+    double4 r;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+#if CEM_GEO_AOS
+// geometry record per tet (96 B): V, V/6, gradN1..3 (x, y, z), 0 -- three 32-B loads
+__device__ __forceinline__ double geo_V(const Dev &d, uint32_t e) { return __ldg(d.geoT + 12u * e); }
+__device__ __forceinline__ void geo_record(const Dev &d, uint32_t e, double (&g)[4][3], double &V, double &V6) {
+    const double *p = d.geoT + 12u * e;
+    const double4 a = ldro256(p), b = ldro256(p + 4), c = ldro256(p + 8);
+    V = a.x;
+    V6 = a.y;
+    g[1][0] = a.z; g[1][1] = a.w; g[1][2] = b.x;
+    g[2][0] = b.y; g[2][1] = b.z; g[2][2] = b.w;
+    g[3][0] = c.x; g[3][1] = c.y; g[3][2] = c.z;
+}
+#else
 // warp-tiled geometry: tet e -> tile e>>5, lane e&31, component c at [tile][c][lane]
 __device__ __forceinline__ const double *geo_ptr(const Dev &d, uint32_t e) { return d.geoT + ((e >> 5) * 352u + (e & 31u)); }
+__device__ __forceinline__ double geo_V(const Dev &d, uint32_t e) { return __ldg(geo_ptr(d, e)); }
+__device__ __forceinline__ void geo_record(const Dev &d, uint32_t e, double (&g)[4][3], double &V, double &V6) {
+    const double *gp = geo_ptr(d, e);
+#pragma unroll
+    for (int a = 1; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
+    V = __ldg(gp);
+    V6 = __ldg(gp + 32);
+}
+#endif
 #if CEM_FES == 3
 __device__ __forceinline__ int64_t slot_tet(int32_t slot) { return slot >> 2; }  // slot = 4e + a
 #else
@@ -92,7 +121,7 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
         if (sl == d.zslot) break;
         const int64_t e = slot_tet(sl);
         if (!__ldcg(d.state + e)) continue;
-        acc = acc + (d.rho * __ldg(geo_ptr(d, e))) / 4.0;
+        acc = acc + (d.rho * geo_V(d, (uint32_t)e)) / 4.0;
     }
     return acc;
 }
@@ -164,18 +193,14 @@ __device__ __noinline__ double vhat_recompute(const Dev *__restrict__ dp, int64_
     double acc = 0.0;
     for (int32_t j = __ldg(d.e_off + s); j < __ldg(d.e_off + s + 1); ++j) {
         const int32_t e = __ldg(d.e_inc + j);
-        if (__ldcg(d.state + e)) acc = acc + __ldg(geo_ptr(d, (uint32_t)e));
+        if (__ldcg(d.state + e)) acc = acc + geo_V(d, (uint32_t)e);
     }
     return acc;
 }
 // the 9 stored gradients (nodes 1..3) and V of tet e; gradN0 = -((gradN1 + gradN2) + gradN3)
 __device__ __forceinline__ void load_geo(const Dev &d, uint32_t e, double (&g)[4][3], double &V) {
-    const double *gp = geo_ptr(d, e);
-#pragma unroll
-    for (int a = 1; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
-    V = __ldg(gp);
+    double V6;
+    geo_record(d, e, g, V, V6);
 }
 __device__ __forceinline__ void grad0(double (&g)[4][3]) {
 #pragma unroll
@@ -724,12 +749,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #if CEM_C_GEOX
         lc = __ldg(reinterpret_cast<const ushort4 *>(d.lconn) + e);
 #else
-        const double *gp = geo_ptr(d, (uint32_t)e);
-#pragma unroll
-        for (int a = 1; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) g[a][c] = __ldg(gp + 32 * (2 + 3 * (a - 1) + c));
-        cc = __ldg(gp + 32);
+        double Vd;
+        geo_record(d, (uint32_t)e, g, Vd, cc);
 #endif
     }
     __syncthreads();

@@ -439,6 +439,18 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     // ---------------------------------------------------------------- instruction-lean layouts
     {
         const int64_t nt = (E + 31) / 32;
+#if CEM_GEO_AOS
+        // per tet 12 doubles (96 B, 32-B aligned): V, V/6, gradN1..3 (x, y, z), 0
+        (void)nt;
+        p.geoT.assign((size_t)E * 12, 0.0);
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < E; ++e) {
+            double *g = p.geoT.data() + 12 * e;
+            g[0] = p.geoV[e];
+            g[1] = p.geoC[e];
+            for (int c = 0; c < 9; ++c) g[2 + c] = p.geoG[(int64_t)c * E + e];
+        }
+#else
         p.geoT.assign(nt * 11 * 32, 0.0);
 #pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < E; ++e) {
@@ -447,6 +459,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             g[32] = p.geoC[e];
             for (int c = 0; c < 9; ++c) g[32 * (2 + c)] = p.geoG[(int64_t)c * E + e];
         }
+#endif
         int mx = 1;
         for (int64_t s = 0; s < S; ++s) mx = std::max(mx, p.edge_off[s + 1] - p.edge_off[s]);
         p.we = (mx + 7) / 8 * 8;
