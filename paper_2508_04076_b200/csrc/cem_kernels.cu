@@ -482,6 +482,9 @@ __device__ __forceinline__ void load_sigma(const Dev &d, int64_t s, double *s6) 
     s6[5] = b.y;
 }
 
+#ifndef CEM_CRIT_GRID
+#define CEM_CRIT_GRID (148 * 2)  // k_crit blocks (8 warps each, grid-stride over the list)
+#endif
 #ifndef CEM_CRIT_COOP_MAX
 #define CEM_CRIT_COOP_MAX 1
 #endif
@@ -1271,7 +1274,7 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
 
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
     const bool crit = crack_on(crack_every, s);
-    const unsigned gcrit = 148 * 8;  // one warp per flagged tet, grid-stride
+    const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
         launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
         launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
