@@ -73,6 +73,8 @@ def test_validation_errors():
     assert _status(lambda: _sim(ci.make_problem(X, p.tets))) in (cem.CEM_EDEGENERATE, cem.CEM_ENEGVOL)
     assert _status(lambda: _sim(ci.make_problem(p.X, p.tets, nu=0.5))) == cem.CEM_EINVAL
     assert _status(lambda: _sim(ci.make_problem(p.X, p.tets, E=-1.0))) == cem.CEM_EINVAL
+    none_active = ci.make_problem(p.X, p.tets, tet_state=np.zeros(p.n_tets, np.uint8))
+    assert _status(lambda: _sim(none_active)) == cem.CEM_EINVAL      # no active tet to derive dt from
 
 
 def test_workspace_size_counts_edges():

@@ -216,3 +216,48 @@ def test_compact_tension_full_size():
     p = ci.config(6)
     sim, orc = run_pair(p, 8)
     assert_parity(sim, orc, p)
+
+
+# ---------------------------------------------------------------- degenerate and edge cases
+def test_single_tet():
+    """E = 1 (one partial warp, one block per stage) under a traction on one face."""
+    X, T = ci.single_tet(0.01)
+    p = ci.make_problem(X, T, tface=np.array([[1, 2, 3]]), tface_t=np.array([[2e6, 1e6, 0.0]]))
+    sim, orc = run_pair(p, 50)
+    assert_parity(sim, orc, p)
+
+
+def test_all_tets_inactive():
+    """No active tet: no stiffness, every mass 0 -> every node frozen, u stays 0."""
+    X, T, _ = ci.kuhn_lattice((3, 2, 2), (0.03, 0.02, 0.02), 1)
+    p = ci.make_problem(X, T, tet_state=np.zeros(T.shape[0], np.uint8), dt=1e-7)  # no tet to derive dt from
+    sim, orc = run_pair(p, 20)
+    g = assert_parity(sim, orc, p)
+    assert np.all(g.u == 0.0) and np.all(g.mass == 0.0)
+
+
+def test_isolated_node_and_partial_notch():
+    """A node referenced by no tet (mass 0, frozen) next to a loaded, partly inactive plate."""
+    p = ci.notched_plate(cells=(6, 4, 2), dims=(0.03, 0.02, 0.005), seed=9, steps=0)
+    X = np.vstack([p.X, [[0.5, 0.5, 0.5]]])
+    q = ci.make_problem(X, p.tets, tet_state=p.tet_state, tet_gc=p.tet_gc, tface=p.tface, tface_t=p.tface_t)
+    sim, orc = run_pair(q, 80)
+    g = assert_parity(sim, orc, q)
+    assert g.mass[-1] == 0.0 and np.all(g.u[-1] == 0.0)
+
+
+@pytest.mark.parametrize("E_target", [31, 33, 257, 511, 513])
+def test_ragged_sizes(E_target):
+    """Tet counts around warp (32) and block (256) boundaries: the first E_target tets of a
+    lattice (their nodes renumbered densely)."""
+    X, T, _ = ci.kuhn_lattice((8, 6, 2), (0.04, 0.03, 0.01), 3)
+    T = T[:E_target]
+    used, inv = np.unique(T.ravel(), return_inverse=True)
+    p = ci.make_problem(X[used], inv.reshape(-1, 4).astype(np.int32),
+                        tface=np.zeros((0, 3), np.int32), tface_t=np.zeros((0, 3)))
+    # an initial kick through a prescribed velocity on the first node keeps the run non-trivial
+    p = ci.make_problem(p.X, p.tets, vbc=(np.array([0], np.int32), np.array([7], np.uint8),
+                                          np.array([[1.0, -0.5, 0.25]]), 1e-6))
+    sim, orc = run_pair(p, 60)
+    g = assert_parity(sim, orc, p)
+    assert np.abs(g.u).max() > 0
