@@ -193,10 +193,11 @@ def test_nonfinite_detected():
     assert s.nonfinite == 1 and s.nonfinite_node >= 0
 
 
-@pytest.mark.parametrize("k,steps", [(3, 8), (2, 6)])
+@pytest.mark.parametrize("k,steps", [(3, 8), (2, 6), (1, 200), (4, 3)])
 def test_full_size_config_bitwise(k, steps):
-    """BASELINE configs[3] (1.02M tets) and configs[2] (1.08M tets) at full size in the
-    bench's launch configuration (CUDA graph), first steps against the oracle."""
+    """BASELINE configs at full size in the bench's launch configuration (PDL-chained stage
+    kernels): configs[3] (1.02M tets), [2] (1.08M), [1] (207k, 200 steps), [4] (7.68M tets on
+    one B200, 3 steps) against the oracle."""
     p = ci.config(k)
     sim, orc = run_pair(p, steps, 1)
     assert_parity(sim, orc, p)
