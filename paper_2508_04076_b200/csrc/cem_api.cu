@@ -250,6 +250,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.t0 = h.t0;
     d.flags = ctx->flags;
     d.blk = p.blk;
+    d.blk_ab = p.blk_ab;
     d.P = (int)p.sched.size();
     d.maxblk = p.maxblk;
     for (int g = 0; g < ST_COUNT; ++g) d.nblk[g] = p.nblk[g];

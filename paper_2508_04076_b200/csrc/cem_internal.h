@@ -33,6 +33,13 @@ namespace cem {
 #define CEM_C_GEOX 0
 #endif
 
+// stage AB: edges per thread (an AB block covers CEM_AB_EPT * blk consecutive edges).  2 cuts
+// AB's own time (64 vs 68 us: fewer duplicated tets) but its larger blocks overlap less with the
+// neighbouring stages under programmatic dependent launch: 164 vs 156 us per step -> 1
+#ifndef CEM_AB_EPT
+#define CEM_AB_EPT 1
+#endif
+
 // phase timer of the host preprocessing (CEM_TIMING=1 prints to stderr)
 struct PhaseClock {
     bool on = getenv("CEM_TIMING") != nullptr;
@@ -96,7 +103,8 @@ struct Plan {
     std::vector<uint8_t> tflag;       // [E] bit0 evaluate the criterion, bit1 record splits (multi-GPU masks)
     std::vector<double> gc;
     // blocks and the wavefront schedule
-    int blk = 256;                    // entities per work item
+    int blk = 256;                    // entities per work item (C: tets, D: nodes)
+    int blk_ab = 256;                 // edges per stage-AB block (CEM_AB_EPT * blk)
     int nblk[ST_COUNT] = {0, 0, 0};
     int maxblk = 0;
     std::vector<int32_t> dep_off;     // [ST_COUNT * maxblk + 1] CSR of producer blocks per (stage, block)
@@ -188,7 +196,7 @@ struct Dev {
     int32_t *cons_done;        // [ST_COUNT][maxblk] consumers finished with the block this step
     const int32_t *sched;      // [P]
     unsigned long long *head;  // work-queue head
-    int blk, P, maxblk;
+    int blk, blk_ab, P, maxblk;
     int nblk[ST_COUNT];
 };
 

@@ -207,6 +207,72 @@ __device__ __forceinline__ void grad0(double (&g)[4][3]) {
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
 }
 
+// Vhat_s from the table; an edge with a tet split since the last step is recomputed (splits
+// mark their 6 edges; ghost splits arrive marked by the halo unpack); `update` writes it back
+__device__ __forceinline__ double fetch_vhat(const Dev &d, int64_t s, bool update) {
+    const uint8_t dirty = __ldcg(d.edge_dirty + s);
+    double Vh = __ldcg(d.vhat + s);  // issued together with the flag (one round trip)
+    if (dirty) {
+        Vh = vhat_recompute(d.self, s);
+        if (update) {
+            d.vhat[s] = Vh;
+            d.edge_dirty[s] = 0;
+        }
+    }
+    return Vh;
+}
+
+// edge s: T = sum of tau over its incidences (ELL row, 8 per 16-B load, ascending original id;
+// padding -> the all-zero sentinel row nt), eps~ = T / Vhat, sigma = D eps~ -> the two sigma
+// planes; energy mode (epart): psi(eps~_s) Vhat_s / 6 added to U instead (oracle
+// orc_strain_energy, same association)
+__device__ __forceinline__ void edge_sigma(const Dev &d, int64_t s, const double *T, int tn, int nt, uint4 q,
+                                           double Vh, const double *epart, double &U) {
+    double T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
+    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
+    for (int w = 0;;) {
+        const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+        const int lim = d.we_max - w;  // warp-uniform: slots past the mesh's max incidence are skipped
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (t >= lim) break;
+            const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
+            T0 = T0 + T[r];
+            T1 = T1 + T[tn + r];
+            T2 = T2 + T[2 * tn + r];
+            T3 = T3 + T[3 * tn + r];
+            T4 = T4 + T[4 * tn + r];
+            T5 = T5 + T[5 * tn + r];
+        }
+        w += 8;
+        if (w >= d.we_max) break;  // (we_max <= we)
+        q = __ldg(row + (w >> 3));
+    }
+    if (epart) {
+        if (Vh != 0.0 && __ldg(d.edge_own + s)) {
+            const double inv = 1.0 / Vh;
+            const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
+            const double tr = e11 + e22 + e33;
+            const double ee = e11 * e11 + e22 * e22 + e33 * e33 + 0.5 * (g12 * g12 + g23 * g23 + g13 * g13);
+            U = U + (0.5 * d.lam * tr * tr + d.mu * ee) * (Vh / 6.0);
+        }
+        return;
+    }
+    // sigma_s in two planes: (11, 22, 33, 12) as one 32-B record, (23, 13) as one 16-B record
+    double4 *o4 = reinterpret_cast<double4 *>(d.srec) + s;
+    double *o2 = d.srec2 + 2 * s;
+    if (Vh == 0.0) {
+        st256(o4, 0.0, 0.0, 0.0, 0.0);
+        st128(o2, 0.0, 0.0);
+        return;
+    }
+    const double inv = 1.0 / Vh;
+    const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
+    st256(o4, d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33), d.l2m * e33 + d.lam * (e11 + e22),
+          d.mu * g12);
+    st128(o2, d.mu * g23, d.mu * g13);
+}
+
 __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm, double *epart = nullptr) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t t0 = __ldg(d.tl_off + b);
@@ -284,76 +350,28 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
         grad0(g);
         tau_row(T, tn, r, U, un, g, V, lc);
     }
-    const int64_t s = (int64_t)b * d.blk + tid;
-    const bool hs = s < d.S;
-    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
-    uint4 q = hs ? __ldg(row) : make_uint4(0, 0, 0, 0);  // first 8 incidences, before the barrier
-    double Vh = 0.0;
-    if (hs) {
-        // Vhat from the table; an edge with a tet split since the last step is recomputed
-        // (splits mark their 6 edges; ghost splits arrive marked by the halo unpack)
-        const uint8_t dirty = __ldcg(d.edge_dirty + s);
-        Vh = __ldcg(d.vhat + s);  // issued together with the flag (one round trip)
-        if (dirty) {
-            Vh = vhat_recompute(d.self, s);
-            if (!epart) {
-                d.vhat[s] = Vh;
-                d.edge_dirty[s] = 0;
-            }
-        }
-    }
+    // the block's edges: blk_ab = CEM_AB_EPT * nthr consecutive edges, thread tid takes edges
+    // sbase + j nthr + tid (j < CEM_AB_EPT); the first one's row and Vhat before the barrier
+    const int64_t sbase = (int64_t)b * d.blk_ab;
+    const int64_t send = min(d.S, sbase + d.blk_ab);
+    const int64_t s0 = sbase + tid;
+    const bool hs0 = s0 < send;
+    const uint4 qe0 = hs0 ? __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s0 * (uint32_t)d.we))
+                          : make_uint4(0, 0, 0, 0);
+    const double Vh0 = hs0 ? fetch_vhat(d, s0, epart == nullptr) : 0.0;
     __syncthreads();
-    double T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    if (hs) {
-        for (int w = 0;;) {  // ELL row: 8 incidences per 16-B load, in order
-            const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
-            const int lim = d.we_max - w;  // warp-uniform: slots past the mesh's max incidence are skipped
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                if (t >= lim) break;
-                // padding (0xffff) -> the all-zero sentinel row nt; inactive tets hold zeros
-                const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
-                T0 = T0 + T[r];
-                T1 = T1 + T[tn + r];
-                T2 = T2 + T[2 * tn + r];
-                T3 = T3 + T[3 * tn + r];
-                T4 = T4 + T[4 * tn + r];
-                T5 = T5 + T[5 * tn + r];
-            }
-            w += 8;
-            if (w >= d.we_max) break;  // (we_max <= we)
-            q = __ldg(row + (w >> 3));
-        }
+    double Ue = 0.0;  // energy mode: this thread's strain energy
+    if (hs0) edge_sigma(d, s0, T, tn, nt, qe0, Vh0, epart, Ue);
+    for (int j = 1; j < CEM_AB_EPT; ++j) {
+        const int64_t s = sbase + (int64_t)j * nthr + tid;
+        if (s < send)
+            edge_sigma(d, s, T, tn, nt, __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we)),
+                       fetch_vhat(d, s, epart == nullptr), epart, Ue);
     }
     if (epart) {
-        // energy ledger: psi(eps~_s) Vhat_s / 6, psi = 1/2 lam tr^2 + mu eps:eps (oracle
-        // orc_strain_energy, same association), summed per block in a fixed order
-        double U = 0.0;
-        if (hs && Vh != 0.0 && __ldg(d.edge_own + s)) {
-            const double inv = 1.0 / Vh;
-            const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-            const double tr = e11 + e22 + e33;
-            const double ee = e11 * e11 + e22 * e22 + e33 * e33 + 0.5 * (g12 * g12 + g23 * g23 + g13 * g13);
-            U = (0.5 * d.lam * tr * tr + d.mu * ee) * (Vh / 6.0);
-        }
-        const double t = block_sum(U, sm);  // the planes are no longer read
+        const double t = block_sum(Ue, sm);  // the planes are no longer read
         if (tid == 0) epart[b] = t;
-        return;
     }
-    if (!hs) return;
-    // sigma_s in two planes: (11, 22, 33, 12) as one 32-B record, (23, 13) as one 16-B record
-    double4 *o4 = reinterpret_cast<double4 *>(d.srec) + s;
-    double *o2 = d.srec2 + 2 * s;
-    if (Vh == 0.0) {
-        st256(o4, 0.0, 0.0, 0.0, 0.0);
-        st128(o2, 0.0, 0.0);
-        return;
-    }
-    const double inv = 1.0 / Vh;
-    const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
-    st256(o4, d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33), d.l2m * e33 + d.lam * (e11 + e22),
-          d.mu * g12);
-    st128(o2, d.mu * g23, d.mu * g13);
 }
 
 // ------------------------------------------------------------------ crack criterion (rare path)
@@ -1034,8 +1052,8 @@ __device__ __forceinline__ void discard_block(const Dev &d, int pg, int pb) {
     int64_t bytes, off;
     if (pg == ST_AB) {  // the 16-B plane is left to the normal eviction
         base = reinterpret_cast<const char *>(d.srec);
-        off = (int64_t)pb * d.blk * 32;
-        bytes = min((int64_t)d.blk, d.S - (int64_t)pb * d.blk) * 32;
+        off = (int64_t)pb * d.blk_ab * 32;
+        bytes = min((int64_t)d.blk_ab, d.S - (int64_t)pb * d.blk_ab) * 32;
     } else {
         base = reinterpret_cast<const char *>(d.fe);
         off = (int64_t)pb * d.blk * 32 * CEM_FES;

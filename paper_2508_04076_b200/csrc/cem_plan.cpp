@@ -152,6 +152,8 @@ void permute_rows(T *list, int n, const std::vector<int32_t> &row) {
 void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) {
     const int64_t N = h.N, E = h.E, S = h.S;
     p.blk = blk;
+    p.blk_ab = CEM_AB_EPT * blk;
+    const int blk_ab = p.blk_ab;
     PhaseClock clk;
     // ---------------------------------------------------------------- sweep axis + slabs
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -306,7 +308,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     clk.mark("plan: storage tables");
     // ---------------------------------------------------------------- gather lists
     {
-        const int nbt = (int)((E + blk - 1) / blk), nbs = (int)((S + blk - 1) / blk);
+        const int nbt = (int)((E + blk - 1) / blk), nbs = (int)((S + blk_ab - 1) / blk_ab);
         // per-block lists built in parallel, then concatenated
         auto concat = [](std::vector<std::vector<int32_t>> &parts, std::vector<int32_t> &off, std::vector<int32_t> &out,
                          int &mx) {
@@ -352,7 +354,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             std::vector<std::vector<int32_t>> tlv(nbs);
 #pragma omp parallel for schedule(dynamic, 16)
             for (int b = 0; b < nbs; ++b) {
-                const int64_t s0 = (int64_t)b * blk, s1 = std::min<int64_t>(S, s0 + blk);
+                const int64_t s0 = (int64_t)b * blk_ab, s1 = std::min<int64_t>(S, s0 + blk_ab);
                 auto &tmp = tlv[b];
                 tmp.assign(p.edge_inc.begin() + p.edge_off[s0], p.edge_inc.begin() + p.edge_off[s1]);
                 std::sort(tmp.begin(), tmp.end());
@@ -376,7 +378,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
 #pragma omp parallel for schedule(dynamic, 16)
             for (int b = 0; b < nbs; ++b) {
                 std::vector<int32_t> goff, gitem, row;
-                const int64_t s0 = (int64_t)b * blk, s1 = std::min<int64_t>(S, s0 + blk);
+                const int64_t s0 = (int64_t)b * blk_ab, s1 = std::min<int64_t>(S, s0 + blk_ab);
                 const int nt = p.tl_off[b + 1] - p.tl_off[b];
                 half_warp_groups(incw.data(), s0, s1, 8, wmax, goff, gitem, 0xFFFF);
                 bank_rows(nt, goff, gitem, row);
@@ -487,9 +489,10 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     clk.mark("plan: ELL tables");
     // ---------------------------------------------------------------- blocks and dependencies
     const int64_t cnt[ST_COUNT] = {S, E, N};
+    const int per[ST_COUNT] = {blk_ab, blk, blk};
     p.maxblk = 0;
     for (int g = 0; g < ST_COUNT; ++g) {
-        p.nblk[g] = (int)((cnt[g] + blk - 1) / blk);
+        p.nblk[g] = (int)((cnt[g] + per[g] - 1) / per[g]);
         p.maxblk = std::max(p.maxblk, p.nblk[g]);
     }
     // explicit producer-block lists per (stage, block)
@@ -507,7 +510,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
 #pragma omp parallel for schedule(dynamic, 64)
     for (int b = 0; b < p.nblk[ST_C]; ++b) {  // C: AB-blocks of its edge list
         auto &v = deps[(size_t)ST_C * p.maxblk + b];
-        for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) v.push_back(p.el[i] / blk);
+        for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) v.push_back(p.el[i] / blk_ab);
         finish(v);
     }
 #pragma omp parallel for schedule(dynamic, 64)
