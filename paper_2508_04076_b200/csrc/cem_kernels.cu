@@ -485,6 +485,9 @@ __device__ __forceinline__ double dsgn(double x) { return x > 0.0 ? 1.0 : (x < 0
 // (G, area, -k), which equals the oracle's sequential scan.  Split: deactivate
 // now (this step's readers of the state are done), append a record (unordered; sorted by
 // (step, element) on readback), stamp the 4 nodes so stage D recomputes their mass.
+#ifndef CEM_D_PIPE
+#define CEM_D_PIPE 1  // stage D: double-buffered slot gathers (batch i+1 in flight while batch i is summed)
+#endif
 #ifndef CEM_D_BATCH
 #define CEM_D_BATCH 8  // stage D: force slots gathered per batch (multiple of 4)
 #endif
@@ -946,6 +949,55 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     const int32_t dirty = __ldcg(d.dirty + k);
     const double *fec = d.fe + (c < 3 ? c : 0);  // lane c: component c of each slot (lane 3: unused sum)
     double f = 0.0;
+#if CEM_D_PIPE
+    // software pipeline: batch i+1's slot loads are issued before batch i is summed
+    {
+        auto unpack = [&](const int4 (&qq)[kQ], int32_t (&sl)[kB]) {
+#pragma unroll
+            for (int j = 0; j < kQ; ++j) {
+                sl[4 * j] = qq[j].x;
+                sl[4 * j + 1] = qq[j].y;
+                sl[4 * j + 2] = qq[j].z;
+                sl[4 * j + 3] = qq[j].w;
+            }
+        };
+        int32_t sl[kB];
+        unpack(q, sl);
+        double x[kB];
+#pragma unroll
+        for (int t = 0; t < kB; ++t) x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+        int w = kB;
+        bool more = sl[kB - 1] != d.zslot && w < d.wn;
+        if (more) {
+#pragma unroll
+            for (int j = 0; j < kQ; ++j)
+                q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+        }
+        for (;;) {
+            double y[kB];
+            bool more2 = false;
+            if (more) {
+                unpack(q, sl);
+#pragma unroll
+                for (int t = 0; t < kB; ++t) y[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+                w += kB;
+                more2 = sl[kB - 1] != d.zslot && w < d.wn;
+                if (more2) {
+#pragma unroll
+                    for (int j = 0; j < kQ; ++j)
+                        q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j)
+                                                : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kB; ++t) f = f + x[t];
+            if (!more) break;
+#pragma unroll
+            for (int t = 0; t < kB; ++t) x[t] = y[t];
+            more = more2;
+        }
+    }
+#else
     for (int w = 0;;) {
         // padding entries point at an all-zero slot: adding +0.0 is an exact no-op here
         int32_t sl[kB];
@@ -970,6 +1022,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
         for (int t = 0; t < kB; ++t) f = f + x[t];
         if (!more) break;
     }
+#endif
     const double dt = d.dt;
     const double t1 = (double)(s + 1) * dt;
     if (c == 3) {
