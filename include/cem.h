@@ -14,7 +14,9 @@
  *   split pass: the element is deactivated and excluded from subsequent computations (L151)
  *
  * Conventions
- *  - All floating point is IEEE fp64; indices int32 (meshes up to 2^31-1 entities).
+ *  - All floating point is IEEE fp64; indices int32 (meshes up to 2^31-1 entities); one context
+ *    holds at most 357M tets (32-bit device offsets; about 520 B of device memory per tet) --
+ *    larger meshes are partitioned over ranks (nranks > 1).
  *  - Host pointers passed to cem_init_mesh are read during the call only (copied);
  *    the caller keeps ownership and may free them afterwards.
  *  - Device memory: either the caller hands a device workspace (opts.workspace, at least
