@@ -262,3 +262,30 @@ def test_ragged_sizes(E_target):
     sim, orc = run_pair(p, 60)
     g = assert_parity(sim, orc, p)
     assert np.abs(g.u).max() > 0
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_randomized_problems(seed):
+    """Seeded random problems: lattice size, jitter, material, traction direction, a random
+    inactive set, random per-element Gc (some pre-damaged), an optional prescribed-velocity
+    patch -- 120 steps with the criterion every step, bitwise vs the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    cells = tuple(int(c) for c in rng.integers([4, 3, 2], [14, 9, 5]))
+    dims = tuple(float(x) for x in rng.uniform(0.01, 0.05, 3))
+    X, T, ijk = ci.kuhn_lattice(cells, dims, int(rng.integers(1 << 30)), jitter=float(rng.uniform(0.0, 0.2)))
+    E = T.shape[0]
+    state = (rng.random(E) > 0.05).astype(np.uint8)
+    gc = rng.uniform(0.5, 20.0, E)
+    gc[rng.random(E) < 0.02] = 0.0
+    trac = rng.normal(0.0, 2e6, 3)
+    faces, tr, _ = ci._loaded_faces(T, state, ijk, int(rng.integers(3)), 0, tuple(trac))
+    vbc = None
+    if seed % 2:
+        nodes = np.nonzero(ijk[:, 0] == cells[0])[0][:6].astype(np.int32)
+        vbc = (nodes, rng.integers(1, 8, nodes.size).astype(np.uint8), rng.normal(0.0, 2.0, (nodes.size, 3)),
+               float(rng.uniform(0.0, 2e-6)))
+    p = ci.make_problem(X, T, E=float(rng.uniform(10e9, 200e9)), nu=float(rng.uniform(0.1, 0.35)),
+                        rho=float(rng.uniform(1500, 8000)), tet_state=state, tet_gc=gc, tface=faces, tface_t=tr,
+                        vbc=vbc)
+    sim, orc = run_pair(p, 120, 1, chunks=2)
+    assert_parity(sim, orc, p)
