@@ -92,3 +92,29 @@ def test_loopback_p2p_halo(P):
         assert np.array_equal(g["tet_state"], o["state"])
         assert np.array_equal(g["rec_elem"], r.elem) and np.array_equal(g["rec_G"], r.G)
         assert g["rec_elem"].size > 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_loopback_randomized(seed):
+    """Seeded random problems on P = 2..4 ranks, copy and P2P halos alternately: bitwise."""
+    dist = _gpu()
+    import paper_2508_04076_b200 as cem
+    rng = np.random.default_rng(2000 + seed)
+    cells = tuple(int(c) for c in rng.integers([8, 4, 2], [16, 9, 4]))
+    X, T, ijk = ci.kuhn_lattice(cells, tuple(float(x) for x in rng.uniform(0.01, 0.05, 3)),
+                                int(rng.integers(1 << 30)), jitter=0.1)
+    E = T.shape[0]
+    gc = rng.uniform(0.5, 10.0, E)
+    gc[rng.random(E) < 0.03] = 0.0
+    faces, tr, _ = ci._loaded_faces(T, np.ones(E, np.uint8), ijk, 1, 0, tuple(rng.normal(0.0, 2e6, 3)))
+    p = ci.make_problem(X, T, tet_gc=gc, tface=faces, tface_t=tr)
+    P = int(rng.integers(2, 5))
+    grp = dist.LoopbackGroup(p, P, flags=cem.CEM_F_P2P if seed % 2 else 0)
+    orc = oracle.Oracle(p)
+    grp.step(100, 1)
+    orc.run(100, 1)
+    g, o, r = grp.state(), orc.state(), orc.records()
+    for k in ("u", "v", "a"):
+        assert np.array_equal(g[k], o[k]), k
+    assert np.array_equal(g["rec_elem"], r.elem) and np.array_equal(g["tet_state"], o["state"])
+    assert r.elem.size > 0
