@@ -45,6 +45,14 @@ def b_alg_per_step(N, E, S):
     return 177 * N + 17 * E + 96 * S
 
 
+# the same bytes charged to the stage kernel that moves them (DESIGN.md "Algorithmic bytes",
+# per-stage table): AB reads u (24 B/node), conn + state (17 B/tet) and writes sigma (48 B/edge);
+# C reads sigma (48 B/edge); D moves the rest of the node terms (153 B/node)
+STAGE_KERNELS = {"stage_AB_strain_edge_stress": ("k_AB", lambda N, E, S: 24 * N + 17 * E + 48 * S),
+                 "stage_C_force_criterion": ("k_C", lambda N, E, S: 48 * S),
+                 "stage_D_node_update": ("k_D", lambda N, E, S: 153 * N)}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -265,13 +273,39 @@ def main():
     for k in kernels:
         kernels[k]["share"] = kt[k] / tot_k if tot_k > 0 else None
     traffic = traffic_live = None
+    tj = {}
     tpath = os.path.join(ROOT, "profiles", "traffic_per_step.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.config == 3 and ws == 1:  # the committed capture is config 3, 1 GPU
         try:
             tj = json.load(open(tpath))
             traffic, traffic_live = tj.get("dram_bytes_per_step"), tj.get("dram_bytes_per_step_live")
         except Exception:
             traffic = traffic_live = None
+    # roofline of the dominant stage kernel: its algorithmic bytes per launch over its average
+    # launch duration (CUDA events on the launching stream, measured above); traffic = its ncu
+    # DRAM bytes per launch (one --set full capture, profiles/traffic_per_step.json)
+    roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None, "traffic": None,
+            "peak_kind": peak_kind}
+    if kernels:
+        dom = max((k for k in kernels if k in STAGE_KERNELS), key=lambda k: kernels[k]["ms_per_launch"], default=None)
+        if dom:
+            kname, fb = STAGE_KERNELS[dom]
+            b_launch = fb(N, E, S)
+            ach = b_launch / (kernels[dom]["ms_per_launch"] / 1e3) / 1e9
+            cold = tj.get("per_kernel_cold", {}).get(kname)
+            roof.update({"kernel": kname, "achieved": ach, "frac": ach / hbm, "b_alg_bytes_per_launch": b_launch,
+                         "ms_per_launch": kernels[dom]["ms_per_launch"],
+                         "traffic": (cold["dram_read"] + cold["dram_write"]) if cold else None})
+    # the whole step as one unit (SURVEY.md §8(d)'s "% of HBM roofline" of the metric)
+    roof["step"] = {"achieved": achieved, "frac": achieved / hbm, "b_alg_bytes_per_step": balg,
+                    "traffic": traffic,
+                    # DRAM bytes the step really moves (ncu, no flush between kernels; profiles/)
+                    # over this run's step time: the share of HBM bandwidth the kernels sustain
+                    "traffic_live": traffic_live,
+                    "dram_frac_live": (traffic_live / (ms_step / 1e3) / 1e9 / hbm) if traffic_live else None}
+    if roof["achieved"] is None:  # (no per-kernel times, N > 1): the step view
+        roof.update({"kernel": "cem_step (unit = one step)", "achieved": achieved, "frac": achieved / hbm,
+                     "traffic": traffic})
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -283,14 +317,7 @@ def main():
                    "parallelism": f"{ws} GPUs: RCB slabs + 2-ring ghost layer, NCCL halo exchange per step"
                    if ws > 1 else "1 GPU",
                    "l2": "per-step working set > 126 MB L2 (no flush needed)"},
-        "roofline": {"bound": "hbm", "kernel": "cem_step: k_AB + k_C (+ k_crit on crack steps) + k_D per step (PDL-chained); unit = one step",
-                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_kind": peak_kind, "traffic": traffic,
-                     "b_alg_bytes_per_step": balg,
-                     # DRAM bytes the step really moves (ncu, no flush between kernels; profiles/) over
-                     # this run's step time: the share of HBM bandwidth the kernels sustain
-                     "traffic_live": traffic_live,
-                     "dram_frac_live": (traffic_live / (ms_step / 1e3) / 1e9 / hbm) if traffic_live else None},
+        "roofline": roof,
         "kernels": kernels,
         "gpu_launches": int(launches),
         "clocks": clocks,

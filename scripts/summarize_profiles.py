@@ -92,6 +92,9 @@ json.dump({"round": rnd,
            "ncu_step_time_ns_live": live_t,
            "per_kernel_live": {n: {"time_ns": live[n]["gpu__time_duration.sum"], "dram_read": live[n]["dram__bytes_read.sum"],
                                    "dram_write": live[n]["dram__bytes_write.sum"]} for n in ALL},
+           "per_kernel_cold": {n: {"time_ns": gv(full[n], "gpu__time_duration.sum") * 1e3,
+                                   "dram_read": mb(full[n], "dram__bytes_read.sum") * 1e6,
+                                   "dram_write": mb(full[n], "dram__bytes_write.sum") * 1e6} for n in STAGES},
            "source": {"dram_bytes_per_step": "ncu --set full (default cache flush) of k_AB, k_C, k_D at step ~350",
                       "dram_bytes_per_step_live": "ncu --cache-control none --metrics dram__bytes_*.sum, steady state"}},
           open(os.path.join(out_dir, "traffic_per_step.json"), "w"), indent=1)
