@@ -42,6 +42,8 @@ struct cem_ctx {
     bool init_exchange_pending = false;
     std::vector<void *> dist_allocs;
     P2P p2p;                      // P2P halo (multi-GPU), see cem_dist.h
+    volatile int32_t *crit_seen = nullptr;  // mapped: criterion-list length of a recent step
+    int critb_min = 4096;         // lists at least this long use k_critb (env CEM_CRITB_MIN at init)
     double *epart = nullptr;      // energy-ledger partials (device)
     int64_t n_epart_edges = 0, n_epart_nodes = 0;
 };
@@ -935,6 +937,21 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         ctx->ws_bytes = o.total;
     }
     bind_views(ctx, o);
+    {
+        // the criterion kernel is chosen per step on the host from the list length of a recent
+        // step, which stage D stores here (a heuristic: results do not depend on the choice)
+        void *hp = nullptr, *dp = nullptr;
+        cudaError_t e = cudaHostAlloc(&hp, sizeof(int32_t), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(&dp, hp, 0);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cudaHostAlloc (mapped): ") + cudaGetErrorString(e);
+            return fail(CEM_ECUDA);
+        }
+        *static_cast<int32_t *>(hp) = 0;
+        if (const char *m = getenv("CEM_CRITB_MIN")) ctx->critb_min = atoi(m);
+        ctx->crit_seen = static_cast<volatile int32_t *>(hp);
+        ctx->d.crit_seen = static_cast<int32_t *>(dp);
+    }
     st = upload(ctx, o);
     if (st) return fail(st);
     if (ctx->dist) {
@@ -970,6 +987,7 @@ void cem_destroy(cem_ctx *ctx) {
     for (void *p : ctx->dist_allocs) cudaFree(p);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->crit_seen) cudaFreeHost(const_cast<int32_t *>(ctx->crit_seen));
     delete ctx;
 }
 
@@ -990,6 +1008,9 @@ cem_status cem_set_profiling(cem_ctx *ctx, int on) {
     return CEM_OK;
 }
 
+// long criterion lists (cracking phases) go to k_critb; CEM_CRITB_MIN overrides the threshold
+bool crit_heavy(const cem_ctx *ctx) { return ctx->crit_seen && *ctx->crit_seen >= ctx->critb_min; }
+
 cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (!ctx || nsteps < 0) return CEM_EINVAL;
     if (nsteps == 0) return CEM_OK;
@@ -1003,7 +1024,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
-            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr);
+            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx));
             if (ctx->p2p.on) {  // stage D / the split pass already stored into the peers' buffers
                 p2p_sync(ctx->p2p, (int)ctx->part.peers.size(), sstep + 2, true, ctx->stream);
                 exchange_unpack(ctx->xch, ctx->d.ubuf[sstep & 1], ctx->d.state, ctx->d.eedge, ctx->h.E,
@@ -1031,7 +1052,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * (ST_COUNT + 1) : nullptr;
-            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E);
+            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx));
         }
         CUDA_TRY(cudaGetLastError());
         if (ctx->profiling) ctx->prof_steps += nsteps;
@@ -1272,7 +1293,7 @@ cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_
     for (int64_t i = 0; i < nsteps; ++i) {
         const int64_t sstep = c[0]->step + i;
         for (int r = 0; r < n; ++r) {
-            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr);
+            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(c[r]));
         }
         if (c[0]->p2p.on) {  // the stores went straight into the peers' buffers; stream order syncs
             for (int r = 0; r < n; ++r) {

@@ -174,6 +174,7 @@ struct Dev {
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length
     int32_t *crit_list;        // [E] tets stage C flagged for the full criterion this step (staged path)
+    int32_t *crit_seen;        // mapped host int: stage D writes the step's list length (kernel choice)
     double *vhat;              // [S] Vhat_s = sum V_e over the active incident tets (original order)
     uint8_t *edge_dirty;       // [S] 1: an incident tet split since stage AB last recomputed vhat[s]
     const int32_t *e_off, *e_inc;  // edge -> incident tets (storage ids, ascending original id)
@@ -202,7 +203,9 @@ struct Dev {
 
 // cem_kernels.cu
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
-int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*4 or null*/);  // kernels launched
+// heavy: the criterion list is long (recent steps): k_critb instead of k_crit
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*4 or null*/,
+                       bool heavy = false);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel

@@ -506,6 +506,18 @@ __device__ __forceinline__ void load_sigma(const Dev &d, int64_t s, double *s6) 
 #ifndef CEM_CRIT_GRID
 #define CEM_CRIT_GRID (148 * 2)  // k_crit blocks (8 warps each, grid-stride over the list)
 #endif
+#ifndef CEM_CRIT_BATCH
+#define CEM_CRIT_BATCH 5  // k_critb: survivors evaluated together by one warp (6 x 5 = 30 eigen lanes)
+#endif
+#ifndef CEM_CRIT_THREADS
+#define CEM_CRIT_THREADS 128  // k_critb block size
+#endif
+#ifndef CEM_CRITB_GRID
+#define CEM_CRITB_GRID (148 * 4)
+#endif
+#ifndef CEM_CRITB_MINB
+#define CEM_CRITB_MINB 6
+#endif
 #ifndef CEM_CRIT_COOP_MAX
 #define CEM_CRIT_COOP_MAX 1
 #endif
@@ -672,6 +684,55 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
     }
     if (lane == 0 && G > gc) split_tet(d, e, t, G, k, A, rec_step, stamp, record);
     __syncwarp();  // the scratch is reused by the warp's next call
+}
+
+// Refined early-out of one listed tet, evaluated by one lane (k_crit's first pass).  With H_l the
+// Heaviside flags (the criterion's own expression), Hn_l = H_l |du_l| and g_s the Gershgorin bound
+// of sigma_s, |S(s,m)| <= |sigma_1(s)| <= g_s and |Dd(a,b,m)| <= H_ab |du_ab| |m| give for every
+// candidate |G_k| <= b_k = 1/2 (g_pr Hn_cp + g_qr Hn_cq) (pattern I) or 1/2 g_cr (Hn_cp + Hn_cq)
+// (pattern II); the tet needs the full evaluation unless max_k b_k (1 + 1e-6) <= Gc_e (the margin
+// dwarfs the rounding of b).  Tighter than stage C's bound (which ignores H and pairs the largest g
+// with the largest |du|), at a fraction of the full evaluation's cost (no eigen-solves).
+__device__ __noinline__ bool crit_refined_need(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc) {
+    const Dev &d = *dp;
+    const int4 t = __ldg(&d.conn[e]);
+    const int nid[4] = {t.x, t.y, t.z, t.w};
+    double X[4][3], U[4][3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const double4 x = ldro4(&d.X[nid[a]]);
+        const double4 uu = ldcg256(&u[nid[a]]);
+        X[a][0] = x.x; X[a][1] = x.y; X[a][2] = x.z;
+        U[a][0] = uu.x; U[a][1] = uu.y; U[a][2] = uu.z;
+    }
+    double hn[6], g[6];
+#pragma unroll
+    for (int l = 0; l < 6; ++l) {
+        const int pp = l < 3 ? 0 : (l < 5 ? 1 : 2), qq = l < 3 ? l + 1 : (l < 5 ? l - 1 : 3);
+        const Vec3 du = {U[qq][0] - U[pp][0], U[qq][1] - U[pp][1], U[qq][2] - U[pp][2]};
+        const Vec3 dX = {X[qq][0] - X[pp][0], X[qq][1] - X[pp][1], X[qq][2] - X[pp][2]};
+        const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+        hn[l] = vdot(du, ww) > 0.0 ? sqrt(vdot(du, du)) : 0.0;
+        double s6[6];
+        load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + e), s6);
+        const double r0 = fabs(s6[0]) + fabs(s6[3]) + fabs(s6[5]);
+        const double r1 = fabs(s6[1]) + fabs(s6[3]) + fabs(s6[4]);
+        const double r2 = fabs(s6[2]) + fabs(s6[4]) + fabs(s6[5]);
+        g[l] = fmax(r0, fmax(r1, r2));
+    }
+    double b = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int o0 = c == 0 ? 1 : 0, o1 = c <= 1 ? 2 : 1, o2 = c == 3 ? 2 : 3;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            const int p = f == 2 ? o1 : o0, q = f == 0 ? o1 : o2, r = f == 0 ? o2 : (f == 1 ? o1 : o0);
+            const double hp = hn[ledge(c, p)], hq = hn[ledge(c, q)];
+            b = fmax(b, 0.5 * (g[ledge(p, r)] * hp + g[ledge(q, r)] * hq));
+            b = fmax(b, 0.5 * (g[ledge(c, r)] * (hp + hq)));
+        }
+    }
+    return !(b * (1.0 + 1e-6) <= gc);
 }
 
 // ------------------------------------------------------------------ stage C: force + criterion
@@ -927,6 +988,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     const int64_t k = kbase + (threadIdx.x >> 2);
     if (kbase == 0 && threadIdx.x == 0) {  // k_crit (if any) has consumed the step's list
         pdl_wait();
+        if (d.crit_seen && (s & 15) == 0) *(volatile int32_t *)d.crit_seen = d.ctr[3];  // (host-side kernel choice)
         d.ctr[3] = 0;
     }
     if (k >= kend) return;
@@ -1231,10 +1293,110 @@ __global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
     pdl_wait();  // the list and the sigma records come from stage C / AB
     const int n = *(volatile int32_t *)&d.ctr[3];
     const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+    const double4 *u = d.ubuf[(s + 1) & 1];
     for (int i = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); i < n; i += nw) {
         const int64_t e = d.crit_list[i];
-        criterion_warp(d.self, e, d.ubuf[(s + 1) & 1], ldro(d.gc + e), s + 1, (int32_t)(s + 1),
-                       (__ldg(d.tflag + e) & 2) != 0, scratch[threadIdx.x >> 5]);
+        criterion_warp(d.self, e, u, ldro(d.gc + e), s + 1, (int32_t)(s + 1), (__ldg(d.tflag + e) & 2) != 0,
+                       scratch[threadIdx.x >> 5]);
+    }
+}
+
+// The same decisions for long lists (cracking phases), in two passes per warp round: 32 listed
+// tets, one per lane, go through the refined early-out (crit_refined_need); the survivors are
+// evaluated kCB at a time so that every warp instruction carries several tets: lanes (j, a)
+// gather the nodes, lanes (j, l) the Heaviside flags and principal pairs of the kCB x 6 edges,
+// all lanes the kCB x 24 candidates, then lane j scans tet j's candidates in the oracle's order
+// (k = 0..23; max G, ties -> larger area, then lower k: R14) and splits.
+constexpr int kCB = CEM_CRIT_BATCH;
+struct CritBatch {
+    CritScratch t[kCB];
+    double G[kCB][24], A[kCB][24];
+    int64_t ids[32];
+};
+__host__ __device__ constexpr int crit_batch_warps() { return CEM_CRIT_THREADS / 32; }
+__global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_critb(Dev d, int64_t s) {
+    extern __shared__ __align__(16) unsigned char crit_smem[];
+    CritBatch &wb = reinterpret_cast<CritBatch *>(crit_smem)[threadIdx.x >> 5];
+    pdl_trigger();
+    pdl_wait();
+    const int n = *(volatile int32_t *)&d.ctr[3];
+    const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+    const double4 *u = d.ubuf[(s + 1) & 1];
+    const int lane = threadIdx.x & 31;
+    // entries per warp round: the list spread evenly over the grid's warps (short lists: one tet
+    // per warp, as in k_crit), at most one per lane
+    const int chunk = min(32, max(1, (n + nw - 1) / nw));
+    for (int base = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * chunk; base < n; base += nw * chunk) {
+        const int i = base + lane;
+        int64_t e = 0;
+        bool need = false;
+        if (lane < chunk && i < n) {
+            e = d.crit_list[i];
+            need = crit_refined_need(d.self, e, u, ldro(d.gc + e));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (need) wb.ids[__popc(m & ((1u << lane) - 1u))] = e;
+        __syncwarp();
+        const int ns = __popc(m);
+        for (int b0 = 0; b0 < ns; b0 += kCB) {
+            const int cnt = min(kCB, ns - b0);
+            if (lane < 4 * cnt) {  // (j, a): node a of tet j
+                const int j = lane >> 2, a = lane & 3;
+                const int4 t = __ldg(&d.conn[wb.ids[b0 + j]]);
+                const int nd = a == 0 ? t.x : (a == 1 ? t.y : (a == 2 ? t.z : t.w));
+                const double4 x = ldro4(&d.X[nd]);
+                const double4 uu = ldcg256(&u[nd]);
+                CritScratch &w = wb.t[j];
+                w.X[a][0] = x.x;
+                w.X[a][1] = x.y;
+                w.X[a][2] = x.z;
+                w.U[a][0] = uu.x;
+                w.U[a][1] = uu.y;
+                w.U[a][2] = uu.z;
+            }
+            __syncwarp();
+            if (lane < 6 * cnt) {  // (j, l): edge l of tet j
+                const int j = lane / 6, l = lane - 6 * j;
+                CritScratch &w = wb.t[j];
+                const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
+                                 w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
+                const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
+                                 w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
+                const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+                w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
+                double s6[6];
+                load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + wb.ids[b0 + j]), s6);
+                Eig eg;
+                principal(s6, eg);
+                w.eg[l] = eg;
+            }
+            __syncwarp();
+            for (int q = lane; q < 24 * cnt; q += 32) {  // (j, k): candidate k of tet j
+                const int j = q / 24, k = q - 24 * j;
+                double G, A;
+                candidate(wb.t[j], k, G, A);
+                wb.G[j][k] = G;
+                wb.A[j][k] = A;
+            }
+            __syncwarp();
+            if (lane < cnt) {
+                const int j = lane;
+                const int64_t te = wb.ids[b0 + j];
+                double Gb = 0.0, Ab = 0.0;
+                int kb = -1;
+                for (int k = 0; k < 24; ++k) {
+                    const double G = wb.G[j][k], A = wb.A[j][k];
+                    if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
+                        Gb = G;
+                        kb = k;
+                        Ab = A;
+                    }
+                }
+                if (Gb > ldro(d.gc + te))
+                    split_tet(d, te, __ldg(&d.conn[te]), Gb, kb, Ab, s + 1, (int32_t)(s + 1), (__ldg(d.tflag + te) & 2) != 0);
+            }
+            __syncwarp();  // the scratch is reused by the next batch
+        }
     }
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
@@ -1297,6 +1459,7 @@ __global__ void __launch_bounds__(256) k_fix_cur(Dev d, int64_t n, int32_t stamp
 }
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
+inline size_t crit_smem_bytes() { return sizeof(CritBatch) * crit_batch_warps(); }
 inline unsigned nblk_d(const Dev &d) {  // staged D: 10 nodes per warp
     const int64_t per = d_nodes_per_block(d.blk);
     return (unsigned)((d.N + per - 1) / per);
@@ -1321,6 +1484,7 @@ void set_smem_limits(int smem_bytes) {
     cudaFuncSetAttribute(k_energy_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_critb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crit_smem_bytes());
 }
 
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st) {
@@ -1343,13 +1507,16 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev) {
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, bool heavy) {
     const bool crit = crack_on(crack_every, s);
     const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
         launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
         launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
-        if (crit) launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
+        if (crit) {
+            if (heavy) launch_pdl(k_critb, (unsigned)CEM_CRITB_GRID, (unsigned)CEM_CRIT_THREADS, crit_smem_bytes(), st, d, s);
+            else launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
+        }
         launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
         return crit ? 4 : 3;
     }
@@ -1357,7 +1524,10 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
     cudaEventRecord(ev[1], st);
     k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
-    if (crit) k_crit<<<gcrit, 256, 0, st>>>(d, s);  // timed with stage C
+    if (crit) {  // timed with stage C
+        if (heavy) k_critb<<<CEM_CRITB_GRID, CEM_CRIT_THREADS, crit_smem_bytes(), st>>>(d, s);
+        else k_crit<<<gcrit, 256, 0, st>>>(d, s);
+    }
     cudaEventRecord(ev[2], st);
     k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     cudaEventRecord(ev[3], st);

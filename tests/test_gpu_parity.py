@@ -99,6 +99,30 @@ def test_weak_block_predamage():
     assert g.rec_elem.size > 50
 
 
+@pytest.mark.parametrize("critb_min", ["0", "300"])
+@pytest.mark.parametrize("case", ["cfg0", "plate", "ct", "predamage", "overflow"])
+def test_long_list_criterion_kernel(case, critb_min, monkeypatch):
+    """The long-list criterion kernel (k_critb: refined early-out per lane, then 5 tets per warp)
+    gives the oracle's bits: forced for every step (CEM_CRITB_MIN=0) and switched in mid-run by
+    the list length (300)."""
+    monkeypatch.setenv("CEM_CRITB_MIN", critb_min)
+    if case == "cfg0":
+        p, steps = ci.config(0), 200
+    elif case == "plate":
+        p, steps = ci.notched_plate(cells=(40, 16, 4), dims=(0.1, 0.04, 0.005), seed=11, steps=300), 300
+    elif case == "ct":
+        p, steps = ci.compact_tension(cells=(24, 24, 3), dims=(0.2, 0.2, 0.025), v0=60.0, t0=20e-6), 250
+    elif case == "predamage":
+        p, steps = ci.weak_scaling_block(P=1, cells_per_rank=(30, 30, 5), steps=300), 300
+    else:
+        p = ci.notched_plate(cells=(60, 4, 20), dims=(0.06, 0.004, 0.02), seed=21, notch=False, steps=0)
+        p.tet_gc[:] = 0.0
+        steps = 8
+    sim, orc = run_pair(p, steps, 1, chunks=2)
+    g = assert_parity(sim, orc, p)
+    assert g.rec_elem.size > 0
+
+
 def test_early_out_is_conservative():
     p = ci.config(0)
     cem = _gpu()
