@@ -516,7 +516,7 @@ __device__ __forceinline__ void load_sigma(const Dev &d, int64_t s, double *s6) 
 #define CEM_CRITB_GRID (148 * 4)
 #endif
 #ifndef CEM_CRITB_MINB
-#define CEM_CRITB_MINB 6
+#define CEM_CRITB_MINB 4
 #endif
 #ifndef CEM_CRIT_COOP_MAX
 #define CEM_CRIT_COOP_MAX 1
@@ -686,33 +686,38 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
     __syncwarp();  // the scratch is reused by the warp's next call
 }
 
-// Refined early-out of one listed tet, evaluated by one lane (k_crit's first pass).  With H_l the
-// Heaviside flags (the criterion's own expression), Hn_l = H_l |du_l| and g_s the Gershgorin bound
-// of sigma_s, |S(s,m)| <= |sigma_1(s)| <= g_s and |Dd(a,b,m)| <= H_ab |du_ab| |m| give for every
-// candidate |G_k| <= b_k = 1/2 (g_pr Hn_cp + g_qr Hn_cq) (pattern I) or 1/2 g_cr (Hn_cp + Hn_cq)
-// (pattern II); the tet needs the full evaluation unless max_k b_k (1 + 1e-6) <= Gc_e (the margin
-// dwarfs the rounding of b).  Tighter than stage C's bound (which ignores H and pairs the largest g
-// with the largest |du|), at a fraction of the full evaluation's cost (no eigen-solves).
-__device__ __noinline__ bool crit_refined_need(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc) {
+#ifndef CEM_REFINED_INLINE
+#define CEM_REFINED_INLINE __device__ __noinline__
+#endif
+// Refined early-out of one listed tet, evaluated by one lane (k_critb's first pass).  Candidate k
+// has G_k = 1/2 (S(s1,m) Dd1 + S(s2,m) Dd2) / |m|^2 with |S(s,m)| <= |sigma_1(s)| |m| <= g_s |m|
+// (g_s: Gershgorin bound of sigma_s) and |Dd(a,b,m)| = H_ab |du_ab . m|, so
+//   |G_k| <= N_k / |m|,  N_k = 1/2 (g_pr H_cp |du_cp.m| + g_qr H_cq |du_cq.m|)   (pattern I)
+//                        N_k = 1/2 g_cr (H_cp |du_cp.m| + H_cq |du_cq.m|)      (pattern II),
+// with m, du and H computed by the same expressions as the full evaluation (candidate()).  The
+// tet needs the full evaluation unless every candidate has (N_k (1 + 1e-6))^2 <= Gc_e^2 |m|^2
+// (the margin dwarfs the rounding; Gc_e = 0 keeps exactly the tets with some N_k > 0, for which
+// G_k could be positive).  Costs no eigen-solve, square root or division.
+CEM_REFINED_INLINE bool crit_refined_need(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc) {
     const Dev &d = *dp;
     const int4 t = __ldg(&d.conn[e]);
     const int nid[4] = {t.x, t.y, t.z, t.w};
-    double X[4][3], U[4][3];
+    Vec3 X[4], U[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const double4 x = ldro4(&d.X[nid[a]]);
         const double4 uu = ldcg256(&u[nid[a]]);
-        X[a][0] = x.x; X[a][1] = x.y; X[a][2] = x.z;
-        U[a][0] = uu.x; U[a][1] = uu.y; U[a][2] = uu.z;
+        X[a] = Vec3{x.x, x.y, x.z};
+        U[a] = Vec3{uu.x, uu.y, uu.z};
     }
-    double hn[6], g[6];
+    double g[6];
+    bool H[6];
 #pragma unroll
     for (int l = 0; l < 6; ++l) {
-        const int pp = l < 3 ? 0 : (l < 5 ? 1 : 2), qq = l < 3 ? l + 1 : (l < 5 ? l - 1 : 3);
-        const Vec3 du = {U[qq][0] - U[pp][0], U[qq][1] - U[pp][1], U[qq][2] - U[pp][2]};
-        const Vec3 dX = {X[qq][0] - X[pp][0], X[qq][1] - X[pp][1], X[qq][2] - X[pp][2]};
+        const int pp = c_ep[l], qq = c_eq[l];
+        const Vec3 du = vsub(U[qq], U[pp]), dX = vsub(X[qq], X[pp]);
         const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
-        hn[l] = vdot(du, ww) > 0.0 ? sqrt(vdot(du, du)) : 0.0;
+        H[l] = vdot(du, ww) > 0.0;
         double s6[6];
         load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + e), s6);
         const double r0 = fabs(s6[0]) + fabs(s6[3]) + fabs(s6[5]);
@@ -720,19 +725,24 @@ __device__ __noinline__ bool crit_refined_need(const Dev *__restrict__ dp, int64
         const double r2 = fabs(s6[2]) + fabs(s6[4]) + fabs(s6[5]);
         g[l] = fmax(r0, fmax(r1, r2));
     }
-    double b = 0.0;
+    const double thr2 = gc * gc;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int k = 0; k < 24; ++k) {
+        const int c = k / 6, f = (k % 6) / 2, tt = k & 1;
         const int o0 = c == 0 ? 1 : 0, o1 = c <= 1 ? 2 : 1, o2 = c == 3 ? 2 : 3;
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-            const int p = f == 2 ? o1 : o0, q = f == 0 ? o1 : o2, r = f == 0 ? o2 : (f == 1 ? o1 : o0);
-            const double hp = hn[ledge(c, p)], hq = hn[ledge(c, q)];
-            b = fmax(b, 0.5 * (g[ledge(p, r)] * hp + g[ledge(q, r)] * hq));
-            b = fmax(b, 0.5 * (g[ledge(c, r)] * (hp + hq)));
-        }
+        const int p = f == 2 ? o1 : o0, q = f == 0 ? o1 : o2, r = f == 0 ? o2 : (f == 1 ? o1 : o0);
+        const Vec3 d1 = vsub(X[q], X[p]);
+        const Vec3 d2 = tt == 0 ? vsub(X[r], X[c]) : vsub(X[r], X[p]);
+        const Vec3 mv = vcross(d1, d2);
+        const double mm = vdot(mv, mv);
+        const int lp = ledge(c, p), lq = ledge(c, q);
+        const double ap = H[lp] ? fabs(vdot(vsub(U[p], U[c]), mv)) : 0.0;
+        const double aq = H[lq] ? fabs(vdot(vsub(U[q], U[c]), mv)) : 0.0;
+        const double N = tt == 0 ? 0.5 * (g[ledge(p, r)] * ap + g[ledge(q, r)] * aq) : 0.5 * (g[ledge(c, r)] * (ap + aq));
+        const double Nm = N * (1.0 + 1e-6);
+        if (!(Nm * Nm <= thr2 * mm)) return true;
     }
-    return !(b * (1.0 + 1e-6) <= gc);
+    return false;
 }
 
 // ------------------------------------------------------------------ stage C: force + criterion
