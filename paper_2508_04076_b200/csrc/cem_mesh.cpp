@@ -226,29 +226,62 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
     }
     clk.mark("mesh: duplicate tets");
     // ---------------------------------------------------------------- edges (ES-FEM smoothing domains)
+    // The unique (min, max) node pairs in lexicographic order, each with its incident tets in
+    // ascending id -- the order of one global sort of the (lo, hi, 6e + l) keys, built as buckets
+    // by lo (counting pass + scatter) each sorted by (hi, 6e + l): O(6E) plus small sorts, parallel.
     {
-        std::vector<std::pair<uint64_t, int64_t>> k;
-        edge_keys(m, k);
-        int64_t S = 0;
-        for (size_t i = 0; i < k.size(); ++i)
-            if (i == 0 || k[i].first != k[i - 1].first) ++S;
+        const int64_t NE = 6 * E;
+        std::vector<int32_t> boff(N + 1, 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < E; ++e)
+            for (int l = 0; l < 6; ++l) {
+                const int32_t i = m->tets[4 * e + kEdgeP[l]], j = m->tets[4 * e + kEdgeQ[l]];
+                __atomic_fetch_add(&boff[std::min(i, j) + 1], 1, __ATOMIC_RELAXED);
+            }
+        for (int64_t n = 0; n < N; ++n) boff[n + 1] += boff[n];
+        std::vector<uint64_t> item(NE);  // hi << 32 | (6e + l)   (6E < 2^32: cem_init_mesh's size limit)
+        {
+            std::vector<int32_t> fill(boff.begin(), boff.end() - 1);
+#pragma omp parallel for schedule(static)
+            for (int64_t e = 0; e < E; ++e)
+                for (int l = 0; l < 6; ++l) {
+                    const int32_t i = m->tets[4 * e + kEdgeP[l]], j = m->tets[4 * e + kEdgeQ[l]];
+                    const int32_t pos = __atomic_fetch_add(&fill[std::min(i, j)], 1, __ATOMIC_RELAXED);
+                    item[pos] = (uint64_t)(uint32_t)std::max(i, j) << 32 | (uint64_t)(6 * e + l);
+                }
+        }
+        std::vector<int64_t> ecnt(N + 1, 0);  // distinct edges per bucket -> first edge id of a bucket
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t n = 0; n < N; ++n) {
+            std::sort(item.begin() + boff[n], item.begin() + boff[n + 1]);
+            int64_t c = 0;
+            for (int32_t i = boff[n]; i < boff[n + 1]; ++i)
+                if (i == boff[n] || (item[i] >> 32) != (item[i - 1] >> 32)) ++c;
+            ecnt[n + 1] = c;
+        }
+        for (int64_t n = 0; n < N; ++n) ecnt[n + 1] += ecnt[n];
+        const int64_t S = ecnt[N];
         h.S = S;
         h.edge_nodes.resize(2 * S);
         h.edge_off.assign(S + 1, 0);
-        h.edge_inc.resize(6 * E);
-        h.elem_edge.resize(6 * E);
-        int64_t s = -1;
-        for (size_t i = 0; i < k.size(); ++i) {
-            if (i == 0 || k[i].first != k[i - 1].first) {
-                ++s;
-                h.edge_nodes[2 * s] = (int32_t)(k[i].first >> 32);
-                h.edge_nodes[2 * s + 1] = (int32_t)(k[i].first & 0xffffffffu);
-                h.edge_off[s] = (int32_t)i;
+        h.edge_inc.resize(NE);
+        h.elem_edge.resize(NE);
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t s = ecnt[n] - 1;
+            for (int32_t i = boff[n]; i < boff[n + 1]; ++i) {
+                const uint32_t hi = (uint32_t)(item[i] >> 32), te = (uint32_t)item[i];
+                if (i == boff[n] || hi != (uint32_t)(item[i - 1] >> 32)) {
+                    ++s;
+                    h.edge_nodes[2 * s] = (int32_t)n;
+                    h.edge_nodes[2 * s + 1] = (int32_t)hi;
+                    h.edge_off[s] = i;
+                }
+                h.edge_inc[i] = (int32_t)(te / 6);  // ascending tet id within an edge
+                h.elem_edge[te] = (int32_t)s;
             }
-            h.edge_inc[i] = (int32_t)(k[i].second / 6);  // ascending tet id within an edge
-            h.elem_edge[k[i].second] = (int32_t)s;
         }
-        h.edge_off[S] = (int32_t)k.size();
+        h.edge_off[S] = (int32_t)NE;
     }
     clk.mark("mesh: edges");
     // ---------------------------------------------------------------- node incidence (ascending e)

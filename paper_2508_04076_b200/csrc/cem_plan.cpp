@@ -25,6 +25,9 @@ namespace {
 // colours where possible (greedy, most-constrained item first, then a swap pass that lowers
 // sum_g sum_k cnt[g][k]^2).  Colour capacities are exact, so rows stay 0..n-1; inside a colour
 // items keep ascending order (gather locality).  Returns row[item].
+#ifndef CEM_BANK_SWAP
+#define CEM_BANK_SWAP 0  // swap passes after the greedy colouring (1: -0.3 us/step, +45 ms host time)
+#endif
 void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_t> &gitem, std::vector<int32_t> &row) {
     row.assign(n, 0);
     if (n <= 16) {
@@ -80,7 +83,7 @@ void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_
         }
         col[it] = to;
     };
-    for (int pass = 0; pass < 1; ++pass) {
+    for (int pass = 0; pass < CEM_BANK_SWAP; ++pass) {
         bool any = false;
         for (int a = 0; a < n; ++a) {
             const int ka = col[a];
@@ -145,6 +148,21 @@ template <class T>
 void permute_rows(T *list, int n, const std::vector<int32_t> &row) {
     std::vector<T> tmp(list, list + n);
     for (int i = 0; i < n; ++i) list[row[i]] = tmp[i];
+}
+
+// Deduplicate vals[0..n) into the ascending list `uniq` and report every entry's position in it
+// through put(i, pos): one sort of (value, index) keys instead of a sort plus n binary searches.
+template <class Put>
+void dedupe(const int32_t *vals, int n, std::vector<int32_t> &uniq, std::vector<uint64_t> &scratch, Put put) {
+    scratch.resize(n);
+    for (int i = 0; i < n; ++i) scratch[i] = (uint64_t)(uint32_t)vals[i] << 32 | (uint32_t)i;
+    std::sort(scratch.begin(), scratch.end());
+    uniq.clear();
+    for (int i = 0; i < n; ++i) {
+        const int32_t v = (int32_t)(scratch[i] >> 32);
+        if (uniq.empty() || uniq.back() != v) uniq.push_back(v);
+        put((int)(uint32_t)scratch[i], (int)uniq.size() - 1);
+    }
 }
 
 }  // namespace
@@ -326,25 +344,22 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         p.ledge.assign(8 * E, 0);
         {
             std::vector<std::vector<int32_t>> nlv(nbt), elv(nbt);
-#pragma omp parallel for schedule(dynamic, 16)
-            for (int b = 0; b < nbt; ++b) {
-                const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
-                auto &tn = nlv[b];
-                tn.assign(p.conn.begin() + 4 * e0, p.conn.begin() + 4 * e1);
-                std::sort(tn.begin(), tn.end());
-                tn.erase(std::unique(tn.begin(), tn.end()), tn.end());
-                for (int64_t e = e0; e < e1; ++e)
-                    for (int a = 0; a < 4; ++a)
-                        p.lconn[4 * e + a] = (uint16_t)(std::lower_bound(tn.begin(), tn.end(), p.conn[4 * e + a]) - tn.begin());
-                auto &te = elv[b];
-                for (int64_t e = e0; e < e1; ++e)
-                    for (int l = 0; l < 6; ++l) te.push_back(p.eedge[(int64_t)l * E + e]);
-                std::sort(te.begin(), te.end());
-                te.erase(std::unique(te.begin(), te.end()), te.end());
-                for (int64_t e = e0; e < e1; ++e)
-                    for (int l = 0; l < 6; ++l)
-                        p.ledge[8 * e + l] =
-                            (uint16_t)(std::lower_bound(te.begin(), te.end(), p.eedge[(int64_t)l * E + e]) - te.begin());
+#pragma omp parallel
+            {
+                std::vector<uint64_t> scratch;
+                std::vector<int32_t> vals;
+#pragma omp for schedule(dynamic, 16)
+                for (int b = 0; b < nbt; ++b) {
+                    const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
+                    const int n = (int)(e1 - e0);
+                    dedupe(p.conn.data() + 4 * e0, 4 * n, nlv[b], scratch,
+                           [&](int i, int pos) { p.lconn[4 * e0 + i] = (uint16_t)pos; });
+                    vals.resize(6 * n);
+                    for (int i = 0; i < n; ++i)
+                        for (int l = 0; l < 6; ++l) vals[6 * i + l] = p.eedge[(int64_t)l * E + e0 + i];
+                    dedupe(vals.data(), 6 * n, elv[b], scratch,
+                           [&](int i, int pos) { p.ledge[8 * (e0 + i / 6) + i % 6] = (uint16_t)pos; });
+                }
             }
             concat(nlv, p.nl_off, p.nl, p.max_nl);
             concat(elv, p.el_off, p.el, p.max_el);
@@ -352,15 +367,16 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         p.inc_local.assign(p.edge_inc.size(), 0);
         {
             std::vector<std::vector<int32_t>> tlv(nbs);
-#pragma omp parallel for schedule(dynamic, 16)
-            for (int b = 0; b < nbs; ++b) {
-                const int64_t s0 = (int64_t)b * blk_ab, s1 = std::min<int64_t>(S, s0 + blk_ab);
-                auto &tmp = tlv[b];
-                tmp.assign(p.edge_inc.begin() + p.edge_off[s0], p.edge_inc.begin() + p.edge_off[s1]);
-                std::sort(tmp.begin(), tmp.end());
-                tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-                for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j)
-                    p.inc_local[j] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), p.edge_inc[j]) - tmp.begin());
+#pragma omp parallel
+            {
+                std::vector<uint64_t> scratch;
+#pragma omp for schedule(dynamic, 16)
+                for (int b = 0; b < nbs; ++b) {
+                    const int64_t s0 = (int64_t)b * blk_ab, s1 = std::min<int64_t>(S, s0 + blk_ab);
+                    const int32_t j0 = p.edge_off[s0];
+                    dedupe(p.edge_inc.data() + j0, p.edge_off[s1] - j0, tlv[b], scratch,
+                           [&](int i, int pos) { p.inc_local[j0 + i] = (uint16_t)pos; });
+                }
             }
             concat(tlv, p.tl_off, p.tl, p.max_tl);
         }
@@ -368,6 +384,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         // bank-aware order of each edge block's tet list: lanes = edges, column t = t-th incidence
         {
             std::vector<uint16_t> incw((size_t)S * 8, 0xFFFF);  // first 8 incidences per edge (ELL view)
+#pragma omp parallel for schedule(static)
             for (int64_t s = 0; s < S; ++s)
                 for (int32_t j = p.edge_off[s]; j < std::min(p.edge_off[s + 1], p.edge_off[s] + 8); ++j)
                     incw[8 * s + (j - p.edge_off[s])] = p.inc_local[j];
@@ -393,17 +410,19 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         p.tconn.assign(4 * p.tl.size(), 0);
         {
             std::vector<std::vector<int32_t>> nbv(nbs);
-#pragma omp parallel for schedule(dynamic, 16)
-            for (int b = 0; b < nbs; ++b) {
-                auto &nodes = nbv[b];
-                for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
-                    for (int a = 0; a < 4; ++a) nodes.push_back(p.conn[4 * (int64_t)p.tl[i] + a]);
-                std::sort(nodes.begin(), nodes.end());
-                nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
-                for (int32_t i = p.tl_off[b]; i < p.tl_off[b + 1]; ++i)
-                    for (int a = 0; a < 4; ++a)
-                        p.tconn[4 * (int64_t)i + a] = (uint16_t)(std::lower_bound(nodes.begin(), nodes.end(),
-                                                                                   p.conn[4 * (int64_t)p.tl[i] + a]) - nodes.begin());
+#pragma omp parallel
+            {
+                std::vector<uint64_t> scratch;
+                std::vector<int32_t> vals;
+#pragma omp for schedule(dynamic, 16)
+                for (int b = 0; b < nbs; ++b) {
+                    const int32_t t0 = p.tl_off[b], nt = p.tl_off[b + 1] - t0;
+                    vals.resize(4 * (size_t)nt);
+                    for (int32_t i = 0; i < nt; ++i)
+                        for (int a = 0; a < 4; ++a) vals[4 * i + a] = p.conn[4 * (int64_t)p.tl[t0 + i] + a];
+                    dedupe(vals.data(), 4 * nt, nbv[b], scratch,
+                           [&](int i, int pos) { p.tconn[4 * (int64_t)t0 + i] = (uint16_t)pos; });
+                }
             }
             concat(nbv, p.nlb_off, p.nlb, p.max_nlb);
         }

@@ -118,3 +118,25 @@ def test_loopback_randomized(seed):
         assert np.array_equal(g[k], o[k]), k
     assert np.array_equal(g["rec_elem"], r.elem) and np.array_equal(g["tet_state"], o["state"])
     assert r.elem.size > 0
+
+
+@pytest.mark.parametrize("P,p2p", [(2, False), (3, True)])
+def test_loopback_long_list_criterion_kernel(P, p2p, monkeypatch):
+    """Every step through the long-list criterion kernel (k_critb) on P ranks: owner-only
+    records, ghost splits delivered by the halo (copy or P2P), bitwise equal to the oracle."""
+    monkeypatch.setenv("CEM_CRITB_MIN", "0")
+    dist = _gpu()
+    import paper_2508_04076_b200 as cem
+    p = ci.compact_tension(cells=(24, 24, 3), dims=(0.2, 0.2, 0.025), v0=60.0, t0=20e-6)
+    grp = dist.LoopbackGroup(p, P, flags=cem.CEM_F_P2P if p2p else 0)
+    orc = oracle.Oracle(p)
+    for _ in range(2):
+        grp.step(100, 1)
+        orc.run(100, 1)
+    g, o, r = grp.state(), orc.state(), orc.records()
+    for k in ("u", "v", "a"):
+        assert np.array_equal(g[k], o[k]), k
+    assert np.array_equal(g["mass"], o["m"])
+    assert np.array_equal(g["tet_state"], o["state"])
+    assert np.array_equal(g["rec_elem"], r.elem) and np.array_equal(g["rec_G"], r.G)
+    assert r.elem.size > 0
