@@ -95,7 +95,6 @@ struct Plan {
     // storage-order arrays
     std::vector<int32_t> conn;        // [E][4] new node ids (int4)
     std::vector<double> geoV, geoC;   // [E] V, V/6
-    std::vector<double> geoG;         // [9][E] gradN1x,1y,1z,2x,...,3z
     std::vector<int32_t> eedge;       // [6][E] new edge ids
     std::vector<int32_t> edge_off, edge_inc;   // CSR over new edges, new tet ids, original order
     std::vector<int32_t> node_off, node_ent;   // CSR over new nodes, (new e << 2 | a), original order

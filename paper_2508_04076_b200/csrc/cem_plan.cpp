@@ -278,7 +278,12 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     p.conn.resize(4 * E);
     p.geoV.resize(E);
     p.geoC.resize(E);
-    p.geoG.resize(9 * E);
+    // geometry records written straight into the device layout (CEM_GEO_AOS)
+#if CEM_GEO_AOS
+    p.geoT.assign((size_t)E * 12, 0.0);  // per tet 12 doubles (96 B): V, V/6, gradN1..3 (x, y, z), 0
+#else
+    p.geoT.assign((size_t)((E + 31) / 32) * 11 * 32, 0.0);  // [E/32][11][32] warp tiles
+#endif
     p.eedge.resize(6 * E);
     p.state.resize(E);
     p.tflag.resize(E);
@@ -289,8 +294,17 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         for (int a = 0; a < 4; ++a) p.conn[4 * en + a] = p.node_old2new[h.tet[4 * eo + a]];
         p.geoV[en] = h.V[eo];
         p.geoC[en] = h.V[eo] / 6.0;
+#if CEM_GEO_AOS
+        double *g = p.geoT.data() + 12 * en;
+        const int gs = 1;
+#else
+        double *g = p.geoT.data() + (en >> 5) * 352 + (en & 31);
+        const int gs = 32;
+#endif
+        g[0] = p.geoV[en];
+        g[gs] = p.geoC[en];
         for (int a = 1; a < 4; ++a)
-            for (int c = 0; c < 3; ++c) p.geoG[(int64_t)(3 * (a - 1) + c) * E + en] = h.grad[12 * eo + 3 * a + c];
+            for (int c = 0; c < 3; ++c) g[gs * (2 + 3 * (a - 1) + c)] = h.grad[12 * eo + 3 * a + c];
         for (int l = 0; l < 6; ++l) p.eedge[(int64_t)l * E + en] = edge_old2new[h.elem_edge[6 * eo + l]];
         p.state[en] = h.state[eo];
         p.tflag[en] = tflag_orig ? tflag_orig[eo] : 3;
@@ -459,28 +473,6 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     }
     // ---------------------------------------------------------------- instruction-lean layouts
     {
-        const int64_t nt = (E + 31) / 32;
-#if CEM_GEO_AOS
-        // per tet 12 doubles (96 B, 32-B aligned): V, V/6, gradN1..3 (x, y, z), 0
-        (void)nt;
-        p.geoT.assign((size_t)E * 12, 0.0);
-#pragma omp parallel for schedule(static)
-        for (int64_t e = 0; e < E; ++e) {
-            double *g = p.geoT.data() + 12 * e;
-            g[0] = p.geoV[e];
-            g[1] = p.geoC[e];
-            for (int c = 0; c < 9; ++c) g[2 + c] = p.geoG[(int64_t)c * E + e];
-        }
-#else
-        p.geoT.assign(nt * 11 * 32, 0.0);
-#pragma omp parallel for schedule(static)
-        for (int64_t e = 0; e < E; ++e) {
-            double *g = p.geoT.data() + (e >> 5) * 352 + (e & 31);
-            g[0] = p.geoV[e];
-            g[32] = p.geoC[e];
-            for (int c = 0; c < 9; ++c) g[32 * (2 + c)] = p.geoG[(int64_t)c * E + e];
-        }
-#endif
         int mx = 1;
         for (int64_t s = 0; s < S; ++s) mx = std::max(mx, p.edge_off[s + 1] - p.edge_off[s]);
         p.we = (mx + 7) / 8 * 8;
