@@ -43,7 +43,7 @@ struct cem_ctx {
     std::vector<void *> dist_allocs;
     P2P p2p;                      // P2P halo (multi-GPU), see cem_dist.h
     volatile int32_t *crit_seen = nullptr;  // mapped: criterion-list length of a recent step
-    int critb_min = 4096;         // lists at least this long use k_critb (env CEM_CRITB_MIN at init)
+    int critb_min = 4096;         // lists at least this long use k_filter + k_eval (env CEM_CRITB_MIN at init)
     double *epart = nullptr;      // energy-ledger partials (device)
     int64_t n_epart_edges = 0, n_epart_nodes = 0;
 };
@@ -120,7 +120,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.srec = L.take<double>(4 * S);
     o.srec2 = L.take<double>(2 * S);
     o.fe = L.take<double>(CEM_FES * fe_slots(E));  // + the zero slot
-    o.ctr = L.take<int32_t>(8);
+    o.ctr = L.take<int32_t>(16);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
     o.rec_cand = L.take<int32_t>(E);
@@ -152,7 +152,7 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.wr_dof = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.epart = L.take<double>(p.nblk[ST_AB] + 3 * ((N + 255) / 256));
-    o.crit_list = L.take<int32_t>(E);
+    o.crit_list = L.take<int32_t>(2 * E);  // the step's list + the refined filter's survivors
     o.vhat = L.take<double>(S);
     o.edge_dirty = L.take<uint8_t>(S);
     o.e_off = L.take<int32_t>(S + 1);
@@ -378,7 +378,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 4 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec2), 0, sizeof(double) * 2 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
-    int32_t ctr[8] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0};
+    int32_t ctr[16] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
     CUDA_TRY(put(o.dep_off, p.dep_off.data(), sizeof(int32_t) * p.dep_off.size()));
@@ -1008,7 +1008,7 @@ cem_status cem_set_profiling(cem_ctx *ctx, int on) {
     return CEM_OK;
 }
 
-// long criterion lists (cracking phases) go to k_critb; CEM_CRITB_MIN overrides the threshold
+// long criterion lists (cracking phases) go to k_filter + k_eval; CEM_CRITB_MIN overrides the threshold
 bool crit_heavy(const cem_ctx *ctx) { return ctx->crit_seen && *ctx->crit_seen >= ctx->critb_min; }
 
 cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {

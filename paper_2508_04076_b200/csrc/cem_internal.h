@@ -171,7 +171,8 @@ struct Dev {
     const uint16_t *lconn, *ledge;
     int smem_bytes, smem_ab, smem_c;  // dynamic shared memory: persistent kernel (max), per stage
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
-    int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length
+    int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length,
+                               // [8] survivors of the refined filter (crit_list + E)
     int32_t *crit_list;        // [E] tets stage C flagged for the full criterion this step (staged path)
     int32_t *crit_seen;        // mapped host int: stage D writes the step's list length (kernel choice)
     double *vhat;              // [S] Vhat_s = sum V_e over the active incident tets (original order)
@@ -202,7 +203,7 @@ struct Dev {
 
 // cem_kernels.cu
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
-// heavy: the criterion list is long (recent steps): k_critb instead of k_crit
+// heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*4 or null*/,
                        bool heavy = false);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);

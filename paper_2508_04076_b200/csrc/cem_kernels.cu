@@ -507,13 +507,19 @@ __device__ __forceinline__ void load_sigma(const Dev &d, int64_t s, double *s6) 
 #define CEM_CRIT_GRID (148 * 2)  // k_crit blocks (8 warps each, grid-stride over the list)
 #endif
 #ifndef CEM_CRIT_BATCH
-#define CEM_CRIT_BATCH 5  // k_critb: survivors evaluated together by one warp (6 x 5 = 30 eigen lanes)
+#define CEM_CRIT_BATCH 5  // k_eval: survivors evaluated together by one warp (6 x 5 = 30 eigen lanes)
 #endif
 #ifndef CEM_CRIT_THREADS
-#define CEM_CRIT_THREADS 128  // k_critb block size
+#define CEM_CRIT_THREADS 128  // k_eval block size
 #endif
 #ifndef CEM_CRITB_GRID
-#define CEM_CRITB_GRID (148 * 4)
+#define CEM_CRITB_GRID (148 * 4)  // k_eval blocks
+#endif
+#ifndef CEM_FILTER_MINB
+#define CEM_FILTER_MINB 2  // 128 registers: fewer warps but no large spills (measured best)
+#endif
+#ifndef CEM_FILTER_GRID
+#define CEM_FILTER_GRID (148 * 2)  // k_filter blocks (256 threads, grid-stride over the list)
 #endif
 #ifndef CEM_CRITB_MINB
 #define CEM_CRITB_MINB 4
@@ -686,10 +692,7 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
     __syncwarp();  // the scratch is reused by the warp's next call
 }
 
-#ifndef CEM_REFINED_INLINE
-#define CEM_REFINED_INLINE __device__ __noinline__
-#endif
-// Refined early-out of one listed tet, evaluated by one lane (k_critb's first pass).  Candidate k
+// Refined early-out of one listed tet, evaluated by one thread (k_filter).  Candidate k
 // has G_k = 1/2 (S(s1,m) Dd1 + S(s2,m) Dd2) / |m|^2 with |S(s,m)| <= |sigma_1(s)| |m| <= g_s |m|
 // (g_s: Gershgorin bound of sigma_s) and |Dd(a,b,m)| = H_ab |du_ab . m|, so
 //   |G_k| <= N_k / |m|,  N_k = 1/2 (g_pr H_cp |du_cp.m| + g_qr H_cq |du_cq.m|)   (pattern I)
@@ -698,7 +701,7 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
 // tet needs the full evaluation unless every candidate has (N_k (1 + 1e-6))^2 <= Gc_e^2 |m|^2
 // (the margin dwarfs the rounding; Gc_e = 0 keeps exactly the tets with some N_k > 0, for which
 // G_k could be positive).  Costs no eigen-solve, square root or division.
-CEM_REFINED_INLINE bool crit_refined_need(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc) {
+__device__ __forceinline__ bool crit_refined_need(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc) {
     const Dev &d = *dp;
     const int4 t = __ldg(&d.conn[e]);
     const int nid[4] = {t.x, t.y, t.z, t.w};
@@ -999,7 +1002,11 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     if (kbase == 0 && threadIdx.x == 0) {  // k_crit (if any) has consumed the step's list
         pdl_wait();
         if (d.crit_seen && (s & 15) == 0) *(volatile int32_t *)d.crit_seen = d.ctr[3];  // (host-side kernel choice)
+#ifdef CEM_DEBUG_LIST
+        if (s % 100 == 0) printf("[list] step %lld: %d listed of %lld tets\n", (long long)s, d.ctr[3], (long long)d.E);
+#endif
         d.ctr[3] = 0;
+        d.ctr[8] = 0;
     }
     if (k >= kend) return;
     const uint8_t fl = __ldg(&d.nflag[k]);
@@ -1311,102 +1318,113 @@ __global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
     }
 }
 
-// The same decisions for long lists (cracking phases), in two passes per warp round: 32 listed
-// tets, one per lane, go through the refined early-out (crit_refined_need); the survivors are
-// evaluated kCB at a time so that every warp instruction carries several tets: lanes (j, a)
-// gather the nodes, lanes (j, l) the Heaviside flags and principal pairs of the kCB x 6 edges,
-// all lanes the kCB x 24 candidates, then lane j scans tet j's candidates in the oracle's order
-// (k = 0..23; max G, ties -> larger area, then lower k: R14) and splits.
+// The same decisions for long lists (cracking phases), in two kernels.  k_filter: one thread per
+// listed tet applies the refined early-out (crit_refined_need) and appends the survivors (order
+// irrelevant: every decision is independent) -- a latency-bound pass that runs at full
+// occupancy.  k_eval: each warp evaluates kCB survivors at a time so that every warp instruction
+// carries several tets: lanes (j, a) gather the nodes, lanes (j, l) the Heaviside flags and
+// principal pairs of the kCB x 6 edges, all lanes the kCB x 24 candidates, then lane j scans tet
+// j's candidates in the oracle's order (k = 0..23; max G, ties -> larger area, then lower k: R14)
+// and splits.
 constexpr int kCB = CEM_CRIT_BATCH;
 struct CritBatch {
     CritScratch t[kCB];
     double G[kCB][24], A[kCB][24];
-    int64_t ids[32];
 };
 __host__ __device__ constexpr int crit_batch_warps() { return CEM_CRIT_THREADS / 32; }
-__global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_critb(Dev d, int64_t s) {
-    extern __shared__ __align__(16) unsigned char crit_smem[];
-    CritBatch &wb = reinterpret_cast<CritBatch *>(crit_smem)[threadIdx.x >> 5];
+__global__ void __launch_bounds__(256, CEM_FILTER_MINB) k_filter(Dev d, int64_t s) {
     pdl_trigger();
-    pdl_wait();
+    pdl_wait();  // the list and the sigma records come from stage C / AB
     const int n = *(volatile int32_t *)&d.ctr[3];
-    const int nw = (int)(gridDim.x * (blockDim.x >> 5));
     const double4 *u = d.ubuf[(s + 1) & 1];
     const int lane = threadIdx.x & 31;
-    // entries per warp round: the list spread evenly over the grid's warps (short lists: one tet
-    // per warp, as in k_crit), at most one per lane
-    const int chunk = min(32, max(1, (n + nw - 1) / nw));
-    for (int base = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * chunk; base < n; base += nw * chunk) {
-        const int i = base + lane;
-        int64_t e = 0;
+    const int stride = (int)(gridDim.x * blockDim.x);
+    for (int i0 = (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); i0 < n; i0 += stride) {  // warp-uniform
+        const int i = i0 + lane;
+        int32_t e = 0;
         bool need = false;
-        if (lane < chunk && i < n) {
+        if (i < n) {
             e = d.crit_list[i];
             need = crit_refined_need(d.self, e, u, ldro(d.gc + e));
         }
-        const unsigned m = __ballot_sync(0xffffffffu, need);
-        if (need) wb.ids[__popc(m & ((1u << lane) - 1u))] = e;
-        __syncwarp();
-        const int ns = __popc(m);
-        for (int b0 = 0; b0 < ns; b0 += kCB) {
-            const int cnt = min(kCB, ns - b0);
-            if (lane < 4 * cnt) {  // (j, a): node a of tet j
-                const int j = lane >> 2, a = lane & 3;
-                const int4 t = __ldg(&d.conn[wb.ids[b0 + j]]);
-                const int nd = a == 0 ? t.x : (a == 1 ? t.y : (a == 2 ? t.z : t.w));
-                const double4 x = ldro4(&d.X[nd]);
-                const double4 uu = ldcg256(&u[nd]);
-                CritScratch &w = wb.t[j];
-                w.X[a][0] = x.x;
-                w.X[a][1] = x.y;
-                w.X[a][2] = x.z;
-                w.U[a][0] = uu.x;
-                w.U[a][1] = uu.y;
-                w.U[a][2] = uu.z;
-            }
-            __syncwarp();
-            if (lane < 6 * cnt) {  // (j, l): edge l of tet j
-                const int j = lane / 6, l = lane - 6 * j;
-                CritScratch &w = wb.t[j];
-                const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
-                                 w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
-                const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
-                                 w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
-                const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
-                w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
-                double s6[6];
-                load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + wb.ids[b0 + j]), s6);
-                Eig eg;
-                principal(s6, eg);
-                w.eg[l] = eg;
-            }
-            __syncwarp();
-            for (int q = lane; q < 24 * cnt; q += 32) {  // (j, k): candidate k of tet j
-                const int j = q / 24, k = q - 24 * j;
-                double G, A;
-                candidate(wb.t[j], k, G, A);
-                wb.G[j][k] = G;
-                wb.A[j][k] = A;
-            }
-            __syncwarp();
-            if (lane < cnt) {
-                const int j = lane;
-                const int64_t te = wb.ids[b0 + j];
-                double Gb = 0.0, Ab = 0.0;
-                int kb = -1;
-                for (int k = 0; k < 24; ++k) {
-                    const double G = wb.G[j][k], A = wb.A[j][k];
-                    if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
-                        Gb = G;
-                        kb = k;
-                        Ab = A;
-                    }
-                }
-                if (Gb > ldro(d.gc + te))
-                    split_tet(d, te, __ldg(&d.conn[te]), Gb, kb, Ab, s + 1, (int32_t)(s + 1), (__ldg(d.tflag + te) & 2) != 0);
-            }
-            __syncwarp();  // the scratch is reused by the next batch
+        const unsigned mm = __ballot_sync(0xffffffffu, need);
+        if (mm) {
+            const int lead = __ffs(mm) - 1;
+            int base = 0;
+            if (lane == lead) base = atomicAdd(&d.ctr[8], __popc(mm));
+            base = __shfl_sync(0xffffffffu, base, lead);
+            if (need) d.crit_list[d.E + base + __popc(mm & ((1u << lane) - 1u))] = e;
         }
+    }
+}
+__global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_eval(Dev d, int64_t s) {
+    extern __shared__ __align__(16) unsigned char crit_smem[];
+    CritBatch &wb = reinterpret_cast<CritBatch *>(crit_smem)[threadIdx.x >> 5];
+    pdl_trigger();
+    pdl_wait();  // the survivors come from k_filter
+    const int ns = *(volatile int32_t *)&d.ctr[8];
+    const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+    const double4 *u = d.ubuf[(s + 1) & 1];
+    const int lane = threadIdx.x & 31;
+    const int32_t *ids = d.crit_list + d.E;
+    for (int b0 = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kCB; b0 < ns; b0 += nw * kCB) {
+        const int cnt = min(kCB, ns - b0);
+        if (lane < 4 * cnt) {  // (j, a): node a of tet j
+            const int j = lane >> 2, a = lane & 3;
+            const int4 t = __ldg(&d.conn[ids[b0 + j]]);
+            const int nd = a == 0 ? t.x : (a == 1 ? t.y : (a == 2 ? t.z : t.w));
+            const double4 x = ldro4(&d.X[nd]);
+            const double4 uu = ldcg256(&u[nd]);
+            CritScratch &w = wb.t[j];
+            w.X[a][0] = x.x;
+            w.X[a][1] = x.y;
+            w.X[a][2] = x.z;
+            w.U[a][0] = uu.x;
+            w.U[a][1] = uu.y;
+            w.U[a][2] = uu.z;
+        }
+        __syncwarp();
+        if (lane < 6 * cnt) {  // (j, l): edge l of tet j
+            const int j = lane / 6, l = lane - 6 * j;
+            CritScratch &w = wb.t[j];
+            const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
+                             w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
+            const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
+                             w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
+            const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+            w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
+            double s6[6];
+            load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + ids[b0 + j]), s6);
+            Eig eg;
+            principal(s6, eg);
+            w.eg[l] = eg;
+        }
+        __syncwarp();
+        for (int q = lane; q < 24 * cnt; q += 32) {  // (j, k): candidate k of tet j
+            const int j = q / 24, k = q - 24 * j;
+            double G, A;
+            candidate(wb.t[j], k, G, A);
+            wb.G[j][k] = G;
+            wb.A[j][k] = A;
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            const int j = lane;
+            const int64_t te = ids[b0 + j];
+            double Gb = 0.0, Ab = 0.0;
+            int kb = -1;
+            for (int k = 0; k < 24; ++k) {
+                const double G = wb.G[j][k], A = wb.A[j][k];
+                if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
+                    Gb = G;
+                    kb = k;
+                    Ab = A;
+                }
+            }
+            if (Gb > ldro(d.gc + te))
+                split_tet(d, te, __ldg(&d.conn[te]), Gb, kb, Ab, s + 1, (int32_t)(s + 1), (__ldg(d.tflag + te) & 2) != 0);
+        }
+        __syncwarp();  // the scratch is reused by the next batch
     }
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
@@ -1494,7 +1512,7 @@ void set_smem_limits(int smem_bytes) {
     cudaFuncSetAttribute(k_energy_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    cudaFuncSetAttribute(k_critb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crit_smem_bytes());
+    cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crit_smem_bytes());
 }
 
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st) {
@@ -1524,24 +1542,32 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
         launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
         launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
         if (crit) {
-            if (heavy) launch_pdl(k_critb, (unsigned)CEM_CRITB_GRID, (unsigned)CEM_CRIT_THREADS, crit_smem_bytes(), st, d, s);
-            else launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
+            if (heavy) {
+                launch_pdl(k_filter, (unsigned)CEM_FILTER_GRID, 256u, (size_t)0, st, d, s);
+                launch_pdl(k_eval, (unsigned)CEM_CRITB_GRID, (unsigned)CEM_CRIT_THREADS, crit_smem_bytes(), st, d, s);
+            } else {
+                launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
+            }
         }
         launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
-        return crit ? 4 : 3;
+        return crit ? (heavy ? 5 : 4) : 3;
     }
     cudaEventRecord(ev[0], st);
     k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
     cudaEventRecord(ev[1], st);
     k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
     if (crit) {  // timed with stage C
-        if (heavy) k_critb<<<CEM_CRITB_GRID, CEM_CRIT_THREADS, crit_smem_bytes(), st>>>(d, s);
-        else k_crit<<<gcrit, 256, 0, st>>>(d, s);
+        if (heavy) {
+            k_filter<<<CEM_FILTER_GRID, 256, 0, st>>>(d, s);
+            k_eval<<<CEM_CRITB_GRID, CEM_CRIT_THREADS, crit_smem_bytes(), st>>>(d, s);
+        } else {
+            k_crit<<<gcrit, 256, 0, st>>>(d, s);
+        }
     }
     cudaEventRecord(ev[2], st);
     k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     cudaEventRecord(ev[3], st);
-    return crit ? 4 : 3;
+    return crit ? (heavy ? 5 : 4) : 3;
 }
 
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st) {
