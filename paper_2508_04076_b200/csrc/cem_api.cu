@@ -43,7 +43,7 @@ struct cem_ctx {
     std::vector<void *> dist_allocs;
     P2P p2p;                      // P2P halo (multi-GPU), see cem_dist.h
     volatile int32_t *crit_seen = nullptr;  // mapped: criterion-list length of a recent step
-    int critb_min = 4096;         // lists at least this long use k_filter + k_eval (env CEM_CRITB_MIN at init)
+    int critb_min = 1024;         // lists at least this long use k_filter + k_eval (env CEM_CRITB_MIN at init)
     double *epart = nullptr;      // energy-ledger partials (device)
     int64_t n_epart_edges = 0, n_epart_nodes = 0;
 };
