@@ -28,26 +28,38 @@ namespace {
 #ifndef CEM_BANK_SWAP
 #define CEM_BANK_SWAP 0  // swap passes after the greedy colouring (1: -0.3 us/step, +45 ms host time)
 #endif
-void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_t> &gitem, std::vector<int32_t> &row) {
+// reusable per-thread buffers of bank_rows (the plan calls it once per block)
+struct BankScratch {
+    std::vector<int32_t> moff, mem, f, cnt, col, cap, order, goff, gitem, row;
+    std::vector<std::vector<int32_t>> byc;
+};
+
+void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_t> &gitem, std::vector<int32_t> &row,
+               BankScratch &w) {
     row.assign(n, 0);
     if (n <= 16) {
         std::iota(row.begin(), row.end(), 0);
         return;
     }
     const int ng = (int)goff.size() - 1;
-    std::vector<int32_t> moff(n + 1, 0), mem;
+    std::vector<int32_t> &moff = w.moff, &mem = w.mem;
+    moff.assign(n + 1, 0);
     for (int g = 0; g < ng; ++g)
         for (int32_t i = goff[g]; i < goff[g + 1]; ++i) moff[gitem[i] + 1]++;
     for (int i = 0; i < n; ++i) moff[i + 1] += moff[i];
     mem.resize(moff[n]);
     {
-        std::vector<int32_t> f(moff.begin(), moff.end() - 1);
+        std::vector<int32_t> &f = w.f;
+        f.assign(moff.begin(), moff.end() - 1);
         for (int g = 0; g < ng; ++g)
             for (int32_t i = goff[g]; i < goff[g + 1]; ++i) mem[f[gitem[i]]++] = g;
     }
-    std::vector<int32_t> cnt((size_t)ng * 16, 0), col(n, -1), cap(16);
+    std::vector<int32_t> &cnt = w.cnt, &col = w.col, &cap = w.cap, &order = w.order;
+    cnt.assign((size_t)ng * 16, 0);
+    col.assign(n, -1);
+    cap.assign(16, 0);
     for (int k = 0; k < 16; ++k) cap[k] = n / 16 + (k < n % 16 ? 1 : 0);
-    std::vector<int32_t> order(n);
+    order.resize(n);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return moff[a + 1] - moff[a] > moff[b + 1] - moff[b]; });
@@ -66,7 +78,9 @@ void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_
         for (int32_t j = moff[it]; j < moff[it + 1]; ++j) cnt[(size_t)mem[j] * 16 + best]++;
     }
     // swap pass: move a to its best colour k, b (colour k) to a's colour, if the sum of squares drops
-    std::vector<std::vector<int32_t>> byc(16);
+    std::vector<std::vector<int32_t>> &byc = w.byc;
+    byc.resize(16);
+    for (auto &v : byc) v.clear();
     for (int i = 0; i < n; ++i) byc[col[i]].push_back(i);
     auto move_delta = [&](int it, int from, int to) {  // change of sum cnt^2 when `it` moves
         long dd = 0;
@@ -406,17 +420,21 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             for (int64_t s = 0; s < S; ++s) wmax = std::max(wmax, p.edge_off[s + 1] - p.edge_off[s]);
             wmax = std::min(wmax, 8);
             p.trow.assign(p.tl.size(), 0);
-#pragma omp parallel for schedule(dynamic, 16)
-            for (int b = 0; b < nbs; ++b) {
-                std::vector<int32_t> goff, gitem, row;
-                const int64_t s0 = (int64_t)b * blk_ab, s1 = std::min<int64_t>(S, s0 + blk_ab);
-                const int nt = p.tl_off[b + 1] - p.tl_off[b];
-                half_warp_groups(incw.data(), s0, s1, 8, wmax, goff, gitem, 0xFFFF);
-                bank_rows(nt, goff, gitem, row);
-                // the list keeps ascending tet order (thread i gathers entry i: coalesced); entry i
-                // writes its tau into shared-memory row trow[i]
-                for (int i = 0; i < nt; ++i) p.trow[p.tl_off[b] + i] = (uint16_t)row[i];
-                for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j) p.inc_local[j] = (uint16_t)row[p.inc_local[j]];
+#pragma omp parallel
+            {
+                BankScratch w;
+                std::vector<int32_t> &goff = w.goff, &gitem = w.gitem, &row = w.row;
+#pragma omp for schedule(dynamic, 16)
+                for (int b = 0; b < nbs; ++b) {
+                    const int64_t s0 = (int64_t)b * blk_ab, s1 = std::min<int64_t>(S, s0 + blk_ab);
+                    const int nt = p.tl_off[b + 1] - p.tl_off[b];
+                    half_warp_groups(incw.data(), s0, s1, 8, wmax, goff, gitem, 0xFFFF);
+                    bank_rows(nt, goff, gitem, row, w);
+                    // the list keeps ascending tet order (thread i gathers entry i: coalesced); entry i
+                    // writes its tau into shared-memory row trow[i]
+                    for (int i = 0; i < nt; ++i) p.trow[p.tl_off[b] + i] = (uint16_t)row[i];
+                    for (int32_t j = p.edge_off[s0]; j < p.edge_off[s1]; ++j) p.inc_local[j] = (uint16_t)row[p.inc_local[j]];
+                }
             }
         }
         clk.mark("plan: bank order (tets)");
@@ -444,30 +462,33 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         // bank-aware order of the staged node lists: AB (lanes = tet-list rows, column a) and
         // C's early-out (lanes = tets, column a); C's edge lists (lanes = tets, column l)
         p.nrow.assign(p.nlb.size(), 0);
-#pragma omp parallel for schedule(dynamic, 16)
-        for (int b = 0; b < nbs; ++b) {
-            std::vector<int32_t> goff, gitem, row;
-            const int32_t t0 = p.tl_off[b];
-            const int nt = p.tl_off[b + 1] - t0, nn = p.nlb_off[b + 1] - p.nlb_off[b];
-            half_warp_groups(p.tconn.data() + 4 * (int64_t)t0, 0, nt, 4, 4, goff, gitem);
-            bank_rows(nn, goff, gitem, row);
-            for (int i = 0; i < nn; ++i) p.nrow[p.nlb_off[b] + i] = (uint16_t)row[i];  // staging row of entry i
-            for (int64_t i = 4 * (int64_t)t0; i < 4 * (int64_t)(t0 + nt); ++i) p.tconn[i] = (uint16_t)row[p.tconn[i]];
-        }
-#pragma omp parallel for schedule(dynamic, 16)
-        for (int b = 0; b < nbt; ++b) {
-            std::vector<int32_t> goff, gitem, row;
-            const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
-            const int ne = p.el_off[b + 1] - p.el_off[b], nn = p.nl_off[b + 1] - p.nl_off[b];
-            half_warp_groups(p.ledge.data(), e0, e1, 8, 6, goff, gitem);
-            bank_rows(ne, goff, gitem, row);
-            permute_rows(p.el.data() + p.el_off[b], ne, row);
-            for (int64_t e = e0; e < e1; ++e)
-                for (int l = 0; l < 6; ++l) p.ledge[8 * e + l] = (uint16_t)row[p.ledge[8 * e + l]];
-            half_warp_groups(p.lconn.data(), e0, e1, 4, 4, goff, gitem);
-            bank_rows(nn, goff, gitem, row);
-            permute_rows(p.nl.data() + p.nl_off[b], nn, row);
-            for (int64_t i = 4 * e0; i < 4 * e1; ++i) p.lconn[i] = (uint16_t)row[p.lconn[i]];
+#pragma omp parallel
+        {
+            BankScratch w;
+            std::vector<int32_t> &goff = w.goff, &gitem = w.gitem, &row = w.row;
+#pragma omp for schedule(dynamic, 16) nowait
+            for (int b = 0; b < nbs; ++b) {
+                const int32_t t0 = p.tl_off[b];
+                const int nt = p.tl_off[b + 1] - t0, nn = p.nlb_off[b + 1] - p.nlb_off[b];
+                half_warp_groups(p.tconn.data() + 4 * (int64_t)t0, 0, nt, 4, 4, goff, gitem);
+                bank_rows(nn, goff, gitem, row, w);
+                for (int i = 0; i < nn; ++i) p.nrow[p.nlb_off[b] + i] = (uint16_t)row[i];  // staging row of entry i
+                for (int64_t i = 4 * (int64_t)t0; i < 4 * (int64_t)(t0 + nt); ++i) p.tconn[i] = (uint16_t)row[p.tconn[i]];
+            }
+#pragma omp for schedule(dynamic, 16)
+            for (int b = 0; b < nbt; ++b) {
+                const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
+                const int ne = p.el_off[b + 1] - p.el_off[b], nn = p.nl_off[b + 1] - p.nl_off[b];
+                half_warp_groups(p.ledge.data(), e0, e1, 8, 6, goff, gitem);
+                bank_rows(ne, goff, gitem, row, w);
+                permute_rows(p.el.data() + p.el_off[b], ne, row);
+                for (int64_t e = e0; e < e1; ++e)
+                    for (int l = 0; l < 6; ++l) p.ledge[8 * e + l] = (uint16_t)row[p.ledge[8 * e + l]];
+                half_warp_groups(p.lconn.data(), e0, e1, 4, 4, goff, gitem);
+                bank_rows(nn, goff, gitem, row, w);
+                permute_rows(p.nl.data() + p.nl_off[b], nn, row);
+                for (int64_t i = 4 * e0; i < 4 * e1; ++i) p.lconn[i] = (uint16_t)row[p.lconn[i]];
+            }
         }
         clk.mark("plan: bank order (nodes, edges)");
     }
