@@ -890,6 +890,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         return fail(CEM_ECUDA);
     }
     build_plan(ctx->h, block_size(), ctx->p, tflag_local.empty() ? nullptr : tflag_local.data());
+    PhaseClock clk;
     const int smem = smem_bytes_for(ctx->p);
     if (smem > 227 * 1024) {
         ctx->err = "a block's gather list exceeds shared memory (" + std::to_string(smem) + " bytes)";
@@ -905,6 +906,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         const double slack = ev ? atof(ev) : 3.0;
         build_schedule(ctx->p, (int)(slack * ctx->grid));
     }
+    clk.mark("init: schedule");
     if (!ctx->stream) {  // graphs / persistent launches never use the legacy default stream
         if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
             ctx->err = "cudaStreamCreate failed";
@@ -936,6 +938,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         ctx->own_ws = true;
         ctx->ws_bytes = o.total;
     }
+    clk.mark("init: workspace");
     bind_views(ctx, o);
     {
         // the criterion kernel is chosen per step on the host from the list length of a recent
@@ -954,6 +957,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     }
     st = upload(ctx, o);
     if (st) return fail(st);
+    clk.mark("init: upload");
     if (ctx->dist) {
         st = setup_exchange(ctx);
         if (st) return fail(st);
