@@ -313,3 +313,22 @@ def test_randomized_problems(seed):
                         vbc=vbc)
     sim, orc = run_pair(p, 120, 1, chunks=2)
     assert_parity(sim, orc, p)
+
+
+def test_full_size_cracking_phase_kernel_choice(monkeypatch):
+    """BASELINE configs[1] at full size into its cracking phase (~60k listed tets per step by
+    step 3000): the long-list kernels on every step and the one-warp-per-tet kernel on every
+    step give the same bits (the oracle parity of both is tested at small sizes above)."""
+    cem = _gpu()
+    p = ci.config(1)
+    out = []
+    for m in ("0", "1000000000"):
+        monkeypatch.setenv("CEM_CRITB_MIN", m)
+        sim = cem.Simulation.from_problem(p)
+        sim.step(3000, 1)
+        out.append(sim.state())
+        sim.close()
+    a, b = out
+    assert a.rec_elem.size > 10000
+    for k in ("u", "v", "a", "mass", "tet_state", "rec_elem", "rec_step", "rec_cand", "rec_G", "rec_area"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
