@@ -11,6 +11,8 @@
 #include <cmath>
 #include <numeric>
 
+#include <omp.h>
+
 #include "cem_internal.h"
 
 namespace cem {
@@ -215,10 +217,33 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         }
         key[e] = (int64_t)std::floor((cen[3 * e + ax] - lo[ax]) / (kSlab * hb));
     }
+    // tets by slab key, ascending id inside a slab (a stable counting sort, parallel)
     p.tet_new2old.resize(E);
-    std::iota(p.tet_new2old.begin(), p.tet_new2old.end(), 0);
-    std::stable_sort(p.tet_new2old.begin(), p.tet_new2old.end(),
-                     [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+    {
+        int64_t kmax = 0;
+        for (int64_t e = 0; e < E; ++e) kmax = std::max(kmax, key[e]);
+        const int nk = (int)kmax + 1;
+        const int nth = omp_get_max_threads();
+        std::vector<int64_t> cnt((size_t)nth * nk + 1, 0);  // [thread][key] -> start
+#pragma omp parallel num_threads(nth)
+        {
+            const int t = omp_get_thread_num();
+            const int64_t e0 = E * t / nth, e1 = E * (t + 1) / nth;
+            for (int64_t e = e0; e < e1; ++e) cnt[(size_t)t * nk + key[e]]++;
+#pragma omp barrier
+#pragma omp single
+            {
+                int64_t acc = 0;
+                for (int k = 0; k < nk; ++k)
+                    for (int tt = 0; tt < nth; ++tt) {
+                        const int64_t c = cnt[(size_t)tt * nk + k];
+                        cnt[(size_t)tt * nk + k] = acc;
+                        acc += c;
+                    }
+            }
+            for (int64_t e = e0; e < e1; ++e) p.tet_new2old[cnt[(size_t)t * nk + key[e]]++] = (int32_t)e;
+        }
+    }
     {
         const int64_t leaf = std::max(1, blk / 2);
         std::vector<int64_t> slab0;  // slab boundaries in the key-sorted order
@@ -255,38 +280,73 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             }
         }
     }
-    p.tet_old2new.assign(E, -1);
-    for (int64_t e = 0; e < E; ++e) p.tet_old2new[p.tet_new2old[e]] = (int32_t)e;
     clk.mark("plan: tet order");
-    // nodes and edges by first appearance
-    p.node_old2new.assign(N, -1);
-    p.node_new2old.clear();
-    p.node_new2old.reserve(N);
+    // nodes and edges by first appearance in the tet storage order: position of an entity =
+    // min over its incidences of (new tet index, local index); entities sorted by it (a
+    // compaction over the positions), entities referenced by no tet last in original order
+    p.tet_old2new.assign(E, -1);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e) p.tet_old2new[p.tet_new2old[e]] = (int32_t)e;
     std::vector<int32_t> edge_old2new(S, -1);
-    p.edge_new2old.clear();
-    p.edge_new2old.reserve(S);
-    for (int64_t en = 0; en < E; ++en) {
-        const int64_t eo = p.tet_new2old[en];
-        for (int a = 0; a < 4; ++a) {
-            int32_t k = h.tet[4 * eo + a];
-            if (p.node_old2new[k] < 0) {
-                p.node_old2new[k] = (int32_t)p.node_new2old.size();
-                p.node_new2old.push_back(k);
+    auto number = [&](int64_t n, int per, auto first_pos, std::vector<int32_t> &old2new, std::vector<int32_t> &new2old) {
+        std::vector<int32_t> at((size_t)per * E, -1);  // position -> entity
+        std::vector<uint8_t> unused(n, 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < n; ++k) {
+            const int64_t fp = first_pos(k);
+            if (fp >= 0) at[fp] = (int32_t)k;
+            else unused[k] = 1;
+        }
+        const int nth = omp_get_max_threads();
+        const int64_t P = (int64_t)per * E;
+        std::vector<int64_t> base(nth + 1, 0);
+        new2old.resize(n);
+        old2new.assign(n, -1);
+#pragma omp parallel num_threads(nth)
+        {
+            const int t = omp_get_thread_num();
+            const int64_t i0 = P * t / nth, i1 = P * (t + 1) / nth;
+            int64_t c = 0;
+            for (int64_t i = i0; i < i1; ++i) c += at[i] >= 0;
+            base[t + 1] = c;
+#pragma omp barrier
+#pragma omp single
+            for (int tt = 0; tt < nth; ++tt) base[tt + 1] += base[tt];
+            int64_t j = base[t];
+            for (int64_t i = i0; i < i1; ++i)
+                if (at[i] >= 0) {
+                    new2old[j] = at[i];
+                    old2new[at[i]] = (int32_t)j;
+                    ++j;
+                }
+        }
+        int64_t j = base[nth];
+        for (int64_t k = 0; k < n; ++k)
+            if (unused[k]) {
+                new2old[j] = (int32_t)k;
+                old2new[k] = (int32_t)j++;
             }
+    };
+    number(N, 4, [&](int64_t k) -> int64_t {
+        int64_t best = -1;
+        for (int32_t i = h.node_off[k]; i < h.node_off[k + 1]; ++i) {
+            const int32_t ent = h.node_ent[i];
+            const int64_t pos = 4 * (int64_t)p.tet_old2new[ent >> 2] + (ent & 3);
+            if (best < 0 || pos < best) best = pos;
         }
-        for (int l = 0; l < 6; ++l) {
-            int32_t s = h.elem_edge[6 * eo + l];
-            if (edge_old2new[s] < 0) {
-                edge_old2new[s] = (int32_t)p.edge_new2old.size();
-                p.edge_new2old.push_back(s);
-            }
+        return best;
+    }, p.node_old2new, p.node_new2old);
+    number(S, 6, [&](int64_t s) -> int64_t {
+        int64_t best = -1;
+        for (int32_t i = h.edge_off[s]; i < h.edge_off[s + 1]; ++i) {
+            const int32_t eo = h.edge_inc[i];
+            int l = 0;
+            while (h.elem_edge[6 * (int64_t)eo + l] != (int32_t)s) ++l;
+            const int64_t pos = 6 * (int64_t)p.tet_old2new[eo] + l;
+            if (best < 0 || pos < best) best = pos;
         }
-    }
-    for (int64_t k = 0; k < N; ++k)  // nodes referenced by no tet go last
-        if (p.node_old2new[k] < 0) {
-            p.node_old2new[k] = (int32_t)p.node_new2old.size();
-            p.node_new2old.push_back((int32_t)k);
-        }
+        return best;
+    }, edge_old2new, p.edge_new2old);
     clk.mark("plan: node/edge order");
     // ---------------------------------------------------------------- storage-order tables
     p.conn.resize(4 * E);
