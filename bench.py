@@ -331,6 +331,7 @@ def main():
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         sim2 = cem.Simulation.from_problem(prob, device=local)
+        ta = time.perf_counter()
         sim2.step(args.steps, crack_every)
         s2 = sim2.state(records=True)
         t1 = time.perf_counter()
@@ -339,6 +340,7 @@ def main():
         d2h = 3 * s2.u.nbytes + s2.tet_state.nbytes + s2.mass.nbytes
         line["e2e"] = {"value": E * args.steps / (t1 - t0), "unit": UNIT,
                        "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                       "init_s": ta - t0, "steps_and_readback_s": t1 - ta,
                        "what": "cem_init_mesh from host arrays (host preprocessing + H2D) + K steps + "
                                "cem_get_state(CEM_HOST)"}
         sim2.close()

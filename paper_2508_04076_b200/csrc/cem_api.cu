@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -269,6 +270,58 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     ctx->n_epart_nodes = (h.N + 255) / 256;
 }
 
+// Host -> device copies of the plan tables through two pinned staging halves (allocated once per
+// process): the host copies chunk i+1 (OpenMP) while the DMA engine moves chunk i, instead of the
+// driver's synchronous pageable staging.  Small copies go straight through.
+struct Stager {
+    static constexpr size_t kHalf = 16u << 20;
+    std::mutex mu;
+    char *buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int cur = 0;
+    bool tried = false;
+    bool ready() {
+        if (!tried) {
+            tried = true;
+            for (int i = 0; i < 2; ++i)
+                if (cudaHostAlloc(reinterpret_cast<void **>(&buf[i]), kHalf, cudaHostAllocPortable) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
+                    buf[0] = buf[1] = nullptr;
+                    cudaGetLastError();
+                    return false;
+                }
+        }
+        return buf[0] && buf[1];
+    }
+    cudaError_t put(char *dst, const void *src, size_t bytes, cudaStream_t st) {
+        if (bytes < (256u << 10) || !ready()) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+        const char *s = static_cast<const char *>(src);
+        for (size_t done = 0; done < bytes;) {
+            const size_t n = std::min(kHalf, bytes - done);
+            cudaError_t e = cudaEventSynchronize(ev[cur]);  // the half's previous DMA has finished
+            if (e != cudaSuccess) return e;
+            char *d = buf[cur];
+            const int64_t np = (int64_t)((n + (1u << 20) - 1) >> 20);
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < np; ++i) {
+                const size_t a = (size_t)i << 20, m = std::min<size_t>(1u << 20, n - a);
+                std::memcpy(d + a, s + done + a, m);
+            }
+            e = cudaMemcpyAsync(dst + done, d, n, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return e;
+            e = cudaEventRecord(ev[cur], st);
+            if (e != cudaSuccess) return e;
+            cur ^= 1;
+            done += n;
+        }
+        return cudaSuccess;
+    }
+};
+Stager &stager() {
+    static Stager *g = new Stager();  // process lifetime (pinned halves reused by every context)
+    return *g;
+}
+
 cem_status upload(cem_ctx *ctx, const Offs &o) {
     const HostMesh &h = ctx->h;
     const Plan &p = ctx->p;
@@ -315,8 +368,10 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
         u1[kn] = make_double4(uu[0], uu[1], uu[2], 0.0);
     }
     std::vector<int32_t> node_orig(p.node_new2old.begin(), p.node_new2old.end());
+    Stager &sg = stager();
+    std::lock_guard<std::mutex> lock(sg.mu);
     auto put = [&](size_t off, const void *src, size_t bytes) -> cudaError_t {
-        return cudaMemcpyAsync(at<char>(b, off), src, bytes, cudaMemcpyHostToDevice, st);
+        return sg.put(at<char>(b, off), src, bytes, st);
     };
     CUDA_TRY(put(o.conn, p.conn.data(), sizeof(int32_t) * 4 * E));
     CUDA_TRY(put(o.geoT, p.geoT.data(), sizeof(double) * p.geoT.size()));
