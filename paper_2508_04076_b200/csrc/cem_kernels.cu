@@ -113,15 +113,27 @@ __device__ __forceinline__ int64_t slot_tet(int32_t slot) { return ((int64_t)(sl
 #endif
 
 // lumped mass of node k from its active incidences in original order
+// (8 incidences at a time: their slot, state and volume loads are issued together, three round
+// trips per batch instead of three per incidence; the sum stays sequential in ascending order)
 __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
     double acc = 0.0;
-    const int32_t *row = d.nodeE + k * d.wn;
-    for (int j = 0; j < d.wn; ++j) {
-        const int32_t sl = __ldg(row + j);
-        if (sl == d.zslot) break;
-        const int64_t e = slot_tet(sl);
-        if (!__ldcg(d.state + e)) continue;
-        acc = acc + (d.rho * geo_V(d, (uint32_t)e)) / 4.0;
+    const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + k * d.wn);  // wn is a multiple of 8
+    for (int j = 0; j < d.wn; j += 8) {
+        const int4 q0 = __ldg(row + (j >> 2)), q1 = __ldg(row + (j >> 2) + 1);
+        const int32_t sl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        uint8_t st[8];
+        double V[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const bool ok = sl[t] != d.zslot;
+            const int64_t e = ok ? slot_tet(sl[t]) : 0;
+            st[t] = ok ? __ldcg(d.state + e) : (uint8_t)0;
+            V[t] = ok ? geo_V(d, (uint32_t)e) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (st[t]) acc = acc + (d.rho * V[t]) / 4.0;
+        if (sl[7] == d.zslot) break;  // padding only at the row's end
     }
     return acc;
 }
@@ -188,12 +200,26 @@ __device__ __forceinline__ void zero_row(double *T, int tn, int i) {
 }
 // Vhat_s = sum of V_e over the edge's active incident tets in ascending original id (the
 // oracle's stage_edge sum); inactive tets are skipped (equivalently: add +0.0)
+// (8 incidences at a time: index, state and volume loads issued together -- three round trips
+// per batch instead of per incidence; the sum stays sequential in ascending order)
 __device__ __noinline__ double vhat_recompute(const Dev *__restrict__ dp, int64_t s) {
     const Dev &d = *dp;
     double acc = 0.0;
-    for (int32_t j = __ldg(d.e_off + s); j < __ldg(d.e_off + s + 1); ++j) {
-        const int32_t e = __ldg(d.e_inc + j);
-        if (__ldcg(d.state + e)) acc = acc + geo_V(d, (uint32_t)e);
+    const int32_t j0 = __ldg(d.e_off + s), j1 = __ldg(d.e_off + s + 1);
+    for (int32_t j = j0; j < j1; j += 8) {
+        int32_t e[8];
+        uint8_t st[8];
+        double V[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) e[t] = j + t < j1 ? __ldg(d.e_inc + j + t) : -1;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            st[t] = e[t] >= 0 ? __ldcg(d.state + e[t]) : (uint8_t)0;
+            V[t] = e[t] >= 0 ? geo_V(d, (uint32_t)e[t]) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (st[t]) acc = acc + V[t];
     }
     return acc;
 }
