@@ -117,6 +117,13 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         return CEM_EINVAL;
     }
     const int64_t N = m->n_nodes, E = m->n_tets;
+    // index ranges of the device layout: 32-bit element offsets of 12 E force-slot doubles
+    // (4 slots x 3 components per tet) and of the 6-E edge incidences (checked before any array
+    // is read)
+    if (E > ((int64_t)1 << 32) / 12 - 64 || N >= ((int64_t)1 << 31)) {
+        err = "mesh too large for one context (E must be < 357M tets; partition it over ranks)";
+        return CEM_EINVAL;
+    }
     h.N = N;
     h.E = E;
     h.X.assign(m->X, m->X + 3 * N);
@@ -129,12 +136,6 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
     }
     PhaseClock clk;
     // ---------------------------------------------------------------- validation
-    // index ranges of the device layout: 32-bit element offsets of 12 E force-slot doubles
-    // (4 slots x 3 components per tet) and of the 6-E edge incidences
-    if (E > ((int64_t)1 << 32) / 12 - 64 || N >= ((int64_t)1 << 31)) {
-        err = "mesh too large for one context (E must be < 357M tets; partition it over ranks)";
-        return CEM_EINVAL;
-    }
     for (int64_t e = 0; e < E; ++e) {
         const int32_t *t = m->tets + 4 * e;
         for (int a = 0; a < 4; ++a) {

@@ -83,3 +83,16 @@ def test_workspace_size_counts_edges():
     b = cem.workspace_size(p.X, p.tets)
     # at least the edge stress field (6 doubles per edge) and the element tables
     assert b > 2918 * 48 + 1920 * (16 * 8 + 24 + 48 + 96)
+
+
+def test_maximum_size_rejected_before_reading():
+    """Meshes beyond one context's 32-bit index ranges (E >= 2^32/12 - 64 tets or N >= 2^31
+    nodes) are rejected with CEM_EINVAL before any array is read (include/cem.h)."""
+    import ctypes as C
+    import paper_2508_04076_b200 as cem
+    X = np.zeros((4, 3)); T = np.array([[0, 1, 2, 3]], np.int32)
+    for n_nodes, n_tets in ((4, (1 << 32) // 12), (1 << 31, 1)):
+        mesh = cem.cem_mesh_in(n_nodes, X.ctypes.data_as(C.POINTER(C.c_double)), n_tets,
+                               T.ctypes.data_as(C.POINTER(C.c_int32)), None, None)
+        b = C.c_size_t()
+        assert cem._lib.cem_workspace_size(C.byref(mesh), None, C.byref(b)) == cem.CEM_EINVAL
