@@ -122,7 +122,7 @@ def test_loopback_randomized(seed):
 
 @pytest.mark.parametrize("P,p2p", [(2, False), (3, True)])
 def test_loopback_long_list_criterion_kernel(P, p2p, monkeypatch):
-    """Every step through the long-list criterion kernel (k_critb) on P ranks: owner-only
+    """Every step through the long-list criterion kernels (k_filter + k_eval) on P ranks: owner-only
     records, ghost splits delivered by the halo (copy or P2P), bitwise equal to the oracle."""
     monkeypatch.setenv("CEM_CRITB_MIN", "0")
     dist = _gpu()

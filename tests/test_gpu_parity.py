@@ -102,7 +102,7 @@ def test_weak_block_predamage():
 @pytest.mark.parametrize("critb_min", ["0", "300"])
 @pytest.mark.parametrize("case", ["cfg0", "plate", "ct", "predamage", "overflow"])
 def test_long_list_criterion_kernel(case, critb_min, monkeypatch):
-    """The long-list criterion kernel (k_critb: refined early-out per lane, then 5 tets per warp)
+    """The long-list criterion kernels (k_filter: refined early-out per listed tet; k_eval: 5 tets per warp)
     gives the oracle's bits: forced for every step (CEM_CRITB_MIN=0) and switched in mid-run by
     the list length (300)."""
     monkeypatch.setenv("CEM_CRITB_MIN", critb_min)
