@@ -649,9 +649,10 @@ cem_status p2p_alloc(cem_ctx *ctx) {
         ctx->dist_allocs.push_back(q.recv[par]);
         CUDA_TRY(cudaMemcpy(q.recv[par], ctx->xch.d_recvbuf, bytes, cudaMemcpyDeviceToDevice));
     }
-    CUDA_TRY(cudaMalloc(&q.flags, sizeof(int64_t) * std::max(1, ctx->nranks)));
+    CUDA_TRY(cudaMalloc(&q.flags, sizeof(int64_t) * (std::max(1, ctx->nranks) + 1)));
     ctx->dist_allocs.push_back(q.flags);
-    CUDA_TRY(cudaMemset(q.flags, 0, sizeof(int64_t) * std::max(1, ctx->nranks)));
+    CUDA_TRY(cudaMemset(q.flags, 0, sizeof(int64_t) * (std::max(1, ctx->nranks) + 1)));
+    q.timeout = q.flags + std::max(1, ctx->nranks);
     return CEM_OK;
 }
 
@@ -1207,7 +1208,14 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     const int64_t N = h.N, E = h.E;
     int32_t ctr[8];
     CUDA_TRY(cudaMemcpyAsync(ctr, ctx->d.ctr, sizeof ctr, cudaMemcpyDeviceToHost, st));
+    int64_t p2p_timeout = 0;
+    if (ctx->p2p.on && ctx->p2p.timeout)
+        CUDA_TRY(cudaMemcpyAsync(&p2p_timeout, ctx->p2p.timeout, sizeof p2p_timeout, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (p2p_timeout) {
+        ctx->err = "P2P halo: a peer stopped signalling (waited 60 s); the state is invalid";
+        return CEM_ENCCL;
+    }
     const int64_t nrec = ctr[0];
 #ifdef CEM_POLL_STATS
     fprintf(stderr, "[cem poll stats] polls AB %d C %d D %d, items that waited %d\n", ctr[4], ctr[5], ctr[6], ctr[7]);

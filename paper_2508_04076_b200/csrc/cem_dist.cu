@@ -61,13 +61,28 @@ __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
 
 // one warp: lane j signals peer j (after a system fence: the stage kernels' remote stores,
 // complete by stream order, are ordered before the flag), then waits for peer j's flag
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// (watchdog: a peer that stops signalling -- a dead rank -- ends the wait after 60 s with the
+// timeout word set, which cem_get_state reports, instead of hanging the GPU)
 __global__ void k_p2p_sync(int64_t *flags, int64_t *const *peer_flag, const int32_t *peer_rank, int np, int64_t target,
-                           int wait) {
+                           int wait, int64_t *timeout) {
     __threadfence_system();
     for (int j = threadIdx.x; j < np; j += blockDim.x) st_release_sys(peer_flag[j], target);
-    if (wait)
+    if (wait) {
+        const uint64_t t0 = globaltimer_ns();
         for (int j = threadIdx.x; j < np; j += blockDim.x)
-            while (ld_acquire_sys(flags + peer_rank[j]) < target) __nanosleep(100);
+            while (ld_acquire_sys(flags + peer_rank[j]) < target) {
+                __nanosleep(100);
+                if (globaltimer_ns() - t0 > 60000000000ull) {
+                    atomicExch(reinterpret_cast<unsigned long long *>(timeout), 1ull);
+                    break;
+                }
+            }
+    }
     __syncwarp();
     __threadfence_system();
 }
@@ -204,7 +219,7 @@ void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, const int32_
 }
 
 void p2p_sync(const P2P &q, int npeers, int64_t target, bool wait, cudaStream_t st) {
-    if (npeers) k_p2p_sync<<<1, 32, 0, st>>>(q.flags, q.d_peer_flag, q.d_peer_rank, npeers, target, wait ? 1 : 0);
+    if (npeers) k_p2p_sync<<<1, 32, 0, st>>>(q.flags, q.d_peer_flag, q.d_peer_rank, npeers, target, wait ? 1 : 0, q.timeout);
 }
 
 void p2p_push_nodes(const P2P &q, const double4 *u, int64_t N, int par, int npeers, cudaStream_t st) {

@@ -29,6 +29,7 @@ struct P2P {
     bool on = false;
     uint8_t *recv[2] = {nullptr, nullptr};  // this rank's receive buffers (layout of Exchange::recv_off)
     int64_t *flags = nullptr;               // [nranks] last step each peer has completed its stores for
+    int64_t *timeout = nullptr;             // = flags + nranks: set when a wait for a peer gave up
     std::vector<void *> opened;             // IPC-mapped peer allocations
     uint8_t **d_peer_recv = nullptr;        // [2][npeers] peer buffer + the offset of this rank's segment
     int64_t **d_peer_flag = nullptr;        // [npeers] &peer.flags[this rank]
