@@ -179,7 +179,11 @@ CEM_API cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *ma
 
 /* Enqueue nsteps explicit steps.  crack_every > 0: evaluate the crack criterion and run
  * the split pass after every crack_every-th step (criterion on u_{n+1} and the same
- * sigma(u_{n+1}) used for f_int, R16); 0 = pure elastodynamics. */
+ * sigma(u_{n+1}) used for f_int, R16); 0 = pure elastodynamics.
+ * Asynchronous on the context's stream.  The criterion kernels are chosen per step from the
+ * list length of a recent step (long lists, >= 1024 tets or env CEM_CRITB_MIN at init, use the
+ * filtered, batched kernels); the choice never changes results.  Multi-GPU contexts: a halo
+ * wait that exceeds 60 s (a dead peer) is reported by the next cem_get_state (CEM_ENCCL). */
 CEM_API cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every);
 
 /* Criterion + split pass on the current state (u_n, sigma(u_n)) without advancing time;
