@@ -288,11 +288,15 @@ def test_ragged_sizes(E_target):
     assert np.abs(g.u).max() > 0
 
 
+@pytest.mark.parametrize("critb_min", [None, "0"])
 @pytest.mark.parametrize("seed", range(8))
-def test_randomized_problems(seed):
+def test_randomized_problems(seed, critb_min, monkeypatch):
     """Seeded random problems: lattice size, jitter, material, traction direction, a random
     inactive set, random per-element Gc (some pre-damaged), an optional prescribed-velocity
-    patch -- 120 steps with the criterion every step, bitwise vs the oracle."""
+    patch -- 120 steps with the criterion every step, bitwise vs the oracle; with the default
+    criterion-kernel choice and with the long-list kernels forced on every step."""
+    if critb_min is not None:
+        monkeypatch.setenv("CEM_CRITB_MIN", critb_min)
     rng = np.random.default_rng(1000 + seed)
     cells = tuple(int(c) for c in rng.integers([4, 3, 2], [14, 9, 5]))
     dims = tuple(float(x) for x in rng.uniform(0.01, 0.05, 3))
