@@ -328,6 +328,20 @@ def random_tet_mesh(seed, n_cells=(2, 2, 1), jitter=0.2):
     return X, tets, ijk
 
 
+def fan_mesh(m=40, r=0.01, h=0.01, seed=0, jitter=0.2):
+    """m tets around one axis edge (0,0,-h)-(0,0,h) with a ring of m nodes near radius r: the axis
+    edge and its two end nodes have valence m (tests the ELL widths past 8/24).  Tet i =
+    (bottom, top, ring_i, ring_{i+1}), positively oriented for a counter-clockwise ring; seeded
+    jitter of the ring radii, angles (< half a sector) and heights breaks the symmetry."""
+    rng = np.random.default_rng(seed)
+    th = 2.0 * np.pi * (np.arange(m) + jitter * rng.uniform(-0.5, 0.5, m)) / m
+    rr = r * (1.0 + jitter * rng.uniform(-0.5, 0.5, m))
+    z = h * jitter * rng.uniform(-0.5, 0.5, m)
+    X = np.concatenate([[[0.0, 0.0, -h], [0.0, 0.0, h]], np.stack([rr * np.cos(th), rr * np.sin(th), z], 1)])
+    T = np.array([[0, 1, 2 + i, 2 + (i + 1) % m] for i in range(m)], np.int32)
+    return X, T
+
+
 def make_problem(X, tets, E=32e9, nu=0.2, rho=2450.0, Gc=3.0, tet_state=None, tet_gc=None,
                  tface=None, tface_t=None, vbc=None, dt=0.0, name="custom", steps=0):
     """Wrap raw arrays into a Problem (tests)."""

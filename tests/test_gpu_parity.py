@@ -252,6 +252,22 @@ def test_single_tet():
     assert_parity(sim, orc, p)
 
 
+@pytest.mark.parametrize("critb_min", [None, "0"])
+def test_high_valence_fan(critb_min, monkeypatch):
+    """40 tets around one edge: the edge's incidence row and its end nodes' force-slot rows are
+    40 long (several ELL chunks in stages AB and D, several batches in the mass recomputation),
+    ring nodes pulled radially with a velocity ramp, low Gc so tets split."""
+    if critb_min is not None:
+        monkeypatch.setenv("CEM_CRITB_MIN", critb_min)
+    X, T = ci.fan_mesh(40)
+    ring = np.arange(2, X.shape[0], dtype=np.int32)
+    v0 = 0.02 * X[ring] / np.linalg.norm(X[ring], axis=1)[:, None]   # splits spread over steps ~110-260
+    p = ci.make_problem(X, T, Gc=0.5, vbc=(ring, np.full(ring.size, 7, np.uint8), v0, 2e-6))
+    sim, orc = run_pair(p, 300, 1, chunks=3)
+    g = assert_parity(sim, orc, p)
+    assert g.rec_elem.size > 0
+
+
 def test_all_tets_inactive():
     """No active tet: no stiffness, every mass 0 -> every node frozen, u stays 0."""
     X, T, _ = ci.kuhn_lattice((3, 2, 2), (0.03, 0.02, 0.02), 1)
