@@ -388,12 +388,9 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     __syncthreads();
     double Ue = 0.0;  // energy mode: this thread's strain energy
     if (hs0) edge_sigma(d, s0, T, tn, nt, qe0, Vh0, epart, Ue);
-    for (int j = 1; j < CEM_AB_EPT; ++j) {
-        const int64_t s = sbase + (int64_t)j * nthr + tid;
-        if (s < send)
-            edge_sigma(d, s, T, tn, nt, __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we)),
-                       fetch_vhat(d, s, epart == nullptr), epart, Ue);
-    }
+    for (int64_t s = s0 + nthr; s < send; s += nthr)  // (CEM_AB_EPT > 1: more edges per thread)
+        edge_sigma(d, s, T, tn, nt, __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we)),
+                   fetch_vhat(d, s, epart == nullptr), epart, Ue);
     if (epart) {
         const double t = block_sum(Ue, sm);  // the planes are no longer read
         if (tid == 0) epart[b] = t;
