@@ -2,6 +2,8 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -90,12 +92,36 @@ cem_status global_cfl_dt(const cem_mesh_in *m, const cem_material *mat, double c
 // criterion, D: node update.
 enum Stage { ST_AB = 0, ST_C = 1, ST_D = 2, ST_COUNT = 3 };
 
+// host vector whose resize() leaves new elements uninitialised (default-init): the large plan tables
+// are written in full by parallel loops, so the serial zero-fill (and its page faults on one core)
+// is skipped -- first touch happens in those loops
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = DefaultInitAlloc<U>;
+    };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U> &) noexcept {}
+    template <class U>
+    void construct(U *p) noexcept {
+        ::new (static_cast<void *>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U *p, A &&...a) {
+        ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using hvec = std::vector<T, DefaultInitAlloc<T>>;
+
 struct Plan {
     std::vector<int32_t> tet_new2old, tet_old2new, node_new2old, node_old2new, edge_new2old;
     // storage-order arrays
-    std::vector<int32_t> conn;        // [E][4] new node ids (int4)
+    hvec<int32_t> conn;               // [E][4] new node ids (int4)
     std::vector<double> geoV, geoC;   // [E] V, V/6
-    std::vector<int32_t> eedge;       // [6][E] new edge ids
+    hvec<int32_t> eedge;              // [6][E] new edge ids
     std::vector<int32_t> edge_off, edge_inc;   // CSR over new edges, new tet ids, original order
     std::vector<int32_t> node_off, node_ent;   // CSR over new nodes, (new e << 2 | a), original order
     std::vector<uint8_t> state;
@@ -112,23 +138,23 @@ struct Plan {
     std::vector<int32_t> sched;       // [P]: stage << 28 | block
     // block gather lists (deduplicated producer records staged in shared memory)
     std::vector<int32_t> nl_off, nl;  // tet block -> sorted unique node ids
-    std::vector<uint16_t> lconn;      // [E][4] index of each tet node in its block's node list
+    hvec<uint16_t> lconn;             // [E][4] index of each tet node in its block's node list
     std::vector<int32_t> el_off, el;  // tet block -> sorted unique edge ids
-    std::vector<uint16_t> ledge;      // [E][8] index of each tet edge in its block's edge list (6 used)
+    hvec<uint16_t> ledge;             // [E][8] index of each tet edge in its block's edge list (6 used)
     std::vector<int32_t> tl_off, tl;  // edge block -> sorted unique incident tet ids
     std::vector<int32_t> nlb_off, nlb;  // edge block -> sorted unique nodes of its tet list
-    std::vector<uint16_t> tconn;      // [|tl|][4] staging row (in nlb) of each tet-list entry's nodes
+    hvec<uint16_t> tconn;             // [|tl|][4] staging row (in nlb) of each tet-list entry's nodes
     std::vector<uint16_t> trow;       // [|tl|] shared-memory row of each tet-list entry (bank-aware)
     std::vector<uint16_t> nrow;       // [|nlb|] shared-memory row of each node-list entry (bank-aware)
-    std::vector<uint16_t> inc_local;  // [6E] (CSR order of edge_inc) index into the edge block's tet list
+    hvec<uint16_t> inc_local;         // [6E] (CSR order of edge_inc) index into the edge block's tet list
     int max_nl = 0, max_el = 0, max_tl = 0, max_nlb = 0;
     // instruction-lean layouts
-    std::vector<double> geoT;         // geometry: [E][12] records or [E/32][11][32] tiles (CEM_GEO_AOS)
+    hvec<double> geoT;                // geometry: [E][12] records or [E/32][11][32] tiles (CEM_GEO_AOS)
     int we = 8;                       // ELL width of edge incidences (multiple of 8)
     int we_max = 8;                   // largest incidence count (loop bound)
-    std::vector<uint16_t> incE;       // [S][we] index into the edge block's tet list, 0xFFFF = none
+    hvec<uint16_t> incE;              // [S][we] index into the edge block's tet list, 0xFFFF = none
     int wn = 8;                       // ELL width of node incidences (multiple of 8)
-    std::vector<int32_t> nodeE;       // [N][wn] force slot of each incidence (original order), zslot = none
+    hvec<int32_t> nodeE;              // [N][wn] force slot of each incidence (original order), zslot = none
     int32_t zslot = 0;
 };
 

@@ -354,9 +354,9 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     p.geoC.resize(E);
     // geometry records written straight into the device layout (CEM_GEO_AOS)
 #if CEM_GEO_AOS
-    p.geoT.assign((size_t)E * 12, 0.0);  // per tet 12 doubles (96 B): V, V/6, gradN1..3 (x, y, z), 0
+    p.geoT.resize((size_t)E * 12);  // per tet 12 doubles (96 B): V, V/6, gradN1..3 (x, y, z), (pad)
 #else
-    p.geoT.assign((size_t)((E + 31) / 32) * 11 * 32, 0.0);  // [E/32][11][32] warp tiles
+    p.geoT.resize((size_t)((E + 31) / 32) * 11 * 32);  // [E/32][11][32] warp tiles (tail lanes unused)
 #endif
     p.eedge.resize(6 * E);
     p.state.resize(E);
@@ -428,8 +428,8 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
 #pragma omp parallel for schedule(static)
             for (int64_t b = 0; b < (int64_t)parts.size(); ++b) std::copy(parts[b].begin(), parts[b].end(), out.begin() + off[b]);
         };
-        p.lconn.assign(4 * E, 0);
-        p.ledge.assign(8 * E, 0);
+        p.lconn.resize(4 * E);  // (written in full below)
+        p.ledge.resize(8 * E);  // (6 of 8 written per tet; the rest is never read)
         {
             std::vector<std::vector<int32_t>> nlv(nbt), elv(nbt);
 #pragma omp parallel
@@ -452,7 +452,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
             concat(nlv, p.nl_off, p.nl, p.max_nl);
             concat(elv, p.el_off, p.el, p.max_el);
         }
-        p.inc_local.assign(p.edge_inc.size(), 0);
+        p.inc_local.resize(p.edge_inc.size());  // (written in full below)
         {
             std::vector<std::vector<int32_t>> tlv(nbs);
 #pragma omp parallel
@@ -499,7 +499,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         }
         clk.mark("plan: bank order (tets)");
         // nodes of each edge block's tet list (the fused AB stage recomputes tau from them)
-        p.tconn.assign(4 * p.tl.size(), 0);
+        p.tconn.resize(4 * p.tl.size());  // (written in full below)
         {
             std::vector<std::vector<int32_t>> nbv(nbs);
 #pragma omp parallel
@@ -558,17 +558,21 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
         for (int64_t s = 0; s < S; ++s) mx = std::max(mx, p.edge_off[s + 1] - p.edge_off[s]);
         p.we = (mx + 7) / 8 * 8;
         p.we_max = mx;
-        p.incE.assign((size_t)S * p.we, 0xFFFF);
+        p.incE.resize((size_t)S * p.we);
 #pragma omp parallel for schedule(static)
-        for (int64_t s = 0; s < S; ++s)
-            for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j) p.incE[(size_t)s * p.we + (j - p.edge_off[s])] = p.inc_local[j];
+        for (int64_t s = 0; s < S; ++s) {
+            const int32_t n = p.edge_off[s + 1] - p.edge_off[s];
+            for (int32_t j = 0; j < n; ++j) p.incE[(size_t)s * p.we + j] = p.inc_local[p.edge_off[s] + j];
+            for (int32_t j = n; j < p.we; ++j) p.incE[(size_t)s * p.we + j] = 0xFFFF;
+        }
         mx = 1;
         for (int64_t k = 0; k < N; ++k) mx = std::max(mx, p.node_off[k + 1] - p.node_off[k]);
         p.wn = (mx + 7) / 8 * 8;
         p.zslot = (int32_t)(((E + 31) / 32) * 128);  // first slot past the last tile: kept zero
-        p.nodeE.assign((size_t)N * p.wn, p.zslot);
+        p.nodeE.resize((size_t)N * p.wn);
 #pragma omp parallel for schedule(static)
-        for (int64_t k = 0; k < N; ++k)
+        for (int64_t k = 0; k < N; ++k) {
+            for (int32_t j = p.node_off[k + 1] - p.node_off[k]; j < p.wn; ++j) p.nodeE[(size_t)k * p.wn + j] = p.zslot;
             for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) {
                 const int64_t e = p.node_ent[j] >> 2, a = p.node_ent[j] & 3;
 #if CEM_FES == 3
@@ -577,6 +581,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
                 p.nodeE[(size_t)k * p.wn + (j - p.node_off[k])] = (int32_t)((((e >> 5) * 4 + a) << 5) + (e & 31));
 #endif
             }
+        }
     }
     clk.mark("plan: ELL tables");
     // ---------------------------------------------------------------- blocks and dependencies
