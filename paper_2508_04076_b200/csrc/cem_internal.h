@@ -54,6 +54,30 @@ struct PhaseClock {
     }
 };
 
+// host vector whose resize() leaves new elements uninitialised (default-init): the large plan tables
+// are written in full by parallel loops, so the serial zero-fill (and its page faults on one core)
+// is skipped -- first touch happens in those loops
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = DefaultInitAlloc<U>;
+    };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U> &) noexcept {}
+    template <class U>
+    void construct(U *p) noexcept {
+        ::new (static_cast<void *>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U *p, A &&...a) {
+        ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using hvec = std::vector<T, DefaultInitAlloc<T>>;
+
 // ---------------------------------------------------------------- host preprocessing
 // HostMesh holds the mesh in the caller's ("original") numbering (cem_mesh.cpp).
 struct HostMesh {
@@ -63,11 +87,11 @@ struct HostMesh {
     std::vector<uint8_t> state;       // [E]
     std::vector<double> gc;           // [E]
     std::vector<double> V;            // [E]
-    std::vector<double> grad;         // [E][4][3]
-    std::vector<int32_t> elem_edge;   // [E][6]
+    hvec<double> grad;                // [E][4][3]
+    hvec<int32_t> elem_edge;          // [E][6]
     std::vector<int32_t> edge_nodes;  // [S][2]
     std::vector<int32_t> edge_off;    // [S+1]
-    std::vector<int32_t> edge_inc;    // [6E] ascending tet id per edge
+    hvec<int32_t> edge_inc;           // [6E] ascending tet id per edge
     std::vector<int32_t> node_off;    // [N+1]
     std::vector<int32_t> node_ent;    // [4E] 4e+a, ascending e per node
     std::vector<double> mass;         // [N]
@@ -92,29 +116,6 @@ cem_status global_cfl_dt(const cem_mesh_in *m, const cem_material *mat, double c
 // criterion, D: node update.
 enum Stage { ST_AB = 0, ST_C = 1, ST_D = 2, ST_COUNT = 3 };
 
-// host vector whose resize() leaves new elements uninitialised (default-init): the large plan tables
-// are written in full by parallel loops, so the serial zero-fill (and its page faults on one core)
-// is skipped -- first touch happens in those loops
-template <class T>
-struct DefaultInitAlloc : std::allocator<T> {
-    template <class U>
-    struct rebind {
-        using other = DefaultInitAlloc<U>;
-    };
-    DefaultInitAlloc() = default;
-    template <class U>
-    DefaultInitAlloc(const DefaultInitAlloc<U> &) noexcept {}
-    template <class U>
-    void construct(U *p) noexcept {
-        ::new (static_cast<void *>(p)) U;
-    }
-    template <class U, class... A>
-    void construct(U *p, A &&...a) {
-        ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
-    }
-};
-template <class T>
-using hvec = std::vector<T, DefaultInitAlloc<T>>;
 
 struct Plan {
     std::vector<int32_t> tet_new2old, tet_old2new, node_new2old, node_old2new, edge_new2old;

@@ -168,7 +168,7 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
     // det = d1.(d2 x d3), V = det/6, inv = 1/det, gradN1 = (d2xd3) inv, gradN2 = (d3xd1) inv,
     // gradN3 = (d1xd2) inv, gradN0 = -((gradN1 + gradN2) + gradN3)
     h.V.assign(E, 0.0);
-    h.grad.assign(12 * E, 0.0);
+    h.grad.resize(12 * E);  // (written for every valid tet; an invalid one fails the init)
     int64_t bad_neg = -1, bad_deg = -1;
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < E; ++e) {
