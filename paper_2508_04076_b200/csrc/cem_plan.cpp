@@ -61,10 +61,17 @@ void bank_rows(int n, const std::vector<int32_t> &goff, const std::vector<int32_
     col.assign(n, -1);
     cap.assign(16, 0);
     for (int k = 0; k < 16; ++k) cap[k] = n / 16 + (k < n % 16 ? 1 : 0);
+    // items by degree, descending, ties in index order (a stable counting sort)
     order.resize(n);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return moff[a + 1] - moff[a] > moff[b + 1] - moff[b]; });
+    {
+        int dmax = 0;
+        for (int i = 0; i < n; ++i) dmax = std::max(dmax, moff[i + 1] - moff[i]);
+        std::vector<int32_t> &f = w.f;
+        f.assign(dmax + 2, 0);
+        for (int i = 0; i < n; ++i) f[dmax - (moff[i + 1] - moff[i]) + 1]++;
+        for (int k = 0; k <= dmax; ++k) f[k + 1] += f[k];
+        for (int i = 0; i < n; ++i) order[f[dmax - (moff[i + 1] - moff[i])]++] = i;
+    }
     for (int it : order) {
         int best = -1;
         long bc = 0;
@@ -151,10 +158,16 @@ void half_warp_groups(const T *tab, int64_t lo, int64_t hi, int stride, int widt
             const size_t st = gitem.size();
             for (int64_t i = h0; i < std::min<int64_t>(hi, h0 + 16); ++i) {
                 const int v = (int)tab[(int64_t)stride * i + l];
-                if (v != skip) gitem.push_back(v);
+                if (v == skip) continue;
+                // insertion into the group's sorted, duplicate-free run (<= 16 items)
+                size_t j = gitem.size();
+                bool dup = false;
+                while (j > st && gitem[j - 1] >= v) {
+                    if (gitem[j - 1] == v) dup = true;
+                    --j;
+                }
+                if (!dup) gitem.insert(gitem.begin() + j, v);
             }
-            std::sort(gitem.begin() + st, gitem.end());
-            gitem.erase(std::unique(gitem.begin() + st, gitem.end()), gitem.end());
             goff.push_back((int32_t)gitem.size());
         }
 }
@@ -162,7 +175,8 @@ void half_warp_groups(const T *tab, int64_t lo, int64_t hi, int stride, int widt
 // reorder list[off..off+n) so that item i moves to row[i]
 template <class T>
 void permute_rows(T *list, int n, const std::vector<int32_t> &row) {
-    std::vector<T> tmp(list, list + n);
+    thread_local std::vector<T> tmp;
+    tmp.assign(list, list + n);
     for (int i = 0; i < n; ++i) list[row[i]] = tmp[i];
 }
 
