@@ -113,27 +113,33 @@ __device__ __forceinline__ int64_t slot_tet(int32_t slot) { return ((int64_t)(sl
 #endif
 
 // lumped mass of node k from its active incidences in original order
-// (8 incidences at a time: their slot, state and volume loads are issued together, three round
-// trips per batch instead of three per incidence; the sum stays sequential in ascending order)
+#ifndef CEM_MASS_BATCH
+#define CEM_MASS_BATCH 4  // (8 costs stage D a spill: +2.6 us per step on config 3)
+#endif
+// (CEM_MASS_BATCH incidences at a time: their slot, state and volume loads are issued together,
+// three round trips per batch instead of three per incidence; the sum stays sequential in
+// ascending order)
 __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
+    constexpr int B = CEM_MASS_BATCH;
     double acc = 0.0;
-    const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + k * d.wn);  // wn is a multiple of 8
-    for (int j = 0; j < d.wn; j += 8) {
-        const int4 q0 = __ldg(row + (j >> 2)), q1 = __ldg(row + (j >> 2) + 1);
-        const int32_t sl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        uint8_t st[8];
-        double V[8];
+    const int32_t *row = d.nodeE + k * d.wn;  // wn is a multiple of 8
+    for (int j = 0; j < d.wn; j += B) {
+        int32_t sl[B];
+        uint8_t st[B];
+        double V[B];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < B; ++t) sl[t] = __ldg(row + j + t);
+#pragma unroll
+        for (int t = 0; t < B; ++t) {
             const bool ok = sl[t] != d.zslot;
             const int64_t e = ok ? slot_tet(sl[t]) : 0;
             st[t] = ok ? __ldcg(d.state + e) : (uint8_t)0;
             V[t] = ok ? geo_V(d, (uint32_t)e) : 0.0;
         }
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
+        for (int t = 0; t < B; ++t)
             if (st[t]) acc = acc + (d.rho * V[t]) / 4.0;
-        if (sl[7] == d.zslot) break;  // padding only at the row's end
+        if (sl[B - 1] == d.zslot) break;  // padding only at the row's end
     }
     return acc;
 }
