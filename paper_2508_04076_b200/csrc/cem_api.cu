@@ -945,7 +945,8 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         ctx->err = "cudaSetDevice failed (no CUDA device?)";
         return fail(CEM_ECUDA);
     }
-    build_plan(ctx->h, block_size(), ctx->p, tflag_local.empty() ? nullptr : tflag_local.data());
+    const bool persistent = opts && (opts->flags & CEM_F_PERSISTENT);
+    build_plan(ctx->h, block_size(), ctx->p, tflag_local.empty() ? nullptr : tflag_local.data(), persistent);
     PhaseClock clk;
     const int smem = smem_bytes_for(ctx->p);
     if (smem > 227 * 1024) {
@@ -957,7 +958,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     const int occ = std::max(1, persistent_occupancy(smem, ctx->p.blk));
     ctx->grid = sms * occ;
-    {
+    if (persistent) {
         const char *ev = getenv("CEM_SCHED_SLACK");  // tuning knob: slack in units of resident CTAs
         const double slack = ev ? atof(ev) : 3.0;
         build_schedule(ctx->p, (int)(slack * ctx->grid));

@@ -159,7 +159,7 @@ struct Plan {
     int32_t zslot = 0;
 };
 
-void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig = nullptr);
+void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig = nullptr, bool with_deps = true);
 void build_schedule(Plan &p, int resident_ctas);
 
 // ---------------------------------------------------------------- device view

@@ -197,7 +197,7 @@ void dedupe(const int32_t *vals, int n, std::vector<int32_t> &uniq, std::vector<
 
 }  // namespace
 
-void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) {
+void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, bool with_deps) {
     const int64_t N = h.N, E = h.E, S = h.S;
     p.blk = blk;
     p.blk_ab = CEM_AB_EPT * blk;
@@ -605,6 +605,12 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig) 
     for (int g = 0; g < ST_COUNT; ++g) {
         p.nblk[g] = (int)((cnt[g] + per[g] - 1) / per[g]);
         p.maxblk = std::max(p.maxblk, p.nblk[g]);
+    }
+    if (!with_deps) {  // the producer lists serve only the persistent wavefront kernel
+        p.dep_off.clear();
+        p.dep.clear();
+        p.ncons.clear();
+        return;
     }
     // explicit producer-block lists per (stage, block)
     std::vector<std::vector<int32_t>> deps((size_t)ST_COUNT * p.maxblk);
