@@ -188,6 +188,7 @@ void dedupe(const int32_t *vals, int n, std::vector<int32_t> &uniq, std::vector<
     for (int i = 0; i < n; ++i) scratch[i] = (uint64_t)(uint32_t)vals[i] << 32 | (uint32_t)i;
     std::sort(scratch.begin(), scratch.end());
     uniq.clear();
+    uniq.reserve(n);
     for (int i = 0; i < n; ++i) {
         const int32_t v = (int32_t)(scratch[i] >> 32);
         if (uniq.empty() || uniq.back() != v) uniq.push_back(v);
