@@ -1043,6 +1043,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
             a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
             a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
             cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+            cudaCtxResetPersistingL2Cache();  // lines left persisting by earlier work start normal
             cudaGetLastError();  // best effort: a refused window only costs the speed-up
         }
     }
