@@ -87,6 +87,8 @@ class Problem:
     cells: tuple = (0, 0, 0)
     dims: tuple = (0.0, 0.0, 0.0)
     node_ijk: Optional[np.ndarray] = None   # [N,3] lattice indices (tests only)
+    f_nodal: Optional[np.ndarray] = None    # [N,3] constant nodal point forces (N), or None
+    body: tuple = (0.0, 0.0, 0.0)           # uniform body force density b (N/m^3)
     meta: dict = field(default_factory=dict)
 
     @property

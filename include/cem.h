@@ -23,8 +23,12 @@
  *    cem_workspace_size bytes), or an allocation callback (opts.dev_alloc, e.g. a torch
  *    allocator), or neither, in which case the library uses cudaMalloc and frees on
  *    cem_destroy.
- *  - Asynchrony: cem_step enqueues work on opts.stream (NULL = the legacy default stream)
- *    and returns; cem_get_state and cem_crack_update synchronise that stream.
+ *  - Asynchrony: the library runs its work on a private non-blocking stream of its own (CUDA
+ *    graphs and the L2 access-policy window live there).  Every call that enqueues work first
+ *    makes that stream wait for opts.stream (NULL = the legacy default stream) and, on return,
+ *    makes opts.stream wait for the library's work, so work on opts.stream is ordered with the
+ *    library's in both directions.  cem_step returns without waiting; cem_get_state,
+ *    cem_crack_update and cem_energy synchronise.
  *  - Errors: every call returns a cem_status; cem_last_error(ctx) gives a message (also for
  *    a NULL ctx: the last error of cem_init_mesh in this thread).  No exception crosses the
  *    ABI.  A ctx is not thread-safe.
@@ -41,7 +45,7 @@
 extern "C" {
 #endif
 
-#define CEM_ABI_VERSION 1
+#define CEM_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define CEM_API __attribute__((visibility("default")))
@@ -83,7 +87,11 @@ typedef struct {
 } cem_mesh_in;
 
 /* Loads (PAPER.md:L191 Dirichlet/Neumann boundaries; L408-L412 external force;
- * L572-L579 velocity ramp; L1119 constant traction). */
+ * L572-L579 velocity ramp; L1119 constant traction).  The external force is assembled once at
+ * init and is constant from t = 0 (R4, R4b), in this order per node and component:
+ * body force b (V_e/4) over the active incident tets (ascending tet id; PAPER.md:L410
+ * "A_e [N^e] b A_e"), then the traction triangles in the given order (t A/3 per node), then
+ * f_nodal. */
 typedef struct {
     int64_t n_tfaces;
     const int32_t *tface;     /* [n_tfaces][3] boundary triangles carrying a traction */
@@ -93,6 +101,8 @@ typedef struct {
     const uint8_t *vbc_mask;  /* [n_vbc] bit0 = x, bit1 = y, bit2 = z */
     const double *vbc_v0;     /* [n_vbc][3] target velocity (m/s) */
     double vbc_t0;            /* ramp time (s): v = (t/t0) v0 for t <= t0, else v0; 0 = step */
+    const double *f_nodal;    /* NULL | [n_nodes][3] constant nodal point forces (N) (ABI >= 2) */
+    double body[3];           /* uniform body force density b (N/m^3), e.g. rho g; 0 = none (ABI >= 2) */
 } cem_load_in;
 
 /* flags */
@@ -105,6 +115,9 @@ typedef struct {
                                  * Multi-GPU (NCCL) contexts use the P2P halo whenever every rank can
                                  * map its peers' buffers (CUDA IPC over NVLink) and a self-check at
                                  * init passes; CEM_NO_P2P=1 in the environment keeps NCCL send/recv. */
+#define CEM_F_FRONT_BOTH_STRETCHED 0x40u /* criterion variant (R11, "whose
+                                 * tensile stretches at two edges"): a candidate whose front edges c-p,
+                                 * c-q are not both stretched has G = 0 (default: no such condition) */
 
 typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
 
@@ -140,9 +153,12 @@ typedef struct {
     int32_t *node_owner;      /* [global n_nodes] */
 } cem_part_out;
 
-/* State snapshot.  For CEM_HOST every non-NULL array pointer must point to caller-owned
- * host memory of the stated size and is filled; for CEM_DEVICE the pointers are set to
- * device views valid until the next cem_step / cem_crack_update / cem_destroy. */
+/* State snapshot, always in the caller's numbering (node / tet ids of cem_init_mesh) and the
+ * layouts below.  where = CEM_HOST: every non-NULL array pointer is caller-owned HOST memory of
+ * the stated size and is filled.  where = CEM_DEVICE: every non-NULL array pointer is caller-owned
+ * DEVICE memory (same sizes and layouts, e.g. torch tensors on the ctx device) and is filled by
+ * kernels / copies on the ctx stream; the call returns after that stream has synchronised.  In
+ * both cases records come sorted by (step, element). */
 #define CEM_HOST 0
 #define CEM_DEVICE 1
 typedef struct {

@@ -53,7 +53,7 @@ def lib():
         L.orc_create.restype = C.c_void_p
         L.orc_create.argtypes = [C.c_int64, D, C.c_int64, I32, U8, D, C.c_double, C.c_double, C.c_double,
                                  C.c_int64, I32, D, C.c_int64, I32, U8, D, C.c_double, C.c_double,
-                                 C.c_double, C.c_double, C.c_char_p, C.c_int]
+                                 C.c_double, C.c_double, D, D, C.c_uint32, C.c_char_p, C.c_int]
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_run.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
         L.orc_run.restype = C.c_int
@@ -75,6 +75,7 @@ def lib():
         L.orc_candidates.argtypes = [C.c_void_p, D, C.c_int64, D, D]
         L.orc_principal.argtypes = [D, D, D, I32, I32]
         L.orc_tet_geometry.argtypes = [D, D, D]
+        L.orc_sig_proj.argtypes = [D, D]; L.orc_sig_proj.restype = C.c_double
         L.orc_lame.argtypes = [C.c_double, C.c_double, D, D]
         L.orc_lame_of.argtypes = [C.c_void_p, D, D]
         L.orc_newmark_free.argtypes = [C.c_int64, D, D, D, D, D, C.c_double, C.c_double]
@@ -105,7 +106,10 @@ class Records:
 class Oracle:
     """One oracle simulation (mirrors the product's cem_init_mesh / cem_step semantics)."""
 
-    def __init__(self, prob, dt=None):
+    # criterion variant flag (R11; the product's CEM_F_FRONT_BOTH_STRETCHED has the same value)
+    FRONT_BOTH_STRETCHED = 0x40
+
+    def __init__(self, prob, dt=None, flags=0):
         L = lib()
         self.prob = prob
         self._keep = [
@@ -114,12 +118,17 @@ class Oracle:
             _c(prob.vbc_node, np.int32), _c(prob.vbc_mask, np.uint8), _c(prob.vbc_v0, np.float64),
         ]
         X, T, st, gc, tf, tt, vn, vm, vv = self._keep
+        fn = getattr(prob, "f_nodal", None)
+        fn = None if fn is None else _c(fn, np.float64).reshape(-1, 3)
+        body = _c(getattr(prob, "body", (0.0, 0.0, 0.0)), np.float64)
+        self._keep += [fn, body]
         err = C.create_string_buffer(256)
         self.N, self.E = prob.n_nodes, prob.n_tets
         self.h = L.orc_create(self.N, _p(X, D), self.E, _p(T, I32), _p(st, U8), _p(gc, D),
                               prob.E, prob.nu, prob.rho, tf.shape[0], _p(tf, I32), _p(tt, D),
                               vn.shape[0], _p(vn, I32), _p(vm, U8), _p(vv, D), prob.vbc_t0,
-                              prob.dt if dt is None else dt, prob.cfl, prob.gamma, err, 256)
+                              prob.dt if dt is None else dt, prob.cfl, prob.gamma, _p(fn, D), _p(body, D),
+                              int(flags), err, 256)
         if not self.h:
             raise ValueError("oracle rejected the mesh: " + err.value.decode())
         self.S = L.orc_n_edges(self.h)
@@ -218,6 +227,12 @@ def principal(s6):
     k1 = C.c_int32(); deg = C.c_int32()
     lib().orc_principal(_p(s6, D), _p(lam, D), _p(vec, D), C.byref(k1), C.byref(deg))
     return lam, vec, k1.value, deg.value
+
+
+def sig_proj(s6, m):
+    """sigma_G . m (unnormalised m) of the stress s6, R8."""
+    s6 = _c(s6, np.float64); m = _c(m, np.float64)
+    return lib().orc_sig_proj(_p(s6, D), _p(m, D))
 
 
 def tet_geometry(X4):

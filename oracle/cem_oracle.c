@@ -31,6 +31,11 @@
 static const int EP[6] = {0, 0, 0, 1, 1, 2};
 static const int EQ[6] = {1, 2, 3, 2, 3, 3};
 
+/* criterion variant (R11 / SURVEY.md §8(c) Q11): a candidate counts only when both edges of its
+ * crack front (c-p and c-q) are stretched ("whose tensile stretches at two edges", PAPER.md:L459;
+ * SPEC.md:L305 "front with both stretches nonzero"); other candidates get G = 0 */
+#define ORC_F_FRONT_BOTH_STRETCHED 0x40u
+
 static int local_edge(int a, int b) {
     int p = a < b ? a : b, q = a < b ? b : a;
     for (int l = 0; l < 6; ++l)
@@ -63,6 +68,7 @@ typedef struct orc_sim {
     uint8_t *dir;         /* [N] Dirichlet mask bits */
     double *dir_v0;       /* [N][3] */
     double t0;
+    uint32_t flags;       /* ORC_F_* (criterion variants) */
     double E_mod, nu, rho, lam, mu, l2m;
     double dt, gamma;
     /* state */
@@ -193,6 +199,14 @@ static double sig_proj(const double *lam, const double *vec, int k1, int deg, co
         acc = acc + d * d;
     }
     return lam[k1] * sqrt(acc);
+}
+
+/* probe (tests): sigma_G . m of the stress s6 for an unnormalised normal m (R8) */
+ORC_API double orc_sig_proj(const double *s6, const double *m) {
+    double lam[3], vec[9];
+    int32_t k1, deg;
+    orc_principal(s6, lam, vec, &k1, &deg);
+    return sig_proj(lam, vec, k1, deg, m);
 }
 
 /* ---------------------------------------------------------------- topology */
@@ -467,6 +481,8 @@ static void tet_candidates(const orc_sim *s, int64_t e, const double *u, const e
                     G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
                     area = sqrt(mm) / 8.0;
                 }
+                if ((s->flags & ORC_F_FRONT_BOTH_STRETCHED) && !(H[local_edge(c, p)] && H[local_edge(c, q)]))
+                    G = 0.0; /* R11 variant: the front is not stretched at both edges */
                 int k = 6 * c + 2 * f + t;
                 G24[k] = G; A24[k] = area;
             }
@@ -534,10 +550,11 @@ ORC_API orc_sim *orc_create(int64_t n_nodes, const double *X, int64_t n_tets, co
                             int64_t n_tf, const int32_t *tface, const double *tface_t,
                             int64_t n_vbc, const int32_t *vbc_node, const uint8_t *vbc_mask,
                             const double *vbc_v0, double vbc_t0, double dt, double cfl, double gamma,
+                            const double *f_nodal, const double *body, uint32_t flags,
                             char *err, int errlen) {
     orc_sim *s = xcalloc(1, sizeof(orc_sim));
     s->N = n_nodes; s->E = n_tets; s->F = n_tf; s->B = n_vbc;
-    s->E_mod = E; s->nu = nu; s->rho = rho; s->gamma = gamma; s->t0 = vbc_t0;
+    s->E_mod = E; s->nu = nu; s->rho = rho; s->gamma = gamma; s->t0 = vbc_t0; s->flags = flags;
     orc_lame(E, nu, &s->lam, &s->mu);
     s->l2m = s->lam + 2.0 * s->mu;
     s->X = xcalloc(3 * n_nodes, sizeof(double)); memcpy(s->X, X, sizeof(double) * 3 * n_nodes);
@@ -628,9 +645,22 @@ ORC_API orc_sim *orc_create(int64_t n_nodes, const double *X, int64_t n_tets, co
     /* mass */
     s->m = xcalloc(n_nodes, sizeof(double));
     for (int64_t k = 0; k < n_nodes; ++k) s->m[k] = node_mass(s, k);
-    /* external force: traction t on triangle (x0,x1,x2), A = |(x1-x0)x(x2-x0)|/2,
-     * f_k += t (A/3) per node (R4), faces in the given order. */
+    /* external force (f_ext = A_e [N^e] b A_e + A_e [N^e] t ell_e), constant
+     * from t = 0 like the tractions:
+     *  1. body force b (N/m^3, uniform): consistent lumping of the constant-b integral over each
+     *     active tet, f_k += b (V_e / 4) per incidence, ascending e (R4b);
+     *  2. traction t on triangle (x0,x1,x2), A = |(x1-x0)x(x2-x0)|/2, f_k += t (A/3) per node
+     *     (R4), faces in the given order;
+     *  3. nodal point forces f_nodal[k] added last (SURVEY.md §8(b) cem_load_in.f_ext). */
     s->fext = xcalloc(3 * n_nodes, sizeof(double));
+    if (body && (body[0] != 0.0 || body[1] != 0.0 || body[2] != 0.0))
+        for (int64_t k = 0; k < n_nodes; ++k)
+            for (int64_t j = s->nod_off[k]; j < s->nod_off[k + 1]; ++j) {
+                int32_t e = s->nod_ent[j] >> 2;
+                if (!s->active[e]) continue;
+                double w = s->V[e] / 4.0;
+                for (int c = 0; c < 3; ++c) s->fext[3 * k + c] = s->fext[3 * k + c] + body[c] * w;
+            }
     for (int64_t f = 0; f < n_tf; ++f) {
         const int32_t *tri = tface + 3 * f;
         double d1[3], d2[3], cr[3];
@@ -642,6 +672,8 @@ ORC_API orc_sim *orc_create(int64_t n_nodes, const double *X, int64_t n_tets, co
         for (int i = 0; i < 3; ++i)
             for (int c = 0; c < 3; ++c) s->fext[3 * (int64_t)tri[i] + c] = s->fext[3 * (int64_t)tri[i] + c] + tface_t[3 * f + c] * w;
     }
+    if (f_nodal)
+        for (int64_t i = 0; i < 3 * n_nodes; ++i) s->fext[i] = s->fext[i] + f_nodal[i];
     /* Dirichlet */
     s->dir = xcalloc(n_nodes, 1);
     s->dir_v0 = xcalloc(3 * n_nodes, sizeof(double));

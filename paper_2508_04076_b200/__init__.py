@@ -37,6 +37,7 @@ CEM_F_NO_DISCARD = 0x4
 CEM_F_PERSISTENT = 0x8
 CEM_F_LOOPBACK = 0x10
 CEM_F_P2P = 0x20
+CEM_F_FRONT_BOTH_STRETCHED = 0x40
 CEM_HOST, CEM_DEVICE = 0, 1
 
 D = C.POINTER(C.c_double)
@@ -56,7 +57,8 @@ class cem_mesh_in(C.Structure):
 
 class cem_load_in(C.Structure):
     _fields_ = [("n_tfaces", C.c_int64), ("tface", I32), ("tface_t", D), ("n_vbc", C.c_int64),
-                ("vbc_node", I32), ("vbc_mask", U8), ("vbc_v0", D), ("vbc_t0", C.c_double)]
+                ("vbc_node", I32), ("vbc_mask", U8), ("vbc_v0", D), ("vbc_t0", C.c_double),
+                ("f_nodal", D), ("body", C.c_double * 3)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_size_t, C.c_void_p, C.POINTER(C.c_void_p))
@@ -171,7 +173,7 @@ class Simulation:
     def __init__(self, X, tets, E, nu, rho, Gc=np.inf, tet_state=None, tet_gc=None,
                  tface=None, tface_t=None, vbc_node=None, vbc_mask=None, vbc_v0=None, vbc_t0=0.0,
                  dt=0.0, cfl=0.5, gamma=0.5, flags=0, device=0, stream=None, use_torch=True,
-                 rank=0, nranks=1, nccl_id=None):
+                 rank=0, nranks=1, nccl_id=None, f_nodal=None, body=(0.0, 0.0, 0.0)):
         self._h = C.c_void_p()
         keep = []
         Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, 4))
@@ -185,9 +187,10 @@ class Simulation:
         vn = _arr(np.zeros(0) if vbc_node is None else vbc_node, np.int32)
         vm = _arr(np.zeros(0) if vbc_mask is None else vbc_mask, np.uint8)
         vv = _arr(np.zeros((0, 3)) if vbc_v0 is None else vbc_v0, np.float64, (-1, 3))
-        keep += [tf, tt, vn, vm, vv]
+        fn = None if f_nodal is None else _arr(f_nodal, np.float64, (-1, 3))
+        keep += [tf, tt, vn, vm, vv, fn]
         load = cem_load_in(tf.shape[0], _ptr(tf, I32), _ptr(tt, D), vn.shape[0], _ptr(vn, I32),
-                           _ptr(vm, U8), _ptr(vv, D), vbc_t0)
+                           _ptr(vm, U8), _ptr(vv, D), vbc_t0, _ptr(fn, D), (C.c_double * 3)(*[float(b) for b in body]))
         self._tensors = []
         self._alloc_cb = None
         self.device = device
@@ -232,7 +235,8 @@ class Simulation:
         return cls(prob.X, prob.tets, prob.E, prob.nu, prob.rho, Gc=prob.Gc, tet_state=prob.tet_state,
                    tet_gc=prob.tet_gc, tface=prob.tface, tface_t=prob.tface_t, vbc_node=prob.vbc_node,
                    vbc_mask=prob.vbc_mask, vbc_v0=prob.vbc_v0, vbc_t0=prob.vbc_t0, dt=prob.dt,
-                   cfl=prob.cfl, gamma=prob.gamma, **kw)
+                   cfl=prob.cfl, gamma=prob.gamma, f_nodal=getattr(prob, "f_nodal", None),
+                   body=getattr(prob, "body", (0.0, 0.0, 0.0)), **kw)
 
     def _check(self, rc):
         if rc != CEM_OK:
@@ -280,6 +284,42 @@ class Simulation:
         nr = min(out.n_records, cap)
         return State(u, v, a, st, m, out.step, out.time, out.dt, out.n_active, out.dissipated,
                      out.nonfinite, out.nonfinite_node, rs[:nr], re[:nr], rk[:nr], rg[:nr], ra[:nr])
+
+    def device_state(self, records=True) -> dict:
+        """cem_get_state(CEM_DEVICE): torch tensors on the simulation's device, filled by the
+        library in the caller's numbering (u, v, a [N,3]; tet_state [E]; mass [N]; records
+        sorted by (step, element))."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        N, E = self.n_nodes, self.n_tets
+        t = dict(u=torch.empty((N, 3), dtype=torch.float64, device=dev),
+                 v=torch.empty((N, 3), dtype=torch.float64, device=dev),
+                 a=torch.empty((N, 3), dtype=torch.float64, device=dev),
+                 tet_state=torch.empty(E, dtype=torch.uint8, device=dev),
+                 mass=torch.empty(N, dtype=torch.float64, device=dev))
+        cap = E if records else 0
+        r = dict(rec_step=torch.empty(cap, dtype=torch.int64, device=dev),
+                 rec_elem=torch.empty(cap, dtype=torch.int32, device=dev),
+                 rec_cand=torch.empty(cap, dtype=torch.int32, device=dev),
+                 rec_G=torch.empty(cap, dtype=torch.float64, device=dev),
+                 rec_area=torch.empty(cap, dtype=torch.float64, device=dev))
+        torch.cuda.synchronize(dev)  # the tensors' allocation is ordered before the library's stream
+        out = cem_state_out()
+        vp = lambda x, ty: C.cast(C.c_void_p(x.data_ptr()), ty)
+        out.u, out.v, out.a = vp(t["u"], D), vp(t["v"], D), vp(t["a"], D)
+        out.tet_state, out.mass = vp(t["tet_state"], U8), vp(t["mass"], D)
+        if cap:
+            out.rec_step, out.rec_elem = vp(r["rec_step"], I64), vp(r["rec_elem"], I32)
+            out.rec_cand, out.rec_G, out.rec_area = vp(r["rec_cand"], I32), vp(r["rec_G"], D), vp(r["rec_area"], D)
+        out.rec_capacity = cap
+        rc = _lib.cem_get_state(self._h, C.byref(out), CEM_DEVICE)
+        if rc not in (CEM_OK, CEM_ENONFINITE):
+            self._check(rc)
+        nr = min(out.n_records, cap)
+        t.update({k: v[:nr] for k, v in r.items()})
+        t.update(step=out.step, time=out.time, n_active=out.n_active, dissipated=out.dissipated,
+                 nonfinite=out.nonfinite)
+        return t
 
     def energy(self) -> dict:
         """Energy ledger at the current step (cem_energy): kinetic, strain, external, reaction,

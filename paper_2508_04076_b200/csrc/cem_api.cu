@@ -19,8 +19,12 @@ struct cem_ctx {
     HostMesh h;
     Plan p;
     Dev d{};
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;       // the library's private non-blocking stream (all its work)
+    cudaStream_t user_stream = nullptr;  // opts.stream (NULL = the legacy default stream)
+    cudaEvent_t fence_in = nullptr, fence_out = nullptr;  // ordering between the two
     bool own_stream = false;
+    bool l2_limit_raised = false;        // this ctx raised the device's persisting-L2 set-aside
+    size_t l2_limit_prev = 0;
     int device = 0;
     void *ws = nullptr;
     size_t ws_bytes = 0;
@@ -52,6 +56,26 @@ struct cem_ctx {
 namespace {
 
 thread_local std::string g_init_err;
+
+// Every entry point that enqueues work orders the library's private stream after the caller's
+// stream on entry and the caller's stream after the private one on exit (include/cem.h
+// "Asynchrony"), so work the caller put on opts.stream -- or on the legacy default stream when
+// opts.stream is NULL -- is ordered with the library's in both directions.
+struct StreamFence {
+    cem_ctx *c;
+    explicit StreamFence(cem_ctx *ctx) : c(ctx) {
+        if (c && c->fence_in) {
+            cudaEventRecord(c->fence_in, c->user_stream);
+            cudaStreamWaitEvent(c->stream, c->fence_in, 0);
+        }
+    }
+    ~StreamFence() {
+        if (c && c->fence_out) {
+            cudaEventRecord(c->fence_out, c->stream);
+            cudaStreamWaitEvent(c->user_stream, c->fence_out, 0);
+        }
+    }
+};
 
 #define CUDA_TRY(x)                                                                   \
     do {                                                                              \
@@ -317,9 +341,15 @@ struct Stager {
         return cudaSuccess;
     }
 };
-Stager &stager() {
-    static Stager *g = new Stager();  // process lifetime (pinned halves reused by every context)
-    return *g;
+// one Stager per device: its events are recorded on streams of that device only
+Stager &stager(int device) {
+    static std::mutex mu;
+    static std::vector<Stager *> per_dev;  // process lifetime (pinned halves reused by the device's contexts)
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 0) device = 0;
+    if ((size_t)device >= per_dev.size()) per_dev.resize(device + 1, nullptr);
+    if (!per_dev[device]) per_dev[device] = new Stager();
+    return *per_dev[device];
 }
 
 cem_status upload(cem_ctx *ctx, const Offs &o) {
@@ -368,7 +398,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
         u1[kn] = make_double4(uu[0], uu[1], uu[2], 0.0);
     }
     std::vector<int32_t> node_orig(p.node_new2old.begin(), p.node_new2old.end());
-    Stager &sg = stager();
+    Stager &sg = stager(ctx->device);
     std::lock_guard<std::mutex> lock(sg.mu);
     auto put = [&](size_t off, const void *src, size_t bytes) -> cudaError_t {
         return sg.put(at<char>(b, off), src, bytes, st);
@@ -467,10 +497,30 @@ __global__ void k_fill(int32_t *p, int64_t n, int32_t v) {
     if (i < n) p[i] = v;
 }
 
+// CEM_DEVICE readback (cem_get_state): storage-order device arrays -> the caller's device
+// buffers in the caller's numbering ([n][3] for node vectors)
+__global__ void k_export_vec(const double4 *__restrict__ src, const int32_t *__restrict__ node_orig, double *dst, int64_t N) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const double4 w = src[k];
+    const int64_t o = 3 * (int64_t)node_orig[k];
+    dst[o] = w.x;
+    dst[o + 1] = w.y;
+    dst[o + 2] = w.z;
+}
+__global__ void k_export_f64(const double *__restrict__ src, const int32_t *__restrict__ orig, double *dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[orig[i]] = src[i];
+}
+__global__ void k_export_u8(const uint8_t *__restrict__ src, const int32_t *__restrict__ orig, uint8_t *dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[orig[i]] = src[i];
+}
+
 
 // ---------------------------------------------------------------- multi-GPU helpers
 struct LocalMesh {
-    std::vector<double> X, tface_t, vbc_v0;
+    std::vector<double> X, tface_t, vbc_v0, f_nodal;
     std::vector<int32_t> tets, tface, vbc_node;
     std::vector<uint8_t> state, vbc_mask;
     std::vector<double> gc;
@@ -503,6 +553,11 @@ void extract_local(const cem_mesh_in *m, const cem_material *mat, const cem_load
                 lm.tface_t.push_back(ld->tface_t[3 * f + i]);
             }
         }
+    if (ld && ld->f_nodal) {
+        lm.f_nodal.resize(3 * Nl);
+        for (int64_t i = 0; i < Nl; ++i)
+            for (int c = 0; c < 3; ++c) lm.f_nodal[3 * i + c] = ld->f_nodal[3 * (int64_t)L.node_global[i] + c];
+    }
     if (ld)
         for (int64_t b = 0; b < ld->n_vbc; ++b) {
             if (g2l[ld->vbc_node[b]] < 0) continue;
@@ -864,6 +919,23 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
     o->node_owner = dup32(g.node_owner);
 }
 
+// undo this context's L2 persistence: clear the window on its stream and, if it raised the
+// device's persisting set-aside, restore the previous limit and demote the lines it pinned
+void release_l2(cem_ctx *ctx) {
+    if (ctx->stream) {
+        cudaStreamAttrValue a = {};
+        a.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+    }
+    if (ctx->l2_limit_raised) {
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->l2_limit_prev);
+        ctx->l2_limit_raised = false;
+    }
+    cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -897,8 +969,11 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     cem_ctx *ctx = new cem_ctx();
     auto fail = [&](cem_status s) {
         g_init_err = ctx->err;
+        release_l2(ctx);
         if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->fence_in) cudaEventDestroy(ctx->fence_in);
+        if (ctx->fence_out) cudaEventDestroy(ctx->fence_out);
         delete ctx;
         return s;
     };
@@ -928,7 +1003,9 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         cem_mesh_in m2 = {(int64_t)ctx->part.node_global.size(), lm.X.data(), (int64_t)ctx->part.tet_global.size(),
                           lm.tets.data(), lm.state.data(), lm.gc.data()};
         cem_load_in l2 = {(int64_t)lm.tface.size() / 3, lm.tface.data(), lm.tface_t.data(), (int64_t)lm.vbc_node.size(),
-                          lm.vbc_node.data(), lm.vbc_mask.data(), lm.vbc_v0.data(), load ? load->vbc_t0 : 0.0};
+                          lm.vbc_node.data(), lm.vbc_mask.data(), lm.vbc_v0.data(), load ? load->vbc_t0 : 0.0,
+                          lm.f_nodal.empty() ? nullptr : lm.f_nodal.data(),
+                          {load ? load->body[0] : 0.0, load ? load->body[1] : 0.0, load ? load->body[2] : 0.0}};
         st = build_host_mesh(&m2, mat, &l2, &lo, ctx->h, ctx->err);
         if (st) return fail(st);
         for (size_t i = 0; i < ctx->part.node_owned.size(); ++i)
@@ -940,7 +1017,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     }
     ctx->device = opts ? opts->device : 0;
     ctx->flags = opts ? opts->flags : 0;
-    ctx->stream = opts ? (cudaStream_t)opts->stream : nullptr;
+    ctx->user_stream = opts ? (cudaStream_t)opts->stream : nullptr;
     if (cudaSetDevice(ctx->device) != cudaSuccess) {
         ctx->err = "cudaSetDevice failed (no CUDA device?)";
         return fail(CEM_ECUDA);
@@ -964,12 +1041,16 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         build_schedule(ctx->p, (int)(slack * ctx->grid));
     }
     clk.mark("init: schedule");
-    if (!ctx->stream) {  // graphs / persistent launches never use the legacy default stream
-        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-            ctx->err = "cudaStreamCreate failed";
+    {  // the library's own stream (graphs, access-policy window); fenced against opts.stream
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->fence_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->fence_out, cudaEventDisableTiming) != cudaSuccess) {
+            ctx->err = "cudaStreamCreate / cudaEventCreate failed";
             return fail(CEM_ECUDA);
         }
         ctx->own_stream = true;
+        cudaEventRecord(ctx->fence_in, ctx->user_stream);  // a caller-allocated workspace is ready
+        cudaStreamWaitEvent(ctx->stream, ctx->fence_in, 0);
     }
     Offs o = layout(ctx->h, ctx->p);
     if (opts && opts->workspace) {
@@ -1030,12 +1111,17 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         const size_t win = std::min(bytes, (size_t)std::max(0, maxwin));
         // only when the planes fit the set-aside whole: a partial window (hit ratio < 1 over a larger
         // mesh's planes) thrashed -- config 4 on one GPU 1087 -> 1614 us/step
-        if (want > 0.0 && win > 0 && win == bytes && bytes <= (size_t)std::max(0, maxpers)) {
+        // (single-GPU contexts only: loopback ranks share rank 0's stream; the window lives on the
+        // library's private stream, and cem_destroy restores the set-aside it raised)
+        if (!ctx->dist && want > 0.0 && win > 0 && win == bytes && bytes <= (size_t)std::max(0, maxpers)) {
             const double hit = std::min(want, 1.0);
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             const size_t aside = std::min((size_t)maxpers, (size_t)(win * hit));
-            if (aside > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside);  // (device-wide)
+            if (aside > cur && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside) == cudaSuccess) {
+                ctx->l2_limit_raised = true;  // (device-wide: restored by cem_destroy)
+                ctx->l2_limit_prev = cur;
+            }
             cudaStreamAttrValue a = {};
             a.accessPolicyWindow.base_ptr = ctx->d.srec;
             a.accessPolicyWindow.num_bytes = win;
@@ -1043,7 +1129,6 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
             a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
             a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
             cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &a);
-            cudaCtxResetPersistingL2Cache();  // lines left persisting by earlier work start normal
             cudaGetLastError();  // best effort: a refused window only costs the speed-up
         }
     }
@@ -1074,12 +1159,15 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
 void cem_destroy(cem_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    release_l2(ctx);
     for (auto e : ctx->ev) cudaEventDestroy(e);
     for (void *p : ctx->p2p.opened) cudaIpcCloseMemHandle(p);
     if (ctx->comm) nccl_comm_destroy(ctx->comm);
     for (void *p : ctx->dist_allocs) cudaFree(p);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->fence_in) cudaEventDestroy(ctx->fence_in);
+    if (ctx->fence_out) cudaEventDestroy(ctx->fence_out);
     if (ctx->crit_seen) cudaFreeHost(const_cast<int32_t *>(ctx->crit_seen));
     delete ctx;
 }
@@ -1108,6 +1196,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (!ctx || nsteps < 0) return CEM_EINVAL;
     if (nsteps == 0) return CEM_OK;
     if (crack_every < 0) crack_every = 0;
+    StreamFence fence(ctx);
     // default: one kernel per stage (measured faster than the persistent wavefront kernel on
     // B200 for the current stage bodies; CEM_F_PERSISTENT selects the latter)
     if (ctx->dist) {
@@ -1193,6 +1282,7 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
         ctx->err = "cem_crack_update: single-GPU contexts only";
         return CEM_ESTATE;
     }
+    StreamFence fence(ctx);
     int32_t before = 0, after = 0;
     CUDA_TRY(cudaMemcpyAsync(&before, ctx->d.ctr, sizeof before, cudaMemcpyDeviceToHost, ctx->stream));
     launch_crack_only(ctx->d, ctx->step, ctx->stream);
@@ -1206,6 +1296,7 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
 
 cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
     if (!ctx || !out) return CEM_EINVAL;
+    StreamFence fence(ctx);
     cudaStream_t st = ctx->stream;
     cem_state_out so{};
     const cem_status rc = cem_get_state(ctx, &so, CEM_HOST);  // synchronises; U_d, nonfinite
@@ -1235,6 +1326,7 @@ cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
 
 cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     if (!ctx || !out) return CEM_EINVAL;
+    StreamFence fence(ctx);
     cudaStream_t st = ctx->stream;
     const HostMesh &h = ctx->h;
     const Plan &p = ctx->p;
@@ -1282,17 +1374,38 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     for (int64_t e = 0; e < E; ++e) na += stt[e] != 0;
     double4 *ucur = ctx->d.ubuf[ctx->step & 1];
     if (where == CEM_DEVICE) {
-        // storage-order device views; double4-strided node arrays
-        out->u = reinterpret_cast<double *>(ucur);
-        out->v = reinterpret_cast<double *>(ctx->d.v);
-        out->a = reinterpret_cast<double *>(ctx->d.a);
-        out->tet_state = ctx->d.state;
-        out->mass = ctx->d.mass;
-        out->rec_step = ctx->d.rec_step;
-        out->rec_elem = ctx->d.rec_elem;
-        out->rec_cand = ctx->d.rec_cand;
-        out->rec_G = ctx->d.rec_G;
-        out->rec_area = ctx->d.rec_area;
+        // the caller's DEVICE buffers, filled in the caller's numbering on the ctx stream (same
+        // layout as CEM_HOST); records sorted here and copied up
+        const unsigned gn = (unsigned)((N + 255) / 256), ge = (unsigned)((E + 255) / 256);
+        if (N > 0) {
+            if (out->u) k_export_vec<<<gn, 256, 0, st>>>(ucur, ctx->d.node_orig, out->u, N);
+            if (out->v) k_export_vec<<<gn, 256, 0, st>>>(ctx->d.v, ctx->d.node_orig, out->v, N);
+            if (out->a) k_export_vec<<<gn, 256, 0, st>>>(ctx->d.a, ctx->d.node_orig, out->a, N);
+            if (out->mass) k_export_f64<<<gn, 256, 0, st>>>(ctx->d.mass, ctx->d.node_orig, out->mass, N);
+        }
+        if (out->tet_state && E > 0) k_export_u8<<<ge, 256, 0, st>>>(ctx->d.state, ctx->d.tet_orig, out->tet_state, E);
+        const int64_t nr = std::min<int64_t>(nrec, out->rec_capacity);
+        if (nr > 0) {
+            std::vector<int64_t> s2(nr);
+            std::vector<int32_t> e2(nr), k2(nr);
+            std::vector<double> g2(nr), a2(nr);
+            for (int64_t i = 0; i < nr; ++i) {
+                const int64_t j = ord[i];
+                s2[i] = rs[j]; e2[i] = re[j]; k2[i] = rk[j]; g2[i] = rg[j]; a2[i] = ra[j];
+            }
+            auto up = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
+                return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+            };
+            CUDA_TRY(up(out->rec_step, s2.data(), 8 * nr));
+            CUDA_TRY(up(out->rec_elem, e2.data(), 4 * nr));
+            CUDA_TRY(up(out->rec_cand, k2.data(), 4 * nr));
+            CUDA_TRY(up(out->rec_G, g2.data(), 8 * nr));
+            CUDA_TRY(up(out->rec_area, a2.data(), 8 * nr));
+        }
+        ctx->launches += (N > 0 ? (out->u != nullptr) + (out->v != nullptr) + (out->a != nullptr) + (out->mass != nullptr) : 0) +
+                         (out->tet_state && E > 0 ? 1 : 0);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(st));  // the host record vectors above go out of scope
     } else {
         std::vector<double4> tmp;
         auto get3 = [&](double *dst, const double4 *src) -> cudaError_t {
@@ -1379,6 +1492,10 @@ cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_
     if (crack_every < 0) crack_every = 0;
     for (int r = 1; r < n; ++r) {  // every rank's work goes on rank 0's stream, in rank order
         CUDA_TRY(cudaStreamSynchronize(c[r]->stream));
+    }
+    for (int r = 0; r < n; ++r) {  // ... after the work the callers put on their streams
+        CUDA_TRY(cudaEventRecord(c[r]->fence_in, c[r]->user_stream));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, c[r]->fence_in, 0));
     }
     if (c[0]->init_exchange_pending) {
         cem_status st = exchange_loopback(c, n, 1);

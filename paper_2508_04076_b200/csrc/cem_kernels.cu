@@ -22,6 +22,7 @@
 // completed-step counters of the producer blocks they read.  Consecutive steps overlap;
 // intermediates stay L2-resident between producer and consumer.
 #include <cstdint>
+#include <mutex>
 
 #include "cem_internal.h"
 
@@ -564,7 +565,7 @@ struct CritScratch {
 
 static_assert(sizeof(CritScratch) <= 1024, "stage C's staging area holds 8 warp scratches of <= 1 KB");
 
-__device__ void candidate(const CritScratch &w, int k, double &G, double &area) {
+__device__ void candidate(const CritScratch &w, int k, bool both, double &G, double &area) {
     const int c = k / 6, f = (k % 6) / 2, tt = k & 1;
     int o[3], no = 0;
     for (int b = 0; b < 4; ++b)
@@ -597,6 +598,8 @@ __device__ void candidate(const CritScratch &w, int k, double &G, double &area) 
         G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
         area = sqrt(mm) / 8.0;
     }
+    // R11 variant (CEM_F_FRONT_BOTH_STRETCHED): the front must be stretched at both edges
+    if (both && !(w.H[ledge(c, p)] && w.H[ledge(c, q)])) G = 0.0;
 }
 
 __device__ __forceinline__ void split_tet(const Dev &d, int64_t e, int4 t, double G, int k, double A, int64_t rec_step,
@@ -659,7 +662,7 @@ __device__ __noinline__ void criterion_lane(const Dev *__restrict__ dp, int64_t 
     int kb = -1;
     for (int k = 0; k < 24; ++k) {
         double G, A;
-        candidate(w, k, G, A);
+        candidate(w, k, (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0, G, A);
         if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
             Gb = G;
             kb = k;
@@ -704,7 +707,7 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
     double G = -INFINITY, A = -INFINITY;
     int k = 1 << 20;
     if (lane < 24) {
-        candidate(w, lane, G, A);
+        candidate(w, lane, (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0, G, A);
         k = lane;
     }
 #pragma unroll
@@ -1374,7 +1377,8 @@ __global__ void __launch_bounds__(256, CEM_FILTER_MINB) k_filter(Dev d, int64_t 
         bool need = false;
         if (i < n) {
             e = d.crit_list[i];
-            need = crit_refined_need(d.self, e, u, ldro(d.gc + e));
+            // CEM_F_NO_EARLY_OUT: every listed tet gets the full 24-candidate evaluation
+            need = (d.flags & CEM_F_NO_EARLY_OUT) || crit_refined_need(d.self, e, u, ldro(d.gc + e));
         }
         const unsigned mm = __ballot_sync(0xffffffffu, need);
         if (mm) {
@@ -1432,7 +1436,7 @@ __global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_eval(Dev d
         for (int q = lane; q < 24 * cnt; q += 32) {  // (j, k): candidate k of tet j
             const int j = q / 24, k = q - 24 * j;
             double G, A;
-            candidate(wb.t[j], k, G, A);
+            candidate(wb.t[j], k, (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0, G, A);
             wb.G[j][k] = G;
             wb.A[j][k] = A;
         }
@@ -1532,9 +1536,16 @@ int persistent_occupancy(int smem_bytes, int blk) {
 }
 
 void set_smem_limits(int smem_bytes) {
-    static int cur = 0;  // the attribute is per function: keep the largest any context needs
-    if (smem_bytes <= cur) return;
-    cur = smem_bytes;
+    // the attribute is per function AND per device: keep the largest any context of the current
+    // device needs (called after cudaSetDevice)
+    static std::mutex mu;
+    static int cur[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (smem_bytes <= cur[dev]) return;
+    cur[dev] = smem_bytes;
     cudaFuncSetAttribute(k_AB, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_AB_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);

@@ -313,10 +313,30 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
         }
         h.mass[n] = acc;
     }
-    // ---------------------------------------------------------------- traction: f_k += t (A/3)
+    // ---------------------------------------------------------------- external force
+    // body force b (V_e/4) over the active incident tets in ascending tet id, then the traction
+    // triangles f_k += t (A/3) in the given order, then the nodal point forces (include/cem.h)
     h.fext.assign(3 * N, 0.0);
     h.nflag.assign(N, 0);
     h.dir_v0.assign(3 * N, 0.0);
+    if (ld && (ld->body[0] != 0.0 || ld->body[1] != 0.0 || ld->body[2] != 0.0)) {
+        if (!std::isfinite(ld->body[0]) || !std::isfinite(ld->body[1]) || !std::isfinite(ld->body[2])) {
+            err = "cem_init_mesh: non-finite body force";
+            return CEM_EINVAL;
+        }
+#pragma omp parallel for schedule(static)
+        for (int64_t n = 0; n < N; ++n) {
+            bool any = false;
+            for (int32_t j = h.node_off[n]; j < h.node_off[n + 1]; ++j) {
+                const int32_t e = h.node_ent[j] >> 2;
+                if (!h.state[e]) continue;
+                const double w = h.V[e] / 4.0;
+                for (int c = 0; c < 3; ++c) h.fext[3 * n + c] = h.fext[3 * n + c] + ld->body[c] * w;
+                any = true;
+            }
+            if (any) h.nflag[n] |= 8;
+        }
+    }
     if (ld && ld->n_tfaces > 0) {
         if (!ld->tface || !ld->tface_t) {
             err = "cem_init_mesh: n_tfaces > 0 with NULL arrays";
@@ -337,6 +357,21 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
                 for (int c = 0; c < 3; ++c) h.fext[3 * (int64_t)tri[i] + c] = h.fext[3 * (int64_t)tri[i] + c] + ld->tface_t[3 * f + c] * w;
                 h.nflag[tri[i]] |= 8;
             }
+        }
+    }
+    if (ld && ld->f_nodal) {
+        for (int64_t n = 0; n < N; ++n) {
+            bool any = false;
+            for (int c = 0; c < 3; ++c) {
+                const double f = ld->f_nodal[3 * n + c];
+                if (!std::isfinite(f)) {
+                    err = "cem_init_mesh: non-finite f_nodal";
+                    return CEM_EINVAL;
+                }
+                h.fext[3 * n + c] = h.fext[3 * n + c] + f;
+                any = any || f != 0.0;
+            }
+            if (any) h.nflag[n] |= 8;
         }
     }
     if (ld && ld->n_vbc > 0) {

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s)
     assert set(cem.EXPORTED) == set(declared_symbols())
-    assert cem.abi_version() == 1
+    assert cem.abi_version() == 2
 
 
 def test_library_is_sm100a():
