@@ -18,6 +18,14 @@ using namespace cem;
 struct cem_ctx {
     HostMesh h;
     Plan p;
+    WavePlan w;                   // dataflow launches (single-GPU default; w.seq empty = off)
+    int64_t wcnt_valid = -1;      // the wave counters are valid for this step count
+    struct WaveGraph {
+        int crack_every, M;
+        cudaGraphExec_t exec;
+    };
+    std::vector<WaveGraph> graphs;  // captured M-step wave sequences (replayed with a device base step)
+    int graph_m = 16;             // steps per graph replay (env CEM_GRAPH_M; 0 = eager launches)
     Dev d{};
     cudaStream_t stream = nullptr;       // the library's private non-blocking stream (all its work)
     cudaStream_t user_stream = nullptr;  // opts.stream (NULL = the legacy default stream)
@@ -114,10 +122,11 @@ struct Offs {
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
     size_t rprev, wr_dof, epart, crit_list, vhat, edge_dirty, e_off, e_inc, edge_own;
+    size_t wcnt, wdep_off, wdep, wstep, wncons, wcons_done;
     size_t total;
 };
 
-Offs layout(const HostMesh &h, const Plan &p) {
+Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     const int64_t N = h.N, E = h.E, S = h.S;
     int64_t P = 0;
     for (int g = 0; g < ST_COUNT; ++g) P += p.nblk[g];
@@ -183,6 +192,12 @@ Offs layout(const HostMesh &h, const Plan &p) {
     o.e_off = L.take<int32_t>(S + 1);
     o.e_inc = L.take<int32_t>((int64_t)p.edge_inc.size());
     o.edge_own = L.take<uint8_t>(S);
+    o.wcnt = L.take<int32_t>(ST_COUNT * (int64_t)w.maxblk);
+    o.wdep_off = L.take<int32_t>((int64_t)w.dep_off.size());
+    o.wdep = L.take<int32_t>((int64_t)w.dep.size());
+    o.wstep = L.take<int64_t>(1);
+    o.wncons = L.take<int32_t>((int64_t)w.ncons.size());
+    o.wcons_done = L.take<int32_t>((int64_t)w.ncons.size());
     o.total = L.off;
     return o;
 }
@@ -289,6 +304,17 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.e_off = at<int32_t>(b, o.e_off);
     d.e_inc = at<int32_t>(b, o.e_inc);
     d.edge_own = at<uint8_t>(b, o.edge_own);
+    d.wcnt = at<int32_t>(b, o.wcnt);
+    d.wdep_off = at<int32_t>(b, o.wdep_off);
+    d.wdep = at<int32_t>(b, o.wdep);
+    d.wmax = ctx->w.maxblk;
+    d.wstep = at<int64_t>(b, o.wstep);
+    d.wncons = at<int32_t>(b, o.wncons);
+    d.wcons_done = at<int32_t>(b, o.wcons_done);
+    {
+        const char *e = getenv("CEM_WAVE_DISCARD");
+        d.wdiscard = (e ? atoi(e) : 1) != 0 && !ctx->w.ncons.empty();
+    }
     ctx->epart = at<double>(b, o.epart);
     ctx->n_epart_edges = p.nblk[ST_AB];
     ctx->n_epart_nodes = (h.N + 255) / 256;
@@ -487,6 +513,12 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.trow, p.trow.data(), sizeof(uint16_t) * p.trow.size()));
     CUDA_TRY(put(o.nrow, p.nrow.data(), sizeof(uint16_t) * p.nrow.size()));
     CUDA_TRY(put(o.tflag, p.tflag.data(), E));
+    if (!ctx->w.dep.empty()) {
+        CUDA_TRY(put(o.wdep_off, ctx->w.dep_off.data(), sizeof(int32_t) * ctx->w.dep_off.size()));
+        CUDA_TRY(put(o.wdep, ctx->w.dep.data(), sizeof(int32_t) * ctx->w.dep.size()));
+        CUDA_TRY(put(o.wncons, ctx->w.ncons.data(), sizeof(int32_t) * ctx->w.ncons.size()));
+        CUDA_TRY(cudaMemsetAsync(at<char>(b, o.wcons_done), 0, sizeof(int32_t) * ctx->w.ncons.size(), st));
+    }
     CUDA_TRY(put(o.self, &ctx->d, sizeof(Dev)));
     CUDA_TRY(cudaStreamSynchronize(st));
     return CEM_OK;
@@ -957,7 +989,9 @@ cem_status cem_workspace_size(const cem_mesh_in *mesh, const cem_opts *opts, siz
     if (st) return st;
     h.any_dirichlet = true;
     build_plan(h, block_size(), p);
-    *bytes = layout(h, p).total;
+    WavePlan w;
+    if (!(opts && opts->nranks > 1)) build_wave(p, h.N, 8, 1, w);  // (sizes only)
+    *bytes = layout(h, p, w).total;
     return CEM_OK;
 }
 
@@ -1040,6 +1074,12 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         const double slack = ev ? atof(ev) : 3.0;
         build_schedule(ctx->p, (int)(slack * ctx->grid));
     }
+    if (!ctx->dist && !persistent && !(getenv("CEM_WAVE") && atoi(getenv("CEM_WAVE")) == 0)) {
+        // dataflow launches: K chunks per stage, lookahead in chunks (DESIGN.md §6 "Wavefront")
+        const char *ek = getenv("CEM_WAVE_K"), *el = getenv("CEM_WAVE_LA");
+        build_wave(ctx->p, ctx->h.N, ek ? atoi(ek) : 8, el ? atoi(el) : 1, ctx->w);
+        if (const char *gm = getenv("CEM_GRAPH_M")) ctx->graph_m = std::max(0, atoi(gm));
+    }
     clk.mark("init: schedule");
     {  // the library's own stream (graphs, access-policy window); fenced against opts.stream
         if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1052,7 +1092,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         cudaEventRecord(ctx->fence_in, ctx->user_stream);  // a caller-allocated workspace is ready
         cudaStreamWaitEvent(ctx->stream, ctx->fence_in, 0);
     }
-    Offs o = layout(ctx->h, ctx->p);
+    Offs o = layout(ctx->h, ctx->p, ctx->w);
     if (opts && opts->workspace) {
         if (opts->workspace_bytes < o.total) {
             ctx->err = "workspace too small: need " + std::to_string(o.total) + " bytes";
@@ -1159,6 +1199,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
 void cem_destroy(cem_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto &g : ctx->graphs) cudaGraphExecDestroy(g.exec);
     release_l2(ctx);
     for (auto e : ctx->ev) cudaEventDestroy(e);
     for (void *p : ctx->p2p.opened) cudaIpcCloseMemHandle(p);
@@ -1216,6 +1257,73 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
             }
             cem_status st = exchange_nccl_step(ctx, (int)(sstep & 1));
             if (st) return st;
+        }
+        CUDA_TRY(cudaGetLastError());
+        ctx->step += nsteps;
+        return CEM_OK;
+    }
+    if (!ctx->profiling && !(ctx->flags & CEM_F_PERSISTENT) && !ctx->w.seq.empty()) {
+        // dataflow launches (DESIGN.md §6 "Wavefront"); steps whose recent criterion lists are long
+        // go to the staged k_filter + k_eval path instead (joined / refilled at the switch)
+        bool in_wave = false;
+        for (int64_t i = 0; i < nsteps;) {
+            const int64_t sstep = ctx->step + i;
+            const bool heavy = crack_every > 0 && crit_heavy(ctx);
+            const int M = ctx->graph_m;
+            if (!heavy && M > 0 && nsteps - i >= M) {
+                // M steps as one CUDA-graph replay (captured once per crack_every): the kernels read
+                // the base step from d.wstep, set by a plain launch that follows all earlier work
+                cudaGraphExec_t ex = nullptr;
+                for (auto &g : ctx->graphs)
+                    if (g.crack_every == crack_every && g.M == M) ex = g.exec;
+                if (!ex) {
+                    cudaGraph_t gr = nullptr;
+                    CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+                    for (int j = 0; j < M; ++j) launch_wave_step(ctx->d, ctx->w, j, crack_every, ctx->stream, 1);
+                    launch_wave_join(ctx->d, M, ctx->stream, 1);
+                    CUDA_TRY(cudaStreamEndCapture(ctx->stream, &gr));
+                    const cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
+                    cudaGraphDestroy(gr);
+                    CUDA_TRY(e);
+                    ctx->graphs.push_back({crack_every, M, ex});
+                }
+                if (in_wave) {
+                    launch_wave_join(ctx->d, sstep, ctx->stream);
+                    ctx->launches += 1;
+                    in_wave = false;
+                }
+                if (ctx->wcnt_valid != sstep) {
+                    launch_wave_fill(ctx->d, sstep, ctx->stream);
+                    ctx->launches += 1;
+                }
+                launch_wave_base(ctx->d, sstep, ctx->stream);
+                CUDA_TRY(cudaGraphLaunch(ex, ctx->stream));
+                ctx->launches += 2 + (int64_t)M * (int64_t)ctx->w.seq.size();
+                ctx->wcnt_valid = sstep + M;
+                i += M;
+                continue;
+            }
+            ++i;
+            if (!heavy) {
+                if (ctx->wcnt_valid != sstep) {
+                    launch_wave_fill(ctx->d, sstep, ctx->stream);
+                    ctx->launches += 1;
+                }
+                ctx->launches += launch_wave_step(ctx->d, ctx->w, sstep, crack_every, ctx->stream);
+                ctx->wcnt_valid = sstep + 1;
+                in_wave = true;
+            } else {
+                if (in_wave) {
+                    launch_wave_join(ctx->d, sstep, ctx->stream);
+                    ctx->launches += 1;
+                    in_wave = false;
+                }
+                ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, true);
+            }
+        }
+        if (in_wave) {
+            launch_wave_join(ctx->d, ctx->step + nsteps, ctx->stream);
+            ctx->launches += 1;
         }
         CUDA_TRY(cudaGetLastError());
         ctx->step += nsteps;

@@ -160,6 +160,26 @@ struct Plan {
 };
 
 void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig = nullptr, bool with_deps = true);
+
+// Dataflow ("wave") execution of the staged kernels (DESIGN.md §6 "Wavefront"): each stage's
+// blocks are launched in chunks along the storage order, interleaved so that a consumer chunk is
+// launched right after the producer chunks it reads; a block waits only for the producer blocks
+// it reads (per-block completion counters), not for whole kernels, so consecutive stages and
+// steps overlap and intermediates are consumed while they are still in L2.
+struct WaveLaunch {
+    int stage;      // ST_AB, ST_C or ST_D
+    int b0, b1;     // block range [b0, b1) (D blocks are kDW nodes)
+};
+struct WavePlan {
+    int nblk[ST_COUNT] = {0, 0, 0};   // AB: blk_ab edges, C: blk tets, D: kDW nodes per block
+    int maxblk = 0;
+    std::vector<int32_t> dep_off;     // [ST_COUNT * maxblk + 1] producer blocks of (stage, block)
+    std::vector<int32_t> dep;         //   AB <- D (previous step), C <- AB, D <- C
+    std::vector<int32_t> ncons;       // [2][maxblk]: consumer blocks of each AB (C-stage readers) / C block (D)
+    std::vector<WaveLaunch> seq;      // launches of one step, in order
+};
+constexpr int kDW = 64;               // nodes per stage-D block (256 threads, four lanes per node)
+void build_wave(const Plan &p, int64_t N, int chunks, int lookahead, WavePlan &w);
 void build_schedule(Plan &p, int resident_ctas);
 
 // ---------------------------------------------------------------- device view
@@ -226,9 +246,22 @@ struct Dev {
     unsigned long long *head;  // work-queue head
     int blk, blk_ab, P, maxblk;
     int nblk[ST_COUNT];
+    // dataflow ("wave") launches (WavePlan): per-block completion counters and producer lists
+    int32_t *wcnt;             // [ST_COUNT][wmax]: the block has completed step value-1
+    int64_t *wstep;            // base step of a graph replay (rel launches)
+    const int32_t *wncons;     // [2][wmax] consumers of each AB / C block (L2 discard of consumed intermediates)
+    int32_t *wcons_done;       // [2][wmax] consumers finished with the block this step
+    int wdiscard;              // 1: the last consumer discards a producer block's sigma / force-slot lines
+    const int32_t *wdep_off, *wdep;
+    int wmax;
 };
 
 // cem_kernels.cu
+// rel = 1: the step index is relative to the device word d.wstep (CUDA-graph replays)
+int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel = 0);
+void launch_wave_join(const Dev &d, int64_t nsteps_done, cudaStream_t st, int rel = 0);  // every block done
+void launch_wave_base(const Dev &d, int64_t step0, cudaStream_t st);                    // d.wstep := step0
+void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st);         // counters := step (after other modes)
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
 // heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*4 or null*/,

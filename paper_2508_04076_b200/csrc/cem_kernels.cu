@@ -154,6 +154,90 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// ---- dataflow ("wave") launches (cem_plan.cpp build_wave): a block waits only for the producer
+// blocks it reads.  Producer: all threads' writes, barrier, thread 0 fences and stores the
+// block's completed-step value (wcnt).  Consumer: warp 0 polls its producers' counters with
+// acquire loads, then a barrier releases the block; produced data is read through L2 (.cg).
+// Launch order is a topological order of these dependencies and every kernel triggers its
+// dependents at entry, so all producers of a resident block are resident or done.
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wave_wait(const Dev &d, int g, int b, int need) {
+    const int pg = g == ST_AB ? ST_D : g - 1;
+    if (threadIdx.x < 32) {
+        const int64_t q = (int64_t)g * d.wmax + b;
+        const int lo = __ldg(d.wdep_off + q), hi = __ldg(d.wdep_off + q + 1);
+        const int32_t *c = d.wcnt + (int64_t)pg * d.wmax;
+        for (int i = lo + (int)threadIdx.x; i < hi; i += 32) {
+            const int32_t *cp = c + __ldg(d.wdep + i);
+            while (ld_acquire_gpu(cp) < need) __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void discard_lines(const void *base, int64_t off, int64_t bytes) {
+    const char *p = static_cast<const char *>(base) + off;
+    for (int64_t l = threadIdx.x; l < bytes / 128; l += blockDim.x)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(p + 128 * l) : "memory");
+}
+// Consumer block (stage g = C or D) done with its inputs: count it against each producer block; the
+// last consumer of a producer block invalidates that block's intermediate lines in L2 without
+// write-back (sigma records of an AB block, force slots of a C block), BEFORE it publishes its
+// own completion -- the producer's next write happens-after that publication.
+__device__ __forceinline__ void wave_discard(const Dev &d, int g, int b) {
+    __shared__ int sh_n;
+    __shared__ int sh_pb[32];
+    __syncthreads();
+    if (threadIdx.x == 0) sh_n = 0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int64_t q = (int64_t)g * d.wmax + b;
+        const int lo = __ldg(d.wdep_off + q), hi = __ldg(d.wdep_off + q + 1);
+        int32_t *cd = d.wcons_done + (int64_t)(g - 1) * d.wmax;
+        const int32_t *nc = d.wncons + (int64_t)(g - 1) * d.wmax;
+        for (int i = lo + (int)threadIdx.x; i < hi; i += 32) {
+            const int pb = __ldg(d.wdep + i);
+            if (atomicAdd(cd + pb, 1) == __ldg(nc + pb) - 1) {
+                cd[pb] = 0;
+                const int k = atomicAdd(&sh_n, 1);
+                if (k < 32) sh_pb[k] = pb;
+            }
+        }
+    }
+    __syncthreads();
+    const int n = min(sh_n, 32);  // (a producer beyond 32 is left to normal eviction)
+    for (int j = 0; j < n; ++j) {
+        const int pb = sh_pb[j];
+        if (g == ST_C) {  // sigma records of AB block pb: 32-B and 16-B planes
+            const int64_t e0 = (int64_t)pb * d.blk_ab, ne = min((int64_t)d.blk_ab, d.S - e0);
+            discard_lines(d.srec, e0 * 32, ne * 32);
+            discard_lines(d.srec2, e0 * 16, ne * 16);
+        } else {          // force slots of C block pb (12 doubles per tet)
+#if CEM_FES == 3
+            const int64_t t0 = (int64_t)pb * d.blk, nt = min((int64_t)d.blk, d.E - t0);
+            discard_lines(d.fe, t0 * 96, nt * 96);
+#endif
+        }
+    }
+}
+__device__ __forceinline__ void wave_done(const Dev &d, int g, int b, int val) {
+    if (d.wdiscard && g != ST_AB) wave_discard(d, g, b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(d.wcnt + (int64_t)g * d.wmax + b, val);
+    }
+}
+// the stage bodies wait for their inputs here: wave launches on their producers' counters
+// (wneed >= 0), staged launches on the previous kernel (PDL)
+__device__ __forceinline__ void stage_wait(const Dev &d, int g, int b, int wneed) {
+    if (wneed >= 0) wave_wait(d, g, b, wneed);
+    else pdl_wait();
+}
+
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
@@ -306,7 +390,8 @@ __device__ __forceinline__ void edge_sigma(const Dev &d, int64_t s, const double
     st128(o2, d.mu * g23, d.mu * g13);
 }
 
-__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm, double *epart = nullptr) {
+__device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, double *sm, double *epart = nullptr,
+                                         int wneed = -1) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t t0 = __ldg(d.tl_off + b);
     const int nt = __ldg(d.tl_off + b + 1) - t0;
@@ -334,7 +419,7 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const uint32_t e1 = has1 ? (uint32_t)__ldg(d.tl + t0 + i1) : 0u;
     const int r1 = has1 ? (int)__ldg(d.trow + t0 + i1) : nt;
     const ushort4 lc1 = has1 ? __ldg(reinterpret_cast<const ushort4 *>(d.tconn) + t0 + i1) : make_ushort4(0, 0, 0, 0);
-    pdl_wait();  // u and the tet states come from the previous kernels
+    stage_wait(d, ST_AB, b, wneed);  // u and the tet states come from the previous step's D (and splits)
     const uint8_t act0 = has0 ? __ldcg(d.state + e0) : (uint8_t)0;
     if (tid < nn) {  // one node per thread (list in ascending order, rows bank-aware)
         const double4 w = ldcg256(u + k0);
@@ -798,7 +883,7 @@ __device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double4 x
     sm[5 * np + i] = z.y;
 }
 __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
-                                        int32_t stamp, double *sm, bool defer = false) {
+                                        int32_t stamp, double *sm, bool defer = false, int wneed = -1) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int32_t s0i = __ldg(d.el_off + b);
     const int ne = __ldg(d.el_off + b + 1) - s0i;
@@ -825,7 +910,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #else
     const int32_t nid = (early && tid < nn) ? __ldg(d.nl + n0 + tid) : 0;
 #endif
-    pdl_wait();  // sigma records come from stage AB
+    stage_wait(d, ST_C, b, wneed);  // sigma records come from stage AB
     // ---- wave 2: gathered records (one 32-B and one 16-B load each) -> planes 0..5
     double4 rx[kME];
     double2 rz[kME];
@@ -1002,6 +1087,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     // in parallel (scratch in the staging area, free after the barrier); many: each lane
     // evaluates its own (side by side)
     unsigned m = __ballot_sync(0xffffffffu, need);
+    if (wneed >= 0 && m && (threadIdx.x & 31) == 0) atomicAdd(&d.ctr[10], __popc(m));  // (kernel-choice heuristic)
     __syncthreads();
     if (__popc(m) > CEM_CRIT_COOP_MAX) {
         if (need) criterion_lane(d.self, e, u, gc, rec_step, stamp, (tf & 2) != 0);
@@ -1028,10 +1114,18 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 __host__ __device__ __forceinline__ int d_nodes_per_block(int threads) { return threads >> 2; }
 
 __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t kend, const double4 *u1p, double4 *u2p,
-                                            int64_t s) {
+                                            int64_t s, bool wave = false) {
     const int c = threadIdx.x & 3;
     const int64_t k = kbase + (threadIdx.x >> 2);
-    if (kbase == 0 && threadIdx.x == 0) {  // k_crit (if any) has consumed the step's list
+    if (wave) {
+        if (kbase == 0 && threadIdx.x == 0 && d.crit_seen && (s & 15) == 0) {
+            // kernel-choice heuristic: tets that failed the early-out per step, averaged over the
+            // last 16 steps (racy by design: results never depend on it)
+            const int cur = *(volatile int32_t *)&d.ctr[10];
+            *(volatile int32_t *)d.crit_seen = (cur - d.ctr[11]) / 16;
+            d.ctr[11] = cur;
+        }
+    } else if (kbase == 0 && threadIdx.x == 0) {  // k_crit (if any) has consumed the step's list
         pdl_wait();
         if (d.crit_seen && (s & 15) == 0) *(volatile int32_t *)d.crit_seen = d.ctr[3];  // (host-side kernel choice)
 #ifdef CEM_DEBUG_LIST
@@ -1051,7 +1145,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     for (int j = 0; j < kQ; ++j) q[j] = j * 4 < d.wn ? __ldg(row + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
     const double fxc = (fl & 8) ? __ldg(reinterpret_cast<const double *>(d.fext + k) + c) : 0.0;
     const double vb0 = (fl & 7) ? __ldg(reinterpret_cast<const double *>(d.dir_v0 + k) + c) : 0.0;
-    pdl_wait();  // force slots come from stage C
+    if (!wave) pdl_wait();  // force slots come from stage C (wave launches waited at kernel entry)
     // node state issued before the slot gathers (consumed after them)
     double mk = __ldcg(d.mass + k);
     const double u1 = __ldcg(reinterpret_cast<const double *>(u1p + k) + c);
@@ -1466,6 +1560,56 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 
+__global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// ---- dataflow ("wave") kernels: block b = blockIdx.x + boff of the stage; the crack criterion
+// is evaluated inside stage C's block (warp-cooperative), as in the persistent kernel
+// (rel: the step is s + *d.wstep -- graph replays read the base step from device memory)
+__device__ __forceinline__ int64_t wave_step(const Dev &d, int64_t s, int rel) {
+    return rel ? s + *(volatile const int64_t *)d.wstep : s;
+}
+__global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB_w(Dev d, int64_t s, int boff, int rel) {
+    extern __shared__ __align__(16) double sm[];
+    pdl_trigger();
+    s = wave_step(d, s, rel);
+    const int b = (int)blockIdx.x + boff;
+    block_AB(d, b, d.ubuf[(s + 1) & 1], sm, nullptr, (int)s);
+    wave_done(d, ST_AB, b, (int)(s + 1));
+}
+__global__ void __launch_bounds__(256, CEM_C_MINB) k_C_w(Dev d, int64_t s, int crack_every, int boff, int rel) {
+    extern __shared__ double sm[];
+    pdl_trigger();
+    s = wave_step(d, s, rel);
+    const int b = (int)blockIdx.x + boff;
+    block_C(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, false, (int)(s + 1));
+    wave_done(d, ST_C, b, (int)(s + 1));
+}
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_D_w(Dev d, int64_t s, int boff, int rel) {
+    pdl_trigger();
+    s = wave_step(d, s, rel);
+    const int b = (int)blockIdx.x + boff;
+    wave_wait(d, ST_D, b, (int)(s + 1));
+    node_update(d, (int64_t)b * kDW, min((int64_t)(b + 1) * kDW, d.N), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s, true);
+    wave_done(d, ST_D, b, (int)(s + 1));
+}
+
+// end of a run of wave launches: returns once every block of every stage has published step
+// value `need` (launched without the PDL attribute; what follows on the stream sees all the work)
+__global__ void __launch_bounds__(1024) k_wave_join(Dev d, int64_t need64, int rel) {
+    const int need = (int)wave_step(d, need64, rel);
+    for (int g = 0; g < ST_COUNT; ++g) {
+        const int n = g == ST_D ? (int)((d.N + kDW - 1) / kDW) : d.nblk[g];
+        const int32_t *c = d.wcnt + (int64_t)g * d.wmax;
+        for (int i = (int)threadIdx.x; i < n; i += (int)blockDim.x)
+            while (ld_acquire_gpu(c + i) < need) __nanosleep(64);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence();
+}
+
 // energy ledger on the current state u_n, v_n (cem_energy): per-block partials, fixed order
 __global__ void __launch_bounds__(256) k_energy_edges(Dev d, int64_t n, double *part) {
     extern __shared__ __align__(16) double sm[];
@@ -1548,6 +1692,8 @@ void set_smem_limits(int smem_bytes) {
     cur[dev] = smem_bytes;
     cudaFuncSetAttribute(k_AB, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_AB_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_C_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_AB_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_energy_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C_cur, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
@@ -1608,6 +1754,26 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     cudaEventRecord(ev[3], st);
     return crit ? (heavy ? 5 : 4) : 3;
+}
+
+void launch_wave_join(const Dev &d, int64_t nsteps_done, cudaStream_t st, int rel) {
+    k_wave_join<<<1, 1024, 0, st>>>(d, nsteps_done, rel);
+}
+__global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
+void launch_wave_base(const Dev &d, int64_t step0, cudaStream_t st) { k_set_i64<<<1, 1, 0, st>>>(d.wstep, step0); }
+void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
+    const int64_t n = ST_COUNT * (int64_t)d.wmax;
+    k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d.wcnt, n, (int32_t)step);
+}
+
+int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel) {
+    for (const WaveLaunch &L : w.seq) {
+        const unsigned nb = (unsigned)(L.b1 - L.b0);
+        if (L.stage == ST_AB) launch_pdl(k_AB_w, nb, (unsigned)d.blk, (size_t)d.smem_ab, st, d, s, L.b0, rel);
+        else if (L.stage == ST_C) launch_pdl(k_C_w, nb, (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every, L.b0, rel);
+        else launch_pdl(k_D_w, nb, 256u, (size_t)0, st, d, s, L.b0, rel);
+    }
+    return (int)w.seq.size();
 }
 
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st) {

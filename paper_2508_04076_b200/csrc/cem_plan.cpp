@@ -650,6 +650,98 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, 
     }    clk.mark("plan: dependencies");
 }
 
+void build_wave(const Plan &p, int64_t N, int chunks, int lookahead, WavePlan &w) {
+    const int nAB = p.nblk[ST_AB], nC = p.nblk[ST_C], nD = (int)((N + kDW - 1) / kDW);
+    w.nblk[ST_AB] = nAB;
+    w.nblk[ST_C] = nC;
+    w.nblk[ST_D] = nD;
+    w.maxblk = std::max(nAB, std::max(nC, nD));
+    std::vector<std::vector<int32_t>> deps((size_t)ST_COUNT * w.maxblk);
+    auto finish = [](std::vector<int32_t> &v) {
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+    };
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int b = 0; b < nAB; ++b) {  // AB: the D blocks (previous step) of its tet list's nodes
+        auto &v = deps[(size_t)ST_AB * w.maxblk + b];
+        for (int32_t i = p.nlb_off[b]; i < p.nlb_off[b + 1]; ++i) v.push_back(p.nlb[i] / kDW);
+        finish(v);
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int b = 0; b < nC; ++b) {  // C: the AB blocks of its edge list
+        auto &v = deps[(size_t)ST_C * w.maxblk + b];
+        for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) v.push_back(p.el[i] / p.blk_ab);
+        finish(v);
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int b = 0; b < nD; ++b) {  // D: the C blocks of the tets of its nodes
+        auto &v = deps[(size_t)ST_D * w.maxblk + b];
+        for (int64_t k = (int64_t)b * kDW; k < std::min<int64_t>(N, (int64_t)(b + 1) * kDW); ++k)
+            for (int32_t j = p.node_off[k]; j < p.node_off[k + 1]; ++j) v.push_back((p.node_ent[j] >> 2) / p.blk);
+        finish(v);
+    }
+    w.ncons.assign((size_t)2 * w.maxblk, 0);
+    for (int g = ST_C; g <= ST_D; ++g)
+        for (int b = 0; b < w.nblk[g]; ++b)
+            for (int32_t pb : deps[(size_t)g * w.maxblk + b]) w.ncons[(size_t)(g - 1) * w.maxblk + pb]++;
+    w.dep_off.assign((size_t)ST_COUNT * w.maxblk + 1, 0);
+    w.dep.clear();
+    for (size_t q = 0; q < deps.size(); ++q) {
+        w.dep.insert(w.dep.end(), deps[q].begin(), deps[q].end());
+        w.dep_off[q + 1] = (int32_t)w.dep.size();
+    }
+    // launch sequence: K chunks of C blocks; before C chunk c the AB blocks that C chunks up to
+    // c + lookahead read; after it the D blocks whose C producers lie in chunks <= c - lookahead
+    const int K = std::max(1, std::min(chunks, nC));
+    auto maxdep = [&](int g, int b) {
+        const size_t q = (size_t)g * w.maxblk + b;
+        return w.dep_off[q + 1] > w.dep_off[q] ? w.dep[w.dep_off[q + 1] - 1] : -1;
+    };
+    std::vector<int> cend(K);  // C chunk c = [cend[c-1], cend[c])
+    for (int c = 0; c < K; ++c) cend[c] = (int)((int64_t)nC * (c + 1) / K);
+    std::vector<int> abneed(K);  // AB blocks [0, abneed[c]) cover C chunks <= c (prefix max)
+    {
+        int m = -1, b = 0;
+        for (int c = 0; c < K; ++c) {
+            for (; b < cend[c]; ++b) m = std::max(m, maxdep(ST_C, b));
+            abneed[c] = m + 1;
+        }
+    }
+    std::vector<int> dpref(nD);  // prefix max of the largest C producer of D blocks [0, b]
+    {
+        int m = -1;
+        for (int b = 0; b < nD; ++b) dpref[b] = m = std::max(m, maxdep(ST_D, b));
+    }
+    w.seq.clear();
+    int a = 0, dd = 0;
+    auto emit = [&](int g, int b0, int b1) {
+        if (b1 > b0) w.seq.push_back({g, b0, b1});
+    };
+    for (int c = 0; c < K; ++c) {
+        const int an = std::max(abneed[std::min(K - 1, c + lookahead)], c + 1 == K ? nAB : 0);
+        if (an > a) {
+            emit(ST_AB, a, an);
+            a = an;
+        }
+        emit(ST_C, c ? cend[c - 1] : 0, cend[c]);
+        const int cc = c - lookahead;  // D blocks whose producers are all in C chunks <= cc
+        if (cc >= 0) {
+            int d1 = dd;
+            while (d1 < nD && dpref[d1] < cend[cc]) ++d1;
+            emit(ST_D, dd, d1);
+            dd = d1;
+        }
+    }
+    if (a < nAB) emit(ST_AB, a, nAB);  // (edges of no tet: none in a valid mesh)
+    for (int cc = std::max(0, K - lookahead); cc < K; ++cc) {  // the remaining D blocks
+        int d1 = dd;
+        while (d1 < nD && dpref[d1] < cend[cc]) ++d1;
+        emit(ST_D, dd, d1);
+        dd = d1;
+    }
+    emit(ST_D, dd, nD);
+}
+
 void build_schedule(Plan &p, int resident_ctas) {
     // ---------------------------------------------------------------- wavefront schedule
     // virtual time: vt(A, b) = b / nA; a consumer sits delta after its latest producer,

@@ -74,10 +74,12 @@ def test_front_both_stretched_variant_bitwise(case, critb_min, monkeypatch):
     sim, orc = _pair(p, steps, 1, flags=cem.CEM_F_FRONT_BOTH_STRETCHED)
     g = assert_parity(sim, orc, p)
     assert g.rec_elem.size > 0
-    # the variant is a different reading: it changes the records somewhere (non-vacuous)
-    ref = oracle.Oracle(p).run(steps, 1).records()
-    assert not (np.array_equal(ref.elem, g.rec_elem) and np.array_equal(ref.cand, g.rec_cand)
-                and np.array_equal(ref.G, g.rec_G))
+    if case == "cfg0":
+        # the variant is a different reading: on config 0 it changes the records (non-vacuous);
+        # on the pre-damaged block (Gc_e = 0) the winning candidates have both fronts stretched
+        ref = oracle.Oracle(p).run(steps, 1).records()
+        assert not (np.array_equal(ref.elem, g.rec_elem) and np.array_equal(ref.cand, g.rec_cand)
+                    and np.array_equal(ref.G, g.rec_G))
 
 
 @pytest.mark.parametrize("critb_min", ["1024", "0"])
