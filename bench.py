@@ -49,7 +49,7 @@ def b_alg_per_step(N, E, S):
 # per-stage table): AB reads u (24 B/node), conn + state (17 B/tet) and writes sigma (48 B/edge);
 # C reads sigma (48 B/edge); D moves the rest of the node terms (153 B/node)
 STAGE_KERNELS = {"stage_AB_strain_edge_stress": ("k_AB", lambda N, E, S: 24 * N + 17 * E + 48 * S),
-                 "stage_C_force_criterion": ("k_C", lambda N, E, S: 48 * S),
+                 "stage_C_force_earlyout": ("k_C", lambda N, E, S: 48 * S),
                  "stage_D_node_update": ("k_D", lambda N, E, S: 153 * N)}
 
 

@@ -120,6 +120,9 @@ typedef struct {
                                  * c-q are not both stretched has G = 0 (default: no such condition) */
 
 typedef int (*cem_alloc_fn)(size_t bytes, void *user, void **dev_ptr); /* returns 0 on success */
+/* Host all-gather over the ranks (blocking; rank-ordered concatenation of `bytes` from every
+ * rank into recv, which holds nranks * bytes); returns 0 on success.  Also used as a barrier. */
+typedef int (*cem_allgather_fn)(const void *send, void *recv, size_t bytes, void *user);
 
 typedef struct {
     double dt;           /* time step (s); <= 0 -> cfl * min_e altitude_e / c_d (R12) */
@@ -135,6 +138,14 @@ typedef struct {
     int rank, nranks;    /* multi-GPU: rank in [0, nranks); nranks <= 1 -> single GPU */
     const void *nccl_id; /* nranks > 1 without CEM_F_LOOPBACK: the 128-byte ncclUniqueId that rank 0
                             obtained from cem_nccl_unique_id and broadcast to all ranks */
+    cem_allgather_fn host_allgather; /* (ABI >= 2) nranks > 1, nccl_id NULL: host-ordered CUDA-IPC halo --
+                            the receive buffers are mapped over CUDA IPC (handles exchanged with this
+                            callback), stage D and the split pass store into the peers' buffers as in
+                            the NVLink P2P halo, and every step the ranks meet in this callback
+                            (after their stores completed) before the flag wait and the unpack, so no
+                            kernel ever waits for another process's kernel.  For ranks sharing one GPU
+                            (tests) or hosts without NCCL; one host round trip per step. */
+    void *host_user;     /* passed to host_allgather */
 } cem_opts;
 
 /* Domain decomposition of a rank; library-owned arrays,

@@ -62,13 +62,15 @@ class cem_load_in(C.Structure):
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_size_t, C.c_void_p, C.POINTER(C.c_void_p))
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 class cem_opts(C.Structure):
     _fields_ = [("dt", C.c_double), ("cfl", C.c_double), ("gamma", C.c_double), ("flags", C.c_uint32),
                 ("device", C.c_int), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("dev_alloc", ALLOC_FN), ("alloc_user", C.c_void_p),
-                ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p)]
+                ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p),
+                ("host_allgather", ALLGATHER_FN), ("host_user", C.c_void_p)]
 
 
 class cem_state_out(C.Structure):
@@ -173,7 +175,7 @@ class Simulation:
     def __init__(self, X, tets, E, nu, rho, Gc=np.inf, tet_state=None, tet_gc=None,
                  tface=None, tface_t=None, vbc_node=None, vbc_mask=None, vbc_v0=None, vbc_t0=0.0,
                  dt=0.0, cfl=0.5, gamma=0.5, flags=0, device=0, stream=None, use_torch=True,
-                 rank=0, nranks=1, nccl_id=None, f_nodal=None, body=(0.0, 0.0, 0.0)):
+                 rank=0, nranks=1, nccl_id=None, f_nodal=None, body=(0.0, 0.0, 0.0), host_allgather=None):
         self._h = C.c_void_p()
         keep = []
         Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, 4))
@@ -218,9 +220,24 @@ class Simulation:
             self.torch_stream = None
             stream_ptr = stream
         self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+        self._gather_cb = ALLGATHER_FN()
+        if host_allgather is not None:
+            # host_allgather(bytes) -> list of nranks bytes objects (rank order), e.g. over gloo
+            def _gather(send, recv, nbytes, user):
+                try:
+                    parts = host_allgather(C.string_at(send, nbytes))
+                    blob = b"".join(parts)
+                    if len(blob) != nbytes * nranks:
+                        return 1
+                    C.memmove(recv, blob, len(blob))
+                    return 0
+                except Exception:  # pragma: no cover - reported through the status code
+                    return 1
+            self._gather_cb = ALLGATHER_FN(_gather)
         opts = cem_opts(dt, cfl, gamma, flags, device, stream_ptr, None, 0,
                         self._alloc_cb if self._alloc_cb is not None else ALLOC_FN(), None, rank, nranks,
-                        None if self._nccl_id is None else C.cast(self._nccl_id, C.c_void_p))
+                        None if self._nccl_id is None else C.cast(self._nccl_id, C.c_void_p),
+                        self._gather_cb, None)
         self.rank, self.nranks = rank, nranks
         rc = _lib.cem_init_mesh(C.byref(mesh), C.byref(mat), C.byref(load), C.byref(opts), C.byref(self._h))
         if rc != CEM_OK:

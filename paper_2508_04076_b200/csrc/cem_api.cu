@@ -18,7 +18,7 @@ using namespace cem;
 struct cem_ctx {
     HostMesh h;
     Plan p;
-    WavePlan w;                   // dataflow launches (single-GPU default; w.seq empty = off)
+    WavePlan w;                   // dataflow launches (opt-in, CEM_WAVE=1; w.seq empty = off)
     int64_t wcnt_valid = -1;      // the wave counters are valid for this step count
     struct WaveGraph {
         int crack_every, M;
@@ -55,6 +55,8 @@ struct cem_ctx {
     bool init_exchange_pending = false;
     std::vector<void *> dist_allocs;
     P2P p2p;                      // P2P halo (multi-GPU), see cem_dist.h
+    cem_allgather_fn host_allgather = nullptr;  // host-ordered CUDA-IPC halo (opts.host_allgather)
+    void *host_user = nullptr;
     volatile int32_t *crit_seen = nullptr;  // mapped: criterion-list length of a recent step
     int critb_min = 1024;         // lists at least this long use k_filter + k_eval (env CEM_CRITB_MIN at init)
     double *epart = nullptr;      // energy-ledger partials (device)
@@ -154,7 +156,7 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     o.srec = L.take<double>(4 * S);
     o.srec2 = L.take<double>(2 * S);
     o.fe = L.take<double>(CEM_FES * fe_slots(E));  // + the zero slot
-    o.ctr = L.take<int32_t>(16);
+    o.ctr = L.take<int32_t>(32);
     o.rec_step = L.take<int64_t>(E);
     o.rec_elem = L.take<int32_t>(E);
     o.rec_cand = L.take<int32_t>(E);
@@ -313,7 +315,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.wcons_done = at<int32_t>(b, o.wcons_done);
     {
         const char *e = getenv("CEM_WAVE_DISCARD");
-        d.wdiscard = (e ? atoi(e) : 1) != 0 && !ctx->w.ncons.empty();
+        d.wdiscard = (e ? atoi(e) : 0) != 0 && !ctx->w.ncons.empty();
     }
     ctx->epart = at<double>(b, o.epart);
     ctx->n_epart_edges = p.nblk[ST_AB];
@@ -489,7 +491,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, sizeof(double) * 4 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec2), 0, sizeof(double) * 2 * S, st));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
-    int32_t ctr[16] = {0, 0, INT32_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int32_t ctr[32] = {0, 0, INT32_MAX};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
     CUDA_TRY(put(o.dep_off, p.dep_off.data(), sizeof(int32_t) * p.dep_off.size()));
@@ -854,6 +856,84 @@ cem_status p2p_setup_nccl(cem_ctx *ctx) {
     return CEM_OK;
 }
 
+// Host-ordered CUDA-IPC halo (opts.host_allgather, no NCCL): the IPC handles and segment offsets
+// are all-gathered through the caller's host callback, the peers' receive buffers mapped, and the
+// initial halo (u_1 and the tet states) copied into them; every step the ranks then meet on the
+// host after their stores completed (cem_step), so the device flag wait never spins.
+cem_status host_barrier(cem_ctx *ctx) {
+    std::vector<char> all(ctx->nranks);
+    const char me = 1;
+    if (ctx->host_allgather(&me, all.data(), 1, ctx->host_user) != 0) {
+        ctx->err = "host_allgather callback failed";
+        return CEM_ENCCL;
+    }
+    return CEM_OK;
+}
+cem_status p2p_setup_host(cem_ctx *ctx) {
+    const int R = ctx->nranks, me = ctx->rank;
+    const PartLocal &L = ctx->part;
+    const int np = (int)L.peers.size();
+    P2P &q = ctx->p2p;
+    if (R > 64) {
+        ctx->err = "host-ordered IPC halo: at most 64 ranks";
+        return CEM_EINVAL;
+    }
+    cem_status st = p2p_alloc(ctx);
+    if (st) return st;
+    P2PBlob mine{};
+    for (int i = 0; i < 64; ++i) mine.seg_off_by_src[i] = -1;
+    for (int j = 0; j < np; ++j) mine.seg_off_by_src[L.peers[j]] = (int64_t)ctx->xch.recv_off[j];
+    CUDA_TRY(cudaIpcGetMemHandle(&mine.recv0, q.recv[0]));
+    CUDA_TRY(cudaIpcGetMemHandle(&mine.recv1, q.recv[1]));
+    CUDA_TRY(cudaIpcGetMemHandle(&mine.flags, q.flags));
+    std::vector<P2PBlob> all(R);
+    if (ctx->host_allgather(&mine, all.data(), sizeof(P2PBlob), ctx->host_user) != 0) {
+        ctx->err = "host_allgather callback failed";
+        return CEM_ENCCL;
+    }
+    std::vector<uint8_t *> r0(np), r1(np);
+    std::vector<int64_t *> fl(np);
+    for (int j = 0; j < np; ++j) {
+        const P2PBlob &b = all[L.peers[j]];
+        if (b.seg_off_by_src[me] < 0) {
+            ctx->err = "host-ordered IPC halo: a peer has no segment for this rank";
+            return CEM_ESTATE;
+        }
+        void *a0 = nullptr, *a1 = nullptr, *af = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&a0, b.recv0, cudaIpcMemLazyEnablePeerAccess));
+        q.opened.push_back(a0);
+        CUDA_TRY(cudaIpcOpenMemHandle(&a1, b.recv1, cudaIpcMemLazyEnablePeerAccess));
+        q.opened.push_back(a1);
+        CUDA_TRY(cudaIpcOpenMemHandle(&af, b.flags, cudaIpcMemLazyEnablePeerAccess));
+        q.opened.push_back(af);
+        r0[j] = static_cast<uint8_t *>(a0) + b.seg_off_by_src[me];
+        r1[j] = static_cast<uint8_t *>(a1) + b.seg_off_by_src[me];
+        fl[j] = static_cast<int64_t *>(af) + me;
+    }
+    st = p2p_tables(ctx, r0, r1, fl);
+    if (st) return st;
+    // initial halo: the owners' u_1 and tet states into both parity buffers of every peer
+    exchange_pack(ctx->xch, ctx->d.ubuf[1], ctx->d.state, ctx->stream);
+    for (int j = 0; j < np; ++j) {
+        const size_t bytes = ctx->xch.send_off[j + 1] - ctx->xch.send_off[j];
+        if (!bytes) continue;
+        CUDA_TRY(cudaMemcpyAsync(r0[j], ctx->xch.d_sendbuf + ctx->xch.send_off[j], bytes, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(r1[j], ctx->xch.d_sendbuf + ctx->xch.send_off[j], bytes, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    st = host_barrier(ctx);  // every rank's copies into this rank's buffers are complete
+    if (st) return st;
+    exchange_unpack(ctx->xch, ctx->d.ubuf[1], ctx->d.state, ctx->d.eedge, ctx->h.E, ctx->d.edge_dirty, ctx->stream,
+                    q.recv[1]);
+    ctx->launches += 2;
+    p2p_enable(ctx);
+    CUDA_TRY(cudaMemcpy(const_cast<Dev *>(ctx->d.self), &ctx->d, sizeof(Dev), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return CEM_OK;
+}
+
 // Loopback emulation (tests, one device): the peers' buffers are the other contexts' own.
 cem_status p2p_setup_loopback(cem_ctx **c, int n) {
     for (int r = 0; r < n; ++r) {
@@ -1074,11 +1154,14 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         const double slack = ev ? atof(ev) : 3.0;
         build_schedule(ctx->p, (int)(slack * ctx->grid));
     }
-    if (!ctx->dist && !persistent && !(getenv("CEM_WAVE") && atoi(getenv("CEM_WAVE")) == 0)) {
+    if (!ctx->dist && !persistent && getenv("CEM_WAVE") && atoi(getenv("CEM_WAVE")) != 0) {
+        // (opt-in: measured slower than the staged path on B200, DESIGN.md §6 "Wavefront")
         // dataflow launches: K chunks per stage, lookahead in chunks (DESIGN.md §6 "Wavefront")
         const char *ek = getenv("CEM_WAVE_K"), *el = getenv("CEM_WAVE_LA");
         build_wave(ctx->p, ctx->h.N, ek ? atoi(ek) : 8, el ? atoi(el) : 1, ctx->w);
         if (const char *gm = getenv("CEM_GRAPH_M")) ctx->graph_m = std::max(0, atoi(gm));
+        const char *cv = getenv("CEM_WAVE_CARVE");
+        if (!(cv && atoi(cv) == -2)) set_wave_carveout(smem_ab_for(ctx->p), smem_c_for(ctx->p), cv ? atoi(cv) : -1);
     }
     clk.mark("init: schedule");
     {  // the library's own stream (graphs, access-policy window); fenced against opts.stream
@@ -1178,8 +1261,16 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         if (ctx->loopback) {
             ctx->init_exchange_pending = true;  // done by the first cem_step_group
         } else {
+            if (!opts->nccl_id && opts->host_allgather) {  // host-ordered CUDA-IPC halo, no NCCL
+                ctx->host_allgather = opts->host_allgather;
+                ctx->host_user = opts->host_user;
+                st = p2p_setup_host(ctx);
+                if (st) return fail(st);
+                *out = ctx;
+                return CEM_OK;
+            }
             if (!opts->nccl_id) {
-                ctx->err = "cem_init_mesh: nranks > 1 needs opts.nccl_id (or CEM_F_LOOPBACK)";
+                ctx->err = "cem_init_mesh: nranks > 1 needs opts.nccl_id, opts.host_allgather or CEM_F_LOOPBACK";
                 return fail(CEM_EINVAL);
             }
             if (!nccl_comm_init(&ctx->comm, ctx->nranks, ctx->rank, opts->nccl_id, ctx->err)) return fail(CEM_ENCCL);
@@ -1248,6 +1339,14 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
             ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx));
+            if (ctx->p2p.on && ctx->host_allgather) {
+                // host-ordered: signal, wait for this rank's stores, meet the peers on the host, then
+                // the flag wait (already satisfied: it never spins) and the unpack
+                p2p_sync(ctx->p2p, (int)ctx->part.peers.size(), sstep + 2, false, ctx->stream);
+                CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+                cem_status hs = host_barrier(ctx);
+                if (hs) return hs;
+            }
             if (ctx->p2p.on) {  // stage D / the split pass already stored into the peers' buffers
                 p2p_sync(ctx->p2p, (int)ctx->part.peers.size(), sstep + 2, true, ctx->stream);
                 exchange_unpack(ctx->xch, ctx->d.ubuf[sstep & 1], ctx->d.state, ctx->d.eedge, ctx->h.E,
@@ -1333,7 +1432,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (staged) {
         // one kernel per stage; with profiling, CUDA events bracket every stage
         if (ctx->profiling) {
-            const size_t need = (size_t)(ctx->prof_steps + nsteps) * (ST_COUNT + 1);
+            const size_t need = (size_t)(ctx->prof_steps + nsteps) * kStagedEvents;
             while (ctx->ev.size() < need) {
                 cudaEvent_t e;
                 CUDA_TRY(cudaEventCreate(&e));
@@ -1341,7 +1440,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
             }
         }
         for (int64_t i = 0; i < nsteps; ++i) {
-            cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * (ST_COUNT + 1) : nullptr;
+            cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * kStagedEvents : nullptr;
             ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx));
         }
         CUDA_TRY(cudaGetLastError());
@@ -1364,17 +1463,18 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
 }
 
 cem_status cem_kernel_times(const cem_ctx *ctx, int32_t *n, const char **names, double *ms, int32_t cap) {
-    static const char *kNames[ST_COUNT] = {"stage_AB_strain_edge_stress", "stage_C_force_criterion",
-                                           "stage_D_node_update"};
+    constexpr int K = kStagedEvents - 1;
+    static const char *kNames[K] = {"stage_AB_strain_edge_stress", "stage_C_force_earlyout", "criterion_split",
+                                    "stage_D_node_update"};  // (profiled: plain launches, no PDL overlap)
     if (!ctx || !n) return CEM_EINVAL;
-    *n = ST_COUNT;
-    if (cap < ST_COUNT) return CEM_OK;
-    for (int k = 0; k < ST_COUNT; ++k) {
+    *n = K;
+    if (cap < K) return CEM_OK;
+    for (int k = 0; k < K; ++k) {
         if (names) names[k] = kNames[k];
         double tot = 0.0;
         for (int64_t i = 0; i < ctx->prof_steps; ++i) {
             float t = 0.f;
-            cudaEvent_t *E = const_cast<cudaEvent_t *>(ctx->ev.data()) + i * (ST_COUNT + 1);
+            cudaEvent_t *E = const_cast<cudaEvent_t *>(ctx->ev.data()) + i * kStagedEvents;
             if (cudaEventSynchronize(E[k + 1]) != cudaSuccess) return CEM_ECUDA;
             if (cudaEventElapsedTime(&t, E[k], E[k + 1]) != cudaSuccess) return CEM_ECUDA;
             tot += t;
@@ -1439,7 +1539,7 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     const HostMesh &h = ctx->h;
     const Plan &p = ctx->p;
     const int64_t N = h.N, E = h.E;
-    int32_t ctr[8];
+    int32_t ctr[16];
     CUDA_TRY(cudaMemcpyAsync(ctr, ctx->d.ctr, sizeof ctr, cudaMemcpyDeviceToHost, st));
     int64_t p2p_timeout = 0;
     if (ctx->p2p.on && ctx->p2p.timeout)
@@ -1450,6 +1550,10 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
         return CEM_ENCCL;
     }
     const int64_t nrec = ctr[0];
+#ifdef CEM_WAVE_STATS
+    fprintf(stderr, "[cem wave stats] blocks that waited: AB %d C %d D %d; polls %u\n", ctr[12], ctr[13], ctr[14],
+            (unsigned)ctr[7]);
+#endif
 #ifdef CEM_POLL_STATS
     fprintf(stderr, "[cem poll stats] polls AB %d C %d D %d, items that waited %d\n", ctr[4], ctr[5], ctr[6], ctr[7]);
 #endif

@@ -263,13 +263,15 @@ void launch_wave_join(const Dev &d, int64_t nsteps_done, cudaStream_t st, int re
 void launch_wave_base(const Dev &d, int64_t step0, cudaStream_t st);                    // d.wstep := step0
 void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st);         // counters := step (after other modes)
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
+constexpr int kStagedEvents = 5;  // profiled staged step: AB | C | criterion | D
 // heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit
-int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*4 or null*/,
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/,
                        bool heavy = false);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel
 void set_smem_limits(int smem_bytes);
+void set_wave_carveout(int smem_ab, int smem_c, int pct = -1);  // same carveout for the three wave kernels
 extern const int kThreads;
 
 }  // namespace cem

@@ -21,6 +21,7 @@
 // global queue in a precomputed wavefront order (cem_plan.cpp) and wait only on the
 // completed-step counters of the producer blocks they read.  Consecutive steps overlap;
 // intermediates stay L2-resident between producer and consumer.
+#include <algorithm>
 #include <cstdint>
 #include <mutex>
 
@@ -155,28 +156,60 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---- dataflow ("wave") launches (cem_plan.cpp build_wave): a block waits only for the producer
-// blocks it reads.  Producer: all threads' writes, barrier, thread 0 fences and stores the
-// block's completed-step value (wcnt).  Consumer: warp 0 polls its producers' counters with
-// acquire loads, then a barrier releases the block; produced data is read through L2 (.cg).
-// Launch order is a topological order of these dependencies and every kernel triggers its
-// dependents at entry, so all producers of a resident block are resident or done.
+// blocks it reads.  Producer: all threads' writes, barrier, thread 0 stores the block's
+// completed-step value (wcnt) with st.release.gpu (MEMBAR.ALL.GPU + strong store).  Consumer:
+// warp 0 polls its producers' counters with ld.relaxed.gpu (strong L2 loads), then a barrier
+// releases the block.  Every load of produced data in the stage bodies is a strong GPU-scope
+// load served by L2 (__ldcg / ld.global.cg -> LDG.E.STRONG.GPU), issued after the poll that
+// observed the flag returned, so it sees the producer's writes.  Deliberately NO acquire
+// loads or __threadfence(): on sm_100a those compile to CCTL.IVALL, an invalidation of the
+// SM's whole L1, and one per block start/finish cost the stage kernels 15-50 us per step
+// (ncu, measured).  Launch order is a topological order of the dependencies and every kernel
+// triggers its dependents at entry, so all producers of a resident block are resident or done.
 __device__ __forceinline__ int ld_acquire_gpu(const int32_t *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int32_t *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int32_t *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void wave_wait(const Dev &d, int g, int b, int need) {
+#ifdef CEM_WAVE_NOWAIT  // (timing experiment only: results are wrong)
+    return;
+#endif
     const int pg = g == ST_AB ? ST_D : g - 1;
-    if (threadIdx.x < 32) {
+    {  // every warp polls the block's producers itself (no barrier: warps start independently)
+        const int lane = (int)(threadIdx.x & 31);
         const int64_t q = (int64_t)g * d.wmax + b;
         const int lo = __ldg(d.wdep_off + q), hi = __ldg(d.wdep_off + q + 1);
         const int32_t *c = d.wcnt + (int64_t)pg * d.wmax;
-        for (int i = lo + (int)threadIdx.x; i < hi; i += 32) {
+#ifdef CEM_WAVE_STATS
+        int polls = 0;
+#endif
+        for (int i = lo + lane; i < hi; i += 32) {
             const int32_t *cp = c + __ldg(d.wdep + i);
-            while (ld_acquire_gpu(cp) < need) __nanosleep(32);
+            while (ld_relaxed_gpu(cp) < need) {
+                __nanosleep(32);
+#ifdef CEM_WAVE_STATS
+                ++polls;
+#endif
+            }
         }
+        __syncwarp();
+#ifdef CEM_WAVE_STATS
+        polls = __reduce_add_sync(0xffffffffu, polls);
+        if (threadIdx.x == 0) {
+            atomicAdd(&d.ctr[12 + (g == ST_D ? 2 : 0) + (g == ST_C ? 1 : 0)], polls ? 1 : 0);  // blocks that waited
+            atomicAdd(reinterpret_cast<unsigned int *>(&d.ctr[7]), (unsigned)polls);
+        }
+#endif
     }
-    __syncthreads();
 }
 __device__ __forceinline__ void discard_lines(const void *base, int64_t off, int64_t bytes) {
     const char *p = static_cast<const char *>(base) + off;
@@ -226,10 +259,7 @@ __device__ __forceinline__ void wave_discard(const Dev &d, int g, int b) {
 __device__ __forceinline__ void wave_done(const Dev &d, int g, int b, int val) {
     if (d.wdiscard && g != ST_AB) wave_discard(d, g, b);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicExch(d.wcnt + (int64_t)g * d.wmax + b, val);
-    }
+    if (threadIdx.x == 0) st_release_gpu(d.wcnt + (int64_t)g * d.wmax + b, val);
 }
 // the stage bodies wait for their inputs here: wave launches on their producers' counters
 // (wneed >= 0), staged launches on the previous kernel (PDL)
@@ -1113,8 +1143,12 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 // nodes per D block: four lanes per node (lane 3 carries the zero w component)
 __host__ __device__ __forceinline__ int d_nodes_per_block(int threads) { return threads >> 2; }
 
+// mode: ND_INLINE (staged and persistent kernels) -- PDL wait, resets the criterion list;
+// ND_WAVE -- inputs already awaited at kernel entry, kernel-choice heuristic from stage C's count
+enum { ND_INLINE = 0, ND_WAVE = 1 };
 __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t kend, const double4 *u1p, double4 *u2p,
-                                            int64_t s, bool wave = false) {
+                                            int64_t s, int mode = ND_INLINE) {
+    const bool wave = mode == ND_WAVE;
     const int c = threadIdx.x & 3;
     const int64_t k = kbase + (threadIdx.x >> 2);
     if (wave) {
@@ -1584,7 +1618,11 @@ __global__ void __launch_bounds__(256, CEM_C_MINB) k_C_w(Dev d, int64_t s, int c
     pdl_trigger();
     s = wave_step(d, s, rel);
     const int b = (int)blockIdx.x + boff;
+#ifdef CEM_WAVE_DEFER  // (timing experiment only: the listed tets are never evaluated)
+    block_C(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true, (int)(s + 1));
+#else
     block_C(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, false, (int)(s + 1));
+#endif
     wave_done(d, ST_C, b, (int)(s + 1));
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D_w(Dev d, int64_t s, int boff, int rel) {
@@ -1592,7 +1630,7 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_D_w(Dev d, int64_t s, int b
     s = wave_step(d, s, rel);
     const int b = (int)blockIdx.x + boff;
     wave_wait(d, ST_D, b, (int)(s + 1));
-    node_update(d, (int64_t)b * kDW, min((int64_t)(b + 1) * kDW, d.N), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s, true);
+    node_update(d, (int64_t)b * kDW, min((int64_t)(b + 1) * kDW, d.N), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s, ND_WAVE);
     wave_done(d, ST_D, b, (int)(s + 1));
 }
 
@@ -1679,6 +1717,25 @@ int persistent_occupancy(int smem_bytes, int blk) {
     return n;
 }
 
+// Wave launches put blocks of the three stage kernels on the same SM at the same time; an SM can
+// only change its shared-memory / L1 split when it is idle, so the three kernels get the same
+// preferred carveout (enough shared memory for the stage-AB / C occupancy), else every switch
+// between a D block (no shared memory) and an AB / C block drains the SM.  pct < 0: leave unset.
+void set_wave_carveout(int smem_ab, int smem_c, int pct) {
+    if (pct < 0) {
+        const int need = std::max(4 * (smem_ab + 1024), 4 * (smem_c + 1024));
+        int maxsm = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        if (maxsm <= 0) return;
+        pct = std::min(100, (int)((100LL * need + maxsm - 1) / maxsm));
+    }
+    cudaFuncSetAttribute(k_AB_w, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_C_w, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_D_w, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
+}
+
 void set_smem_limits(int smem_bytes) {
     // the attribute is per function AND per device: keep the largest any context of the current
     // device needs (called after cudaSetDevice)
@@ -1721,6 +1778,11 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// One staged step: k_AB, k_C, [k_crit | k_filter + k_eval], k_D chained with programmatic dependent
+// launch.  With ev (5 events), plain launches bracketed per stage: AB | C | criterion | D.
+// (Measured and rejected: stage D waiting on stage C's block-completion count so that the criterion
+// kernels run concurrently with it, plus a fix-up kernel for the split nodes' masses -- config 3
+// 152.3 / 168.9 us per step steady / cracking vs 148.3 / 166.7.)
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, bool heavy) {
     const bool crit = crack_on(crack_every, s);
     const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
@@ -1742,7 +1804,8 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
     cudaEventRecord(ev[1], st);
     k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
-    if (crit) {  // timed with stage C
+    cudaEventRecord(ev[2], st);
+    if (crit) {
         if (heavy) {
             k_filter<<<CEM_FILTER_GRID, 256, 0, st>>>(d, s);
             k_eval<<<CEM_CRITB_GRID, CEM_CRIT_THREADS, crit_smem_bytes(), st>>>(d, s);
@@ -1750,9 +1813,9 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
             k_crit<<<gcrit, 256, 0, st>>>(d, s);
         }
     }
-    cudaEventRecord(ev[2], st);
-    k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     cudaEventRecord(ev[3], st);
+    k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
+    cudaEventRecord(ev[4], st);
     return crit ? (heavy ? 5 : 4) : 3;
 }
 

@@ -114,11 +114,28 @@ class LoopbackGroup:
 class DistSimulation:
     """One rank of a torchrun job (one GPU per rank, NCCL halo exchange inside cem_step)."""
 
-    def __init__(self, prob, device=0, **kw):
+    def __init__(self, prob, device=0, transport="nccl", **kw):
+        """transport "nccl": NCCL communicator (+ the NVLink P2P halo when every rank can map its
+        peers); "host_ipc": no NCCL -- CUDA-IPC receive buffers whose handles, and a per-step host
+        rendezvous, go through torch.distributed on the CPU (gloo works; ranks may share a GPU)."""
         import torch.distributed as dist
         self.dist = dist
         self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
         self.prob = prob
+        if transport == "host_ipc":
+            import torch
+
+            def allgather(blob):
+                t = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+                out = [torch.empty_like(t) for _ in range(self.nranks)]
+                dist.all_gather(out, t)
+                return [bytes(x.numpy().tobytes()) for x in out]
+            self.part = partition(prob.X, prob.tets, self.nranks, self.rank)
+            self.sim = Simulation.from_problem(prob, device=device, rank=self.rank, nranks=self.nranks,
+                                               host_allgather=allgather, **kw)
+            self.torch_stream = self.sim.torch_stream
+            self.n_tets_owned = int(((self.part["tet_flag"] & 2) != 0).sum())
+            return
         buf = [None]
         if self.rank == 0:
             idb = C.create_string_buffer(128)

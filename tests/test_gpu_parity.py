@@ -164,7 +164,7 @@ def test_profiled_paths_agree():
     sim, orc = run_pair(p, 120, 1, profile=True)
     assert_parity(sim, orc, p)
     t = sim.kernel_times()
-    assert set(t) == {"stage_AB_strain_edge_stress", "stage_C_force_criterion", "stage_D_node_update"}
+    assert set(t) == {"stage_AB_strain_edge_stress", "stage_C_force_earlyout", "criterion_split", "stage_D_node_update"}
     assert all(v > 0 for v in t.values())
 
 
