@@ -151,6 +151,48 @@ def kuhn_lattice(cells, dims, seed, jitter=0.05):
     return X, tets.reshape(-1, 4).astype(np.int32), ijk
 
 
+def hex_lattice(cells, dims, seed, jitter=0.05):
+    """Jittered structured hexahedral lattice (same node numbering and jitter as kuhn_lattice).
+    Hex = cell (i,j,k), local nodes 0-3 on the k face counter-clockwise from (i,j), 4-7 above.
+    Returns (X [N,3], hexes [E,8] int32, node_ijk [N,3])."""
+    X, _, ijk = kuhn_lattice(cells, dims, seed, jitter=jitter)
+    nx, ny, nz = (int(c) for c in cells)
+    ci, cj, ck = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    ci = ci.transpose(2, 1, 0).ravel(); cj = cj.transpose(2, 1, 0).ravel(); ck = ck.transpose(2, 1, 0).ravel()
+    sx, sy = nx + 1, (nx + 1) * (ny + 1)
+
+    def nid(di, dj, dk):
+        return (ci + di) + sx * (cj + dj) + sy * (ck + dk)
+
+    H = np.stack([nid(0, 0, 0), nid(1, 0, 0), nid(1, 1, 0), nid(0, 1, 0),
+                  nid(0, 0, 1), nid(1, 0, 1), nid(1, 1, 1), nid(0, 1, 1)], axis=1)
+    return X, H.astype(np.int32), ijk
+
+
+def hex_block(cells=(12, 8, 4), dims=(0.06, 0.04, 0.02), seed=8, traction=1e6, jitter=0.05, steps=0,
+              material=None):
+    """Hexahedral block for the ES-H-FEM path: traction +-t on the y faces as
+    two triangles per loaded quad face (t A/3 per triangle node), no cracking (Gc = inf)."""
+    mat = dict(E=32e9, nu=0.2, rho=2450.0) if material is None else material
+    X, H, ijk = hex_lattice(cells, dims, seed, jitter=jitter)
+    ny = int(cells[1])
+    faces, tr = [], []
+    for jv, sgn in ((0, -1.0), (ny, 1.0)):
+        on = ijk[:, 1] == jv
+        for e in range(H.shape[0]):
+            for quad in ([0, 1, 5, 4], [3, 2, 6, 7]):
+                q = H[e, quad]
+                if on[q].all():
+                    faces += [[q[0], q[1], q[2]], [q[0], q[2], q[3]]]
+                    tr += [[0.0, sgn * traction, 0.0]] * 2
+    E = H.shape[0]
+    return Problem(name=f"hex_block_{cells[0]}x{cells[1]}x{cells[2]}", X=X, tets=H,
+                   tet_state=np.ones(E, np.uint8), tet_gc=np.full(E, np.inf), Gc=np.inf,
+                   tface=np.asarray(faces, np.int32).reshape(-1, 3), tface_t=np.asarray(tr, np.float64).reshape(-1, 3),
+                   vbc_node=np.zeros(0, np.int32), vbc_mask=np.zeros(0, np.uint8), vbc_v0=np.zeros((0, 3)),
+                   steps=steps, cells=tuple(cells), dims=tuple(dims), node_ijk=ijk, **mat)
+
+
 def _loaded_faces(tets, tet_state, node_ijk, axis, index, traction):
     """Boundary triangles of active tets whose 3 nodes have lattice index `index` on `axis`."""
     E = tets.shape[0]

@@ -24,15 +24,17 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "cem_oracle.c")
+_SRC_HEX = os.path.join(_HERE, "cem_oracle_hex.c")
 
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=gnu11"]
 
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so in-tree (gcc)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(_SRC),
+                                                                           os.path.getmtime(_SRC_HEX)):
         tmp = _SO + ".tmp"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC_HEX, "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -82,6 +84,23 @@ def lib():
         L.orc_predict.argtypes = [C.c_int64, D, D, D, C.c_double]
         L.orc_num_threads.restype = C.c_int
         L.orc_energy.argtypes = [C.c_void_p, D]
+        # ES-H-FEM hexahedra (cem_oracle_hex.c)
+        L.hx_create.restype = C.c_void_p
+        L.hx_create.argtypes = [C.c_int64, D, C.c_int64, I32, U8, C.c_double, C.c_double, C.c_double,
+                                C.c_int64, I32, D, C.c_int64, I32, U8, D, C.c_double, C.c_double, C.c_double,
+                                C.c_double, D, D, C.c_char_p, C.c_int]
+        L.hx_destroy.argtypes = [C.c_void_p]
+        L.hx_run.argtypes = [C.c_void_p, C.c_int64]
+        L.hx_n_edges.argtypes = [C.c_void_p]; L.hx_n_edges.restype = C.c_int64
+        L.hx_dt.argtypes = [C.c_void_p]; L.hx_dt.restype = C.c_double
+        L.hx_get_state.argtypes = [C.c_void_p, D, D, D, D]
+        L.hx_get_fext.argtypes = [C.c_void_p, D]
+        L.hx_get_geometry.argtypes = [C.c_void_p, D, D]
+        L.hx_edge_stress.argtypes = [C.c_void_p, D, D, D, I32]
+        L.hx_internal_force.argtypes = [C.c_void_p, D, D]
+        L.hx_strain_energy.argtypes = [C.c_void_p, D]; L.hx_strain_energy.restype = C.c_double
+        L.hx_set_state.argtypes = [C.c_void_p, D, D, D]
+        L.hx_geometry.argtypes = [D, D, D]; L.hx_geometry.restype = C.c_int
         _lib = L
     return _lib
 
@@ -220,6 +239,81 @@ class Oracle:
     def candidates(self, u, e):
         u = _c(u, np.float64); G = np.empty(24); A = np.empty(24)
         lib().orc_candidates(self.h, _p(u, D), int(e), _p(G, D), _p(A, D)); return G, A
+
+
+class HexOracle:
+    """ES-H-FEM oracle on trilinear hexahedra (cem_oracle_hex.c; elastodynamics, no cracking)."""
+
+    def __init__(self, prob, dt=None):
+        L = lib()
+        self.prob = prob
+        fn = getattr(prob, "f_nodal", None)
+        fn = None if fn is None else _c(fn, np.float64).reshape(-1, 3)
+        self._keep = [_c(prob.X, np.float64), _c(prob.tets, np.int32), _c(prob.tet_state, np.uint8),
+                      _c(prob.tface, np.int32), _c(prob.tface_t, np.float64), _c(prob.vbc_node, np.int32),
+                      _c(prob.vbc_mask, np.uint8), _c(prob.vbc_v0, np.float64), fn,
+                      _c(getattr(prob, "body", (0.0, 0.0, 0.0)), np.float64)]
+        X, H, st, tf, tt, vn, vm, vv, fn, body = self._keep
+        err = C.create_string_buffer(256)
+        self.N, self.E = X.shape[0], H.shape[0]
+        self.h = L.hx_create(self.N, _p(X, D), self.E, _p(H, I32), _p(st, U8), prob.E, prob.nu, prob.rho,
+                             tf.shape[0], _p(tf, I32), _p(tt, D), vn.shape[0], _p(vn, I32), _p(vm, U8), _p(vv, D),
+                             prob.vbc_t0, prob.dt if dt is None else dt, prob.cfl, prob.gamma, _p(fn, D),
+                             _p(body, D), err, 256)
+        if not self.h:
+            raise ValueError("hex oracle rejected the mesh: " + err.value.decode())
+        self.S = L.hx_n_edges(self.h)
+        self.step_count = 0
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().hx_destroy(self.h)
+            self.h = None
+
+    @property
+    def dt(self):
+        return lib().hx_dt(self.h)
+
+    def run(self, nsteps):
+        lib().hx_run(self.h, int(nsteps))
+        self.step_count += int(nsteps)
+        return self
+
+    def state(self):
+        u = np.empty((self.N, 3)); v = np.empty((self.N, 3)); a = np.empty((self.N, 3)); m = np.empty(self.N)
+        lib().hx_get_state(self.h, _p(u, D), _p(v, D), _p(a, D), _p(m, D))
+        return dict(u=u, v=v, a=a, m=m)
+
+    def set_state(self, u=None, v=None, a=None):
+        u = None if u is None else _c(u, np.float64)
+        v = None if v is None else _c(v, np.float64)
+        a = None if a is None else _c(a, np.float64)
+        lib().hx_set_state(self.h, _p(u, D), _p(v, D), _p(a, D))
+
+    def fext(self):
+        f = np.empty((self.N, 3)); lib().hx_get_fext(self.h, _p(f, D)); return f
+
+    def geometry(self):
+        V = np.empty(self.E); g = np.empty((self.E, 8, 3))
+        lib().hx_get_geometry(self.h, _p(V, D), _p(g, D)); return V, g
+
+    def edge_stress(self, u):
+        u = _c(u, np.float64); s = np.empty((self.S, 6)); vh = np.empty(self.S); en = np.empty((self.S, 2), np.int32)
+        lib().hx_edge_stress(self.h, _p(u, D), _p(s, D), _p(vh, D), _p(en, I32)); return s, vh, en
+
+    def internal_force(self, u):
+        u = _c(u, np.float64); f = np.empty((self.N, 3))
+        lib().hx_internal_force(self.h, _p(u, D), _p(f, D)); return f
+
+    def strain_energy(self, u):
+        u = _c(u, np.float64); return lib().hx_strain_energy(self.h, _p(u, D))
+
+
+def hex_geometry(X8):
+    """(V, grad [8,3]) of one hexahedron, or None if its Jacobian is not positive."""
+    X8 = _c(X8, np.float64); V = C.c_double(); g = np.empty((8, 3))
+    ok = lib().hx_geometry(_p(X8, D), C.byref(V), _p(g, D))
+    return (V.value, g) if ok else None
 
 
 def principal(s6):

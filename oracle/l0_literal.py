@@ -22,6 +22,50 @@ from collections import defaultdict
 import numpy as np
 
 LOCAL_EDGES = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+# trilinear hexahedron (eq:hex_strain_discretization / eq:hex_fint_discretization, PAPER.md:L311-L390):
+# 12 edges, smoothing-domain volume (1/12) sum_j V_j; element strain = the volume-averaged strain (R23)
+HEX_EDGES = [(0, 1), (1, 2), (2, 3), (0, 3), (4, 5), (5, 6), (6, 7), (4, 7), (0, 4), (1, 5), (2, 6), (3, 7)]
+HEX_XI = np.array([[-1, -1, -1], [1, -1, -1], [1, 1, -1], [-1, 1, -1],
+                   [-1, -1, 1], [1, -1, 1], [1, 1, 1], [-1, 1, 1]], dtype=np.float64)
+
+
+def _hex_dN(p):
+    """[8,3] derivatives of the trilinear shape functions w.r.t. (xi, eta, zeta) at p."""
+    f = 1.0 + HEX_XI * np.asarray(p)[None, :]             # (1 + xi_i xi), ...
+    d = np.empty((8, 3))
+    d[:, 0] = HEX_XI[:, 0] * f[:, 1] * f[:, 2] / 8.0
+    d[:, 1] = f[:, 0] * HEX_XI[:, 1] * f[:, 2] / 8.0
+    d[:, 2] = f[:, 0] * f[:, 1] * HEX_XI[:, 2] / 8.0
+    return d
+
+
+def hex_B(Xe):
+    """Volume and the 6x24 mean-gradient B matrix (1/V) integral grad N dV of one hex by 3x3x3
+    Gauss-Legendre with numpy.linalg.det / inv (independent of the C oracle's 2x2x2 rule and
+    cofactor form; both are exact for the trilinear map)."""
+    pts, wts = np.polynomial.legendre.leggauss(3)
+    V = 0.0
+    G = np.zeros((8, 3))
+    for i, a in enumerate(pts):
+        for j, b in enumerate(pts):
+            for k, c in enumerate(pts):
+                dN = _hex_dN((a, b, c))
+                J = Xe.T @ dN
+                w = wts[i] * wts[j] * wts[k] * np.linalg.det(J)
+                V += w
+                G += w * (dN @ np.linalg.inv(J))
+    g = G / V                                              # [8,3] mean dN/dx
+    B = np.zeros((6, 24))
+    for a in range(8):
+        gx, gy, gz = g[a]
+        c = 3 * a
+        B[0, c] = gx
+        B[1, c + 1] = gy
+        B[2, c + 2] = gz
+        B[3, c] = gy; B[3, c + 1] = gx
+        B[4, c + 1] = gz; B[4, c + 2] = gy
+        B[5, c] = gz; B[5, c + 2] = gx
+    return V, B
 
 
 def tet_B(Xe):
@@ -55,8 +99,9 @@ def D_matrix(E, nu):
 
 def edge_incidence(tets):
     inc = defaultdict(list)
+    edges = HEX_EDGES if tets.shape[1] == 8 else LOCAL_EDGES
     for e, t in enumerate(tets):
-        for p, q in LOCAL_EDGES:
+        for p, q in edges:
             i, j = int(t[p]), int(t[q])
             inc[(min(i, j), max(i, j))].append(e)
     return dict(sorted(inc.items()))
@@ -65,7 +110,9 @@ def edge_incidence(tets):
 def smoothed_operators(X, tets, active):
     """Per edge: (edge, support nodes, B̃ [6 x 3|supp|], V_s) over active incident tets."""
     inc = edge_incidence(tets)
-    geo = [tet_B(X[t]) for t in tets]
+    hexa = tets.shape[1] == 8
+    npe, nedge = (8, 12) if hexa else (4, 6)
+    geo = [(hex_B if hexa else tet_B)(X[t]) for t in tets]
     ops = []
     for edge, elems in inc.items():
         act = [e for e in elems if active[e]]
@@ -79,10 +126,10 @@ def smoothed_operators(X, tets, active):
         for e in act:
             Ve, Be = geo[e]
             w = Ve / Vsum
-            for a in range(4):
+            for a in range(npe):
                 c = col[int(tets[e][a])]
                 Bt[:, 3 * c:3 * c + 3] += w * Be[:, 3 * a:3 * a + 3]
-        ops.append((edge, np.array(supp), Bt, Vsum / 6.0))
+        ops.append((edge, np.array(supp), Bt, Vsum / nedge))
     return ops
 
 
