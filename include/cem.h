@@ -84,6 +84,14 @@ typedef struct {
     const int32_t *tets;      /* [n_tets][4] node ids, positive orientation required */
     const uint8_t *tet_state; /* NULL | [n_tets]: 0 inactive from the start (notch), 1 active */
     const double *tet_gc;     /* NULL | [n_tets] per-element Gc (J/m^2); 0 = pre-damaged */
+    int32_t nodes_per_elem;   /* (ABI >= 2) 0 or 4: linear tets (ES-T-FEM, the default); 8: trilinear
+                                 hexahedra (ES-H-FEM; `tets` then holds [n][8]
+                                 node ids, nodes 0-3 one face counter-clockwise seen from outside...
+                                 i.e. a right-handed (xi, eta) order, 4-7 the opposite face in the same
+                                 order; element strain = the volume-averaged strain, R23-R26).
+                                 Hexahedral contexts run elastodynamics only: crack patterns III-VI are
+                                 not built (cem_step with crack_every > 0, cem_crack_update and
+                                 cem_energy return CEM_ESTATE); one GPU (nranks = 1). */
 } cem_mesh_in;
 
 /* Loads (PAPER.md:L191 Dirichlet/Neumann boundaries; L408-L412 external force;

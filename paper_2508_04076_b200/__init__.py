@@ -52,7 +52,7 @@ class cem_material(C.Structure):
 
 class cem_mesh_in(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("X", D), ("n_tets", C.c_int64), ("tets", I32),
-                ("tet_state", U8), ("tet_gc", D)]
+                ("tet_state", U8), ("tet_gc", D), ("nodes_per_elem", C.c_int32)]
 
 
 class cem_load_in(C.Structure):
@@ -178,11 +178,13 @@ class Simulation:
                  rank=0, nranks=1, nccl_id=None, f_nodal=None, body=(0.0, 0.0, 0.0), host_allgather=None):
         self._h = C.c_void_p()
         keep = []
-        Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, 4))
+        # elements: [E,4] linear tets (ES-T-FEM) or [E,8] trilinear hexahedra (ES-H-FEM)
+        npe = 8 if np.ndim(tets) == 2 and np.shape(tets)[1] == 8 else 4
+        Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, npe))
         st = None if tet_state is None else _arr(tet_state, np.uint8)
         gc = None if tet_gc is None else _arr(tet_gc, np.float64)
         keep += [Xa, Ta, st, gc]
-        mesh = cem_mesh_in(Xa.shape[0], _ptr(Xa, D), Ta.shape[0], _ptr(Ta, I32), _ptr(st, U8), _ptr(gc, D))
+        mesh = cem_mesh_in(Xa.shape[0], _ptr(Xa, D), Ta.shape[0], _ptr(Ta, I32), _ptr(st, U8), _ptr(gc, D), npe)
         mat = cem_material(E, nu, rho, Gc)
         tf = _arr(np.zeros((0, 3)) if tface is None else tface, np.int32, (-1, 3))
         tt = _arr(np.zeros((0, 3)) if tface_t is None else tface_t, np.float64, (-1, 3))
@@ -360,8 +362,9 @@ class Simulation:
 
 
 def workspace_size(X, tets):
-    Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, 4))
-    mesh = cem_mesh_in(Xa.shape[0], _ptr(Xa, D), Ta.shape[0], _ptr(Ta, I32), None, None)
+    npe = 8 if np.ndim(tets) == 2 and np.shape(tets)[1] == 8 else 4
+    Xa = _arr(X, np.float64, (-1, 3)); Ta = _arr(tets, np.int32, (-1, npe))
+    mesh = cem_mesh_in(Xa.shape[0], _ptr(Xa, D), Ta.shape[0], _ptr(Ta, I32), None, None, npe)
     b = C.c_size_t()
     rc = _lib.cem_workspace_size(C.byref(mesh), None, C.byref(b))
     if rc:

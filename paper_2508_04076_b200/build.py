@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcem.so")
-SOURCES = ["cem_mesh.cpp", "cem_plan.cpp", "cem_part.cpp", "cem_kernels.cu", "cem_dist.cu", "cem_api.cu"]
+SOURCES = ["cem_mesh.cpp", "cem_plan.cpp", "cem_part.cpp", "cem_hex_mesh.cpp", "cem_kernels.cu", "cem_dist.cu", "cem_hex.cu",
+           "cem_api.cu"]
 HEADERS = ["cem_internal.h", "cem_part.h", "cem_dist.h", os.path.join("..", "..", "include", "cem.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

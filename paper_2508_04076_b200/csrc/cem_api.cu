@@ -48,6 +48,7 @@ struct cem_ctx {
     std::string err;
     // multi-GPU (nranks > 1)
     bool dist = false, loopback = false;
+    bool hexa = false;            // trilinear hexahedra (ES-H-FEM, cem_hex.cpp / cem_hex.cu)
     int rank = 0, nranks = 1;
     PartLocal part;
     Exchange xch;
@@ -1031,6 +1032,251 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
     o->node_owner = dup32(g.node_owner);
 }
 
+// ---------------------------------------------------------------- hexahedral contexts (N3)
+struct HexOffs {
+    size_t hgeo, hconn, heedge, htau, e_off, e_inc, vhat, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
+        srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, total;
+};
+HexOffs hex_layout(const HexHost &h) {
+    Layout L;
+    HexOffs o{};
+    const int64_t N = h.N, E = h.E, S = h.S;
+    o.hgeo = L.take<double>(25 * E);
+    o.hconn = L.take<int32_t>(8 * E);
+    o.heedge = L.take<int32_t>(12 * E);
+    o.htau = L.take<double>(6 * E);
+    o.e_off = L.take<int32_t>(S + 1);
+    o.e_inc = L.take<int32_t>((int64_t)h.edge_inc.size());
+    o.vhat = L.take<double>(S);
+    o.nodeE = L.take<int32_t>((int64_t)h.nodeE.size());
+    o.fext = L.take<double4>(N);
+    o.nflag = L.take<uint8_t>(N);
+    o.dir_v0 = L.take<double4>(h.any_dirichlet ? N : 1);
+    o.state = L.take<uint8_t>(E);
+    o.mass = L.take<double>(N);
+    o.dirty = L.take<int32_t>(N);
+    o.u0 = L.take<double4>(N);
+    o.u1 = L.take<double4>(N);
+    o.v = L.take<double4>(N);
+    o.a = L.take<double4>(N);
+    o.srec = L.take<double>(4 * S);
+    o.srec2 = L.take<double>(2 * S);
+    o.fe = L.take<double>(3 * (8 * E + 1));
+    o.ctr = L.take<int32_t>(32);
+    o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
+    o.wr_dof = L.take<double>(h.any_dirichlet ? 3 * N : 1);
+    o.node_orig = L.take<int32_t>(N);
+    o.tet_orig = L.take<int32_t>(E);
+    o.self = L.take<Dev>(1);
+    o.total = L.off;
+    return o;
+}
+
+// allocate the device workspace as cem_init_mesh does (caller buffer, allocation callback or cudaMalloc)
+cem_status alloc_workspace(cem_ctx *ctx, const cem_opts *opts, size_t total) {
+    if (opts && opts->workspace) {
+        if (opts->workspace_bytes < total) {
+            ctx->err = "workspace too small: need " + std::to_string(total) + " bytes";
+            return CEM_ENOMEM;
+        }
+        ctx->ws = opts->workspace;
+        ctx->ws_bytes = opts->workspace_bytes;
+    } else if (opts && opts->dev_alloc) {
+        if (opts->dev_alloc(total, opts->alloc_user, &ctx->ws) != 0 || !ctx->ws) {
+            ctx->err = "dev_alloc callback failed for " + std::to_string(total) + " bytes";
+            return CEM_ENOMEM;
+        }
+        ctx->ws_bytes = total;
+    } else {
+        cudaError_t e = cudaMalloc(&ctx->ws, total);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+            ctx->ws = nullptr;
+            return CEM_ENOMEM;
+        }
+        ctx->own_ws = true;
+        ctx->ws_bytes = total;
+    }
+    return CEM_OK;
+}
+
+cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_load_in *load, const cem_opts *opts,
+                    cem_ctx **out) {
+    cem_ctx *ctx = new cem_ctx();
+    auto fail = [&](cem_status s) {
+        g_init_err = ctx->err;
+        if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->fence_in) cudaEventDestroy(ctx->fence_in);
+        if (ctx->fence_out) cudaEventDestroy(ctx->fence_out);
+        delete ctx;
+        return s;
+    };
+    if (opts && opts->nranks > 1) {
+        ctx->err = "hexahedral meshes run on one GPU (nranks = 1)";
+        return fail(CEM_EINVAL);
+    }
+    HexHost h;
+    cem_status st = build_hex_host(mesh, mat, load, opts, h, ctx->err);
+    if (st) return fail(st);
+    ctx->hexa = true;
+    ctx->device = opts ? opts->device : 0;
+    ctx->flags = opts ? opts->flags : 0;
+    ctx->user_stream = opts ? (cudaStream_t)opts->stream : nullptr;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) {
+        ctx->err = "cudaSetDevice failed (no CUDA device?)";
+        return fail(CEM_ECUDA);
+    }
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->fence_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->fence_out, cudaEventDisableTiming) != cudaSuccess) {
+        ctx->err = "cudaStreamCreate / cudaEventCreate failed";
+        return fail(CEM_ECUDA);
+    }
+    ctx->own_stream = true;
+    cudaEventRecord(ctx->fence_in, ctx->user_stream);
+    cudaStreamWaitEvent(ctx->stream, ctx->fence_in, 0);
+    const int64_t N = h.N, E = h.E, S = h.S;
+    // the host views cem_get_state uses (identity numbering: no storage reordering for hexes)
+    ctx->h.N = N;
+    ctx->h.E = E;
+    ctx->h.S = S;
+    ctx->h.dt = h.dt;
+    ctx->h.gc.assign(E, INFINITY);
+    ctx->p.node_new2old.resize(N);
+    std::iota(ctx->p.node_new2old.begin(), ctx->p.node_new2old.end(), 0);
+    ctx->p.tet_new2old.resize(E);
+    std::iota(ctx->p.tet_new2old.begin(), ctx->p.tet_new2old.end(), 0);
+    const HexOffs o = hex_layout(h);
+    st = alloc_workspace(ctx, opts, o.total);
+    if (st) return fail(st);
+    void *b = ctx->ws;
+    Dev &d = ctx->d;
+    d = Dev{};
+    d.N = N;
+    d.E = E;
+    d.S = S;
+    d.npe = 8;
+    d.hgeo = at<double>(b, o.hgeo);
+    d.hconn = at<int32_t>(b, o.hconn);
+    d.heedge = at<int32_t>(b, o.heedge);
+    d.htau = at<double>(b, o.htau);
+    d.e_off = at<int32_t>(b, o.e_off);
+    d.e_inc = at<int32_t>(b, o.e_inc);
+    d.vhat = at<double>(b, o.vhat);
+    d.nodeE = at<int32_t>(b, o.nodeE);
+    d.wn = h.wn;
+    d.zslot = h.zslot;
+    d.fext = at<double4>(b, o.fext);
+    d.nflag = at<uint8_t>(b, o.nflag);
+    d.dir_v0 = at<double4>(b, o.dir_v0);
+    d.state = at<uint8_t>(b, o.state);
+    d.mass = at<double>(b, o.mass);
+    d.dirty = at<int32_t>(b, o.dirty);
+    d.ubuf[0] = at<double4>(b, o.u0);
+    d.ubuf[1] = at<double4>(b, o.u1);
+    d.v = at<double4>(b, o.v);
+    d.a = at<double4>(b, o.a);
+    d.srec = at<double>(b, o.srec);
+    d.srec2 = at<double>(b, o.srec2);
+    d.fe = at<double>(b, o.fe);
+    d.ctr = at<int32_t>(b, o.ctr);
+    d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
+    d.wr_dof = at<double>(b, o.wr_dof);
+    d.node_orig = at<int32_t>(b, o.node_orig);
+    d.tet_orig = at<int32_t>(b, o.tet_orig);
+    d.self = at<Dev>(b, o.self);
+    d.lam = h.lam;
+    d.mu = h.mu;
+    d.l2m = h.l2m;
+    d.rho = h.rho;
+    d.dt = h.dt;
+    d.hdt2 = 0.5 * h.dt * h.dt;
+    d.gamma = h.gamma;
+    d.omg = 1.0 - h.gamma;
+    d.t0 = h.t0;
+    d.flags = ctx->flags;
+    d.blk = 256;
+    d.blk_ab = 256;
+    // device tables: planes [25][E] (V, then dN_a/dx_c at 1 + 3a + c), [8][E], [12][E]
+    cudaStream_t s = ctx->stream;
+    std::vector<double> geo(25 * E);
+    std::vector<int32_t> conn(8 * E);
+    for (int64_t e = 0; e < E; ++e) {
+        geo[e] = h.V[e];
+        for (int i = 0; i < 24; ++i) geo[(1 + i) * E + e] = h.grad[24 * e + i];
+        for (int a = 0; a < 8; ++a) conn[a * E + e] = h.hex[8 * e + a];
+    }
+    // initial state as the tet path (R17): u_0 = 0, a_0 = M^-1 f_ext (prescribed: v(0), v'(0)), u_1 predicted
+    std::vector<double4> f4(N), d4(h.any_dirichlet ? N : 1), z4(N, make_double4(0, 0, 0, 0)), v4(N), a4(N), u1(N);
+    std::vector<double> r0(h.any_dirichlet ? 3 * N : 1, 0.0);
+    const double dt = h.dt, hdt2 = 0.5 * h.dt * h.dt;
+    for (int64_t n = 0; n < N; ++n) {
+        f4[n] = make_double4(h.fext[3 * n], h.fext[3 * n + 1], h.fext[3 * n + 2], 0.0);
+        if (h.any_dirichlet) d4[n] = make_double4(h.dir_v0[3 * n], h.dir_v0[3 * n + 1], h.dir_v0[3 * n + 2], 0.0);
+        double vv[3], aa[3], uu[3];
+        for (int c = 0; c < 3; ++c) {
+            const double mk = h.mass[n];
+            if (mk == 0.0) {
+                vv[c] = 0.0;
+                aa[c] = 0.0;
+            } else if (h.nflag[n] >> c & 1) {
+                const double v0 = h.dir_v0[3 * n + c];
+                if (h.t0 <= 0.0) {
+                    vv[c] = v0;
+                    aa[c] = 0.0;
+                } else {
+                    vv[c] = (0.0 / h.t0) * v0;
+                    aa[c] = (0.0 < h.t0) ? v0 / h.t0 : 0.0;
+                }
+            } else {
+                vv[c] = 0.0;
+                aa[c] = (h.fext[3 * n + c] - 0.0) / mk;
+            }
+            uu[c] = (0.0 + dt * vv[c]) + hdt2 * aa[c];
+            if (h.any_dirichlet && (h.nflag[n] >> c & 1)) r0[3 * n + c] = mk * aa[c] - (h.fext[3 * n + c] - 0.0);
+        }
+        v4[n] = make_double4(vv[0], vv[1], vv[2], 0.0);
+        a4[n] = make_double4(aa[0], aa[1], aa[2], 0.0);
+        u1[n] = make_double4(uu[0], uu[1], uu[2], 0.0);
+    }
+    std::vector<int32_t> ident(std::max(N, E));
+    std::iota(ident.begin(), ident.end(), 0);
+    int32_t ctr[32] = {0, 0, INT32_MAX};
+    auto put = [&](size_t off, const void *src, size_t bytes) { return cudaMemcpyAsync(at<char>(b, off), src, bytes, cudaMemcpyHostToDevice, s); };
+    CUDA_TRY(put(o.hgeo, geo.data(), 8 * geo.size()));
+    CUDA_TRY(put(o.hconn, conn.data(), 4 * conn.size()));
+    CUDA_TRY(put(o.heedge, h.eedge.data(), 4 * h.eedge.size()));
+    CUDA_TRY(put(o.e_off, h.edge_off.data(), 4 * h.edge_off.size()));
+    CUDA_TRY(put(o.e_inc, h.edge_inc.data(), 4 * h.edge_inc.size()));
+    CUDA_TRY(put(o.vhat, h.vhat.data(), 8 * h.vhat.size()));
+    CUDA_TRY(put(o.nodeE, h.nodeE.data(), 4 * h.nodeE.size()));
+    CUDA_TRY(put(o.fext, f4.data(), sizeof(double4) * N));
+    CUDA_TRY(put(o.nflag, h.nflag.data(), N));
+    if (h.any_dirichlet) {
+        CUDA_TRY(put(o.dir_v0, d4.data(), sizeof(double4) * N));
+        CUDA_TRY(put(o.rprev, r0.data(), 8 * r0.size()));
+    }
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.wr_dof), 0, 8 * (h.any_dirichlet ? 3 * N : 1), s));
+    CUDA_TRY(put(o.state, h.state.data(), E));
+    CUDA_TRY(put(o.mass, h.mass.data(), 8 * N));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.dirty), 0, 4 * N, s));
+    CUDA_TRY(put(o.u0, z4.data(), sizeof(double4) * N));
+    CUDA_TRY(put(o.u1, u1.data(), sizeof(double4) * N));
+    CUDA_TRY(put(o.v, v4.data(), sizeof(double4) * N));
+    CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, 8 * 4 * S, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec2), 0, 8 * 2 * S, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, 8 * 3 * (8 * E + 1), s));
+    CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
+    CUDA_TRY(put(o.node_orig, ident.data(), 4 * N));
+    CUDA_TRY(put(o.tet_orig, ident.data(), 4 * E));
+    CUDA_TRY(put(o.self, &ctx->d, sizeof(Dev)));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *out = ctx;
+    return CEM_OK;
+}
+
 // undo this context's L2 persistence: clear the window on its stream and, if it raised the
 // device's persisting set-aside, restore the previous limit and demote the lines it pinned
 void release_l2(cem_ctx *ctx) {
@@ -1063,6 +1309,16 @@ cem_status cem_workspace_size(const cem_mesh_in *mesh, const cem_opts *opts, siz
     cem_opts o{};
     if (opts) o = *opts;
     o.dt = 1.0;
+    if (mesh->nodes_per_elem == 8) {
+        HexHost hh;
+        cem_load_in ld{};
+        ld.n_vbc = 0;
+        cem_status st = build_hex_host(mesh, &mat, &ld, &o, hh, g_init_err);
+        if (st) return st;
+        hh.any_dirichlet = true;
+        *bytes = hex_layout(hh).total;
+        return CEM_OK;
+    }
     HostMesh h;
     Plan p;
     cem_status st = build_host_mesh(mesh, &mat, nullptr, &o, h, g_init_err);
@@ -1080,6 +1336,11 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
     if (!out) return CEM_EINVAL;
     *out = nullptr;
     g_init_err.clear();
+    if (mesh && mesh->nodes_per_elem != 0 && mesh->nodes_per_elem != 4 && mesh->nodes_per_elem != 8) {
+        g_init_err = "cem_init_mesh: nodes_per_elem must be 0, 4 (tets) or 8 (hexahedra)";
+        return CEM_EINVAL;
+    }
+    if (mesh && mesh->nodes_per_elem == 8) return hex_init(mesh, mat, load, opts, out);
     cem_ctx *ctx = new cem_ctx();
     auto fail = [&](cem_status s) {
         g_init_err = ctx->err;
@@ -1328,7 +1589,17 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (!ctx || nsteps < 0) return CEM_EINVAL;
     if (nsteps == 0) return CEM_OK;
     if (crack_every < 0) crack_every = 0;
+    if (ctx->hexa && crack_every > 0) {
+        ctx->err = "hexahedral contexts run elastodynamics only (crack patterns III-VI are not built): crack_every must be 0";
+        return CEM_ESTATE;
+    }
     StreamFence fence(ctx);
+    if (ctx->hexa) {
+        for (int64_t i = 0; i < nsteps; ++i) ctx->launches += launch_hex_step(ctx->d, ctx->step + i, ctx->stream);
+        CUDA_TRY(cudaGetLastError());
+        ctx->step += nsteps;
+        return CEM_OK;
+    }
     // default: one kernel per stage (measured faster than the persistent wavefront kernel on
     // B200 for the current stage bodies; CEM_F_PERSISTENT selects the latter)
     if (ctx->dist) {
@@ -1490,6 +1761,10 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
         ctx->err = "cem_crack_update: single-GPU contexts only";
         return CEM_ESTATE;
     }
+    if (ctx->hexa) {
+        ctx->err = "cem_crack_update: not available for hexahedral contexts (patterns III-VI are not built)";
+        return CEM_ESTATE;
+    }
     StreamFence fence(ctx);
     int32_t before = 0, after = 0;
     CUDA_TRY(cudaMemcpyAsync(&before, ctx->d.ctr, sizeof before, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1504,6 +1779,10 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
 
 cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
     if (!ctx || !out) return CEM_EINVAL;
+    if (ctx->hexa) {
+        ctx->err = "cem_energy: tetrahedral contexts only";
+        return CEM_ESTATE;
+    }
     StreamFence fence(ctx);
     cudaStream_t st = ctx->stream;
     cem_state_out so{};

@@ -105,6 +105,29 @@ struct HostMesh {
 
 cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const cem_load_in *ld,
                            const cem_opts *o, HostMesh &h, std::string &err);
+
+// ---------------------------------------------------------------- hexahedra (ES-H-FEM, N3)
+// local edges of a trilinear hex (p < q): bottom ring, top ring, verticals
+constexpr int kHexEdgeP[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 2, 3};
+constexpr int kHexEdgeQ[12] = {1, 2, 3, 3, 5, 6, 7, 7, 4, 5, 6, 7};
+struct HexHost {
+    int64_t N = 0, E = 0, S = 0;
+    std::vector<int32_t> hex;         // [E][8]
+    std::vector<uint8_t> state;       // [E]
+    std::vector<double> V, grad;      // [E], [E][8][3] mean gradients (R23)
+    std::vector<int32_t> eedge;       // [12][E] edge of local edge l
+    std::vector<int32_t> edge_off, edge_inc, node_off, node_ent;
+    std::vector<double> vhat, mass, fext, dir_v0;
+    std::vector<uint8_t> nflag;
+    std::vector<int32_t> nodeE;       // [N][wn] slot 8e + a, padded with zslot
+    int wn = 8;
+    int32_t zslot = 0;
+    double lam = 0, mu = 0, l2m = 0, rho = 0, dt = 0, gamma = 0.5, t0 = 0;
+    bool any_dirichlet = false;
+};
+bool hex_geometry(const double *X8, double &V, double *grad);
+cem_status build_hex_host(const cem_mesh_in *m, const cem_material *mat, const cem_load_in *ld, const cem_opts *o,
+                          HexHost &h, std::string &err);
 cem_status count_edges(const cem_mesh_in *m, int64_t *S, std::string &err);
 cem_status global_cfl_dt(const cem_mesh_in *m, const cem_material *mat, double cfl, double *dt, std::string &err);
 
@@ -249,6 +272,12 @@ struct Dev {
     // dataflow ("wave") launches (WavePlan): per-block completion counters and producer lists
     int32_t *wcnt;             // [ST_COUNT][wmax]: the block has completed step value-1
     int64_t *wstep;            // base step of a graph replay (rel launches)
+    // hexahedral contexts (npe = 8): [25][E] V + mean gradients, [8][E] connectivity, [12][E] edges,
+    // [6][E] element strain planes
+    int npe;
+    const double *hgeo;
+    const int32_t *hconn, *heedge;
+    double *htau;
     const int32_t *wncons;     // [2][wmax] consumers of each AB / C block (L2 discard of consumed intermediates)
     int32_t *wcons_done;       // [2][wmax] consumers finished with the block this step
     int wdiscard;              // 1: the last consumer discards a producer block's sigma / force-slot lines
@@ -269,6 +298,11 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                        bool heavy = false);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
+// cem_hex.cu: one explicit step of a hexahedral context (4 kernels, PDL-chained; stage D is the
+// tet path's node update); returns the kernels launched
+int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st);
+// stage D alone (cem_kernels.cu), PDL-chained after the previous kernel
+void launch_node_update(const Dev &d, int64_t s, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel
 void set_smem_limits(int smem_bytes);
 void set_wave_carveout(int smem_ab, int smem_c, int pct = -1);  // same carveout for the three wave kernels

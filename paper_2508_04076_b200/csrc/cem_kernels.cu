@@ -1829,6 +1829,10 @@ void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
     k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d.wcnt, n, (int32_t)step);
 }
 
+void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {
+    launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+}
+
 int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel) {
     for (const WaveLaunch &L : w.seq) {
         const unsigned nb = (unsigned)(L.b1 - L.b0);
