@@ -117,8 +117,21 @@ def make_problem(cfg, P=1):
     return ci.config(cfg, P=1) if cfg == 3 else ci.config(cfg)
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(prob, budget_s=12.0):
-    """The oracle as it stands, timed on this host's cores on a bounded sample."""
+    """The oracle as it stands, timed on this host's cores on a bounded sample, plus the same
+    oracle on ONE thread (OMP_NUM_THREADS = nproc and = 1; results do not depend
+    on the thread count)."""
     import oracle
     t0 = time.time()
     o = oracle.Oracle(prob)
@@ -131,9 +144,28 @@ def cpu_baseline(prob, budget_s=12.0):
         if time.time() - t0 > budget_s or steps >= 50:
             break
     el = time.time() - t0
-    return {"value": prob.n_tets * steps / el, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{prob.name}: {steps} oracle steps (criterion every step) after 1 warm step, "
-                      f"init {init_s:.1f}s excluded"}
+    cores = oracle.num_threads()
+    oracle.set_threads(1)
+    t1 = time.time()
+    o.run(2, 1)
+    el1 = time.time() - t1
+    oracle.set_threads(cores)
+    return {"value": prob.n_tets * steps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "value_1_thread": prob.n_tets * 2 / el1,
+            "sample": f"{prob.name}: {steps} oracle steps (criterion every step) after 1 warm step on {cores} "
+                      f"threads, then 2 steps on 1 thread; init {init_s:.1f}s excluded"}
+
+
+def fp64_peak():
+    """Measured fp64 FMA throughput (tools/dfma_peak, built by __graft_entry__.build())."""
+    tool = os.path.join(ROOT, "tools", "dfma_peak")
+    if not os.path.exists(tool):
+        return None
+    try:
+        out = subprocess.run([tool], capture_output=True, text=True, timeout=60).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception:
+        return None
 
 
 def run_reference(args):
@@ -143,17 +175,16 @@ def run_reference(args):
         return 0
     import cem_inputs as ci
     import oracle
-    # bounded sample: the config-3 block cut to nz' cells so one oracle step is ~0.1-0.3 s
-    nz = int(os.environ.get("CEM_REF_NZ", "2"))
-    prob = ci.weak_scaling_block(P=1, cells_per_rank=(100, 100, nz))
+    # the cem arm's workload itself (config 3, 1.02M tets): one oracle step is ~0.06 s on 16 cores,
+    # so W + K steps stay within a few minutes up to K ~ 2000
+    prob = ci.config(3)
     o = oracle.Oracle(prob)
     o.run(args.warmup, 1)
     t0 = time.time()
     o.run(args.steps, 1)
     el = time.time() - t0
     val = prob.n_tets * args.steps / el
-    # the config of the cem arm's line for this workload (per-GPU counts of the config-3 block)
-    full = ci.config(3)
+    full = prob
     T = full.tets.astype(np.int64)
     pairs = np.concatenate([np.sort(T[:, [a, b]], axis=1) for a, b in ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))])
     S_full = int(np.unique(pairs[:, 0] * full.n_nodes + pairs[:, 1]).size)
@@ -170,8 +201,9 @@ def run_reference(args):
             "data": "synthetic (seeded Kuhn lattice, cem_inputs)",
             "config": config,
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": f"config-3 block cut to 100x100x{nz} cells ({prob.n_tets} tets) x "
-                                       f"{args.steps} steps on the host cores (OpenMP), crack check every step"},
+                             "cpu_model": cpu_model(),
+                             "sample": f"the full config-3 block ({prob.n_tets} tets) x {args.steps} steps after "
+                                       f"{args.warmup} warm-up steps on the host cores (OpenMP), crack check every step"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -295,7 +327,9 @@ def main():
             cold = tj.get("per_kernel_cold", {}).get(kname)
             roof.update({"kernel": kname, "achieved": ach, "frac": ach / hbm, "b_alg_bytes_per_launch": b_launch,
                          "ms_per_launch": kernels[dom]["ms_per_launch"],
-                         "traffic": (cold["dram_read"] + cold["dram_write"]) if cold else None})
+                         "traffic": (cold["dram_read"] + cold["dram_write"]) if cold else None,
+                         "traffic_source": ("stored ncu --set full capture of this build, config 3: "
+                                            f"profiles/traffic_per_step.json ({tj.get('round', '?')})") if cold else None})
     # the whole step as one unit (SURVEY.md §8(d)'s "% of HBM roofline" of the metric)
     roof["step"] = {"achieved": achieved, "frac": achieved / hbm, "b_alg_bytes_per_step": balg,
                     "traffic": traffic,
@@ -321,6 +355,7 @@ def main():
         "kernels": kernels,
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "fp64_peak_measured": fp64_peak() if rank == 0 else None,
         "n_active_end": int(st.n_active),
     }
     if ws == 1:

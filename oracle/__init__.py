@@ -83,6 +83,7 @@ def lib():
         L.orc_newmark_free.argtypes = [C.c_int64, D, D, D, D, D, C.c_double, C.c_double]
         L.orc_predict.argtypes = [C.c_int64, D, D, D, C.c_double]
         L.orc_num_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
         L.orc_energy.argtypes = [C.c_void_p, D]
         # ES-H-FEM hexahedra (cem_oracle_hex.c)
         L.hx_create.restype = C.c_void_p
@@ -353,3 +354,8 @@ def predict(u, v, a, dt):
 
 def num_threads():
     return lib().orc_num_threads()
+
+
+def set_threads(n):
+    """OpenMP threads of subsequent oracle calls (bench.py's single-thread baseline)."""
+    lib().orc_set_threads(int(n))

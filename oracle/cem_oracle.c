@@ -909,6 +909,16 @@ ORC_API void orc_candidates(orc_sim *s, const double *u, int64_t e, double *G24,
     tet_candidates(s, e, u, eg, G24, A24);
 }
 
+/* bench.py's single-thread baseline: OpenMP threads of the following calls (results do not
+ * depend on it: OpenMP only splits loops over independent outputs) */
+ORC_API void orc_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 ORC_API int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
