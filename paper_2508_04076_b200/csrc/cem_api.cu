@@ -1829,6 +1829,16 @@ cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
         return CEM_ENCCL;
     }
     const int64_t nrec = ctr[0];
+#ifdef CEM_DEBUG_BOUNDS
+    {
+        int32_t bline = 0;
+        CUDA_TRY(cudaMemcpy(&bline, ctx->d.ctr + 20, sizeof bline, cudaMemcpyDeviceToHost));
+        if (bline) {
+            ctx->err = "debug build: a device bounds check failed at cem_kernels.cu line " + std::to_string(bline);
+            return CEM_ESTATE;
+        }
+    }
+#endif
 #ifdef CEM_WAVE_STATS
     fprintf(stderr, "[cem wave stats] blocks that waited: AB %d C %d D %d; polls %u\n", ctr[12], ctr[13], ctr[14],
             (unsigned)ctr[7]);

@@ -33,6 +33,20 @@ const int kThreads = 256;
 
 namespace {
 
+// Bounds checks of the debug build (-DCEM_DEBUG_BOUNDS, libcem_dbg.so; compute-sanitizer is not
+// available on the GPU pool): the first violated check stores its source line in ctr[20], which
+// cem_get_state reports as CEM_ESTATE.  Compiled out of the product build.
+#ifdef CEM_DEBUG_BOUNDS
+#define CEM_BOUND(dev, cond)                                        \
+    do {                                                            \
+        if (!(cond)) atomicCAS(&(dev).ctr[20], 0, (int)__LINE__);   \
+    } while (0)
+#else
+#define CEM_BOUND(dev, cond) \
+    do {                     \
+    } while (0)
+#endif
+
 // read-only tables: non-coherent path
 __device__ __forceinline__ double ldro(const double *p) { return __ldg(p); }
 __device__ __forceinline__ int ldro(const int32_t *p) { return __ldg(p); }
@@ -383,7 +397,9 @@ __device__ __forceinline__ void edge_sigma(const Dev &d, int64_t s, const double
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             if (t >= lim) break;
-            const int r = min((int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff), nt);
+            const int raw = (int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff);
+            CEM_BOUND(d, raw == 0xffff || raw <= nt);
+            const int r = min(raw, nt);
             T0 = T0 + T[r];
             T1 = T1 + T[tn + r];
             T2 = T2 + T[2 * tn + r];
@@ -443,6 +459,8 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     }
     const int32_t k0 = tid < nn ? __ldg(d.nlb + n0 + tid) : 0;
     const int q0 = tid < nn ? __ldg(d.nrow + n0 + tid) : 0;
+    CEM_BOUND(d, k0 >= 0 && k0 < d.N && q0 >= 0 && q0 < un);
+    CEM_BOUND(d, !has0 || (e0 < (uint32_t)d.E && r0 >= 0 && r0 < tn && lc0.x < un && lc0.y < un && lc0.z < un && lc0.w < un));
     // the second tet's list entry (most blocks hold 1.5 tets per thread): index, row, nodes
     const int i1 = tid + nthr;
     const bool has1 = i1 < nt;
@@ -732,6 +750,7 @@ __device__ __forceinline__ void split_tet(const Dev &d, int64_t e, int4 t, doubl
     }
     if (record) {  // multi-GPU: only the owning rank records (every holder deactivates)
         const int slot = atomicAdd(&d.ctr[0], 1);
+        CEM_BOUND(d, slot < d.E);
         d.rec_step[slot] = rec_step;
         d.rec_elem[slot] = ldro(d.tet_orig + e);
         d.rec_cand[slot] = k;
@@ -927,6 +946,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     uint32_t sid[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m) sid[m] = tid + m * nthr < ne ? (uint32_t)__ldg(d.el + s0i + tid + m * nthr) : 0u;
+#pragma unroll
+    for (int m = 0; m < kME; ++m) CEM_BOUND(d, sid[m] < (uint32_t)d.S);
 #if CEM_C_GEOX
     // geometry from the block's node coordinates (static: staged before the dependency wait)
     double *smx = smu + 3 * nq;
@@ -1036,6 +1057,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         } else {
             const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
                                (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
+#pragma unroll
+            for (int l = 0; l < 6; ++l) CEM_BOUND(d, le[l] < ne);
             double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
@@ -1204,7 +1227,10 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
         unpack(q, sl);
         double x[kB];
 #pragma unroll
-        for (int t = 0; t < kB; ++t) x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+        for (int t = 0; t < kB; ++t) {
+            CEM_BOUND(d, sl[t] >= 0 && sl[t] <= d.zslot);
+            x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+        }
         int w = kB;
         bool more = sl[kB - 1] != d.zslot && w < d.wn;
         if (more) {
@@ -1218,7 +1244,10 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
             if (more) {
                 unpack(q, sl);
 #pragma unroll
-                for (int t = 0; t < kB; ++t) y[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+                for (int t = 0; t < kB; ++t) {
+                    CEM_BOUND(d, sl[t] >= 0 && sl[t] <= d.zslot);
+                    y[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+                }
                 w += kB;
                 more2 = sl[kB - 1] != d.zslot && w < d.wn;
                 if (more2) {
@@ -1249,7 +1278,10 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
         }
         double x[kB];
 #pragma unroll
-        for (int t = 0; t < kB; ++t) x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+        for (int t = 0; t < kB; ++t) {
+            CEM_BOUND(d, sl[t] >= 0 && sl[t] <= d.zslot);
+            x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
+        }
         w += kB;
         const bool more = sl[kB - 1] != d.zslot && w < d.wn;
         if (more) {
@@ -1473,6 +1505,7 @@ __global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
     const double4 *u = d.ubuf[(s + 1) & 1];
     for (int i = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); i < n; i += nw) {
         const int64_t e = d.crit_list[i];
+        CEM_BOUND(d, n <= d.E && e >= 0 && e < d.E);
         criterion_warp(d.self, e, u, ldro(d.gc + e), s + 1, (int32_t)(s + 1), (__ldg(d.tflag + e) & 2) != 0,
                        scratch[threadIdx.x >> 5]);
     }
@@ -1505,6 +1538,7 @@ __global__ void __launch_bounds__(256, CEM_FILTER_MINB) k_filter(Dev d, int64_t 
         bool need = false;
         if (i < n) {
             e = d.crit_list[i];
+            CEM_BOUND(d, n <= d.E && e >= 0 && e < d.E);
             // CEM_F_NO_EARLY_OUT: every listed tet gets the full 24-candidate evaluation
             need = (d.flags & CEM_F_NO_EARLY_OUT) || crit_refined_need(d.self, e, u, ldro(d.gc + e));
         }
