@@ -31,19 +31,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(f) > t for f in files)
 
 
-def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=(), device_fma: bool = False) -> str:
+    """device_fma: the "fast build" of SURVEY.md §8(c) -- FMA contraction in device code only (the host
+    preprocessing keeps -ffp-contract=off, so geometry and masses stay the oracle's); results then
+    meet the north star's tolerance instead of bit equality (tests/test_gpu_fast_build.py)."""
     if not force and out == SO and not _stale():
         return SO
+    flags = [f for f in NVCC_FLAGS if not (device_fma and f == "--fmad=false")]
+    if device_fma:
+        flags.append("--fmad=true")
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, os.path.splitext(src)[0] + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *flags, *[f"-D{x}" for x in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = out + ".tmp"
-    subprocess.check_call([NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *objs, "-lgomp", "-ldl"])
+    subprocess.check_call([NVCC, *flags, "-shared", "-o", tmp, *objs, "-lgomp", "-ldl"])
     os.replace(tmp, out)
     for o in objs:
         os.remove(o)

@@ -18,6 +18,7 @@ using namespace cem;
 struct cem_ctx {
     HostMesh h;
     Plan p;
+    StagedSync sy;                // cumulative counts of the staged path (multi-GPU early signal)
     WavePlan w;                   // dataflow launches (opt-in, CEM_WAVE=1; w.seq empty = off)
     int64_t wcnt_valid = -1;      // the wave counters are valid for this step count
     struct WaveGraph {
@@ -757,6 +758,38 @@ void p2p_enable(cem_ctx *ctx) {
     d.p2p_toff = q.d_toff;
     d.p2p_tpeer = q.d_tpeer;
     d.p2p_tbyte = q.d_tbyte;
+    d.p2p_flag_out = q.d_peer_flag;
+    // stage-D block order for the early signal: blocks holding a node some peer receives first
+    // (CEM_P2P_EARLY=0 keeps the plain order and signals after the whole stage)
+    const char *ee = getenv("CEM_P2P_EARLY");
+    if (!(ee && atoi(ee) == 0) && d.p2p_np > 0) {
+        const int64_t per = std::max(1, ctx->p.blk / 4), nD = (ctx->h.N + per - 1) / per;
+        std::vector<uint8_t> hasp(nD, 0);
+        for (const auto &sn : ctx->part.send_nodes)
+            for (int32_t k : sn) hasp[ctx->p.node_old2new[k] / per] = 1;
+        std::vector<int32_t> order;
+        order.reserve(nD);
+        for (int64_t b = 0; b < nD; ++b)
+            if (hasp[b]) order.push_back((int32_t)b);
+        const int nb = (int)order.size();
+        for (int64_t b = 0; b < nD; ++b)
+            if (!hasp[b]) order.push_back((int32_t)b);
+        void *dord = nullptr, *dcnt = nullptr;
+        if (cudaMalloc(&dord, 4 * order.size()) == cudaSuccess && cudaMalloc(&dcnt, 8) == cudaSuccess &&
+            cudaMemcpy(dord, order.data(), 4 * order.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemset(dcnt, 0, 8) == cudaSuccess) {
+            ctx->dist_allocs.push_back(dord);
+            ctx->dist_allocs.push_back(dcnt);
+            d.d_order = static_cast<const int32_t *>(dord);
+            d.d_nbound = nb;
+            d.bdone = static_cast<unsigned long long *>(dcnt);
+            ctx->sy.bdone = 0;
+        } else {
+            if (dord) cudaFree(dord);
+            if (dcnt) cudaFree(dcnt);
+            cudaGetLastError();
+        }
+    }
     q.on = true;
 }
 
@@ -1609,7 +1642,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
-            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx));
+            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx), &ctx->sy);
             if (ctx->p2p.on && ctx->host_allgather) {
                 // host-ordered: signal, wait for this rank's stores, meet the peers on the host, then
                 // the flag wait (already satisfied: it never spins) and the unpack
@@ -1712,7 +1745,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * kStagedEvents : nullptr;
-            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx));
+            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx), &ctx->sy);
         }
         CUDA_TRY(cudaGetLastError());
         if (ctx->profiling) ctx->prof_steps += nsteps;
@@ -2011,7 +2044,7 @@ cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_
     for (int64_t i = 0; i < nsteps; ++i) {
         const int64_t sstep = c[0]->step + i;
         for (int r = 0; r < n; ++r) {
-            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(c[r]));
+            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(c[r]), &c[r]->sy);
         }
         if (c[0]->p2p.on) {  // the stores went straight into the peers' buffers; stream order syncs
             for (int r = 0; r < n; ++r) {

@@ -254,6 +254,10 @@ struct Dev {
     int p2p_np;
     const int32_t *p2p_noff, *p2p_npeer, *p2p_nbyte;  // storage node -> (peer, byte in segment) CSR
     const int32_t *p2p_toff, *p2p_tpeer, *p2p_tbyte;  // storage tet -> (peer, byte in segment) CSR
+    int64_t *const *p2p_flag_out;  // [p2p_np] the peers' flag words for this rank (early signal)
+    const int32_t *d_order;        // [nD] stage-D block order: blocks with peer-held nodes first
+    int d_nbound;                  // how many of them
+    unsigned long long *bdone;     // boundary D blocks finished (cumulative)
     int64_t *rec_step;
     int32_t *rec_elem, *rec_cand;
     double *rec_G, *rec_area;
@@ -293,9 +297,13 @@ void launch_wave_base(const Dev &d, int64_t step0, cudaStream_t st);            
 void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st);         // counters := step (after other modes)
 void launch_persistent(const Dev &d, int64_t step0, int64_t nsteps, int crack_every, int grid, cudaStream_t st);
 constexpr int kStagedEvents = 5;  // profiled staged step: AB | C | criterion | D
-// heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit
+struct StagedSync {
+    unsigned long long bdone = 0;  // cumulative boundary D blocks launched (early P2P signal)
+};
+// heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit; sy: the
+// context's cumulative counts (multi-GPU early signal), may be null
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/,
-                       bool heavy = false);  // kernels launched
+                       bool heavy = false, StagedSync *sy = nullptr);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 // cem_hex.cu: one explicit step of a hexahedral context (4 kernels, PDL-chained; stage D is the

@@ -1622,10 +1622,26 @@ __global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_eval(Dev d
         __syncwarp();  // the scratch is reused by the next batch
     }
 }
-__global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
+// bd_target > 0 (multi-GPU P2P halo): the blocks are taken in d.d_order, the blocks holding nodes
+// that peers need first; the last of those to finish signals the peers (st.release.sys of step
+// s + 2, the value the per-step sync kernel waits for) while the interior blocks still run, so a
+// peer's unpack and next step overlap this rank's interior update (SURVEY.md §8(e) "update the
+// boundary nodes first").  bd_target = the cumulative count of boundary blocks after this step.
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s, unsigned long long bd_target) {
     pdl_trigger();
-    const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
+    const int bi = (int)blockIdx.x;
+    const int b = (bd_target && d.d_order) ? __ldg(d.d_order + bi) : bi;
+    const int64_t k0 = (int64_t)b * d_nodes_per_block(blockDim.x);
     block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+    if (bd_target && bi < d.d_nbound) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();  // this block's stores into the peers' buffers
+            if (atomicAdd(d.bdone, 1ull) + 1ull == bd_target)
+                for (int j = 0; j < d.p2p_np; ++j)
+                    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(d.p2p_flag_out[j]), "l"(s + 2) : "memory");
+        }
+    }
 }
 
 __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
@@ -1817,7 +1833,10 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
 // (Measured and rejected: stage D waiting on stage C's block-completion count so that the criterion
 // kernels run concurrently with it, plus a fix-up kernel for the split nodes' masses -- config 3
 // 152.3 / 168.9 us per step steady / cracking vs 148.3 / 166.7.)
-int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, bool heavy) {
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, bool heavy,
+                       StagedSync *sy) {
+    unsigned long long bd = 0;  // early peer signal from stage D (P2P halo, boundary blocks first)
+    if (sy && d.p2p_np && d.d_order && d.d_nbound > 0) bd = sy->bdone += (unsigned long long)d.d_nbound;
     const bool crit = crack_on(crack_every, s);
     const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
@@ -1831,7 +1850,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
             }
         }
-        launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+        launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
         return crit ? (heavy ? 5 : 4) : 3;
     }
     cudaEventRecord(ev[0], st);
@@ -1848,7 +1867,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
         }
     }
     cudaEventRecord(ev[3], st);
-    k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
+    k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s, bd);
     cudaEventRecord(ev[4], st);
     return crit ? (heavy ? 5 : 4) : 3;
 }
@@ -1864,7 +1883,7 @@ void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
 }
 
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {
-    launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+    launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, 0ull);
 }
 
 int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel) {
