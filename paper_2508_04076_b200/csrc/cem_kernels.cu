@@ -946,8 +946,10 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     uint32_t sid[kME];
 #pragma unroll
     for (int m = 0; m < kME; ++m) sid[m] = tid + m * nthr < ne ? (uint32_t)__ldg(d.el + s0i + tid + m * nthr) : 0u;
+#ifdef CEM_DEBUG_BOUNDS
 #pragma unroll
     for (int m = 0; m < kME; ++m) CEM_BOUND(d, sid[m] < (uint32_t)d.S);
+#endif
 #if CEM_C_GEOX
     // geometry from the block's node coordinates (static: staged before the dependency wait)
     double *smx = smu + 3 * nq;
@@ -1057,8 +1059,10 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         } else {
             const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
                                (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
+#ifdef CEM_DEBUG_BOUNDS
 #pragma unroll
             for (int l = 0; l < 6; ++l) CEM_BOUND(d, le[l] < ne);
+#endif
             double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
@@ -1627,13 +1631,19 @@ __global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_eval(Dev d
 // s + 2, the value the per-step sync kernel waits for) while the interior blocks still run, so a
 // peer's unpack and next step overlap this rank's interior update (SURVEY.md §8(e) "update the
 // boundary nodes first").  bd_target = the cumulative count of boundary blocks after this step.
-__global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s, unsigned long long bd_target) {
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
+    pdl_trigger();
+    const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
+    block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+}
+// (a separate kernel, so that the single-GPU stage D keeps its register allocation)
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_Db(Dev d, int64_t s, unsigned long long bd_target) {
     pdl_trigger();
     const int bi = (int)blockIdx.x;
-    const int b = (bd_target && d.d_order) ? __ldg(d.d_order + bi) : bi;
+    const int b = __ldg(d.d_order + bi);
     const int64_t k0 = (int64_t)b * d_nodes_per_block(blockDim.x);
     block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
-    if (bd_target && bi < d.d_nbound) {
+    if (bi < d.d_nbound) {
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence_system();  // this block's stores into the peers' buffers
@@ -1850,7 +1860,8 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
             }
         }
-        launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
+        if (bd) launch_pdl(k_Db, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
+        else launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
         return crit ? (heavy ? 5 : 4) : 3;
     }
     cudaEventRecord(ev[0], st);
@@ -1867,7 +1878,8 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
         }
     }
     cudaEventRecord(ev[3], st);
-    k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s, bd);
+    if (bd) k_Db<<<nblk_d(d), d.blk, 0, st>>>(d, s, bd);
+    else k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     cudaEventRecord(ev[4], st);
     return crit ? (heavy ? 5 : 4) : 3;
 }
@@ -1883,7 +1895,7 @@ void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
 }
 
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {
-    launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, 0ull);
+    launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
 }
 
 int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel) {
