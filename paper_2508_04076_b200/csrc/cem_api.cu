@@ -19,6 +19,7 @@ struct cem_ctx {
     HostMesh h;
     Plan p;
     StagedSync sy;                // cumulative counts of the staged path (multi-GPU early signal)
+    int cp_on = 0, cp_grid = 0;   // pipelined stage C (CEM_C_PIPE)
     WavePlan w;                   // dataflow launches (opt-in, CEM_WAVE=1; w.seq empty = off)
     int64_t wcnt_valid = -1;      // the wave counters are valid for this step count
     struct WaveGraph {
@@ -265,6 +266,10 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.smem_bytes = smem_bytes_for(p);
     d.smem_ab = smem_ab_for(p);
     d.smem_c = smem_c_for(p);
+    d.cp_max_el = p.max_el;
+    d.cp_max_nl = p.max_nl;
+    d.cp_on = ctx->cp_on;
+    d.cp_grid = ctx->cp_grid;
     d.self = at<Dev>(b, o.self);
     d.ncons = at<int32_t>(b, o.ncons);
     d.cons_done = at<int32_t>(b, o.cons_done);
@@ -1439,6 +1444,15 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         return fail(CEM_EINVAL);
     }
     set_smem_limits(smem);
+    {  // software-pipelined stage C (k_Cp): CEM_C_PIPE=1 (measured in DESIGN.md §6)
+        const char *e = getenv("CEM_C_PIPE");
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        if (e && atoi(e) > 0 && ctx->p.blk == 256 && cp_stage_c_smem(ctx->p.max_el, ctx->p.max_nl) > 0) {
+            ctx->cp_on = 1;
+            ctx->cp_grid = std::max(1, sms) * std::max(1, atoi(e));
+        }
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     const int occ = std::max(1, persistent_occupancy(smem, ctx->p.blk));

@@ -240,6 +240,8 @@ struct Dev {
     const uint16_t *tconn, *trow, *nrow;
     const uint16_t *lconn, *ledge;
     int smem_bytes, smem_ab, smem_c;  // dynamic shared memory: persistent kernel (max), per stage
+    int cp_max_el, cp_max_nl;  // largest stage-C block edge / node lists (pipelined stage C, k_Cp)
+    int cp_on, cp_grid;        // 1: stage C runs as k_Cp on cp_grid persistent CTAs
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length,
                                // [8] survivors of the refined filter (crit_list + E)
@@ -314,6 +316,7 @@ void launch_node_update(const Dev &d, int64_t s, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel
 void set_smem_limits(int smem_bytes);
 void set_wave_carveout(int smem_ab, int smem_c, int pct = -1);  // same carveout for the three wave kernels
+int cp_stage_c_smem(int max_el, int max_nl);  // dynamic shared memory of k_Cp (0: does not fit)
 extern const int kThreads;
 
 }  // namespace cem

@@ -1161,6 +1161,237 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     }
 }
 
+__host__ __device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
+    return crack_every > 0 && ((s + 1) % crack_every) == 0;
+}
+
+// ------------------------------------------------------------------ stage C, software-pipelined
+// k_Cp: one persistent CTA per SM walks the stage-C blocks b = blockIdx.x + j gridDim.x.  While it
+// computes block j, the asynchronous copies (cp.async, no registers held) of block j+1's inputs are
+// in flight: the sigma records and node displacements it gathers (the index lists came one block
+// earlier) and its contiguous per-tet tables (geometry tile, local edge / node indices, Gc, state,
+// flags).  The per-tet arithmetic and every store are those of block_C (same bits); only the data
+// movement differs: sigma rows (48 B) and u rows (32 B) are AoS in shared memory.
+struct CpSlot {  // byte offsets inside one data slot
+    int sig, u, geo, ledge, lconn, gc, st, tf, bytes;
+};
+__host__ __device__ inline CpSlot cp_slot(int max_el, int max_nl) {
+    CpSlot c;
+    c.sig = 0;
+    c.u = (48 * max_el + 15) & ~15;
+    c.geo = c.u + 32 * max_nl;
+    c.ledge = c.geo + 8 * 352 * 8;
+    c.lconn = c.ledge + 256 * 16;
+    c.gc = c.lconn + 256 * 8;
+    c.st = c.gc + 256 * 8;
+    c.tf = c.st + 256;
+    c.bytes = (c.tf + 256 + 127) & ~127;
+    return c;
+}
+__host__ __device__ inline int cp_idx_ints(int max_el, int max_nl) { return (max_el + max_nl + 3) & ~3; }
+#ifndef CEM_CP_DEPTH
+#define CEM_CP_DEPTH 3  // data slots in flight (block j computed while j+1 .. j+DEPTH-1 load)
+#endif
+__host__ __device__ inline int cp_smem_bytes(int max_el, int max_nl) {
+    return CEM_CP_DEPTH * cp_slot(max_el, max_nl).bytes + (CEM_CP_DEPTH + 2) * 4 * cp_idx_ints(max_el, max_nl);
+}
+__device__ __forceinline__ void cpa16(void *sdst, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa8(void *sdst, const void *g) {  // static tables only (.ca)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa4(void *sdst, const void *g) {  // static tables only (.ca)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// the index lists (edge list, node list) of block b -> an index slot
+__device__ __forceinline__ void cp_issue_idx(const Dev &d, int b, int32_t *idx, bool early) {
+    const int32_t s0i = __ldg(d.el_off + b), ne = __ldg(d.el_off + b + 1) - s0i;
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) cpa4(idx + i, d.el + s0i + i);
+    if (early) {
+        const int32_t n0 = __ldg(d.nl_off + b), nn = __ldg(d.nl_off + b + 1) - n0;
+        for (int i = threadIdx.x; i < nn; i += blockDim.x) cpa4(idx + d.cp_max_el + i, d.nl + n0 + i);
+    }
+}
+// the gathered records and the contiguous per-tet tables of block b -> a data slot
+__device__ __forceinline__ void cp_issue_data(const Dev &d, int b, char *slot, const CpSlot &L, const int32_t *idx,
+                                              const double4 *u, bool early) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int ne = __ldg(d.el_off + b + 1) - __ldg(d.el_off + b);
+    for (int i = tid; i < ne; i += nthr) {  // sigma: 32-B record (11,22,33,12) + 16-B record (23,13) -> 48-B row
+        const int64_t e = idx[i];
+        char *row = slot + L.sig + 48 * i;
+        cpa16(row, d.srec + 4 * e);
+        cpa16(row + 16, d.srec + 4 * e + 2);
+        cpa16(row + 32, d.srec2 + 2 * e);
+    }
+    if (early) {
+        const int nn = __ldg(d.nl_off + b + 1) - __ldg(d.nl_off + b);
+        for (int i = tid; i < nn; i += nthr) {
+            const double *w = reinterpret_cast<const double *>(u + idx[d.cp_max_el + i]);
+            char *row = slot + L.u + 32 * i;
+            cpa16(row, w);
+            cpa16(row + 16, w + 2);
+        }
+    }
+    const int64_t t0 = (int64_t)b * d.blk;
+    const int nt = (int)min((int64_t)d.blk, d.E - t0);
+    const int ntile = (nt + 31) >> 5;
+    const double *gsrc = d.geoT + (t0 >> 5) * 352;  // (blk is a multiple of 32)
+    for (int i = tid; i < ntile * 176; i += nthr) cpa16(slot + L.geo + 16 * i, gsrc + 2 * i);
+    for (int i = tid; i < nt; i += nthr) {
+        cpa16(slot + L.ledge + 16 * i, d.ledge + 8 * (t0 + i));
+        cpa8(slot + L.lconn + 8 * i, d.lconn + 4 * (t0 + i));
+        cpa8(slot + L.gc + 8 * i, d.gc + t0 + i);
+    }
+    for (int i = tid; i < (nt + 3) / 4; i += nthr) {  // (the byte arrays are padded past E)
+        cpa4(slot + L.st + 4 * i, d.state + t0 + 4 * i);
+        cpa4(slot + L.tf + 4 * i, d.tflag + t0 + 4 * i);
+    }
+}
+
+__global__ void __launch_bounds__(256, 1) k_Cp(Dev d, int64_t s, int crack_every) {
+    extern __shared__ __align__(128) char cpsm[];
+    pdl_trigger();
+    const bool crack = crack_on(crack_every, s);
+    const bool early = crack && !(d.flags & CEM_F_NO_EARLY_OUT);
+    // ring: data slot of block j = j % D, index slot of block j = j % (D + 2); cp.async groups:
+    // group g (one per iteration) = {data of block g + D - 1, indices of block g + D + 1}, so the
+    // indices a data issue needs are two groups old (complete after wait_group D - 2)
+    constexpr int D = CEM_CP_DEPTH;
+    const CpSlot L = cp_slot(d.cp_max_el, d.cp_max_nl);
+    const int nidx = cp_idx_ints(d.cp_max_el, d.cp_max_nl);
+    int32_t *idx = reinterpret_cast<int32_t *>(cpsm + D * L.bytes);
+    const double4 *u = d.ubuf[(s + 1) & 1];
+    const int nC = d.nblk[ST_C], G = (int)gridDim.x;
+    const int64_t rec_step = s + 1;
+    const int32_t stamp = (int32_t)(s + 1);
+    const int b0 = (int)blockIdx.x;
+    for (int q = 0; q <= D; ++q)
+        if (b0 + q * G < nC) cp_issue_idx(d, b0 + q * G, idx + (q % (D + 2)) * nidx, early);
+    cpa_commit();
+    pdl_wait();  // sigma (stage AB) and u (previous stage D) are complete from here on
+    cpa_wait_all();
+    __syncthreads();
+    for (int q = 0; q < D - 1; ++q) {  // data of blocks 0 .. D-2, one group each
+        if (b0 + q * G < nC)
+            cp_issue_data(d, b0 + q * G, cpsm + (q % D) * L.bytes, L, idx + (q % (D + 2)) * nidx, u, early);
+        cpa_commit();
+    }
+    const int tid = threadIdx.x;
+    for (int j = 0;; ++j) {
+        const int b = b0 + j * G;
+        if (b >= nC) break;
+        // block j's data (committed D - 1 groups ago) has arrived; later groups may still fly
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
+        __syncthreads();
+        {
+            const int jn = j + D - 1, bn = b0 + jn * G;  // its indices arrived earlier
+            if (bn < nC) cp_issue_data(d, bn, cpsm + (jn % D) * L.bytes, L, idx + (jn % (D + 2)) * nidx, u, early);
+            const int ji = j + D + 1, bi = b0 + ji * G;
+            if (bi < nC) cp_issue_idx(d, bi, idx + (ji % (D + 2)) * nidx, early);
+            cpa_commit();
+        }
+        // ---- compute block b from its data slot (block_C's per-tet arithmetic)
+        const char *sl = cpsm + (j % D) * L.bytes;
+        const int64_t e = (int64_t)b * d.blk + tid;
+        const bool he = e < d.E;
+        bool need = false;
+        if (he) {
+            const uint8_t act = reinterpret_cast<const uint8_t *>(sl + L.st)[tid];
+            double *fo = d.fe + 12 * (uint32_t)e;
+            if (!act) {
+                for (int q = 0; q < 3; ++q) st256(reinterpret_cast<double4 *>(fo) + q, 0.0, 0.0, 0.0, 0.0);
+            } else {
+                const uint4 lq = reinterpret_cast<const uint4 *>(sl + L.ledge)[tid];
+                const int le[6] = {(int)(lq.x & 0xffff), (int)(lq.x >> 16), (int)(lq.y & 0xffff),
+                                   (int)(lq.y >> 16), (int)(lq.z & 0xffff), (int)(lq.z >> 16)};
+                double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0, gmax = 0.0;
+#pragma unroll
+                for (int l = 0; l < 6; ++l) {
+                    const double2 *row = reinterpret_cast<const double2 *>(sl + L.sig + 48 * le[l]);
+                    const double2 p0 = row[0], p1 = row[1], p2 = row[2];
+                    const double a0 = p0.x, a1 = p0.y, a2 = p1.x, a3 = p1.y, a4 = p2.x, a5 = p2.y;
+                    S0 = S0 + a0;
+                    S1 = S1 + a1;
+                    S2 = S2 + a2;
+                    S3 = S3 + a3;
+                    S4 = S4 + a4;
+                    S5 = S5 + a5;
+                    if (early) {
+                        const double r0 = fabs(a0) + fabs(a3) + fabs(a5);
+                        const double r1 = fabs(a1) + fabs(a3) + fabs(a4);
+                        const double r2 = fabs(a2) + fabs(a4) + fabs(a5);
+                        gmax = fmax(gmax, fmax(r0, fmax(r1, r2)));
+                    }
+                }
+                const double *gt = reinterpret_cast<const double *>(sl + L.geo) + (tid >> 5) * 352 + (tid & 31);
+                double g[4][3];
+#pragma unroll
+                for (int a = 1; a < 4; ++a)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) g[a][c] = gt[32 * (2 + 3 * (a - 1) + c)];
+                const double cc = gt[32];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
+                double f[12];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    f[3 * a] = cc * ((g[a][0] * S0 + g[a][1] * S3) + g[a][2] * S5);
+                    f[3 * a + 1] = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
+                    f[3 * a + 2] = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    st256(reinterpret_cast<double4 *>(fo) + q, f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                const uint8_t tf = reinterpret_cast<const uint8_t *>(sl + L.tf)[tid];
+                need = crack && (tf & 1);
+                if (need && early) {
+                    const ushort4 lc = reinterpret_cast<const ushort4 *>(sl + L.lconn)[tid];
+                    const int li[4] = {lc.x, lc.y, lc.z, lc.w};
+                    double ux[4], uy[4], uz[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        const double2 *row = reinterpret_cast<const double2 *>(sl + L.u + 32 * li[a]);
+                        const double2 q0 = row[0], q1 = row[1];
+                        ux[a] = q0.x;
+                        uy[a] = q0.y;
+                        uz[a] = q1.x;
+                    }
+                    double d2 = 0.0;
+#pragma unroll
+                    for (int l = 0; l < 6; ++l) {
+                        const int p = l < 3 ? 0 : (l < 5 ? 1 : 2), q = l < 3 ? l + 1 : (l < 5 ? l - 1 : 3);
+                        const double dx = ux[q] - ux[p], dy = uy[q] - uy[p], dz = uz[q] - uz[p];
+                        d2 = fmax(d2, (dx * dx + dy * dy) + dz * dz);
+                    }
+                    const double gcv = reinterpret_cast<const double *>(sl + L.gc)[tid];
+                    need = !(gmax * sqrt(d2) * (1.0 + 1e-6) <= gcv);
+                }
+            }
+        }
+        if (crack) {  // the tets that fail the early-out: the step's criterion list (k_crit / k_filter)
+            const unsigned mm = __ballot_sync(0xffffffffu, need);
+            if (mm) {
+                const int lane = threadIdx.x & 31, lead = __ffs(mm) - 1;
+                int base = 0;
+                if (lane == lead) base = atomicAdd(&d.ctr[3], __popc(mm));
+                base = __shfl_sync(0xffffffffu, base, lead);
+                if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = (int32_t)e;
+            }
+        }
+        __syncthreads();  // this data slot is refilled by the copies issued in iteration j + 1
+    }
+    (void)rec_step;
+    (void)stamp;
+}
+
 // ------------------------------------------------------------------ stage D: node update
 // Four lanes per node, lane c = component c (lane 3 carries the zero w component): the three
 // component sums f_int,k,c = sum over the node's ELL row of force-slot components (ascending
@@ -1357,9 +1588,6 @@ __device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, int64_t ken
     node_update(d, kbase, min(kend, d.N), u1p, u2p, s);
 }
 
-__host__ __device__ __forceinline__ bool crack_on(int crack_every, int64_t s) {
-    return crack_every > 0 && ((s + 1) % crack_every) == 0;
-}
 
 // ------------------------------------------------------------------ persistent wavefront kernel
 __device__ __forceinline__ int ld_relaxed(const int32_t *p) {  // poll without invalidating L1
@@ -1796,6 +2024,16 @@ void set_wave_carveout(int smem_ab, int smem_c, int pct) {
     cudaGetLastError();
 }
 
+int cp_stage_c_smem(int max_el, int max_nl) {
+    const int b = cp_smem_bytes(max_el, max_nl);
+    if (b > 227 * 1024) return 0;
+    if (cudaFuncSetAttribute(k_Cp, cudaFuncAttributeMaxDynamicSharedMemorySize, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return b;
+}
+
 void set_smem_limits(int smem_bytes) {
     // the attribute is per function AND per device: keep the largest any context of the current
     // device needs (called after cudaSetDevice)
@@ -1851,7 +2089,11 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
         launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
-        launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
+        if (d.cp_on)
+            launch_pdl(k_Cp, (unsigned)d.cp_grid, 256u, (size_t)cp_smem_bytes(d.cp_max_el, d.cp_max_nl), st, d, s,
+                       crack_every);
+        else
+            launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
         if (crit) {
             if (heavy) {
                 launch_pdl(k_filter, (unsigned)CEM_FILTER_GRID, 256u, (size_t)0, st, d, s);
@@ -1867,7 +2109,10 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     cudaEventRecord(ev[0], st);
     k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
     cudaEventRecord(ev[1], st);
-    k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
+    if (d.cp_on)
+        k_Cp<<<d.cp_grid, 256, cp_smem_bytes(d.cp_max_el, d.cp_max_nl), st>>>(d, s, crack_every);
+    else
+        k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
     cudaEventRecord(ev[2], st);
     if (crit) {
         if (heavy) {

@@ -89,3 +89,22 @@ def test_wave_opt_in_counts_launches(monkeypatch):
     assert per_step > 10
     orc = oracle.Oracle(p).run(32, 1)
     assert_parity(sim, orc, p)
+
+
+@pytest.mark.parametrize("case", ["cfg0", "plate", "predamage"])
+def test_pipelined_stage_c_bitwise(case, monkeypatch):
+    """The software-pipelined stage C (k_Cp, cp.async ring of D blocks per persistent CTA; opt-in
+    CEM_C_PIPE=1, measured slower -- DESIGN.md §6) gives the oracle's bits."""
+    monkeypatch.setenv("CEM_C_PIPE", "1")
+    cem = _gpu()
+    if case == "cfg0":
+        p, steps = ci.config(0), 200
+    elif case == "plate":
+        p, steps = _plate(), 150
+    else:
+        p, steps = ci.weak_scaling_block(P=1, cells_per_rank=(30, 30, 5), steps=120), 120
+    sim = cem.Simulation.from_problem(p)
+    orc = oracle.Oracle(p)
+    sim.step(steps, 1)
+    orc.run(steps, 1)
+    assert assert_parity(sim, orc, p).rec_elem.size > 0
