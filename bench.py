@@ -353,6 +353,10 @@ def main():
                    "l2": "per-step working set > 126 MB L2 (no flush needed)"},
         "roofline": roof,
         "kernels": kernels,
+        "timed_steps": [args.warmup, args.warmup + args.steps],
+        "phase": ("cracking (config 3 splits its 5143 pre-damaged tets by step ~45; the criterion kernels "
+                  "evaluate them every step until then)" if args.config == 3 and args.warmup < 45 else
+                  "steady state" if args.config == 3 else None),
         "gpu_launches": int(launches),
         "clocks": clocks,
         "fp64_peak_measured": fp64_peak() if rank == 0 else None,
