@@ -90,8 +90,9 @@ typedef struct {
                                  i.e. a right-handed (xi, eta) order, 4-7 the opposite face in the same
                                  order; element strain = the volume-averaged strain, R23-R26).
                                  Hexahedral contexts run elastodynamics only: crack patterns III-VI are
-                                 not built (cem_step with crack_every > 0, cem_crack_update and
-                                 cem_energy return CEM_ESTATE); one GPU (nranks = 1). */
+                                 not built (cem_step with crack_every > 0 and cem_crack_update return
+                                 CEM_ESTATE; cem_energy works, with the smoothing-domain volume
+                                 Vhat_s / 12); one GPU (nranks = 1). */
 } cem_mesh_in;
 
 /* Loads (PAPER.md:L191 Dirichlet/Neumann boundaries; L408-L412 external force;

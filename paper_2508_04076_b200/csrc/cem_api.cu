@@ -1073,7 +1073,7 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
 // ---------------------------------------------------------------- hexahedral contexts (N3)
 struct HexOffs {
     size_t hgeo, hconn, heedge, htau, e_off, e_inc, vhat, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
-        srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, total;
+        srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, epart, total;
 };
 HexOffs hex_layout(const HexHost &h) {
     Layout L;
@@ -1106,6 +1106,7 @@ HexOffs hex_layout(const HexHost &h) {
     o.node_orig = L.take<int32_t>(N);
     o.tet_orig = L.take<int32_t>(E);
     o.self = L.take<Dev>(1);
+    o.epart = L.take<double>((S + 255) / 256 + 3 * ((N + 255) / 256));
     o.total = L.off;
     return o;
 }
@@ -1224,6 +1225,9 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.node_orig = at<int32_t>(b, o.node_orig);
     d.tet_orig = at<int32_t>(b, o.tet_orig);
     d.self = at<Dev>(b, o.self);
+    ctx->epart = at<double>(b, o.epart);
+    ctx->n_epart_edges = (S + 255) / 256;
+    ctx->n_epart_nodes = (N + 255) / 256;
     d.lam = h.lam;
     d.mu = h.mu;
     d.l2m = h.l2m;
@@ -1826,16 +1830,17 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
 
 cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
     if (!ctx || !out) return CEM_EINVAL;
-    if (ctx->hexa) {
-        ctx->err = "cem_energy: tetrahedral contexts only";
-        return CEM_ESTATE;
-    }
     StreamFence fence(ctx);
     cudaStream_t st = ctx->stream;
     cem_state_out so{};
     const cem_status rc = cem_get_state(ctx, &so, CEM_HOST);  // synchronises; U_d, nonfinite
     if (rc != CEM_OK) return rc;
-    launch_energy(ctx->d, ctx->step, ctx->epart, ctx->epart + ctx->n_epart_edges, st);
+    if (ctx->hexa) {
+        launch_hex_energy(ctx->d, ctx->step, ctx->epart, ctx->epart + ctx->n_epart_edges, st);
+        ctx->launches += 1;
+    } else {
+        launch_energy(ctx->d, ctx->step, ctx->epart, ctx->epart + ctx->n_epart_edges, st);
+    }
     ctx->launches += 2;
     std::vector<double> pe(ctx->n_epart_edges + 3 * ctx->n_epart_nodes);
     CUDA_TRY(cudaMemcpyAsync(pe.data(), ctx->epart, sizeof(double) * pe.size(), cudaMemcpyDeviceToHost, st));

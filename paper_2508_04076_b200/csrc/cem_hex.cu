@@ -131,6 +131,43 @@ __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
     }
 }
 
+// strain energy of the edges of one 256-edge block on u_n (tau from k_hexA(n - 1)): psi(eps~_s)
+// Vhat_s / 12 with psi = 1/2 lam tr^2 + mu eps:eps (the hex oracle's hx_strain_energy), summed by a
+// fixed shuffle tree and the warps in order
+__global__ void __launch_bounds__(256) k_hex_energy_edges(Dev d, double *part) {
+    __shared__ double red[8];
+    const int64_t S = d.S, E = d.E;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double U = 0.0;
+    if (k < S) {
+        const double Vh = __ldg(d.vhat + k);
+        if (Vh != 0.0) {
+            double T[6] = {0, 0, 0, 0, 0, 0};
+            for (int32_t j = __ldg(d.e_off + k); j < __ldg(d.e_off + k + 1); ++j) {
+                const int64_t e = __ldg(d.e_inc + j);
+                if (!__ldcg(d.state + e)) continue;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.htau + c * E + e);
+            }
+            const double inv = 1.0 / Vh;
+            const double e11 = T[0] * inv, e22 = T[1] * inv, e33 = T[2] * inv, g12 = T[3] * inv, g23 = T[4] * inv,
+                         g13 = T[5] * inv;
+            const double tr = e11 + e22 + e33;
+            const double ee = e11 * e11 + e22 * e22 + e33 * e33 + 0.5 * (g12 * g12 + g23 * g23 + g13 * g13);
+            U = (0.5 * d.lam * tr * tr + d.mu * ee) * (Vh / 12.0);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) U = U + __shfl_down_sync(0xffffffffu, U, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = U;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = t + red[i];
+        part[blockIdx.x] = t;
+    }
+}
+
 template <class K, class... Args>
 void launch_pdl_h(K kern, unsigned grid, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
@@ -146,6 +183,13 @@ void launch_pdl_h(K kern, unsigned grid, cudaStream_t st, Args... args) {
 }
 
 }  // namespace
+
+void launch_hex_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st) {
+    const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)((d.S + 255) / 256);
+    k_hexA<<<ge, 256, 0, st>>>(d, n - 1);  // tau of u_n = ubuf[n & 1]
+    k_hex_energy_edges<<<gs, 256, 0, st>>>(d, part_edges);
+    launch_energy_nodes(d, n, part_nodes, st);
+}
 
 int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st) {
     const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)((d.S + 255) / 256);

@@ -311,6 +311,10 @@ void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 // cem_hex.cu: one explicit step of a hexahedral context (4 kernels, PDL-chained; stage D is the
 // tet path's node update); returns the kernels launched
 int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st);
+// energy ledger of a hexahedral context at step n: strain energy per edge block (U = sum_s
+// psi(eps~_s) Vhat_s / 12, R26) into part_edges[ceil(S/256)], node terms as the tet ledger
+void launch_hex_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
+void launch_energy_nodes(const Dev &d, int64_t n, double *part_nodes, cudaStream_t st);
 // stage D alone (cem_kernels.cu), PDL-chained after the previous kernel
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st);
 int persistent_occupancy(int smem_bytes, int blk);  // resident CTAs per SM of the persistent kernel

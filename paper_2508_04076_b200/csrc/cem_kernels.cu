@@ -2153,6 +2153,10 @@ int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every
     return (int)w.seq.size();
 }
 
+void launch_energy_nodes(const Dev &d, int64_t n, double *part_nodes, cudaStream_t st) {
+    k_energy_nodes<<<nblk(d.N), 256, 0, st>>>(d, n, part_nodes);
+}
+
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st) {
     k_energy_edges<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, n, part_edges);
     k_energy_nodes<<<nblk(d.N), 256, 0, st>>>(d, n, part_nodes);

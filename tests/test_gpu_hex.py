@@ -59,13 +59,31 @@ def test_hex_ragged_distorted_inactive_body_dirichlet(cells, seed):
     _assert_bitwise(sim, orc)
 
 
-def test_hex_rejects_cracking_and_energy():
+def test_hex_rejects_cracking():
     cem = _gpu()
     p = ci.hex_block((4, 3, 2))
     sim = cem.Simulation.from_problem(p)
     with pytest.raises(cem.CemError):
         sim.step(5, 1)
     with pytest.raises(cem.CemError):
-        sim.energy()
+        sim.crack_update()
     sim.step(5, 0)
     assert sim.state(records=False).step == 5
+
+
+def test_hex_energy_ledger():
+    """cem_energy on a hexahedral context: kinetic 1/2 sum m v.v, strain sum psi Vhat/12 (the hex
+    oracle's hx_strain_energy), external sum f.u -- equal to the oracle to the rounding of the sums --
+    and the discrete balance T + U ~ W of a traction-loaded block."""
+    p = ci.hex_block((10, 6, 3), dims=(0.05, 0.03, 0.015), seed=4)
+    sim, orc = _pair(p, 300)
+    e = sim.energy()
+    o = orc.state()
+    T = 0.5 * (o["m"][:, None] * o["v"] ** 2).sum()
+    W = (orc.fext() * o["u"]).sum()
+    U = orc.strain_energy(o["u"])
+    assert e["kinetic"] == pytest.approx(T, rel=1e-12)
+    assert e["strain"] == pytest.approx(U, rel=1e-12)
+    assert e["external"] == pytest.approx(W, rel=1e-12)
+    assert e["dissipated"] == 0.0 and e["step"] == 300
+    assert abs(e["kinetic"] + e["strain"] - e["external"]) <= 5e-3 * abs(e["external"])
