@@ -20,6 +20,7 @@ struct cem_ctx {
     Plan p;
     StagedSync sy;                // cumulative counts of the staged path (multi-GPU early signal)
     int cp_on = 0, cp_grid = 0;   // pipelined stage C (CEM_C_PIPE)
+    std::vector<StageChunk> chunks;  // AB / C launched in chunks (CEM_STAGE_CHUNKS > 1)
     WavePlan w;                   // dataflow launches (opt-in, CEM_WAVE=1; w.seq empty = off)
     int64_t wcnt_valid = -1;      // the wave counters are valid for this step count
     struct WaveGraph {
@@ -1448,6 +1449,8 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         return fail(CEM_EINVAL);
     }
     set_smem_limits(smem);
+    if (const char *ek = getenv("CEM_STAGE_CHUNKS"))
+        if (atoi(ek) > 1) ctx->chunks = build_stage_chunks(ctx->p, atoi(ek));
     {  // software-pipelined stage C (k_Cp): CEM_C_PIPE=1 (measured in DESIGN.md §6)
         const char *e = getenv("CEM_C_PIPE");
         int sms = 0;
@@ -1660,7 +1663,8 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
-            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx), &ctx->sy);
+            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx), &ctx->sy,
+                                                &ctx->chunks);
             if (ctx->p2p.on && ctx->host_allgather) {
                 // host-ordered: signal, wait for this rank's stores, meet the peers on the host, then
                 // the flag wait (already satisfied: it never spins) and the unpack
@@ -1763,7 +1767,8 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * kStagedEvents : nullptr;
-            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx), &ctx->sy);
+            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx), &ctx->sy,
+                                                &ctx->chunks);
         }
         CUDA_TRY(cudaGetLastError());
         if (ctx->profiling) ctx->prof_steps += nsteps;

@@ -302,10 +302,16 @@ constexpr int kStagedEvents = 5;  // profiled staged step: AB | C | criterion | 
 struct StagedSync {
     unsigned long long bdone = 0;  // cumulative boundary D blocks launched (early P2P signal)
 };
+// stage AB / C blocks of one chunk of a chunked staged step (CEM_STAGE_CHUNKS)
+struct StageChunk {
+    int ab0, ab1, c0, c1;
+};
+std::vector<StageChunk> build_stage_chunks(const Plan &p, int K);
 // heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit; sy: the
-// context's cumulative counts (multi-GPU early signal), may be null
+// context's cumulative counts (multi-GPU early signal), may be null; chunks: AB/C in chunks
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/,
-                       bool heavy = false, StagedSync *sy = nullptr);  // kernels launched
+                       bool heavy = false, StagedSync *sy = nullptr,
+                       const std::vector<StageChunk> *chunks = nullptr);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 // cem_hex.cu: one explicit step of a hexahedral context (4 kernels, PDL-chained; stage D is the

@@ -1717,15 +1717,15 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
 #define CEM_D_MINB 5
 #endif
 
-__global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s) {
+__global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s, int boff) {
     extern __shared__ __align__(16) double sm[];
     pdl_trigger();
-    block_AB(d, blockIdx.x, d.ubuf[(s + 1) & 1], sm);
+    block_AB(d, (int)blockIdx.x + boff, d.ubuf[(s + 1) & 1], sm);
 }
-__global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every) {
+__global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every, int boff) {
     extern __shared__ double sm[];
     pdl_trigger();
-    block_C(d, blockIdx.x, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true);
+    block_C(d, (int)blockIdx.x + boff, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true);
 }
 // full criterion of the tets stage C flagged (ctr[3] of them in crit_list), one warp per tet
 __global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
@@ -2082,18 +2082,47 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
 // kernels run concurrently with it, plus a fix-up kernel for the split nodes' masses -- config 3
 // 152.3 / 168.9 us per step steady / cracking vs 148.3 / 166.7.)
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, bool heavy,
-                       StagedSync *sy) {
+                       StagedSync *sy, const std::vector<StageChunk> *chunks) {
     unsigned long long bd = 0;  // early peer signal from stage D (P2P halo, boundary blocks first)
     if (sy && d.p2p_np && d.d_order && d.d_nbound > 0) bd = sy->bdone += (unsigned long long)d.d_nbound;
     const bool crit = crack_on(crack_every, s);
     const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
+    if (!ev && chunks && chunks->size() > 1) {
+        // AB and C in chunks along the storage order, AB(c) C(c) AB(c+1) ...: each C chunk reads
+        // only the AB chunks before it (chunk bounds from the plan), every kernel waits for its
+        // predecessor, so the chain is transitive; C(c) runs while AB(c)'s outputs are in L2
+        int n = 0;
+        for (const StageChunk &c : *chunks) {
+            if (c.ab1 > c.ab0) {
+                launch_pdl(k_AB, (unsigned)(c.ab1 - c.ab0), (unsigned)d.blk, (size_t)d.smem_ab, st, d, s, c.ab0);
+                ++n;
+            }
+            if (c.c1 > c.c0) {
+                launch_pdl(k_C, (unsigned)(c.c1 - c.c0), (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every, c.c0);
+                ++n;
+            }
+        }
+        if (crit) {
+            if (heavy) {
+                launch_pdl(k_filter, (unsigned)CEM_FILTER_GRID, 256u, (size_t)0, st, d, s);
+                launch_pdl(k_eval, (unsigned)CEM_CRITB_GRID, (unsigned)CEM_CRIT_THREADS, crit_smem_bytes(), st, d, s);
+                n += 2;
+            } else {
+                launch_pdl(k_crit, (unsigned)CEM_CRIT_GRID, 256u, (size_t)0, st, d, s);
+                ++n;
+            }
+        }
+        if (bd) launch_pdl(k_Db, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
+        else launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+        return n + 1;
+    }
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
-        launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s);
+        launch_pdl(k_AB, (unsigned)d.nblk[ST_AB], (unsigned)d.blk, (size_t)d.smem_ab, st, d, s, 0);
         if (d.cp_on)
             launch_pdl(k_Cp, (unsigned)d.cp_grid, 256u, (size_t)cp_smem_bytes(d.cp_max_el, d.cp_max_nl), st, d, s,
                        crack_every);
         else
-            launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every);
+            launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every, 0);
         if (crit) {
             if (heavy) {
                 launch_pdl(k_filter, (unsigned)CEM_FILTER_GRID, 256u, (size_t)0, st, d, s);
@@ -2107,12 +2136,12 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
         return crit ? (heavy ? 5 : 4) : 3;
     }
     cudaEventRecord(ev[0], st);
-    k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s);
+    k_AB<<<d.nblk[ST_AB], d.blk, d.smem_ab, st>>>(d, s, 0);
     cudaEventRecord(ev[1], st);
     if (d.cp_on)
         k_Cp<<<d.cp_grid, 256, cp_smem_bytes(d.cp_max_el, d.cp_max_nl), st>>>(d, s, crack_every);
     else
-        k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every);
+        k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every, 0);
     cudaEventRecord(ev[2], st);
     if (crit) {
         if (heavy) {

@@ -650,6 +650,24 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, 
     }    clk.mark("plan: dependencies");
 }
 
+// K chunks of stage-C blocks; chunk c is preceded by the AB blocks its edges need that earlier
+// chunks did not already launch (AB blocks of the edges of C blocks [0, c1) = prefix max)
+std::vector<StageChunk> build_stage_chunks(const Plan &p, int K) {
+    std::vector<StageChunk> out;
+    const int nC = p.nblk[ST_C], nAB = p.nblk[ST_AB];
+    K = std::max(1, std::min(K, nC));
+    int a = 0, m = -1, b = 0;
+    for (int c = 0; c < K; ++c) {
+        const int c1 = (int)((int64_t)nC * (c + 1) / K);
+        for (; b < c1; ++b)
+            for (int32_t i = p.el_off[b]; i < p.el_off[b + 1]; ++i) m = std::max(m, p.el[i] / p.blk_ab);
+        const int a1 = c + 1 == K ? nAB : std::max(a, m + 1);
+        out.push_back({a, a1, (int)((int64_t)nC * c / K), c1});
+        a = a1;
+    }
+    return out;
+}
+
 void build_wave(const Plan &p, int64_t N, int chunks, int lookahead, WavePlan &w) {
     const int nAB = p.nblk[ST_AB], nC = p.nblk[ST_C], nD = (int)((N + kDW - 1) / kDW);
     w.nblk[ST_AB] = nAB;
