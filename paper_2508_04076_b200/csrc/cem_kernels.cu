@@ -194,9 +194,6 @@ __device__ __forceinline__ void st_release_gpu(int32_t *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void wave_wait(const Dev &d, int g, int b, int need) {
-#ifdef CEM_WAVE_NOWAIT  // (timing experiment only: results are wrong)
-    return;
-#endif
     const int pg = g == ST_AB ? ST_D : g - 1;
     {  // every warp polls the block's producers itself (no barrier: warps start independently)
         const int lane = (int)(threadIdx.x & 31);
@@ -1906,11 +1903,7 @@ __global__ void __launch_bounds__(256, CEM_C_MINB) k_C_w(Dev d, int64_t s, int c
     pdl_trigger();
     s = wave_step(d, s, rel);
     const int b = (int)blockIdx.x + boff;
-#ifdef CEM_WAVE_DEFER  // (timing experiment only: the listed tets are never evaluated)
-    block_C(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true, (int)(s + 1));
-#else
     block_C(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, false, (int)(s + 1));
-#endif
     wave_done(d, ST_C, b, (int)(s + 1));
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D_w(Dev d, int64_t s, int boff, int rel) {

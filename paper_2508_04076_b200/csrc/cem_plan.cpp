@@ -202,6 +202,7 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, 
     const int64_t N = h.N, E = h.E, S = h.S;
     p.blk = blk;
     p.blk_ab = CEM_AB_EPT * blk;
+    if (const char *ea = getenv("CEM_AB_EDGES")) p.blk_ab = std::max(blk, atoi(ea));  // (edges per AB block)
     const int blk_ab = p.blk_ab;
     PhaseClock clk;
     // ---------------------------------------------------------------- sweep axis + slabs
