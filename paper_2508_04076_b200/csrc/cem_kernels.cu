@@ -160,6 +160,38 @@ __device__ __forceinline__ double node_mass(const Dev &d, int64_t k) {
     return acc;
 }
 
+// The same mass, computed by the node's four stage-D lanes together (called by all four, lane c
+// = threadIdx.x & 3): each round, lane c loads incidences j+4c .. j+4c+3 (one 16-B row load, then
+// their state and volume), so 16 incidences cost one round trip instead of four; every lane then
+// forms the identical sequential sum in ascending order from the shuffled terms.  An inactive
+// incidence contributes -0.0, which leaves any partial sum bit-for-bit unchanged (acc + -0 = acc),
+// so the sum equals node_mass()'s conditional one.
+__device__ __forceinline__ double node_mass4(const Dev &d, int64_t k, int c) {
+    const unsigned gm = 0xFu << (threadIdx.x & 28u);
+    const int g0 = (int)(threadIdx.x & 28u);
+    const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + k * d.wn);  // wn is a multiple of 8
+    double acc = 0.0;
+    for (int j = 0; j < d.wn; j += 16) {
+        const int4 q = j + 4 * c < d.wn ? __ldg(row + (j >> 2) + c) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+        const int32_t sl[4] = {q.x, q.y, q.z, q.w};
+        double x[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const bool ok = sl[t] != d.zslot;
+            const int64_t e = ok ? slot_tet(sl[t]) : 0;
+            const uint8_t st = ok ? __ldcg(d.state + e) : (uint8_t)0;
+            const double V = ok ? geo_V(d, (uint32_t)e) : 0.0;
+            x[t] = st ? (d.rho * V) / 4.0 : -0.0;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc = acc + __shfl_sync(gm, x[t], g0 + cc);
+        if (__shfl_sync(gm, q.w, g0 + 3) == d.zslot) break;  // padding only at the row's end
+    }
+    return acc;
+}
+
 // Shared-memory staging: a block's deduplicated producer records (u of its nodes, sigma of its
 // edges) are loaded once into component planes plane[c][row], so that every later per-thread
 // gather hits shared memory; rows are assigned bank-aware by the plan (cem_plan.cpp bank_rows).
@@ -807,11 +839,25 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
                                             int64_t rec_step, int32_t stamp, bool record, CritScratch &w) {
     const Dev &d = *dp;
     const int lane = threadIdx.x & 31;
+    // every load that depends only on e is issued first: the edge ids (lanes 0-5), then the nodes'
+    // X and u (lanes 0-3) and the edges' sigma, so that the eigen-solves start as soon as sigma
+    // arrives and the node loads land while they run
     const int4 t = __ldg(&d.conn[e]);
+    const int64_t es = lane < 6 ? ldro(d.eedge + (int64_t)lane * d.E + e) : 0;
+    const int n = lane == 0 ? t.x : (lane == 1 ? t.y : (lane == 2 ? t.z : t.w));
+    const int32_t orig = lane == 0 && record ? ldro(d.tet_orig + e) : 0;  // (the record, if it splits)
+    double4 x = make_double4(0.0, 0.0, 0.0, 0.0), uu = x;
     if (lane < 4) {
-        const int n = lane == 0 ? t.x : (lane == 1 ? t.y : (lane == 2 ? t.z : t.w));
-        const double4 x = ldro4(&d.X[n]);
-        const double4 uu = ldcg256(&u[n]);
+        x = ldro4(&d.X[n]);
+        uu = ldcg256(&u[n]);
+    }
+    Eig eg;
+    if (lane < 6) {
+        double s6[6];
+        load_sigma(d, es, s6);
+        principal(s6, eg);
+    }
+    if (lane < 4) {
         w.X[lane][0] = x.x;
         w.X[lane][1] = x.y;
         w.X[lane][2] = x.z;
@@ -828,10 +874,6 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
                          w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
         const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
         w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
-        double s6[6];
-        load_sigma(d, ldro(d.eedge + (int64_t)l * d.E + e), s6);
-        Eig eg;
-        principal(s6, eg);
         w.eg[l] = eg;
     }
     __syncwarp();
@@ -851,7 +893,31 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
             k = k2;
         }
     }
-    if (lane == 0 && G > gc) split_tet(d, e, t, G, k, A, rec_step, stamp, record);
+    // lane 0's selection decides for the whole warp (with a NaN G the butterfly need not agree)
+    G = __shfl_sync(0xffffffffu, G, 0);
+    if (G > gc) {  // split_tet's stores, spread over the lanes that hold their indices
+        A = __shfl_sync(0xffffffffu, A, 0);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (lane < 6) d.edge_dirty[es] = 1;  // their Vhat changes
+        if (lane < 4) d.dirty[n] = stamp;
+        if (lane == 0) {
+            d.state[e] = 0;
+            if (d.p2p_np && record) {
+                const int par = (int)((stamp > 0 ? rec_step - 1 : rec_step) & 1);
+                for (int32_t i = __ldg(d.p2p_toff + e); i < __ldg(d.p2p_toff + e + 1); ++i)
+                    d.p2p_recv[par * d.p2p_np + __ldg(d.p2p_tpeer + i)][__ldg(d.p2p_tbyte + i)] = 0;
+            }
+            if (record) {
+                const int slot = atomicAdd(&d.ctr[0], 1);
+                CEM_BOUND(d, slot < d.E);
+                d.rec_step[slot] = rec_step;
+                d.rec_elem[slot] = orig;
+                d.rec_cand[slot] = k;
+                d.rec_G[slot] = G;
+                d.rec_area[slot] = A;
+            }
+        }
+    }
     __syncwarp();  // the scratch is reused by the warp's next call
 }
 
@@ -1560,7 +1626,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     if (dirty == (int32_t)(s + 1)) {
         // an incident tet split in this step: lumped mass from the active incidences;
         // m = 0 -> frozen, v = a = 0 (R15)
-        mk = node_mass(d, k);
+        mk = node_mass4(d, k, c);
         if (c == 0) d.mass[k] = mk;
         if (mk == 0.0) vv = aa = 0.0;
     }
