@@ -1638,6 +1638,12 @@ cem_status cem_set_profiling(cem_ctx *ctx, int on) {
 
 // long criterion lists (cracking phases) go to k_filter + k_eval; CEM_CRITB_MIN overrides the threshold
 bool crit_heavy(const cem_ctx *ctx) { return ctx->crit_seen && *ctx->crit_seen >= ctx->critb_min; }
+// the staged path's criterion mode from the recent list length (racy by design: results never depend on it)
+int crit_mode(const cem_ctx *ctx) {
+    if (!ctx->crit_seen) return CRIT_LIST;
+    const int n = *ctx->crit_seen;
+    return n >= ctx->critb_min ? CRIT_HEAVY : CRIT_LIST;
+}
 
 cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (!ctx || nsteps < 0) return CEM_EINVAL;
@@ -1663,7 +1669,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t sstep = ctx->step + i;
-            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(ctx), &ctx->sy,
+            ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, crit_mode(ctx), &ctx->sy,
                                                 &ctx->chunks);
             if (ctx->p2p.on && ctx->host_allgather) {
                 // host-ordered: signal, wait for this rank's stores, meet the peers on the host, then
@@ -1743,7 +1749,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
                     ctx->launches += 1;
                     in_wave = false;
                 }
-                ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, true);
+                ctx->launches += launch_staged_step(ctx->d, sstep, crack_every, ctx->stream, nullptr, CRIT_HEAVY);
             }
         }
         if (in_wave) {
@@ -1767,7 +1773,7 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
         }
         for (int64_t i = 0; i < nsteps; ++i) {
             cudaEvent_t *E = ctx->profiling ? ctx->ev.data() + (ctx->prof_steps + i) * kStagedEvents : nullptr;
-            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_heavy(ctx), &ctx->sy,
+            ctx->launches += launch_staged_step(ctx->d, ctx->step + i, crack_every, ctx->stream, E, crit_mode(ctx), &ctx->sy,
                                                 &ctx->chunks);
         }
         CUDA_TRY(cudaGetLastError());
@@ -2068,7 +2074,8 @@ cem_status cem_step_group(cem_ctx **c, int32_t n, int64_t nsteps, int32_t crack_
     for (int64_t i = 0; i < nsteps; ++i) {
         const int64_t sstep = c[0]->step + i;
         for (int r = 0; r < n; ++r) {
-            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr, crit_heavy(c[r]), &c[r]->sy);
+            c[r]->launches += launch_staged_step(c[r]->d, sstep, crack_every, ctx->stream, nullptr,
+                                                    crit_heavy(c[r]) ? CRIT_HEAVY : CRIT_LIST, &c[r]->sy);
         }
         if (c[0]->p2p.on) {  // the stores went straight into the peers' buffers; stream order syncs
             for (int r = 0; r < n; ++r) {

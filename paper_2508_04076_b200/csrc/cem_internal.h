@@ -307,10 +307,13 @@ struct StageChunk {
     int ab0, ab1, c0, c1;
 };
 std::vector<StageChunk> build_stage_chunks(const Plan &p, int K);
-// heavy: the criterion list is long (recent steps): k_filter + k_eval instead of k_crit; sy: the
-// context's cumulative counts (multi-GPU early signal), may be null; chunks: AB/C in chunks
+// crit: how the criterion runs, from the recent list lengths -- CRIT_LIST: stage C lists the
+// tets that fail the early-out, k_crit evaluates them (one warp each); CRIT_HEAVY (long lists):
+// k_filter + k_eval instead of k_crit.  sy: the context's cumulative counts (multi-GPU early
+// signal), may be null; chunks: AB/C in chunks
+enum { CRIT_LIST = 0, CRIT_HEAVY = 1 };
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/,
-                       bool heavy = false, StagedSync *sy = nullptr,
+                       int crit = CRIT_LIST, StagedSync *sy = nullptr,
                        const std::vector<StageChunk> *chunks = nullptr);  // kernels launched
 void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);

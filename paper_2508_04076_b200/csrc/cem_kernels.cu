@@ -727,41 +727,36 @@ struct CritScratch {
 
 static_assert(sizeof(CritScratch) <= 1024, "stage C's staging area holds 8 warp scratches of <= 1 KB");
 
+// Candidate k of a tet (R7): both patterns through one instruction stream (no divergent branch
+// per pattern or per Heaviside flag: selects instead), so a warp evaluating 24 candidates side by
+// side runs one division and one square root per lane.  Every value is the same expression as
+// the oracle's (orc candidate): pattern I  A1 = S(s_pr,m) Dd_p, A2 = S(s_qr,m) Dd_q,
+// G = (1/2 (A1 + A2)) / |m|^2, area |m| / 4; pattern II  G = (1/2 (S(s_cr,m) (Dd_p + Dd_q))) / |m|^2,
+// area |m| / 8 (x / 4 and x * 0.25 are the same correctly rounded value); Dd = 0 where H = 0.
 __device__ void candidate(const CritScratch &w, int k, bool both, double &G, double &area) {
     const int c = k / 6, f = (k % 6) / 2, tt = k & 1;
-    int o[3], no = 0;
-    for (int b = 0; b < 4; ++b)
-        if (b != c) o[no++] = b;
-    const int p = o[f == 2 ? 1 : 0], q = o[f == 0 ? 1 : 2], r = o[2 - f];
+    // the other three nodes in ascending order, o0 < o1 < o2
+    const int o0 = c == 0 ? 1 : 0, o1 = c <= 1 ? 2 : 1, o2 = c <= 2 ? 3 : 2;
+    const int p = f == 2 ? o1 : o0, q = f == 0 ? o1 : o2, r = f == 0 ? o2 : (f == 1 ? o1 : o0);
     auto X = [&](int a) { return Vec3{w.X[a][0], w.X[a][1], w.X[a][2]}; };
     auto U = [&](int a) { return Vec3{w.U[a][0], w.U[a][1], w.U[a][2]}; };
-    const Vec3 d1 = vsub(X(q), X(p));
-    const Vec3 d2 = tt == 0 ? vsub(X(r), X(c)) : vsub(X(r), X(p));
+    const Vec3 Xc = X(c), Xp = X(p), Xq = X(q), Xr = X(r);
+    const Vec3 d1 = vsub(Xq, Xp);
+    const Vec3 d2 = vsub(Xr, tt == 0 ? Xc : Xp);
     const Vec3 mv = vcross(d1, d2);
     const double mm = vdot(mv, mv);
-    double Dd[2];
-    const int ends[2] = {p, q};
-    for (int z = 0; z < 2; ++z) {
-        const int b = ends[z];
-        if (!w.H[ledge(c, b)]) {
-            Dd[z] = 0.0;
-            continue;
-        }
-        const Vec3 du = vsub(U(b), U(c)), dX = vsub(X(b), X(c));
-        Dd[z] = vdot(du, mv) * dsgn(vdot(dX, mv));
-    }
-    if (tt == 0) {
-        const double A1 = sig_proj(w.eg[ledge(p, r)], mv) * Dd[0];
-        const double A2 = sig_proj(w.eg[ledge(q, r)], mv) * Dd[1];
-        G = (0.5 * (A1 + A2)) / mm;
-        area = sqrt(mm) / 4.0;
-    } else {
-        const double Sg = sig_proj(w.eg[ledge(c, r)], mv);
-        G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
-        area = sqrt(mm) / 8.0;
-    }
+    const Vec3 Uc = U(c);
+    const bool hp = w.H[ledge(c, p)], hq = w.H[ledge(c, q)];
+    const double vp = vdot(vsub(U(p), Uc), mv) * dsgn(vdot(vsub(Xp, Xc), mv));
+    const double vq = vdot(vsub(U(q), Uc), mv) * dsgn(vdot(vsub(Xq, Xc), mv));
+    const double Dp = hp ? vp : 0.0, Dq = hq ? vq : 0.0;
+    const double S1 = sig_proj(w.eg[tt == 0 ? ledge(p, r) : ledge(c, r)], mv);
+    const double S2 = sig_proj(w.eg[ledge(q, r)], mv);  // (pattern I only)
+    const double num = tt == 0 ? S1 * Dp + S2 * Dq : S1 * (Dp + Dq);
+    G = (0.5 * num) / mm;
+    area = sqrt(mm) * (tt == 0 ? 0.25 : 0.125);
     // R11 variant (CEM_F_FRONT_BOTH_STRETCHED): the front must be stretched at both edges
-    if (both && !(w.H[ledge(c, p)] && w.H[ledge(c, q)])) G = 0.0;
+    if (both && !(hp && hq)) G = 0.0;
 }
 
 __device__ __forceinline__ void split_tet(const Dev &d, int64_t e, int4 t, double G, int k, double A, int64_t rec_step,
@@ -835,10 +830,25 @@ __device__ __noinline__ void criterion_lane(const Dev *__restrict__ dp, int64_t 
     if (Gb > gc) split_tet(d, e, t, Gb, kb, Ab, rec_step, stamp, record);
 }
 
-__device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc,
-                                            int64_t rec_step, int32_t stamp, bool record, CritScratch &w) {
-    const Dev &d = *dp;
+#ifdef CEM_CRIT_TRACE
+// (measurement build only) SM clock after the value v has arrived: the setp consumes v
+__device__ __forceinline__ long long clk_after(double v) {
+    long long t;
+    asm volatile("{ .reg .pred p; setp.eq.f64 p, %1, 0d7FF0DEADBEEF0001; mov.u64 %0, %%clock64; @p mov.u64 %0, 0; }"
+                 : "=l"(t) : "d"(v) : "memory");
+    return t;
+}
+#define CT(i, v) tr[i] = clk_after((double)(v))
+#else
+#define CT(i, v) ((void)0)
+#endif
+__device__ __forceinline__ void criterion_warp_body(const Dev &d, int64_t e, const double4 *u, double gc,
+                                                    int64_t rec_step, int32_t stamp, bool record, CritScratch &w) {
     const int lane = threadIdx.x & 31;
+#ifdef CEM_CRIT_TRACE
+    long long tr[10] = {0};
+    CT(0, e);
+#endif
     // every load that depends only on e is issued first: the edge ids (lanes 0-5), then the nodes'
     // X and u (lanes 0-3) and the edges' sigma, so that the eigen-solves start as soon as sigma
     // arrives and the node loads land while they run
@@ -854,8 +864,11 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
     Eig eg;
     if (lane < 6) {
         double s6[6];
+        CT(1, t.x + es);
         load_sigma(d, es, s6);
+        CT(2, s6[0] + s6[5]);
         principal(s6, eg);
+        CT(3, eg.l[0] + eg.ev[2][2]);
     }
     if (lane < 4) {
         w.X[lane][0] = x.x;
@@ -868,10 +881,11 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
     __syncwarp();
     if (lane < 6) {
         const int l = lane;
-        const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
-                         w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
-        const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
-                         w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
+        // local edge l = (ep, eq): (0,1) (0,2) (0,3) (1,2) (1,3) (2,3) -- c_ep / c_eq without
+        // lane-divergent constant-bank reads
+        const int ep = l < 3 ? 0 : (l < 5 ? 1 : 2), eq = l < 3 ? l + 1 : (l == 3 ? 2 : 3);
+        const Vec3 du = {w.U[eq][0] - w.U[ep][0], w.U[eq][1] - w.U[ep][1], w.U[eq][2] - w.U[ep][2]};
+        const Vec3 dX = {w.X[eq][0] - w.X[ep][0], w.X[eq][1] - w.X[ep][1], w.X[eq][2] - w.X[ep][2]};
         const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
         w.H[l] = vdot(du, ww) > 0.0;  // eq:stretch-delta Heaviside, R6
         w.eg[l] = eg;
@@ -894,7 +908,13 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
         }
     }
     // lane 0's selection decides for the whole warp (with a NaN G the butterfly need not agree)
+    CT(4, G);
     G = __shfl_sync(0xffffffffu, G, 0);
+#ifdef CEM_CRIT_TRACE
+    if (lane == 0 && blockIdx.x < 3 && threadIdx.x == 0)
+        printf("[crit] blk %d: eedge+conn %lld  sigma %lld  jacobi %lld  cand+argmax %lld  (G %.3g gc %.3g)\n", blockIdx.x,
+               tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], G, gc);
+#endif
     if (G > gc) {  // split_tet's stores, spread over the lanes that hold their indices
         A = __shfl_sync(0xffffffffu, A, 0);
         k = __shfl_sync(0xffffffffu, k, 0);
@@ -919,6 +939,13 @@ __device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t 
         }
     }
     __syncwarp();  // the scratch is reused by the warp's next call
+}
+
+// (out of line for the stage-C callers, whose register budget it must not raise; k_crit inlines the
+// body and reads the Dev fields from its parameter bank instead of through d.self)
+__device__ __noinline__ void criterion_warp(const Dev *__restrict__ dp, int64_t e, const double4 *u, double gc,
+                                            int64_t rec_step, int32_t stamp, bool record, CritScratch &w) {
+    criterion_warp_body(*dp, e, u, gc, rec_step, stamp, record, w);
 }
 
 // Refined early-out of one listed tet, evaluated by one thread (k_filter).  Candidate k
@@ -1795,14 +1822,24 @@ __global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
     __shared__ CritScratch scratch[8];
     pdl_trigger();
     pdl_wait();  // the list and the sigma records come from stage C / AB
+#ifdef CEM_CRIT_TRACE
+    const long long k0 = clock64();
+#endif
+    const int i0 = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    // the warp's first list entry is read together with the list length (speculatively: the
+    // list holds E entries, the value is used only if i0 < n)
+    const int32_t e0 = i0 < d.E ? __ldcg(d.crit_list + i0) : 0;
     const int n = *(volatile int32_t *)&d.ctr[3];
     const int nw = (int)(gridDim.x * (blockDim.x >> 5));
     const double4 *u = d.ubuf[(s + 1) & 1];
-    for (int i = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); i < n; i += nw) {
-        const int64_t e = d.crit_list[i];
+#ifdef CEM_CRIT_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 3) printf("[crit] blk %d: n %d, list+ctr %lld cycles\n", blockIdx.x, n, clk_after((double)(n + e0)) - k0);
+#endif
+    for (int i = i0; i < n; i += nw) {
+        const int64_t e = i == i0 ? e0 : d.crit_list[i];
         CEM_BOUND(d, n <= d.E && e >= 0 && e < d.E);
-        criterion_warp(d.self, e, u, ldro(d.gc + e), s + 1, (int32_t)(s + 1), (__ldg(d.tflag + e) & 2) != 0,
-                       scratch[threadIdx.x >> 5]);
+        criterion_warp_body(d, e, u, ldro(d.gc + e), s + 1, (int32_t)(s + 1), (__ldg(d.tflag + e) & 2) != 0,
+                            scratch[threadIdx.x >> 5]);
     }
 }
 
@@ -2140,8 +2177,9 @@ void launch_pdl(K kern, unsigned grid, unsigned blk, size_t smem, cudaStream_t s
 // (Measured and rejected: stage D waiting on stage C's block-completion count so that the criterion
 // kernels run concurrently with it, plus a fix-up kernel for the split nodes' masses -- config 3
 // 152.3 / 168.9 us per step steady / cracking vs 148.3 / 166.7.)
-int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, bool heavy,
+int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev, int cmode,
                        StagedSync *sy, const std::vector<StageChunk> *chunks) {
+    const bool heavy = cmode == CRIT_HEAVY;
     unsigned long long bd = 0;  // early peer signal from stage D (P2P halo, boundary blocks first)
     if (sy && d.p2p_np && d.d_order && d.d_nbound > 0) bd = sy->bdone += (unsigned long long)d.d_nbound;
     const bool crit = crack_on(crack_every, s);

@@ -16,7 +16,7 @@ import paper_2508_04076_b200 as cem  # noqa: E402
 cfg = int(os.environ.get("CEM_CFG", "3"))
 p = ci.config(cfg)
 KNOBS = ("CEM_WAVE", "CEM_WAVE_K", "CEM_WAVE_LA", "CEM_GRAPH_M", "CEM_WAVE_DISCARD", "CEM_L2_PERSIST", "CEM_CRITB_MIN",
-         "CEM_C_PIPE", "CEM_STAGE_CHUNKS", "CEM_AB_EDGES")
+         "CEM_C_PIPE", "CEM_STAGE_CHUNKS", "CEM_AB_EDGES", "CEM_CRITB_MIN")
 
 
 def timed(sim, n):
