@@ -63,6 +63,7 @@ struct cem_ctx {
     void *host_user = nullptr;
     volatile int32_t *crit_seen = nullptr;  // mapped: criterion-list length of a recent step
     int critb_min = 1024;         // lists at least this long use k_filter + k_eval (env CEM_CRITB_MIN at init)
+    bool crit_stream = true;      // k_crit takes its entries while stage C runs (env CEM_CRIT_STREAM=0: after it)
     double *epart = nullptr;      // energy-ledger partials (device)
     int64_t n_epart_edges = 0, n_epart_nodes = 0;
 };
@@ -127,7 +128,7 @@ struct Offs {
     size_t rec_step, rec_elem, rec_cand, rec_G, rec_area, cnt, dep_off, dep, sched, head;
     size_t nl_off, nl, lconn, el_off, el, ledge, tl_off, tl, self, ncons, cons_done;
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
-    size_t rprev, wr_dof, epart, crit_list, vhat, edge_dirty, e_off, e_inc, edge_own;
+    size_t rprev, wr_dof, epart, crit_list, crit_surv, vhat, edge_dirty, e_off, e_inc, edge_own;
     size_t wcnt, wdep_off, wdep, wstep, wncons, wcons_done;
     size_t total;
 };
@@ -192,7 +193,8 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.wr_dof = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.epart = L.take<double>(p.nblk[ST_AB] + 3 * ((N + 255) / 256));
-    o.crit_list = L.take<int32_t>(2 * E);  // the step's list + the refined filter's survivors
+    o.crit_list = L.take<int64_t>(E);  // the step's list (stamped entries)
+    o.crit_surv = L.take<int32_t>(E);  // the refined filter's survivors
     o.vhat = L.take<double>(S);
     o.edge_dirty = L.take<uint8_t>(S);
     o.e_off = L.take<int32_t>(S + 1);
@@ -308,7 +310,8 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     for (int g = 0; g < ST_COUNT; ++g) d.nblk[g] = p.nblk[g];
     d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
     d.wr_dof = at<double>(b, o.wr_dof);
-    d.crit_list = at<int32_t>(b, o.crit_list);
+    d.crit_list = at<int64_t>(b, o.crit_list);
+    d.crit_surv = at<int32_t>(b, o.crit_surv);
     d.vhat = at<double>(b, o.vhat);
     d.edge_dirty = at<uint8_t>(b, o.edge_dirty);
     d.e_off = at<int32_t>(b, o.e_off);
@@ -501,6 +504,7 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, sizeof(double) * CEM_FES * fe_slots(E), st));
     int32_t ctr[32] = {0, 0, INT32_MAX};
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.crit_list), 0, sizeof(int64_t) * E, st));  // stamp 0: no step's entry
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.cnt), 0, sizeof(int32_t) * ST_COUNT * p.maxblk, st));
     CUDA_TRY(put(o.dep_off, p.dep_off.data(), sizeof(int32_t) * p.dep_off.size()));
     CUDA_TRY(put(o.dep, p.dep.data(), sizeof(int32_t) * p.dep.size()));
@@ -1528,6 +1532,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         }
         *static_cast<int32_t *>(hp) = 0;
         if (const char *m = getenv("CEM_CRITB_MIN")) ctx->critb_min = atoi(m);
+        if (const char *m = getenv("CEM_CRIT_STREAM")) ctx->crit_stream = atoi(m) != 0;
         ctx->crit_seen = static_cast<volatile int32_t *>(hp);
         ctx->d.crit_seen = static_cast<int32_t *>(dp);
     }
@@ -1642,7 +1647,9 @@ bool crit_heavy(const cem_ctx *ctx) { return ctx->crit_seen && *ctx->crit_seen >
 int crit_mode(const cem_ctx *ctx) {
     if (!ctx->crit_seen) return CRIT_LIST;
     const int n = *ctx->crit_seen;
-    return n >= ctx->critb_min ? CRIT_HEAVY : CRIT_LIST;
+    if (n >= ctx->critb_min) return CRIT_HEAVY;
+    if (!ctx->crit_stream) return CRIT_LIST;
+    return n == 0 ? CRIT_IDLE : CRIT_STREAM;
 }
 
 cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {

@@ -244,8 +244,10 @@ struct Dev {
     int cp_on, cp_grid;        // 1: stage C runs as k_Cp on cp_grid persistent CTAs
     const Dev *self;           // device-resident copy of this struct (for noinline helpers)
     int32_t *ctr;              // [0] records, [1] nonfinite, [2] first bad node (orig), [3] crit_list length,
-                               // [8] survivors of the refined filter (crit_list + E)
-    int32_t *crit_list;        // [E] tets stage C flagged for the full criterion this step (staged path)
+                               // [8] survivors of the refined filter (crit_surv)
+    int64_t *crit_list;        // [E] tets stage C flagged for the full criterion, entry (step + 1) << 32 | e
+                               // (stamped: k_crit polls the entries of its own step while stage C runs)
+    int32_t *crit_surv;        // [E] survivors of the refined filter (k_filter -> k_eval)
     int32_t *crit_seen;        // mapped host int: stage D writes the step's list length (kernel choice)
     double *vhat;              // [S] Vhat_s = sum V_e over the active incident tets (original order)
     uint8_t *edge_dirty;       // [S] 1: an incident tet split since stage AB last recomputed vhat[s]
@@ -308,10 +310,11 @@ struct StageChunk {
 };
 std::vector<StageChunk> build_stage_chunks(const Plan &p, int K);
 // crit: how the criterion runs, from the recent list lengths -- CRIT_LIST: stage C lists the
-// tets that fail the early-out, k_crit evaluates them (one warp each); CRIT_HEAVY (long lists):
-// k_filter + k_eval instead of k_crit.  sy: the context's cumulative counts (multi-GPU early
-// signal), may be null; chunks: AB/C in chunks
-enum { CRIT_LIST = 0, CRIT_HEAVY = 1 };
+// tets that fail the early-out, k_crit evaluates them after stage C (one warp each); CRIT_STREAM:
+// k_crit takes the entries while stage C is still running; CRIT_IDLE: the same with a small grid
+// (no recent list: fewer pollers); CRIT_HEAVY (long lists): k_filter + k_eval instead of k_crit.
+// sy: the context's cumulative counts (multi-GPU early signal), may be null; chunks: AB/C in chunks
+enum { CRIT_LIST = 0, CRIT_HEAVY = 1, CRIT_STREAM = 2, CRIT_IDLE = 3 };
 int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st, cudaEvent_t *ev /*5 or null*/,
                        int crit = CRIT_LIST, StagedSync *sy = nullptr,
                        const std::vector<StageChunk> *chunks = nullptr);  // kernels launched

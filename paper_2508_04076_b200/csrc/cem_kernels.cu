@@ -50,6 +50,9 @@ namespace {
 // read-only tables: non-coherent path
 __device__ __forceinline__ double ldro(const double *p) { return __ldg(p); }
 __device__ __forceinline__ int ldro(const int32_t *p) { return __ldg(p); }
+// criterion-list entry of step s's crack check (rec_step = s + 1): the stamp tells k_crit's
+// pollers an entry of their own step from one left by an earlier step
+__device__ __forceinline__ int64_t crit_entry(int64_t rec_step, int64_t e) { return (rec_step << 32) | e; }
 __device__ __forceinline__ double4 ldro4(const double4 *p) {
     const double2 *q = reinterpret_cast<const double2 *>(p);
     const double2 a = __ldg(q), b = __ldg(q + 1);
@@ -893,10 +896,12 @@ __device__ __forceinline__ void criterion_warp_body(const Dev &d, int64_t e, con
     __syncwarp();
     double G = -INFINITY, A = -INFINITY;
     int k = 1 << 20;
+    CT(5, w.H[0]);
     if (lane < 24) {
         candidate(w, lane, (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0, G, A);
         k = lane;
     }
+    CT(6, G + A);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const double G2 = __shfl_xor_sync(0xffffffffu, G, o), A2 = __shfl_xor_sync(0xffffffffu, A, o);
@@ -912,8 +917,8 @@ __device__ __forceinline__ void criterion_warp_body(const Dev &d, int64_t e, con
     G = __shfl_sync(0xffffffffu, G, 0);
 #ifdef CEM_CRIT_TRACE
     if (lane == 0 && blockIdx.x < 3 && threadIdx.x == 0)
-        printf("[crit] blk %d: eedge+conn %lld  sigma %lld  jacobi %lld  cand+argmax %lld  (G %.3g gc %.3g)\n", blockIdx.x,
-               tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], G, gc);
+        printf("[crit] blk %d: eedge+conn %lld  sigma %lld  jacobi %lld  heaviside %lld  cand %lld  argmax %lld\n", blockIdx.x,
+               tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[5] - tr[3], tr[6] - tr[5], tr[4] - tr[6]);
 #endif
     if (G > gc) {  // split_tet's stores, spread over the lanes that hold their indices
         A = __shfl_sync(0xffffffffu, A, 0);
@@ -1219,14 +1224,17 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     if (!crack) return;  // block-uniform
     if (defer) {
         // staged path: append the flagged tets to the step's list (warp-aggregated); k_crit
-        // evaluates them all concurrently, one warp per tet, before stage D
+        // evaluates them all concurrently, one warp per tet, as they appear (it polls the
+        // entries while stage C runs); ctr[9] counts the stage-C blocks that got here, a hint
+        // only (k_crit stops polling at the block count, then waits for stage C's completion)
+        if (threadIdx.x == 0) atomicAdd(&d.ctr[9], 1);
         const unsigned mm = __ballot_sync(0xffffffffu, need);
         if (mm) {
             const int lane = threadIdx.x & 31, lead = __ffs(mm) - 1;
             int base = 0;
             if (lane == lead) base = atomicAdd(&d.ctr[3], __popc(mm));
             base = __shfl_sync(0xffffffffu, base, lead);
-            if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = (int32_t)e;
+            if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = crit_entry(rec_step, e);
         }
         return;
     }
@@ -1473,12 +1481,12 @@ __global__ void __launch_bounds__(256, 1) k_Cp(Dev d, int64_t s, int crack_every
                 int base = 0;
                 if (lane == lead) base = atomicAdd(&d.ctr[3], __popc(mm));
                 base = __shfl_sync(0xffffffffu, base, lead);
-                if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = (int32_t)e;
+                if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = crit_entry(rec_step, e);
             }
+            if (threadIdx.x == 0) atomicAdd(&d.ctr[9], 1);  // (k_crit's polling hint, as in block_C)
         }
         __syncthreads();  // this data slot is refilled by the copies issued in iteration j + 1
     }
-    (void)rec_step;
     (void)stamp;
 }
 
@@ -1515,6 +1523,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
 #endif
         d.ctr[3] = 0;
         d.ctr[8] = 0;
+        d.ctr[9] = 0;
     }
     if (k >= kend) return;
     const uint8_t fl = __ldg(&d.nflag[k]);
@@ -1817,28 +1826,65 @@ __global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int cra
     pdl_trigger();
     block_C(d, (int)blockIdx.x + boff, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true);
 }
-// full criterion of the tets stage C flagged (ctr[3] of them in crit_list), one warp per tet
-__global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s) {
+// full criterion of the tets stage C flagged (ctr[3] of them in crit_list), one warp per tet.
+// Its inputs other than the list (sigma from stage AB, u, X, the tables) are final before stage C
+// writes any entry, and its outputs (the split tets' state, Vhat flags, node stamps, records) are
+// read only by stage D and the next step -- never by stage C, which is done with a tet when it
+// lists it.  So the warps take their entries while stage C is still running (PDL launches k_crit
+// once every stage-C block has started): the warp owning list index i polls it (relaxed, no L1
+// invalidation, with a back-off) until it holds an entry stamped with this step -- visible only
+// after stage C passed its wait, hence after every earlier kernel completed -- or stage C's blocks
+// have all reached their list append (ctr[9], a hint) or a poll budget runs out; then it waits for
+// stage C's completion (griddepcontrol.wait: the list and its length ctr[3] are final) and takes
+// its remaining indices.  Every listed tet is evaluated exactly once, by the warp owning its
+// index, with the same inputs whatever the timing.
+__device__ __forceinline__ long long ld_relaxed64(const int64_t *p) {
+    long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+#ifndef CEM_CRIT_POLLS
+#define CEM_CRIT_POLLS 256  // poll budget per warp before the completion wait (a safety bound)
+#endif
+#ifndef CEM_CRIT_IGRID
+#define CEM_CRIT_IGRID 37  // k_crit blocks when no recent step had a list (fewer pollers beside stage C's tail)
+#endif
+__global__ void __launch_bounds__(256) k_crit(Dev d, int64_t s, int poll_budget) {
     __shared__ CritScratch scratch[8];
     pdl_trigger();
-    pdl_wait();  // the list and the sigma records come from stage C / AB
-#ifdef CEM_CRIT_TRACE
-    const long long k0 = clock64();
-#endif
-    const int i0 = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-    // the warp's first list entry is read together with the list length (speculatively: the
-    // list holds E entries, the value is used only if i0 < n)
-    const int32_t e0 = i0 < d.E ? __ldcg(d.crit_list + i0) : 0;
-    const int n = *(volatile int32_t *)&d.ctr[3];
+    const int lane = threadIdx.x & 31;
     const int nw = (int)(gridDim.x * (blockDim.x >> 5));
     const double4 *u = d.ubuf[(s + 1) & 1];
-#ifdef CEM_CRIT_TRACE
-    if (threadIdx.x == 0 && blockIdx.x < 3) printf("[crit] blk %d: n %d, list+ctr %lld cycles\n", blockIdx.x, n, clk_after((double)(n + e0)) - k0);
-#endif
-    for (int i = i0; i < n; i += nw) {
-        const int64_t e = i == i0 ? e0 : d.crit_list[i];
-        CEM_BOUND(d, n <= d.E && e >= 0 && e < d.E);
-        criterion_warp_body(d, e, u, ldro(d.gc + e), s + 1, (int32_t)(s + 1), (__ldg(d.tflag + e) & 2) != 0,
+    const int64_t rec = s + 1;
+    int i = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    // phase 1: entries as stage C writes them
+    for (int polls = 0; i < d.E && polls < poll_budget;) {
+        long long v = 0;
+        int done = 0;
+        if (lane == 0) {
+            v = ld_relaxed64(d.crit_list + i);
+            if ((v >> 32) != rec) done = ld_relaxed(&d.ctr[9]) >= d.nblk[ST_C];
+        }
+        v = __shfl_sync(0xffffffffu, v, 0);
+        if ((v >> 32) == rec) {
+            const int64_t e = (int32_t)(v & 0xffffffff);
+            CEM_BOUND(d, e >= 0 && e < d.E);
+            criterion_warp_body(d, e, u, ldro(d.gc + e), rec, (int32_t)rec, (__ldg(d.tflag + e) & 2) != 0,
+                                scratch[threadIdx.x >> 5]);
+            i += nw;
+            continue;
+        }
+        if (__shfl_sync(0xffffffffu, done, 0)) break;
+        ++polls;
+        __nanosleep(256);
+    }
+    // phase 2: stage C complete, the list final
+    pdl_wait();
+    const int n = *(volatile int32_t *)&d.ctr[3];
+    for (; i < n; i += nw) {
+        const int64_t e = (int32_t)(d.crit_list[i] & 0xffffffff);
+        CEM_BOUND(d, n <= d.E && e >= 0 && e < d.E && (d.crit_list[i] >> 32) == rec);
+        criterion_warp_body(d, e, u, ldro(d.gc + e), rec, (int32_t)rec, (__ldg(d.tflag + e) & 2) != 0,
                             scratch[threadIdx.x >> 5]);
     }
 }
@@ -1869,7 +1915,7 @@ __global__ void __launch_bounds__(256, CEM_FILTER_MINB) k_filter(Dev d, int64_t 
         int32_t e = 0;
         bool need = false;
         if (i < n) {
-            e = d.crit_list[i];
+            e = (int32_t)(d.crit_list[i] & 0xffffffff);
             CEM_BOUND(d, n <= d.E && e >= 0 && e < d.E);
             // CEM_F_NO_EARLY_OUT: every listed tet gets the full 24-candidate evaluation
             need = (d.flags & CEM_F_NO_EARLY_OUT) || crit_refined_need(d.self, e, u, ldro(d.gc + e));
@@ -1880,7 +1926,7 @@ __global__ void __launch_bounds__(256, CEM_FILTER_MINB) k_filter(Dev d, int64_t 
             int base = 0;
             if (lane == lead) base = atomicAdd(&d.ctr[8], __popc(mm));
             base = __shfl_sync(0xffffffffu, base, lead);
-            if (need) d.crit_list[d.E + base + __popc(mm & ((1u << lane) - 1u))] = e;
+            if (need) d.crit_surv[base + __popc(mm & ((1u << lane) - 1u))] = e;
         }
     }
 }
@@ -1893,7 +1939,7 @@ __global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_eval(Dev d
     const int nw = (int)(gridDim.x * (blockDim.x >> 5));
     const double4 *u = d.ubuf[(s + 1) & 1];
     const int lane = threadIdx.x & 31;
-    const int32_t *ids = d.crit_list + d.E;
+    const int32_t *ids = d.crit_surv;
     for (int b0 = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kCB; b0 < ns; b0 += nw * kCB) {
         const int cnt = min(kCB, ns - b0);
         if (lane < 4 * cnt) {  // (j, a): node a of tet j
@@ -2183,7 +2229,9 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     unsigned long long bd = 0;  // early peer signal from stage D (P2P halo, boundary blocks first)
     if (sy && d.p2p_np && d.d_order && d.d_nbound > 0) bd = sy->bdone += (unsigned long long)d.d_nbound;
     const bool crit = crack_on(crack_every, s);
-    const unsigned gcrit = CEM_CRIT_GRID;  // one warp per flagged tet, grid-stride
+    // one warp per flagged tet, grid-stride; streaming (short recent lists): fewer blocks, polling
+    const bool stream = (cmode == CRIT_STREAM || cmode == CRIT_IDLE) && !ev;
+    const unsigned gcrit = stream && cmode == CRIT_IDLE ? CEM_CRIT_IGRID : CEM_CRIT_GRID;
     if (!ev && chunks && chunks->size() > 1) {
         // AB and C in chunks along the storage order, AB(c) C(c) AB(c+1) ...: each C chunk reads
         // only the AB chunks before it (chunk bounds from the plan), every kernel waits for its
@@ -2205,7 +2253,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 launch_pdl(k_eval, (unsigned)CEM_CRITB_GRID, (unsigned)CEM_CRIT_THREADS, crit_smem_bytes(), st, d, s);
                 n += 2;
             } else {
-                launch_pdl(k_crit, (unsigned)CEM_CRIT_GRID, 256u, (size_t)0, st, d, s);
+                launch_pdl(k_crit, (unsigned)CEM_CRIT_GRID, 256u, (size_t)0, st, d, s, 0);
                 ++n;
             }
         }
@@ -2225,7 +2273,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 launch_pdl(k_filter, (unsigned)CEM_FILTER_GRID, 256u, (size_t)0, st, d, s);
                 launch_pdl(k_eval, (unsigned)CEM_CRITB_GRID, (unsigned)CEM_CRIT_THREADS, crit_smem_bytes(), st, d, s);
             } else {
-                launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s);
+                launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s, stream ? CEM_CRIT_POLLS : 0);
             }
         }
         if (bd) launch_pdl(k_Db, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
@@ -2245,7 +2293,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
             k_filter<<<CEM_FILTER_GRID, 256, 0, st>>>(d, s);
             k_eval<<<CEM_CRITB_GRID, CEM_CRIT_THREADS, crit_smem_bytes(), st>>>(d, s);
         } else {
-            k_crit<<<gcrit, 256, 0, st>>>(d, s);
+            k_crit<<<gcrit, 256, 0, st>>>(d, s, 0);
         }
     }
     cudaEventRecord(ev[3], st);
