@@ -210,7 +210,7 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     return o;
 }
 
-int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 6 * ((p.max_tl + 1) | 1)); }
+int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 7 * ((p.max_tl + 1) | 1)); }  // u: 3, tau + V: 7 planes
 // stage C reuses its staging area for the warps' criterion scratch (<= 8 warps x ~840 B)
 // (CEM_C_GEOX adds 3 planes of node coordinates; the default keeps stage C's shared memory small:
 // its blocks then share the SM with a larger L1, which stage C measurably needs)

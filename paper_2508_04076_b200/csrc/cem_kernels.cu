@@ -360,35 +360,12 @@ __device__ __forceinline__ void tau_row(double *T, int tn, int i, const double *
     T[3 * tn + i] = V * gxy;
     T[4 * tn + i] = V * gyz;
     T[5 * tn + i] = V * gxz;
+    T[6 * tn + i] = V;  // (plane 6: the volume of an active tet, for a dirty edge's Vhat)
 }
 __device__ __forceinline__ void zero_row(double *T, int tn, int i) {
 #pragma unroll
     for (int c = 0; c < 6; ++c) T[c * tn + i] = 0.0;
-}
-// Vhat_s = sum of V_e over the edge's active incident tets in ascending original id (the
-// oracle's stage_edge sum); inactive tets are skipped (equivalently: add +0.0)
-// (8 incidences at a time: index, state and volume loads issued together -- three round trips
-// per batch instead of per incidence; the sum stays sequential in ascending order)
-__device__ __noinline__ double vhat_recompute(const Dev *__restrict__ dp, int64_t s) {
-    const Dev &d = *dp;
-    double acc = 0.0;
-    const int32_t j0 = __ldg(d.e_off + s), j1 = __ldg(d.e_off + s + 1);
-    for (int32_t j = j0; j < j1; j += 8) {
-        int32_t e[8];
-        uint8_t st[8];
-        double V[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) e[t] = j + t < j1 ? __ldg(d.e_inc + j + t) : -1;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            st[t] = e[t] >= 0 ? __ldcg(d.state + e[t]) : (uint8_t)0;
-            V[t] = e[t] >= 0 ? geo_V(d, (uint32_t)e[t]) : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-            if (st[t]) acc = acc + V[t];
-    }
-    return acc;
+    T[6 * tn + i] = -0.0;  // inactive tet / sentinel: adding -0.0 leaves any sum bit-for-bit unchanged
 }
 // the 9 stored gradients (nodes 1..3) and V of tet e; gradN0 = -((gradN1 + gradN2) + gradN3)
 __device__ __forceinline__ void load_geo(const Dev &d, uint32_t e, double (&g)[4][3], double &V) {
@@ -400,19 +377,35 @@ __device__ __forceinline__ void grad0(double (&g)[4][3]) {
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
 }
 
-// Vhat_s from the table; an edge with a tet split since the last step is recomputed (splits
-// mark their 6 edges; ghost splits arrive marked by the halo unpack); `update` writes it back
-__device__ __forceinline__ double fetch_vhat(const Dev &d, int64_t s, bool update) {
-    const uint8_t dirty = __ldcg(d.edge_dirty + s);
-    double Vh = __ldcg(d.vhat + s);  // issued together with the flag (one round trip)
-    if (dirty) {
-        Vh = vhat_recompute(d.self, s);
-        if (update) {
-            d.vhat[s] = Vh;
-            d.edge_dirty[s] = 0;
+// Vhat_s of an edge with a tet split since the last step (splits mark their 6 edges; ghost splits
+// arrive marked by the halo unpack), recomputed inside stage AB from the block's staged rows:
+// plane 6 holds V of each active tet of the block's list (-0.0 for an inactive tet and for the
+// sentinel row), and the edge's ELL row lists its incident tets in ascending original id -- the
+// same terms in the same order as the oracle's stage_edge sum (V_e of the active incident tets,
+// ascending original id; an inactive one adds -0.0), without a walk of the global incidence lists.  `update` writes the value back and clears the flag.
+__device__ __forceinline__ double vhat_rows(const Dev &d, int64_t s, const double *T, int tn, int nt, uint4 q,
+                                            bool update) {
+    const double *Vr = T + 6 * tn;
+    const uint4 *row = reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we);
+    double acc = 0.0;
+    for (int w = 0;;) {
+        const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+        const int lim = d.we_max - w;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (t >= lim) break;
+            const int raw = (int)((qq[t >> 1] >> (16 * (t & 1))) & 0xffff);
+            acc = acc + Vr[min(raw, nt)];
         }
+        w += 8;
+        if (w >= d.we_max) break;
+        q = __ldg(row + (w >> 3));
     }
-    return Vh;
+    if (update) {
+        d.vhat[s] = acc;
+        d.edge_dirty[s] = 0;
+    }
+    return acc;
 }
 
 // edge s: T = sum of tau over its incidences (ELL row, 8 per 16-B load, ascending original id;
@@ -556,13 +549,21 @@ __device__ __forceinline__ void block_AB(const Dev &d, int b, const double4 *u, 
     const bool hs0 = s0 < send;
     const uint4 qe0 = hs0 ? __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s0 * (uint32_t)d.we))
                           : make_uint4(0, 0, 0, 0);
-    const double Vh0 = hs0 ? fetch_vhat(d, s0, epart == nullptr) : 0.0;
+    // Vhat from the table, issued with its dirty flag (one round trip) before the barrier
+    const uint8_t dty0 = hs0 ? __ldcg(d.edge_dirty + s0) : (uint8_t)0;
+    double Vh0 = hs0 ? __ldcg(d.vhat + s0) : 0.0;
     __syncthreads();
     double Ue = 0.0;  // energy mode: this thread's strain energy
-    if (hs0) edge_sigma(d, s0, T, tn, nt, qe0, Vh0, epart, Ue);
-    for (int64_t s = s0 + nthr; s < send; s += nthr)  // (CEM_AB_EPT > 1: more edges per thread)
-        edge_sigma(d, s, T, tn, nt, __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we)),
-                   fetch_vhat(d, s, epart == nullptr), epart, Ue);
+    if (hs0) {
+        if (dty0) Vh0 = vhat_rows(d, s0, T, tn, nt, qe0, epart == nullptr);
+        edge_sigma(d, s0, T, tn, nt, qe0, Vh0, epart, Ue);
+    }
+    for (int64_t s = s0 + nthr; s < send; s += nthr) {  // (CEM_AB_EPT > 1: more edges per thread)
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(d.incE + (uint32_t)s * (uint32_t)d.we));
+        double Vh = __ldcg(d.vhat + s);
+        if (__ldcg(d.edge_dirty + s)) Vh = vhat_rows(d, s, T, tn, nt, q, epart == nullptr);
+        edge_sigma(d, s, T, tn, nt, q, Vh, epart, Ue);
+    }
     if (epart) {
         const double t = block_sum(Ue, sm);  // the planes are no longer read
         if (tid == 0) epart[b] = t;
