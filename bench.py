@@ -251,14 +251,16 @@ def main():
     stream = sim.torch_stream
     crack_every = 1
 
-    # warm-up (untimed)
-    sim.step(args.warmup, crack_every)
-    l0 = sim.launch_count
-    torch.cuda.synchronize(dev)
-
+    # clock sampler first (nvidia-smi needs a moment to start), then the warm-up steps (untimed)
+    # directly followed by the timed ones: no idle gap between them
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    sim.step(args.warmup, crack_every)
+    l0 = sim.launch_count
+    torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
