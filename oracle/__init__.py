@@ -25,6 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "cem_oracle.c")
 _SRC_HEX = os.path.join(_HERE, "cem_oracle_hex.c")
+_HDR_XS = os.path.join(_HERE, "exact_sum.h")
 
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=gnu11"]
 
@@ -32,7 +33,8 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-s
 def build(force: bool = False) -> str:
     """Compile liboracle.so in-tree (gcc)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(_SRC),
-                                                                           os.path.getmtime(_SRC_HEX)):
+                                                                           os.path.getmtime(_SRC_HEX),
+                                                                           os.path.getmtime(_HDR_XS)):
         tmp = _SO + ".tmp"
         subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC_HEX, "-lm"])
         os.replace(tmp, _SO)
@@ -78,6 +80,8 @@ def lib():
         L.orc_principal.argtypes = [D, D, D, I32, I32]
         L.orc_tet_geometry.argtypes = [D, D, D]
         L.orc_sig_proj.argtypes = [D, D]; L.orc_sig_proj.restype = C.c_double
+        L.orc_exact_sum.argtypes = [C.c_int64, D]; L.orc_exact_sum.restype = C.c_double
+        L.orc_element_forces.argtypes = [C.c_void_p, D]
         L.orc_lame.argtypes = [C.c_double, C.c_double, D, D]
         L.orc_lame_of.argtypes = [C.c_void_p, D, D]
         L.orc_newmark_free.argtypes = [C.c_int64, D, D, D, D, D, C.c_double, C.c_double]
@@ -222,6 +226,10 @@ class Oracle:
         u = _c(u, np.float64); f = np.empty((self.N, 3))
         lib().orc_internal_force(self.h, _p(u, D), _p(f, D)); return f
 
+    def element_forces(self):
+        """f_{e,a} [E][4][3] of the last internal_force call"""
+        fe = np.empty((self.E, 4, 3)); lib().orc_element_forces(self.h, _p(fe, D)); return fe
+
     def strain_energy(self, u):
         u = _c(u, np.float64); return lib().orc_strain_energy(self.h, _p(u, D))
 
@@ -322,6 +330,12 @@ def principal(s6):
     k1 = C.c_int32(); deg = C.c_int32()
     lib().orc_principal(_p(s6, D), _p(lam, D), _p(vec, D), C.byref(k1), C.byref(deg))
     return lam, vec, k1.value, deg.value
+
+
+def exact_sum(x):
+    """The oracle's nodal-assembly sum (R27): exact sum of the doubles, rounded once."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return lib().orc_exact_sum(x.size, _p(x, D))
 
 
 def sig_proj(s6, m):

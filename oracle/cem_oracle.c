@@ -9,7 +9,8 @@
  *
  * Arithmetic: IEEE fp64, compiled with -O2 -ffp-contract=off -fno-fast-math, every sum
  * sequential in the order written here (the GPU path reproduces this order; the oracle
- * is the definition of that order).  OpenMP only
+ * is the definition of that order) except the nodal
+ * assembly sum, which is exact and rounded once (R27, exact_sum.h).  OpenMP only
  * parallelises loops over independent outputs, so results are identical at any
  * thread count.
  *
@@ -26,6 +27,8 @@
 #endif
 
 #define ORC_API __attribute__((visibility("default")))
+
+#include "exact_sum.h"
 
 /* local edge l -> (p,q), p<q   (SURVEY.md §8(c) Init 2) */
 static const int EP[6] = {0, 0, 0, 1, 1, 2};
@@ -353,20 +356,30 @@ static void stage_element_force(orc_sim *s) {
 
 /* ---------------------------------------------------------------- stage 4: node force
  * Assembly operator A over elements: f_int,k = sum over (e,a) in the
- * node's incidence list (ascending e), active e only. */
+ * node's incidence list, active e only.  The sum is evaluated exactly and rounded once to
+ * fp64 (reading R27, exact_sum.h): its value does not depend on the order of the terms. */
 static void stage_node_force(orc_sim *s) {
 #pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < s->N; ++k) {
-        double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+        xsum acc[3];
+        for (int c = 0; c < 3; ++c) xsum_init(&acc[c]);
         for (int64_t j = s->nod_off[k]; j < s->nod_off[k + 1]; ++j) {
             int32_t ent = s->nod_ent[j];
             int32_t e = ent >> 2, a = ent & 3;
             if (!s->active[e]) continue;
             const double *f = s->fe + 12 * (int64_t)e + 3 * a;
-            f0 = f0 + f[0]; f1 = f1 + f[1]; f2 = f2 + f[2];
+            for (int c = 0; c < 3; ++c) xsum_add(&acc[c], f[c]);
         }
-        s->fint[3 * k] = f0; s->fint[3 * k + 1] = f1; s->fint[3 * k + 2] = f2;
+        for (int c = 0; c < 3; ++c) s->fint[3 * k + c] = xsum_round(&acc[c]);
     }
+}
+
+/* probe (tests): the exact sum of n doubles rounded once (R27) */
+ORC_API double orc_exact_sum(int64_t n, const double *x) {
+    xsum acc;
+    xsum_init(&acc);
+    for (int64_t i = 0; i < n; ++i) xsum_add(&acc, x[i]);
+    return xsum_round(&acc);
 }
 
 static void internal_force(orc_sim *s, const double *u) {
@@ -841,6 +854,9 @@ ORC_API void orc_internal_force(orc_sim *s, const double *u, double *f) {
     internal_force(s, u);
     memcpy(f, s->fint, sizeof(double) * 3 * s->N);
 }
+
+/* element contributions f_{e,a} [E][4][3] of the last internal_force evaluation (tests) */
+ORC_API void orc_element_forces(const orc_sim *s, double *fe) { memcpy(fe, s->fe, sizeof(double) * 12 * s->E); }
 
 /* strain energy U = sum_s psi(eps~_s) V_s, V_s = Vhat_s / 6, psi = 1/2 lam (tr eps)^2 + mu eps:eps
  * (PAPER.md:L197-L202 with R1; eps:eps = e11^2+e22^2+e33^2 + (g12^2+g23^2+g13^2)/2) */

@@ -31,6 +31,8 @@
 
 #define HX_API __attribute__((visibility("default")))
 
+#include "exact_sum.h"
+
 /* reference coordinates of the 8 nodes (bottom face 0-3 counter-clockwise, top 4-7 above) */
 static const double XI[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1, 1, -1},
                                 {-1, -1, 1},  {1, -1, 1},  {1, 1, 1},  {-1, 1, 1}};
@@ -239,15 +241,17 @@ static void internal_force(hx_sim *s, const double *u) {
             f[3 * a + 2] = c * ((g[2] * S[2] + g[1] * S[4]) + g[0] * S[5]);
         }
     }
+    /* nodal assembly: exact sum rounded once (R27, exact_sum.h) */
     for (int64_t k = 0; k < s->N; ++k) {
-        double f[3] = {0, 0, 0};
+        xsum acc[3];
+        for (int c = 0; c < 3; ++c) xsum_init(&acc[c]);
         for (int64_t j = s->nod_off[k]; j < s->nod_off[k + 1]; ++j) {
             const int32_t ent = s->nod_ent[j];
             if (!s->active[ent >> 3]) continue;
             const double *x = s->fe + 24 * (int64_t)(ent >> 3) + 3 * (ent & 7);
-            f[0] = f[0] + x[0]; f[1] = f[1] + x[1]; f[2] = f[2] + x[2];
+            for (int c = 0; c < 3; ++c) xsum_add(&acc[c], x[c]);
         }
-        s->fint[3 * k] = f[0]; s->fint[3 * k + 1] = f[1]; s->fint[3 * k + 2] = f[2];
+        for (int c = 0; c < 3; ++c) s->fint[3 * k + c] = xsum_round(&acc[c]);
     }
 }
 
