@@ -130,6 +130,7 @@ struct Offs {
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
     size_t rprev, wr_dof, epart, crit_list, crit_surv, vhat, edge_dirty, e_off, e_inc, edge_own;
     size_t wcnt, wdep_off, wdep, wstep, wncons, wcons_done;
+    size_t part, pinc_off, pinc, nodeP, pord;
     size_t total;
 };
 
@@ -206,6 +207,11 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     o.wstep = L.take<int64_t>(1);
     o.wncons = L.take<int32_t>((int64_t)w.ncons.size());
     o.wcons_done = L.take<int32_t>((int64_t)w.ncons.size());
+    o.part = L.take<double>(6 * ((int64_t)p.nl.size() + 1));  // + the all-zero partial
+    o.pinc_off = L.take<int32_t>((int64_t)p.pinc_off.size());
+    o.pinc = L.take<uint16_t>((int64_t)p.pinc.size());
+    o.nodeP = L.take<int32_t>((int64_t)p.nodeP.size());
+    o.pord = L.take<int32_t>((int64_t)p.pord.size());
     o.total = L.off;
     return o;
 }
@@ -214,8 +220,13 @@ int smem_ab_for(const Plan &p) { return 8 * (3 * (p.max_nlb | 1) + 7 * ((p.max_t
 // stage C reuses its staging area for the warps' criterion scratch (<= 8 warps x ~840 B)
 // (CEM_C_GEOX adds 3 planes of node coordinates; the default keeps stage C's shared memory small:
 // its blocks then share the SM with a larger L1, which stage C measurably needs)
+// (partials: + 12 planes of the block's element forces, f_{t,a,c} at [(3a + c) blk + t])
 int smem_c_for(const Plan &p) {
-    return std::max(8 * (6 * (p.max_el | 1) + (CEM_C_GEOX ? 6 : 3) * (p.max_nl | 1)), 8 * 1024);
+    // (partials also stage the block's incidence entries, 4 x u16 per tet, and per-entry offsets)
+    // the force planes (12 doubles per tet) overlay the sigma planes
+    const int sig = p.partials ? std::max(6 * (p.max_el | 1), 12 * p.blk) : 6 * (p.max_el | 1);
+    const int part = p.partials ? p.blk + (2 * p.max_nl + 2) / 2 + 1 : 0;  // pinc; offsets + order (int32)
+    return std::max(8 * (sig + (CEM_C_GEOX ? 6 : 3) * (p.max_nl | 1) + part), 8 * 1024);
 }
 int smem_bytes_for(const Plan &p) { return std::max(smem_ab_for(p), smem_c_for(p)); }  // odd plane strides
 
@@ -258,6 +269,13 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.srec = at<double>(b, o.srec);
     d.srec2 = at<double>(b, o.srec2);
     d.fe = at<double>(b, o.fe);
+    d.part = p.partials ? at<double>(b, o.part) : nullptr;
+    d.pinc_off = at<int32_t>(b, o.pinc_off);
+    d.pinc = at<uint16_t>(b, o.pinc);
+    d.nodeP = at<int32_t>(b, o.nodeP);
+    d.pord = at<int32_t>(b, o.pord);
+    d.wp = p.wp;
+    d.zpart = (int32_t)p.nl.size();
     d.nl_off = at<int32_t>(b, o.nl_off);
     d.nl = at<int32_t>(b, o.nl);
     d.lconn = at<uint16_t>(b, o.lconn);
@@ -516,6 +534,11 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.ledge, p.ledge.data(), sizeof(uint16_t) * p.ledge.size()));
     CUDA_TRY(put(o.tl_off, p.tl_off.data(), sizeof(int32_t) * p.tl_off.size()));
     CUDA_TRY(put(o.tl, p.tl.data(), sizeof(int32_t) * p.tl.size()));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.part), 0, sizeof(double) * 6 * (p.nl.size() + 1), st));
+    CUDA_TRY(put(o.pinc_off, p.pinc_off.data(), sizeof(int32_t) * p.pinc_off.size()));
+    CUDA_TRY(put(o.pinc, p.pinc.data(), sizeof(uint16_t) * p.pinc.size()));
+    CUDA_TRY(put(o.nodeP, p.nodeP.data(), sizeof(int32_t) * p.nodeP.size()));
+    CUDA_TRY(put(o.pord, p.pord.data(), sizeof(int32_t) * p.pord.size()));
 
     CUDA_TRY(put(o.sched, p.sched.data(), sizeof(int32_t) * p.sched.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.head), 0, sizeof(unsigned long long), st));
@@ -1224,6 +1247,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.srec = at<double>(b, o.srec);
     d.srec2 = at<double>(b, o.srec2);
     d.fe = at<double>(b, o.fe);
+    d.part = nullptr;  // hexahedra: force slots (8 per hex)
     d.ctr = at<int32_t>(b, o.ctr);
     d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
     d.wr_dof = at<double>(b, o.wr_dof);
@@ -1459,7 +1483,9 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         const char *e = getenv("CEM_C_PIPE");
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        if (e && atoi(e) > 0 && ctx->p.blk == 256 && cp_stage_c_smem(ctx->p.max_el, ctx->p.max_nl) > 0) {
+        // (k_Cp writes force slots: only with CEM_PARTIALS=0)
+        if (e && atoi(e) > 0 && ctx->p.blk == 256 && !ctx->p.partials &&
+            cp_stage_c_smem(ctx->p.max_el, ctx->p.max_nl) > 0) {
             ctx->cp_on = 1;
             ctx->cp_grid = std::max(1, sms) * std::max(1, atoi(e));
         }

@@ -180,6 +180,15 @@ struct Plan {
     int wn = 8;                       // ELL width of node incidences (multiple of 8)
     hvec<int32_t> nodeE;              // [N][wn] force slot of each incidence (original order), zslot = none
     int32_t zslot = 0;
+    // exact partial sums of the nodal assembly (R27, DESIGN.md §6 "Partials"): stage C sums, for
+    // each entry q of its block's node list, the contributions of the block's tets to that node
+    // (partial q); stage D adds the partials of its node.  partials = false: force slots instead.
+    bool partials = true;
+    std::vector<int32_t> pinc_off;    // [|nl| + 1] entries of partial q in pinc
+    hvec<uint16_t> pinc;              // [4E] a blk + t (t: tet within the block, a: corner), per partial
+    std::vector<int32_t> pord;        // [|nl|] per block: node-list entries by descending incidence count
+    int wp = 4;                       // ELL width of a node's partials (multiple of 4)
+    hvec<int32_t> nodeP;              // [N][wp] partials of each node, padded with |nl| (all-zero partial)
 };
 
 void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig = nullptr, bool with_deps = true);
@@ -236,6 +245,13 @@ struct Dev {
     const int32_t *nodeE;      // [N][wn]
     int we, wn, we_max;        // ELL widths; we_max = largest edge incidence count
     int32_t zslot;             // index of the all-zero force slot (ELL padding)
+    double *part;              // [|nl| + 1][6] exact partials (s_x, s_y, s_z, c_x, c_y, c_z); null: force slots
+    const int32_t *pinc_off;   // [|nl| + 1]
+    const uint16_t *pinc;      // [4E] a blk + t per partial (stage C's force row)
+    const int32_t *pord;       // [|nl|] per block: its node-list entries by descending incidence count
+    const int32_t *nodeP;      // [N][wp]
+    int wp;
+    int32_t zpart;             // index of the all-zero partial (ELL padding)
     const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
     const uint16_t *tconn, *trow, *nrow;
     const uint16_t *lconn, *ledge;

@@ -317,6 +317,17 @@ __device__ __forceinline__ void stage_wait(const Dev &d, int g, int b, int wneed
 // plane strides are odd so the 8-byte planes of a record fall into different bank pairs
 __host__ __device__ __forceinline__ int pstride(int n) { return n | 1; }
 
+// exact-sum accumulation of the nodal assembly (reading R27): s is the running rounded sum, c
+// collects the TwoSum rounding errors; RN(s + c) is the exact sum rounded once whenever c's
+// additions are exact (the node's partial sums within 2^49 of its smallest nonzero term).
+// Compiled with --fmad=false: no contraction may fuse these operations.
+__device__ __forceinline__ void xacc(double &s, double &c, double x) {
+    const double t = s + x;
+    const double z = t - s;
+    c = c + ((s - (t - z)) + (x - z));
+    s = t;
+}
+
 // deterministic block sum (fixed shuffle tree, then the warps in order); valid in thread 0.
 // Every thread of the block must call it.
 __device__ __forceinline__ double block_sum(double x, double *red) {
@@ -1027,6 +1038,77 @@ __device__ __forceinline__ void stage_sigma(double *sm, int np, int i, double4 x
     sm[4 * np + i] = z.x;
     sm[5 * np + i] = z.y;
 }
+// asynchronous global -> shared copies (cp.async: no registers held while in flight)
+__device__ __forceinline__ void cpa16(void *sdst, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa8(void *sdst, const void *g) {  // static tables only (.ca)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa4(void *sdst, const void *g) {  // static tables only (.ca)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// stage C, partial mode (R27): entry i of the block's node list sums the contributions of the
+// block's tets to that node (any order: the sum is exact), stored as (s, c) per component.  One
+// thread per entry, entries in descending incidence count (nearly equal trip counts per warp);
+// the forces are row a nthr + t of an (x, y) plane and a z plane.  Every thread calls it (barrier).
+__device__ __forceinline__ void c_partials(const Dev &d, int b, const double *sm) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    // (block geometry reloaded here rather than kept live through stage C's body: registers)
+    const int32_t n0 = __ldg(d.nl_off + b);
+    const int nn = __ldg(d.nl_off + b + 1) - n0;
+    const int ne = __ldg(d.el_off + b + 1) - __ldg(d.el_off + b);
+    // (x, y) plane of 16-B rows and z plane of 8-B rows (overlay the sigma planes): random rows of
+    // a warp then spread over 8 / 16 bank positions (32-B rows would give 4: 3x the wavefronts)
+    const double2 *fxy = reinterpret_cast<const double2 *>(sm);
+    const double *fz = sm + 8 * nthr;
+    const uint16_t *spinc = reinterpret_cast<const uint16_t *>(sm + max(6 * pstride(ne), 12 * nthr) +
+                                                               (CEM_C_GEOX ? 6 : 3) * pstride(nn));  // staged at block start
+    const int32_t *spoff = reinterpret_cast<const int32_t *>(spinc + 4 * nthr);  // global offsets [nn + 1]
+    const int32_t *spord = spoff + nn + 1;                                       // entry order [nn]
+    const int32_t base = 4 * b * d.blk;
+    cpa_wait_all();
+    __syncthreads();
+    for (int k = tid; k < nn; k += nthr) {
+        const int i = spord[k];
+        const int32_t j1 = spoff[i + 1] - base;
+        double sx = 0.0, sy = 0.0, sz = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+        // eight entries per pass (their shared-memory loads all in flight); padding adds +0.0
+        for (int32_t j = spoff[i] - base; j < j1; j += 8) {
+            int ri[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ri[u] = j + u < j1 ? (int)spinc[j + u] : -1;
+            double2 xy[8];
+            double z[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int r = ri[u] < 0 ? 0 : ri[u];
+                xy[u] = ri[u] < 0 ? make_double2(0.0, 0.0) : fxy[r];
+                z[u] = ri[u] < 0 ? 0.0 : fz[r];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                xacc(sx, cx, xy[u].x);
+                xacc(sy, cy, xy[u].y);
+                xacc(sz, cz, z[u]);
+            }
+        }
+        double2 *o = reinterpret_cast<double2 *>(d.part + 6 * (int64_t)(n0 + i));
+        o[0] = make_double2(sx, sy);
+        o[1] = make_double2(sz, cx);
+        o[2] = make_double2(cy, cz);
+    }
+}
+
+// PM: exact partials (d.part != null, R27) instead of force slots (a compile-time choice: one
+// register allocation per mode)
+template <bool PM>
 __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, bool crack, int64_t rec_step,
                                         int32_t stamp, double *sm, bool defer = false, int wneed = -1) {
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -1036,7 +1118,12 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     const int nn = __ldg(d.nl_off + b + 1) - n0;
     const bool early = crack && !(d.flags & CEM_F_NO_EARLY_OUT);
     const int np = pstride(ne), nq = pstride(nn);
-    double *smu = sm + 6 * np;
+    // partials: the block's element forces, row a nthr + t in a (f_x, f_y) 16-B plane and an f_z plane, overlay the sigma
+    // planes once every thread has formed its S (barrier); the u (/ X) planes and the staged
+    // partial tables follow
+    double *smu = sm + (PM ? max(6 * np, 12 * nthr) : 6 * np);
+    double *smf = sm;
+    uint16_t *spinc_w = reinterpret_cast<uint16_t *>(smu + (CEM_C_GEOX ? 6 : 3) * nq);
     // ---- wave 1: list indices
     constexpr int kME = CEM_C_KME;  // sigma records per thread in flight (more -> tail loop)
     uint32_t sid[kME];
@@ -1059,6 +1146,18 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #else
     const int32_t nid = (early && tid < nn) ? __ldg(d.nl + n0 + tid) : 0;
 #endif
+    if (PM) {
+        // partial tables of this block (static; staged before the dependency wait): its tets'
+        // incidence entries (4 per tet, grouped by node-list entry) and the per-entry offsets
+        // (cp.async: in flight without registers until c_partials waits for them)
+        uint16_t *spinc = spinc_w;
+        int32_t *spoff = reinterpret_cast<int32_t *>(spinc + 4 * nthr);
+        const int64_t e0 = (int64_t)b * d.blk;
+        if (e0 + tid < d.E) cpa8(reinterpret_cast<uint2 *>(spinc) + tid, reinterpret_cast<const uint2 *>(d.pinc) + e0 + tid);
+        for (int i = tid; i <= nn; i += nthr) cpa4(spoff + i, d.pinc_off + n0 + i);
+        for (int i = tid; i < nn; i += nthr) cpa4(spoff + nn + 1 + i, d.pord + n0 + i);
+        cpa_commit();
+    }
     stage_wait(d, ST_C, b, wneed);  // sigma records come from stage AB
     // ---- wave 2: gathered records (one 32-B and one 16-B load each) -> planes 0..5
     double4 rx[kME];
@@ -1137,6 +1236,9 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
     }
 #endif
     bool need = false;  // this tet needs the full criterion (failed the early-out)
+    double fr[PM ? 12 : 1];  // partials: the tet's forces, stored after the barrier (zeros if inactive)
+#pragma unroll
+    for (int q = 0; q < (PM ? 12 : 1); ++q) fr[q] = 0.0;
     if (he) {
 #if CEM_FES == 3
         // the tet's 4 slots packed (f0, f1, f2, f3: 12 doubles, 96 B) -> three 256-bit stores
@@ -1147,7 +1249,8 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
 #endif
         if (!act) {
 #if CEM_FES == 3
-            for (int q = 0; q < 3; ++q) st256(reinterpret_cast<double4 *>(fo) + q, 0.0, 0.0, 0.0, 0.0);
+            if (!PM)
+                for (int q = 0; q < 3; ++q) st256(reinterpret_cast<double4 *>(fo) + q, 0.0, 0.0, 0.0, 0.0);
 #else
 #pragma unroll
             for (int a = 0; a < 4; ++a) store_slot(fo + 32 * CEM_FES * a, 0.0, 0.0, 0.0);
@@ -1188,9 +1291,14 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
                 f[3 * a + 1] = cc * ((g[a][1] * S1 + g[a][0] * S3) + g[a][2] * S4);
                 f[3 * a + 2] = cc * ((g[a][2] * S2 + g[a][1] * S4) + g[a][0] * S5);
             }
+            if (PM) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q)
-                st256(reinterpret_cast<double4 *>(fo) + q, f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                for (int q = 0; q < 12; ++q) fr[q] = f[q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    st256(reinterpret_cast<double4 *>(fo) + q, f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+            }
 #else
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
@@ -1222,7 +1330,20 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
             }
         }
     }
-    if (!crack) return;  // block-uniform
+    if (PM) {
+        __syncthreads();  // every S is formed: the sigma planes are free
+        if (he) {  // row a nthr + t of corner a: (f_x, f_y) in the 16-B plane, f_z in the 8-B plane
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                reinterpret_cast<double2 *>(smf)[a * nthr + tid] = make_double2(fr[3 * a], fr[3 * a + 1]);
+                smf[8 * nthr + a * nthr + tid] = fr[3 * a + 2];
+            }
+        }
+    }
+    if (!crack) {  // block-uniform
+        if (PM) c_partials(d, b, sm);
+        return;
+    }
     if (defer) {
         // staged path: append the flagged tets to the step's list (warp-aggregated); k_crit
         // evaluates them all concurrently, one warp per tet, as they appear (it polls the
@@ -1237,8 +1358,10 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
             base = __shfl_sync(0xffffffffu, base, lead);
             if (need) d.crit_list[base + __popc(mm & ((1u << lane) - 1))] = crit_entry(rec_step, e);
         }
+        if (PM) c_partials(d, b, sm);
         return;
     }
+    if (PM) c_partials(d, b, sm);
     // few flagged tets in the warp: the warp evaluates them one after another, 24 candidates
     // in parallel (scratch in the staging area, free after the barrier); many: each lane
     // evaluates its own (side by side)
@@ -1294,20 +1417,6 @@ __host__ __device__ inline int cp_idx_ints(int max_el, int max_nl) { return (max
 __host__ __device__ inline int cp_smem_bytes(int max_el, int max_nl) {
     return CEM_CP_DEPTH * cp_slot(max_el, max_nl).bytes + (CEM_CP_DEPTH + 2) * 4 * cp_idx_ints(max_el, max_nl);
 }
-__device__ __forceinline__ void cpa16(void *sdst, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
-                 : "memory");
-}
-__device__ __forceinline__ void cpa8(void *sdst, const void *g) {  // static tables only (.ca)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
-                 : "memory");
-}
-__device__ __forceinline__ void cpa4(void *sdst, const void *g) {  // static tables only (.ca)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(g)
-                 : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // the index lists (edge list, node list) of block b -> an index slot
 __device__ __forceinline__ void cp_issue_idx(const Dev &d, int b, int32_t *idx, bool early) {
@@ -1503,6 +1612,7 @@ __host__ __device__ __forceinline__ int d_nodes_per_block(int threads) { return 
 // mode: ND_INLINE (staged and persistent kernels) -- PDL wait, resets the criterion list;
 // ND_WAVE -- inputs already awaited at kernel entry, kernel-choice heuristic from stage C's count
 enum { ND_INLINE = 0, ND_WAVE = 1 };
+template <bool PM>
 __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t kend, const double4 *u1p, double4 *u2p,
                                             int64_t s, int mode = ND_INLINE) {
     const bool wave = mode == ND_WAVE;
@@ -1533,8 +1643,15 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
     constexpr int kB = CEM_D_BATCH, kQ = kB / 4;  // slots per batch, int4 index loads per batch
     int4 q[kQ];
+    // partial mode (R27): the node's exact partials from stage C (ELL row of nodeP, 4 per int4)
+    constexpr bool pm = PM;
+    const int4 *prow = reinterpret_cast<const int4 *>(d.nodeP + (uint32_t)k * (uint32_t)d.wp);
+    if (pm) {
+        q[0] = __ldg(prow);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kQ; ++j) q[j] = j * 4 < d.wn ? __ldg(row + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+        for (int j = 0; j < kQ; ++j) q[j] = j * 4 < d.wn ? __ldg(row + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+    }
     const double fxc = (fl & 8) ? __ldg(reinterpret_cast<const double *>(d.fext + k) + c) : 0.0;
     const double vb0 = (fl & 7) ? __ldg(reinterpret_cast<const double *>(d.dir_v0 + k) + c) : 0.0;
     if (!wave) pdl_wait();  // force slots come from stage C (wave launches waited at kernel entry)
@@ -1545,7 +1662,32 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     double aa = __ldcg(reinterpret_cast<const double *>(d.a + k) + c);
     const int32_t dirty = __ldcg(d.dirty + k);
     const double *fec = d.fe + (c < 3 ? c : 0);  // lane c: component c of each slot (lane 3: unused sum)
-    double f = 0.0;
+    double f = 0.0, fc = 0.0;  // exact-sum accumulator (R27)
+    if (pm) {
+        // lane c: component c of each partial, s and c terms (padding: the all-zero partial)
+        const double *pc = d.part + (c < 3 ? c : 0);
+        for (int w = 0;;) {
+            const int32_t pq[4] = {q[0].x, q[0].y, q[0].z, q[0].w};
+            double xs[4], xe[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                CEM_BOUND(d, pq[t] >= 0 && pq[t] <= d.zpart);
+                // padding: no load (every padded entry would hit the one all-zero record: a hot L2 line)
+                const bool live = pq[t] != d.zpart;
+                xs[t] = live ? __ldcg(pc + 6 * (int64_t)pq[t]) : 0.0;
+                xe[t] = live ? __ldcg(pc + 6 * (int64_t)pq[t] + 3) : 0.0;
+            }
+            w += 4;
+            const bool more = pq[3] != d.zpart && w < d.wp;
+            if (more) q[0] = __ldg(prow + (w >> 2));
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                xacc(f, fc, xs[t]);
+                xacc(f, fc, xe[t]);
+            }
+            if (!more) break;
+        }
+    } else {
 #if CEM_D_PIPE
     // software pipeline: batch i+1's slot loads are issued before batch i is summed
     {
@@ -1593,7 +1735,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
                 }
             }
 #pragma unroll
-            for (int t = 0; t < kB; ++t) f = f + x[t];
+            for (int t = 0; t < kB; ++t) xacc(f, fc, x[t]);
             if (!more) break;
 #pragma unroll
             for (int t = 0; t < kB; ++t) x[t] = y[t];
@@ -1625,10 +1767,12 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
                 q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
         }
 #pragma unroll
-        for (int t = 0; t < kB; ++t) f = f + x[t];
+        for (int t = 0; t < kB; ++t) xacc(f, fc, x[t]);
         if (!more) break;
     }
 #endif
+    }
+    f = f + fc;  // RN(s + c) (R27)
     const double dt = d.dt;
     const double t1 = (double)(s + 1) * dt;
     if (c == 3) {
@@ -1683,9 +1827,10 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
 
 
 
+template <bool PM>
 __device__ __forceinline__ void block_D(const Dev &d, int64_t kbase, int64_t kend, const double4 *u1p, double4 *u2p,
                                         int64_t s) {
-    node_update(d, kbase, min(kend, d.N), u1p, u2p, s);
+    node_update<PM>(d, kbase, min(kend, d.N), u1p, u2p, s);
 }
 
 
@@ -1771,10 +1916,14 @@ __global__ void __launch_bounds__(256, CEM_PERSIST_MINB) k_persistent(Dev d, int
         const double4 *u1 = d.ubuf[(s + 1) & 1];
         switch (g) {
             case ST_AB: block_AB(d, b, u1, sm); break;
-            case ST_C: block_C(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm); break;
+            case ST_C:
+                if (d.part) block_C<true>(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
+                else block_C<false>(d, b, u1, crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm);
+                break;
             default:
                 for (int64_t k0 = (int64_t)b * d.blk; k0 < (int64_t)(b + 1) * d.blk; k0 += d_nodes_per_block(blockDim.x))
-                    block_D(d, k0, (int64_t)(b + 1) * d.blk, u1, d.ubuf[s & 1], s);  // a D item covers blk nodes
+                    if (d.part) block_D<true>(d, k0, (int64_t)(b + 1) * d.blk, u1, d.ubuf[s & 1], s);  // a D item covers blk nodes
+                    else block_D<false>(d, k0, (int64_t)(b + 1) * d.blk, u1, d.ubuf[s & 1], s);
                 break;
         }
         __syncthreads();
@@ -1822,11 +1971,14 @@ __global__ void __launch_bounds__(256, CEM_AB_MINB) k_AB(Dev d, int64_t s, int b
     pdl_trigger();
     block_AB(d, (int)blockIdx.x + boff, d.ubuf[(s + 1) & 1], sm);
 }
-__global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack_every, int boff) {
-    extern __shared__ double sm[];
-    pdl_trigger();
-    block_C(d, (int)blockIdx.x + boff, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, true);
-}
+// crack: crack_on(crack_every, s), decided on the host (a 64-bit modulo per thread otherwise).
+// k_C: exact partials (R27, the default); k_Cs: force slots (CEM_PARTIALS=0, hexahedral D path)
+#define CEM_K_C_BODY(PM)                                                                                      \
+    extern __shared__ double sm[];                                                                            \
+    pdl_trigger();                                                                                            \
+    block_C<PM>(d, (int)blockIdx.x + boff, d.ubuf[(s + 1) & 1], crack != 0, s + 1, (int32_t)(s + 1), sm, true);
+__global__ void __launch_bounds__(256, CEM_C_MINB) k_C(Dev d, int64_t s, int crack, int boff) { CEM_K_C_BODY(true) }
+__global__ void __launch_bounds__(256, CEM_C_MINB) k_Cs(Dev d, int64_t s, int crack, int boff) { CEM_K_C_BODY(false) }
 // full criterion of the tets stage C flagged (ctr[3] of them in crit_list), one warp per tet.
 // Its inputs other than the list (sigma from stage AB, u, X, the tables) are final before stage C
 // writes any entry, and its outputs (the split tets' state, Vhat flags, node stamps, records) are
@@ -2006,18 +2158,25 @@ __global__ void __launch_bounds__(CEM_CRIT_THREADS, CEM_CRITB_MINB) k_eval(Dev d
 // s + 2, the value the per-step sync kernel waits for) while the interior blocks still run, so a
 // peer's unpack and next step overlap this rank's interior update (SURVEY.md §8(e) "update the
 // boundary nodes first").  bd_target = the cumulative count of boundary blocks after this step.
+// k_D: exact partials (default); k_Ds: force slots
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D(Dev d, int64_t s) {
     pdl_trigger();
     const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
-    block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+    block_D<true>(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+}
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_Ds(Dev d, int64_t s) {
+    pdl_trigger();
+    const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
+    block_D<false>(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
 // (a separate kernel, so that the single-GPU stage D keeps its register allocation)
-__global__ void __launch_bounds__(256, CEM_D_MINB) k_Db(Dev d, int64_t s, unsigned long long bd_target) {
+template <bool PM>
+__device__ __forceinline__ void k_Db_body(const Dev &d, int64_t s, unsigned long long bd_target) {
     pdl_trigger();
     const int bi = (int)blockIdx.x;
     const int b = __ldg(d.d_order + bi);
     const int64_t k0 = (int64_t)b * d_nodes_per_block(blockDim.x);
-    block_D(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+    block_D<PM>(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
     if (bi < d.d_nbound) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -2028,6 +2187,8 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_Db(Dev d, int64_t s, unsign
         }
     }
 }
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_Db(Dev d, int64_t s, unsigned long long bd_target) { k_Db_body<true>(d, s, bd_target); }
+__global__ void __launch_bounds__(256, CEM_D_MINB) k_Dbs(Dev d, int64_t s, unsigned long long bd_target) { k_Db_body<false>(d, s, bd_target); }
 
 __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2053,7 +2214,8 @@ __global__ void __launch_bounds__(256, CEM_C_MINB) k_C_w(Dev d, int64_t s, int c
     pdl_trigger();
     s = wave_step(d, s, rel);
     const int b = (int)blockIdx.x + boff;
-    block_C(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, false, (int)(s + 1));
+    if (d.part) block_C<true>(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, false, (int)(s + 1));
+    else block_C<false>(d, b, d.ubuf[(s + 1) & 1], crack_on(crack_every, s), s + 1, (int32_t)(s + 1), sm, false, (int)(s + 1));
     wave_done(d, ST_C, b, (int)(s + 1));
 }
 __global__ void __launch_bounds__(256, CEM_D_MINB) k_D_w(Dev d, int64_t s, int boff, int rel) {
@@ -2061,7 +2223,8 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_D_w(Dev d, int64_t s, int b
     s = wave_step(d, s, rel);
     const int b = (int)blockIdx.x + boff;
     wave_wait(d, ST_D, b, (int)(s + 1));
-    node_update(d, (int64_t)b * kDW, min((int64_t)(b + 1) * kDW, d.N), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s, ND_WAVE);
+    if (d.part) node_update<true>(d, (int64_t)b * kDW, min((int64_t)(b + 1) * kDW, d.N), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s, ND_WAVE);
+    else node_update<false>(d, (int64_t)b * kDW, min((int64_t)(b + 1) * kDW, d.N), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s, ND_WAVE);
     wave_done(d, ST_D, b, (int)(s + 1));
 }
 
@@ -2114,7 +2277,8 @@ __global__ void __launch_bounds__(256) k_AB_cur(Dev d, int64_t n) {
 }
 __global__ void __launch_bounds__(256, 4) k_C_cur(Dev d, int64_t n, int32_t stamp) {
     extern __shared__ double sm[];
-    block_C(d, blockIdx.x, d.ubuf[n & 1], true, n, stamp, sm);
+    if (d.part) block_C<true>(d, blockIdx.x, d.ubuf[n & 1], true, n, stamp, sm);
+    else block_C<false>(d, blockIdx.x, d.ubuf[n & 1], true, n, stamp, sm);
 }
 // nodes of tets split by cem_crack_update: new mass; frozen -> v = a = 0 and the pending
 // prediction u_{n+1} restarts from u_n
@@ -2189,6 +2353,7 @@ void set_smem_limits(int smem_bytes) {
     if (smem_bytes <= cur[dev]) return;
     cur[dev] = smem_bytes;
     cudaFuncSetAttribute(k_AB, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_Cs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_AB_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_C_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
@@ -2244,7 +2409,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 ++n;
             }
             if (c.c1 > c.c0) {
-                launch_pdl(k_C, (unsigned)(c.c1 - c.c0), (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every, c.c0);
+                launch_pdl(d.part ? k_C : k_Cs, (unsigned)(c.c1 - c.c0), (unsigned)d.blk, (size_t)d.smem_c, st, d, s, (int)crack_on(crack_every, s), c.c0);
                 ++n;
             }
         }
@@ -2258,8 +2423,8 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 ++n;
             }
         }
-        if (bd) launch_pdl(k_Db, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
-        else launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+        if (bd) launch_pdl(d.part ? k_Db : k_Dbs, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
+        else launch_pdl(d.part ? k_D : k_Ds, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
         return n + 1;
     }
     if (!ev) {  // programmatic dependent launches: stages overlap each other's launch and tail
@@ -2268,7 +2433,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
             launch_pdl(k_Cp, (unsigned)d.cp_grid, 256u, (size_t)cp_smem_bytes(d.cp_max_el, d.cp_max_nl), st, d, s,
                        crack_every);
         else
-            launch_pdl(k_C, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, crack_every, 0);
+            launch_pdl(d.part ? k_C : k_Cs, (unsigned)d.nblk[ST_C], (unsigned)d.blk, (size_t)d.smem_c, st, d, s, (int)crack_on(crack_every, s), 0);
         if (crit) {
             if (heavy) {
                 launch_pdl(k_filter, (unsigned)CEM_FILTER_GRID, 256u, (size_t)0, st, d, s);
@@ -2277,8 +2442,8 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
                 launch_pdl(k_crit, gcrit, 256u, (size_t)0, st, d, s, stream ? CEM_CRIT_POLLS : 0);
             }
         }
-        if (bd) launch_pdl(k_Db, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
-        else launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+        if (bd) launch_pdl(d.part ? k_Db : k_Dbs, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s, bd);
+        else launch_pdl(d.part ? k_D : k_Ds, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
         return crit ? (heavy ? 5 : 4) : 3;
     }
     cudaEventRecord(ev[0], st);
@@ -2287,7 +2452,7 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
     if (d.cp_on)
         k_Cp<<<d.cp_grid, 256, cp_smem_bytes(d.cp_max_el, d.cp_max_nl), st>>>(d, s, crack_every);
     else
-        k_C<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, crack_every, 0);
+        (d.part ? k_C : k_Cs)<<<d.nblk[ST_C], d.blk, d.smem_c, st>>>(d, s, (int)crack_on(crack_every, s), 0);
     cudaEventRecord(ev[2], st);
     if (crit) {
         if (heavy) {
@@ -2298,8 +2463,8 @@ int launch_staged_step(const Dev &d, int64_t s, int crack_every, cudaStream_t st
         }
     }
     cudaEventRecord(ev[3], st);
-    if (bd) k_Db<<<nblk_d(d), d.blk, 0, st>>>(d, s, bd);
-    else k_D<<<nblk_d(d), d.blk, 0, st>>>(d, s);
+    if (bd) (d.part ? k_Db : k_Dbs)<<<nblk_d(d), d.blk, 0, st>>>(d, s, bd);
+    else (d.part ? k_D : k_Ds)<<<nblk_d(d), d.blk, 0, st>>>(d, s);
     cudaEventRecord(ev[4], st);
     return crit ? (heavy ? 5 : 4) : 3;
 }
@@ -2315,7 +2480,7 @@ void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
 }
 
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {
-    launch_pdl(k_D, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+    launch_pdl(d.part ? k_D : k_Ds, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
 }
 
 int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel) {

@@ -568,6 +568,89 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, 
         }
         clk.mark("plan: bank order (nodes, edges)");
     }
+    // ---------------------------------------------------------------- exact partials (R27)
+    // partial q = entry q of a stage-C block's node list (final, bank-permuted order): its
+    // incidences among the block's tets as a blk + t (t local tet, a corner: stage C's force row)
+    // in pinc[pinc_off[q] ..);
+    // block b's entries fill pinc[4 e0, 4 e1) of its tet range.  nodeP: each node's partials in
+    // ascending q (= ascending block), padded with the all-zero partial |nl|.
+    {
+        const char *ev = getenv("CEM_PARTIALS");
+        p.partials = !(ev && atoi(ev) == 0);
+        const int nbt = (int)((E + blk - 1) / blk);
+        const int64_t NP = (int64_t)p.nl.size();
+        p.pinc_off.resize(NP + 1);
+        p.pinc.resize(4 * E);
+#pragma omp parallel
+        {
+            std::vector<int32_t> cnt, fill;
+#pragma omp for schedule(dynamic, 16)
+            for (int b = 0; b < nbt; ++b) {
+                const int64_t e0 = (int64_t)b * blk, e1 = std::min<int64_t>(E, e0 + blk);
+                const int32_t n0 = p.nl_off[b], nn = p.nl_off[b + 1] - n0;
+                cnt.assign(nn + 1, 0);
+                for (int64_t i = 4 * e0; i < 4 * e1; ++i) cnt[p.lconn[i] + 1]++;
+                for (int i = 0; i < nn; ++i) cnt[i + 1] += cnt[i];
+                for (int i = 0; i < nn; ++i) p.pinc_off[n0 + i] = (int32_t)(4 * e0 + cnt[i]);
+                fill.assign(cnt.begin(), cnt.end() - 1);
+                for (int64_t e = e0; e < e1; ++e)
+                    for (int a = 0; a < 4; ++a)  // stage C's shared-memory force row of (t, a): a blk + t
+                        p.pinc[4 * e0 + fill[p.lconn[4 * e + a]]++] = (uint16_t)(a * blk + (e - e0));
+            }
+        }
+        p.pinc_off[NP] = (int32_t)(4 * E);
+        // per block, its entries by descending incidence count (a warp's 32 lanes then loop
+        // over nearly equal counts)
+        p.pord.resize(NP);
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int b = 0; b < nbt; ++b) {
+            const int32_t n0 = p.nl_off[b], nn = p.nl_off[b + 1] - n0;
+            int32_t *o = p.pord.data() + n0;
+            for (int i = 0; i < nn; ++i) o[i] = i;
+            std::stable_sort(o, o + nn, [&](int32_t x, int32_t y) {
+                return p.pinc_off[n0 + x + 1] - p.pinc_off[n0 + x] > p.pinc_off[n0 + y + 1] - p.pinc_off[n0 + y];
+            });
+            // bank-aware order inside each entry's incidence list: the 32 lanes of a warp (32
+            // consecutive entries of o) read their u-th incidences together; force row a blk + t
+            // sits at bank position t mod 16 of the f_z plane (t mod 8 of the (x, y) plane), so
+            // step u greedily gives each lane the remaining incidence of the least-used position
+            for (int w0 = 0; w0 < nn; w0 += 32) {
+                const int w1 = std::min(nn, w0 + 32);
+                int mxc = 0;
+                for (int k = w0; k < w1; ++k) mxc = std::max(mxc, p.pinc_off[n0 + o[k] + 1] - p.pinc_off[n0 + o[k]]);
+                for (int u = 0; u < mxc; ++u) {
+                    int used[16] = {0};
+                    for (int k = w0; k < w1; ++k) {
+                        const int32_t j0 = p.pinc_off[n0 + o[k]], j1 = p.pinc_off[n0 + o[k] + 1];
+                        if (j0 + u >= j1) continue;
+                        int best = j0 + u;
+                        for (int j = j0 + u + 1; j < j1; ++j)
+                            if (used[(p.pinc[j] % blk) & 15] < used[(p.pinc[best] % blk) & 15]) best = j;
+                        std::swap(p.pinc[j0 + u], p.pinc[best]);
+                        ++used[(p.pinc[j0 + u] % blk) & 15];
+                    }
+                }
+            }
+        }
+        std::vector<int32_t> pc(N + 1, 0);
+        for (int64_t q = 0; q < NP; ++q) pc[p.nl[q] + 1]++;
+        int mx = 1;
+        for (int64_t k = 0; k < N; ++k) mx = std::max(mx, pc[k + 1]);
+        p.wp = (mx + 3) / 4 * 4;
+        for (int64_t k = 0; k < N; ++k) pc[k + 1] += pc[k];
+        p.nodeP.resize((size_t)N * p.wp);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < N * (int64_t)p.wp; ++i) p.nodeP[i] = (int32_t)NP;
+        std::vector<int32_t> fk(N, 0);
+        for (int64_t q = 0; q < NP; ++q) {
+            const int32_t k = p.nl[q];
+            p.nodeP[(size_t)k * p.wp + fk[k]++] = (int32_t)q;
+        }
+        clk.mark("plan: partials");
+        if (clk.on)
+            fprintf(stderr, "[cem timing] blocks: max_el %d max_nl %d max_tl %d max_nlb %d wp %d wn %d partials %zu\n",
+                    p.max_el, p.max_nl, p.max_tl, p.max_nlb, p.wp, p.wn, p.nl.size());
+    }
     // ---------------------------------------------------------------- instruction-lean layouts
     {
         int mx = 1;
