@@ -130,7 +130,7 @@ struct Offs {
     size_t nlb_off, nlb, tconn, trow, nrow, tflag;
     size_t rprev, wr_dof, epart, crit_list, crit_surv, vhat, edge_dirty, e_off, e_inc, edge_own;
     size_t wcnt, wdep_off, wdep, wstep, wncons, wcons_done;
-    size_t part, pinc_off, pinc, nodeP, pord;
+    size_t part, pinc_off, pinc, poff, pdst, pord;
     size_t total;
 };
 
@@ -207,10 +207,11 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     o.wstep = L.take<int64_t>(1);
     o.wncons = L.take<int32_t>((int64_t)w.ncons.size());
     o.wcons_done = L.take<int32_t>((int64_t)w.ncons.size());
-    o.part = L.take<double>(6 * ((int64_t)p.nl.size() + 1));  // + the all-zero partial
+    o.part = L.take<double>(6 * (int64_t)p.nl.size());
     o.pinc_off = L.take<int32_t>((int64_t)p.pinc_off.size());
     o.pinc = L.take<uint16_t>((int64_t)p.pinc.size());
-    o.nodeP = L.take<int32_t>((int64_t)p.nodeP.size());
+    o.poff = L.take<int32_t>((int64_t)p.poff.size());
+    o.pdst = L.take<int32_t>((int64_t)p.pdst.size());
     o.pord = L.take<int32_t>((int64_t)p.pord.size());
     o.total = L.off;
     return o;
@@ -225,7 +226,7 @@ int smem_c_for(const Plan &p) {
     // (partials also stage the block's incidence entries, 4 x u16 per tet, and per-entry offsets)
     // the force planes (12 doubles per tet) overlay the sigma planes
     const int sig = p.partials ? std::max(6 * (p.max_el | 1), 12 * p.blk) : 6 * (p.max_el | 1);
-    const int part = p.partials ? p.blk + (2 * p.max_nl + 2) / 2 + 1 : 0;  // pinc; offsets + order (int32)
+    const int part = p.partials ? p.blk + (3 * p.max_nl + 2) / 2 + 1 : 0;  // pinc; offsets, order, destinations (int32)
     return std::max(8 * (sig + (CEM_C_GEOX ? 6 : 3) * (p.max_nl | 1) + part), 8 * 1024);
 }
 int smem_bytes_for(const Plan &p) { return std::max(smem_ab_for(p), smem_c_for(p)); }  // odd plane strides
@@ -272,10 +273,9 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.part = p.partials ? at<double>(b, o.part) : nullptr;
     d.pinc_off = at<int32_t>(b, o.pinc_off);
     d.pinc = at<uint16_t>(b, o.pinc);
-    d.nodeP = at<int32_t>(b, o.nodeP);
+    d.poff = at<int32_t>(b, o.poff);
+    d.pdst = at<int32_t>(b, o.pdst);
     d.pord = at<int32_t>(b, o.pord);
-    d.wp = p.wp;
-    d.zpart = (int32_t)p.nl.size();
     d.nl_off = at<int32_t>(b, o.nl_off);
     d.nl = at<int32_t>(b, o.nl);
     d.lconn = at<uint16_t>(b, o.lconn);
@@ -534,10 +534,11 @@ cem_status upload(cem_ctx *ctx, const Offs &o) {
     CUDA_TRY(put(o.ledge, p.ledge.data(), sizeof(uint16_t) * p.ledge.size()));
     CUDA_TRY(put(o.tl_off, p.tl_off.data(), sizeof(int32_t) * p.tl_off.size()));
     CUDA_TRY(put(o.tl, p.tl.data(), sizeof(int32_t) * p.tl.size()));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.part), 0, sizeof(double) * 6 * (p.nl.size() + 1), st));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.part), 0, sizeof(double) * 6 * p.nl.size(), st));
     CUDA_TRY(put(o.pinc_off, p.pinc_off.data(), sizeof(int32_t) * p.pinc_off.size()));
     CUDA_TRY(put(o.pinc, p.pinc.data(), sizeof(uint16_t) * p.pinc.size()));
-    CUDA_TRY(put(o.nodeP, p.nodeP.data(), sizeof(int32_t) * p.nodeP.size()));
+    CUDA_TRY(put(o.poff, p.poff.data(), sizeof(int32_t) * p.poff.size()));
+    CUDA_TRY(put(o.pdst, p.pdst.data(), sizeof(int32_t) * p.pdst.size()));
     CUDA_TRY(put(o.pord, p.pord.data(), sizeof(int32_t) * p.pord.size()));
 
     CUDA_TRY(put(o.sched, p.sched.data(), sizeof(int32_t) * p.sched.size()));
@@ -1671,6 +1672,8 @@ cem_status cem_set_profiling(cem_ctx *ctx, int on) {
 bool crit_heavy(const cem_ctx *ctx) { return ctx->crit_seen && *ctx->crit_seen >= ctx->critb_min; }
 // the staged path's criterion mode from the recent list length (racy by design: results never depend on it)
 int crit_mode(const cem_ctx *ctx) {
+    static const int forced = getenv("CEM_CRIT_MODE") ? atoi(getenv("CEM_CRIT_MODE")) : -1;  // (measurement knob)
+    if (forced >= 0 && forced <= CRIT_IDLE) return forced;
     if (!ctx->crit_seen) return CRIT_LIST;
     const int n = *ctx->crit_seen;
     if (n >= ctx->critb_min) return CRIT_HEAVY;

@@ -187,8 +187,8 @@ struct Plan {
     std::vector<int32_t> pinc_off;    // [|nl| + 1] entries of partial q in pinc
     hvec<uint16_t> pinc;              // [4E] a blk + t (t: tet within the block, a: corner), per partial
     std::vector<int32_t> pord;        // [|nl|] per block: node-list entries by descending incidence count
-    int wp = 4;                       // ELL width of a node's partials (multiple of 4)
-    hvec<int32_t> nodeP;              // [N][wp] partials of each node, padded with |nl| (all-zero partial)
+    std::vector<int32_t> poff;        // [N + 1] node-major partial records: node k's at [poff[k], poff[k+1])
+    std::vector<int32_t> pdst;        // [|nl|] node-major record of partial q (ascending q per node)
 };
 
 void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig = nullptr, bool with_deps = true);
@@ -245,13 +245,12 @@ struct Dev {
     const int32_t *nodeE;      // [N][wn]
     int we, wn, we_max;        // ELL widths; we_max = largest edge incidence count
     int32_t zslot;             // index of the all-zero force slot (ELL padding)
-    double *part;              // [|nl| + 1][6] exact partials (s_x, s_y, s_z, c_x, c_y, c_z); null: force slots
+    double *part;              // [|nl|][6] exact partials (s_x, s_y, s_z, c_x, c_y, c_z), node-major; null: force slots
     const int32_t *pinc_off;   // [|nl| + 1]
     const uint16_t *pinc;      // [4E] a blk + t per partial (stage C's force row)
     const int32_t *pord;       // [|nl|] per block: its node-list entries by descending incidence count
-    const int32_t *nodeP;      // [N][wp]
-    int wp;
-    int32_t zpart;             // index of the all-zero partial (ELL padding)
+    const int32_t *poff;       // [N + 1] node k's partial records (node-major) at [poff[k], poff[k+1])
+    const int32_t *pdst;       // [|nl|] node-major record of partial q
     const int32_t *nl_off, *nl, *el_off, *el, *tl_off, *tl, *nlb_off, *nlb;
     const uint16_t *tconn, *trow, *nrow;
     const uint16_t *lconn, *ledge;

@@ -1072,6 +1072,7 @@ __device__ __forceinline__ void c_partials(const Dev &d, int b, const double *sm
                                                                (CEM_C_GEOX ? 6 : 3) * pstride(nn));  // staged at block start
     const int32_t *spoff = reinterpret_cast<const int32_t *>(spinc + 4 * nthr);  // global offsets [nn + 1]
     const int32_t *spord = spoff + nn + 1;                                       // entry order [nn]
+    const int32_t *spdst = spord + nn;                                           // node-major record [nn]
     const int32_t base = 4 * b * d.blk;
     cpa_wait_all();
     __syncthreads();
@@ -1099,7 +1100,7 @@ __device__ __forceinline__ void c_partials(const Dev &d, int b, const double *sm
                 xacc(sz, cz, z[u]);
             }
         }
-        double2 *o = reinterpret_cast<double2 *>(d.part + 6 * (int64_t)(n0 + i));
+        double2 *o = reinterpret_cast<double2 *>(d.part + 6 * (int64_t)spdst[i]);
         o[0] = make_double2(sx, sy);
         o[1] = make_double2(sz, cx);
         o[2] = make_double2(cy, cz);
@@ -1156,6 +1157,7 @@ __device__ __forceinline__ void block_C(const Dev &d, int b, const double4 *u, b
         if (e0 + tid < d.E) cpa8(reinterpret_cast<uint2 *>(spinc) + tid, reinterpret_cast<const uint2 *>(d.pinc) + e0 + tid);
         for (int i = tid; i <= nn; i += nthr) cpa4(spoff + i, d.pinc_off + n0 + i);
         for (int i = tid; i < nn; i += nthr) cpa4(spoff + nn + 1 + i, d.pord + n0 + i);
+        for (int i = tid; i < nn; i += nthr) cpa4(spoff + 2 * nn + 1 + i, d.pdst + n0 + i);
         cpa_commit();
     }
     stage_wait(d, ST_C, b, wneed);  // sigma records come from stage AB
@@ -1643,11 +1645,12 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     const int4 *row = reinterpret_cast<const int4 *>(d.nodeE + (uint32_t)k * (uint32_t)d.wn);
     constexpr int kB = CEM_D_BATCH, kQ = kB / 4;  // slots per batch, int4 index loads per batch
     int4 q[kQ];
-    // partial mode (R27): the node's exact partials from stage C (ELL row of nodeP, 4 per int4)
+    // partial mode (R27): the node's exact partials from stage C, consecutive records [p0, p1)
     constexpr bool pm = PM;
-    const int4 *prow = reinterpret_cast<const int4 *>(d.nodeP + (uint32_t)k * (uint32_t)d.wp);
+    int32_t p0 = 0, p1 = 0;
     if (pm) {
-        q[0] = __ldg(prow);
+        p0 = __ldg(d.poff + k);
+        p1 = __ldg(d.poff + k + 1);
     } else {
 #pragma unroll
         for (int j = 0; j < kQ; ++j) q[j] = j * 4 < d.wn ? __ldg(row + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
@@ -1664,28 +1667,21 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     const double *fec = d.fe + (c < 3 ? c : 0);  // lane c: component c of each slot (lane 3: unused sum)
     double f = 0.0, fc = 0.0;  // exact-sum accumulator (R27)
     if (pm) {
-        // lane c: component c of each partial, s and c terms (padding: the all-zero partial)
+        // lane c: component c of each partial, s and c terms, four records per pass
         const double *pc = d.part + (c < 3 ? c : 0);
-        for (int w = 0;;) {
-            const int32_t pq[4] = {q[0].x, q[0].y, q[0].z, q[0].w};
+        for (int32_t p = p0; p < p1; p += 4) {
             double xs[4], xe[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                CEM_BOUND(d, pq[t] >= 0 && pq[t] <= d.zpart);
-                // padding: no load (every padded entry would hit the one all-zero record: a hot L2 line)
-                const bool live = pq[t] != d.zpart;
-                xs[t] = live ? __ldcg(pc + 6 * (int64_t)pq[t]) : 0.0;
-                xe[t] = live ? __ldcg(pc + 6 * (int64_t)pq[t] + 3) : 0.0;
+                const bool live = p + t < p1;
+                xs[t] = live ? __ldcg(pc + 6 * (int64_t)(p + t)) : 0.0;  // (+0.0: an exact no-op)
+                xe[t] = live ? __ldcg(pc + 6 * (int64_t)(p + t) + 3) : 0.0;
             }
-            w += 4;
-            const bool more = pq[3] != d.zpart && w < d.wp;
-            if (more) q[0] = __ldg(prow + (w >> 2));
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 xacc(f, fc, xs[t]);
                 xacc(f, fc, xe[t]);
             }
-            if (!more) break;
         }
     } else {
 #if CEM_D_PIPE

@@ -572,8 +572,8 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, 
     // partial q = entry q of a stage-C block's node list (final, bank-permuted order): its
     // incidences among the block's tets as a blk + t (t local tet, a corner: stage C's force row)
     // in pinc[pinc_off[q] ..);
-    // block b's entries fill pinc[4 e0, 4 e1) of its tet range.  nodeP: each node's partials in
-    // ascending q (= ascending block), padded with the all-zero partial |nl|.
+    // block b's entries fill pinc[4 e0, 4 e1) of its tet range.  Records are node-major: partial q
+    // goes to record pdst[q], node k's records are [poff[k], poff[k+1]) (ascending block).
     {
         const char *ev = getenv("CEM_PARTIALS");
         p.partials = !(ev && atoi(ev) == 0);
@@ -632,24 +632,17 @@ void build_plan(const HostMesh &h, int blk, Plan &p, const uint8_t *tflag_orig, 
                 }
             }
         }
-        std::vector<int32_t> pc(N + 1, 0);
-        for (int64_t q = 0; q < NP; ++q) pc[p.nl[q] + 1]++;
-        int mx = 1;
-        for (int64_t k = 0; k < N; ++k) mx = std::max(mx, pc[k + 1]);
-        p.wp = (mx + 3) / 4 * 4;
-        for (int64_t k = 0; k < N; ++k) pc[k + 1] += pc[k];
-        p.nodeP.resize((size_t)N * p.wp);
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < N * (int64_t)p.wp; ++i) p.nodeP[i] = (int32_t)NP;
-        std::vector<int32_t> fk(N, 0);
-        for (int64_t q = 0; q < NP; ++q) {
-            const int32_t k = p.nl[q];
-            p.nodeP[(size_t)k * p.wp + fk[k]++] = (int32_t)q;
-        }
+        // node-major records: node k's partials (ascending q, i.e. ascending block) are consecutive
+        p.poff.assign(N + 1, 0);
+        for (int64_t q = 0; q < NP; ++q) p.poff[p.nl[q] + 1]++;
+        for (int64_t k = 0; k < N; ++k) p.poff[k + 1] += p.poff[k];
+        p.pdst.resize(NP);
+        std::vector<int32_t> fk(p.poff.begin(), p.poff.end() - 1);
+        for (int64_t q = 0; q < NP; ++q) p.pdst[q] = fk[p.nl[q]]++;
         clk.mark("plan: partials");
         if (clk.on)
-            fprintf(stderr, "[cem timing] blocks: max_el %d max_nl %d max_tl %d max_nlb %d wp %d wn %d partials %zu\n",
-                    p.max_el, p.max_nl, p.max_tl, p.max_nlb, p.wp, p.wn, p.nl.size());
+            fprintf(stderr, "[cem timing] blocks: max_el %d max_nl %d max_tl %d max_nlb %d partials %zu\n",
+                    p.max_el, p.max_nl, p.max_tl, p.max_nlb, p.nl.size());
     }
     // ---------------------------------------------------------------- instruction-lean layouts
     {
