@@ -161,6 +161,7 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     o.a = L.take<double4>(N);
     o.srec = L.take<double>(4 * S);
     o.srec2 = L.take<double>(2 * S);
+    o.part = L.take<double>(6 * (int64_t)p.nl.size());  // (after the sigma planes: one L2 window can span both)
     o.fe = L.take<double>(CEM_FES * fe_slots(E));  // + the zero slot
     o.ctr = L.take<int32_t>(32);
     o.rec_step = L.take<int64_t>(E);
@@ -207,7 +208,6 @@ Offs layout(const HostMesh &h, const Plan &p, const WavePlan &w) {
     o.wstep = L.take<int64_t>(1);
     o.wncons = L.take<int32_t>((int64_t)w.ncons.size());
     o.wcons_done = L.take<int32_t>((int64_t)w.ncons.size());
-    o.part = L.take<double>(6 * (int64_t)p.nl.size());
     o.pinc_off = L.take<int32_t>((int64_t)p.pinc_off.size());
     o.pinc = L.take<uint16_t>((int64_t)p.pinc.size());
     o.poff = L.take<int32_t>((int64_t)p.poff.size());
@@ -1577,14 +1577,22 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
         int maxwin = 0, maxpers = 0;
         cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
         cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
-        const size_t bytes = (size_t)((char *)(ctx->d.srec2 + 2 * ctx->h.S) - (char *)ctx->d.srec);
+        // CEM_L2_WIN (measurement knob): 1 sigma planes (default), 2 the partials, 3 both
+        const int wsel = getenv("CEM_L2_WIN") ? atoi(getenv("CEM_L2_WIN")) : 1;
+        char *wbase = (char *)ctx->d.srec, *wend = (char *)(ctx->d.srec2 + 2 * ctx->h.S);
+        if (ctx->d.part && wsel >= 2) {
+            if (wsel == 2) wbase = (char *)ctx->d.part;
+            wend = (char *)(ctx->d.part + 6 * ctx->p.nl.size());
+        }
+        const size_t bytes = (size_t)(wend - wbase);
         const size_t win = std::min(bytes, (size_t)std::max(0, maxwin));
         // only when the planes fit the set-aside whole: a partial window (hit ratio < 1 over a larger
         // mesh's planes) thrashed -- config 4 on one GPU 1087 -> 1614 us/step
         // (single-GPU contexts only: loopback ranks share rank 0's stream; the window lives on the
         // library's private stream, and cem_destroy restores the set-aside it raised)
-        if (!ctx->dist && want > 0.0 && win > 0 && win == bytes && bytes <= (size_t)std::max(0, maxpers)) {
-            const double hit = std::min(want, 1.0);
+        const bool fits = bytes <= (size_t)std::max(0, maxpers) || wsel == 3;
+        if (!ctx->dist && want > 0.0 && win > 0 && win == bytes && fits) {
+            const double hit = std::min(want, std::min(1.0, (double)std::max(0, maxpers) / (double)bytes));
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             const size_t aside = std::min((size_t)maxpers, (size_t)(win * hit));
@@ -1593,7 +1601,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
                 ctx->l2_limit_prev = cur;
             }
             cudaStreamAttrValue a = {};
-            a.accessPolicyWindow.base_ptr = ctx->d.srec;
+            a.accessPolicyWindow.base_ptr = wbase;
             a.accessPolicyWindow.num_bytes = win;
             a.accessPolicyWindow.hitRatio = (float)hit;
             a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
