@@ -229,6 +229,22 @@ CEM_API cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out);
 /* Synchronise and fill *out (see cem_state_out). Returns CEM_ENONFINITE if flagged. */
 CEM_API cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where);
 
+/* Checkpoint / resume (SURVEY.md §5 "Checkpoint / resume"): overwrite the state of a
+ * single-GPU tetrahedral context with a snapshot taken by cem_get_state(CEM_HOST) -- possibly
+ * of another context built from the same mesh, material and loads.  `in` uses cem_state_out's
+ * layouts in the caller's numbering, HOST memory, all read-only:
+ *   u, v, a [n_nodes][3], tet_state [n_tets], mass [n_nodes]   required (non-NULL)
+ *   rec_step/rec_elem/rec_cand/rec_G/rec_area [n_records]       required when n_records > 0
+ *   step                                                        the step index n of the snapshot
+ * Everything the next step reads is rebuilt from these: the predictor u_{n+1} = (u_n + dt v_n)
+ * + (dt^2/2) a_n (the stage kernels' expression), the smoothing-domain volumes
+ * Vhat_s from the active flags (ascending original tet id), the split records (U_d follows from
+ * them).  Continuing from the snapshot is then bitwise identical to never having stopped.
+ * Not part of the checkpoint: the energy ledger's reaction work of prescribed dofs, which reads
+ * NaN after this call.  Synchronises.  CEM_ESTATE for multi-rank and hexahedral contexts,
+ * CEM_EINVAL for a NULL required array or n_records < 0 / > n_tets. */
+CEM_API cem_status cem_set_state(cem_ctx *ctx, const cem_state_out *in);
+
 /* Energy ledger at the current step n (SPEC.md update_energy_ledger;
  * oracle/cem_oracle.c orc_energy defines each quantity and its association order):
  *   kinetic        T   = 1/2 sum_k m_k |v_k|^2

@@ -94,6 +94,7 @@ _lib.cem_step.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
 _lib.cem_crack_update.argtypes = [C.c_void_p, I64]
 _lib.cem_get_state.argtypes = [C.c_void_p, _P(cem_state_out), C.c_int]
 _lib.cem_energy.argtypes = [C.c_void_p, _P(cem_energy_out)]
+_lib.cem_set_state.argtypes = [C.c_void_p, _P(cem_state_out)]
 _lib.cem_sizes.argtypes = [C.c_void_p, I64, I64, I64]
 _lib.cem_launch_count.argtypes = [C.c_void_p]
 _lib.cem_launch_count.restype = C.c_int64
@@ -104,7 +105,7 @@ _lib.cem_last_error.restype = C.c_char_p
 _lib.cem_destroy.argtypes = [C.c_void_p]
 _lib.cem_abi_version.restype = C.c_int32
 for _f in ("cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state",
-           "cem_sizes", "cem_set_profiling", "cem_kernel_times", "cem_energy"):
+           "cem_sizes", "cem_set_profiling", "cem_kernel_times", "cem_energy", "cem_set_state"):
     getattr(_lib, _f).restype = C.c_int
 
 class cem_part_out(C.Structure):
@@ -125,7 +126,8 @@ _lib.cem_step_group.restype = C.c_int
 _lib.cem_merge_records.argtypes = [C.c_int64, I64, I32, D, D, I64, D]
 _lib.cem_merge_records.restype = C.c_int
 
-EXPORTED = ["cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state", "cem_energy",
+EXPORTED = ["cem_workspace_size", "cem_init_mesh", "cem_step", "cem_crack_update", "cem_get_state", "cem_set_state",
+            "cem_energy",
             "cem_sizes", "cem_launch_count", "cem_set_profiling", "cem_kernel_times",
             "cem_last_error", "cem_destroy", "cem_abi_version", "cem_partition", "cem_partition_free",
             "cem_nccl_unique_id", "cem_step_group", "cem_merge_records"]
@@ -303,6 +305,21 @@ class Simulation:
         nr = min(out.n_records, cap)
         return State(u, v, a, st, m, out.step, out.time, out.dt, out.n_active, out.dissipated,
                      out.nonfinite, out.nonfinite_node, rs[:nr], re[:nr], rk[:nr], rg[:nr], ra[:nr])
+
+    def set_state(self, s: State) -> None:
+        """cem_set_state: resume from a snapshot of state() (this or another simulation of the same
+        mesh, material and loads); the records must be complete (state(records=True))."""
+        keep = [_arr(s.u, np.float64, (-1, 3)), _arr(s.v, np.float64, (-1, 3)), _arr(s.a, np.float64, (-1, 3)),
+                _arr(s.tet_state, np.uint8), _arr(s.mass, np.float64), _arr(s.rec_step, np.int64),
+                _arr(s.rec_elem, np.int32), _arr(s.rec_cand, np.int32), _arr(s.rec_G, np.float64),
+                _arr(s.rec_area, np.float64)]
+        inp = cem_state_out()
+        inp.u, inp.v, inp.a = _ptr(keep[0], D), _ptr(keep[1], D), _ptr(keep[2], D)
+        inp.tet_state, inp.mass = _ptr(keep[3], U8), _ptr(keep[4], D)
+        inp.rec_step, inp.rec_elem, inp.rec_cand = _ptr(keep[5], I64), _ptr(keep[6], I32), _ptr(keep[7], I32)
+        inp.rec_G, inp.rec_area = _ptr(keep[8], D), _ptr(keep[9], D)
+        inp.n_records, inp.rec_capacity, inp.step = keep[5].size, keep[5].size, int(s.step)
+        self._check(_lib.cem_set_state(self._h, C.byref(inp)))
 
     def device_state(self, records=True) -> dict:
         """cem_get_state(CEM_DEVICE): torch tensors on the simulation's device, filled by the

@@ -1,5 +1,6 @@
 // cem_api.cu -- the C ABI of libcem.so (include/cem.h): context, device workspace layout,
 // host<->device transfers, the persistent-kernel step loop and state readback.
+#include <nvtx3/nvToolsExt.h>  // (header-only NVTX3: ranges cost nothing unless a tool attaches)
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -109,6 +110,12 @@ int block_size() {
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// NVTX range of one ABI call (SURVEY.md §5 "Tracing": nsys / ncu timelines show the calls)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 // force slots: 4 per tet in 32-tet tiles, + the all-zero slot
 int64_t fe_slots(int64_t E) { return 4 * ((E + 31) / 32) * 32 + 1; }
 
@@ -1407,6 +1414,7 @@ cem_status cem_init_mesh(const cem_mesh_in *mesh, const cem_material *mat, const
                          const cem_opts *opts, cem_ctx **out) {
     if (!out) return CEM_EINVAL;
     *out = nullptr;
+    NvtxRange nv("cem_init_mesh");
     g_init_err.clear();
     if (mesh && mesh->nodes_per_elem != 0 && mesh->nodes_per_elem != 4 && mesh->nodes_per_elem != 8) {
         g_init_err = "cem_init_mesh: nodes_per_elem must be 0, 4 (tets) or 8 (hexahedra)";
@@ -1691,6 +1699,14 @@ int crit_mode(const cem_ctx *ctx) {
 
 cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (!ctx || nsteps < 0) return CEM_EINVAL;
+    NvtxRange nv("cem_step");
+    if (ctx->dist && ctx->comm) {  // a failed communicator (ncclCommGetAsyncError) stops the run
+        std::string e;
+        if (nccl_async_error(ctx->comm, e)) {
+            ctx->err = e;
+            return CEM_ENCCL;
+        }
+    }
     if (nsteps == 0) return CEM_OK;
     if (crack_every < 0) crack_every = 0;
     if (ctx->hexa && crack_every > 0) {
@@ -1883,8 +1899,87 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
     return CEM_OK;
 }
 
+cem_status cem_set_state(cem_ctx *ctx, const cem_state_out *in) {
+    if (!ctx || !in) return CEM_EINVAL;
+    NvtxRange nv("cem_set_state");
+    if (ctx->dist || ctx->hexa) {
+        ctx->err = "cem_set_state: single-GPU tetrahedral contexts only";
+        return CEM_ESTATE;
+    }
+    const HostMesh &h = ctx->h;
+    const Plan &p = ctx->p;
+    const int64_t N = h.N, E = h.E, S = h.S, nr = in->n_records;
+    if (!in->u || !in->v || !in->a || !in->tet_state || !in->mass || in->step < 0 || nr < 0 || nr > E ||
+        (nr > 0 && (!in->rec_step || !in->rec_elem || !in->rec_cand || !in->rec_G || !in->rec_area))) {
+        ctx->err = "cem_set_state: a required array is NULL or a count is out of range";
+        return CEM_EINVAL;
+    }
+    StreamFence fence(ctx);
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaStreamSynchronize(st));  // earlier steps done before their buffers are overwritten
+    const int64_t n = in->step;
+    const double dt = ctx->d.dt, hdt2 = ctx->d.hdt2;
+    std::vector<double4> u0(N), u1(N), v4(N), a4(N);
+    std::vector<double> m(N);
+    for (int64_t kn = 0; kn < N; ++kn) {
+        const int64_t k = p.node_new2old[kn];
+        double uu[3], vv[3], aa[3], up[3];
+        for (int c = 0; c < 3; ++c) {
+            uu[c] = in->u[3 * k + c];
+            vv[c] = in->v[3 * k + c];
+            aa[c] = in->a[3 * k + c];
+            up[c] = (uu[c] + dt * vv[c]) + hdt2 * aa[c];  // predictor (stage D's expression)
+        }
+        u0[kn] = make_double4(uu[0], uu[1], uu[2], 0.0);
+        u1[kn] = make_double4(up[0], up[1], up[2], 0.0);
+        v4[kn] = make_double4(vv[0], vv[1], vv[2], 0.0);
+        a4[kn] = make_double4(aa[0], aa[1], aa[2], 0.0);
+        m[kn] = in->mass[k];
+    }
+    std::vector<uint8_t> stt(E);
+    for (int64_t en = 0; en < E; ++en) stt[en] = in->tet_state[p.tet_new2old[en]] ? 1 : 0;
+    std::vector<double> vh(S, 0.0);  // Vhat_s over the active incident tets, ascending original id
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < S; ++s) {
+        double acc = 0.0;
+        for (int32_t j = p.edge_off[s]; j < p.edge_off[s + 1]; ++j)
+            if (stt[p.edge_inc[j]]) acc = acc + p.geoV[p.edge_inc[j]];
+        vh[s] = acc;
+    }
+    std::vector<double> nanv(3 * N, std::nan(""));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.ubuf[n & 1], u0.data(), sizeof(double4) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.ubuf[(n + 1) & 1], u1.data(), sizeof(double4) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.v, v4.data(), sizeof(double4) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.a, a4.data(), sizeof(double4) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.mass, m.data(), sizeof(double) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.state, stt.data(), E, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.vhat, vh.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->d.edge_dirty, 0, S, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->d.dirty, 0, sizeof(int32_t) * N, st));
+    if (ctx->d.rprev) {  // (the reaction-work ledger is not part of the checkpoint)
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.rprev, nanv.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.wr_dof, nanv.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    }
+    if (nr > 0) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.rec_step, in->rec_step, 8 * nr, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.rec_elem, in->rec_elem, 4 * nr, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.rec_cand, in->rec_cand, 4 * nr, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.rec_G, in->rec_G, 8 * nr, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d.rec_area, in->rec_area, 8 * nr, cudaMemcpyHostToDevice, st));
+    }
+    int32_t ctr[32] = {(int32_t)nr, 0, INT32_MAX};  // records, no non-finite value, empty lists
+    CUDA_TRY(cudaMemcpyAsync(ctx->d.ctr, ctr, sizeof ctr, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->d.crit_list, 0, sizeof(int64_t) * E, st));  // (stamps of the old steps)
+    CUDA_TRY(cudaStreamSynchronize(st));  // (the host vectors above go out of scope)
+    ctx->step = n;
+    ctx->cnt_valid = -1;   // persistent / wave counters refilled for the new step
+    ctx->wcnt_valid = -1;
+    return CEM_OK;
+}
+
 cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
     if (!ctx || !out) return CEM_EINVAL;
+    NvtxRange nv("cem_energy");
     StreamFence fence(ctx);
     cudaStream_t st = ctx->stream;
     cem_state_out so{};
@@ -1920,6 +2015,14 @@ cem_status cem_energy(cem_ctx *ctx, cem_energy_out *out) {
 
 cem_status cem_get_state(cem_ctx *ctx, cem_state_out *out, int where) {
     if (!ctx || !out) return CEM_EINVAL;
+    NvtxRange nv("cem_get_state");
+    if (ctx->dist && ctx->comm) {
+        std::string e;
+        if (nccl_async_error(ctx->comm, e)) {
+            ctx->err = e;
+            return CEM_ENCCL;
+        }
+    }
     StreamFence fence(ctx);
     cudaStream_t st = ctx->stream;
     const HostMesh &h = ctx->h;

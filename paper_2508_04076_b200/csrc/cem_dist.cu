@@ -124,6 +124,7 @@ typedef int (*fn_group)();
 typedef const char *(*fn_err)(int);
 typedef int (*fn_allgather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_asyncerr)(ncclComm_t, int *);
 struct Nccl {
     void *h = nullptr;
     fn_getid getid;
@@ -134,6 +135,7 @@ struct Nccl {
     fn_err err;
     fn_allgather allgather;
     fn_allreduce allreduce;
+    fn_asyncerr asyncerr;
 };
 Nccl &nccl() {
     static Nccl n;
@@ -150,6 +152,7 @@ Nccl &nccl() {
         n.err = (fn_err)dlsym(n.h, "ncclGetErrorString");
         n.allgather = (fn_allgather)dlsym(n.h, "ncclAllGather");
         n.allreduce = (fn_allreduce)dlsym(n.h, "ncclAllReduce");
+        n.asyncerr = (fn_asyncerr)dlsym(n.h, "ncclCommGetAsyncError");
         if (!n.getid || !n.init || !n.send || !n.recv || !n.gstart || !n.gend) {
             dlclose(n.h);
             n.h = nullptr;
@@ -194,6 +197,16 @@ bool nccl_comm_init(void **comm, int nranks, int rank, const void *id128, std::s
         return false;
     }
     *comm = c;
+    return true;
+}
+
+bool nccl_async_error(void *comm, std::string &err) {
+    Nccl &n = nccl();
+    if (!n.h || !n.asyncerr || !comm) return false;
+    int res = 0;
+    const int rc = n.asyncerr(static_cast<ncclComm_t>(comm), &res);
+    if (rc == 0 && res == 0) return false;
+    err = std::string("NCCL asynchronous error: ") + (n.err ? n.err(rc ? rc : res) : "error");
     return true;
 }
 

@@ -41,6 +41,8 @@ struct P2P {
 bool nccl_unique_id(void *id128, std::string &err);
 bool nccl_comm_init(void **comm, int nranks, int rank, const void *id128, std::string &err);
 void nccl_comm_destroy(void *comm);
+// ncclCommGetAsyncError: true (and a message) if the communicator has failed asynchronously
+bool nccl_async_error(void *comm, std::string &err);
 void exchange_pack(const Exchange &x, const double4 *u, const uint8_t *state, cudaStream_t st);
 void exchange_unpack(const Exchange &x, double4 *u, uint8_t *state, const int32_t *eedge, int64_t E,
                      uint8_t *edge_dirty, cudaStream_t st, const uint8_t *recvbuf = nullptr);

@@ -96,3 +96,9 @@ def test_maximum_size_rejected_before_reading():
                                T.ctypes.data_as(C.POINTER(C.c_int32)), None, None)
         b = C.c_size_t()
         assert cem._lib.cem_workspace_size(C.byref(mesh), None, C.byref(b)) == cem.CEM_EINVAL
+
+
+def test_set_state_null_arguments():
+    """cem_set_state validates its arguments before touching a context (no GPU needed)."""
+    import paper_2508_04076_b200 as cem
+    assert cem._lib.cem_set_state(None, None) == cem.CEM_EINVAL
