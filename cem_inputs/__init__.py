@@ -170,9 +170,11 @@ def hex_lattice(cells, dims, seed, jitter=0.05):
 
 
 def hex_block(cells=(12, 8, 4), dims=(0.06, 0.04, 0.02), seed=8, traction=1e6, jitter=0.05, steps=0,
-              material=None):
+              material=None, gc=np.inf, notch=0.0):
     """Hexahedral block for the ES-H-FEM path: traction +-t on the y faces as
-    two triangles per loaded quad face (t A/3 per triangle node), no cracking (Gc = inf)."""
+    two triangles per loaded quad face (t A/3 per triangle node).  gc: critical energy release rate
+    of every hex (inf: no cracking); notch > 0: the hexes of the middle y layer with x below
+    notch * length are inactive (an edge notch across the pulled direction)."""
     mat = dict(E=32e9, nu=0.2, rho=2450.0) if material is None else material
     X, H, ijk = hex_lattice(cells, dims, seed, jitter=jitter)
     ny = int(cells[1])
@@ -186,8 +188,14 @@ def hex_block(cells=(12, 8, 4), dims=(0.06, 0.04, 0.02), seed=8, traction=1e6, j
                     faces += [[q[0], q[1], q[2]], [q[0], q[2], q[3]]]
                     tr += [[0.0, sgn * traction, 0.0]] * 2
     E = H.shape[0]
+    state = np.ones(E, np.uint8)
+    if notch > 0:
+        nx = int(cells[0])
+        ci = np.arange(E) % nx
+        cj = (np.arange(E) // nx) % ny
+        state[(cj == ny // 2) & (ci < int(round(notch * nx)))] = 0
     return Problem(name=f"hex_block_{cells[0]}x{cells[1]}x{cells[2]}", X=X, tets=H,
-                   tet_state=np.ones(E, np.uint8), tet_gc=np.full(E, np.inf), Gc=np.inf,
+                   tet_state=state, tet_gc=np.full(E, float(gc)), Gc=float(gc),
                    tface=np.asarray(faces, np.int32).reshape(-1, 3), tface_t=np.asarray(tr, np.float64).reshape(-1, 3),
                    vbc_node=np.zeros(0, np.int32), vbc_mask=np.zeros(0, np.uint8), vbc_v0=np.zeros((0, 3)),
                    steps=steps, cells=tuple(cells), dims=tuple(dims), node_ijk=ijk, **mat)

@@ -93,10 +93,18 @@ def lib():
         L.hx_create.restype = C.c_void_p
         L.hx_create.argtypes = [C.c_int64, D, C.c_int64, I32, U8, C.c_double, C.c_double, C.c_double,
                                 C.c_int64, I32, D, C.c_int64, I32, U8, D, C.c_double, C.c_double, C.c_double,
-                                C.c_double, D, D, C.c_char_p, C.c_int]
+                                C.c_double, D, D, D, C.c_uint32, C.c_char_p, C.c_int]
         L.hx_destroy.argtypes = [C.c_void_p]
-        L.hx_run.argtypes = [C.c_void_p, C.c_int64]
-        L.hx_n_edges.argtypes = [C.c_void_p]; L.hx_n_edges.restype = C.c_int64
+        L.hx_run.argtypes = [C.c_void_p, C.c_int64, C.c_int32]; L.hx_run.restype = C.c_int
+        for f in ("hx_n_edges", "hx_n_edges_all", "hx_n_records"):
+            getattr(L, f).argtypes = [C.c_void_p]; getattr(L, f).restype = C.c_int64
+        L.hx_dissipated.argtypes = [C.c_void_p]; L.hx_dissipated.restype = C.c_double
+        L.hx_get_records.argtypes = [C.c_void_p, I64, I32, I32, D, D]
+        L.hx_get_elements.argtypes = [C.c_void_p, U8, U8, I32, D]
+        L.hx_candidates.argtypes = [C.c_void_p, D, C.c_int64, D, D, I32]
+        L.hx_force_split.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
+        L.hx_edge_stress_all.argtypes = [C.c_void_p, D, D, D, I32]
+        L.orc_tet_cand_x.argtypes = [D, D, D, C.c_uint32, D, D]
         L.hx_dt.argtypes = [C.c_void_p]; L.hx_dt.restype = C.c_double
         L.hx_get_state.argtypes = [C.c_void_p, D, D, D, D]
         L.hx_get_fext.argtypes = [C.c_void_p, D]
@@ -251,9 +259,10 @@ class Oracle:
 
 
 class HexOracle:
-    """ES-H-FEM oracle on trilinear hexahedra (cem_oracle_hex.c; elastodynamics, no cracking)."""
+    """ES-H-FEM oracle on trilinear hexahedra (cem_oracle_hex.c): elastodynamics and crack patterns
+    III-VI with triangular-prism remainders (readings R23-R29)."""
 
-    def __init__(self, prob, dt=None):
+    def __init__(self, prob, dt=None, flags=0):
         L = lib()
         self.prob = prob
         fn = getattr(prob, "f_nodal", None)
@@ -261,17 +270,19 @@ class HexOracle:
         self._keep = [_c(prob.X, np.float64), _c(prob.tets, np.int32), _c(prob.tet_state, np.uint8),
                       _c(prob.tface, np.int32), _c(prob.tface_t, np.float64), _c(prob.vbc_node, np.int32),
                       _c(prob.vbc_mask, np.uint8), _c(prob.vbc_v0, np.float64), fn,
-                      _c(getattr(prob, "body", (0.0, 0.0, 0.0)), np.float64)]
-        X, H, st, tf, tt, vn, vm, vv, fn, body = self._keep
+                      _c(getattr(prob, "body", (0.0, 0.0, 0.0)), np.float64),
+                      _c(getattr(prob, "tet_gc", np.full(prob.tets.shape[0], np.inf)), np.float64)]
+        X, H, st, tf, tt, vn, vm, vv, fn, body, gc = self._keep
         err = C.create_string_buffer(256)
         self.N, self.E = X.shape[0], H.shape[0]
         self.h = L.hx_create(self.N, _p(X, D), self.E, _p(H, I32), _p(st, U8), prob.E, prob.nu, prob.rho,
                              tf.shape[0], _p(tf, I32), _p(tt, D), vn.shape[0], _p(vn, I32), _p(vm, U8), _p(vv, D),
                              prob.vbc_t0, prob.dt if dt is None else dt, prob.cfl, prob.gamma, _p(fn, D),
-                             _p(body, D), err, 256)
+                             _p(body, D), _p(gc, D), int(flags), err, 256)
         if not self.h:
             raise ValueError("hex oracle rejected the mesh: " + err.value.decode())
         self.S = L.hx_n_edges(self.h)
+        self.S_all = L.hx_n_edges_all(self.h)
         self.step_count = 0
 
     def __del__(self):
@@ -283,10 +294,42 @@ class HexOracle:
     def dt(self):
         return lib().hx_dt(self.h)
 
-    def run(self, nsteps):
-        lib().hx_run(self.h, int(nsteps))
+    def run(self, nsteps, crack_every=0):
+        rc = lib().hx_run(self.h, int(nsteps), int(crack_every))
         self.step_count += int(nsteps)
+        if rc:
+            raise FloatingPointError("hex oracle: non-finite state")
         return self
+
+    @property
+    def dissipated(self):
+        return lib().hx_dissipated(self.h)
+
+    def records(self):
+        n = lib().hx_n_records(self.h)
+        r = Records(np.empty(n, np.int64), np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n), np.empty(n))
+        lib().hx_get_records(self.h, _p(r.step, I64), _p(r.elem, I32), _p(r.cand, I32), _p(r.G, D), _p(r.area, D))
+        return r
+
+    def elements(self):
+        """hex_active [E], tet_active [E,3], tet_nodes [E,3,4] (global; -1 without remainder), tet V [E,3]"""
+        ha = np.empty(self.E, np.uint8); ta = np.empty((self.E, 3), np.uint8)
+        tn = np.empty((self.E, 3, 4), np.int32); tv = np.empty((self.E, 3))
+        lib().hx_get_elements(self.h, _p(ha, U8), _p(ta, U8), _p(tn, I32), _p(tv, D))
+        return dict(hex_active=ha, tet_active=ta, tet_nodes=tn, tet_V=tv)
+
+    def candidates(self, u, e):
+        """G [84], area [84], remainder prism local nodes [84, 6] (-1: none) of hex e for u"""
+        u = _c(u, np.float64); G = np.empty(84); A = np.empty(84); P = np.empty((84, 6), np.int32)
+        lib().hx_candidates(self.h, _p(u, D), int(e), _p(G, D), _p(A, D), _p(P, I32)); return G, A, P
+
+    def force_split(self, e, k):
+        lib().hx_force_split(self.h, int(e), int(k))
+
+    def edge_stress_all(self, u):
+        u = _c(u, np.float64); S = self.S_all
+        s = np.empty((S, 6)); vh = np.empty(S); en = np.empty((S, 2), np.int32)
+        lib().hx_edge_stress_all(self.h, _p(u, D), _p(s, D), _p(vh, D), _p(en, I32)); return s, vh, en
 
     def state(self):
         u = np.empty((self.N, 3)); v = np.empty((self.N, 3)); a = np.empty((self.N, 3)); m = np.empty(self.N)

@@ -443,13 +443,8 @@ static void update_node(orc_sim *s, int64_t k, double t1) {
 static double sgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
 
 
-static void tet_candidates(const orc_sim *s, int64_t e, const double *u, const eig_t *eg /*[6] by local edge*/,
-                           double *G24, double *A24) {
-    double Xn[4][3], un[4][3];
-    for (int a = 0; a < 4; ++a) {
-        int64_t n = s->tet[4 * e + a];
-        for (int c = 0; c < 3; ++c) { Xn[a][c] = s->X[3 * n + c]; un[a][c] = u[3 * n + c]; }
-    }
+static void cand_core(double Xn[4][3], double un[4][3], const eig_t *eg /*[6] by local edge*/, uint32_t flags,
+                      double *G24, double *A24) {
     int H[6];
     for (int l = 0; l < 6; ++l) {
         double du[3], dX[3], w[3];
@@ -494,13 +489,40 @@ static void tet_candidates(const orc_sim *s, int64_t e, const double *u, const e
                     G = (0.5 * (Sg * (Dd[0] + Dd[1]))) / mm;
                     area = sqrt(mm) / 8.0;
                 }
-                if ((s->flags & ORC_F_FRONT_BOTH_STRETCHED) && !(H[local_edge(c, p)] && H[local_edge(c, q)]))
+                if ((flags & ORC_F_FRONT_BOTH_STRETCHED) && !(H[local_edge(c, p)] && H[local_edge(c, q)]))
                     G = 0.0; /* R11 variant: the front is not stretched at both edges */
                 int k = 6 * c + 2 * f + t;
                 G24[k] = G; A24[k] = area;
             }
         }
     }
+}
+
+static void tet_candidates(const orc_sim *s, int64_t e, const double *u, const eig_t *eg /*[6] by local edge*/,
+                           double *G24, double *A24) {
+    double Xn[4][3], un[4][3];
+    for (int a = 0; a < 4; ++a) {
+        int64_t n = s->tet[4 * e + a];
+        for (int c = 0; c < 3; ++c) { Xn[a][c] = s->X[3 * n + c]; un[a][c] = u[3 * n + c]; }
+    }
+    cand_core(Xn, un, eg, s->flags, G24, A24);
+}
+
+/* the 24 candidates of one tet from its node coordinates X12 [4][3], displacements u12 [4][3] and
+ * the stresses s36 [6][6] of its local edges (EP/EQ order); flags: ORC_F_FRONT_BOTH_STRETCHED.
+ * Used by the hexahedral oracle for the tets of a remainder prism (R28). */
+ORC_API void orc_tet_cand_x(const double *X12, const double *u12, const double *s36, uint32_t flags, double *G24,
+                            double *A24) {
+    double Xn[4][3], un[4][3];
+    for (int a = 0; a < 4; ++a)
+        for (int c = 0; c < 3; ++c) { Xn[a][c] = X12[3 * a + c]; un[a][c] = u12[3 * a + c]; }
+    eig_t eg[6];
+    for (int l = 0; l < 6; ++l) {
+        int32_t kk, dg;
+        orc_principal(s36 + 6 * l, eg[l].lam, eg[l].vec, &kk, &dg);
+        eg[l].k1 = kk; eg[l].deg = dg;
+    }
+    cand_core(Xn, un, eg, flags, G24, A24);
 }
 
 /* select: max G, ties -> larger area, then lower k (R14); split iff G > Gc (R10) */
