@@ -89,10 +89,15 @@ typedef struct {
                                  node ids, nodes 0-3 one face counter-clockwise seen from outside...
                                  i.e. a right-handed (xi, eta) order, 4-7 the opposite face in the same
                                  order; element strain = the volume-averaged strain, R23-R26).
-                                 Hexahedral contexts run elastodynamics only: crack patterns III-VI are
-                                 not built (cem_step with crack_every > 0 and cem_crack_update return
-                                 CEM_ESTATE; cem_energy works, with the smoothing-domain volume
-                                 Vhat_s / 12); one GPU (nranks = 1). */
+                                 Hexahedral contexts crack by patterns III-VI (PAPER.md:L478-L540,
+                                 DESIGN.md R28-R29): cem_step with crack_every > 0 evaluates 84
+                                 candidates per active hex (record cand k: III 2f+j, IV 12+4f+2j+t,
+                                 V 36+4f+i, VI 60+4f+i); IV-VI leave a half-hex prism of three tets
+                                 recorded as elements n_tets + 3e + i when they split (tet criterion,
+                                 cand 0..23), so the record arrays need up to 4 n_tets entries and
+                                 tet_state reports the hexes only.  cem_crack_update returns
+                                 CEM_ESTATE; cem_energy uses the smoothing-domain volume sum V/12
+                                 (hex) + V/6 (tet); one GPU (nranks = 1). */
 } cem_mesh_in;
 
 /* Loads (PAPER.md:L191 Dirichlet/Neumann boundaries; L408-L412 external force;
@@ -190,7 +195,7 @@ typedef struct {
     int32_t *rec_cand;        /*   candidate k = 6c + 2f + t (R7) */
     double *rec_G;            /*   energy release rate at the split (J/m^2) */
     double *rec_area;         /*   crack-surface area (m^2) */
-    int64_t rec_capacity;     /* in: size of the host record arrays */
+    int64_t rec_capacity;     /* in: size of the record arrays (n_tets; 4 n_tets for hexahedra) */
     /* scalars (always filled) */
     int64_t step;             /* n */
     double time;              /* n dt */

@@ -249,6 +249,8 @@ class Simulation:
         n, e, s = C.c_int64(), C.c_int64(), C.c_int64()
         _lib.cem_sizes(self._h, C.byref(n), C.byref(e), C.byref(s))
         self.n_nodes, self.n_tets, self.n_edges = n.value, e.value, s.value
+        # split records: one per element; a hexahedral context also records its remainder tets E + 3e + i
+        self.rec_capacity = (4 if npe == 8 else 1) * e.value
 
     @classmethod
     def from_problem(cls, prob, **kw):
@@ -294,7 +296,7 @@ class Simulation:
         out = cem_state_out()
         out.u, out.v, out.a = _ptr(u, D), _ptr(v, D), _ptr(a, D)
         out.tet_state, out.mass = _ptr(st, U8), _ptr(m, D)
-        cap = E if records else 0
+        cap = self.rec_capacity if records else 0
         rs = np.empty(cap, np.int64); re = np.empty(cap, np.int32); rk = np.empty(cap, np.int32)
         rg = np.empty(cap); ra = np.empty(cap)
         out.rec_step, out.rec_elem, out.rec_cand = _ptr(rs, I64), _ptr(re, I32), _ptr(rk, I32)
@@ -333,7 +335,7 @@ class Simulation:
                  a=torch.empty((N, 3), dtype=torch.float64, device=dev),
                  tet_state=torch.empty(E, dtype=torch.uint8, device=dev),
                  mass=torch.empty(N, dtype=torch.float64, device=dev))
-        cap = E if records else 0
+        cap = self.rec_capacity if records else 0
         r = dict(rec_step=torch.empty(cap, dtype=torch.int64, device=dev),
                  rec_elem=torch.empty(cap, dtype=torch.int32, device=dev),
                  rec_cand=torch.empty(cap, dtype=torch.int32, device=dev),

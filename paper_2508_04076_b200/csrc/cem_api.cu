@@ -1108,7 +1108,8 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
 
 // ---------------------------------------------------------------- hexahedral contexts (N3)
 struct HexOffs {
-    size_t hgeo, hconn, heedge, htau, e_off, e_inc, vhat, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
+    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, htgeo, httau, gc, X, rec_step, rec_elem,
+        rec_cand, rec_G, rec_area, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
         srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, epart, total;
 };
 HexOffs hex_layout(const HexHost &h) {
@@ -1121,7 +1122,19 @@ HexOffs hex_layout(const HexHost &h) {
     o.htau = L.take<double>(6 * E);
     o.e_off = L.take<int32_t>(S + 1);
     o.e_inc = L.take<int32_t>((int64_t)h.edge_inc.size());
-    o.vhat = L.take<double>(S);
+    o.hpair = L.take<int32_t>(28 * E);
+    o.hrem = L.take<int8_t>(E);
+    o.htact = L.take<uint8_t>(E);
+    o.htloc = L.take<uint8_t>(12 * E);
+    o.htgeo = L.take<double>(39 * E);
+    o.httau = L.take<double>(18 * E);
+    o.gc = L.take<double>(E);
+    o.X = L.take<double4>(N);
+    o.rec_step = L.take<int64_t>(4 * E);
+    o.rec_elem = L.take<int32_t>(4 * E);
+    o.rec_cand = L.take<int32_t>(4 * E);
+    o.rec_G = L.take<double>(4 * E);
+    o.rec_area = L.take<double>(4 * E);
     o.nodeE = L.take<int32_t>((int64_t)h.nodeE.size());
     o.fext = L.take<double4>(N);
     o.nflag = L.take<uint8_t>(N);
@@ -1135,7 +1148,7 @@ HexOffs hex_layout(const HexHost &h) {
     o.a = L.take<double4>(N);
     o.srec = L.take<double>(4 * S);
     o.srec2 = L.take<double>(2 * S);
-    o.fe = L.take<double>(3 * (8 * E + 1));
+    o.fe = L.take<double>(3 * (32 * E + 1));
     o.ctr = L.take<int32_t>(32);
     o.rprev = L.take<double>(h.any_dirichlet ? 3 * N : 1);
     o.wr_dof = L.take<double>(h.any_dirichlet ? 3 * N : 1);
@@ -1217,7 +1230,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     ctx->h.E = E;
     ctx->h.S = S;
     ctx->h.dt = h.dt;
-    ctx->h.gc.assign(E, INFINITY);
+    ctx->h.gc = h.gc;  // [4E]: records of remainder tets E + 3e + i carry their parent's Gc
     ctx->p.node_new2old.resize(N);
     std::iota(ctx->p.node_new2old.begin(), ctx->p.node_new2old.end(), 0);
     ctx->p.tet_new2old.resize(E);
@@ -1238,7 +1251,20 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.htau = at<double>(b, o.htau);
     d.e_off = at<int32_t>(b, o.e_off);
     d.e_inc = at<int32_t>(b, o.e_inc);
-    d.vhat = at<double>(b, o.vhat);
+    d.vhat = nullptr;  // Vhat summed per step by stage B (splits change it)
+    d.hpair = at<int32_t>(b, o.hpair);
+    d.hrem = at<int8_t>(b, o.hrem);
+    d.htact = at<uint8_t>(b, o.htact);
+    d.htloc = at<uint8_t>(b, o.htloc);
+    d.htgeo = at<double>(b, o.htgeo);
+    d.httau = at<double>(b, o.httau);
+    d.gc = at<double>(b, o.gc);
+    d.X = at<double4>(b, o.X);
+    d.rec_step = at<int64_t>(b, o.rec_step);
+    d.rec_elem = at<int32_t>(b, o.rec_elem);
+    d.rec_cand = at<int32_t>(b, o.rec_cand);
+    d.rec_G = at<double>(b, o.rec_G);
+    d.rec_area = at<double>(b, o.rec_area);
     d.nodeE = at<int32_t>(b, o.nodeE);
     d.wn = h.wn;
     d.zslot = h.zslot;
@@ -1255,7 +1281,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.srec = at<double>(b, o.srec);
     d.srec2 = at<double>(b, o.srec2);
     d.fe = at<double>(b, o.fe);
-    d.part = nullptr;  // hexahedra: force slots (8 per hex)
+    d.part = nullptr;  // hexahedra: force slots (4 per hex incidence: the hex, its 3 remainder tets)
     d.ctr = at<int32_t>(b, o.ctr);
     d.rprev = h.any_dirichlet ? at<double>(b, o.rprev) : nullptr;
     d.wr_dof = at<double>(b, o.wr_dof);
@@ -1328,7 +1354,19 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     CUDA_TRY(put(o.heedge, h.eedge.data(), 4 * h.eedge.size()));
     CUDA_TRY(put(o.e_off, h.edge_off.data(), 4 * h.edge_off.size()));
     CUDA_TRY(put(o.e_inc, h.edge_inc.data(), 4 * h.edge_inc.size()));
-    CUDA_TRY(put(o.vhat, h.vhat.data(), 8 * h.vhat.size()));
+    CUDA_TRY(put(o.hpair, h.pair.data(), 4 * h.pair.size()));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hrem), 0xff, E, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htact), 0, E, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htloc), 0, 12 * E, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htgeo), 0, 8 * 39 * E, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.httau), 0, 8 * 18 * E, s));
+    CUDA_TRY(put(o.gc, h.gc.data(), 8 * E));
+    {
+        std::vector<double4> x4(N);
+        for (int64_t n = 0; n < N; ++n) x4[n] = make_double4(mesh->X[3 * n], mesh->X[3 * n + 1], mesh->X[3 * n + 2], 0.0);
+        CUDA_TRY(put(o.X, x4.data(), sizeof(double4) * N));
+        CUDA_TRY(cudaStreamSynchronize(s));  // x4 leaves scope
+    }
     CUDA_TRY(put(o.nodeE, h.nodeE.data(), 4 * h.nodeE.size()));
     CUDA_TRY(put(o.fext, f4.data(), sizeof(double4) * N));
     CUDA_TRY(put(o.nflag, h.nflag.data(), N));
@@ -1346,7 +1384,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     CUDA_TRY(put(o.a, a4.data(), sizeof(double4) * N));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec), 0, 8 * 4 * S, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.srec2), 0, 8 * 2 * S, s));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, 8 * 3 * (8 * E + 1), s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.fe), 0, 8 * 3 * (32 * E + 1), s));
     CUDA_TRY(put(o.ctr, ctr, sizeof ctr));
     CUDA_TRY(put(o.node_orig, ident.data(), 4 * N));
     CUDA_TRY(put(o.tet_orig, ident.data(), 4 * E));
@@ -1709,13 +1747,12 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     }
     if (nsteps == 0) return CEM_OK;
     if (crack_every < 0) crack_every = 0;
-    if (ctx->hexa && crack_every > 0) {
-        ctx->err = "hexahedral contexts run elastodynamics only (crack patterns III-VI are not built): crack_every must be 0";
-        return CEM_ESTATE;
-    }
     StreamFence fence(ctx);
-    if (ctx->hexa) {
-        for (int64_t i = 0; i < nsteps; ++i) ctx->launches += launch_hex_step(ctx->d, ctx->step + i, ctx->stream);
+    if (ctx->hexa) {  // crack steps (R16): the criterion of patterns III-VI between stages C and D
+        for (int64_t i = 0; i < nsteps; ++i) {
+            const int64_t s1 = ctx->step + i + 1;
+            ctx->launches += launch_hex_step(ctx->d, ctx->step + i, ctx->stream, crack_every > 0 && s1 % crack_every == 0);
+        }
         CUDA_TRY(cudaGetLastError());
         ctx->step += nsteps;
         return CEM_OK;
@@ -1884,7 +1921,7 @@ cem_status cem_crack_update(cem_ctx *ctx, int64_t *n_split_out) {
         return CEM_ESTATE;
     }
     if (ctx->hexa) {
-        ctx->err = "cem_crack_update: not available for hexahedral contexts (patterns III-VI are not built)";
+        ctx->err = "cem_crack_update: not available for hexahedral contexts (their criterion runs inside cem_step)";
         return CEM_ESTATE;
     }
     StreamFence fence(ctx);

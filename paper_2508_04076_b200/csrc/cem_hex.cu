@@ -1,11 +1,16 @@
 // cem_hex.cu -- sm_100a kernels of the ES-H-FEM step on trilinear hexahedra (
 // PAPER.md:L311-L338 eq:hex_strain_discretization, L368-L390 eq:hex_fint_discretization).
 // Same bitwise contract as the tet path (--fmad=false, sequential sums in the order of
-// DESIGN.md §5 for hexes); no criterion (crack patterns III-VI are not built).
-//   A  tau_e = V_e eps_e, eps from the mean gradients (R23), a = 0..7      -> [6][E] planes
-//   B  sigma_s = D (sum tau_e) / Vhat_s over the active incident hexes (ascending id)
-//   C  S_e = sum_{l=0..11} sigma_{s(e,l)}; f_{e,a} = (V_e/12) B_a^T S_e (R26)  -> slots 8e + a
-//   D  the tet path's node update (force-slot gather, Newmark, BC, predictor)
+// DESIGN.md §5 for hexes).  Crack patterns III-VI (R28): a split hex may leave a remainder of three
+// tets (E + 3e + i) over its own nodes; their data sit with the parent hex.
+//   A  tau_e = V_e eps_e, eps from the mean gradients (R23), a = 0..7      -> [6][E] planes;
+//      remainder tets tau = V_t eps_t over their 4 nodes                    -> [E][3][6]
+//   B  sigma_s = D (sum tau) / (sum V) over the active elements of edge s (hex e, then its
+//      remainder tets; R29), edges [0, S_h) hex edges, [S_h, S) diagonals
+//   C  S_e = sum_{l=0..11} sigma_{s(e,l)}; f_{e,a} = (V_e/12) B_a^T S_e (R26) -> slot 4(8e + a);
+//      remainder tet i: (V_t/6) B^T sum of its 6 edges -> slot 4(8e + a) + 1 + i of its nodes a
+//   crit (crack steps, cem_kernels.cu k_hexcrit): patterns III-VI / the tet criterion, split
+//   D  the tet path's node update (force-slot gather, Newmark, BC, mass of split nodes, predictor)
 #include <cstdint>
 
 #include "cem_internal.h"
@@ -16,6 +21,23 @@ namespace {
 
 __device__ __forceinline__ void pdl_trigger_h() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_h() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// local node pair (a, b) -> 0..27 and the hex edge of a pair (-1: a face or body diagonal)
+__constant__ int8_t c_hpair[8][8] = {{-1, 0, 1, 2, 3, 4, 5, 6},     {0, -1, 7, 8, 9, 10, 11, 12},
+                                     {1, 7, -1, 13, 14, 15, 16, 17}, {2, 8, 13, -1, 18, 19, 20, 21},
+                                     {3, 9, 14, 18, -1, 22, 23, 24}, {4, 10, 15, 19, 22, -1, 25, 26},
+                                     {5, 11, 16, 20, 23, 25, -1, 27}, {6, 12, 17, 21, 24, 26, 27, -1}};
+__constant__ int8_t c_hedge_of_pair[28] = {0,  -1, 3,  8, -1, -1, -1, 1, -1, -1, 9,  -1, -1, 2,
+                                           -1, -1, 10, -1, -1, -1, -1, 11, 4, -1, 7, 5, -1, 6};
+__constant__ int8_t c_tp[6] = {0, 0, 0, 1, 1, 2};
+__constant__ int8_t c_tq[6] = {1, 2, 3, 2, 3, 3};
+
+__device__ __forceinline__ bool tet_has_pair(const uint8_t *t, int pj) {
+#pragma unroll
+    for (int l = 0; l < 6; ++l)
+        if (c_hpair[t[c_tp[l]]][t[c_tq[l]]] == pj) return true;
+    return false;
+}
 
 __global__ void __launch_bounds__(256) k_hexA(Dev d, int64_t s) {
     pdl_trigger_h();
@@ -55,27 +77,77 @@ __global__ void __launch_bounds__(256) k_hexA(Dev d, int64_t s) {
     t[3 * E + e] = act ? V * gxy : 0.0;
     t[4 * E + e] = act ? V * gyz : 0.0;
     t[5 * E + e] = act ? V * gxz : 0.0;
+    if (__ldcg(d.hrem + e) < 0) return;
+    const uint8_t ta = __ldcg(d.htact + e);
+    for (int i = 0; i < 3; ++i) {
+        double *tt = d.httau + 18 * e + 6 * i;
+        if (!(ta >> i & 1)) continue;
+        const uint8_t *tl = d.htloc + 12 * e + 4 * i;
+        const double *tg = d.htgeo + 39 * e + 13 * i;
+        double x = 0.0, y = 0.0, z = 0.0, xy = 0.0, yz = 0.0, xz = 0.0;
+        for (int a = 0; a < 4; ++a) {
+            const double *ua = reinterpret_cast<const double *>(u + n[tl[a]]);
+            const double ux = __ldcg(ua), uy = __ldcg(ua + 1), uz = __ldcg(ua + 2);
+            const double g0 = tg[1 + 3 * a], g1 = tg[2 + 3 * a], g2 = tg[3 + 3 * a];
+            x = x + g0 * ux;
+            y = y + g1 * uy;
+            z = z + g2 * uz;
+            xy = xy + (g1 * ux + g0 * uy);
+            yz = yz + (g2 * uy + g1 * uz);
+            xz = xz + (g2 * ux + g0 * uz);
+        }
+        const double Vt = tg[0];
+        tt[0] = Vt * x;
+        tt[1] = Vt * y;
+        tt[2] = Vt * z;
+        tt[3] = Vt * xy;
+        tt[4] = Vt * yz;
+        tt[5] = Vt * xz;
+    }
+}
+
+// the active elements of edge k in element order (hex e, then its remainder tets i): sum V, sum tau
+// and (energy) the smoothing-domain volume sum V/n_e (R29)
+__device__ __forceinline__ double edge_gather(const Dev &d, int64_t k, double *T, double *W) {
+    const int64_t E = d.E;
+    const int32_t j0 = __ldg(d.e_off + k), j1 = __ldg(d.e_off + k + 1);
+    double Vh = 0.0, w = 0.0;
+    for (int32_t j = j0; j < j1; ++j) {
+        const int32_t ent = __ldg(d.e_inc + j);
+        const int64_t e = ent >> 5;
+        const int pj = ent & 31;
+        if (__ldcg(d.state + e)) {
+            if (c_hedge_of_pair[pj] < 0) continue;
+            const double V = __ldg(d.hgeo + e);
+            Vh = Vh + V;
+            if (W) w = w + V / 12.0;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.htau + c * E + e);
+            continue;
+        }
+        if (__ldcg(d.hrem + e) < 0) continue;
+        const uint8_t ta = __ldcg(d.htact + e);
+        for (int i = 0; i < 3; ++i) {
+            if (!(ta >> i & 1) || !tet_has_pair(d.htloc + 12 * e + 4 * i, pj)) continue;
+            const double V = __ldcg(d.htgeo + 39 * e + 13 * i);
+            Vh = Vh + V;
+            if (W) w = w + V / 6.0;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.httau + 18 * e + 6 * i + c);
+        }
+    }
+    if (W) *W = w;
+    return Vh;
 }
 
 __global__ void __launch_bounds__(256) k_hexB(Dev d, int64_t s) {
     pdl_trigger_h();
-    const int64_t S = d.S, E = d.E;
+    const int64_t S = d.S;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= S) return;
-    const int32_t j0 = __ldg(d.e_off + k), j1 = __ldg(d.e_off + k + 1);
-    const double Vh = __ldg(d.vhat + k);
     pdl_wait_h();  // tau from stage A
-    double T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0, T4 = 0.0, T5 = 0.0;
-    for (int32_t j = j0; j < j1; ++j) {  // ascending hex id; inactive hexes hold exact zeros
-        const int64_t e = __ldg(d.e_inc + j);
-        if (!__ldcg(d.state + e)) continue;
-        T0 = T0 + __ldcg(d.htau + e);
-        T1 = T1 + __ldcg(d.htau + E + e);
-        T2 = T2 + __ldcg(d.htau + 2 * E + e);
-        T3 = T3 + __ldcg(d.htau + 3 * E + e);
-        T4 = T4 + __ldcg(d.htau + 4 * E + e);
-        T5 = T5 + __ldcg(d.htau + 5 * E + e);
-    }
+    double T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const double Vh = edge_gather(d, k, T, nullptr);
     double4 *o4 = reinterpret_cast<double4 *>(d.srec) + k;
     double2 *o2 = reinterpret_cast<double2 *>(d.srec2) + k;
     if (Vh == 0.0) {
@@ -84,10 +156,23 @@ __global__ void __launch_bounds__(256) k_hexB(Dev d, int64_t s) {
         return;
     }
     const double inv = 1.0 / Vh;
-    const double e11 = T0 * inv, e22 = T1 * inv, e33 = T2 * inv, g12 = T3 * inv, g23 = T4 * inv, g13 = T5 * inv;
+    const double e11 = T[0] * inv, e22 = T[1] * inv, e33 = T[2] * inv, g12 = T[3] * inv, g23 = T[4] * inv,
+                 g13 = T[5] * inv;
     *o4 = make_double4(d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33),
                        d.l2m * e33 + d.lam * (e11 + e22), d.mu * g12);
     *o2 = make_double2(d.mu * g23, d.mu * g13);
+}
+
+__device__ __forceinline__ void sigma_sum(const Dev &d, int32_t sid, double *S) {
+    const double2 a0 = __ldcg(reinterpret_cast<const double2 *>(d.srec) + 2 * (int64_t)sid);
+    const double2 a1 = __ldcg(reinterpret_cast<const double2 *>(d.srec) + 2 * (int64_t)sid + 1);
+    const double2 b = __ldcg(reinterpret_cast<const double2 *>(d.srec2) + sid);
+    S[0] = S[0] + a0.x;
+    S[1] = S[1] + a0.y;
+    S[2] = S[2] + a1.x;
+    S[3] = S[3] + a1.y;
+    S[4] = S[4] + b.x;
+    S[5] = S[5] + b.y;
 }
 
 __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
@@ -100,34 +185,46 @@ __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
     for (int l = 0; l < 12; ++l) sid[l] = __ldg(d.heedge + l * E + e);
     const double V = __ldg(d.hgeo + e);
     pdl_wait_h();  // sigma from stage B
-    double *fo = d.fe + 24 * e;  // slots 8e + a, 3 doubles each
+    double *fo = d.fe + 96 * e;  // slot 4(8e + a) + sub at fo + 12a + 3 sub
     if (!__ldcg(d.state + e)) {
 #pragma unroll
-        for (int i = 0; i < 24; ++i) fo[i] = 0.0;
-        return;
-    }
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0;
+        for (int a = 0; a < 8; ++a) fo[12 * a] = fo[12 * a + 1] = fo[12 * a + 2] = 0.0;
+    } else {
+        double S[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int l = 0; l < 12; ++l) {
-        const double2 a0 = __ldcg(reinterpret_cast<const double2 *>(d.srec) + 2 * (int64_t)sid[l]);
-        const double2 a1 = __ldcg(reinterpret_cast<const double2 *>(d.srec) + 2 * (int64_t)sid[l] + 1);
-        const double4 a = make_double4(a0.x, a0.y, a1.x, a1.y);
-        const double2 b = __ldcg(reinterpret_cast<const double2 *>(d.srec2) + sid[l]);
-        S0 = S0 + a.x;
-        S1 = S1 + a.y;
-        S2 = S2 + a.z;
-        S3 = S3 + a.w;
-        S4 = S4 + b.x;
-        S5 = S5 + b.y;
-    }
-    const double c = V / 12.0;  // R26: the smoothing-domain share of each of the 12 edges
+        for (int l = 0; l < 12; ++l) sigma_sum(d, sid[l], S);
+        const double c = V / 12.0;  // R26: the smoothing-domain share of each of the 12 edges
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        const double gx = __ldg(d.hgeo + (1 + 3 * a) * E + e), gy = __ldg(d.hgeo + (2 + 3 * a) * E + e),
-                     gz = __ldg(d.hgeo + (3 + 3 * a) * E + e);
-        fo[3 * a] = c * ((gx * S0 + gy * S3) + gz * S5);
-        fo[3 * a + 1] = c * ((gy * S1 + gx * S3) + gz * S4);
-        fo[3 * a + 2] = c * ((gz * S2 + gy * S4) + gx * S5);
+        for (int a = 0; a < 8; ++a) {
+            const double gx = __ldg(d.hgeo + (1 + 3 * a) * E + e), gy = __ldg(d.hgeo + (2 + 3 * a) * E + e),
+                         gz = __ldg(d.hgeo + (3 + 3 * a) * E + e);
+            fo[12 * a] = c * ((gx * S[0] + gy * S[3]) + gz * S[5]);
+            fo[12 * a + 1] = c * ((gy * S[1] + gx * S[3]) + gz * S[4]);
+            fo[12 * a + 2] = c * ((gz * S[2] + gy * S[4]) + gx * S[5]);
+        }
+    }
+    if (__ldcg(d.hrem + e) < 0) return;
+    const uint8_t ta = __ldcg(d.htact + e);
+    for (int i = 0; i < 3; ++i) {
+        const uint8_t *tl = d.htloc + 12 * e + 4 * i;
+        if (!(ta >> i & 1)) {  // a split tet contributes nothing from now on
+            for (int b = 0; b < 4; ++b) {
+                double *f = fo + 12 * tl[b] + 3 * (1 + i);
+                f[0] = f[1] = f[2] = 0.0;
+            }
+            continue;
+        }
+        double S[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int l = 0; l < 6; ++l) sigma_sum(d, __ldg(d.hpair + (int64_t)c_hpair[tl[c_tp[l]]][tl[c_tq[l]]] * E + e), S);
+        const double *tg = d.htgeo + 39 * e + 13 * i;
+        const double c = tg[0] / 6.0;  // R5: V_t / 6 per tet edge
+        for (int b = 0; b < 4; ++b) {
+            const double gx = tg[1 + 3 * b], gy = tg[2 + 3 * b], gz = tg[3 + 3 * b];
+            double *f = fo + 12 * tl[b] + 3 * (1 + i);
+            f[0] = c * ((gx * S[0] + gy * S[3]) + gz * S[5]);
+            f[1] = c * ((gy * S[1] + gx * S[3]) + gz * S[4]);
+            f[2] = c * ((gz * S[2] + gy * S[4]) + gx * S[5]);
+        }
     }
 }
 
@@ -136,25 +233,19 @@ __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
 // fixed shuffle tree and the warps in order
 __global__ void __launch_bounds__(256) k_hex_energy_edges(Dev d, double *part) {
     __shared__ double red[8];
-    const int64_t S = d.S, E = d.E;
+    const int64_t S = d.S;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double U = 0.0;
     if (k < S) {
-        const double Vh = __ldg(d.vhat + k);
+        double T[6] = {0, 0, 0, 0, 0, 0}, W = 0.0;
+        const double Vh = edge_gather(d, k, T, &W);
         if (Vh != 0.0) {
-            double T[6] = {0, 0, 0, 0, 0, 0};
-            for (int32_t j = __ldg(d.e_off + k); j < __ldg(d.e_off + k + 1); ++j) {
-                const int64_t e = __ldg(d.e_inc + j);
-                if (!__ldcg(d.state + e)) continue;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.htau + c * E + e);
-            }
             const double inv = 1.0 / Vh;
             const double e11 = T[0] * inv, e22 = T[1] * inv, e33 = T[2] * inv, g12 = T[3] * inv, g23 = T[4] * inv,
                          g13 = T[5] * inv;
             const double tr = e11 + e22 + e33;
             const double ee = e11 * e11 + e22 * e22 + e33 * e33 + 0.5 * (g12 * g12 + g23 * g23 + g13 * g13);
-            U = (0.5 * d.lam * tr * tr + d.mu * ee) * (Vh / 12.0);
+            U = (0.5 * d.lam * tr * tr + d.mu * ee) * W;
         }
     }
 #pragma unroll
@@ -191,13 +282,14 @@ void launch_hex_energy(const Dev &d, int64_t n, double *part_edges, double *part
     launch_energy_nodes(d, n, part_nodes, st);
 }
 
-int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st) {
+int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack) {
     const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)((d.S + 255) / 256);
     launch_pdl_h(k_hexA, ge, st, d, s);
     launch_pdl_h(k_hexB, gs, st, d, s);
     launch_pdl_h(k_hexC, ge, st, d, s);
+    if (crack) launch_hex_crit(d, s, st);
     launch_node_update(d, s, st);
-    return 4;
+    return crack ? 5 : 4;
 }
 
 }  // namespace cem

@@ -98,8 +98,8 @@ cem_status build_hex_host(const cem_mesh_in *m, const cem_material *mat, const c
         return CEM_EINVAL;
     }
     const int64_t N = m->n_nodes, E = m->n_tets;
-    if (E > ((int64_t)1 << 31) / 24 - 64 || N >= ((int64_t)1 << 31)) {
-        err = "hex mesh too large for one context (E < 89M)";
+    if (E > ((int64_t)1 << 31) / 96 - 64 || N >= ((int64_t)1 << 31)) {
+        err = "hex mesh too large for one context (E < 22M)";
         return CEM_EINVAL;
     }
     h.N = N;
@@ -145,30 +145,56 @@ cem_status build_hex_host(const cem_mesh_in *m, const cem_material *mat, const c
         err = "hex " + std::to_string(bad) + ": non-positive Jacobian at a corner";
         return CEM_ENEGVOL;
     }
-    // ---------------------------------------------------------------- 12-edge topology
-    // unique (min, max) node pairs sorted; local edge order: bottom ring, top ring, verticals
-    std::vector<std::pair<uint64_t, int64_t>> k(12 * E);
+    // ---------------------------------------------------------------- edges (R28)
+    // every local node pair of every hex (28, pair index kHexPair) as a (min, max) key: the pairs that
+    // are hex edges of some hex first (the mesh's smoothing domains, edges [0, S_h)), then the face
+    // and body diagonals only remainder tets use; each group sorted by key.  Incidence entries
+    // (e << 5) | pair in ascending hex id.
+    std::vector<std::pair<uint64_t, int64_t>> k(28 * E);
     for (int64_t e = 0; e < E; ++e)
-        for (int l = 0; l < 12; ++l) {
-            uint64_t i = (uint32_t)h.hex[8 * e + kHexEdgeP[l]], j = (uint32_t)h.hex[8 * e + kHexEdgeQ[l]];
-            k[12 * e + l] = {std::min(i, j) << 32 | std::max(i, j), 12 * e + l};
-        }
+        for (int a = 0; a < 8; ++a)
+            for (int b = a + 1; b < 8; ++b) {
+                uint64_t i = (uint32_t)h.hex[8 * e + a], j = (uint32_t)h.hex[8 * e + b];
+                const uint64_t key = std::min(i, j) << 32 | std::max(i, j);
+                const int pj = kHexPair[a][b];
+                k[28 * e + pj] = {key | (kHexEdgeOfPair[pj] >= 0 ? 0 : (uint64_t)1 << 63), 28 * e + pj};
+            }
+    {  // a pair that is a hex edge anywhere is a hex edge everywhere (conforming meshes: never both)
+        std::vector<uint64_t> he;
+        he.reserve(12 * E);
+        for (auto &x : k)
+            if (!(x.first >> 63)) he.push_back(x.first);
+        std::sort(he.begin(), he.end());
+        for (auto &x : k)
+            if (x.first >> 63 && std::binary_search(he.begin(), he.end(), x.first & ~((uint64_t)1 << 63)))
+                x.first &= ~((uint64_t)1 << 63);
+    }
     std::sort(k.begin(), k.end());
+    h.pair.resize(28 * E);
     h.eedge.resize(12 * E);
     h.edge_off.clear();
     h.edge_inc.clear();
-    int64_t S = 0;
+    int64_t S = 0, S_h = 0;
     for (size_t i = 0; i < k.size(); ++i) {
         if (i == 0 || k[i].first != k[i - 1].first) {
             h.edge_off.push_back((int32_t)h.edge_inc.size());
             ++S;
+            if (!(k[i].first >> 63)) S_h = S;
         }
-        const int64_t e = k[i].second / 12, l = k[i].second % 12;
-        h.eedge[(size_t)l * E + e] = (int32_t)(S - 1);  // [12][E]
-        h.edge_inc.push_back((int32_t)e);               // ascending hex id within an edge (pairs sorted)
+        const int64_t e = k[i].second / 28, pj = k[i].second % 28;
+        h.pair[(size_t)pj * E + e] = (int32_t)(S - 1);             // [28][E]
+        h.edge_inc.push_back((int32_t)((e << 5) | pj));            // ascending hex id within an edge
     }
     h.edge_off.push_back((int32_t)h.edge_inc.size());
+    for (int64_t e = 0; e < E; ++e)
+        for (int l = 0; l < 12; ++l) h.eedge[(size_t)l * E + e] = h.pair[(size_t)kHexPair[kHexEdgeP[l]][kHexEdgeQ[l]] * E + e];
     h.S = S;
+    h.S_h = S_h;
+    h.gc.resize(4 * E);  // hexes, then the remainder tets E + 3e + i (the parent's Gc)
+    for (int64_t e = 0; e < E; ++e) {
+        h.gc[e] = m->tet_gc ? m->tet_gc[e] : mat->Gc;
+        for (int i = 0; i < 3; ++i) h.gc[E + 3 * e + i] = h.gc[e];
+    }
     // node incidences 8e + a in ascending e
     h.node_off.assign(N + 1, 0);
     for (int64_t i = 0; i < 8 * E; ++i) h.node_off[h.hex[i] + 1]++;
@@ -193,13 +219,6 @@ cem_status build_hex_host(const cem_mesh_in *m, const cem_material *mat, const c
             if (h.state[e]) acc = acc + (h.rho * h.V[e]) / 8.0;
         }
         h.mass[n] = acc;
-    }
-    h.vhat.assign(S, 0.0);  // sum of V over the active incident hexes (ascending), fixed: no splits
-    for (int64_t s = 0; s < S; ++s) {
-        double acc = 0.0;
-        for (int32_t j = h.edge_off[s]; j < h.edge_off[s + 1]; ++j)
-            if (h.state[h.edge_inc[j]]) acc = acc + h.V[h.edge_inc[j]];
-        h.vhat[s] = acc;
     }
     // ---------------------------------------------------------------- external force, Dirichlet
     h.fext.assign(3 * N, 0.0);
@@ -292,14 +311,17 @@ cem_status build_hex_host(const cem_mesh_in *m, const cem_material *mat, const c
         dt = (cfl * hmin) / cd;
     }
     h.dt = dt;
-    // node -> force-slot ELL (slot 8e + a, ascending e), padded with the zero slot 8E
+    // node -> force-slot ELL: incidence (e, a) owns slots 4 (8e + a) + sub, sub 0 the hex's force, sub 1 + i
+    // remainder tet i's (zero while unused); ascending e, padded with the zero slot 32E
     int mx = 1;
     for (int64_t n = 0; n < N; ++n) mx = std::max(mx, h.node_off[n + 1] - h.node_off[n]);
-    h.wn = (mx + 7) / 8 * 8;
-    h.zslot = (int32_t)(8 * E);
+    h.wn = (4 * mx + 7) / 8 * 8;
+    h.zslot = (int32_t)(32 * E);
     h.nodeE.assign((size_t)N * h.wn, h.zslot);
     for (int64_t n = 0; n < N; ++n)
-        for (int32_t j = h.node_off[n]; j < h.node_off[n + 1]; ++j) h.nodeE[(size_t)n * h.wn + (j - h.node_off[n])] = h.node_ent[j];
+        for (int32_t j = h.node_off[n]; j < h.node_off[n + 1]; ++j)
+            for (int sub = 0; sub < 4; ++sub)
+                h.nodeE[(size_t)n * h.wn + 4 * (j - h.node_off[n]) + sub] = 4 * h.node_ent[j] + sub;
     return CEM_OK;
 }
 

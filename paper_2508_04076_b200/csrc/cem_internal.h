@@ -110,8 +110,32 @@ cem_status build_host_mesh(const cem_mesh_in *m, const cem_material *mat, const 
 // local edges of a trilinear hex (p < q): bottom ring, top ring, verticals
 constexpr int kHexEdgeP[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 2, 3};
 constexpr int kHexEdgeQ[12] = {1, 2, 3, 3, 5, 6, 7, 7, 4, 5, 6, 7};
+// local node pair (a, b) -> 0..27 (lexicographic over a < b), and the hex edge of a pair (-1: diagonal)
+constexpr int kHexPairOf(int a, int b) {
+    return a < b ? 7 * a - a * (a - 1) / 2 + (b - a - 1) : 7 * b - b * (b - 1) / 2 + (a - b - 1);
+}
+struct HexPairTab {
+    int p[8][8];
+    constexpr HexPairTab() : p() {
+        for (int a = 0; a < 8; ++a)
+            for (int b = 0; b < 8; ++b) p[a][b] = a == b ? -1 : kHexPairOf(a, b);
+    }
+    constexpr const int *operator[](int a) const { return p[a]; }
+};
+constexpr HexPairTab kHexPair{};
+struct HexEdgeOfPairTab {
+    int v[28];
+    constexpr HexEdgeOfPairTab() : v() {
+        for (int j = 0; j < 28; ++j) v[j] = -1;
+        for (int l = 0; l < 12; ++l) v[kHexPairOf(kHexEdgeP[l], kHexEdgeQ[l])] = l;
+    }
+    constexpr int operator[](int j) const { return v[j]; }
+};
+constexpr HexEdgeOfPairTab kHexEdgeOfPair{};
 struct HexHost {
-    int64_t N = 0, E = 0, S = 0;
+    int64_t N = 0, E = 0, S = 0, S_h = 0;
+    std::vector<int32_t> pair;        // [28][E] edge of the local node pair (R28)
+    std::vector<double> gc;           // [4E] hexes, then remainder tets E + 3e + i
     std::vector<int32_t> hex;         // [E][8]
     std::vector<uint8_t> state;       // [E]
     std::vector<double> V, grad;      // [E], [E][8][3] mean gradients (R23)
@@ -119,7 +143,7 @@ struct HexHost {
     std::vector<int32_t> edge_off, edge_inc, node_off, node_ent;
     std::vector<double> vhat, mass, fext, dir_v0;
     std::vector<uint8_t> nflag;
-    std::vector<int32_t> nodeE;       // [N][wn] slot 8e + a, padded with zslot
+    std::vector<int32_t> nodeE;       // [N][wn] slots 4 (8e + a) + sub, padded with zslot
     int wn = 8;
     int32_t zslot = 0;
     double lam = 0, mu = 0, l2m = 0, rho = 0, dt = 0, gamma = 0.5, t0 = 0;
@@ -301,6 +325,13 @@ struct Dev {
     const double *hgeo;
     const int32_t *hconn, *heedge;
     double *htau;
+    // hex crack patterns III-VI (R28): [28][E] edge of each local node pair; per hex the remainder
+    // (candidate k, -1 none), its tets' activity bits, local nodes [E][12], geometry [E][3][13]
+    // (V, grad[4][3]) and strain [E][3][6]
+    const int32_t *hpair;
+    int8_t *hrem;
+    uint8_t *htact, *htloc;
+    double *htgeo, *httau;
     const int32_t *wncons;     // [2][wmax] consumers of each AB / C block (L2 discard of consumed intermediates)
     int32_t *wcons_done;       // [2][wmax] consumers finished with the block this step
     int wdiscard;              // 1: the last consumer discards a producer block's sigma / force-slot lines
@@ -337,7 +368,10 @@ void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nod
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 // cem_hex.cu: one explicit step of a hexahedral context (4 kernels, PDL-chained; stage D is the
 // tet path's node update); returns the kernels launched
-int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st);
+int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack = false);
+// hex criterion (patterns III-VI, remainder tets: the tet criterion) and split pass of step s
+// (cem_kernels.cu), PDL-chained between stage C and stage D
+void launch_hex_crit(const Dev &d, int64_t s, cudaStream_t st);
 // energy ledger of a hexahedral context at step n: strain energy per edge block (U = sum_s
 // psi(eps~_s) Vhat_s / 12, R26) into part_edges[ceil(S/256)], node terms as the tet ledger
 void launch_hex_energy(const Dev &d, int64_t n, double *part_edges, double *part_nodes, cudaStream_t st);

@@ -195,6 +195,33 @@ __device__ __forceinline__ double node_mass4(const Dev &d, int64_t k, int c) {
     return acc;
 }
 
+// lumped mass of node k of a hexahedral context (R24, R29; the hex oracle's node_mass): incidences
+// (e, a) ascending, the hex's rho V / 8 or its active remainder tets' rho V_t / 4
+__device__ __noinline__ double hex_node_mass(const Dev *__restrict__ dp, int64_t k) {
+    const Dev &d = *dp;
+    const int32_t *row = d.nodeE + k * d.wn;
+    double acc = 0.0;
+    for (int j = 0; j < d.wn; j += 4) {
+        const int32_t sl = __ldg(row + j);
+        if (sl == d.zslot) break;
+        const int64_t e = (sl >> 2) >> 3;
+        const int a = (sl >> 2) & 7;
+        if (__ldcg(d.state + e)) {
+            acc = acc + (d.rho * __ldg(d.hgeo + e)) / 8.0;
+            continue;
+        }
+        if (__ldcg(d.hrem + e) < 0) continue;
+        const uint8_t ta = __ldcg(d.htact + e);
+        for (int i = 0; i < 3; ++i) {
+            if (!(ta >> i & 1)) continue;
+            const uint8_t *tl = d.htloc + 12 * e + 4 * i;
+            if (tl[0] == a || tl[1] == a || tl[2] == a || tl[3] == a)
+                acc = acc + (d.rho * __ldcg(d.htgeo + 39 * e + 13 * i)) / 4.0;
+        }
+    }
+    return acc;
+}
+
 // Shared-memory staging: a block's deduplicated producer records (u of its nodes, sigma of its
 // edges) are loaded once into component planes plane[c][row], so that every later per-thread
 // gather hits shared memory; rows are assigned bank-aware by the plan (cem_plan.cpp bank_rows).
@@ -1803,7 +1830,7 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     if (dirty == (int32_t)(s + 1)) {
         // an incident tet split in this step: lumped mass from the active incidences;
         // m = 0 -> frozen, v = a = 0 (R15)
-        mk = node_mass4(d, k, c);
+        mk = d.npe == 8 ? hex_node_mass(d.self, k) : node_mass4(d, k, c);
         if (c == 0) d.mass[k] = mk;
         if (mk == 0.0) vv = aa = 0.0;
     }
@@ -2292,6 +2319,267 @@ __global__ void __launch_bounds__(256) k_fix_cur(Dev d, int64_t n, int32_t stamp
     }
 }
 
+// ------------------------------------------------------------------ hexahedral crack patterns III-VI
+// (R28; the hex oracle's hex_candidate / hex_crack, same expressions).  One thread
+// per hex on crack steps, between stage C and stage D: an active hex evaluates its 84 candidates
+// (III k = 2f + j, IV 12 + 4f + 2j + t, V 36 + 4f + i, VI 60 + 4f + i), a split hex with a remainder
+// evaluates its active tets with the tet criterion (candidate(), R7).  Decisions use the pre-split
+// state (R18): this thread's own hex and tets only.  A split deactivates, records (hex e or tet
+// E + 3e + i) and stamps the element's nodes for stage D's mass recomputation; IV-VI activate the
+// three tets of the half-hex prism (A,B,C,A'), (B,C,A',B'), (C,A',B',C').
+__constant__ int8_t c_hf[6][4] = {{0, 1, 2, 3}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+__constant__ int8_t c_hpartner[6][8] = {{4, 5, 6, 7, -1, -1, -1, -1}, {-1, -1, -1, -1, 0, 1, 2, 3},
+                                        {3, 2, -1, -1, 7, 6, -1, -1},   {-1, 0, 3, -1, -1, 4, 7, -1},
+                                        {-1, -1, 1, 0, -1, -1, 5, 4},   {1, -1, -1, 2, 5, -1, -1, 6}};
+__constant__ int8_t c_hep[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 2, 3};
+__constant__ int8_t c_heq[12] = {1, 2, 3, 3, 5, 6, 7, 7, 4, 5, 6, 7};
+__constant__ int8_t c_hpair2[8][8] = {{-1, 0, 1, 2, 3, 4, 5, 6},     {0, -1, 7, 8, 9, 10, 11, 12},
+                                      {1, 7, -1, 13, 14, 15, 16, 17}, {2, 8, 13, -1, 18, 19, 20, 21},
+                                      {3, 9, 14, 18, -1, 22, 23, 24}, {4, 10, 15, 19, 22, -1, 25, 26},
+                                      {5, 11, 16, 20, 23, 25, -1, 27}, {6, 12, 17, 21, 24, 26, 27, -1}};
+__device__ __forceinline__ int hedge(int a, int b) {  // local hex edge of (a, b), -1 for a diagonal
+    const int p = a < b ? a : b, q = a < b ? b : a;
+    for (int l = 0; l < 12; ++l)
+        if (c_hep[l] == p && c_heq[l] == q) return l;
+    return -1;
+}
+struct HexScratch {
+    double X[8][3], U[8][3], G[12][3];
+    int H[12];
+    Eig eg[12];
+};
+__device__ double hex_Dd(const HexScratch &w, int l, Vec3 m) {
+    if (!w.H[l]) return 0.0;
+    const int p = c_hep[l], q = c_heq[l];
+    const Vec3 du = {w.U[q][0] - w.U[p][0], w.U[q][1] - w.U[p][1], w.U[q][2] - w.U[p][2]};
+    const Vec3 dX = {w.X[q][0] - w.X[p][0], w.X[q][1] - w.X[p][1], w.X[q][2] - w.X[p][2]};
+    return vdot(du, m) * dsgn(vdot(dX, m));
+}
+// m = (Gq - Gp) x (R - M), M = (Gp + Gq)/2, R = Rm or (Rm + Rn)/2
+__device__ Vec3 hex_m(const double *Gp, const double *Gq, const double *Rm, const double *Rn) {
+    double d1[3], d2[3];
+    for (int c = 0; c < 3; ++c) {
+        const double M = 0.5 * (Gp[c] + Gq[c]), R = Rn ? 0.5 * (Rm[c] + Rn[c]) : Rm[c];
+        d1[c] = Gq[c] - Gp[c];
+        d2[c] = R - M;
+    }
+    return vcross(Vec3{d1[0], d1[1], d1[2]}, Vec3{d2[0], d2[1], d2[2]});
+}
+__device__ __noinline__ bool hex_candidate(const HexScratch &w, int k, bool both, double &G, double &area, int *P) {
+    int lp, lq;
+    bool rem = true;
+    if (k < 36) {
+        int f, j, t = 0;
+        if (k < 12) {
+            f = k / 2;
+            j = k % 2;
+        } else {
+            f = (k - 12) / 4;
+            j = ((k - 12) / 2) % 2;
+            t = (k - 12) % 2;
+        }
+        const int a = c_hf[f][j], b = c_hf[f][j + 1], c = c_hf[f][(j + 2) % 4], dd = c_hf[f][(j + 3) % 4];
+        const int a1 = c_hpartner[f][a], b1 = c_hpartner[f][b], c1 = c_hpartner[f][c], d1 = c_hpartner[f][dd];
+        lp = hedge(a, b);
+        lq = hedge(dd, c);
+        if (k < 12) {
+            const int lp1 = hedge(a1, b1), lq1 = hedge(d1, c1);
+            const Vec3 m = hex_m(w.G[lp], w.G[lq], w.G[lp1], w.G[lq1]);
+            const double mm = vdot(m, m);
+            const double A1 = sig_proj(w.eg[lp1], m) * hex_Dd(w, lp, m);
+            const double A2 = sig_proj(w.eg[lq1], m) * hex_Dd(w, lq, m);
+            G = (0.5 * (A1 + A2)) / mm;
+            area = sqrt(mm);
+            rem = false;
+        } else {
+            const int g = t == 0 ? hedge(a1, d1) : hedge(b1, c1);
+            const Vec3 m = hex_m(w.G[lp], w.G[lq], w.G[g], nullptr);
+            const double mm = vdot(m, m);
+            const double A1 = sig_proj(w.eg[g], m) * hex_Dd(w, lp, m);
+            const double A2 = sig_proj(w.eg[g], m) * hex_Dd(w, lq, m);
+            G = (0.5 * (A1 + A2)) / mm;
+            area = sqrt(mm);
+            if (t == 0) {
+                P[0] = b; P[1] = b1; P[2] = a1; P[3] = c; P[4] = c1; P[5] = d1;
+            } else {
+                P[0] = a; P[1] = a1; P[2] = b1; P[3] = dd; P[4] = d1; P[5] = c1;
+            }
+        }
+    } else {
+        const int vi = k < 60 ? k - 36 : k - 60, f = vi / 4, i = vi % 4;
+        const int c = c_hf[f][i], x = c_hf[f][(i + 1) % 4], z = c_hf[f][(i + 2) % 4], y = c_hf[f][(i + 3) % 4];
+        const int c1 = c_hpartner[f][c], x1 = c_hpartner[f][x], z1 = c_hpartner[f][z], y1 = c_hpartner[f][y];
+        lp = hedge(c, x);
+        lq = hedge(c, y);
+        const int lr = hedge(c, c1);
+        if (k < 60) {
+            const int lp1 = hedge(c1, x1), lq1 = hedge(c1, y1);
+            const Vec3 m = hex_m(w.G[lp], w.G[lq], w.G[lp1], w.G[lq1]);
+            const double mm = vdot(m, m);
+            const double A1 = sig_proj(w.eg[lp1], m) * hex_Dd(w, lp, m);
+            const double A2 = sig_proj(w.eg[lq1], m) * hex_Dd(w, lq, m);
+            G = (0.5 * (A1 + A2)) / mm;
+            area = sqrt(mm);
+        } else {
+            const Vec3 m = hex_m(w.G[lp], w.G[lq], w.G[lr], nullptr);
+            const double mm = vdot(m, m);
+            const double Sg = sig_proj(w.eg[lr], m);
+            G = (0.5 * (Sg * (hex_Dd(w, lp, m) + hex_Dd(w, lq, m)))) / mm;
+            area = sqrt(mm) / 2.0;
+        }
+        P[0] = x; P[1] = z; P[2] = y; P[3] = x1; P[4] = z1; P[5] = y1;
+    }
+    if (both && !(w.H[lp] && w.H[lq])) G = 0.0;
+    return rem;
+}
+// tet volume and gradients (eq:CSTet_strain_discretization; the oracle's orc_tet_geometry)
+__device__ void tet_geo(const double X[4][3], double *g13) {
+    double d1[3], d2[3], d3[3];
+    for (int c = 0; c < 3; ++c) {
+        d1[c] = X[1][c] - X[0][c];
+        d2[c] = X[2][c] - X[0][c];
+        d3[c] = X[3][c] - X[0][c];
+    }
+    const Vec3 a1 = {d1[0], d1[1], d1[2]}, a2 = {d2[0], d2[1], d2[2]}, a3 = {d3[0], d3[1], d3[2]};
+    const Vec3 c23 = vcross(a2, a3), c31 = vcross(a3, a1), c12 = vcross(a1, a2);
+    const double det = vdot(a1, c23);
+    g13[0] = det / 6.0;
+    const double inv = 1.0 / det;
+    const double r1[3] = {c23.x, c23.y, c23.z}, r2[3] = {c31.x, c31.y, c31.z}, r3[3] = {c12.x, c12.y, c12.z};
+    for (int c = 0; c < 3; ++c) {
+        g13[4 + c] = r1[c] * inv;
+        g13[7 + c] = r2[c] * inv;
+        g13[10 + c] = r3[c] * inv;
+        g13[1 + c] = -((g13[4 + c] + g13[7 + c]) + g13[10 + c]);
+    }
+}
+__device__ __forceinline__ void hex_record(const Dev &d, int64_t step, int32_t elem, int k, double G, double A) {
+    const int slot = atomicAdd(&d.ctr[0], 1);
+    CEM_BOUND(d, slot < 4 * d.E);
+    d.rec_step[slot] = step;
+    d.rec_elem[slot] = elem;
+    d.rec_cand[slot] = k;
+    d.rec_G[slot] = G;
+    d.rec_area[slot] = A;
+}
+
+__global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int64_t E = d.E;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int32_t n[8];
+    for (int a = 0; a < 8; ++a) n[a] = __ldg(d.hconn + a * E + e);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // sigma (stage B) and u_{s+1}, stage C done
+    const double4 *u = d.ubuf[(s + 1) & 1];
+    const int32_t stamp = (int32_t)(s + 1);
+    const bool both = (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0;
+    const double gc = ldro(d.gc + e);
+    if (__ldcg(d.state + e)) {
+        HexScratch w;
+        for (int a = 0; a < 8; ++a) {
+            const double4 x = ldro4(&d.X[n[a]]);
+            const double4 uu = ldcg256(&u[n[a]]);
+            w.X[a][0] = x.x; w.X[a][1] = x.y; w.X[a][2] = x.z;
+            w.U[a][0] = uu.x; w.U[a][1] = uu.y; w.U[a][2] = uu.z;
+        }
+        for (int l = 0; l < 12; ++l) {
+            const int p = c_hep[l], q = c_heq[l];
+            double du[3], dX[3], ww[3];
+            for (int c = 0; c < 3; ++c) {
+                w.G[l][c] = 0.5 * (w.X[p][c] + w.X[q][c]);
+                du[c] = w.U[q][c] - w.U[p][c];
+                dX[c] = w.X[q][c] - w.X[p][c];
+                ww[c] = 2.0 * dX[c] + du[c];
+            }
+            w.H[l] = vdot(Vec3{du[0], du[1], du[2]}, Vec3{ww[0], ww[1], ww[2]}) > 0.0;
+            double s6[6];
+            load_sigma(d, __ldg(d.heedge + (int64_t)l * E + e), s6);
+            principal(s6, w.eg[l]);
+        }
+        double Gb = 0.0, Ab = 0.0;
+        int kb = -1, P[6];
+        for (int k = 0; k < 84; ++k) {
+            double G, A;
+            hex_candidate(w, k, both, G, A, P);
+            if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
+                Gb = G;
+                Ab = A;
+                kb = k;
+            }
+        }
+        if (!(Gb > gc)) return;
+        d.state[e] = 0;
+        hex_record(d, s + 1, (int32_t)e, kb, Gb, Ab);
+        double G, A;
+        if (hex_candidate(w, kb, both, G, A, P)) {  // the half-hex prism remainder
+            const int TT[3][4] = {{0, 1, 2, 3}, {1, 2, 3, 4}, {2, 3, 4, 5}};
+            for (int i = 0; i < 3; ++i) {
+                int t[4];
+                for (int a = 0; a < 4; ++a) t[a] = P[TT[i][a]];
+                double g13[13];
+                for (int pass = 0; pass < 2; ++pass) {
+                    double X4[4][3];
+                    for (int a = 0; a < 4; ++a)
+                        for (int c = 0; c < 3; ++c) X4[a][c] = w.X[t[a]][c];
+                    tet_geo(X4, g13);
+                    if (g13[0] >= 0.0 || pass) break;
+                    const int sw = t[0];
+                    t[0] = t[1];
+                    t[1] = sw;
+                }
+                for (int a = 0; a < 4; ++a) d.htloc[12 * e + 4 * i + a] = (uint8_t)t[a];
+                for (int j = 0; j < 13; ++j) d.htgeo[39 * e + 13 * i + j] = g13[j];
+            }
+            d.htact[e] = 7;
+            d.hrem[e] = (int8_t)kb;
+        }
+        for (int a = 0; a < 8; ++a) d.dirty[n[a]] = stamp;
+        return;
+    }
+    if (__ldcg(d.hrem + e) < 0) return;
+    const uint8_t ta = __ldcg(d.htact + e);
+    uint8_t keep = ta;
+    for (int i = 0; i < 3; ++i) {
+        if (!(ta >> i & 1)) continue;
+        const uint8_t *tl = d.htloc + 12 * e + 4 * i;
+        CritScratch w;
+        for (int a = 0; a < 4; ++a) {
+            const double4 x = ldro4(&d.X[n[tl[a]]]);
+            const double4 uu = ldcg256(&u[n[tl[a]]]);
+            w.X[a][0] = x.x; w.X[a][1] = x.y; w.X[a][2] = x.z;
+            w.U[a][0] = uu.x; w.U[a][1] = uu.y; w.U[a][2] = uu.z;
+        }
+        for (int l = 0; l < 6; ++l) {
+            const Vec3 du = {w.U[c_eq[l]][0] - w.U[c_ep[l]][0], w.U[c_eq[l]][1] - w.U[c_ep[l]][1],
+                             w.U[c_eq[l]][2] - w.U[c_ep[l]][2]};
+            const Vec3 dX = {w.X[c_eq[l]][0] - w.X[c_ep[l]][0], w.X[c_eq[l]][1] - w.X[c_ep[l]][1],
+                             w.X[c_eq[l]][2] - w.X[c_ep[l]][2]};
+            const Vec3 ww = {2.0 * dX.x + du.x, 2.0 * dX.y + du.y, 2.0 * dX.z + du.z};
+            w.H[l] = vdot(du, ww) > 0.0;
+            double s6[6];
+            load_sigma(d, __ldg(d.hpair + (int64_t)c_hpair2[tl[c_ep[l]]][tl[c_eq[l]]] * E + e), s6);
+            principal(s6, w.eg[l]);
+        }
+        double Gb = 0.0, Ab = 0.0;
+        int kb = -1;
+        for (int k = 0; k < 24; ++k) {
+            double G, A;
+            candidate(w, k, both, G, A);
+            if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
+                Gb = G;
+                kb = k;
+                Ab = A;
+            }
+        }
+        if (!(Gb > gc)) continue;
+        keep &= (uint8_t)~(1u << i);
+        hex_record(d, s + 1, (int32_t)(E + 3 * e + i), kb, Gb, Ab);
+        for (int a = 0; a < 4; ++a) d.dirty[n[tl[a]]] = stamp;
+    }
+    if (keep != ta) d.htact[e] = keep;
+}
+
 inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 inline size_t crit_smem_bytes() { return sizeof(CritBatch) * crit_batch_warps(); }
 inline unsigned nblk_d(const Dev &d) {  // staged D: 10 nodes per warp
@@ -2473,6 +2761,10 @@ void launch_wave_base(const Dev &d, int64_t step0, cudaStream_t st) { k_set_i64<
 void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
     const int64_t n = ST_COUNT * (int64_t)d.wmax;
     k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d.wcnt, n, (int32_t)step);
+}
+
+void launch_hex_crit(const Dev &d, int64_t s, cudaStream_t st) {
+    launch_pdl(k_hexcrit, (unsigned)((d.E + 127) / 128), 128u, (size_t)0, st, d, s);
 }
 
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {

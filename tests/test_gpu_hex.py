@@ -1,6 +1,7 @@
-"""GPU parity of the ES-H-FEM hexahedral path (cem_hex.cu) through the C ABI,
-bitwise against the hex oracle (oracle/cem_oracle_hex.c, pinned by tests/test_oracle_hex.py):
-u, v, a and the lumped masses equal bit for bit, and the north-star relative L2 of u first."""
+"""GPU parity of the ES-H-FEM hexahedral path (cem_hex.cu, k_hexcrit) through the
+C ABI, bitwise against the hex oracle (oracle/cem_oracle_hex.c, pinned by tests/test_oracle_hex.py and
+tests/test_oracle_hex_crack.py): u, v, a, the lumped masses, the hex states and the split records
+(patterns III-VI, remainder tets) equal bit for bit, and the north-star relative L2 of u first."""
 import numpy as np
 import pytest
 
@@ -11,14 +12,14 @@ from test_gpu_parity import _gpu
 pytestmark = pytest.mark.gpu
 
 
-def _pair(p, steps, chunks=1):
+def _pair(p, steps, chunks=1, crack_every=0, flags=0):
     cem = _gpu()
-    sim = cem.Simulation.from_problem(p)
-    orc = oracle.HexOracle(p)
+    sim = cem.Simulation.from_problem(p, flags=flags)
+    orc = oracle.HexOracle(p, flags=flags)
     per = steps // chunks
     for _ in range(chunks):
-        sim.step(per, 0)
-        orc.run(per)
+        sim.step(per, crack_every)
+        orc.run(per, crack_every)
     return sim, orc
 
 
@@ -59,16 +60,63 @@ def test_hex_ragged_distorted_inactive_body_dirichlet(cells, seed):
     _assert_bitwise(sim, orc)
 
 
-def test_hex_rejects_cracking():
+def test_hex_crack_update_rejected():
     cem = _gpu()
     p = ci.hex_block((4, 3, 2))
     sim = cem.Simulation.from_problem(p)
     with pytest.raises(cem.CemError):
-        sim.step(5, 1)
-    with pytest.raises(cem.CemError):
         sim.crack_update()
     sim.step(5, 0)
     assert sim.state(records=False).step == 5
+
+
+def _assert_cracking(sim, orc, p):
+    _assert_bitwise(sim, orc)
+    g = sim.state()
+    r = orc.records()
+    assert r.step.size > 0
+    assert np.array_equal(g.rec_step, r.step)
+    assert np.array_equal(g.rec_elem, r.elem), "split sets differ"
+    assert np.array_equal(g.rec_cand, r.cand)
+    assert np.array_equal(g.rec_G, r.G)
+    assert np.array_equal(g.rec_area, r.area)
+    assert np.array_equal(g.tet_state, orc.elements()["hex_active"])
+    assert g.dissipated == orc.dissipated
+    return r
+
+
+def test_hex_cracking_bitwise():
+    """Patterns III-VI and remainder-tet splits (R28, R29) on a notched, pulled hex block: 400 steps with
+    the criterion every step, every pattern family and tet splits present in the record."""
+    p = ci.hex_block((10, 6, 2), dims=(0.05, 0.03, 0.01), seed=2, traction=4e6, gc=2.0, notch=0.3)
+    sim, orc = _pair(p, 400, chunks=2, crack_every=1)
+    r = _assert_cracking(sim, orc, p)
+    hexk = r.cand[r.elem < p.n_tets]
+    assert (hexk < 12).any() and ((hexk >= 12) & (hexk < 36)).any()
+    assert ((hexk >= 36) & (hexk < 60)).any() and (hexk >= 60).any()
+    assert (r.elem >= p.n_tets).any()
+
+
+@pytest.mark.parametrize("cells,seed,every,flags", [((13, 7, 3), 3, 3, 0), ((9, 5, 2), 4, 1, 0x40)])
+def test_hex_cracking_ragged_variants(cells, seed, every, flags):
+    """Ragged sizes around the 128/256-thread blocks, strong jitter, a criterion every 3rd step, and the
+    R11v variant (both front edges stretched)."""
+    p = ci.hex_block(cells, dims=(0.004 * cells[0], 0.004 * cells[1], 0.004 * cells[2]), seed=seed,
+                     jitter=0.12, traction=5e6, gc=1.0, notch=0.4)
+    sim, orc = _pair(p, 300, chunks=3, crack_every=every, flags=flags)
+    _assert_cracking(sim, orc, p)
+
+
+def test_hex_cracked_energy_ledger():
+    """cem_energy after splits: strain energy with the mixed smoothing volumes (R29) and U_d."""
+    p = ci.hex_block((10, 6, 2), dims=(0.05, 0.03, 0.01), seed=2, traction=4e6, gc=2.0, notch=0.3)
+    sim, orc = _pair(p, 200, crack_every=1)
+    e = sim.energy()
+    o = orc.state()
+    assert orc.records().step.size > 0
+    assert e["strain"] == pytest.approx(orc.strain_energy(o["u"]), rel=1e-12)
+    assert e["kinetic"] == pytest.approx(0.5 * (o["m"][:, None] * o["v"] ** 2).sum(), rel=1e-12)
+    assert e["dissipated"] == orc.dissipated
 
 
 def test_hex_energy_ledger():
