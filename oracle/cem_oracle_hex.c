@@ -3,7 +3,8 @@
  * (arXiv 2508.04076, §2.2: eq:hex_strain_discretization PAPER.md:L311-L338,
  * eq:hex_fint_discretization L368-L390).  TEST INFRASTRUCTURE ONLY (same rules as
  * cem_oracle.c): only tests/, __graft_entry__.smoke() and bench.py may load it; it shares no
- * code, header, table or helper with paper_2508_04076_b200/ (nor with cem_oracle.c).
+ * code, header, table or helper with paper_2508_04076_b200/.  From cem_oracle.c (the same oracle
+ * library) it calls the tet geometry, the principal-stress projection and the tet candidates.
  *
  * Readings (R23-R26; the paper writes dN_i/dx without a point for the trilinear
  * element):
