@@ -1253,6 +1253,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.e_inc = at<int32_t>(b, o.e_inc);
     d.vhat = nullptr;  // Vhat summed per step by stage B (splits change it)
     d.hpair = at<int32_t>(b, o.hpair);
+    d.hS_h = h.S_h;
     d.hrem = at<int8_t>(b, o.hrem);
     d.htact = at<uint8_t>(b, o.htact);
     d.htloc = at<uint8_t>(b, o.htloc);

@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(256) k_hexB(Dev d, int64_t s) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= S) return;
     pdl_wait_h();  // tau from stage A
+    // a diagonal edge is carried by remainder tets only: none exist until the first such split
+    // (ctr[24] counts them; its sigma record stays the zero it was initialised to)
+    if (k >= d.hS_h && __ldcg(d.ctr + 24) == 0) return;
     double T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const double Vh = edge_gather(d, k, T, nullptr);
     double4 *o4 = reinterpret_cast<double4 *>(d.srec) + k;

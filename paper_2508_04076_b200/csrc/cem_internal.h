@@ -329,6 +329,7 @@ struct Dev {
     // (candidate k, -1 none), its tets' activity bits, local nodes [E][12], geometry [E][3][13]
     // (V, grad[4][3]) and strain [E][3][6]
     const int32_t *hpair;
+    int64_t hS_h;              // edges [0, hS_h) are hex edges; the diagonals after them carry remainder tets only
     int8_t *hrem;
     uint8_t *htact, *htloc;
     double *htgeo, *httau;

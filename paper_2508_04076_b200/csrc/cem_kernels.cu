@@ -2533,6 +2533,7 @@ __global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
             }
             d.htact[e] = 7;
             d.hrem[e] = (int8_t)kb;
+            atomicAdd(&d.ctr[24], 1);  // stage B now sweeps the diagonal edges too
         }
         for (int a = 0; a < 8; ++a) d.dirty[n[a]] = stamp;
         return;
