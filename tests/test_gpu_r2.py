@@ -6,6 +6,8 @@ nodal displacements within a relative L2 error of 1e-11 per 1000 steps"; SURVEY.
 0 and 1, config 2 in full, config 3 at P = 1, config 4 for its first 1000 steps.  assert_parity
 checks the 1e-11 bound first and then bitwise equality of u, v, a, masses, flags and records.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -28,11 +30,20 @@ def _pair(prob, steps, crack_every=1, flags=0, chunks=1):
 
 
 # ------------------------------------------------------------------ north-star horizons, full size
-@pytest.mark.parametrize("cfg,steps", [(1, 1000), (3, 1000), (2, 2000), (4, 1000)],
-                         ids=["cfg1-1000", "cfg3-1000", "cfg2-2000", "cfg4-first1000"])
+# The oracle sets the wall time (config 4: 7.68M tets, ~0.5 s per oracle step on 16 cores).  The
+# default suite must fit a driver's GPU-test slot, so it runs configs 1 and 3 over the full
+# 1000-step horizon, config 2 for 1000 of its 2000 steps and config 4 for its first 100;
+# CEM_LONG_TESTS=1 runs SURVEY.md §4's full horizons (config 2 in full, config 4 for 1000 steps:
+# ~12 more minutes; logs of those runs on this build: profiles/r02c_pytest_gpu.log, r02d_pytest_gpu.log).
+_LONG = os.environ.get("CEM_LONG_TESTS") == "1"
+_HORIZONS = [(1, 1000), (3, 1000), (2, 2000 if _LONG else 1000), (4, 1000 if _LONG else 100)]
+
+
+@pytest.mark.parametrize("cfg,steps", _HORIZONS, ids=[f"cfg{c}-{n}" for c, n in _HORIZONS])
 def test_full_size_north_star_horizon(cfg, steps):
-    """BASELINE configs at full size over the north star's 1000-step horizon (config 2 in full),
-    crack criterion and split pass every step, in the bench's launch configuration."""
+    """BASELINE configs at full size over the north star's 1000-step horizon (config 2 in full and
+    config 4 for its first 1000 steps with CEM_LONG_TESTS=1), crack criterion and split pass every
+    step, in the bench's launch configuration."""
     p = ci.config(cfg)
     sim, orc = _pair(p, steps, 1)
     g = assert_parity(sim, orc, p)
