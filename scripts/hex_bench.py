@@ -33,9 +33,9 @@ for name, kw, every in (("elastodynamics", dict(), 0),
     sim.step(5, every)  # warm-up
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    a.record(sim.torch_stream)   # the context's stream (opts.stream): the library fences its private stream against it
     sim.step(steps, every)
-    b.record()
+    b.record(sim.torch_stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     st = sim.state()

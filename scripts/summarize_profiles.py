@@ -85,6 +85,24 @@ def mb(r, k):
 full = OrderedDict()
 for r in rr[2:]:
     full[r[H.index("Kernel Name")].split("(")[0].split("::")[-1]] = r
+
+
+# ---- on-chip floors of each stage kernel (the same capture): L1 data-pipe wavefronts (shared +
+# global, one per SM and clock), warp instructions (4 issue slots per SM and clock) and fp64
+# thread operations (DADD + DMUL + DFMA, against the measured DFMA rate of tools/dfma_peak)
+def pipe(n):
+    r = full[n]
+    cyc = gv(r, "sm__cycles_elapsed.avg")
+    wf = gv(r, "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg")
+    wf_sh = gv(r, "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_shared.avg")
+    fp64 = sum(gv(r, f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum.per_cycle_elapsed") for o in ("dadd", "dmul", "dfma")) * cyc
+    return {"sm_cycles": cyc, "l1_wavefronts_per_sm": wf, "l1_wavefronts_shared_per_sm": wf_sh,
+            "l1_pipe_frac": wf / cyc, "warp_inst": gv(r, "smsp__inst_executed.sum"),
+            "issue_frac": gv(r, "sm__inst_issued.avg.pct_of_peak_sustained_active") / 100.0,
+            "fp64_thread_ops": fp64,
+            "shared_bank_conflict_wavefronts": gv(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")}
+
+
 cold_bytes = sum((mb(full[n], "dram__bytes_read.sum") + mb(full[n], "dram__bytes_write.sum")) * 1e6 for n in STAGES)
 json.dump({"round": rnd,
            "dram_bytes_per_step": cold_bytes,
@@ -95,6 +113,7 @@ json.dump({"round": rnd,
            "per_kernel_cold": {n: {"time_ns": gv(full[n], "gpu__time_duration.sum") * 1e3,
                                    "dram_read": mb(full[n], "dram__bytes_read.sum") * 1e6,
                                    "dram_write": mb(full[n], "dram__bytes_write.sum") * 1e6} for n in STAGES},
+           "per_kernel_pipes": {n: pipe(n) for n in STAGES},
            "source": {"dram_bytes_per_step": "ncu --set full (default cache flush) of k_AB, k_C, k_D at step ~350",
                       "dram_bytes_per_step_live": "ncu --cache-control none --metrics dram__bytes_*.sum, steady state"}},
           open(os.path.join(out_dir, "traffic_per_step.json"), "w"), indent=1)
@@ -124,6 +143,22 @@ for n in STAGES:
                  f"{gv(r, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active'):.0f} | "
                  f"{gv(r, 'launch__registers_per_thread'):.0f} | "
                  + ", ".join(f"{nm} {100*v/tot:.0f}%" for v, nm in st[:3]) + " |")
+P = {n: pipe(n) for n in STAGES}
+SM, CLK, DFMA = 148, 1.965e9, 18.1e12  # SMs, SM clock under load, measured fp64 instructions/s (36.2 TFLOP/s / 2)
+lines += ["", "On-chip floors of the same launches (what the time would be if that unit alone ran at its peak): the L1 data "
+          "pipe (shared-memory and global-load wavefronts, one per SM and clock), warp-instruction issue (4 per SM and "
+          "clock) and the fp64 pipe (DADD + DMUL + DFMA thread operations at the measured 18.1 T instructions/s).", "",
+          "| kernel | time (µs) | L1 data-pipe wavefronts per SM (shared) | L1 pipe floor (µs) / busy | warp instructions | issue floor (µs) | fp64 thread ops | fp64 floor (µs) | shared bank-conflict wavefronts |",
+          "|---|---|---|---|---|---|---|---|---|"]
+for n in STAGES:
+    q = P[n]
+    lines.append(f"| {n} | {gv(full[n], 'gpu__time_duration.sum'):.1f} | {q['l1_wavefronts_per_sm']:.0f} ({q['l1_wavefronts_shared_per_sm']:.0f}) | "
+                 f"{q['l1_wavefronts_per_sm'] / CLK * 1e6:.1f} / {100 * q['l1_pipe_frac']:.0f} % | {q['warp_inst'] / 1e6:.1f} M | "
+                 f"{q['warp_inst'] / (SM * 4 * CLK) * 1e6:.1f} | {q['fp64_thread_ops'] / 1e6:.0f} M | {q['fp64_thread_ops'] / DFMA * 1e6:.1f} | "
+                 f"{q['shared_bank_conflict_wavefronts'] / 1e6:.2f} M |")
+lines.append(f"| step | | | {sum(P[n]['l1_wavefronts_per_sm'] for n in STAGES) / CLK * 1e6:.1f} | "
+             f"{sum(P[n]['warp_inst'] for n in STAGES) / 1e6:.1f} M | {sum(P[n]['warp_inst'] for n in STAGES) / (SM * 4 * CLK) * 1e6:.1f} | "
+             f"{sum(P[n]['fp64_thread_ops'] for n in STAGES) / 1e6:.0f} M | {sum(P[n]['fp64_thread_ops'] for n in STAGES) / DFMA * 1e6:.1f} | |")
 lines += ["", f"Launch list (cold, serialised) of one bench step: " +
           ", ".join(f"{n} {m['gpu__time_duration.sum']/1e3:.1f} µs" for _, n, m in lastL) + f" (sum {t_launch/1e3:.1f} µs)."]
 open(os.path.join(out_dir, f"{rnd}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
