@@ -339,6 +339,22 @@ def main():
                     # over this run's step time: the share of HBM bandwidth the kernels sustain
                     "traffic_live": traffic_live,
                     "dram_frac_live": (traffic_live / (ms_step / 1e3) / 1e9 / hbm) if traffic_live else None}
+    # on-chip floors of the step from the stored ncu capture of this build (per-launch counters of
+    # k_AB, k_C, k_D: L1 data-pipe wavefronts per SM, warp instructions, fp64 thread operations;
+    # DESIGN.md section 6): the time each unit alone would need at its peak, next to the HBM floor
+    pipes = tj.get("per_kernel_pipes")
+    if pipes:
+        clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        roof["on_chip_floors"] = {
+            "l1_data_pipe_us": sum(q["l1_wavefronts_per_sm"] for q in pipes.values()) / clk * 1e6,
+            "issue_us": sum(q["warp_inst"] for q in pipes.values()) / (sms * 4 * clk) * 1e6,
+            "fp64_us": sum(q["fp64_thread_ops"] for q in pipes.values()) / 18.1e12 * 1e6,
+            "hbm_b_alg_us": balg / hbm / 1e3,
+            "measured_us": ms_step * 1e3,
+            "binding": "l1_data_pipe (shared-memory + global-load wavefronts, one per SM and clock)",
+            "source": f"stored ncu --set full capture, profiles/traffic_per_step.json ({tj.get('round', '?')}); "
+                      "fp64 at the measured 18.1 T instructions/s (tools/dfma_peak)"}
     if roof["achieved"] is None:  # (no per-kernel times, N > 1): the step view
         roof.update({"kernel": "cem_step (unit = one step)", "achieved": achieved, "frac": achieved / hbm,
                      "traffic": traffic})

@@ -53,6 +53,7 @@ struct cem_ctx {
     // multi-GPU (nranks > 1)
     bool dist = false, loopback = false;
     bool hexa = false;            // trilinear hexahedra (ES-H-FEM, cem_hex.cpp / cem_hex.cu)
+    bool hex_cracked = false;     // a crack step has run: remainder tets (and their diagonal edges) may exist
     int rank = 0, nranks = 1;
     PartLocal part;
     Exchange xch;
@@ -260,6 +261,7 @@ void bind_views(cem_ctx *ctx, const Offs &o) {
     d.we_max = p.we_max;
     d.zslot = p.zslot;
     d.wn = p.wn;
+    d.wn0 = p.wn;
     d.X = at<double4>(b, o.X);
     d.fext = at<double4>(b, o.fext);
     d.nflag = at<uint8_t>(b, o.nflag);
@@ -1108,7 +1110,7 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
 
 // ---------------------------------------------------------------- hexahedral contexts (N3)
 struct HexOffs {
-    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, htgeo, httau, gc, X, rec_step, rec_elem,
+    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, hnrem, hediag, htgeo, httau, gc, X, rec_step, rec_elem,
         rec_cand, rec_G, rec_area, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
         srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, epart, total;
 };
@@ -1125,6 +1127,8 @@ HexOffs hex_layout(const HexHost &h) {
     o.hpair = L.take<int32_t>(28 * E);
     o.hrem = L.take<int8_t>(E);
     o.htact = L.take<uint8_t>(E);
+    o.hnrem = L.take<uint8_t>(N);
+    o.hediag = L.take<uint8_t>(S - h.S_h);
     o.htloc = L.take<uint8_t>(12 * E);
     o.htgeo = L.take<double>(39 * E);
     o.httau = L.take<double>(18 * E);
@@ -1256,6 +1260,8 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.hS_h = h.S_h;
     d.hrem = at<int8_t>(b, o.hrem);
     d.htact = at<uint8_t>(b, o.htact);
+    d.hnrem = at<uint8_t>(b, o.hnrem);
+    d.hediag = at<uint8_t>(b, o.hediag);
     d.htloc = at<uint8_t>(b, o.htloc);
     d.htgeo = at<double>(b, o.htgeo);
     d.httau = at<double>(b, o.httau);
@@ -1268,6 +1274,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.rec_area = at<double>(b, o.rec_area);
     d.nodeE = at<int32_t>(b, o.nodeE);
     d.wn = h.wn;
+    d.wn0 = h.wn0;
     d.zslot = h.zslot;
     d.fext = at<double4>(b, o.fext);
     d.nflag = at<uint8_t>(b, o.nflag);
@@ -1358,6 +1365,8 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     CUDA_TRY(put(o.hpair, h.pair.data(), 4 * h.pair.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hrem), 0xff, E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htact), 0, E, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hnrem), 0, N, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hediag), 0, S - h.S_h > 0 ? S - h.S_h : 1, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htloc), 0, 12 * E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htgeo), 0, 8 * 39 * E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.httau), 0, 8 * 18 * E, s));
@@ -1752,7 +1761,9 @@ cem_status cem_step(cem_ctx *ctx, int64_t nsteps, int32_t crack_every) {
     if (ctx->hexa) {  // crack steps (R16): the criterion of patterns III-VI between stages C and D
         for (int64_t i = 0; i < nsteps; ++i) {
             const int64_t s1 = ctx->step + i + 1;
-            ctx->launches += launch_hex_step(ctx->d, ctx->step + i, ctx->stream, crack_every > 0 && s1 % crack_every == 0);
+            const bool crack = crack_every > 0 && s1 % crack_every == 0;
+            ctx->launches += launch_hex_step(ctx->d, ctx->step + i, ctx->stream, crack, ctx->hex_cracked);
+            ctx->hex_cracked |= crack;
         }
         CUDA_TRY(cudaGetLastError());
         ctx->step += nsteps;

@@ -3,12 +3,12 @@
 // Same bitwise contract as the tet path (--fmad=false, sequential sums in the order of
 // DESIGN.md §5 for hexes).  Crack patterns III-VI (R28): a split hex may leave a remainder of three
 // tets (E + 3e + i) over its own nodes; their data sit with the parent hex.
-//   A  tau_e = V_e eps_e, eps from the mean gradients (R23), a = 0..7      -> [6][E] planes;
+//   A  tau_e = V_e eps_e, eps from the mean gradients (R23), a = 0..7      -> 32-B + 16-B record planes;
 //      remainder tets tau = V_t eps_t over their 4 nodes                    -> [E][3][6]
 //   B  sigma_s = D (sum tau) / (sum V) over the active elements of edge s (hex e, then its
 //      remainder tets; R29), edges [0, S_h) hex edges, [S_h, S) diagonals
-//   C  S_e = sum_{l=0..11} sigma_{s(e,l)}; f_{e,a} = (V_e/12) B_a^T S_e (R26) -> slot 4(8e + a);
-//      remainder tet i: (V_t/6) B^T sum of its 6 edges -> slot 4(8e + a) + 1 + i of its nodes a
+//   C  S_e = sum_{l=0..11} sigma_{s(e,l)}; f_{e,a} = (V_e/12) B_a^T S_e (R26) -> slot 8e + a (192 B per hex);
+//      remainder tet i: (V_t/6) B^T sum of its 6 edges -> slot 8E + 3(8e + a) + i of its nodes a
 //   crit (crack steps, cem_kernels.cu k_hexcrit): patterns III-VI / the tet criterion, split
 //   D  the tet path's node update (force-slot gather, Newmark, BC, mass of split nodes, predictor)
 #include <cstdint>
@@ -21,6 +21,20 @@ namespace {
 
 __device__ __forceinline__ void pdl_trigger_h() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_h() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// 32-B / 16-B L2 loads and stores (one sector each: u of a node, the two planes of a tau record)
+__device__ __forceinline__ double4 ldcg256h(const double4 *p) {
+    double4 r;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ldcg128h(const double2 *p) {
+    double2 r;
+    asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st256h(double4 *p, double x, double y, double z, double w) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
+}
 
 // local node pair (a, b) -> 0..27 and the hex edge of a pair (-1: a face or body diagonal)
 __constant__ int8_t c_hpair[8][8] = {{-1, 0, 1, 2, 3, 4, 5, 6},     {0, -1, 7, 8, 9, 10, 11, 12},
@@ -29,6 +43,9 @@ __constant__ int8_t c_hpair[8][8] = {{-1, 0, 1, 2, 3, 4, 5, 6},     {0, -1, 7, 8
                                      {5, 11, 16, 20, 23, 25, -1, 27}, {6, 12, 17, 21, 24, 26, 27, -1}};
 __constant__ int8_t c_hedge_of_pair[28] = {0,  -1, 3,  8, -1, -1, -1, 1, -1, -1, 9,  -1, -1, 2,
                                            -1, -1, 10, -1, -1, -1, -1, 11, 4, -1, 7, 5, -1, 6};
+#ifndef CEM_HEXB_BATCH
+#define CEM_HEXB_BATCH 2  // stage B: incidences gathered per pass (their loads in flight together; measured 1 / 2 / 4: 403 / 385 / 427 us per step on 100^3 hexes)
+#endif
 __constant__ int8_t c_tp[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int8_t c_tq[6] = {1, 2, 3, 2, 3, 3};
 
@@ -60,8 +77,8 @@ __global__ void __launch_bounds__(256) k_hexA(Dev d, int64_t s) {
     if (act) {
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-            const double *ua = reinterpret_cast<const double *>(u + n[a]);
-            const double ux = __ldcg(ua), uy = __ldcg(ua + 1), uz = __ldcg(ua + 2);
+            const double4 ua = ldcg256h(u + n[a]);
+            const double ux = ua.x, uy = ua.y, uz = ua.z;
             ex = ex + g[a][0] * ux;
             ey = ey + g[a][1] * uy;
             ez = ez + g[a][2] * uz;
@@ -70,13 +87,11 @@ __global__ void __launch_bounds__(256) k_hexA(Dev d, int64_t s) {
             gxz = gxz + (g[a][2] * ux + g[a][0] * uz);
         }
     }
-    double *t = d.htau;
-    t[e] = act ? V * ex : 0.0;
-    t[E + e] = act ? V * ey : 0.0;
-    t[2 * E + e] = act ? V * ez : 0.0;
-    t[3 * E + e] = act ? V * gxy : 0.0;
-    t[4 * E + e] = act ? V * gyz : 0.0;
-    t[5 * E + e] = act ? V * gxz : 0.0;
+    // tau record of hex e: (11, 22, 33, 12) as one 32-B record in plane [E], (23, 13) as one 16-B
+    // record in the plane after it (stage B gathers a record with two loads instead of six)
+    st256h(reinterpret_cast<double4 *>(d.htau) + e, act ? V * ex : 0.0, act ? V * ey : 0.0, act ? V * ez : 0.0,
+           act ? V * gxy : 0.0);
+    reinterpret_cast<double2 *>(d.htau + 4 * E)[e] = make_double2(act ? V * gyz : 0.0, act ? V * gxz : 0.0);
     if (__ldcg(d.hrem + e) < 0) return;
     const uint8_t ta = __ldcg(d.htact + e);
     for (int i = 0; i < 3; ++i) {
@@ -86,8 +101,8 @@ __global__ void __launch_bounds__(256) k_hexA(Dev d, int64_t s) {
         const double *tg = d.htgeo + 39 * e + 13 * i;
         double x = 0.0, y = 0.0, z = 0.0, xy = 0.0, yz = 0.0, xz = 0.0;
         for (int a = 0; a < 4; ++a) {
-            const double *ua = reinterpret_cast<const double *>(u + n[tl[a]]);
-            const double ux = __ldcg(ua), uy = __ldcg(ua + 1), uz = __ldcg(ua + 2);
+            const double4 ua = ldcg256h(u + n[tl[a]]);
+            const double ux = ua.x, uy = ua.y, uz = ua.z;
             const double g0 = tg[1 + 3 * a], g1 = tg[2 + 3 * a], g2 = tg[3 + 3 * a];
             x = x + g0 * ux;
             y = y + g1 * uy;
@@ -112,17 +127,42 @@ __device__ __forceinline__ double edge_gather(const Dev &d, int64_t k, double *T
     const int64_t E = d.E;
     const int32_t j0 = __ldg(d.e_off + k), j1 = __ldg(d.e_off + k + 1);
     double Vh = 0.0, w = 0.0;
-    for (int32_t j = j0; j < j1; ++j) {
-        const int32_t ent = __ldg(d.e_inc + j);
-        const int64_t e = ent >> 5;
-        const int pj = ent & 31;
-        if (__ldcg(d.state + e)) {
+    // four incidences per pass: their entries, then state, V and the tau record of all four in
+    // flight together (one round trip per pass instead of three per incidence); the sums below take
+    // them one after another in the incidence order
+    constexpr int kHB = CEM_HEXB_BATCH;
+    for (int32_t jb = j0; jb < j1; jb += kHB) {
+      int32_t ent4[kHB];
+      uint8_t st4[kHB];
+      double V4[kHB];
+      double4 ta4[kHB];
+      double2 tb4[kHB];
+#pragma unroll
+      for (int t = 0; t < kHB; ++t) ent4[t] = jb + t < j1 ? __ldg(d.e_inc + jb + t) : -1;
+#pragma unroll
+      for (int t = 0; t < kHB; ++t) {
+          const int64_t e = ent4[t] >= 0 ? (int64_t)(ent4[t] >> 5) : 0;
+          st4[t] = ent4[t] >= 0 ? __ldcg(d.state + e) : (uint8_t)0;
+          V4[t] = __ldg(d.hgeo + e);
+          ta4[t] = ldcg256h(reinterpret_cast<const double4 *>(d.htau) + e);
+          tb4[t] = ldcg128h(reinterpret_cast<const double2 *>(d.htau + 4 * E) + e);
+      }
+#pragma unroll
+      for (int t = 0; t < kHB; ++t) {
+        if (ent4[t] < 0) break;
+        const int64_t e = ent4[t] >> 5;
+        const int pj = ent4[t] & 31;
+        if (st4[t]) {
             if (c_hedge_of_pair[pj] < 0) continue;
-            const double V = __ldg(d.hgeo + e);
+            const double V = V4[t];
             Vh = Vh + V;
             if (W) w = w + V / 12.0;
-#pragma unroll
-            for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.htau + c * E + e);
+            T[0] = T[0] + ta4[t].x;
+            T[1] = T[1] + ta4[t].y;
+            T[2] = T[2] + ta4[t].z;
+            T[3] = T[3] + ta4[t].w;
+            T[4] = T[4] + tb4[t].x;
+            T[5] = T[5] + tb4[t].y;
             continue;
         }
         if (__ldcg(d.hrem + e) < 0) continue;
@@ -135,20 +175,22 @@ __device__ __forceinline__ double edge_gather(const Dev &d, int64_t k, double *T
 #pragma unroll
             for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.httau + 18 * e + 6 * i + c);
         }
+      }
     }
     if (W) *W = w;
     return Vh;
 }
 
-__global__ void __launch_bounds__(256) k_hexB(Dev d, int64_t s) {
+__global__ void __launch_bounds__(256, CEM_HEXB_BATCH >= 4 ? 2 : 4) k_hexB(Dev d, int64_t s) {
     pdl_trigger_h();
     const int64_t S = d.S;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= S) return;
     pdl_wait_h();  // tau from stage A
-    // a diagonal edge is carried by remainder tets only: none exist until the first such split
-    // (ctr[24] counts them; its sigma record stays the zero it was initialised to)
-    if (k >= d.hS_h && __ldcg(d.ctr + 24) == 0) return;
+    // a diagonal edge is carried by remainder tets only: k_hexcrit marks the 16 diagonals of a hex it
+    // leaves a remainder in (hediag); the sigma record of an unmarked one stays the zero it was
+    // initialised to
+    if (k >= d.hS_h && !__ldcg(d.hediag + (k - d.hS_h))) return;
     double T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const double Vh = edge_gather(d, k, T, nullptr);
     double4 *o4 = reinterpret_cast<double4 *>(d.srec) + k;
@@ -188,23 +230,27 @@ __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
     for (int l = 0; l < 12; ++l) sid[l] = __ldg(d.heedge + l * E + e);
     const double V = __ldg(d.hgeo + e);
     pdl_wait_h();  // sigma from stage B
-    double *fo = d.fe + 96 * e;  // slot 4(8e + a) + sub at fo + 12a + 3 sub
+    double4 *fo = reinterpret_cast<double4 *>(d.fe + 24 * e);  // slots 8e + a: 24 doubles, six 32-B stores
+    double *fr = d.fe + 3 * (8 * E + 24 * e);                  // remainder slots 8E + 3(8e + a) + i at fr + 9a + 3i
     if (!__ldcg(d.state + e)) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a) fo[12 * a] = fo[12 * a + 1] = fo[12 * a + 2] = 0.0;
+        for (int q = 0; q < 6; ++q) st256h(fo + q, 0.0, 0.0, 0.0, 0.0);
     } else {
         double S[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int l = 0; l < 12; ++l) sigma_sum(d, sid[l], S);
         const double c = V / 12.0;  // R26: the smoothing-domain share of each of the 12 edges
+        double f[24];
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
             const double gx = __ldg(d.hgeo + (1 + 3 * a) * E + e), gy = __ldg(d.hgeo + (2 + 3 * a) * E + e),
                          gz = __ldg(d.hgeo + (3 + 3 * a) * E + e);
-            fo[12 * a] = c * ((gx * S[0] + gy * S[3]) + gz * S[5]);
-            fo[12 * a + 1] = c * ((gy * S[1] + gx * S[3]) + gz * S[4]);
-            fo[12 * a + 2] = c * ((gz * S[2] + gy * S[4]) + gx * S[5]);
+            f[3 * a] = c * ((gx * S[0] + gy * S[3]) + gz * S[5]);
+            f[3 * a + 1] = c * ((gy * S[1] + gx * S[3]) + gz * S[4]);
+            f[3 * a + 2] = c * ((gz * S[2] + gy * S[4]) + gx * S[5]);
         }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) st256h(fo + q, f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
     }
     if (__ldcg(d.hrem + e) < 0) return;
     const uint8_t ta = __ldcg(d.htact + e);
@@ -212,7 +258,7 @@ __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
         const uint8_t *tl = d.htloc + 12 * e + 4 * i;
         if (!(ta >> i & 1)) {  // a split tet contributes nothing from now on
             for (int b = 0; b < 4; ++b) {
-                double *f = fo + 12 * tl[b] + 3 * (1 + i);
+                double *f = fr + 9 * tl[b] + 3 * i;
                 f[0] = f[1] = f[2] = 0.0;
             }
             continue;
@@ -223,7 +269,7 @@ __global__ void __launch_bounds__(256) k_hexC(Dev d, int64_t s) {
         const double c = tg[0] / 6.0;  // R5: V_t / 6 per tet edge
         for (int b = 0; b < 4; ++b) {
             const double gx = tg[1 + 3 * b], gy = tg[2 + 3 * b], gz = tg[3 + 3 * b];
-            double *f = fo + 12 * tl[b] + 3 * (1 + i);
+            double *f = fr + 9 * tl[b] + 3 * i;
             f[0] = c * ((gx * S[0] + gy * S[3]) + gz * S[5]);
             f[1] = c * ((gy * S[1] + gx * S[3]) + gz * S[4]);
             f[2] = c * ((gz * S[2] + gy * S[4]) + gx * S[5]);
@@ -285,8 +331,10 @@ void launch_hex_energy(const Dev &d, int64_t n, double *part_edges, double *part
     launch_energy_nodes(d, n, part_nodes, st);
 }
 
-int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack) {
-    const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)((d.S + 255) / 256);
+int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack, bool diagonals) {
+    // stage B's grid covers the diagonal edges (carried by remainder tets only) once a crack step has
+    // run in this context (`diagonals`, host-known); before that no remainder can exist
+    const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)(((diagonals ? d.S : d.hS_h) + 255) / 256);
     launch_pdl_h(k_hexA, ge, st, d, s);
     launch_pdl_h(k_hexB, gs, st, d, s);
     launch_pdl_h(k_hexC, ge, st, d, s);

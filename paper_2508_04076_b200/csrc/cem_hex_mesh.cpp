@@ -311,17 +311,26 @@ cem_status build_hex_host(const cem_mesh_in *m, const cem_material *mat, const c
         dt = (cfl * hmin) / cd;
     }
     h.dt = dt;
-    // node -> force-slot ELL: incidence (e, a) owns slots 4 (8e + a) + sub, sub 0 the hex's force, sub 1 + i
-    // remainder tet i's (zero while unused); ascending e, padded with the zero slot 32E
+    // node -> force-slot ELL: incidence (e, a) owns slot 8e + a for the hex's force (the hexes' slots are
+    // contiguous: 192 B per hex, written whole by stage C) and slots 8E + 3 (8e + a) + i for remainder
+    // tet i (zero while unused).  Row of a node with k incidences: its k hex slots in
+    // ascending e (the walk of hex_node_mass), then the 3k remainder slots, then the zero slot 32E.
+    // The nodal sum is exact (R27), so its order is free; for a node of no remainder prism (hnrem == 0)
+    // stage D reads only the first wn0 entries (every hex slot; any further entry still zero).
     int mx = 1;
     for (int64_t n = 0; n < N; ++n) mx = std::max(mx, h.node_off[n + 1] - h.node_off[n]);
     h.wn = (4 * mx + 7) / 8 * 8;
+    h.wn0 = (mx + 7) / 8 * 8;
     h.zslot = (int32_t)(32 * E);
     h.nodeE.assign((size_t)N * h.wn, h.zslot);
-    for (int64_t n = 0; n < N; ++n)
-        for (int32_t j = h.node_off[n]; j < h.node_off[n + 1]; ++j)
-            for (int sub = 0; sub < 4; ++sub)
-                h.nodeE[(size_t)n * h.wn + 4 * (j - h.node_off[n]) + sub] = 4 * h.node_ent[j] + sub;
+    for (int64_t n = 0; n < N; ++n) {
+        const int32_t j0 = h.node_off[n], k = h.node_off[n + 1] - j0;
+        int32_t *row = h.nodeE.data() + (size_t)n * h.wn;
+        for (int32_t j = 0; j < k; ++j) {
+            row[j] = h.node_ent[j0 + j];
+            for (int i = 0; i < 3; ++i) row[k + 3 * j + i] = (int32_t)(8 * E) + 3 * h.node_ent[j0 + j] + i;
+        }
+    }
     return CEM_OK;
 }
 

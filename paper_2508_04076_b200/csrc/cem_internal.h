@@ -143,8 +143,9 @@ struct HexHost {
     std::vector<int32_t> edge_off, edge_inc, node_off, node_ent;
     std::vector<double> vhat, mass, fext, dir_v0;
     std::vector<uint8_t> nflag;
-    std::vector<int32_t> nodeE;       // [N][wn] slots 4 (8e + a) + sub, padded with zslot
+    std::vector<int32_t> nodeE;       // [N][wn] hex slots 8e + a, then remainder slots 8E + 3 (8e + a) + i, padded with zslot
     int wn = 8;
+    int wn0 = 8;                      // row prefix holding every sub-0 slot (multiple of 8): all stage D reads until a remainder exists
     int32_t zslot = 0;
     double lam = 0, mu = 0, l2m = 0, rho = 0, dt = 0, gamma = 0.5, t0 = 0;
     bool any_dirichlet = false;
@@ -338,6 +339,11 @@ struct Dev {
     int wdiscard;              // 1: the last consumer discards a producer block's sigma / force-slot lines
     const int32_t *wdep_off, *wdep;
     int wmax;
+    // (appended after every field the tet stage kernels read: their parameter offsets, and with them
+    // the generated code and its measured time, stay those of the profiled build)
+    int wn0;                   // hexahedra: the row prefix stage D reads for a node of no remainder prism (hnrem == 0); tets: wn
+    uint8_t *hnrem;            // [N] node of some remainder prism (stage D then reads the node's remainder slots too)
+    uint8_t *hediag;           // [S - S_h] diagonal edge of some remainder prism (stage B skips the others)
 };
 
 // cem_kernels.cu
@@ -369,7 +375,7 @@ void launch_energy(const Dev &d, int64_t n, double *part_edges, double *part_nod
 void launch_crack_only(const Dev &d, int64_t n, cudaStream_t st);
 // cem_hex.cu: one explicit step of a hexahedral context (4 kernels, PDL-chained; stage D is the
 // tet path's node update); returns the kernels launched
-int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack = false);
+int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack, bool diagonals);
 // hex criterion (patterns III-VI, remainder tets: the tet criterion) and split pass of step s
 // (cem_kernels.cu), PDL-chained between stage C and stage D
 void launch_hex_crit(const Dev &d, int64_t s, cudaStream_t st);

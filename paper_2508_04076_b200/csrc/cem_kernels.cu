@@ -201,11 +201,11 @@ __device__ __noinline__ double hex_node_mass(const Dev *__restrict__ dp, int64_t
     const Dev &d = *dp;
     const int32_t *row = d.nodeE + k * d.wn;
     double acc = 0.0;
-    for (int j = 0; j < d.wn; j += 4) {
+    for (int j = 0; j < d.wn; ++j) {  // the row's sub-0 prefix: one entry per incident hex, ascending e
         const int32_t sl = __ldg(row + j);
-        if (sl == d.zslot) break;
-        const int64_t e = (sl >> 2) >> 3;
-        const int a = (sl >> 2) & 7;
+        if (sl >= 8 * (int32_t)d.E) break;  // (a remainder slot or the padding)
+        const int64_t e = sl >> 3;
+        const int a = sl & 7;
         if (__ldcg(d.state + e)) {
             acc = acc + (d.rho * __ldg(d.hgeo + e)) / 8.0;
             continue;
@@ -1692,6 +1692,10 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
     double aa = __ldcg(reinterpret_cast<const double *>(d.a + k) + c);
     const int32_t dirty = __ldcg(d.dirty + k);
     const double *fec = d.fe + (c < 3 ? c : 0);  // lane c: component c of each slot (lane 3: unused sum)
+    // hexahedra: the remainder-tet slots follow the row's hex-slot prefix and hold zeros unless the
+    // node belongs to a remainder prism (hnrem, set by k_hexcrit; read after the wait: every
+    // earlier kernel has completed)
+    const int wl = (!pm && d.npe == 8 && !__ldcg(d.hnrem + k)) ? d.wn0 : d.wn;
     double f = 0.0, fc = 0.0;  // exact-sum accumulator (R27)
     if (pm) {
         // lane c: component c of each partial, s and c terms, four records per pass
@@ -1732,11 +1736,11 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
             x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
         }
         int w = kB;
-        bool more = sl[kB - 1] != d.zslot && w < d.wn;
+        bool more = sl[kB - 1] != d.zslot && w < wl;
         if (more) {
 #pragma unroll
             for (int j = 0; j < kQ; ++j)
-                q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+                q[j] = w + 4 * j < wl ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
         }
         for (;;) {
             double y[kB];
@@ -1749,11 +1753,11 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
                     y[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
                 }
                 w += kB;
-                more2 = sl[kB - 1] != d.zslot && w < d.wn;
+                more2 = sl[kB - 1] != d.zslot && w < wl;
                 if (more2) {
 #pragma unroll
                     for (int j = 0; j < kQ; ++j)
-                        q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j)
+                        q[j] = w + 4 * j < wl ? __ldg(row + (w >> 2) + j)
                                                 : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
                 }
             }
@@ -1783,11 +1787,11 @@ __device__ __forceinline__ void node_update(const Dev &d, int64_t kbase, int64_t
             x[t] = __ldcg(fec + (uint32_t)CEM_FES * (uint32_t)sl[t]);
         }
         w += kB;
-        const bool more = sl[kB - 1] != d.zslot && w < d.wn;
+        const bool more = sl[kB - 1] != d.zslot && w < wl;
         if (more) {
 #pragma unroll
             for (int j = 0; j < kQ; ++j)
-                q[j] = w + 4 * j < d.wn ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
+                q[j] = w + 4 * j < wl ? __ldg(row + (w >> 2) + j) : make_int4(d.zslot, d.zslot, d.zslot, d.zslot);
         }
 #pragma unroll
         for (int t = 0; t < kB; ++t) xacc(f, fc, x[t]);
@@ -2476,6 +2480,35 @@ __global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
     const bool both = (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0;
     const double gc = ldro(d.gc + e);
     if (__ldcg(d.state + e)) {
+        if (!(d.flags & CEM_F_NO_EARLY_OUT)) {
+            // conservative early-out (as for tets): every candidate is
+            // 1/2 (S_1 Dd_1 + S_2 Dd_2) / |m|^2 with |S_i| <= |sigma_1| |m| <= g |m| (g the Gershgorin
+            // bound of the stress of one of the hex's 12 edges) and |Dd_i| <= |du| |m| (du along one
+            // of them), so |G_k| <= max_l g_l max_l |du_l| for all 84; skipped when that bound
+            // (1 + 1e-6) <= Gc_e -- the decision "no split" either way
+            // (tests/test_early_out_bounds.py pins the bound against the hex oracle's candidates)
+            double U8[8][3];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                const double4 uu = ldcg256(&u[n[a]]);
+                U8[a][0] = uu.x; U8[a][1] = uu.y; U8[a][2] = uu.z;
+            }
+            double d2 = 0.0, gmax = 0.0;
+            constexpr int kp[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 2, 3}, kq[12] = {1, 2, 3, 3, 5, 6, 7, 7, 4, 5, 6, 7};  // (= c_hep, c_heq)
+#pragma unroll
+            for (int l = 0; l < 12; ++l) {
+                const int p = kp[l], q = kq[l];
+                const double dx = U8[q][0] - U8[p][0], dy = U8[q][1] - U8[p][1], dz = U8[q][2] - U8[p][2];
+                d2 = fmax(d2, (dx * dx + dy * dy) + dz * dz);
+                double s6[6];
+                load_sigma(d, __ldg(d.heedge + (int64_t)l * E + e), s6);
+                const double r0 = fabs(s6[0]) + fabs(s6[3]) + fabs(s6[5]);
+                const double r1 = fabs(s6[1]) + fabs(s6[3]) + fabs(s6[4]);
+                const double r2 = fabs(s6[2]) + fabs(s6[4]) + fabs(s6[5]);
+                gmax = fmax(gmax, fmax(r0, fmax(r1, r2)));
+            }
+            if (gmax * sqrt(d2) * (1.0 + 1e-6) <= gc) return;
+        }
         HexScratch w;
         for (int a = 0; a < 8; ++a) {
             const double4 x = ldro4(&d.X[n[a]]);
@@ -2533,7 +2566,13 @@ __global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
             }
             d.htact[e] = 7;
             d.hrem[e] = (int8_t)kb;
-            atomicAdd(&d.ctr[24], 1);  // stage B now sweeps the diagonal edges too
+            atomicAdd(&d.ctr[24], 1);  // (count of remainders)
+            // from the next step on stage D reads the remainder slots of this hex's nodes and stage B
+            // evaluates its 16 diagonal edges (the three tets lie among them)
+            for (int a = 0; a < 8; ++a) d.hnrem[n[a]] = 1;
+            for (int a = 0; a < 8; ++a)
+                for (int b = a + 1; b < 8; ++b)
+                    if (hedge(a, b) < 0) d.hediag[__ldg(d.hpair + (int64_t)c_hpair2[a][b] * E + e) - d.hS_h] = 1;
         }
         for (int a = 0; a < 8; ++a) d.dirty[n[a]] = stamp;
         return;

@@ -104,3 +104,33 @@ def test_refined_bound_is_tighter_on_a_cracking_state():
             listed += 1
             kept += int(b.max() * (1 + 1e-6) > gc[e])
     assert listed > 0 and kept < listed
+
+
+# ------------------------------------------------------------------ hexahedra (patterns III-VI)
+HEX_EDGES = [(0, 1), (1, 2), (2, 3), (0, 3), (4, 5), (5, 6), (6, 7), (4, 7), (0, 4), (1, 5), (2, 6), (3, 7)]
+
+
+@pytest.mark.parametrize("kind", ["random", "tension", "compression", "shear", "rigid"])
+def test_hex_early_out_bound_dominates_all_84_candidates(kind):
+    """k_hexcrit skips an active hex when  max_l g_l * max_l |du_l| (1 + 1e-6) <= Gc_e  over the
+    hex's 12 edges (g_l: Gershgorin bound of the edge stress).  Every pattern III-VI candidate is
+    1/2 (S_1 Dd_1 + S_2 Dd_2)/|m|^2 with S_i the projected stress of one of those edges and Dd_i the
+    stretch of one of them along m (R28), so the bound dominates all 84 values
+    of the hex oracle -- checked on every hex of jittered blocks under five kinds of fields."""
+    rng = np.random.default_rng({"random": 1, "tension": 2, "compression": 3, "shear": 4, "rigid": 5}[kind])
+    p = ci.hex_block((3, 3, 2), dims=(0.03, 0.03, 0.02), seed=7, jitter=0.15)
+    o = oracle.HexOracle(p)
+    u = fields(kind, p.X, rng)
+    s, vh, en = o.edge_stress(u)
+    eid = {(min(a, b), max(a, b)): i for i, (a, b) in enumerate(en)}
+    worst = 0.0
+    for e in range(p.n_tets):
+        nd = p.tets[e]
+        g = max(gershgorin(s[eid[(min(nd[a], nd[b]), max(nd[a], nd[b]))]]) for a, b in HEX_EDGES)
+        dmax = max(np.linalg.norm(u[nd[b]] - u[nd[a]]) for a, b in HEX_EDGES)
+        G, A, P = o.candidates(u, e)
+        B0 = g * dmax
+        assert np.all(np.abs(G) <= B0 * (1 + 1e-9) + 1e-300), (e, np.abs(G).max(), B0)
+        if B0 > 0:
+            worst = max(worst, np.abs(G).max() / B0)
+    assert kind == "rigid" or worst > 1e-3     # the bound is not vacuous (same order as the largest |G|)

@@ -107,6 +107,19 @@ def test_hex_cracking_ragged_variants(cells, seed, every, flags):
     _assert_cracking(sim, orc, p)
 
 
+def test_hex_criterion_without_early_out_bitwise():
+    """k_hexcrit skips hexes whose bound max g * max |du| (1 + 1e-6) <= Gc (pinned on the CPU by
+    tests/test_early_out_bounds.py); with CEM_F_NO_EARLY_OUT every active hex evaluates its 84
+    candidates.  Both equal the oracle (the default path in test_hex_cracking_bitwise)."""
+    cem = _gpu()
+    p = ci.hex_block((10, 6, 2), dims=(0.05, 0.03, 0.01), seed=2, traction=4e6, gc=2.0, notch=0.3)
+    sim = cem.Simulation.from_problem(p, flags=cem.CEM_F_NO_EARLY_OUT)
+    orc = oracle.HexOracle(p)
+    sim.step(300, 1)
+    orc.run(300, 1)
+    _assert_cracking(sim, orc, p)
+
+
 def test_hex_cracked_energy_ledger():
     """cem_energy after splits: strain energy with the mixed smoothing volumes (R29) and U_d."""
     p = ci.hex_block((10, 6, 2), dims=(0.05, 0.03, 0.01), seed=2, traction=4e6, gc=2.0, notch=0.3)
