@@ -1110,7 +1110,7 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
 
 // ---------------------------------------------------------------- hexahedral contexts (N3)
 struct HexOffs {
-    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, hnrem, hediag, htgeo, httau, gc, X, rec_step, rec_elem,
+    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, hnrem, hediag, hdlist, heinc4, htgeo, httau, gc, X, rec_step, rec_elem,
         rec_cand, rec_G, rec_area, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
         srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, epart, total;
 };
@@ -1128,7 +1128,9 @@ HexOffs hex_layout(const HexHost &h) {
     o.hrem = L.take<int8_t>(E);
     o.htact = L.take<uint8_t>(E);
     o.hnrem = L.take<uint8_t>(N);
-    o.hediag = L.take<uint8_t>(S - h.S_h);
+    o.hediag = L.take<uint32_t>((S - h.S_h + 31) / 32 + 1);
+    o.hdlist = L.take<int32_t>(S - h.S_h);
+    o.heinc4 = L.take<int4>(S);
     o.htloc = L.take<uint8_t>(12 * E);
     o.htgeo = L.take<double>(39 * E);
     o.httau = L.take<double>(18 * E);
@@ -1261,7 +1263,9 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.hrem = at<int8_t>(b, o.hrem);
     d.htact = at<uint8_t>(b, o.htact);
     d.hnrem = at<uint8_t>(b, o.hnrem);
-    d.hediag = at<uint8_t>(b, o.hediag);
+    d.hediag = at<unsigned>(b, o.hediag);
+    d.hdlist = at<int32_t>(b, o.hdlist);
+    d.heinc4 = at<int4>(b, o.heinc4);
     d.htloc = at<uint8_t>(b, o.htloc);
     d.htgeo = at<double>(b, o.htgeo);
     d.httau = at<double>(b, o.httau);
@@ -1362,11 +1366,20 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     CUDA_TRY(put(o.heedge, h.eedge.data(), 4 * h.eedge.size()));
     CUDA_TRY(put(o.e_off, h.edge_off.data(), 4 * h.edge_off.size()));
     CUDA_TRY(put(o.e_inc, h.edge_inc.data(), 4 * h.edge_inc.size()));
+    {
+        std::vector<int4> q4((size_t)S, make_int4(-1, -1, -1, -1));
+        for (int64_t k = 0; k < S; ++k) {
+            int32_t *q = &q4[k].x;
+            for (int32_t j = h.edge_off[k]; j < std::min(h.edge_off[k + 1], h.edge_off[k] + 4); ++j) q[j - h.edge_off[k]] = h.edge_inc[j];
+        }
+        CUDA_TRY(put(o.heinc4, q4.data(), sizeof(int4) * q4.size()));
+        CUDA_TRY(cudaStreamSynchronize(s));  // q4 leaves scope
+    }
     CUDA_TRY(put(o.hpair, h.pair.data(), 4 * h.pair.size()));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hrem), 0xff, E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htact), 0, E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hnrem), 0, N, s));
-    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hediag), 0, S - h.S_h > 0 ? S - h.S_h : 1, s));
+    CUDA_TRY(cudaMemsetAsync(at<char>(b, o.hediag), 0, 4 * ((S - h.S_h + 31) / 32 + 1), s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htloc), 0, 12 * E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.htgeo), 0, 8 * 39 * E, s));
     CUDA_TRY(cudaMemsetAsync(at<char>(b, o.httau), 0, 8 * 18 * E, s));

@@ -125,72 +125,78 @@ __global__ void __launch_bounds__(256) k_hexA(Dev d, int64_t s) {
 // and (energy) the smoothing-domain volume sum V/n_e (R29)
 __device__ __forceinline__ double edge_gather(const Dev &d, int64_t k, double *T, double *W) {
     const int64_t E = d.E;
-    const int32_t j0 = __ldg(d.e_off + k), j1 = __ldg(d.e_off + k + 1);
     double Vh = 0.0, w = 0.0;
-    // four incidences per pass: their entries, then state, V and the tau record of all four in
-    // flight together (one round trip per pass instead of three per incidence); the sums below take
-    // them one after another in the incidence order
-    constexpr int kHB = CEM_HEXB_BATCH;
-    for (int32_t jb = j0; jb < j1; jb += kHB) {
-      int32_t ent4[kHB];
-      uint8_t st4[kHB];
-      double V4[kHB];
-      double4 ta4[kHB];
-      double2 tb4[kHB];
+    // the edge's first four incidences in one 16-B load (a hex edge of a structured mesh has at most
+    // four), gathered kHB at a time: state, V and the tau record of a pass in flight together; the
+    // sums take them one after another in the incidence order.  Longer lists continue from the CSR.
+    constexpr int kHB = CEM_HEXB_BATCH;  // 1, 2 or 4
+    auto take = [&](const int32_t (&ent4)[kHB]) {
+        uint8_t st4[kHB];
+        double V4[kHB];
+        double4 ta4[kHB];
+        double2 tb4[kHB];
 #pragma unroll
-      for (int t = 0; t < kHB; ++t) ent4[t] = jb + t < j1 ? __ldg(d.e_inc + jb + t) : -1;
-#pragma unroll
-      for (int t = 0; t < kHB; ++t) {
-          const int64_t e = ent4[t] >= 0 ? (int64_t)(ent4[t] >> 5) : 0;
-          st4[t] = ent4[t] >= 0 ? __ldcg(d.state + e) : (uint8_t)0;
-          V4[t] = __ldg(d.hgeo + e);
-          ta4[t] = ldcg256h(reinterpret_cast<const double4 *>(d.htau) + e);
-          tb4[t] = ldcg128h(reinterpret_cast<const double2 *>(d.htau + 4 * E) + e);
-      }
-#pragma unroll
-      for (int t = 0; t < kHB; ++t) {
-        if (ent4[t] < 0) break;
-        const int64_t e = ent4[t] >> 5;
-        const int pj = ent4[t] & 31;
-        if (st4[t]) {
-            if (c_hedge_of_pair[pj] < 0) continue;
-            const double V = V4[t];
-            Vh = Vh + V;
-            if (W) w = w + V / 12.0;
-            T[0] = T[0] + ta4[t].x;
-            T[1] = T[1] + ta4[t].y;
-            T[2] = T[2] + ta4[t].z;
-            T[3] = T[3] + ta4[t].w;
-            T[4] = T[4] + tb4[t].x;
-            T[5] = T[5] + tb4[t].y;
-            continue;
+        for (int t = 0; t < kHB; ++t) {
+            const int64_t e = ent4[t] >= 0 ? (int64_t)(ent4[t] >> 5) : 0;
+            st4[t] = ent4[t] >= 0 ? __ldcg(d.state + e) : (uint8_t)0;
+            V4[t] = __ldg(d.hgeo + e);
+            ta4[t] = ldcg256h(reinterpret_cast<const double4 *>(d.htau) + e);
+            tb4[t] = ldcg128h(reinterpret_cast<const double2 *>(d.htau + 4 * E) + e);
         }
-        if (__ldcg(d.hrem + e) < 0) continue;
-        const uint8_t ta = __ldcg(d.htact + e);
-        for (int i = 0; i < 3; ++i) {
-            if (!(ta >> i & 1) || !tet_has_pair(d.htloc + 12 * e + 4 * i, pj)) continue;
-            const double V = __ldcg(d.htgeo + 39 * e + 13 * i);
-            Vh = Vh + V;
-            if (W) w = w + V / 6.0;
 #pragma unroll
-            for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.httau + 18 * e + 6 * i + c);
+        for (int t = 0; t < kHB; ++t) {
+            if (ent4[t] < 0) break;
+            const int64_t e = ent4[t] >> 5;
+            const int pj = ent4[t] & 31;
+            if (st4[t]) {
+                if (c_hedge_of_pair[pj] < 0) continue;
+                const double V = V4[t];
+                Vh = Vh + V;
+                if (W) w = w + V / 12.0;
+                T[0] = T[0] + ta4[t].x;
+                T[1] = T[1] + ta4[t].y;
+                T[2] = T[2] + ta4[t].z;
+                T[3] = T[3] + ta4[t].w;
+                T[4] = T[4] + tb4[t].x;
+                T[5] = T[5] + tb4[t].y;
+                continue;
+            }
+            if (__ldcg(d.hrem + e) < 0) continue;
+            const uint8_t ta = __ldcg(d.htact + e);
+            for (int i = 0; i < 3; ++i) {
+                if (!(ta >> i & 1) || !tet_has_pair(d.htloc + 12 * e + 4 * i, pj)) continue;
+                const double V = __ldcg(d.htgeo + 39 * e + 13 * i);
+                Vh = Vh + V;
+                if (W) w = w + V / 6.0;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) T[c] = T[c] + __ldcg(d.httau + 18 * e + 6 * i + c);
+            }
         }
-      }
+    };
+    const int4 q4 = __ldg(d.heinc4 + k);
+    const int32_t qq[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+    for (int p = 0; p < 4 / kHB; ++p) {
+        int32_t en[kHB];
+#pragma unroll
+        for (int t = 0; t < kHB; ++t) en[t] = qq[p * kHB + t];
+        if (en[0] >= 0) take(en);
+    }
+    if (q4.w >= 0) {  // more than four incidences: the rest from the CSR
+        const int32_t j1 = __ldg(d.e_off + k + 1);
+        for (int32_t jn = __ldg(d.e_off + k) + 4; jn < j1; jn += kHB) {
+            int32_t en[kHB];
+#pragma unroll
+            for (int t = 0; t < kHB; ++t) en[t] = jn + t < j1 ? __ldg(d.e_inc + jn + t) : -1;
+            take(en);
+        }
     }
     if (W) *W = w;
     return Vh;
 }
 
-__global__ void __launch_bounds__(256, CEM_HEXB_BATCH >= 4 ? 2 : 4) k_hexB(Dev d, int64_t s) {
-    pdl_trigger_h();
-    const int64_t S = d.S;
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= S) return;
-    pdl_wait_h();  // tau from stage A
-    // a diagonal edge is carried by remainder tets only: k_hexcrit marks the 16 diagonals of a hex it
-    // leaves a remainder in (hediag); the sigma record of an unmarked one stays the zero it was
-    // initialised to
-    if (k >= d.hS_h && !__ldcg(d.hediag + (k - d.hS_h))) return;
+// sigma record of edge k
+__device__ __forceinline__ void hexB_edge(const Dev &d, int64_t k) {
     double T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const double Vh = edge_gather(d, k, T, nullptr);
     double4 *o4 = reinterpret_cast<double4 *>(d.srec) + k;
@@ -206,6 +212,26 @@ __global__ void __launch_bounds__(256, CEM_HEXB_BATCH >= 4 ? 2 : 4) k_hexB(Dev d
     *o4 = make_double4(d.l2m * e11 + d.lam * (e22 + e33), d.l2m * e22 + d.lam * (e11 + e33),
                        d.l2m * e33 + d.lam * (e11 + e22), d.mu * g12);
     *o2 = make_double2(d.mu * g23, d.mu * g13);
+}
+
+// blocks [0, ceil(S_h / 256)): one hex edge per thread.  Further blocks (launched once a crack step
+// has run): the diagonal edges of the remainder prisms, from the list k_hexcrit appends to (a
+// diagonal edge is carried by remainder tets only; the sigma record of an unlisted one stays the
+// zero it was initialised to)
+__global__ void __launch_bounds__(256, CEM_HEXB_BATCH >= 4 ? 2 : 4) k_hexB(Dev d, int64_t s) {
+    pdl_trigger_h();
+    const int nbh = (int)((d.hS_h + 255) / 256);
+    if ((int)blockIdx.x < nbh) {
+        const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (k >= d.hS_h) return;
+        pdl_wait_h();  // tau from stage A
+        hexB_edge(d, k);
+        return;
+    }
+    pdl_wait_h();
+    const int n = __ldcg(d.ctr + 25);
+    for (int i = ((int)blockIdx.x - nbh) * (int)blockDim.x + (int)threadIdx.x; i < n; i += ((int)gridDim.x - nbh) * (int)blockDim.x)
+        hexB_edge(d, __ldcg(d.hdlist + i));
 }
 
 __device__ __forceinline__ void sigma_sum(const Dev &d, int32_t sid, double *S) {
@@ -332,9 +358,9 @@ void launch_hex_energy(const Dev &d, int64_t n, double *part_edges, double *part
 }
 
 int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack, bool diagonals) {
-    // stage B's grid covers the diagonal edges (carried by remainder tets only) once a crack step has
-    // run in this context (`diagonals`, host-known); before that no remainder can exist
-    const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)(((diagonals ? d.S : d.hS_h) + 255) / 256);
+    // stage B's grid has blocks for the listed diagonal edges (carried by remainder tets only) once a
+    // crack step has run in this context (`diagonals`, host-known); before that no remainder can exist
+    const unsigned ge = (unsigned)((d.E + 255) / 256), gs = (unsigned)((d.hS_h + 255) / 256) + (diagonals ? 148u * 4u : 0u);
     launch_pdl_h(k_hexA, ge, st, d, s);
     launch_pdl_h(k_hexB, gs, st, d, s);
     launch_pdl_h(k_hexC, ge, st, d, s);

@@ -343,7 +343,9 @@ struct Dev {
     // the generated code and its measured time, stay those of the profiled build)
     int wn0;                   // hexahedra: the row prefix stage D reads for a node of no remainder prism (hnrem == 0); tets: wn
     uint8_t *hnrem;            // [N] node of some remainder prism (stage D then reads the node's remainder slots too)
-    uint8_t *hediag;           // [S - S_h] diagonal edge of some remainder prism (stage B skips the others)
+    unsigned *hediag;          // bitmap over the diagonal edges [S_h, S): edge of some remainder prism, and ...
+    int32_t *hdlist;           // ... the list of those edges (ctr[25] entries, appended by k_hexcrit): all stage B evaluates beyond the hex edges
+    const int4 *heinc4;        // [S] the first four incidences of each edge (e << 5 | pair, -1 padding): one load instead of offsets + entries
 };
 
 // cem_kernels.cu

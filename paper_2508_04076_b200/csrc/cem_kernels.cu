@@ -2196,6 +2196,16 @@ __global__ void __launch_bounds__(256, CEM_D_MINB) k_Ds(Dev d, int64_t s) {
     const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
     block_D<false>(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
 }
+// hexahedral contexts: the slot-mode body under a looser register bound (k_Ds spills 56 B at the 48
+// registers that fit 5 CTAs per SM)
+#ifndef CEM_DH_MINB
+#define CEM_DH_MINB 4  // (61 registers, no spill; 3 / 4 CTAs per SM: 385 / 368 us per step on 100^3 hexes, k_Ds at 5: 387)
+#endif
+__global__ void __launch_bounds__(256, CEM_DH_MINB) k_Dh(Dev d, int64_t s) {
+    pdl_trigger();
+    const int64_t k0 = (int64_t)blockIdx.x * d_nodes_per_block(blockDim.x);
+    block_D<false>(d, k0, k0 + d_nodes_per_block(blockDim.x), d.ubuf[(s + 1) & 1], d.ubuf[s & 1], s);
+}
 // (a separate kernel, so that the single-GPU stage D keeps its register allocation)
 template <bool PM>
 __device__ __forceinline__ void k_Db_body(const Dev &d, int64_t s, unsigned long long bd_target) {
@@ -2572,7 +2582,11 @@ __global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
             for (int a = 0; a < 8; ++a) d.hnrem[n[a]] = 1;
             for (int a = 0; a < 8; ++a)
                 for (int b = a + 1; b < 8; ++b)
-                    if (hedge(a, b) < 0) d.hediag[__ldg(d.hpair + (int64_t)c_hpair2[a][b] * E + e) - d.hS_h] = 1;
+                    if (hedge(a, b) < 0) {  // (a face diagonal is shared with a neighbour: listed once)
+                        const int32_t kd = __ldg(d.hpair + (int64_t)c_hpair2[a][b] * E + e);
+                        const unsigned i = (unsigned)(kd - d.hS_h), bit = 1u << (i & 31);
+                        if (!(atomicOr(d.hediag + (i >> 5), bit) & bit)) d.hdlist[atomicAdd(&d.ctr[25], 1)] = kd;
+                    }
         }
         for (int a = 0; a < 8; ++a) d.dirty[n[a]] = stamp;
         return;
@@ -2808,7 +2822,7 @@ void launch_hex_crit(const Dev &d, int64_t s, cudaStream_t st) {
 }
 
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {
-    launch_pdl(d.part ? k_D : k_Ds, nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
+    launch_pdl(d.part ? k_D : (d.npe == 8 ? k_Dh : k_Ds), nblk_d(d), (unsigned)d.blk, (size_t)0, st, d, s);
 }
 
 int launch_wave_step(const Dev &d, const WavePlan &w, int64_t s, int crack_every, cudaStream_t st, int rel) {
