@@ -120,7 +120,9 @@ typedef struct {
 } cem_load_in;
 
 /* flags */
-#define CEM_F_NO_EARLY_OUT 0x1u /* evaluate all 24 crack candidates on every active tet */
+#define CEM_F_NO_EARLY_OUT 0x1u /* evaluate all 24 crack candidates on every active tet (all 84 on every
+                                 * active hexahedron) instead of skipping the elements whose conservative
+                                 * bound max g * max |du| (1 + 1e-6) <= Gc_e rules a split out; same results */
 #define CEM_F_STAGED 0x2u       /* one kernel per stage (the default; kept for explicitness) */
 #define CEM_F_NO_DISCARD 0x4u   /* persistent kernel: keep consumed intermediates in L2 (no discard) */
 #define CEM_F_PERSISTENT 0x8u   /* one persistent wavefront kernel per cem_step call */
