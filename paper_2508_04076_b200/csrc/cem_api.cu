@@ -1110,7 +1110,7 @@ void fill_part_out(const PartGlobal &g, const PartLocal &L, cem_part_out *o) {
 
 // ---------------------------------------------------------------- hexahedral contexts (N3)
 struct HexOffs {
-    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, hnrem, hediag, hdlist, heinc4, htgeo, httau, gc, X, rec_step, rec_elem,
+    size_t hgeo, hconn, heedge, htau, e_off, e_inc, hpair, hrem, htact, htloc, hnrem, hediag, hdlist, hclist, heinc4, htgeo, httau, gc, X, rec_step, rec_elem,
         rec_cand, rec_G, rec_area, nodeE, fext, nflag, dir_v0, state, mass, dirty, u0, u1, v, a,
         srec, srec2, fe, ctr, rprev, wr_dof, node_orig, tet_orig, self, epart, total;
 };
@@ -1130,6 +1130,7 @@ HexOffs hex_layout(const HexHost &h) {
     o.hnrem = L.take<uint8_t>(N);
     o.hediag = L.take<uint32_t>((S - h.S_h + 31) / 32 + 1);
     o.hdlist = L.take<int32_t>(S - h.S_h);
+    o.hclist = L.take<int32_t>(E);
     o.heinc4 = L.take<int4>(S);
     o.htloc = L.take<uint8_t>(12 * E);
     o.htgeo = L.take<double>(39 * E);
@@ -1265,6 +1266,7 @@ cem_status hex_init(const cem_mesh_in *mesh, const cem_material *mat, const cem_
     d.hnrem = at<uint8_t>(b, o.hnrem);
     d.hediag = at<unsigned>(b, o.hediag);
     d.hdlist = at<int32_t>(b, o.hdlist);
+    d.hclist = at<int32_t>(b, o.hclist);
     d.heinc4 = at<int4>(b, o.heinc4);
     d.htloc = at<uint8_t>(b, o.htloc);
     d.htgeo = at<double>(b, o.htgeo);

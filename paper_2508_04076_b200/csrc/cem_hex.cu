@@ -366,7 +366,7 @@ int launch_hex_step(const Dev &d, int64_t s, cudaStream_t st, bool crack, bool d
     launch_pdl_h(k_hexC, ge, st, d, s);
     if (crack) launch_hex_crit(d, s, st);
     launch_node_update(d, s, st);
-    return crack ? 5 : 4;
+    return crack ? 6 : 4;
 }
 
 }  // namespace cem

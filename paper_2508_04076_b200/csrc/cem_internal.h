@@ -346,6 +346,7 @@ struct Dev {
     unsigned *hediag;          // bitmap over the diagonal edges [S_h, S): edge of some remainder prism, and ...
     int32_t *hdlist;           // ... the list of those edges (ctr[25] entries, appended by k_hexcrit): all stage B evaluates beyond the hex edges
     const int4 *heinc4;        // [S] the first four incidences of each edge (e << 5 | pair, -1 padding): one load instead of offsets + entries
+    int32_t *hclist;           // hexes that failed the criterion's early-out this step (ctr[3] entries; k_hexcrit -> k_hexeval)
 };
 
 // cem_kernels.cu

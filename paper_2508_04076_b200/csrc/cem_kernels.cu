@@ -410,6 +410,7 @@ __device__ __forceinline__ void load_geo(const Dev &d, uint32_t e, double (&g)[4
     double V6;
     geo_record(d, e, g, V, V6);
 }
+
 __device__ __forceinline__ void grad0(double (&g)[4][3]) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[0][c] = -((g[1][c] + g[2][c]) + g[3][c]);
@@ -2519,76 +2520,8 @@ __global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
             }
             if (gmax * sqrt(d2) * (1.0 + 1e-6) <= gc) return;
         }
-        HexScratch w;
-        for (int a = 0; a < 8; ++a) {
-            const double4 x = ldro4(&d.X[n[a]]);
-            const double4 uu = ldcg256(&u[n[a]]);
-            w.X[a][0] = x.x; w.X[a][1] = x.y; w.X[a][2] = x.z;
-            w.U[a][0] = uu.x; w.U[a][1] = uu.y; w.U[a][2] = uu.z;
-        }
-        for (int l = 0; l < 12; ++l) {
-            const int p = c_hep[l], q = c_heq[l];
-            double du[3], dX[3], ww[3];
-            for (int c = 0; c < 3; ++c) {
-                w.G[l][c] = 0.5 * (w.X[p][c] + w.X[q][c]);
-                du[c] = w.U[q][c] - w.U[p][c];
-                dX[c] = w.X[q][c] - w.X[p][c];
-                ww[c] = 2.0 * dX[c] + du[c];
-            }
-            w.H[l] = vdot(Vec3{du[0], du[1], du[2]}, Vec3{ww[0], ww[1], ww[2]}) > 0.0;
-            double s6[6];
-            load_sigma(d, __ldg(d.heedge + (int64_t)l * E + e), s6);
-            principal(s6, w.eg[l]);
-        }
-        double Gb = 0.0, Ab = 0.0;
-        int kb = -1, P[6];
-        for (int k = 0; k < 84; ++k) {
-            double G, A;
-            hex_candidate(w, k, both, G, A, P);
-            if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
-                Gb = G;
-                Ab = A;
-                kb = k;
-            }
-        }
-        if (!(Gb > gc)) return;
-        d.state[e] = 0;
-        hex_record(d, s + 1, (int32_t)e, kb, Gb, Ab);
-        double G, A;
-        if (hex_candidate(w, kb, both, G, A, P)) {  // the half-hex prism remainder
-            const int TT[3][4] = {{0, 1, 2, 3}, {1, 2, 3, 4}, {2, 3, 4, 5}};
-            for (int i = 0; i < 3; ++i) {
-                int t[4];
-                for (int a = 0; a < 4; ++a) t[a] = P[TT[i][a]];
-                double g13[13];
-                for (int pass = 0; pass < 2; ++pass) {
-                    double X4[4][3];
-                    for (int a = 0; a < 4; ++a)
-                        for (int c = 0; c < 3; ++c) X4[a][c] = w.X[t[a]][c];
-                    tet_geo(X4, g13);
-                    if (g13[0] >= 0.0 || pass) break;
-                    const int sw = t[0];
-                    t[0] = t[1];
-                    t[1] = sw;
-                }
-                for (int a = 0; a < 4; ++a) d.htloc[12 * e + 4 * i + a] = (uint8_t)t[a];
-                for (int j = 0; j < 13; ++j) d.htgeo[39 * e + 13 * i + j] = g13[j];
-            }
-            d.htact[e] = 7;
-            d.hrem[e] = (int8_t)kb;
-            atomicAdd(&d.ctr[24], 1);  // (count of remainders)
-            // from the next step on stage D reads the remainder slots of this hex's nodes and stage B
-            // evaluates its 16 diagonal edges (the three tets lie among them)
-            for (int a = 0; a < 8; ++a) d.hnrem[n[a]] = 1;
-            for (int a = 0; a < 8; ++a)
-                for (int b = a + 1; b < 8; ++b)
-                    if (hedge(a, b) < 0) {  // (a face diagonal is shared with a neighbour: listed once)
-                        const int32_t kd = __ldg(d.hpair + (int64_t)c_hpair2[a][b] * E + e);
-                        const unsigned i = (unsigned)(kd - d.hS_h), bit = 1u << (i & 31);
-                        if (!(atomicOr(d.hediag + (i >> 5), bit) & bit)) d.hdlist[atomicAdd(&d.ctr[25], 1)] = kd;
-                    }
-        }
-        for (int a = 0; a < 8; ++a) d.dirty[n[a]] = stamp;
+        // failed the early-out: listed for k_hexeval (one warp per listed hex)
+        d.hclist[atomicAdd(&d.ctr[3], 1)] = (int32_t)e;
         return;
     }
     if (__ldcg(d.hrem + e) < 0) return;
@@ -2632,6 +2565,115 @@ __global__ void __launch_bounds__(128) k_hexcrit(Dev d, int64_t s) {
         for (int a = 0; a < 4; ++a) d.dirty[n[tl[a]]] = stamp;
     }
     if (keep != ta) d.htact[e] = keep;
+}
+
+// The listed hexes (those the early-out could not rule out), one warp each: lanes 0-7 gather the
+// nodes, lanes 0-11 the edge midpoints, Heaviside flags and principal pairs (one cyclic-Jacobi solve
+// per lane instead of twelve in sequence), every lane the candidates k = lane, lane + 32, lane + 64
+// in ascending k; a butterfly argmax over (G, area, -k) equals the oracle's sequential scan (first
+// of the largest (G, area)).  Lane 0 splits: the serial code of the first version, same expressions.
+constexpr int kHexEvalWarps = 4;
+__global__ void __launch_bounds__(32 * kHexEvalWarps) k_hexeval(Dev d, int64_t s) {
+    __shared__ HexScratch ws[kHexEvalWarps];
+    __shared__ int32_t wn[kHexEvalWarps][8];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_hexcrit's list is complete
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    HexScratch &w = ws[wib];
+    int32_t *n = wn[wib];
+    const int64_t E = d.E;
+    const int nl = __ldcg(d.ctr + 3);
+    const double4 *u = d.ubuf[(s + 1) & 1];
+    const int32_t stamp = (int32_t)(s + 1);
+    const bool both = (d.flags & CEM_F_FRONT_BOTH_STRETCHED) != 0;
+    for (int it = (int)blockIdx.x * kHexEvalWarps + wib; it < nl; it += (int)gridDim.x * kHexEvalWarps) {
+        const int64_t e = __ldcg(d.hclist + it);
+        __syncwarp();
+        if (lane < 8) {
+            const int32_t na = __ldg(d.hconn + lane * E + e);
+            n[lane] = na;
+            const double4 x = ldro4(&d.X[na]);
+            const double4 uu = ldcg256(&u[na]);
+            w.X[lane][0] = x.x; w.X[lane][1] = x.y; w.X[lane][2] = x.z;
+            w.U[lane][0] = uu.x; w.U[lane][1] = uu.y; w.U[lane][2] = uu.z;
+        }
+        __syncwarp();
+        if (lane < 12) {
+            const int l = lane;
+            const int p = c_hep[l], q = c_heq[l];
+            double du[3], dX[3], ww[3];
+            for (int c = 0; c < 3; ++c) {
+                w.G[l][c] = 0.5 * (w.X[p][c] + w.X[q][c]);
+                du[c] = w.U[q][c] - w.U[p][c];
+                dX[c] = w.X[q][c] - w.X[p][c];
+                ww[c] = 2.0 * dX[c] + du[c];
+            }
+            w.H[l] = vdot(Vec3{du[0], du[1], du[2]}, Vec3{ww[0], ww[1], ww[2]}) > 0.0;
+            double s6[6];
+            load_sigma(d, __ldg(d.heedge + (int64_t)l * E + e), s6);
+            principal(s6, w.eg[l]);
+        }
+        __syncwarp();
+        double Gb = 0.0, Ab = 0.0;
+        int kb = -1, P[6];
+        for (int k = lane; k < 84; k += 32) {
+            double G, A;
+            hex_candidate(w, k, both, G, A, P);
+            if (kb < 0 || G > Gb || (G == Gb && A > Ab)) {
+                Gb = G;
+                Ab = A;
+                kb = k;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double G2 = __shfl_xor_sync(0xffffffffu, Gb, o), A2 = __shfl_xor_sync(0xffffffffu, Ab, o);
+            const int k2 = __shfl_xor_sync(0xffffffffu, kb, o);
+            if (G2 > Gb || (G2 == Gb && (A2 > Ab || (A2 == Ab && k2 < kb)))) {
+                Gb = G2;
+                Ab = A2;
+                kb = k2;
+            }
+        }
+        if (lane != 0 || !(Gb > ldro(d.gc + e))) continue;
+        d.state[e] = 0;
+        hex_record(d, s + 1, (int32_t)e, kb, Gb, Ab);
+        double G, A;
+        if (hex_candidate(w, kb, both, G, A, P)) {  // the half-hex prism remainder
+            const int TT[3][4] = {{0, 1, 2, 3}, {1, 2, 3, 4}, {2, 3, 4, 5}};
+            for (int i = 0; i < 3; ++i) {
+                int t[4];
+                for (int a = 0; a < 4; ++a) t[a] = P[TT[i][a]];
+                double g13[13];
+                for (int pass = 0; pass < 2; ++pass) {
+                    double X4[4][3];
+                    for (int a = 0; a < 4; ++a)
+                        for (int c = 0; c < 3; ++c) X4[a][c] = w.X[t[a]][c];
+                    tet_geo(X4, g13);
+                    if (g13[0] >= 0.0 || pass) break;
+                    const int sw = t[0];
+                    t[0] = t[1];
+                    t[1] = sw;
+                }
+                for (int a = 0; a < 4; ++a) d.htloc[12 * e + 4 * i + a] = (uint8_t)t[a];
+                for (int j = 0; j < 13; ++j) d.htgeo[39 * e + 13 * i + j] = g13[j];
+            }
+            d.htact[e] = 7;
+            d.hrem[e] = (int8_t)kb;
+            atomicAdd(&d.ctr[24], 1);  // (count of remainders)
+            // from the next step on stage D reads the remainder slots of this hex's nodes and stage B
+            // evaluates its 16 diagonal edges (the three tets lie among them)
+            for (int a = 0; a < 8; ++a) d.hnrem[n[a]] = 1;
+            for (int a = 0; a < 8; ++a)
+                for (int b = a + 1; b < 8; ++b)
+                    if (hedge(a, b) < 0) {  // (a face diagonal is shared with a neighbour: listed once)
+                        const int32_t kd = __ldg(d.hpair + (int64_t)c_hpair2[a][b] * E + e);
+                        const unsigned i = (unsigned)(kd - d.hS_h), bit = 1u << (i & 31);
+                        if (!(atomicOr(d.hediag + (i >> 5), bit) & bit)) d.hdlist[atomicAdd(&d.ctr[25], 1)] = kd;
+                    }
+        }
+        for (int a = 0; a < 8; ++a) d.dirty[n[a]] = stamp;
+    }
 }
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
@@ -2819,6 +2861,7 @@ void launch_wave_fill(const Dev &d, int64_t step, cudaStream_t st) {
 
 void launch_hex_crit(const Dev &d, int64_t s, cudaStream_t st) {
     launch_pdl(k_hexcrit, (unsigned)((d.E + 127) / 128), 128u, (size_t)0, st, d, s);
+    launch_pdl(k_hexeval, 148u * 4u, (unsigned)(32 * kHexEvalWarps), (size_t)0, st, d, s);
 }
 
 void launch_node_update(const Dev &d, int64_t s, cudaStream_t st) {
